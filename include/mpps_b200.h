@@ -1,0 +1,139 @@
+/*
+ * mpps_b200.h -- C-ABI of the B200-native mixed-precision Paterson-Stockmeyer
+ * hot path (arXiv 2312.17396).  Plain pointers and sizes only; no torch types.
+ *
+ * The reference (pkg/src/mpps, pure Python over gmpy2) has no FFI of its own:
+ * its operator seam is the per-op precision-context layer of precision.py
+ * (round_to / mat_mul / mat_axpy / mat_add / one_norm) driven by engine.py.
+ * Each entry point below replaces one reference operator or one fused group
+ * of them; the reference interface it replaces is cited beside it.  The
+ * Python mirror of the reference API (paper_2312_17396_b200/engine.py) is the
+ * only in-tree caller; INTEGRATION.md shows the ctypes stub a maintainer of
+ * the reference would add.
+ *
+ * Conventions
+ *  - Matrices are batches of row-major real matrices; multiword formats are
+ *    stored as separate word planes (SoA): word w of matrix b, entry (i,j) is
+ *    ((T*)data)[w*plane_stride + b*batch_stride + i*ld + j].  fp32 uses float
+ *    words, every other format double words.
+ *  - A format is named by its lattice digits: 7 = fp32, 15 = fp64, 31 = dd
+ *    (double-double), 63 = qd (quad-double) (engine.py:218-240).
+ *  - Every call is asynchronous and stream-ordered on the handle's stream;
+ *    buffers are caller-owned device memory.  A handle is not thread-safe;
+ *    use one handle per host thread.  There is no hidden global state.
+ *  - "sel" arrays (device int32, length nsel) select which batch members a
+ *    call processes (grouped launches for heterogeneous plans); pass NULL to
+ *    process the whole batch.  "exp" arrays (device int32, indexed by batch
+ *    member) give exact power-of-two scalings 2^exp (NULL = 0).
+ *  - Return codes: MPPS_OK; MPPS_EINVAL mirrors the reference's
+ *    DimensionError / ValueError (precision.py:25-26, engine.py:55-63);
+ *    MPPS_EFMT an unsupported format; MPPS_ECUDA a CUDA launch error.  The
+ *    message is available from mpps_last_error().
+ */
+#ifndef MPPS_B200_H
+#define MPPS_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPPS_OK 0
+#define MPPS_EINVAL 1
+#define MPPS_EFMT 2
+#define MPPS_ECUDA 3
+
+#define MPPS_FP32 7
+#define MPPS_FP64 15
+#define MPPS_DD 31
+#define MPPS_QD 63
+
+/* Maximum PS blocks per evaluation supported by the fused assembly kernel
+ * (r + 1 <= MPPS_MAX_BLOCKS; covers Table 1's m = 182, s = 14, r = 13). */
+#define MPPS_MAX_BLOCKS 16
+
+typedef struct mpps_handle mpps_handle;
+
+typedef struct {
+  void *data;              /* device pointer: word 0 of matrix 0           */
+  long long plane_stride;  /* elements between word planes                  */
+  long long batch_stride;  /* elements between matrices of the batch        */
+  int rows, cols, ld;      /* row-major, ld >= cols                         */
+  int batch;               /* number of matrices                            */
+  int fmt;                 /* MPPS_FP32 / MPPS_FP64 / MPPS_DD / MPPS_QD     */
+} mpps_mat;
+
+/* ABI version (major*100 + minor). */
+int mpps_version(void);
+
+/* Handle lifecycle.  stream is a cudaStream_t (NULL = legacy default). */
+int mpps_create(int device, void *stream, mpps_handle **out);
+int mpps_destroy(mpps_handle *h);
+int mpps_set_stream(mpps_handle *h, void *stream);
+const char *mpps_last_error(const mpps_handle *h);
+/* Number of kernels this handle has launched (evidence counter). */
+long long mpps_launch_count(const mpps_handle *h);
+
+/* round_to (precision.py:153-157) and format conversion:
+ * dst = RN_dst(2^exp[b] * src).  Widening is exact. */
+int mpps_convert(mpps_handle *h, const mpps_mat *src, mpps_mat *dst,
+                 const int *sel, int nsel, const int *exp);
+
+/* mat_mul (precision.py:160-184): C = RN_fmt(A * B), A, B, C in one format;
+ * A is rows x k, B is k x cols, C is rows x cols (SUMMA blocks may be
+ * rectangular). */
+int mpps_gemm(mpps_handle *h, const mpps_mat *A, const mpps_mat *B,
+              mpps_mat *C, const int *sel, int nsel);
+
+/* mat_axpy (precision.py:187-197): C = RN(RN(alpha*A) + B) at C's format;
+ * alpha is given as 4 host doubles whose exact sum is the coefficient. */
+int mpps_axpy(mpps_handle *h, const double *alpha_words, const mpps_mat *A,
+              const mpps_mat *B, mpps_mat *C);
+
+/* form_powers / eval_b0_and_power power chain (engine.py:118-124, 141-154):
+ * powers[0] must already hold X at the working format; fills powers[1..s-1]
+ * with X^2..X^s, powers[k] = RN(powers[k-1] * X). */
+int mpps_powers(mpps_handle *h, mpps_mat *powers, int s);
+
+/* assemble_block for i = 0..r plus one_norm of every block and of Y
+ * (engine.py:127-138, 141-154; precision.py:235-249), fused into one pass
+ * over the powers:  B_i = b_{si} I + sum_{j=1..hi_i} b_{si+j} X^j,
+ * accumulated in index order at the working format.  powers holds X^1..X^s
+ * (s entries, powers[s-1] = Y).  coeff_words: device, (m+1) x 4 doubles, the
+ * coefficients already rounded at the working precision.  norms: device,
+ * batch x (r+2) doubles, [b][i] = ||B_i||_1 (i <= r), [b][r+1] = ||Y||_1
+ * (deterministic column-sum order). */
+int mpps_assemble_blocks(mpps_handle *h, const mpps_mat *powers, int s, int m,
+                         const double *coeff_words, mpps_mat *blocks,
+                         double *norms);
+
+/* one_norm (precision.py:235-249) of every batch member: norms[b]. */
+int mpps_one_norm(mpps_handle *h, const mpps_mat *A, double *norms);
+
+/* One fused matrix-Horner step of horner_mixed (engine.py:249-251):
+ *   out = RN_out( 2^eo ( Bprev + 2^-(ey+ei) * RN_fmt(Y * phi) ) )
+ * Y and phi share the level-j format, Bprev is the working-format block and
+ * out is in the level-(j-1) format (>= level j's). */
+int mpps_horner_step(mpps_handle *h, const mpps_mat *Y, const mpps_mat *phi,
+                     const mpps_mat *Bprev, mpps_mat *out, const int *sel,
+                     int nsel, const int *exp_y, const int *exp_in,
+                     const int *exp_out);
+
+/* Top Horner step when B_r = b_m I (m mod s == 0, engine.py:132): the
+ * reference's Y * (b_m I) equals RN_j(b_m * Y) entrywise, so no GEMM runs:
+ *   out = RN_out( 2^eo ( Bprev + RN_{fmt_top}(b_m * Y) ) ).
+ * Y is at the working format; fmt_top is the level-r format. */
+int mpps_horner_scalar_top(mpps_handle *h, const double *bm_words, int fmt_top,
+                           const mpps_mat *Y, const mpps_mat *Bprev,
+                           mpps_mat *out, const int *sel, int nsel,
+                           const int *exp_out);
+
+/* Diagnostic: pipe-peak probe used by bench.py for the per-precision
+ * roofline denominators (not a reference operator).  Launches `blocks`
+ * CTAs x 256 threads, each running 8 independent FMA chains of `iters`
+ * steps in fmt (MPPS_FP32 / MPPS_FP64): 16 * iters flops per thread. */
+int mpps_probe_fma(mpps_handle *h, int fmt, int blocks, int iters, void *scratch);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPPS_B200_H */

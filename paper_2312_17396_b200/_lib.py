@@ -1,0 +1,241 @@
+"""ctypes binding of the C-ABI in include/mpps_b200.h.
+
+The shared library is built in-tree (``__graft_entry__.build()`` or
+``python -m paper_2312_17396_b200.build``) at
+``paper_2312_17396_b200/_lib/libmpps_b200.so``.  There is no fallback: if the
+library is missing or a call fails, the error is raised with the library's
+own message.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from typing import Optional
+
+from .precision import DimensionError, MatBatch, UnsupportedPrecisionError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libmpps_b200.so")
+
+MPPS_OK, MPPS_EINVAL, MPPS_EFMT, MPPS_ECUDA = 0, 1, 2, 3
+
+EXPORTED = (
+    "mpps_version", "mpps_create", "mpps_destroy", "mpps_set_stream",
+    "mpps_last_error", "mpps_launch_count", "mpps_convert", "mpps_gemm",
+    "mpps_axpy", "mpps_powers", "mpps_assemble_blocks", "mpps_one_norm",
+    "mpps_horner_step", "mpps_horner_scalar_top", "mpps_probe_fma",
+)
+
+
+class CMat(ctypes.Structure):
+    _fields_ = [
+        ("data", ctypes.c_void_p),
+        ("plane_stride", ctypes.c_longlong),
+        ("batch_stride", ctypes.c_longlong),
+        ("rows", ctypes.c_int),
+        ("cols", ctypes.c_int),
+        ("ld", ctypes.c_int),
+        ("batch", ctypes.c_int),
+        ("fmt", ctypes.c_int),
+    ]
+
+
+class MppsError(RuntimeError):
+    pass
+
+
+class MppsCudaError(MppsError):
+    pass
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library(path: Optional[str] = None):
+    """Load (once) and declare the C-ABI.  Raises if the .so is missing."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = path or LIB_PATH
+        if not os.path.exists(p):
+            raise ImportError(
+                f"B200 kernel library not built: {p} is missing. Run "
+                "`python -c 'import __graft_entry__ as g; g.build()'` "
+                "(no CPU fallback exists by design).")
+        lib = ctypes.CDLL(p)
+        P = ctypes.POINTER
+        vp, ip = ctypes.c_void_p, ctypes.c_int
+        mp = P(CMat)
+        lib.mpps_version.restype = ip
+        lib.mpps_create.argtypes = [ip, vp, P(vp)]
+        lib.mpps_destroy.argtypes = [vp]
+        lib.mpps_set_stream.argtypes = [vp, vp]
+        lib.mpps_last_error.argtypes = [vp]
+        lib.mpps_last_error.restype = ctypes.c_char_p
+        lib.mpps_launch_count.argtypes = [vp]
+        lib.mpps_launch_count.restype = ctypes.c_longlong
+        lib.mpps_convert.argtypes = [vp, mp, mp, vp, ip, vp]
+        lib.mpps_gemm.argtypes = [vp, mp, mp, mp, vp, ip]
+        lib.mpps_axpy.argtypes = [vp, P(ctypes.c_double), mp, mp, mp]
+        lib.mpps_powers.argtypes = [vp, mp, ip]
+        lib.mpps_assemble_blocks.argtypes = [vp, mp, ip, ip, vp, mp, vp]
+        lib.mpps_one_norm.argtypes = [vp, mp, vp]
+        lib.mpps_horner_step.argtypes = [vp, mp, mp, mp, mp, vp, ip, vp, vp, vp]
+        lib.mpps_horner_scalar_top.argtypes = [vp, P(ctypes.c_double), ip, mp, mp, mp, vp, ip, vp]
+        lib.mpps_probe_fma.argtypes = [vp, ip, ip, ip, vp]
+        for name in EXPORTED:
+            getattr(lib, name).restype = getattr(lib, name).restype or ip
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def cmat(m: MatBatch) -> CMat:
+    d = m.data
+    st = d.stride()
+    return CMat(d.data_ptr(), st[0], st[1], m.rows, m.cols, st[2], m.batch, m.fmt)
+
+
+def cmat_array(ms):
+    arr = (CMat * len(ms))()
+    for i, m in enumerate(ms):
+        arr[i] = cmat(m)
+    return arr
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+class Handle:
+    """One C handle per (device, stream).  Not thread-safe (like the ABI)."""
+
+    def __init__(self, device: int, stream_ptr: int):
+        self.lib = load_library()
+        h = ctypes.c_void_p()
+        rc = self.lib.mpps_create(device, ctypes.c_void_p(stream_ptr), ctypes.byref(h))
+        if rc != MPPS_OK:
+            raise MppsCudaError(f"mpps_create failed on device {device} (rc={rc})")
+        self.h = h
+        self.device = device
+        self.stream_ptr = stream_ptr
+        # optional per-launch CUDA-event probe (bench.py): key -> [(start, end)]
+        self.probe = None
+
+    def _ev(self, key):
+        if self.probe is None:
+            return None
+        import torch
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        self.probe.setdefault(key, []).append((a, b))
+        return b
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.lib.mpps_destroy(self.h)
+        except Exception:
+            pass
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.mpps_launch_count(self.h))
+
+    def _check(self, rc: int, what: str):
+        if rc == MPPS_OK:
+            return
+        msg = self.lib.mpps_last_error(self.h).decode(errors="replace")
+        if rc == MPPS_EINVAL:
+            shape_words = ("mat_mul", "mat_axpy", "shape", "operands must be", "batch mismatch",
+                           "must match", "must share")
+            if any(w in msg for w in shape_words):
+                raise DimensionError(f"{what}: {msg}")
+            raise ValueError(f"{what}: {msg}")
+        if rc == MPPS_EFMT:
+            raise UnsupportedPrecisionError(f"{what}: {msg}")
+        raise MppsCudaError(f"{what}: {msg}")
+
+    # --- operator seam -------------------------------------------------
+    def convert(self, src: MatBatch, dst: MatBatch, sel=None, exp=None):
+        c_src, c_dst = cmat(src), cmat(dst)
+        nsel = 0 if sel is None else sel.numel()
+        self._check(self.lib.mpps_convert(self.h, ctypes.byref(c_src), ctypes.byref(c_dst),
+                                          _ptr(sel), nsel, _ptr(exp)), "convert")
+
+    def gemm(self, A: MatBatch, B: MatBatch, C: MatBatch, sel=None):
+        a, b, c = cmat(A), cmat(B), cmat(C)
+        nsel = 0 if sel is None else sel.numel()
+        end = self._ev(("gemm", A.fmt, C.fmt, A.rows, B.cols, A.cols, nsel or C.batch))
+        self._check(self.lib.mpps_gemm(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
+                                       _ptr(sel), nsel), "mat_mul")
+        if end is not None:
+            end.record()
+
+    def axpy(self, alpha_words, A: MatBatch, B: MatBatch, C: MatBatch):
+        al = (ctypes.c_double * 4)(*[float(x) for x in alpha_words])
+        a, b, c = cmat(A), cmat(B), cmat(C)
+        self._check(self.lib.mpps_axpy(self.h, al, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)),
+                    "mat_axpy")
+
+    def powers(self, powers):
+        arr = cmat_array(powers)
+        self._check(self.lib.mpps_powers(self.h, arr, len(powers)), "powers")
+
+    def assemble_blocks(self, powers, m: int, coeff_dev, blocks, norms_dev):
+        parr, barr = cmat_array(powers), cmat_array(blocks)
+        self._check(self.lib.mpps_assemble_blocks(self.h, parr, len(powers), m, coeff_dev.data_ptr(),
+                                                  barr, norms_dev.data_ptr()), "assemble_blocks")
+
+    def one_norm(self, A: MatBatch, norms_dev):
+        a = cmat(A)
+        self._check(self.lib.mpps_one_norm(self.h, ctypes.byref(a), norms_dev.data_ptr()), "one_norm")
+
+    def horner_step(self, Y, phi, Bprev, out, sel=None, exp_y=None, exp_in=None, exp_out=None):
+        y, p, b, o = cmat(Y), cmat(phi), cmat(Bprev), cmat(out)
+        nsel = 0 if sel is None else sel.numel()
+        end = self._ev(("horner", Y.fmt, out.fmt, Y.rows, Y.rows, Y.rows, nsel or out.batch))
+        self._check(self.lib.mpps_horner_step(self.h, ctypes.byref(y), ctypes.byref(p), ctypes.byref(b),
+                                              ctypes.byref(o), _ptr(sel), nsel, _ptr(exp_y), _ptr(exp_in),
+                                              _ptr(exp_out)), "horner_step")
+        if end is not None:
+            end.record()
+
+    def horner_scalar_top(self, bm_words, fmt_top: int, Y, Bprev, out, sel=None, exp_out=None):
+        bm = (ctypes.c_double * 4)(*[float(x) for x in bm_words])
+        y, b, o = cmat(Y), cmat(Bprev), cmat(out)
+        nsel = 0 if sel is None else sel.numel()
+        self._check(self.lib.mpps_horner_scalar_top(self.h, bm, fmt_top, ctypes.byref(y), ctypes.byref(b),
+                                                    ctypes.byref(o), _ptr(sel), nsel, _ptr(exp_out)),
+                    "horner_scalar_top")
+
+
+    def probe_fma(self, fmt: int, blocks: int, iters: int, scratch):
+        self._check(self.lib.mpps_probe_fma(self.h, fmt, blocks, iters, scratch.data_ptr()), "probe_fma")
+
+
+_handles = {}
+
+
+def handle_for(device=None) -> Handle:
+    """The handle bound to torch's current stream on ``device``."""
+    import torch
+    if not torch.cuda.is_available():
+        raise MppsCudaError("no CUDA device: the B200 path has no CPU fallback")
+    dev = torch.cuda.current_device() if device is None else (
+        device.index if hasattr(device, "index") and device.index is not None else int(device)
+        if not hasattr(device, "type") else torch.cuda.current_device())
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    key = (dev, stream, threading.get_ident())
+    h = _handles.get(key)
+    if h is None:
+        h = Handle(dev, stream)
+        _handles[key] = h
+    return h
+
+
+def total_launches() -> int:
+    return sum(h.launches for h in _handles.values())

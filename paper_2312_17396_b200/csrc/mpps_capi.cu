@@ -1,0 +1,623 @@
+// C-ABI implementation of include/mpps_b200.h: kernel launches for the
+// mixed-precision Paterson-Stockmeyer hot path on sm_100a.
+//
+// Kernels in this file (GEMMs are in gemm.cuh):
+//   convert_kernel      round_to / format conversion      precision.py:153-157
+//   axpy_kernel         mat_axpy                          precision.py:187-197
+//   assemble_kernel     assemble_block x (r+1) + column   engine.py:127-154,
+//                       abs-sum partials of B_i and Y     precision.py:235-249
+//   colsum_kernel       column abs-sum partials (one_norm)
+//   norm_reduce_kernel  deterministic chunk sum + column max
+//   scalar_top_kernel   K3: Y*(b_m I) == RN(b_m Y)         engine.py:132, 249-251
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdarg.h>
+#include <string.h>
+
+#include "../../include/mpps_b200.h"
+#include "gemm.cuh"
+
+using namespace mpps;
+
+struct mpps_handle {
+  int device;
+  cudaStream_t stream;
+  long long launches;
+  char err[512];
+};
+
+namespace {
+
+constexpr int kMaxPowers = 32;
+constexpr int kMaxBlocks = MPPS_MAX_BLOCKS;
+constexpr int kRowsPerChunk = 32;
+
+int set_err(mpps_handle *h, int code, const char *fmt, ...) {
+  if (h) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(h->err, sizeof(h->err), fmt, ap);
+    va_end(ap);
+  }
+  return code;
+}
+
+int fmt_index(int digits) {
+  switch (digits) {
+    case MPPS_FP32: return F32;
+    case MPPS_FP64: return F64;
+    case MPPS_DD: return DD;
+    case MPPS_QD: return QD;
+    default: return -1;
+  }
+}
+int fmt_words(int fi) { return fi == QD ? 4 : (fi == DD ? 2 : 1); }
+
+MatRef ref_of(const mpps_mat *m) {
+  MatRef r;
+  r.data = m->data;
+  r.plane = m->plane_stride;
+  r.bstride = m->batch_stride;
+  r.ld = m->ld;
+  r.words = fmt_words(fmt_index(m->fmt));
+  return r;
+}
+
+int check_mat(mpps_handle *h, const mpps_mat *m, const char *name) {
+  if (!m) return set_err(h, MPPS_EINVAL, "%s: null matrix", name);
+  if (fmt_index(m->fmt) < 0) return set_err(h, MPPS_EFMT, "%s: unsupported format %d", name, m->fmt);
+  if (!m->data) return set_err(h, MPPS_EINVAL, "%s: null data pointer", name);
+  if (m->rows < 0 || m->cols < 0 || m->ld < m->cols || m->batch < 0)
+    return set_err(h, MPPS_EINVAL, "%s: bad shape %dx%d ld=%d batch=%d", name, m->rows, m->cols, m->ld, m->batch);
+  return MPPS_OK;
+}
+
+int after_launch(mpps_handle *h, const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  h->launches++;
+  return MPPS_OK;
+}
+
+// ----------------------------------------------------------- value helpers
+__device__ __forceinline__ mp::qd load_any(const MatRef &m, long long off, int fi) {
+  if (fi == F32) return mp::qd_from_d((double)((const float *)m.data)[off]);
+  return load_qd(m, off);
+}
+
+// Exact RN into format FT with an unbounded exponent (the reference's MPFR
+// semantics), returned as a qd holding the rounded value.
+template <int FT>
+__device__ __forceinline__ mp::qd round_unbounded(const mp::qd &v) {
+  if constexpr (FT == F32) {
+    mp::dd d = mp::qd_to_dd(v);
+    if (d.hi == 0.0 || !isfinite(d.hi)) return mp::qd_from_d((double)(float)d.hi);
+    int k = 0;
+    frexp(d.hi, &k);
+    mp::dd s = mp::dd_ldexp(d, -k);         // |s| in [0.5, 1): fp32 normal range
+    float f = mp::dd_to_float(s.hi, s.lo);
+    return mp::qd_from_d(ldexp((double)f, k));
+  } else if constexpr (FT == F64) {
+    return mp::qd_from_d(mp::qd_to_dd(v).hi);
+  } else if constexpr (FT == DD) {
+    return mp::qd_from_dd(mp::qd_to_dd(v));
+  } else {
+    return v;
+  }
+}
+
+// Working-format value types for the assembly kernel.
+template <int WF> struct WV;
+template <> struct WV<F64> {
+  using T = double;
+  static __device__ __forceinline__ T zero() { return 0.0; }
+  static __device__ __forceinline__ T from(const mp::qd &q) { return q.x[0]; }
+  static __device__ __forceinline__ T axpy(T a, T x, T y) { return __dadd_rn(__dmul_rn(a, x), y); }
+  static __device__ __forceinline__ double hi(T v) { return v; }
+  static __device__ __forceinline__ void store(const MatRef &m, long long off, T v) { ((double *)m.data)[off] = v; }
+};
+template <> struct WV<DD> {
+  using T = mp::dd;
+  static __device__ __forceinline__ T zero() { return mp::dd_make(0.0, 0.0); }
+  static __device__ __forceinline__ T from(const mp::qd &q) { return mp::dd_make(q.x[0], q.x[1]); }
+  static __device__ __forceinline__ T axpy(T a, T x, T y) { return mp::dd_add(mp::dd_mul(a, x), y); }
+  static __device__ __forceinline__ double hi(T v) { return v.hi; }
+  static __device__ __forceinline__ void store(const MatRef &m, long long off, T v) {
+    double *p = (double *)m.data + off; p[0] = v.hi; p[m.plane] = v.lo;
+  }
+};
+template <> struct WV<QD> {
+  using T = mp::qd;
+  static __device__ __forceinline__ T zero() { return mp::qd_make(0.0, 0.0, 0.0, 0.0); }
+  static __device__ __forceinline__ T from(const mp::qd &q) { return q; }
+  static __device__ __forceinline__ T axpy(T a, T x, T y) { return mp::qd_add(mp::qd_mul(a, x), y); }
+  static __device__ __forceinline__ double hi(T v) { return v.x[0]; }
+  static __device__ __forceinline__ void store(const MatRef &m, long long off, T v) {
+    double *p = (double *)m.data + off;
+    p[0] = v.x[0]; p[m.plane] = v.x[1]; p[2 * m.plane] = v.x[2]; p[3 * m.plane] = v.x[3];
+  }
+};
+
+// ------------------------------------------------------------- kernels
+struct ConvertArgs {
+  MatRef src, dst;
+  int rows, cols, src_fi;
+  const int *sel, *exp;
+};
+
+template <int FO>
+__global__ void convert_kernel(const ConvertArgs a) {
+  const int b = a.sel ? a.sel[blockIdx.z] : (int)blockIdx.z;
+  const long long total = (long long)a.rows * a.cols;
+  const int e = a.exp ? a.exp[b] : 0;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t / a.cols), j = (int)(t % a.cols);
+    mp::qd v = load_any(a.src, (long long)b * a.src.bstride + (long long)i * a.src.ld + j, a.src_fi);
+    store_fmt<FO>(a.dst, (long long)b * a.dst.bstride + (long long)i * a.dst.ld + j, v, e);
+  }
+}
+
+struct AxpyArgs {
+  MatRef A, B, C;
+  int rows, cols;
+  double alpha[4];
+};
+
+template <int F>
+__global__ void axpy_kernel(const AxpyArgs a) {
+  const int b = blockIdx.z;
+  const long long total = (long long)a.rows * a.cols;
+  mp::qd al = mp::qd_renorm(a.alpha[0], a.alpha[1], a.alpha[2], a.alpha[3]);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t / a.cols), j = (int)(t % a.cols);
+    const long long oa = (long long)b * a.A.bstride + (long long)i * a.A.ld + j;
+    const long long ob = (long long)b * a.B.bstride + (long long)i * a.B.ld + j;
+    const long long oc = (long long)b * a.C.bstride + (long long)i * a.C.ld + j;
+    if constexpr (F == F32) {
+      float alf = mp::dd_to_float(mp::qd_to_dd(al).hi, mp::qd_to_dd(al).lo);
+      ((float *)a.C.data)[oc] = __fadd_rn(__fmul_rn(alf, ((const float *)a.A.data)[oa]),
+                                          ((const float *)a.B.data)[ob]);
+    } else {
+      using V = WV<F>;
+      typename V::T r = V::axpy(V::from(al), V::from(load_qd(a.A, oa)), V::from(load_qd(a.B, ob)));
+      V::store(a.C, oc, r);
+    }
+  }
+}
+
+struct AssembleArgs {
+  MatRef P[kMaxPowers];   // X^1..X^s
+  MatRef Bk[kMaxBlocks];  // B_0..B_r
+  const double *coeff;    // (m+1) x 4 words
+  double *partial;        // [batch][nchunk][r+2][n]
+  int n, s, m, r, nchunk;
+};
+
+template <int WF>
+__global__ void __launch_bounds__(128) assemble_kernel(const AssembleArgs a) {
+  using V = WV<WF>;
+  using T = typename V::T;
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  const int chunk = blockIdx.y, b = blockIdx.z;
+  const int n = a.n, s = a.s, m = a.m, r = a.r;
+  if (col >= n) return;
+  const int full = m / s;
+  double cs[kMaxBlocks + 1];
+#pragma unroll
+  for (int k = 0; k <= kMaxBlocks; ++k) cs[k] = 0.0;
+  const int row0 = chunk * kRowsPerChunk;
+  const int row1 = min(n, row0 + kRowsPerChunk);
+  for (int row = row0; row < row1; ++row) {
+    T acc[kMaxBlocks];
+#pragma unroll
+    for (int k = 0; k < kMaxBlocks; ++k) {
+      if (k <= r) {
+        const double *c = a.coeff + 4 * (s * k);
+        acc[k] = (row == col) ? V::from(mp::qd_make(__ldg(c), __ldg(c + 1), __ldg(c + 2), __ldg(c + 3)))
+                              : V::zero();
+      }
+    }
+    for (int j = 1; j < s; ++j) {
+      const MatRef &P = a.P[j - 1];
+      T x = V::from(load_qd(P, (long long)b * P.bstride + (long long)row * P.ld + col));
+#pragma unroll
+      for (int k = 0; k < kMaxBlocks; ++k) {
+        if (k <= r) {
+          const int hi = (k < full) ? s - 1 : m - s * full;
+          if (j <= hi) {
+            const double *c = a.coeff + 4 * (s * k + j);
+            T cf = V::from(mp::qd_make(__ldg(c), __ldg(c + 1), __ldg(c + 2), __ldg(c + 3)));
+            acc[k] = V::axpy(cf, x, acc[k]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxBlocks; ++k) {
+      if (k <= r) {
+        const MatRef &B = a.Bk[k];
+        V::store(B, (long long)b * B.bstride + (long long)row * B.ld + col, acc[k]);
+        cs[k] += fabs(V::hi(acc[k]));
+      }
+    }
+    const MatRef &Y = a.P[s - 1];
+    cs[kMaxBlocks] += fabs(((const double *)Y.data)[(long long)b * Y.bstride + (long long)row * Y.ld + col]);
+  }
+  double *out = a.partial + ((long long)b * a.nchunk + chunk) * (long long)(r + 2) * n;
+#pragma unroll
+  for (int k = 0; k < kMaxBlocks; ++k)
+    if (k <= r) out[(long long)k * n + col] = cs[k];
+  out[(long long)(r + 1) * n + col] = cs[kMaxBlocks];
+}
+
+struct ColsumArgs {
+  MatRef A;
+  int rows, cols, fi, nchunk;
+  double *partial;  // [batch][nchunk][cols]
+};
+
+__global__ void colsum_kernel(const ColsumArgs a) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  const int chunk = blockIdx.y, b = blockIdx.z;
+  if (col >= a.cols) return;
+  const int row0 = chunk * kRowsPerChunk, row1 = min(a.rows, row0 + kRowsPerChunk);
+  double s = 0.0;
+  for (int row = row0; row < row1; ++row) {
+    const long long off = (long long)b * a.A.bstride + (long long)row * a.A.ld + col;
+    s += fabs(a.fi == F32 ? (double)((const float *)a.A.data)[off] : ((const double *)a.A.data)[off]);
+  }
+  a.partial[((long long)b * a.nchunk + chunk) * a.cols + col] = s;
+}
+
+// norms[b][k] = max_col sum_chunk partial[b][chunk][k][col]  (fixed order)
+__global__ void norm_reduce_kernel(const double *partial, double *norms, int nblk, int nchunk, int cols) {
+  const int k = blockIdx.x, b = blockIdx.y;
+  double best = 0.0;
+  for (int col = threadIdx.x; col < cols; col += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < nchunk; ++c)
+      s += partial[(((long long)b * nchunk + c) * nblk + k) * cols + col];
+    best = fmax(best, s);
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = best;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) norms[(long long)b * nblk + k] = red[0];
+}
+
+struct ScalarTopArgs {
+  MatRef Y, Bp, out;
+  int n, wf;
+  double bm[4];
+  const int *sel, *exp_out;
+};
+
+template <int FT, int FO>
+__global__ void scalar_top_kernel(const ScalarTopArgs a) {
+  const int b = a.sel ? a.sel[blockIdx.z] : (int)blockIdx.z;
+  const long long total = (long long)a.n * a.n;
+  const int eo = a.exp_out ? a.exp_out[b] : 0;
+  const mp::qd bm = mp::qd_make(a.bm[0], a.bm[1], a.bm[2], a.bm[3]);
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t / a.n), j = (int)(t % a.n);
+    mp::qd y = load_qd(a.Y, (long long)b * a.Y.bstride + (long long)i * a.Y.ld + j);
+    mp::qd prod;
+    if (a.wf == QD) {
+      prod = mp::qd_mul(bm, y);
+    } else {
+      prod = mp::qd_from_dd(mp::dd_mul(mp::dd_make(bm.x[0], bm.x[1]), mp::dd_make(y.x[0], y.x[1])));
+    }
+    mp::qd tv = round_unbounded<FT>(prod);
+    mp::qd bv = load_qd(a.Bp, (long long)b * a.Bp.bstride + (long long)i * a.Bp.ld + j);
+    store_fmt<FO>(a.out, (long long)b * a.out.bstride + (long long)i * a.out.ld + j, horner_add<FO>(bv, tv), eo);
+  }
+}
+
+// --------------------------------------------------------- GEMM launches
+template <int F, int FO, int MODE>
+int launch_gemm(mpps_handle *h, const GemmArgs &g, int nb) {
+  constexpr size_t smem = gemm_smem_bytes<F>();
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<F, FO, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "gemm attr: %s", cudaGetErrorString(e));
+    configured = true;
+  }
+  dim3 grid((g.N + Tile<F>::BN - 1) / Tile<F>::BN, (g.M + Tile<F>::BM - 1) / Tile<F>::BM, nb);
+  if (grid.x == 0 || grid.y == 0 || nb == 0) return MPPS_OK;
+  gemm_kernel<F, FO, MODE><<<grid, kThreads, smem, h->stream>>>(g);
+  return after_launch(h, "gemm_kernel");
+}
+
+int dispatch_gemm(mpps_handle *h, int fi, int fo, int mode, const GemmArgs &g, int nb) {
+  if (mode == 0) {
+    switch (fi) {
+      case F32: return launch_gemm<F32, F32, 0>(h, g, nb);
+      case F64: return launch_gemm<F64, F64, 0>(h, g, nb);
+      case DD: return launch_gemm<DD, DD, 0>(h, g, nb);
+      case QD: return launch_gemm<QD, QD, 0>(h, g, nb);
+    }
+  } else {
+#define CASE(A, B) \
+  if (fi == A && fo == B) return launch_gemm<A, B, 1>(h, g, nb);
+    CASE(F32, F32) CASE(F32, F64) CASE(F32, DD) CASE(F32, QD)
+    CASE(F64, F64) CASE(F64, DD) CASE(F64, QD)
+    CASE(DD, DD) CASE(DD, QD)
+    CASE(QD, QD)
+#undef CASE
+  }
+  return set_err(h, MPPS_EFMT, "no GEMM for level formats %d -> %d (output must be at least as wide)", fi, fo);
+}
+
+// Pipe-peak probes (bench.py roofline denominators): 8 independent FMA
+// chains per thread, full-chip grid.  2 flops per FMA.
+template <typename T>
+__global__ void __launch_bounds__(256) fma_probe_kernel(T *out, int iters, T a, T b) {
+  T c[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) c[k] = (T)(threadIdx.x + k);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k] = fma(c[k], a, b);
+  }
+  T s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += c[k];
+  if (s == (T)-1.2345) out[0] = s;  // keep the chains live
+}
+
+int ew_grid(long long total) {
+  long long g = (total + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace
+
+// ===================================================================== ABI
+extern "C" {
+
+int mpps_version(void) { return 100; }
+
+int mpps_create(int device, void *stream, mpps_handle **out) {
+  if (!out) return MPPS_EINVAL;
+  mpps_handle *h = new mpps_handle();
+  h->device = device;
+  h->stream = (cudaStream_t)stream;
+  h->launches = 0;
+  h->err[0] = 0;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete h;
+    return MPPS_ECUDA;
+  }
+  *out = h;
+  return MPPS_OK;
+}
+
+int mpps_destroy(mpps_handle *h) {
+  delete h;
+  return MPPS_OK;
+}
+
+int mpps_set_stream(mpps_handle *h, void *stream) {
+  if (!h) return MPPS_EINVAL;
+  h->stream = (cudaStream_t)stream;
+  return MPPS_OK;
+}
+
+const char *mpps_last_error(const mpps_handle *h) { return h ? h->err : "null handle"; }
+
+long long mpps_launch_count(const mpps_handle *h) { return h ? h->launches : 0; }
+
+int mpps_convert(mpps_handle *h, const mpps_mat *src, mpps_mat *dst, const int *sel, int nsel,
+                 const int *exp) {
+  int rc;
+  if ((rc = check_mat(h, src, "convert.src")) || (rc = check_mat(h, dst, "convert.dst"))) return rc;
+  if (src->rows != dst->rows || src->cols != dst->cols)
+    return set_err(h, MPPS_EINVAL, "convert: shape %dx%d vs %dx%d", src->rows, src->cols, dst->rows, dst->cols);
+  int nb = sel ? nsel : src->batch;
+  if (!sel && dst->batch != src->batch) return set_err(h, MPPS_EINVAL, "convert: batch mismatch");
+  if (nb == 0 || src->rows == 0 || src->cols == 0) return MPPS_OK;
+  ConvertArgs a;
+  a.src = ref_of(src); a.dst = ref_of(dst);
+  a.rows = src->rows; a.cols = src->cols; a.src_fi = fmt_index(src->fmt);
+  a.sel = sel; a.exp = exp;
+  dim3 grid(ew_grid((long long)a.rows * a.cols / 4 + 1), 1, nb);
+  switch (fmt_index(dst->fmt)) {
+    case F32: convert_kernel<F32><<<grid, 256, 0, h->stream>>>(a); break;
+    case F64: convert_kernel<F64><<<grid, 256, 0, h->stream>>>(a); break;
+    case DD: convert_kernel<DD><<<grid, 256, 0, h->stream>>>(a); break;
+    case QD: convert_kernel<QD><<<grid, 256, 0, h->stream>>>(a); break;
+  }
+  return after_launch(h, "convert_kernel");
+}
+
+int mpps_gemm(mpps_handle *h, const mpps_mat *A, const mpps_mat *B, mpps_mat *C, const int *sel, int nsel) {
+  int rc;
+  if ((rc = check_mat(h, A, "gemm.A")) || (rc = check_mat(h, B, "gemm.B")) || (rc = check_mat(h, C, "gemm.C")))
+    return rc;
+  if (A->fmt != B->fmt || A->fmt != C->fmt)
+    return set_err(h, MPPS_EFMT, "gemm: operand formats %d,%d,%d differ", A->fmt, B->fmt, C->fmt);
+  if (A->cols != B->rows || C->rows != A->rows || C->cols != B->cols)
+    return set_err(h, MPPS_EINVAL, "mat_mul: (%d, %d) x (%d, %d) -> (%d, %d)", A->rows, A->cols, B->rows, B->cols,
+                   C->rows, C->cols);
+  GemmArgs g;
+  memset(&g, 0, sizeof(g));
+  g.M = A->rows; g.N = B->cols; g.K = A->cols;
+  g.A = ref_of(A); g.B = ref_of(B); g.C = ref_of(C);
+  g.sel = sel;
+  int nb = sel ? nsel : C->batch;
+  int fi = fmt_index(A->fmt);
+  return dispatch_gemm(h, fi, fi, 0, g, nb);
+}
+
+int mpps_axpy(mpps_handle *h, const double *alpha, const mpps_mat *A, const mpps_mat *B, mpps_mat *C) {
+  int rc;
+  if ((rc = check_mat(h, A, "axpy.A")) || (rc = check_mat(h, B, "axpy.B")) || (rc = check_mat(h, C, "axpy.C")))
+    return rc;
+  if (!alpha) return set_err(h, MPPS_EINVAL, "axpy: null alpha");
+  if (A->rows != B->rows || A->cols != B->cols || C->rows != A->rows || C->cols != A->cols)
+    return set_err(h, MPPS_EINVAL, "mat_axpy: (%d, %d) vs (%d, %d)", A->rows, A->cols, B->rows, B->cols);
+  if (A->fmt != B->fmt || A->fmt != C->fmt) return set_err(h, MPPS_EFMT, "axpy: formats differ");
+  AxpyArgs a;
+  a.A = ref_of(A); a.B = ref_of(B); a.C = ref_of(C);
+  a.rows = A->rows; a.cols = A->cols;
+  for (int i = 0; i < 4; ++i) a.alpha[i] = alpha[i];
+  if (C->batch == 0 || a.rows == 0 || a.cols == 0) return MPPS_OK;
+  dim3 grid(ew_grid((long long)a.rows * a.cols / 4 + 1), 1, C->batch);
+  switch (fmt_index(C->fmt)) {
+    case F32: axpy_kernel<F32><<<grid, 256, 0, h->stream>>>(a); break;
+    case F64: axpy_kernel<F64><<<grid, 256, 0, h->stream>>>(a); break;
+    case DD: axpy_kernel<DD><<<grid, 256, 0, h->stream>>>(a); break;
+    case QD: axpy_kernel<QD><<<grid, 256, 0, h->stream>>>(a); break;
+  }
+  return after_launch(h, "axpy_kernel");
+}
+
+int mpps_powers(mpps_handle *h, mpps_mat *powers, int s) {
+  if (!powers || s < 1) return set_err(h, MPPS_EINVAL, "powers: need s >= 1");
+  for (int k = 1; k < s; ++k) {
+    int rc = mpps_gemm(h, &powers[k - 1], &powers[0], &powers[k], nullptr, 0);
+    if (rc) return rc;
+  }
+  return MPPS_OK;
+}
+
+int mpps_assemble_blocks(mpps_handle *h, const mpps_mat *powers, int s, int m, const double *coeff,
+                         mpps_mat *blocks, double *norms) {
+  if (!powers || !blocks || !coeff || !norms) return set_err(h, MPPS_EINVAL, "assemble: null argument");
+  if (s < 1 || s > kMaxPowers || m < s) return set_err(h, MPPS_EINVAL, "need 1 <= s <= series degree (s=%d m=%d)", s, m);
+  const int r = m / s;
+  if (r + 1 > kMaxBlocks) return set_err(h, MPPS_EINVAL, "assemble: r+1=%d exceeds %d blocks", r + 1, kMaxBlocks);
+  const int wf = fmt_index(powers[0].fmt);
+  if (wf == F32) return set_err(h, MPPS_EFMT, "assemble: working format must be fp64, dd or qd");
+  AssembleArgs a;
+  memset(&a, 0, sizeof(a));
+  const int n = powers[0].rows, batch = powers[0].batch;
+  for (int k = 0; k < s; ++k) {
+    int rc = check_mat(h, &powers[k], "assemble.power");
+    if (rc) return rc;
+    if (powers[k].fmt != powers[0].fmt || powers[k].rows != n || powers[k].cols != n || powers[k].batch != batch)
+      return set_err(h, MPPS_EINVAL, "assemble: powers must share format and shape");
+    a.P[k] = ref_of(&powers[k]);
+  }
+  for (int k = 0; k <= r; ++k) {
+    int rc = check_mat(h, &blocks[k], "assemble.block");
+    if (rc) return rc;
+    if (blocks[k].fmt != powers[0].fmt || blocks[k].rows != n || blocks[k].cols != n || blocks[k].batch != batch)
+      return set_err(h, MPPS_EINVAL, "assemble: blocks must match the powers");
+    a.Bk[k] = ref_of(&blocks[k]);
+  }
+  if (n == 0 || batch == 0) return MPPS_OK;
+  a.coeff = coeff; a.n = n; a.s = s; a.m = m; a.r = r;
+  a.nchunk = (n + kRowsPerChunk - 1) / kRowsPerChunk;
+  size_t pbytes = sizeof(double) * (size_t)batch * a.nchunk * (r + 2) * n;
+  cudaError_t e = cudaMallocAsync((void **)&a.partial, pbytes, h->stream);
+  if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "assemble scratch: %s", cudaGetErrorString(e));
+  dim3 grid((n + 127) / 128, a.nchunk, batch);
+  switch (wf) {
+    case F64: assemble_kernel<F64><<<grid, 128, 0, h->stream>>>(a); break;
+    case DD: assemble_kernel<DD><<<grid, 128, 0, h->stream>>>(a); break;
+    case QD: assemble_kernel<QD><<<grid, 128, 0, h->stream>>>(a); break;
+  }
+  int rc = after_launch(h, "assemble_kernel");
+  if (rc) return rc;
+  norm_reduce_kernel<<<dim3(r + 2, batch), 256, 0, h->stream>>>(a.partial, norms, r + 2, a.nchunk, n);
+  rc = after_launch(h, "norm_reduce_kernel");
+  cudaFreeAsync(a.partial, h->stream);
+  return rc;
+}
+
+int mpps_one_norm(mpps_handle *h, const mpps_mat *A, double *norms) {
+  int rc = check_mat(h, A, "one_norm.A");
+  if (rc) return rc;
+  if (!norms) return set_err(h, MPPS_EINVAL, "one_norm: null output");
+  if (A->batch == 0 || A->cols == 0) return MPPS_OK;
+  ColsumArgs a;
+  a.A = ref_of(A); a.rows = A->rows; a.cols = A->cols; a.fi = fmt_index(A->fmt);
+  a.nchunk = (A->rows + kRowsPerChunk - 1) / kRowsPerChunk;
+  if (a.nchunk == 0) a.nchunk = 1;
+  size_t pbytes = sizeof(double) * (size_t)A->batch * a.nchunk * A->cols;
+  cudaError_t e = cudaMallocAsync((void **)&a.partial, pbytes, h->stream);
+  if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "one_norm scratch: %s", cudaGetErrorString(e));
+  colsum_kernel<<<dim3((A->cols + 127) / 128, a.nchunk, A->batch), 128, 0, h->stream>>>(a);
+  rc = after_launch(h, "colsum_kernel");
+  if (rc) return rc;
+  norm_reduce_kernel<<<dim3(1, A->batch), 256, 0, h->stream>>>(a.partial, norms, 1, a.nchunk, A->cols);
+  rc = after_launch(h, "norm_reduce_kernel");
+  cudaFreeAsync(a.partial, h->stream);
+  return rc;
+}
+
+int mpps_horner_step(mpps_handle *h, const mpps_mat *Y, const mpps_mat *phi, const mpps_mat *Bprev, mpps_mat *out,
+                     const int *sel, int nsel, const int *exp_y, const int *exp_in, const int *exp_out) {
+  int rc;
+  if ((rc = check_mat(h, Y, "horner.Y")) || (rc = check_mat(h, phi, "horner.phi")) ||
+      (rc = check_mat(h, Bprev, "horner.Bprev")) || (rc = check_mat(h, out, "horner.out")))
+    return rc;
+  if (Y->fmt != phi->fmt) return set_err(h, MPPS_EFMT, "horner: Y and phi formats differ (%d, %d)", Y->fmt, phi->fmt);
+  if (fmt_index(Bprev->fmt) == F32) return set_err(h, MPPS_EFMT, "horner: B_{j-1} must be at the working format");
+  const int n = Y->rows;
+  if (Y->cols != n || phi->rows != n || phi->cols != n || Bprev->rows != n || Bprev->cols != n || out->rows != n ||
+      out->cols != n)
+    return set_err(h, MPPS_EINVAL, "horner: all operands must be %dx%d", n, n);
+  GemmArgs g;
+  memset(&g, 0, sizeof(g));
+  g.M = n; g.N = n; g.K = n;
+  g.A = ref_of(Y); g.B = ref_of(phi); g.C = ref_of(out);
+  g.sel = sel;
+  g.epi.Bprev = ref_of(Bprev);
+  g.epi.exp_y = exp_y; g.epi.exp_in = exp_in; g.epi.exp_out = exp_out;
+  int nb = sel ? nsel : out->batch;
+  return dispatch_gemm(h, fmt_index(Y->fmt), fmt_index(out->fmt), 1, g, nb);
+}
+
+int mpps_horner_scalar_top(mpps_handle *h, const double *bm, int fmt_top, const mpps_mat *Y, const mpps_mat *Bprev,
+                           mpps_mat *out, const int *sel, int nsel, const int *exp_out) {
+  int rc;
+  if ((rc = check_mat(h, Y, "scalar_top.Y")) || (rc = check_mat(h, Bprev, "scalar_top.Bprev")) ||
+      (rc = check_mat(h, out, "scalar_top.out")))
+    return rc;
+  if (!bm) return set_err(h, MPPS_EINVAL, "scalar_top: null coefficient");
+  const int ft = fmt_index(fmt_top), fo = fmt_index(out->fmt), wf = fmt_index(Y->fmt);
+  if (ft < 0) return set_err(h, MPPS_EFMT, "scalar_top: bad level format %d", fmt_top);
+  if (wf == F32) return set_err(h, MPPS_EFMT, "scalar_top: Y must be at the working format");
+  if (fo < ft) return set_err(h, MPPS_EFMT, "scalar_top: output narrower than the level format");
+  ScalarTopArgs a;
+  a.Y = ref_of(Y); a.Bp = ref_of(Bprev); a.out = ref_of(out);
+  a.n = Y->rows; a.wf = wf;
+  for (int i = 0; i < 4; ++i) a.bm[i] = bm[i];
+  a.sel = sel; a.exp_out = exp_out;
+  int nb = sel ? nsel : out->batch;
+  if (nb == 0 || a.n == 0) return MPPS_OK;
+  dim3 grid(ew_grid((long long)a.n * a.n / 4 + 1), 1, nb);
+#define ST(A, B) \
+  if (ft == A && fo == B) scalar_top_kernel<A, B><<<grid, 256, 0, h->stream>>>(a); else
+  ST(F32, F32) ST(F32, F64) ST(F32, DD) ST(F32, QD) ST(F64, F64) ST(F64, DD) ST(F64, QD) ST(DD, DD) ST(DD, QD)
+  ST(QD, QD) { return set_err(h, MPPS_EFMT, "scalar_top: formats"); }
+#undef ST
+  return after_launch(h, "scalar_top_kernel");
+}
+
+int mpps_probe_fma(mpps_handle *h, int fmt, int blocks, int iters, void *scratch) {
+  if (!scratch || blocks < 1 || iters < 1) return set_err(h, MPPS_EINVAL, "probe: bad arguments");
+  if (fmt == MPPS_FP64)
+    fma_probe_kernel<double><<<blocks, 256, 0, h->stream>>>((double *)scratch, iters, 0.999999, 1e-7);
+  else if (fmt == MPPS_FP32)
+    fma_probe_kernel<float><<<blocks, 256, 0, h->stream>>>((float *)scratch, iters, 0.999999f, 1e-7f);
+  else
+    return set_err(h, MPPS_EFMT, "probe: fp32 or fp64 only");
+  return after_launch(h, "fma_probe_kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,548 @@
+"""Paterson-Stockmeyer evaluators on B200: the drop-in for engine.py.
+
+Same entry points, signatures, defaults, plan/report records and errors as
+pkg/src/mpps/engine.py:
+
+    ps_fixed(X, series, ctx, with_bound=False)                 engine.py:304-345
+    ps_mixed_general(X, series, ctx, delta=10., with_bound=False)  348-387
+    ps_mixed_exp(X, m, ctx, fix_params=True, delta=10., with_bound=False) 390-482
+    plan_only(X, series, ctx, delta=10., fix_params=True)          485-504
+
+``X`` is an (n, n) array (numpy / torch, host or device, or a reference
+``MPMatrix`` with real entries) or an (B, n, n) batch; a batch returns a
+``BatchReport`` whose entries are per-matrix ``EvaluationReport`` records
+(every matrix gets its own plan, exactly as if evaluated alone).
+
+Device pipeline per batch (one host sync, for the planner's norms):
+
+  1. convert X (fp64) -> working format (exact widening)           K4
+  2. X^2..X^s by GEMMs at the working format                        K1
+  3. one fused pass: B_0..B_r in index order + column abs-sums       K1b
+  4. norms -> host; bit-exact planner per matrix (planner.py)
+  5. matrix Horner, grouped by each matrix's level formats:
+     top level K3 (B_r = b_m I) or convert B_r; then r GEMMs whose
+     epilogue adds B_{j-1} and rounds into the level-(j-1) format     K2
+
+All arithmetic runs in the sm_100a kernels of libmpps_b200.so; this module
+only plans, allocates (torch caching allocator) and launches.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import time
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib
+from .bigfloat import MPF, exp_rn, fmt7, ln_rn, rn, to_fraction
+from .bounds import BoundInputs, thm21_bound, tau_sequence
+from .coefficients import (CoefficientSeries, coeff_words, eval_coeff,
+                           split_words, taylor_exp_coeffs)
+from .planner import (EvaluationPlan, cost_ratio, default_block_size,
+                      fixed_plan, hardware_lattice, matmul_counts,
+                      plan_precisions, snap_to_lattice)
+from .precision import (DD, FORMAT_NAME, FP32, FP64, NORM_CTX, QD,
+                        DimensionError, MatBatch, PrecisionCtx, as_fp64_batch)
+
+BUCKETS = ("power_formation", "norm_estimation", "mixed_horner", "coefficient_assembly")
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@dataclass
+class EvaluationReport:
+    """engine.py:87-108 (``result`` is a device ``MatBatch`` of batch 1)."""
+    result: MatBatch
+    plan: EvaluationPlan
+    matmuls_by_digits: Dict[int, int]
+    cost_ratio: float
+    savings: float
+    timing_buckets: Dict[str, float]
+    bound: Optional[MPF] = None
+    diagnostics: Dict[str, object] = field(default_factory=dict)
+
+    def to_json(self) -> str:
+        return json.dumps({
+            "plan": self.plan.to_dict(),
+            "matmuls_by_digits": {str(k): v for k, v in self.matmuls_by_digits.items()},
+            "cost_ratio": self.cost_ratio,
+            "savings": self.savings,
+            "timing_buckets": self.timing_buckets,
+            "bound": None if self.bound is None else fmt7(self.bound),
+            "diagnostics": self.diagnostics,
+        })
+
+    def result_numpy(self) -> np.ndarray:
+        return self.result.to_numpy()[0]
+
+
+class BatchReport(list):
+    """A list of per-matrix ``EvaluationReport`` plus the batched result."""
+
+    def __init__(self, reports, result: MatBatch, seconds: Dict[str, float]):
+        super().__init__(reports)
+        self.result = result
+        self.seconds = seconds
+
+
+# ---------------------------------------------------------------- timing
+class _Buckets:
+    """CUDA-event timing of the reference's four buckets (engine.py:268-280);
+    read once at the end, reported as fractions like the reference."""
+
+    def __init__(self, enabled: bool):
+        self.enabled = enabled
+        self.marks: List[Tuple[str, object, object]] = []
+        self._open = None
+
+    def start(self, name: str):
+        if not self.enabled:
+            return
+        torch = _torch()
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self._open = (name, ev)
+
+    def stop(self):
+        if not self.enabled or self._open is None:
+            return
+        torch = _torch()
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.marks.append((self._open[0], self._open[1], ev))
+        self._open = None
+
+    def seconds(self) -> Dict[str, float]:
+        out: Dict[str, float] = {}
+        if not self.enabled:
+            return out
+        _torch().cuda.synchronize()
+        for name, a, b in self.marks:
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b) * 1e-3
+        return out
+
+
+def _fractions(sec: Dict[str, float]) -> Dict[str, float]:
+    total = sum(sec.values())
+    if total <= 0:
+        return {k: 0.0 for k in BUCKETS}
+    return {k: sec.get(k, 0.0) / total for k in BUCKETS}
+
+
+# ------------------------------------------------------------- internals
+def _working_format(ctx: PrecisionCtx) -> int:
+    f = ctx.fmt
+    # fp32 working contexts (d <= 7) run at fp64: the block assembly and the
+    # planner norms need at least fp64; u_hw <= 10^-d still holds.
+    return FP64 if f == FP32 else f
+
+
+def _exp_for(norm: float) -> int:
+    """Exponent e with 2^e * norm ~ 1 (exact power-of-two level scaling)."""
+    if not (norm > 0) or not math.isfinite(norm):
+        return 0
+    return -int(round(math.log2(norm)))
+
+
+class _Workspace:
+    """Per-format ping-pong buffers for the Horner chain."""
+
+    def __init__(self, batch: int, n: int, device):
+        self.batch, self.n, self.device = batch, n, device
+        self.bufs: Dict[int, List[MatBatch]] = {}
+        self.turn: Dict[int, int] = {}
+
+    def next(self, fmt: int) -> MatBatch:
+        if fmt not in self.bufs:
+            self.bufs[fmt] = [MatBatch.empty(fmt, self.batch, self.n, device=self.device) for _ in range(2)]
+            self.turn[fmt] = 0
+        t = self.turn[fmt]
+        self.turn[fmt] = 1 - t
+        return self.bufs[fmt][t]
+
+
+@dataclass
+class _Prepared:
+    """Device state after power formation and block assembly."""
+    wf: int
+    s: int
+    r: int
+    m: int
+    powers: List[MatBatch]
+    blocks: List[MatBatch]
+    norms: np.ndarray          # (B, r+2) float64: ||B_0..B_r||, ||Y||
+    coeffs: np.ndarray         # (m+1, 4) words at the working precision
+
+
+def _prepare(h, Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: int,
+             timer: _Buckets, x_is_working: Optional[MatBatch] = None) -> _Prepared:
+    torch = _torch()
+    dev = Xt.device if Xt is not None else x_is_working.device
+    B = Xt.shape[0] if Xt is not None else x_is_working.batch
+    n = Xt.shape[1] if Xt is not None else x_is_working.rows
+    m = series.degree
+    r = m // s
+    cw = coeff_words(series, ctx)
+    coeffs = torch.from_numpy(cw).to(dev, non_blocking=True)
+    timer.start("power_formation")
+    powers = [MatBatch.empty(wf, B, n, device=dev) for _ in range(s)]
+    if x_is_working is not None:
+        if x_is_working.fmt == wf:
+            powers[0] = x_is_working
+        else:
+            h.convert(x_is_working, powers[0])
+    else:
+        h.convert(MatBatch(Xt.unsqueeze(0), FP64), powers[0])
+    if s > 1:
+        h.powers(powers)
+    timer.stop()
+    timer.start("coefficient_assembly")
+    blocks = [MatBatch.empty(wf, B, n, device=dev) for _ in range(r + 1)]
+    norms = torch.empty((B, r + 2), dtype=torch.float64, device=dev)
+    h.assemble_blocks(powers, m, coeffs, blocks, norms)
+    timer.stop()
+    timer.start("norm_estimation")
+    norms_h = norms.cpu().numpy()   # the one host sync of the pipeline
+    timer.stop()
+    return _Prepared(wf, s, r, m, powers, blocks, norms_h, cw)
+
+
+def _horner(h, prep: _Prepared, plans: List[EvaluationPlan], timer: _Buckets) -> MatBatch:
+    """horner_mixed (engine.py:243-252) for every matrix of the batch,
+    grouped by level-format tuple."""
+    torch = _torch()
+    wf, s, r, m = prep.wf, prep.s, prep.r, prep.m
+    Y = prep.powers[s - 1]
+    blocks = prep.blocks
+    B, n, dev = Y.batch, Y.rows, Y.device
+    result = MatBatch.empty(wf, B, n, device=dev)
+    timer.start("mixed_horner")
+    groups: Dict[Tuple[int, ...], List[int]] = {}
+    nil = []
+    for b, p in enumerate(plans):
+        if p.nilpotent:
+            nil.append(b)
+        else:
+            fm = (wf,) + tuple(p.level_formats[1:])
+            groups.setdefault(fm, []).append(b)
+    for b in nil:
+        result.data[:, b].copy_(blocks[0].data[:, b])
+    ws = _Workspace(B, n, dev)
+    scalar_top = (m % s == 0)
+    bm_words = prep.coeffs[m]
+    for fm, members in groups.items():
+        sel = torch.tensor(members, dtype=torch.int32).to(dev, non_blocking=True)
+        need_exp = FP32 in fm
+        exps = None
+        exp_y = None
+        if need_exp:
+            e = np.zeros((r + 1, B), dtype=np.int32)
+            ey = np.zeros(B, dtype=np.int32)
+            for b in members:
+                for j in range(1, r + 1):
+                    if fm[j] == FP32:
+                        e[j, b] = _exp_for(float(prep.norms[b, j]))
+                ey[b] = _exp_for(float(prep.norms[b, r + 1]))
+            exps = torch.from_numpy(e).to(dev, non_blocking=True)
+            exp_y = torch.from_numpy(ey).to(dev, non_blocking=True)
+
+        def ex(j):
+            return None if (exps is None or fm[j] != FP32) else exps[j]
+
+        ys: Dict[int, MatBatch] = {wf: Y}
+        for f in set(fm[1:]):
+            if f not in ys:
+                yf = MatBatch.empty(f, B, n, device=dev)
+                h.convert(Y, yf, sel, exp_y if f == FP32 else None)
+                ys[f] = yf
+        if scalar_top:
+            out = result if r - 1 == 0 else ws.next(fm[r - 1])
+            h.horner_scalar_top(bm_words, fm[r], Y, blocks[r - 1], out, sel, ex(r - 1))
+            phi, j0 = out, r - 1
+        else:
+            phi = ws.next(fm[r])
+            h.convert(blocks[r], phi, sel, ex(r))
+            j0 = r
+        for j in range(j0, 0, -1):
+            out = result if j - 1 == 0 else ws.next(fm[j - 1])
+            h.horner_step(ys[fm[j]], phi, blocks[j - 1], out, sel,
+                          exp_y if fm[j] == FP32 else None, ex(j), ex(j - 1))
+            phi = out
+    timer.stop()
+    return result
+
+
+def _input(X, device=None):
+    """(torch fp64 (B,n,n) on device or None, working MatBatch or None, single)."""
+    if isinstance(X, MatBatch):
+        return None, X, X.batch == 1
+    Xt, single = as_fp64_batch(X, device)
+    return Xt, None, single
+
+
+def _finish(result: MatBatch, plans, counts, sec, with_bound, single, extra_diag=None):
+    """Per-matrix reports (engine.py:295-301).  Nilpotent plans carry no
+    bound, as in the reference (engine.py:378-379, 473-474)."""
+    reports = []
+    frac = _fractions(sec)
+    n = result.rows
+    for b, p in enumerate(plans):
+        cr, sav = cost_ratio(p)
+        bound = _bound_for(p, n) if (with_bound and not p.nilpotent and p.r > 0) else None
+        lat = hardware_lattice(p.d_working)
+        diag = {"level_formats": [FORMAT_NAME[f] for f in p.level_formats],
+                "snapped_digits": list(snap_to_lattice(p, lat).level_digits) if p.d_working in lat else None}
+        if extra_diag:
+            diag.update(extra_diag)
+        res_b = result if single else result.select(b)
+        reports.append(EvaluationReport(result=res_b, plan=p, matmuls_by_digits=dict(counts[b]),
+                                        cost_ratio=cr, savings=sav, timing_buckets=frac,
+                                        bound=bound, diagnostics=diag))
+    if single:
+        return reports[0]
+    return BatchReport(reports, result, sec)
+
+
+def _bound_for(plan: EvaluationPlan, n: int) -> MPF:
+    """engine.py:283-292."""
+    u = PrecisionCtx(plan.d_working).unit_roundoff
+    nu = plan.nu
+    precisions = [u] + [plan.level_roundoffs[i - 1] for i in range(nu, plan.r + 1)]
+    inp = BoundInputs(n=n, precisions=tuple(precisions), norm_y=plan.norm_y,
+                      norm_bs=tuple(plan.norm_bs[nu - 1:]), s=plan.s, r=plan.r, nu=nu)
+    return thm21_bound(inp)
+
+
+def _check_square(Xt, Xw):
+    if Xt is not None:
+        return Xt.shape[0], Xt.shape[1]
+    if Xw.rows != Xw.cols:
+        raise DimensionError("X must be square")
+    return Xw.batch, Xw.rows
+
+
+# ------------------------------------------------------------ evaluators
+def ps_fixed(X, series: CoefficientSeries, ctx: PrecisionCtx, with_bound: bool = False,
+             timing: bool = True):
+    """Fixed-precision PS with s = ceil(sqrt(m)) (engine.py:304-345)."""
+    Xt, Xw, single = _input(X)
+    B, n = _check_square(Xt, Xw)
+    h = _lib.handle_for()
+    timer = _Buckets(timing)
+    d = ctx.decimal_digits
+    m = series.degree
+    wf = _working_format(ctx)
+    torch = _torch()
+    if m == 0:
+        dev = Xt.device if Xt is not None else Xw.device
+        res = MatBatch.zeros(wf, B, n, device=dev)
+        w = split_words(rn(Fraction(series.coeffs[0]), ctx.binary_precision))
+        idx = torch.arange(n, device=dev)
+        for k in range(res.words):
+            res.data[k][:, idx, idx] = w[k]
+        c0 = abs(rn(Fraction(series.coeffs[0]), ctx.binary_precision))
+        plans = [EvaluationPlan(s=1, r=0, nu=1, d_working=d, level_digits=(), level_roundoffs=(),
+                                tau_seq=(), norm_bs=(MPF(rn(c0, 54), 54),),
+                                norm_y=MPF(0, 64))] * B
+        return _finish(res, plans, [{}] * B, {}, False, single)
+    s = default_block_size(m)
+    prep = _prepare(h, Xt, series, ctx, wf, s, timer, Xw)
+    r = prep.r
+    plans = [fixed_plan(prep.norms[b, :r + 1], prep.norms[b, r + 1], ctx, s) for b in range(B)]
+    result = _horner(h, prep, plans, timer)
+    counts = [{d: s - 1 + r}] * B
+    return _finish(result, plans, counts, timer.seconds(), with_bound, single)
+
+
+def ps_mixed_general(X, series: CoefficientSeries, ctx: PrecisionCtx, delta: float = 10.0,
+                     with_bound: bool = False, timing: bool = True):
+    """Mixed-precision PS for decaying coefficients (engine.py:348-387)."""
+    Xt, Xw, single = _input(X)
+    B, n = _check_square(Xt, Xw)
+    m = series.degree
+    if m < 1:
+        raise ValueError("series degree must be >= 1")
+    h = _lib.handle_for()
+    timer = _Buckets(timing)
+    wf = _working_format(ctx)
+    s = default_block_size(m)
+    prep = _prepare(h, Xt, series, ctx, wf, s, timer, Xw)
+    return _mixed_tail(h, prep, ctx, delta, True, True, with_bound, single, timer)
+
+
+def _mixed_tail(h, prep, ctx, delta, apply_switch, fix_params, with_bound, single, timer,
+                extra_diag=None):
+    """Planner + Horner + report of the mixed evaluators (engine.py:376-387,
+    471-482)."""
+    d = ctx.decimal_digits
+    r, s = prep.r, prep.s
+    B = prep.norms.shape[0]
+    timer.start("norm_estimation")
+    plans = [plan_precisions(prep.norms[b, :r + 1], prep.norms[b, r + 1], ctx, delta, s=s,
+                             apply_switch=apply_switch, fix_params=fix_params) for b in range(B)]
+    timer.stop()
+    result = _horner(h, prep, plans, timer)
+    counts = [({d: s - 1} if p.nilpotent else matmul_counts(p)) for p in plans]
+    return _finish(result, plans, counts, timer.seconds(), with_bound, single, extra_diag)
+
+
+def ps_mixed_exp(X, m: int, ctx: PrecisionCtx, fix_params: bool = True, delta: float = 10.0,
+                 with_bound: bool = False, timing: bool = True):
+    """Mixed-precision PS for the order-m Taylor approximant of exp
+    (engine.py:390-482), including the growth branch (fix_params=False and
+    ||X||_1 <= s/e) and the explicit-powers degenerate case s == m."""
+    Xt, Xw, single = _input(X)
+    B, n = _check_square(Xt, Xw)
+    if m < 1:
+        raise ValueError("m must be >= 1")
+    series = taylor_exp_coeffs(m)
+    s = default_block_size(m)
+    if not fix_params:
+        # growth decisions are per matrix (host loop over norms), so the
+        # batch is split; the common fixed-s case stays batched.
+        norm_x = _one_norms(Xt, Xw)
+        grow = [float(v) <= s / math.e for v in norm_x]
+        if any(grow):
+            reps = []
+            for b in range(B):
+                xb = Xt[b:b + 1] if Xt is not None else None
+                wb = Xw.select(b) if Xw is not None else None
+                reps.append(_ps_mixed_exp_one(xb, wb, m, ctx, fix_params, delta, with_bound, timing,
+                                              grow[b], float(norm_x[b])))
+            if single:
+                return reps[0]
+            res = MatBatch(_torch().cat([r_.result.data for r_ in reps], dim=1), reps[0].result.fmt)
+            return BatchReport(reps, res, {})
+    if s == m:
+        return _explicit_powers(Xt, Xw, m, ctx, s, series, delta, True, fix_params, single, timing)
+    h = _lib.handle_for()
+    timer = _Buckets(timing)
+    wf = _working_format(ctx)
+    prep = _prepare(h, Xt, series, ctx, wf, s, timer, Xw)
+    return _mixed_tail(h, prep, ctx, delta, True, fix_params, with_bound, single, timer)
+
+
+def _one_norms(Xt, Xw) -> np.ndarray:
+    torch = _torch()
+    h = _lib.handle_for()
+    A = Xw if Xw is not None else MatBatch(Xt.unsqueeze(0), FP64)
+    out = torch.empty(A.batch, dtype=torch.float64, device=A.device)
+    h.one_norm(A, out)
+    return out.cpu().numpy()
+
+
+def _explicit_powers(Xt, Xw, m, ctx, s, series, delta, apply_switch, fix_params, single, timing):
+    """engine.py:439-459: p = B_0 + b_m Y with no Horner phase."""
+    torch = _torch()
+    h = _lib.handle_for()
+    timer = _Buckets(timing)
+    wf = _working_format(ctx)
+    d = ctx.decimal_digits
+    # blocks of the s == m layout: r = 1, B_0 = sum_{j<s} b_j X^j, B_1 = b_m I
+    prep = _prepare(h, Xt, series, ctx, wf, s, timer, Xw)
+    Y = prep.powers[s - 1]
+    res = MatBatch.empty(wf, Y.batch, Y.rows, device=Y.device)
+    timer.start("coefficient_assembly")
+    h.axpy(prep.coeffs[m], Y, prep.blocks[0], res)
+    timer.stop()
+    bm_norm = MPF(abs(rn(Fraction(series.coeffs[m]), NORM_CTX.binary_precision)), 54)
+    plans = []
+    for b in range(Y.batch):
+        p = plan_precisions((prep.norms[b, 0], bm_norm), prep.norms[b, prep.r + 1], ctx, delta, s=s,
+                            apply_switch=apply_switch, fix_params=fix_params)
+        plans.append(EvaluationPlan(
+            s=p.s, r=p.r, nu=p.nu, d_working=p.d_working, level_digits=p.level_digits,
+            level_roundoffs=p.level_roundoffs, tau_seq=p.tau_seq, norm_bs=p.norm_bs, norm_y=p.norm_y,
+            delta=delta, fix_params=fix_params, degenerate_levels=p.degenerate_levels,
+            nilpotent=p.nilpotent, explicit_powers=True))
+    counts = [{d: s - 1}] * Y.batch
+    return _finish(res, plans, counts, timer.seconds(), False, single)
+
+
+def _ps_mixed_exp_one(Xt, Xw, m, ctx, fix_params, delta, with_bound, timing, grow, norm_x):
+    """Single-matrix ps_mixed_exp with the growth branch (engine.py:417-437)."""
+    series = taylor_exp_coeffs(m)
+    s = default_block_size(m)
+    if not grow:
+        if s == m:
+            return _explicit_powers(Xt, Xw, m, ctx, s, series, delta, True, fix_params, True, timing)
+        h = _lib.handle_for()
+        timer = _Buckets(timing)
+        prep = _prepare(h, Xt, series, ctx, _working_format(ctx), s, timer, Xw)
+        return _mixed_tail(h, prep, ctx, delta, True, fix_params, with_bound, True, timer)
+    # growth: s increases while ||X^s|| > ||B_0|| ||X||^s (54-bit tests)
+    p54 = NORM_CTX.binary_precision
+    nx = rn(Fraction(norm_x), p54)
+    while s < m:
+        h = _lib.handle_for()
+        prep = _prepare(h, Xt, series.truncate(max(s, m)), ctx, _working_format(ctx), s,
+                        _Buckets(False), Xw)
+        nb0, ny = Fraction(float(prep.norms[0, 0])), Fraction(float(prep.norms[0, prep.r + 1]))
+        xs = exp_rn(rn(Fraction(s) * ln_rn(nx, p54), p54), p54) if nx > 0 else Fraction(0)
+        if ny <= rn(nb0 * xs, p54):
+            break
+        s += 1
+    if s == m:
+        return _explicit_powers(Xt, Xw, m, ctx, s, series, delta, False, fix_params, True, timing)
+    h = _lib.handle_for()
+    timer = _Buckets(timing)
+    prep = _prepare(h, Xt, series, ctx, _working_format(ctx), s, timer, Xw)
+    return _mixed_tail(h, prep, ctx, delta, False, fix_params, with_bound, True, timer)
+
+
+def plan_only(X, series: CoefficientSeries, ctx: PrecisionCtx, delta: float = 10.0,
+              fix_params: bool = True):
+    """Planner only (engine.py:485-504).  The reference forms powers and
+    blocks at the 16-digit NORM_CTX; the B200 build forms them in fp64 (the
+    nearest lattice format; the planner consumes orders of magnitude)."""
+    m = series.degree
+    if m < 1:
+        raise ValueError("series degree must be >= 1")
+    Xt, Xw, single = _input(X)
+    B, n = _check_square(Xt, Xw)
+    s = default_block_size(m)
+    h = _lib.handle_for()
+    prep = _prepare(h, Xt, series, NORM_CTX, FP64, s, _Buckets(False), Xw)
+    plans = [plan_precisions(prep.norms[b, :prep.r + 1], prep.norms[b, prep.r + 1], ctx, delta, s=s,
+                             apply_switch=True, fix_params=fix_params) for b in range(B)]
+    return plans[0] if single else plans
+
+
+def cos_argument(X, ctx: PrecisionCtx) -> MatBatch:
+    """harness.py:100-101: the cosine polynomial variable Z = fl(X X) at the
+    working precision (formed on device, returned as a working-format batch
+    ready for ps_mixed_general)."""
+    Xt, Xw, _ = _input(X)
+    wf = _working_format(ctx)
+    h = _lib.handle_for()
+    if Xw is None:
+        Xw = MatBatch(Xt.unsqueeze(0), FP64)
+    Xk = Xw
+    if Xw.fmt != wf:
+        Xk = MatBatch.empty(wf, Xw.batch, Xw.rows, device=Xw.device)
+        h.convert(Xw, Xk)
+    Z = MatBatch.empty(wf, Xk.batch, Xk.rows, device=Xk.device)
+    h.gemm(Xk, Xk, Z)
+    return Z
+
+
+def horner_mixed(Bs: Sequence[MatBatch], Y: MatBatch, plan: EvaluationPlan) -> MatBatch:
+    """engine.py:243-252 on device blocks: phi = B_r; phi = RN_{j-1}(B_{j-1}
+    + RN_j(Y phi)), j = r..1.  Bs and Y at the working format, batch 1."""
+    if len(Bs) != plan.r + 1:
+        raise ValueError("need r+1 coefficient blocks")
+    if plan.r == 0:
+        return Bs[0]
+    h = _lib.handle_for()
+    norms = np.array([[float(b) for b in plan.norm_bs] + [float(plan.norm_y)]] * Y.batch)
+    prep = _Prepared(Y.fmt, plan.s, plan.r, plan.r * plan.s + 1, [Y] * plan.s, list(Bs), norms,
+                     np.zeros((plan.r * plan.s + 2, 4)))
+    return _horner(h, prep, [plan] * Y.batch, _Buckets(False))

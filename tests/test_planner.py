@@ -1,0 +1,151 @@
+"""Host planner (planner.py) vs the C MPFR restatement of engine.py:157-215
+(oracle/mpfr_oracle.c orc_plan), plus the reference's own planner tests
+(test_engine.py:93-147, 290-326) and cost-ratio goldens."""
+import math
+import random
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from paper_2312_17396_b200 import (EvaluationPlan, PrecisionCtx, cost_ratio, plan_precisions,
+                                   snap_to_lattice, tau_sequence, taylor_exp_coeffs)
+from paper_2312_17396_b200.bigfloat import MPF, rn
+from paper_2312_17396_b200.planner import fixed_plan
+
+
+def _norms2_to_frac(n2):
+    return [Fraction(a) + Fraction(b) for a, b in n2]
+
+
+def _random_norms(rng, r):
+    """Decaying block norms like the PS blocks of a Taylor series, with
+    54-bit values (as one_norm produces) written as (hi, lo) pairs."""
+    out = []
+    y = 10 ** rng.uniform(-3, 2)
+    b = 10 ** rng.uniform(-2, 4)
+    for i in range(r + 1):
+        v = rn(Fraction(b), 54)
+        if rng.random() < 0.3:
+            v = rn(Fraction(b) * (1 + Fraction(rng.randrange(1 << 20), 1 << 53)), 54)
+        hi = float(v)
+        out.append((hi, float(v - Fraction(hi))))
+        b = b * 10 ** rng.uniform(-12, 0.5)
+    yv = rn(Fraction(y), 54)
+    out.append((float(yv), float(yv - Fraction(float(yv)))))
+    return np.array(out)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_planner_matches_mpfr_oracle_random(oracle_lib, seed):
+    rng = random.Random(seed)
+    count = 5000
+    for _ in range(count):
+        r = rng.randint(1, 13)
+        d = rng.choice([15, 16, 31, 32, 63, 64, 128])
+        delta = rng.choice([10.0, 10.0, 2.0, 100.0])
+        n2 = _random_norms(rng, r)
+        fr = _norms2_to_frac(n2)
+        p = plan_precisions(fr[:r + 1], fr[r + 1], PrecisionCtx(d), delta, s=3)
+        dig, nu, nil, _ = oracle_lib.plan_digits(n2, d, delta)
+        assert p.level_digits == dig and p.nu == nu and p.nilpotent == nil, (fr, d, delta)
+
+
+def test_planner_integer_and_zero_edges(oracle_lib):
+    cases = [
+        [1.0, 1.0, 1.0, 1.0], [10.0, 1.0, 0.1, 0.01], [100.0, 0.0, 1e-5, 3.0],
+        [0.0, 1.0, 1.0, 1.0], [1000.0, 1e-300, 1e-310, 0.5], [2.0 ** 30, 2.0 ** -60, 2.0 ** -90, 2.0 ** -3],
+    ]
+    for c in cases:
+        n2 = np.array([[x, 0.0] for x in c])
+        r = len(c) - 2
+        for d in (15, 31, 63):
+            p = plan_precisions(c[:r + 1], c[r + 1], PrecisionCtx(d), s=2)
+            dig, nu, nil, _ = oracle_lib.plan_digits(n2, d)
+            assert (p.level_digits, p.nu) == (dig, nu), c
+
+
+def test_flat_is_fixed():
+    plan = plan_precisions([1.0, 1.0, 1.0], 1.0, PrecisionCtx(24), 10.0, s=2)
+    assert plan.nu == plan.r + 1 and plan.level_digits == (24, 24)
+
+
+def test_monotone_and_bounded():
+    plan = plan_precisions([10.0, 1e-3, 1e-9, 1e-20], 0.5, PrecisionCtx(32), 10.0, s=2)
+    ds = plan.level_digits
+    assert all(a >= b for a, b in zip(ds, ds[1:]))
+    assert all(1 <= x <= 32 for x in ds)
+    assert all(ds[i - 1] == 32 for i in range(1, plan.nu))
+
+
+def test_nilpotent_flag():
+    plan = plan_precisions([5.0, 3.0, 1.0], 0.0, PrecisionCtx(16), 10.0, s=2)
+    assert plan.nilpotent and plan.nu == 1 and plan.level_digits == (1, 1)
+    assert [float(u) for u in plan.level_roundoffs] == [0.1, 0.1]
+
+
+def test_tau_sequence_exact():
+    t = tau_sequence([MPF(4), MPF(2), MPF(0), MPF(1)], MPF(3))
+    assert float(t[0]) == 1.5 and float(t[1]) == 0.0 and t[2].is_inf()
+
+
+def _plan(s, r, d, digits):
+    return EvaluationPlan(s=s, r=r, nu=1, d_working=d, level_digits=tuple(digits),
+                          level_roundoffs=tuple(PrecisionCtx(k).unit_roundoff for k in digits),
+                          tau_seq=(), norm_bs=(MPF(1),) * (r + 1), norm_y=MPF(1))
+
+
+def test_snap_to_lattice_cases():
+    assert snap_to_lattice(_plan(2, 3, 16, [12, 5, 1]), [16]).level_digits == (16, 16, 16)
+    assert snap_to_lattice(_plan(2, 1, 16, [5]), [3, 8, 16]).level_digits == (8,)
+    assert snap_to_lattice(_plan(2, 1, 16, [16]), [3, 8, 16]).level_digits == (16,)
+    with pytest.raises(ValueError):
+        snap_to_lattice(_plan(2, 1, 16, [5]), [3, 8])
+    # the B200 lattice
+    assert snap_to_lattice(_plan(6, 5, 31, [22, 10, 1, 1, 1]), [7, 15, 31]).level_digits == (31, 15, 7, 7, 7)
+
+
+def test_cost_ratio_table1_goldens():
+    cr, sav = cost_ratio(_plan(8, 8, 64, (61, 55, 47, 38, 28, 18, 7, 1)))
+    assert abs(cr - 703 / 960) < 1e-12 and abs(sav - 0.268) < 0.001
+    rows = [(32, 7, 6, (30, 25, 18, 11, 3, 1), 0.271),
+            (128, 10, 10, (124, 115, 104, 92, 78, 64, 49, 34, 18, 1), 0.247),
+            (256, 14, 13, (248, 234, 217, 197, 176, 154, 131, 107, 82, 57, 31, 4, 1), 0.254)]
+    for d, s, r, sched, want in rows:
+        assert abs(cost_ratio(_plan(s, r, d, sched))[1] - want) <= 0.001
+    assert cost_ratio(_plan(3, 4, 16, (16,) * 4)) == (1.0, 0.0)
+
+
+def test_plan_validation():
+    with pytest.raises(ValueError):
+        EvaluationPlan(s=2, r=2, nu=1, d_working=16, level_digits=(5, 9), level_roundoffs=(),
+                       tau_seq=(), norm_bs=(), norm_y=MPF(1))
+    with pytest.raises(ValueError):
+        EvaluationPlan(s=2, r=1, nu=5, d_working=16, level_digits=(16,), level_roundoffs=(),
+                       tau_seq=(), norm_bs=(), norm_y=MPF(1))
+
+
+def test_table1_schedules_via_oracle_norms(oracle_lib):
+    """acceptance.py:119-142 (C4): cauchy(100) plan_only schedules within
+    +-2 digits of Table 1 (rows 1-2).  Norms from the oracle at the
+    reference's 16-digit NORM_CTX; digits from the product planner."""
+    n = 100
+    A = np.array([[1.0 / (i + j) for j in range(1, n + 1)] for i in range(1, n + 1)])
+    # the reference builds cauchy at GEN_CTX (40 digits) then rounds to 16
+    from paper_2312_17396_b200.bigfloat import rn as _rn
+    Xw = np.zeros((2, n, n))
+    for i in range(n):
+        for j in range(n):
+            v = _rn(Fraction(1, i + j + 2), 54)
+            Xw[0, i, j] = float(v)
+            Xw[1, i, j] = float(v - Fraction(float(v)))
+    for d, m, want in ((32, 42, (30, 25, 18, 11, 3, 1)), (64, 64, (61, 55, 47, 38, 28, 18, 7, 1))):
+        s = math.ceil(math.sqrt(m))
+        ps = oracle_lib.OraclePS(n)
+        n2 = ps.prepare(Xw, taylor_exp_coeffs(m).coeffs, s, 54)
+        fr = _norms2_to_frac(n2)
+        r = m // s
+        plan = plan_precisions(fr[:r + 1], fr[r + 1], PrecisionCtx(d), s=s)
+        assert plan.r == len(want)
+        assert all(abs(a - b) <= 2 for a, b in zip(plan.level_digits, want)), plan.level_digits
+        assert plan.level_digits[-1] <= 2
