@@ -44,8 +44,9 @@ from .bounds import BoundInputs, thm21_bound, tau_sequence
 from .coefficients import (CoefficientSeries, coeff_words, eval_coeff,
                            split_words, taylor_exp_coeffs)
 from .planner import (EvaluationPlan, cost_ratio, default_block_size,
-                      fixed_plan, hardware_lattice, matmul_counts,
-                      plan_precisions, snap_to_lattice)
+                      fixed_plan, formats_of_digits, hardware_lattice,
+                      matmul_counts, plan_digits_batch, plan_precisions,
+                      snap_to_lattice)
 from .precision import (DD, FORMAT_NAME, FP32, FP64, NORM_CTX, QD,
                         DimensionError, MatBatch, PrecisionCtx, as_fp64_batch)
 
@@ -57,17 +58,76 @@ def _torch():
     return torch
 
 
-@dataclass
 class EvaluationReport:
-    """engine.py:87-108 (``result`` is a device ``MatBatch`` of batch 1)."""
-    result: MatBatch
-    plan: EvaluationPlan
-    matmuls_by_digits: Dict[int, int]
-    cost_ratio: float
-    savings: float
-    timing_buckets: Dict[str, float]
-    bound: Optional[MPF] = None
-    diagnostics: Dict[str, object] = field(default_factory=dict)
+    """engine.py:87-108.  ``result`` is a device ``MatBatch`` of batch 1.
+
+    Batched evaluations build the per-matrix plan lazily: execution uses the
+    certified batched digit rule (planner.plan_digits_batch), and the full
+    ``EvaluationPlan`` (taus, roundoffs, norms) is produced by the exact
+    ``plan_precisions`` on first access and checked against the executed
+    digits."""
+
+    def __init__(self, result: MatBatch, plan: Optional[EvaluationPlan] = None,
+                 matmuls_by_digits: Optional[Dict[int, int]] = None, cost_ratio: Optional[float] = None,
+                 savings: Optional[float] = None, timing_buckets: Optional[Dict[str, float]] = None,
+                 bound: Optional[MPF] = None, diagnostics: Optional[Dict[str, object]] = None,
+                 *, plan_fn=None, counts_mode: str = "mixed", executed=None):
+        self.result = result
+        self._plan = plan
+        self._plan_fn = plan_fn
+        self._counts = matmuls_by_digits
+        self._cr = None if cost_ratio is None else (cost_ratio, savings)
+        self.timing_buckets = timing_buckets if timing_buckets is not None else {k: 0.0 for k in BUCKETS}
+        self.bound = bound
+        self._diag_extra = diagnostics or {}
+        self._counts_mode = counts_mode
+        self._executed = executed
+
+    @property
+    def plan(self) -> EvaluationPlan:
+        if self._plan is None:
+            p = self._plan_fn()
+            if self._executed is not None:
+                digits, nu = self._executed
+                if tuple(p.level_digits) != tuple(digits) or p.nu != nu:
+                    raise RuntimeError(f"executed schedule {digits}/{nu} != exact plan "
+                                       f"{p.level_digits}/{p.nu}")
+            self._plan = p
+        return self._plan
+
+    @property
+    def matmuls_by_digits(self) -> Dict[int, int]:
+        if self._counts is None:
+            p = self.plan
+            d = p.d_working
+            if self._counts_mode == "fixed":
+                self._counts = {d: p.s - 1 + p.r} if p.r else {}
+            elif self._counts_mode == "explicit" or p.nilpotent:
+                self._counts = {d: p.s - 1}
+            else:
+                self._counts = matmul_counts(p)
+        return self._counts
+
+    @property
+    def cost_ratio(self) -> float:
+        if self._cr is None:
+            self._cr = cost_ratio(self.plan)
+        return self._cr[0]
+
+    @property
+    def savings(self) -> float:
+        if self._cr is None:
+            self._cr = cost_ratio(self.plan)
+        return self._cr[1]
+
+    @property
+    def diagnostics(self) -> Dict[str, object]:
+        p = self.plan
+        lat = hardware_lattice(p.d_working)
+        diag = {"level_formats": [FORMAT_NAME[f] for f in p.level_formats],
+                "snapped_digits": list(snap_to_lattice(p, lat).level_digits) if p.d_working in lat else None}
+        diag.update(self._diag_extra)
+        return diag
 
     def to_json(self) -> str:
         return json.dumps({
@@ -82,6 +142,9 @@ class EvaluationReport:
 
     def result_numpy(self) -> np.ndarray:
         return self.result.to_numpy()[0]
+
+    def __repr__(self):
+        return f"EvaluationReport({self.result!r})"
 
 
 class BatchReport(list):
@@ -184,6 +247,8 @@ class _Prepared:
 
 def _prepare(h, Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: int,
              timer: _Buckets, x_is_working: Optional[MatBatch] = None) -> _Prepared:
+    """eval_b0_and_power + assemble_block + one_norm (engine.py:141-154,
+    127-138, 467-468) for the whole batch, then the one host sync."""
     torch = _torch()
     dev = Xt.device if Xt is not None else x_is_working.device
     B = Xt.shape[0] if Xt is not None else x_is_working.batch
@@ -201,8 +266,8 @@ def _prepare(h, Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: in
             h.convert(x_is_working, powers[0])
     else:
         h.convert(MatBatch(Xt.unsqueeze(0), FP64), powers[0])
-    if s > 1:
-        h.powers(powers)
+    for k in range(1, s):           # X^{k+1} = X^k X   (engine.py:151-153)
+        h.gemm(powers[k - 1], powers[0], powers[k])
     timer.stop()
     timer.start("coefficient_assembly")
     blocks = [MatBatch.empty(wf, B, n, device=dev) for _ in range(r + 1)]
@@ -215,9 +280,9 @@ def _prepare(h, Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: in
     return _Prepared(wf, s, r, m, powers, blocks, norms_h, cw)
 
 
-def _horner(h, prep: _Prepared, plans: List[EvaluationPlan], timer: _Buckets) -> MatBatch:
+def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buckets) -> MatBatch:
     """horner_mixed (engine.py:243-252) for every matrix of the batch,
-    grouped by level-format tuple."""
+    grouped by level-format tuple (one launch per level per group)."""
     torch = _torch()
     wf, s, r, m = prep.wf, prep.s, prep.r, prep.m
     Y = prep.powers[s - 1]
@@ -226,31 +291,32 @@ def _horner(h, prep: _Prepared, plans: List[EvaluationPlan], timer: _Buckets) ->
     result = MatBatch.empty(wf, B, n, device=dev)
     timer.start("mixed_horner")
     groups: Dict[Tuple[int, ...], List[int]] = {}
-    nil = []
-    for b, p in enumerate(plans):
-        if p.nilpotent:
-            nil.append(b)
+    nil_idx = []
+    for b in range(B):
+        if nil[b]:
+            nil_idx.append(b)
         else:
-            fm = (wf,) + tuple(p.level_formats[1:])
+            fm = (wf,) + formats_of_digits(tuple(int(x) for x in digits[b]))
             groups.setdefault(fm, []).append(b)
-    for b in nil:
-        result.data[:, b].copy_(blocks[0].data[:, b])
+    if nil_idx:
+        # p = B_0 (engine.py:378-379, 473-474)
+        ii = torch.tensor(nil_idx, device=dev)
+        result.data[:, ii] = blocks[0].data[:, ii]
     ws = _Workspace(B, n, dev)
     scalar_top = (m % s == 0)
     bm_words = prep.coeffs[m]
+    whole = len(groups) == 1 and not nil_idx
     for fm, members in groups.items():
-        sel = torch.tensor(members, dtype=torch.int32).to(dev, non_blocking=True)
-        need_exp = FP32 in fm
-        exps = None
-        exp_y = None
-        if need_exp:
+        sel = None if whole else torch.tensor(members, dtype=torch.int32).to(dev, non_blocking=True)
+        exps = exp_y = None
+        if FP32 in fm:
             e = np.zeros((r + 1, B), dtype=np.int32)
             ey = np.zeros(B, dtype=np.int32)
-            for b in members:
-                for j in range(1, r + 1):
-                    if fm[j] == FP32:
-                        e[j, b] = _exp_for(float(prep.norms[b, j]))
-                ey[b] = _exp_for(float(prep.norms[b, r + 1]))
+            idx = np.asarray(members)
+            for j in range(1, r + 1):
+                if fm[j] == FP32:
+                    e[j, idx] = [_exp_for(float(v)) for v in prep.norms[idx, j]]
+            ey[idx] = [_exp_for(float(v)) for v in prep.norms[idx, r + 1]]
             exps = torch.from_numpy(e).to(dev, non_blocking=True)
             exp_y = torch.from_numpy(ey).to(dev, non_blocking=True)
 
@@ -258,7 +324,7 @@ def _horner(h, prep: _Prepared, plans: List[EvaluationPlan], timer: _Buckets) ->
             return None if (exps is None or fm[j] != FP32) else exps[j]
 
         ys: Dict[int, MatBatch] = {wf: Y}
-        for f in set(fm[1:]):
+        for f in sorted(set(fm[1:])):
             if f not in ys:
                 yf = MatBatch.empty(f, B, n, device=dev)
                 h.convert(Y, yf, sel, exp_y if f == FP32 else None)
@@ -288,29 +354,6 @@ def _input(X, device=None):
     return Xt, None, single
 
 
-def _finish(result: MatBatch, plans, counts, sec, with_bound, single, extra_diag=None):
-    """Per-matrix reports (engine.py:295-301).  Nilpotent plans carry no
-    bound, as in the reference (engine.py:378-379, 473-474)."""
-    reports = []
-    frac = _fractions(sec)
-    n = result.rows
-    for b, p in enumerate(plans):
-        cr, sav = cost_ratio(p)
-        bound = _bound_for(p, n) if (with_bound and not p.nilpotent and p.r > 0) else None
-        lat = hardware_lattice(p.d_working)
-        diag = {"level_formats": [FORMAT_NAME[f] for f in p.level_formats],
-                "snapped_digits": list(snap_to_lattice(p, lat).level_digits) if p.d_working in lat else None}
-        if extra_diag:
-            diag.update(extra_diag)
-        res_b = result if single else result.select(b)
-        reports.append(EvaluationReport(result=res_b, plan=p, matmuls_by_digits=dict(counts[b]),
-                                        cost_ratio=cr, savings=sav, timing_buckets=frac,
-                                        bound=bound, diagnostics=diag))
-    if single:
-        return reports[0]
-    return BatchReport(reports, result, sec)
-
-
 def _bound_for(plan: EvaluationPlan, n: int) -> MPF:
     """engine.py:283-292."""
     u = PrecisionCtx(plan.d_working).unit_roundoff
@@ -327,6 +370,31 @@ def _check_square(Xt, Xw):
     if Xw.rows != Xw.cols:
         raise DimensionError("X must be square")
     return Xw.batch, Xw.rows
+
+
+def _reports(result: MatBatch, plan_fns, executed, counts_mode, sec, with_bound, single, extra=None):
+    frac = _fractions(sec)
+    n = result.rows
+    reps = []
+    for b, fn in enumerate(plan_fns):
+        rep = EvaluationReport(result if single else result.select(b), plan_fn=fn,
+                               counts_mode=counts_mode, timing_buckets=frac, diagnostics=extra,
+                               executed=None if executed is None else executed[b])
+        if with_bound:
+            p = rep.plan
+            if not p.nilpotent and p.r > 0 and counts_mode != "explicit":
+                rep.bound = _bound_for(p, n)
+        reps.append(rep)
+    if single:
+        return reps[0]
+    return BatchReport(reps, result, sec)
+
+
+def _plan_fn(norms_row, r, ctx, delta, s, apply_switch, fix_params):
+    nb = tuple(float(x) for x in norms_row[:r + 1])
+    ny = float(norms_row[r + 1])
+    return lambda: plan_precisions(nb, ny, ctx, delta, s=s, apply_switch=apply_switch,
+                                   fix_params=fix_params)
 
 
 # ------------------------------------------------------------ evaluators
@@ -349,17 +417,20 @@ def ps_fixed(X, series: CoefficientSeries, ctx: PrecisionCtx, with_bound: bool =
         for k in range(res.words):
             res.data[k][:, idx, idx] = w[k]
         c0 = abs(rn(Fraction(series.coeffs[0]), ctx.binary_precision))
-        plans = [EvaluationPlan(s=1, r=0, nu=1, d_working=d, level_digits=(), level_roundoffs=(),
-                                tau_seq=(), norm_bs=(MPF(rn(c0, 54), 54),),
-                                norm_y=MPF(0, 64))] * B
-        return _finish(res, plans, [{}] * B, {}, False, single)
+        plan = EvaluationPlan(s=1, r=0, nu=1, d_working=d, level_digits=(), level_roundoffs=(),
+                              tau_seq=(), norm_bs=(MPF(rn(c0, 54), 54),), norm_y=MPF(0, 64))
+        return _reports(res, [lambda: plan] * B, None, "fixed", {}, False, single)
     s = default_block_size(m)
     prep = _prepare(h, Xt, series, ctx, wf, s, timer, Xw)
     r = prep.r
-    plans = [fixed_plan(prep.norms[b, :r + 1], prep.norms[b, r + 1], ctx, s) for b in range(B)]
-    result = _horner(h, prep, plans, timer)
-    counts = [{d: s - 1 + r}] * B
-    return _finish(result, plans, counts, timer.seconds(), with_bound, single)
+    digits = np.full((B, r), d, dtype=np.int64)
+    result = _horner(h, prep, digits, np.zeros(B, dtype=bool), timer)
+    fns = []
+    for b in range(B):
+        nb = tuple(float(x) for x in prep.norms[b, :r + 1])
+        ny = float(prep.norms[b, r + 1])
+        fns.append((lambda nb=nb, ny=ny: fixed_plan(nb, ny, ctx, s)))
+    return _reports(result, fns, None, "fixed", timer.seconds(), with_bound, single)
 
 
 def ps_mixed_general(X, series: CoefficientSeries, ctx: PrecisionCtx, delta: float = 10.0,
@@ -378,20 +449,19 @@ def ps_mixed_general(X, series: CoefficientSeries, ctx: PrecisionCtx, delta: flo
     return _mixed_tail(h, prep, ctx, delta, True, True, with_bound, single, timer)
 
 
-def _mixed_tail(h, prep, ctx, delta, apply_switch, fix_params, with_bound, single, timer,
-                extra_diag=None):
-    """Planner + Horner + report of the mixed evaluators (engine.py:376-387,
+def _mixed_tail(h, prep, ctx, delta, apply_switch, fix_params, with_bound, single, timer):
+    """Planner + Horner + reports of the mixed evaluators (engine.py:376-387,
     471-482)."""
     d = ctx.decimal_digits
     r, s = prep.r, prep.s
-    B = prep.norms.shape[0]
     timer.start("norm_estimation")
-    plans = [plan_precisions(prep.norms[b, :r + 1], prep.norms[b, r + 1], ctx, delta, s=s,
-                             apply_switch=apply_switch, fix_params=fix_params) for b in range(B)]
+    digits, nu, nil = plan_digits_batch(prep.norms[:, :r + 1], prep.norms[:, r + 1], d, delta, apply_switch)
     timer.stop()
-    result = _horner(h, prep, plans, timer)
-    counts = [({d: s - 1} if p.nilpotent else matmul_counts(p)) for p in plans]
-    return _finish(result, plans, counts, timer.seconds(), with_bound, single, extra_diag)
+    result = _horner(h, prep, digits, nil, timer)
+    B = prep.norms.shape[0]
+    fns = [_plan_fn(prep.norms[b], r, ctx, delta, s, apply_switch, fix_params) for b in range(B)]
+    executed = [(tuple(int(x) for x in digits[b]), int(nu[b])) for b in range(B)]
+    return _reports(result, fns, executed, "mixed", timer.seconds(), with_bound, single)
 
 
 def ps_mixed_exp(X, m: int, ctx: PrecisionCtx, fix_params: bool = True, delta: float = 10.0,
@@ -441,11 +511,9 @@ def _one_norms(Xt, Xw) -> np.ndarray:
 
 def _explicit_powers(Xt, Xw, m, ctx, s, series, delta, apply_switch, fix_params, single, timing):
     """engine.py:439-459: p = B_0 + b_m Y with no Horner phase."""
-    torch = _torch()
     h = _lib.handle_for()
     timer = _Buckets(timing)
     wf = _working_format(ctx)
-    d = ctx.decimal_digits
     # blocks of the s == m layout: r = 1, B_0 = sum_{j<s} b_j X^j, B_1 = b_m I
     prep = _prepare(h, Xt, series, ctx, wf, s, timer, Xw)
     Y = prep.powers[s - 1]
@@ -454,21 +522,25 @@ def _explicit_powers(Xt, Xw, m, ctx, s, series, delta, apply_switch, fix_params,
     h.axpy(prep.coeffs[m], Y, prep.blocks[0], res)
     timer.stop()
     bm_norm = MPF(abs(rn(Fraction(series.coeffs[m]), NORM_CTX.binary_precision)), 54)
-    plans = []
-    for b in range(Y.batch):
-        p = plan_precisions((prep.norms[b, 0], bm_norm), prep.norms[b, prep.r + 1], ctx, delta, s=s,
-                            apply_switch=apply_switch, fix_params=fix_params)
-        plans.append(EvaluationPlan(
-            s=p.s, r=p.r, nu=p.nu, d_working=p.d_working, level_digits=p.level_digits,
-            level_roundoffs=p.level_roundoffs, tau_seq=p.tau_seq, norm_bs=p.norm_bs, norm_y=p.norm_y,
-            delta=delta, fix_params=fix_params, degenerate_levels=p.degenerate_levels,
-            nilpotent=p.nilpotent, explicit_powers=True))
-    counts = [{d: s - 1}] * Y.batch
-    return _finish(res, plans, counts, timer.seconds(), False, single)
+
+    def fn(b):
+        nb0, ny = float(prep.norms[b, 0]), float(prep.norms[b, prep.r + 1])
+
+        def make():
+            p = plan_precisions((nb0, bm_norm), ny, ctx, delta, s=s, apply_switch=apply_switch,
+                                fix_params=fix_params)
+            return EvaluationPlan(
+                s=p.s, r=p.r, nu=p.nu, d_working=p.d_working, level_digits=p.level_digits,
+                level_roundoffs=p.level_roundoffs, tau_seq=p.tau_seq, norm_bs=p.norm_bs,
+                norm_y=p.norm_y, delta=delta, fix_params=fix_params,
+                degenerate_levels=p.degenerate_levels, nilpotent=p.nilpotent, explicit_powers=True)
+        return make
+    return _reports(res, [fn(b) for b in range(Y.batch)], None, "explicit", timer.seconds(), False, single)
 
 
 def _ps_mixed_exp_one(Xt, Xw, m, ctx, fix_params, delta, with_bound, timing, grow, norm_x):
-    """Single-matrix ps_mixed_exp with the growth branch (engine.py:417-437)."""
+    """Single-matrix ps_mixed_exp with the growth branch (engine.py:417-437):
+    s grows while ||X^s|| > ||B_0|| ||X||^s (54-bit NORM_CTX arithmetic)."""
     series = taylor_exp_coeffs(m)
     s = default_block_size(m)
     if not grow:
@@ -478,13 +550,11 @@ def _ps_mixed_exp_one(Xt, Xw, m, ctx, fix_params, delta, with_bound, timing, gro
         timer = _Buckets(timing)
         prep = _prepare(h, Xt, series, ctx, _working_format(ctx), s, timer, Xw)
         return _mixed_tail(h, prep, ctx, delta, True, fix_params, with_bound, True, timer)
-    # growth: s increases while ||X^s|| > ||B_0|| ||X||^s (54-bit tests)
     p54 = NORM_CTX.binary_precision
     nx = rn(Fraction(norm_x), p54)
     while s < m:
         h = _lib.handle_for()
-        prep = _prepare(h, Xt, series.truncate(max(s, m)), ctx, _working_format(ctx), s,
-                        _Buckets(False), Xw)
+        prep = _prepare(h, Xt, series, ctx, _working_format(ctx), s, _Buckets(False), Xw)
         nb0, ny = Fraction(float(prep.norms[0, 0])), Fraction(float(prep.norms[0, prep.r + 1]))
         xs = exp_rn(rn(Fraction(s) * ln_rn(nx, p54), p54), p54) if nx > 0 else Fraction(0)
         if ny <= rn(nb0 * xs, p54):
@@ -536,13 +606,14 @@ def cos_argument(X, ctx: PrecisionCtx) -> MatBatch:
 
 def horner_mixed(Bs: Sequence[MatBatch], Y: MatBatch, plan: EvaluationPlan) -> MatBatch:
     """engine.py:243-252 on device blocks: phi = B_r; phi = RN_{j-1}(B_{j-1}
-    + RN_j(Y phi)), j = r..1.  Bs and Y at the working format, batch 1."""
+    + RN_j(Y phi)), j = r..1.  Bs and Y at the working format."""
     if len(Bs) != plan.r + 1:
         raise ValueError("need r+1 coefficient blocks")
     if plan.r == 0:
         return Bs[0]
     h = _lib.handle_for()
     norms = np.array([[float(b) for b in plan.norm_bs] + [float(plan.norm_y)]] * Y.batch)
-    prep = _Prepared(Y.fmt, plan.s, plan.r, plan.r * plan.s + 1, [Y] * plan.s, list(Bs), norms,
-                     np.zeros((plan.r * plan.s + 2, 4)))
-    return _horner(h, prep, [plan] * Y.batch, _Buckets(False))
+    m = plan.r * plan.s + 1       # m mod s != 0: B_r is a general block here
+    prep = _Prepared(Y.fmt, plan.s, plan.r, m, [Y] * plan.s, list(Bs), norms, np.zeros((m + 1, 4)))
+    digits = np.array([plan.level_digits] * Y.batch, dtype=np.int64)
+    return _horner(h, prep, digits, np.zeros(Y.batch, dtype=bool), _Buckets(False))

@@ -28,11 +28,14 @@ def _torch():
 
 
 def from_numpy(words, fmt: int, device=None) -> MatBatch:
-    """(w, B, n, n) / (B, n, n) / (n, n) host words -> MatBatch (exact)."""
+    """Host words -> MatBatch (exact).  (n, n): one fp64 matrix;
+    (w, n, n): the w word planes of one matrix; (w, B, n, n): a batch."""
     torch = _torch()
     a = np.asarray(words, dtype=np.float64)
-    while a.ndim < 4:
-        a = a[None]
+    if a.ndim == 2:
+        a = a[None, None]
+    elif a.ndim == 3:
+        a = a[:, None]
     from .precision import FORMAT_WORDS
     w = FORMAT_WORDS[fmt]
     if a.shape[0] < w:

@@ -27,8 +27,14 @@ _P = 107                       # BOUND_CTX bits (engine.py:25 _G)
 _ONE_E_MINUS_9 = rn(Fraction(1, 10 ** 9), 53)   # mpfr("1e-9") at 53 bits
 
 
+_ROUNDOFF = {}
+
+
 def _roundoff(k: int) -> MPF:
-    return MPF(exp10_rn(-k, _P), _P)
+    v = _ROUNDOFF.get(k)
+    if v is None:
+        v = _ROUNDOFF[k] = MPF(exp10_rn(-k, _P), _P)
+    return v
 
 
 @dataclass(frozen=True)
@@ -147,6 +153,75 @@ def plan_precisions(norm_bs: Sequence, norm_y, ctx: PrecisionCtx,
         level_roundoffs=tuple(_roundoff(k) for k in digits), tau_seq=taus,
         norm_bs=nb, norm_y=ny, delta=delta, fix_params=fix_params,
         degenerate_levels=degenerate)
+
+
+# ----------------------------------------------------- batched fast path
+_CERT_MARGIN = 1e-8
+
+
+def plan_digits_batch(norm_bs, norm_y, d: int, delta: float = 10.0, apply_switch: bool = True):
+    """Digits / nu / nilpotent flags of ``plan_precisions`` for a whole batch.
+
+    Vectorised float64 evaluation of e_i, certified: the digit rule only
+    consumes floor(e_i) and the test e_i <= d - log10(delta), and the float64
+    evaluation is within ~1e-11 of the 107-bit value, so every row whose e_i
+    all lie farther than 1e-8 from an integer and from the threshold gets the
+    exact reference digits.  Uncertain rows (and any non-finite input) are
+    recomputed with the exact scalar ``plan_precisions``.
+
+    norm_bs: (B, r+1) float64, norm_y: (B,) float64 (the exact norm values).
+    Returns (digits (B, r) int64, nu (B,) int64, nilpotent (B,) bool)."""
+    import numpy as np
+    nb = np.asarray(norm_bs, dtype=np.float64)
+    ny = np.asarray(norm_y, dtype=np.float64)
+    B, r1 = nb.shape
+    r = r1 - 1
+    digits = np.ones((B, r), dtype=np.int64)
+    nu = np.full(B, r + 1, dtype=np.int64)
+    nil = ny == 0
+    lim = d - math.log10(delta)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        lb0 = np.where(nb[:, 0] > 0, np.log10(np.where(nb[:, 0] > 0, nb[:, 0], 1.0)), 0.0)
+        ly = np.log10(np.where(ny > 0, ny, 1.0))
+        li = np.log10(np.where(nb[:, 1:] > 0, nb[:, 1:], 1.0))
+        i = np.arange(1, r + 1, dtype=np.float64)
+        e = (d - lb0)[:, None] + (li + i[None, :] * ly[:, None]) + 1e-9
+    zero = (nb[:, 1:] == 0) | (nb[:, :1] == 0)
+    qual = np.where(zero, True, e <= lim)
+    dig = np.where(zero, 1, np.clip(np.floor(e), 1, d)).astype(np.int64)
+    risky = ~zero & ((np.abs(e - np.round(e)) < _CERT_MARGIN) | (np.abs(e - lim) < _CERT_MARGIN))
+    bad = ~np.isfinite(nb).all(axis=1) | ~np.isfinite(ny) | risky.any(axis=1)
+    anyq = qual.any(axis=1)
+    first = np.where(anyq, qual.argmax(axis=1) + 1, r + 1)
+    if apply_switch:
+        cols = np.arange(1, r + 1)[None, :]
+        dig = np.where(cols < first[:, None], d, dig)
+    # running max from the outermost level inward (engine.py:209-210)
+    dig = np.maximum.accumulate(dig[:, ::-1], axis=1)[:, ::-1]
+    digits[:] = dig
+    nu[:] = first
+    digits[nil] = 1
+    nu[nil] = 1
+    for b in np.nonzero(bad & ~nil)[0]:
+        p = plan_precisions(nb[b], ny[b], PrecisionCtx(d), delta, s=1, apply_switch=apply_switch)
+        digits[b] = p.level_digits
+        nu[b] = p.nu
+        nil[b] = p.nilpotent
+    return digits, nu, nil
+
+
+_FMT_OF_DIGITS = {}
+
+
+def formats_of_digits(digits):
+    """Lattice format of each digit count (cached)."""
+    out = []
+    for x in digits:
+        f = _FMT_OF_DIGITS.get(x)
+        if f is None:
+            f = _FMT_OF_DIGITS[x] = format_for_digits(int(x))
+        out.append(f)
+    return tuple(out)
 
 
 def fixed_plan(norm_bs: Sequence, norm_y, ctx: PrecisionCtx, s: int) -> EvaluationPlan:

@@ -112,7 +112,7 @@ class MatBatch:
             raise DimensionError(
                 f"MatBatch({FORMAT_NAME[fmt]}) needs a ({FORMAT_WORDS[fmt]}, B, R, C) "
                 f"{want} tensor, got {tuple(data.shape)} {data.dtype}")
-        if not data.is_contiguous():
+        if data.stride(3) != 1 or data.stride(2) < data.shape[3]:
             data = data.contiguous()
         self.data = data
         self.fmt = fmt
@@ -158,7 +158,9 @@ class MatBatch:
         return self.data.device
 
     def select(self, idx: int) -> "MatBatch":
-        return MatBatch(self.data[:, idx:idx + 1].contiguous(), self.fmt)
+        """Batch member idx as a batch-1 view (no copy; the C-ABI takes the
+        plane and batch strides explicitly)."""
+        return MatBatch(self.data[:, idx:idx + 1], self.fmt)
 
     def words_numpy(self) -> np.ndarray:
         """(words, batch, rows, cols) float64 copy on the host."""

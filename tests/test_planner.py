@@ -149,3 +149,27 @@ def test_table1_schedules_via_oracle_norms(oracle_lib):
         assert plan.r == len(want)
         assert all(abs(a - b) <= 2 for a, b in zip(plan.level_digits, want)), plan.level_digits
         assert plan.level_digits[-1] <= 2
+
+
+def test_batched_planner_certified_equals_exact():
+    """plan_digits_batch (vectorised, certified, used on the execution path)
+    equals the exact plan_precisions row by row, including rows placed on
+    integer boundaries that force the exact fallback."""
+    from paper_2312_17396_b200.planner import plan_digits_batch
+    rng = random.Random(7)
+    for d in (15, 31, 63):
+        rows = []
+        for _ in range(300):
+            r = 5
+            n2 = _random_norms(rng, r)
+            rows.append([Fraction(a) + Fraction(b) for a, b in n2])
+        # boundary rows: ||B_i|| ||Y||^i / ||B_0|| = 10^-k exactly-ish
+        rows.append([1.0, 1e-5, 1e-10, 1e-15, 1e-20, 1e-25, 1.0])
+        rows.append([1.0, 0.0, 1e-10, 0.0, 1e-20, 1e-25, 0.5])
+        rows.append([1.0, 1e-5, 1e-10, 1e-15, 1e-20, 1e-25, 0.0])
+        nb = np.array([[float(x) for x in row[:-1]] for row in rows])
+        ny = np.array([float(row[-1]) for row in rows])
+        dig, nu, nil = plan_digits_batch(nb, ny, d)
+        for b in range(len(rows)):
+            p = plan_precisions(nb[b], ny[b], PrecisionCtx(d), s=2)
+            assert tuple(dig[b]) == p.level_digits and nu[b] == p.nu and nil[b] == p.nilpotent
