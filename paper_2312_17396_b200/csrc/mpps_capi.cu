@@ -195,15 +195,30 @@ struct AssembleArgs {
   int n, s, m, r, nchunk;
 };
 
+// One thread per (column, 32-row chunk); the r+1 block accumulators of an
+// entry live in registers, the coefficients in shared memory (broadcast
+// reads), so each power entry is loaded once and used for every block.
 template <int WF>
 __global__ void __launch_bounds__(128) assemble_kernel(const AssembleArgs a) {
   using V = WV<WF>;
   using T = typename V::T;
+  constexpr int CW = (WF == QD) ? 4 : (WF == DD ? 2 : 1);
+  __shared__ double sc[kMaxBlocks * kMaxPowers * CW];
+  const int n = a.n, s = a.s, m = a.m, r = a.r;
+  for (int t = threadIdx.x; t <= m; t += blockDim.x)
+#pragma unroll
+    for (int w = 0; w < CW; ++w) sc[t * CW + w] = a.coeff[4 * t + w];
+  __syncthreads();
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   const int chunk = blockIdx.y, b = blockIdx.z;
-  const int n = a.n, s = a.s, m = a.m, r = a.r;
   if (col >= n) return;
   const int full = m / s;
+  auto coef = [&](int idx) -> T {
+    const double *c = sc + idx * CW;
+    if constexpr (CW == 4) return mp::qd_make(c[0], c[1], c[2], c[3]);
+    else if constexpr (CW == 2) return mp::dd_make(c[0], c[1]);
+    else return c[0];
+  };
   double cs[kMaxBlocks + 1];
 #pragma unroll
   for (int k = 0; k <= kMaxBlocks; ++k) cs[k] = 0.0;
@@ -212,13 +227,8 @@ __global__ void __launch_bounds__(128) assemble_kernel(const AssembleArgs a) {
   for (int row = row0; row < row1; ++row) {
     T acc[kMaxBlocks];
 #pragma unroll
-    for (int k = 0; k < kMaxBlocks; ++k) {
-      if (k <= r) {
-        const double *c = a.coeff + 4 * (s * k);
-        acc[k] = (row == col) ? V::from(mp::qd_make(__ldg(c), __ldg(c + 1), __ldg(c + 2), __ldg(c + 3)))
-                              : V::zero();
-      }
-    }
+    for (int k = 0; k < kMaxBlocks; ++k)
+      if (k <= r) acc[k] = (row == col) ? coef(s * k) : V::zero();
     for (int j = 1; j < s; ++j) {
       const MatRef &P = a.P[j - 1];
       T x = V::from(load_qd(P, (long long)b * P.bstride + (long long)row * P.ld + col));
@@ -226,11 +236,7 @@ __global__ void __launch_bounds__(128) assemble_kernel(const AssembleArgs a) {
       for (int k = 0; k < kMaxBlocks; ++k) {
         if (k <= r) {
           const int hi = (k < full) ? s - 1 : m - s * full;
-          if (j <= hi) {
-            const double *c = a.coeff + 4 * (s * k + j);
-            T cf = V::from(mp::qd_make(__ldg(c), __ldg(c + 1), __ldg(c + 2), __ldg(c + 3)));
-            acc[k] = V::axpy(cf, x, acc[k]);
-          }
+          if (j <= hi) acc[k] = V::axpy(coef(s * k + j), x, acc[k]);
         }
       }
     }

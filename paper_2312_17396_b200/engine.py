@@ -67,12 +67,13 @@ class EvaluationReport:
     ``plan_precisions`` on first access and checked against the executed
     digits."""
 
-    def __init__(self, result: MatBatch, plan: Optional[EvaluationPlan] = None,
+    def __init__(self, result: Optional[MatBatch], plan: Optional[EvaluationPlan] = None,
                  matmuls_by_digits: Optional[Dict[int, int]] = None, cost_ratio: Optional[float] = None,
                  savings: Optional[float] = None, timing_buckets: Optional[Dict[str, float]] = None,
                  bound: Optional[MPF] = None, diagnostics: Optional[Dict[str, object]] = None,
-                 *, plan_fn=None, counts_mode: str = "mixed", executed=None):
-        self.result = result
+                 *, plan_fn=None, counts_mode: str = "mixed", executed=None, batch_view=None):
+        self._result = result
+        self._batch_view = batch_view   # (batch MatBatch, index) -> lazy view
         self._plan = plan
         self._plan_fn = plan_fn
         self._counts = matmuls_by_digits
@@ -82,6 +83,13 @@ class EvaluationReport:
         self._diag_extra = diagnostics or {}
         self._counts_mode = counts_mode
         self._executed = executed
+
+    @property
+    def result(self) -> MatBatch:
+        if self._result is None:
+            bm, i = self._batch_view
+            self._result = bm.select(i)
+        return self._result
 
     @property
     def plan(self) -> EvaluationPlan:
@@ -215,6 +223,15 @@ def _exp_for(norm: float) -> int:
     return -int(round(math.log2(norm)))
 
 
+def _exps_for(norms: np.ndarray) -> np.ndarray:
+    """Vectorised _exp_for."""
+    v = np.asarray(norms, dtype=np.float64)
+    ok = np.isfinite(v) & (v > 0)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        e = -np.round(np.log2(np.where(ok, v, 1.0)))
+    return np.where(ok, e, 0).astype(np.int32)
+
+
 class _Workspace:
     """Per-format ping-pong buffers for the Horner chain."""
 
@@ -230,6 +247,9 @@ class _Workspace:
         t = self.turn[fmt]
         self.turn[fmt] = 1 - t
         return self.bufs[fmt][t]
+
+
+_COEFF_DEV: Dict[tuple, object] = {}
 
 
 @dataclass
@@ -256,7 +276,13 @@ def _prepare(h, Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: in
     m = series.degree
     r = m // s
     cw = coeff_words(series, ctx)
-    coeffs = torch.from_numpy(cw).to(dev, non_blocking=True)
+    key = (series.coeffs, ctx.binary_precision, str(dev))
+    coeffs = _COEFF_DEV.get(key)
+    if coeffs is None:
+        coeffs = torch.tensor(cw, dtype=torch.float64, device=dev)
+        if len(_COEFF_DEV) > 64:
+            _COEFF_DEV.clear()
+        _COEFF_DEV[key] = coeffs
     timer.start("power_formation")
     powers = [MatBatch.empty(wf, B, n, device=dev) for _ in range(s)]
     if x_is_working is not None:
@@ -315,8 +341,8 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
             idx = np.asarray(members)
             for j in range(1, r + 1):
                 if fm[j] == FP32:
-                    e[j, idx] = [_exp_for(float(v)) for v in prep.norms[idx, j]]
-            ey[idx] = [_exp_for(float(v)) for v in prep.norms[idx, r + 1]]
+                    e[j, idx] = _exps_for(prep.norms[idx, j])
+            ey[idx] = _exps_for(prep.norms[idx, r + 1])
             exps = torch.from_numpy(e).to(dev, non_blocking=True)
             exp_y = torch.from_numpy(ey).to(dev, non_blocking=True)
 
@@ -377,7 +403,7 @@ def _reports(result: MatBatch, plan_fns, executed, counts_mode, sec, with_bound,
     n = result.rows
     reps = []
     for b, fn in enumerate(plan_fns):
-        rep = EvaluationReport(result if single else result.select(b), plan_fn=fn,
+        rep = EvaluationReport(result if single else None, plan_fn=fn, batch_view=(result, b),
                                counts_mode=counts_mode, timing_buckets=frac, diagnostics=extra,
                                executed=None if executed is None else executed[b])
         if with_bound:
