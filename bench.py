@@ -35,8 +35,21 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CFG = dict(workload="cfg2: Taylor exp m=30 s=6, batch 64 x n=256, ||X||_1=1, dd working (mixed dd/fp64/fp32 levels)",
-           batch=64, n=256, m=30, digits=31, norm=1.0)
+CONFIGS = {
+    "cfg1": dict(workload="cfg1: Taylor exp m=16 s=4, one n=32 matrix, ||X||_1=0.5, fp64 working (fp32 levels)",
+                 batch=1, n=32, m=16, digits=15, norm=0.5, kind="exp"),
+    "cfg2": dict(workload="cfg2: Taylor exp m=30 s=6, batch 64 x n=256, ||X||_1=1, dd working (mixed dd/fp64/fp32 levels)",
+                 batch=64, n=256, m=30, digits=31, norm=1.0, kind="exp"),
+    "cfg3": dict(workload="cfg3: scaling-and-squaring exp, PS Taylor m=42 s=7 + l=extra_squarings dd squarings, "
+                          "batch 16 x n=1024, ||A||_1 log-uniform [1e-2,1e3], dd working",
+                 batch=16, n=1024, m=42, digits=31, norm=None, kind="expm"),
+    "cfg4": dict(workload="cfg4: Pade [26/26] numerator+denominator by mixed PS at qd, one n=2048 matrix, ||X||_1=2",
+                 batch=1, n=2048, m=26, digits=63, norm=2.0, kind="pade"),
+    "cfg5": dict(workload="cfg5: cos Taylor deg 24 in Z=X^2 (s=5), one n=8192 matrix, ||X||_1=1 (X~N(0,1)/sqrt(n)), "
+                          "dd working, 2-D block SUMMA over NCCL",
+                 batch=1, n=8192, m=24, digits=31, norm=1.0, kind="summa_cos"),
+}
+CFG = dict(CONFIGS["cfg2"])
 METRIC = "matrix-polynomial evals/sec"
 
 
@@ -196,33 +209,150 @@ def cpu_baseline_sample(cores_hint=None):
 
 
 # ---------------------------------------------------------------- ours
+class Workload:
+    """One benchmark config: device-resident inputs, a step through the
+    public API, an end-to-end step from pinned host buffers, and the honest
+    GEMM count per unit."""
+
+    def __init__(self, name, rank, world, torch, mp):
+        self.name, self.cfg = name, CONFIGS[name]
+        self.rank, self.world, self.torch, self.mp = rank, world, torch, mp
+        c = self.cfg
+        self.ctx = mp.PrecisionCtx(c["digits"])
+        self.n, self.B, self.m = c["n"], c["batch"], c["m"]
+        self.kind = c["kind"]
+        self.scaling = "strong" if self.kind == "summa_cos" else "weak"
+        self.grid = None
+        if self.kind == "expm":
+            rng = np.random.default_rng(1000 + rank)
+            targets = 10.0 ** rng.uniform(-2, 3, size=self.B)
+            self.Xh = np.stack([synth(self.n, t, rank * self.B + i) for i, t in enumerate(targets)])
+        elif self.kind == "summa_cos":
+            from paper_2312_17396_b200 import summa
+            pr, pc = summa.ProcessGrid.for_world(world)
+            self.grid = summa.ProcessGrid(pr, pc) if world > 1 else None
+            X = np.random.default_rng(0).standard_normal((self.n, self.n)) / np.sqrt(self.n)
+            X *= c["norm"] / np.abs(X).sum(axis=0).max()
+            if self.grid is None:
+                self.Xh = X
+            else:
+                r0, mr, c0, nc = self.grid.block(self.n)
+                self.Xh = np.ascontiguousarray(X[r0:r0 + mr, c0:c0 + nc])
+            self.parallelism = f"SUMMA {pr}x{pc}"
+        else:
+            self.Xh = make_batch(rank, self.B, self.n, c["norm"])
+            if self.B == 1:
+                self.Xh = self.Xh[0]
+        if self.kind != "summa_cos":
+            self.parallelism = f"batch-sharded x{world}" if world > 1 else "single GPU"
+        self.Xd = torch.from_numpy(self.Xh).cuda()
+        self.Xpin = torch.from_numpy(self.Xh).pin_memory()
+
+    def _summa(self, X):
+        from paper_2312_17396_b200 import summa
+        from paper_2312_17396_b200.precision import MatBatch
+        torch = self.torch
+        grid = self.grid
+        if grid is None:
+            grid = summa.ProcessGrid.__new__(summa.ProcessGrid)
+            grid.pr = grid.pc = 1
+            grid.rank = grid.I = grid.J = 0
+            grid.row_group = grid.col_group = None
+        if X.device.type == "cpu":
+            X = X.to("cuda", non_blocking=True)
+        blk = MatBatch(X.reshape(1, 1, *X.shape), 15)
+        ops = summa.DeviceOps()
+        Z = summa.cos_argument_dist(blk, self.ctx, grid, ops)
+        return summa.ps_mixed_dist(Z, self.mp.taylor_cos_coeffs(self.m), self.ctx, grid, ops)
+
+    def step(self, X):
+        mp, ctx, m = self.mp, self.ctx, self.m
+        if self.kind == "exp":
+            return mp.ps_mixed_exp(X, m, ctx, timing=False)
+        if self.kind == "expm":
+            return mp.expm_ss(X, ctx, m, timing=False)
+        if self.kind == "pade":
+            return mp.ps_mixed_pade(X, m, ctx, timing=False)
+        return self._summa(X)
+
+    def results(self, rep):
+        """Device tensors holding the step's result(s)."""
+        if self.kind == "pade":
+            return [r.result.data for r in rep]
+        if self.kind == "summa_cos":
+            return [rep.block.data]
+        return [rep.result.data]
+
+    def plans(self, rep):
+        if self.kind == "pade":
+            return [rep[0].plan, rep[1].plan]
+        if self.kind == "summa_cos":
+            return [rep.plan(self.ctx)]
+        if hasattr(rep, "plan"):
+            return [rep.plan]
+        return [rep[0].plan]
+
+    def formats(self, rep):
+        if self.kind == "summa_cos":
+            from paper_2312_17396_b200.precision import FORMAT_NAME
+            return [FORMAT_NAME[f] for f in self.plans(rep)[0].level_formats]
+        r0 = rep[0] if self.kind == "pade" or not hasattr(rep, "diagnostics") else rep
+        return r0.diagnostics["level_formats"]
+
+    def gemms(self, rep):
+        """Honest device GEMMs per step, by format (whole local step)."""
+        from paper_2312_17396_b200.precision import FORMAT_NAME
+        counts = {}
+
+        def add(f, c):
+            counts[f] = counts.get(f, 0) + c
+
+        plans = self.plans(rep)
+        for i, p in enumerate(plans):
+            fm = p.level_formats
+            if not (self.kind == "pade" and i > 0):
+                add(FORMAT_NAME[fm[0]], p.s - 1)           # powers (shared by the Pade pair)
+            for j in range(1, p.r + 1):
+                if j == p.r and self.m % p.s == 0:
+                    continue                                # K3: elementwise
+                add(FORMAT_NAME[fm[j]], 1)
+        mult = self.B if self.kind in ("exp", "expm") else 1
+        counts = {k: v * mult for k, v in counts.items()}
+        if self.kind == "summa_cos":
+            add("dd", 1)                                    # Z = X X
+        if self.kind == "expm":
+            ells = [r.diagnostics["squarings"] for r in (rep if not hasattr(rep, "plan") else [rep])]
+            add("dd", sum(ells))
+        return counts
+
+    def units(self):
+        return self.B if self.kind in ("exp", "expm") else 1
+
+    def flop_scale(self):
+        """GEMM flops are 2 n^3 per (global) GEMM; for SUMMA each rank does
+        1/world of every GEMM."""
+        return 2.0 * self.n ** 3 / (self.world if self.kind == "summa_cos" else 1)
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import paper_2312_17396_b200 as mp
     from paper_2312_17396_b200 import _lib
-    from paper_2312_17396_b200.precision import MatBatch
 
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    ctx = mp.PrecisionCtx(CFG["digits"])
-    B, n, m = CFG["batch"], CFG["n"], CFG["m"]
-    Xh = make_batch(rank, B, n, CFG["norm"])
-    Xd = torch.from_numpy(Xh).cuda()
-    Xpin = torch.from_numpy(Xh).pin_memory()
+    wl = Workload(args.config, rank, world, torch, mp)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     h = _lib.handle_for()
 
-    def step(X):
-        return mp.ps_mixed_exp(X, m, ctx, timing=False)
-
     for _ in range(args.warmup):
-        rep = step(Xd)
+        rep = wl.step(wl.Xd)
     torch.cuda.synchronize()
-    plan0 = rep[0].plan
-    gem = honest_gemms(plan0)
+    gem = wl.gemms(rep)
+    plans = wl.plans(rep)
 
     def barrier():
         if dist is not None:
@@ -239,34 +369,39 @@ def run_ours(args, rank, world, local_rank):
     total = 0.0
     for _ in range(args.steps):
         flush.zero_()  # 256 MiB write between steps: L2 (126 MB) flushed
+        barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        rep = step(Xd)
+        rep = wl.step(wl.Xd)
         b.record()
         b.synchronize()
         total += a.elapsed_time(b) * 1e-3
     barrier()
-    launches = (h.launches - l0 - 0) / args.steps
+    launches = (h.launches - l0) / args.steps
     probe = h.probe
     h.probe = None
     clk = clocks.stop() if clocks else None
-    # flush.zero_ is a torch kernel, not ours; launches counts libmpps kernels only
 
     # ---- end-to-end through the public API with host buffers ----
-    out_host = torch.empty((2, B, n, n), dtype=torch.float64).pin_memory()
+    outs = None
     e2e_total = 0.0
     for i in range(args.steps + 1):
         flush.zero_()
+        barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        rep = step(Xpin)
-        out_host.copy_(rep.result.data, non_blocking=True)
+        rep = wl.step(wl.Xpin)
+        res = wl.results(rep)
+        if outs is None:
+            outs = [torch.empty(r.shape, dtype=r.dtype).pin_memory() for r in res]
+        for o, r in zip(outs, res):
+            o.copy_(r, non_blocking=True)
         b.record()
         b.synchronize()
         if i > 0:
             e2e_total += a.elapsed_time(b) * 1e-3
-    h2d = Xh.nbytes
-    d2h = out_host.numel() * 8
+    h2d = wl.Xh.nbytes
+    d2h = sum(o.numel() * o.element_size() for o in outs)
 
     t = torch.tensor([total, e2e_total], dtype=torch.float64, device="cuda")
     if dist is not None:
@@ -275,55 +410,54 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         dist.destroy_process_group()
         return
-    evals = B * world * args.steps
-    value = evals / total
-    e2e = B * world * args.steps / e2e_total
+    per_step_units = wl.units() * (world if wl.scaling == "weak" else 1)
+    value = per_step_units * args.steps / total
+    e2e = per_step_units * args.steps / e2e_total
 
-    # ---- roofline of the dominant kernel (dd power GEMM, batch 64) ----
+    # ---- roofline of the dominant kernel (timed live over the timed region) ----
     peaks = measure_peaks(torch, h)
     by_key = {}
     for key, evs in probe.items():
         durs = [x.elapsed_time(y) * 1e-3 for x, y in evs]
         by_key[key] = (len(durs), sum(durs))
+    names = {7: "fp32", 15: "fp64", 31: "dd", 63: "qd"}
     dom = max(by_key.items(), key=lambda kv: kv[1][1])
     (kind, fin, fout, M, N, K, nb), (cnt, sec) = dom
-    fname = {7: "fp32", 15: "fp64", 31: "dd", 63: "qd"}[fin]
-    flops_per_launch = 2.0 * M * N * K * nb
-    achieved = flops_per_launch / (sec / cnt) / 1e12
-    peak = peaks[fname]
+    fname = names[fin]
+    achieved = 2.0 * M * N * K * nb / (sec / cnt) / 1e12
     step_time = total / args.steps
-    dom_share = sec / args.steps / step_time
-    # whole-evaluation roofline: T_ideal = sum_P 2n^3 #GEMM_P / Peak_P
-    t_ideal = sum(2.0 * n ** 3 * c * B / (peaks[f] * 1e12) for f, c in gem.items())
-    eff_gflops = sum(2.0 * n ** 3 * c for c in gem.values()) * B * world * args.steps / total / 1e9
-
+    fs = wl.flop_scale()
+    t_ideal = sum(fs * c / (peaks[f] * 1e12) for f, c in gem.items())
+    eff_gflops = sum(fs * c for c in gem.values()) * world * args.steps / total / 1e9
+    plan0 = plans[0]
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * step_time, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "dd",
-        "data": "synthetic (seeded N(0,1) rescaled to ||X||_1=1, seeds rank*64+i)",
-        "config": {"workload": CFG["workload"], "batch_per_gpu": B, "n": n, "m": m, "digits": CFG["digits"],
-                   "schedule_digits": list(plan0.level_digits),
-                   "level_formats": rep[0].diagnostics["level_formats"],
-                   "gemms_per_eval": gem, "parallelism": f"batch-sharded x{world}",
+        "scaling": wl.scaling, "vs_baseline": None, "dtype": names[plan0.level_formats[0]],
+        "data": "synthetic (seeded N(0,1) rescaled to the config's ||X||_1; BASELINE configs have no dataset)",
+        "config": {"workload": wl.cfg["workload"], "name": args.config, "units_per_gpu_step": wl.units(),
+                   "n": wl.n, "m": wl.m, "digits": wl.cfg["digits"],
+                   "schedule_digits": [list(p.level_digits) for p in plans],
+                   "level_formats": wl.formats(rep), "gemms_per_step_per_gpu": gem,
+                   "parallelism": wl.parallelism,
                    "l2": "256 MiB buffer written between timed steps (L2 flushed)"},
         "gflops_effective": eff_gflops,
-        "roofline": {"bound": "fp64-pipe", "kernel": f"{kind} {fname}->{ {7: 'fp32', 15: 'fp64', 31: 'dd', 63: 'qd'}[fout]} "
-                                                     f"{M}x{N}x{K} x{nb}",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s (logical)",
-                     "frac": achieved / peak, "traffic": None, "share_of_step": dom_share,
+        "roofline": {"bound": "fp64-pipe" if fname != "fp32" else "fp32-pipe",
+                     "kernel": f"{kind} {fname}->{names[fout]} {M}x{N}x{K} x{nb}",
+                     "achieved": achieved, "peak": peaks[fname], "unit": "TFLOP/s (logical)",
+                     "frac": achieved / peaks[fname], "traffic": None, "share_of_step": sec / args.steps / step_time,
                      "launches_per_step": cnt / args.steps,
                      "peak_source": "FMA pipe microbenchmark in bench.py on this GPU "
                                     f"(fp64 {peaks['fp64']:.2f} TF/s, fp32 {peaks['fp32']:.2f} TF/s); "
-                                    "Peak_dd = Peak_fp64/15 (SURVEY 8d k_dd=15); MEASURED_PEAKS.json "
-                                    "holds only HBM and bf16",
+                                    "Peak_dd = Peak_fp64/15, Peak_qd = Peak_fp64/115 (SURVEY 8d); "
+                                    "MEASURED_PEAKS.json holds only HBM and bf16",
                      "eval_frac": t_ideal / step_time},
         "peaks_tflops": peaks,
         "e2e": {"value": e2e, "unit": "evals/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "clocks": clk,
     }
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and args.config == "cfg2":
         try:
             line["cpu_baseline"] = cpu_baseline_sample()
         except Exception as e:  # the baseline is reported, never required
@@ -340,7 +474,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     args = ap.parse_args()
+    CFG.clear()
+    CFG.update(CONFIGS[args.config])
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

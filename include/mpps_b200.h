@@ -106,13 +106,29 @@ int mpps_assemble_blocks(mpps_handle *h, const mpps_mat *powers, int s, int m,
                          const double *coeff_words, mpps_mat *blocks,
                          double *norms);
 
+/* Distributed variant for a local block (rows x cols) of 2-D block-distributed
+ * matrices (SUMMA, cfg5): the identity of b_{si} I is placed where
+ * row0 + i == col0 + j (global indices), and instead of norms the kernel
+ * writes the local column abs-sums colsums[b][i][j] (i = 0..r blocks, r+1 =
+ * Y), summed over the local rows in a fixed order; the caller all-reduces
+ * them along the process column and applies mpps_colmax. */
+int mpps_assemble_blocks_dist(mpps_handle *h, const mpps_mat *powers, int s,
+                              int m, const double *coeff_words,
+                              mpps_mat *blocks, double *colsums, int row0,
+                              int col0);
+
+/* out[b][i] = max_j colsums[b][i][j] (the column max of one_norm). */
+int mpps_colmax(mpps_handle *h, const double *colsums, int nvec, int cols,
+                int batch, double *out);
+
 /* one_norm (precision.py:235-249) of every batch member: norms[b]. */
 int mpps_one_norm(mpps_handle *h, const mpps_mat *A, double *norms);
 
 /* One fused matrix-Horner step of horner_mixed (engine.py:249-251):
  *   out = RN_out( 2^eo ( Bprev + 2^-(ey+ei) * RN_fmt(Y * phi) ) )
  * Y and phi share the level-j format, Bprev is the working-format block and
- * out is in the level-(j-1) format (>= level j's). */
+ * out is in the level-(j-1) format (>= level j's).  Shapes: Y is M x K, phi
+ * K x N, Bprev and out M x N (K = n; M, N < n for SUMMA blocks). */
 int mpps_horner_step(mpps_handle *h, const mpps_mat *Y, const mpps_mat *phi,
                      const mpps_mat *Bprev, mpps_mat *out, const int *sel,
                      int nsel, const int *exp_y, const int *exp_in,

@@ -17,8 +17,11 @@ from .planner import (EvaluationPlan, cost_ratio, default_block_size,
                       plan_precisions, snap_to_lattice)
 from .bounds import (BoundInputs, BoundInvalidError, extra_squarings, gamma,
                      tau_sequence, thm21_bound)
-from .engine import (BatchReport, EvaluationReport, cos_argument, horner_mixed, plan_only,
+from .engine import (BatchReport, EvaluationReport, cos_argument, horner_mixed, plan_only, ps_mixed_pade,
                      ps_fixed, ps_mixed_exp, ps_mixed_general)
+
+from .expm import expm_ss
+from . import ops, summa
 
 __version__ = "0.1.0"
 
@@ -31,5 +34,5 @@ __all__ = [
     "default_block_size", "horner_mixed", "plan_only", "plan_precisions",
     "ps_fixed", "ps_mixed_exp", "ps_mixed_general", "snap_to_lattice",
     "BoundInputs", "BoundInvalidError", "extra_squarings", "gamma",
-    "tau_sequence", "thm21_bound",
+    "tau_sequence", "thm21_bound", "expm_ss", "ops", "summa", "ps_mixed_pade",
 ]

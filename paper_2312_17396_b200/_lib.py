@@ -25,6 +25,7 @@ EXPORTED = (
     "mpps_last_error", "mpps_launch_count", "mpps_convert", "mpps_gemm",
     "mpps_axpy", "mpps_powers", "mpps_assemble_blocks", "mpps_one_norm",
     "mpps_horner_step", "mpps_horner_scalar_top", "mpps_probe_fma",
+    "mpps_assemble_blocks_dist", "mpps_colmax",
 )
 
 
@@ -86,6 +87,8 @@ def load_library(path: Optional[str] = None):
         lib.mpps_horner_step.argtypes = [vp, mp, mp, mp, mp, vp, ip, vp, vp, vp]
         lib.mpps_horner_scalar_top.argtypes = [vp, P(ctypes.c_double), ip, mp, mp, mp, vp, ip, vp]
         lib.mpps_probe_fma.argtypes = [vp, ip, ip, ip, vp]
+        lib.mpps_assemble_blocks_dist.argtypes = [vp, mp, ip, ip, vp, mp, vp, ip, ip]
+        lib.mpps_colmax.argtypes = [vp, vp, ip, ip, ip, vp]
         for name in EXPORTED:
             getattr(lib, name).restype = getattr(lib, name).restype or ip
         if path is None:
@@ -189,6 +192,16 @@ class Handle:
         parr, barr = cmat_array(powers), cmat_array(blocks)
         self._check(self.lib.mpps_assemble_blocks(self.h, parr, len(powers), m, coeff_dev.data_ptr(),
                                                   barr, norms_dev.data_ptr()), "assemble_blocks")
+
+    def assemble_blocks_dist(self, powers, m: int, coeff_dev, blocks, colsums_dev, row0: int, col0: int):
+        parr, barr = cmat_array(powers), cmat_array(blocks)
+        self._check(self.lib.mpps_assemble_blocks_dist(self.h, parr, len(powers), m, coeff_dev.data_ptr(),
+                                                       barr, colsums_dev.data_ptr(), row0, col0),
+                    "assemble_blocks_dist")
+
+    def colmax(self, colsums_dev, nvec: int, cols: int, batch: int, out_dev):
+        self._check(self.lib.mpps_colmax(self.h, colsums_dev.data_ptr(), nvec, cols, batch, out_dev.data_ptr()),
+                    "colmax")
 
     def one_norm(self, A: MatBatch, norms_dev):
         a = cmat(A)

@@ -191,8 +191,9 @@ struct AssembleArgs {
   MatRef P[kMaxPowers];   // X^1..X^s
   MatRef Bk[kMaxBlocks];  // B_0..B_r
   const double *coeff;    // (m+1) x 4 words
-  double *partial;        // [batch][nchunk][r+2][n]
-  int n, s, m, r, nchunk;
+  double *partial;        // [batch][nchunk][r+2][cols]
+  int rows, cols, s, m, r, nchunk;
+  int row0, col0;         // global offsets of this block (2-D distributed matrices)
 };
 
 // One thread per (column, 32-row chunk); the r+1 block accumulators of an
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(128) assemble_kernel(const AssembleArgs a) {
   using T = typename V::T;
   constexpr int CW = (WF == QD) ? 4 : (WF == DD ? 2 : 1);
   __shared__ double sc[kMaxBlocks * kMaxPowers * CW];
-  const int n = a.n, s = a.s, m = a.m, r = a.r;
+  const int n = a.cols, s = a.s, m = a.m, r = a.r;
   for (int t = threadIdx.x; t <= m; t += blockDim.x)
 #pragma unroll
     for (int w = 0; w < CW; ++w) sc[t * CW + w] = a.coeff[4 * t + w];
@@ -223,12 +224,13 @@ __global__ void __launch_bounds__(128) assemble_kernel(const AssembleArgs a) {
 #pragma unroll
   for (int k = 0; k <= kMaxBlocks; ++k) cs[k] = 0.0;
   const int row0 = chunk * kRowsPerChunk;
-  const int row1 = min(n, row0 + kRowsPerChunk);
+  const int row1 = min(a.rows, row0 + kRowsPerChunk);
   for (int row = row0; row < row1; ++row) {
     T acc[kMaxBlocks];
+    const bool diag = (row + a.row0) == (col + a.col0);
 #pragma unroll
     for (int k = 0; k < kMaxBlocks; ++k)
-      if (k <= r) acc[k] = (row == col) ? coef(s * k) : V::zero();
+      if (k <= r) acc[k] = diag ? coef(s * k) : V::zero();
     for (int j = 1; j < s; ++j) {
       const MatRef &P = a.P[j - 1];
       T x = V::from(load_qd(P, (long long)b * P.bstride + (long long)row * P.ld + col));
@@ -297,9 +299,24 @@ __global__ void norm_reduce_kernel(const double *partial, double *norms, int nbl
   if (threadIdx.x == 0) norms[(long long)b * nblk + k] = red[0];
 }
 
+// colsums[b][k][col] = sum_chunk partial[b][chunk][k][col] (fixed order)
+__global__ void colsum_reduce_kernel(const double *partial, double *colsums, int nblk, int nchunk, int cols,
+                                     int batch) {
+  const long long total = (long long)batch * nblk * cols;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int col = (int)(t % cols);
+    const long long bk = t / cols;
+    const int k = (int)(bk % nblk), b = (int)(bk / nblk);
+    double acc = 0.0;
+    for (int c = 0; c < nchunk; ++c) acc += partial[(((long long)b * nchunk + c) * nblk + k) * cols + col];
+    colsums[t] = acc;
+  }
+}
+
 struct ScalarTopArgs {
   MatRef Y, Bp, out;
-  int n, wf;
+  int rows, cols, wf;
   double bm[4];
   const int *sel, *exp_out;
 };
@@ -307,12 +324,12 @@ struct ScalarTopArgs {
 template <int FT, int FO>
 __global__ void scalar_top_kernel(const ScalarTopArgs a) {
   const int b = a.sel ? a.sel[blockIdx.z] : (int)blockIdx.z;
-  const long long total = (long long)a.n * a.n;
+  const long long total = (long long)a.rows * a.cols;
   const int eo = a.exp_out ? a.exp_out[b] : 0;
   const mp::qd bm = mp::qd_make(a.bm[0], a.bm[1], a.bm[2], a.bm[3]);
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(t / a.n), j = (int)(t % a.n);
+    const int i = (int)(t / a.cols), j = (int)(t % a.cols);
     mp::qd y = load_qd(a.Y, (long long)b * a.Y.bstride + (long long)i * a.Y.ld + j);
     mp::qd prod;
     if (a.wf == QD) {
@@ -499,9 +516,9 @@ int mpps_powers(mpps_handle *h, mpps_mat *powers, int s) {
   return MPPS_OK;
 }
 
-int mpps_assemble_blocks(mpps_handle *h, const mpps_mat *powers, int s, int m, const double *coeff,
-                         mpps_mat *blocks, double *norms) {
-  if (!powers || !blocks || !coeff || !norms) return set_err(h, MPPS_EINVAL, "assemble: null argument");
+static int assemble_common(mpps_handle *h, const mpps_mat *powers, int s, int m, const double *coeff,
+                           mpps_mat *blocks, double *norms, double *colsums, int row0, int col0) {
+  if (!powers || !blocks || !coeff || (!norms && !colsums)) return set_err(h, MPPS_EINVAL, "assemble: null argument");
   if (s < 1 || s > kMaxPowers || m < s) return set_err(h, MPPS_EINVAL, "need 1 <= s <= series degree (s=%d m=%d)", s, m);
   const int r = m / s;
   if (r + 1 > kMaxBlocks) return set_err(h, MPPS_EINVAL, "assemble: r+1=%d exceeds %d blocks", r + 1, kMaxBlocks);
@@ -509,28 +526,31 @@ int mpps_assemble_blocks(mpps_handle *h, const mpps_mat *powers, int s, int m, c
   if (wf == F32) return set_err(h, MPPS_EFMT, "assemble: working format must be fp64, dd or qd");
   AssembleArgs a;
   memset(&a, 0, sizeof(a));
-  const int n = powers[0].rows, batch = powers[0].batch;
+  const int rows = powers[0].rows, cols = powers[0].cols, batch = powers[0].batch;
   for (int k = 0; k < s; ++k) {
     int rc = check_mat(h, &powers[k], "assemble.power");
     if (rc) return rc;
-    if (powers[k].fmt != powers[0].fmt || powers[k].rows != n || powers[k].cols != n || powers[k].batch != batch)
+    if (powers[k].fmt != powers[0].fmt || powers[k].rows != rows || powers[k].cols != cols ||
+        powers[k].batch != batch)
       return set_err(h, MPPS_EINVAL, "assemble: powers must share format and shape");
     a.P[k] = ref_of(&powers[k]);
   }
   for (int k = 0; k <= r; ++k) {
     int rc = check_mat(h, &blocks[k], "assemble.block");
     if (rc) return rc;
-    if (blocks[k].fmt != powers[0].fmt || blocks[k].rows != n || blocks[k].cols != n || blocks[k].batch != batch)
+    if (blocks[k].fmt != powers[0].fmt || blocks[k].rows != rows || blocks[k].cols != cols ||
+        blocks[k].batch != batch)
       return set_err(h, MPPS_EINVAL, "assemble: blocks must match the powers");
     a.Bk[k] = ref_of(&blocks[k]);
   }
-  if (n == 0 || batch == 0) return MPPS_OK;
-  a.coeff = coeff; a.n = n; a.s = s; a.m = m; a.r = r;
-  a.nchunk = (n + kRowsPerChunk - 1) / kRowsPerChunk;
-  size_t pbytes = sizeof(double) * (size_t)batch * a.nchunk * (r + 2) * n;
+  if (rows == 0 || cols == 0 || batch == 0) return MPPS_OK;
+  a.coeff = coeff; a.rows = rows; a.cols = cols; a.s = s; a.m = m; a.r = r;
+  a.row0 = row0; a.col0 = col0;
+  a.nchunk = (rows + kRowsPerChunk - 1) / kRowsPerChunk;
+  size_t pbytes = sizeof(double) * (size_t)batch * a.nchunk * (r + 2) * cols;
   cudaError_t e = cudaMallocAsync((void **)&a.partial, pbytes, h->stream);
   if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "assemble scratch: %s", cudaGetErrorString(e));
-  dim3 grid((n + 127) / 128, a.nchunk, batch);
+  dim3 grid((cols + 127) / 128, a.nchunk, batch);
   switch (wf) {
     case F64: assemble_kernel<F64><<<grid, 128, 0, h->stream>>>(a); break;
     case DD: assemble_kernel<DD><<<grid, 128, 0, h->stream>>>(a); break;
@@ -538,10 +558,37 @@ int mpps_assemble_blocks(mpps_handle *h, const mpps_mat *powers, int s, int m, c
   }
   int rc = after_launch(h, "assemble_kernel");
   if (rc) return rc;
-  norm_reduce_kernel<<<dim3(r + 2, batch), 256, 0, h->stream>>>(a.partial, norms, r + 2, a.nchunk, n);
-  rc = after_launch(h, "norm_reduce_kernel");
+  if (norms) {
+    norm_reduce_kernel<<<dim3(r + 2, batch), 256, 0, h->stream>>>(a.partial, norms, r + 2, a.nchunk, cols);
+    rc = after_launch(h, "norm_reduce_kernel");
+  } else {
+    long long tot = (long long)batch * (r + 2) * cols;
+    colsum_reduce_kernel<<<ew_grid(tot), 256, 0, h->stream>>>(a.partial, colsums, r + 2, a.nchunk, cols, batch);
+    rc = after_launch(h, "colsum_reduce_kernel");
+  }
   cudaFreeAsync(a.partial, h->stream);
   return rc;
+}
+
+int mpps_assemble_blocks(mpps_handle *h, const mpps_mat *powers, int s, int m, const double *coeff,
+                         mpps_mat *blocks, double *norms) {
+  if (powers && (powers[0].rows != powers[0].cols))
+    return set_err(h, MPPS_EINVAL, "assemble: square matrices expected (use mpps_assemble_blocks_dist)");
+  return assemble_common(h, powers, s, m, coeff, blocks, norms, nullptr, 0, 0);
+}
+
+int mpps_assemble_blocks_dist(mpps_handle *h, const mpps_mat *powers, int s, int m, const double *coeff,
+                              mpps_mat *blocks, double *colsums, int row0, int col0) {
+  if (!colsums) return set_err(h, MPPS_EINVAL, "assemble_dist: null colsums");
+  return assemble_common(h, powers, s, m, coeff, blocks, nullptr, colsums, row0, col0);
+}
+
+int mpps_colmax(mpps_handle *h, const double *colsums, int nvec, int cols, int batch, double *out) {
+  if (!colsums || !out || nvec < 1 || cols < 1 || batch < 0) return set_err(h, MPPS_EINVAL, "colmax: bad arguments");
+  if (batch == 0) return MPPS_OK;
+  // colsums laid out [batch][nvec][cols] == partial layout with nchunk = 1
+  norm_reduce_kernel<<<dim3(nvec, batch), 256, 0, h->stream>>>(colsums, out, nvec, 1, cols);
+  return after_launch(h, "norm_reduce_kernel");
 }
 
 int mpps_one_norm(mpps_handle *h, const mpps_mat *A, double *norms) {
@@ -573,13 +620,12 @@ int mpps_horner_step(mpps_handle *h, const mpps_mat *Y, const mpps_mat *phi, con
     return rc;
   if (Y->fmt != phi->fmt) return set_err(h, MPPS_EFMT, "horner: Y and phi formats differ (%d, %d)", Y->fmt, phi->fmt);
   if (fmt_index(Bprev->fmt) == F32) return set_err(h, MPPS_EFMT, "horner: B_{j-1} must be at the working format");
-  const int n = Y->rows;
-  if (Y->cols != n || phi->rows != n || phi->cols != n || Bprev->rows != n || Bprev->cols != n || out->rows != n ||
-      out->cols != n)
-    return set_err(h, MPPS_EINVAL, "horner: all operands must be %dx%d", n, n);
+  const int M = Y->rows, K = Y->cols, N = phi->cols;
+  if (phi->rows != K || Bprev->rows != M || Bprev->cols != N || out->rows != M || out->cols != N)
+    return set_err(h, MPPS_EINVAL, "horner: operands must be Y %dx%d, phi %dx%d, B/out %dx%d", M, K, K, N, M, N);
   GemmArgs g;
   memset(&g, 0, sizeof(g));
-  g.M = n; g.N = n; g.K = n;
+  g.M = M; g.N = N; g.K = K;
   g.A = ref_of(Y); g.B = ref_of(phi); g.C = ref_of(out);
   g.sel = sel;
   g.epi.Bprev = ref_of(Bprev);
@@ -599,14 +645,16 @@ int mpps_horner_scalar_top(mpps_handle *h, const double *bm, int fmt_top, const 
   if (ft < 0) return set_err(h, MPPS_EFMT, "scalar_top: bad level format %d", fmt_top);
   if (wf == F32) return set_err(h, MPPS_EFMT, "scalar_top: Y must be at the working format");
   if (fo < ft) return set_err(h, MPPS_EFMT, "scalar_top: output narrower than the level format");
+  if (Bprev->rows != Y->rows || Bprev->cols != Y->cols || out->rows != Y->rows || out->cols != Y->cols)
+    return set_err(h, MPPS_EINVAL, "scalar_top: operands must share the shape %dx%d", Y->rows, Y->cols);
   ScalarTopArgs a;
   a.Y = ref_of(Y); a.Bp = ref_of(Bprev); a.out = ref_of(out);
-  a.n = Y->rows; a.wf = wf;
+  a.rows = Y->rows; a.cols = Y->cols; a.wf = wf;
   for (int i = 0; i < 4; ++i) a.bm[i] = bm[i];
   a.sel = sel; a.exp_out = exp_out;
   int nb = sel ? nsel : out->batch;
-  if (nb == 0 || a.n == 0) return MPPS_OK;
-  dim3 grid(ew_grid((long long)a.n * a.n / 4 + 1), 1, nb);
+  if (nb == 0 || a.rows == 0 || a.cols == 0) return MPPS_OK;
+  dim3 grid(ew_grid((long long)a.rows * a.cols / 4 + 1), 1, nb);
 #define ST(A, B) \
   if (ft == A && fo == B) scalar_top_kernel<A, B><<<grid, 256, 0, h->stream>>>(a); else
   ST(F32, F32) ST(F32, F64) ST(F32, DD) ST(F32, QD) ST(F64, F64) ST(F64, DD) ST(F64, QD) ST(DD, DD) ST(DD, QD)

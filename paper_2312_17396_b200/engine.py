@@ -265,24 +265,11 @@ class _Prepared:
     coeffs: np.ndarray         # (m+1, 4) words at the working precision
 
 
-def _prepare(h, Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: int,
-             timer: _Buckets, x_is_working: Optional[MatBatch] = None) -> _Prepared:
-    """eval_b0_and_power + assemble_block + one_norm (engine.py:141-154,
-    127-138, 467-468) for the whole batch, then the one host sync."""
-    torch = _torch()
+def _form_powers(h, Xt, wf: int, s: int, timer: _Buckets, x_is_working: Optional[MatBatch] = None):
+    """X, X^2..X^s at the working format (engine.py:141-154 power chain)."""
     dev = Xt.device if Xt is not None else x_is_working.device
     B = Xt.shape[0] if Xt is not None else x_is_working.batch
     n = Xt.shape[1] if Xt is not None else x_is_working.rows
-    m = series.degree
-    r = m // s
-    cw = coeff_words(series, ctx)
-    key = (series.coeffs, ctx.binary_precision, str(dev))
-    coeffs = _COEFF_DEV.get(key)
-    if coeffs is None:
-        coeffs = torch.tensor(cw, dtype=torch.float64, device=dev)
-        if len(_COEFF_DEV) > 64:
-            _COEFF_DEV.clear()
-        _COEFF_DEV[key] = coeffs
     timer.start("power_formation")
     powers = [MatBatch.empty(wf, B, n, device=dev) for _ in range(s)]
     if x_is_working is not None:
@@ -295,6 +282,26 @@ def _prepare(h, Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: in
     for k in range(1, s):           # X^{k+1} = X^k X   (engine.py:151-153)
         h.gemm(powers[k - 1], powers[0], powers[k])
     timer.stop()
+    return powers
+
+
+def _assemble(h, powers: List[MatBatch], series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: int,
+              timer: _Buckets) -> _Prepared:
+    """assemble_block for every block + one_norm (engine.py:127-138,
+    467-468), then the one host sync for the planner's norms."""
+    torch = _torch()
+    dev = powers[0].device
+    B, n = powers[0].batch, powers[0].rows
+    m = series.degree
+    r = m // s
+    cw = coeff_words(series, ctx)
+    key = (series.coeffs, ctx.binary_precision, str(dev))
+    coeffs = _COEFF_DEV.get(key)
+    if coeffs is None:
+        coeffs = torch.tensor(cw, dtype=torch.float64, device=dev)
+        if len(_COEFF_DEV) > 64:
+            _COEFF_DEV.clear()
+        _COEFF_DEV[key] = coeffs
     timer.start("coefficient_assembly")
     blocks = [MatBatch.empty(wf, B, n, device=dev) for _ in range(r + 1)]
     norms = torch.empty((B, r + 2), dtype=torch.float64, device=dev)
@@ -304,6 +311,14 @@ def _prepare(h, Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: in
     norms_h = norms.cpu().numpy()   # the one host sync of the pipeline
     timer.stop()
     return _Prepared(wf, s, r, m, powers, blocks, norms_h, cw)
+
+
+def _prepare(h, Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: int,
+             timer: _Buckets, x_is_working: Optional[MatBatch] = None) -> _Prepared:
+    """eval_b0_and_power + assemble_block + one_norm (engine.py:141-154,
+    127-138, 467-468) for the whole batch."""
+    powers = _form_powers(h, Xt, wf, s, timer, x_is_working)
+    return _assemble(h, powers, series, ctx, wf, s, timer)
 
 
 def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buckets) -> MatBatch:
@@ -592,6 +607,31 @@ def _ps_mixed_exp_one(Xt, Xw, m, ctx, fix_params, delta, with_bound, timing, gro
     timer = _Buckets(timing)
     prep = _prepare(h, Xt, series, ctx, _working_format(ctx), s, timer, Xw)
     return _mixed_tail(h, prep, ctx, delta, False, fix_params, with_bound, True, timer)
+
+
+def ps_mixed_pade(X, k: int, ctx: PrecisionCtx, delta: float = 10.0, with_bound: bool = False,
+                  timing: bool = True):
+    """Numerator and denominator of the diagonal [k/k] Pade approximant of
+    exp, each by ps_mixed_general (engine.py:348-387) with its own plan
+    (config 4), sharing one power chain: both series have degree k, so both
+    use s = ceil(sqrt(k)) and the reference forms identical powers X^2..X^s
+    for the two calls -- forming them once is exact.  Returns (num, den)."""
+    from .coefficients import pade_exp_coeffs
+    Xt, Xw, single = _input(X)
+    B, n = _check_square(Xt, Xw)
+    if k < 1:
+        raise ValueError("series degree must be >= 1")
+    num, den = pade_exp_coeffs(k, k)
+    h = _lib.handle_for()
+    timer = _Buckets(timing)
+    wf = _working_format(ctx)
+    s = default_block_size(k)
+    powers = _form_powers(h, Xt, wf, s, timer, Xw)
+    out = []
+    for series in (num, den):
+        prep = _assemble(h, powers, series, ctx, wf, s, timer)
+        out.append(_mixed_tail(h, prep, ctx, delta, True, True, with_bound, single, timer))
+    return tuple(out)
 
 
 def plan_only(X, series: CoefficientSeries, ctx: PrecisionCtx, delta: float = 10.0,

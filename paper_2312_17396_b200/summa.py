@@ -1,0 +1,288 @@
+"""2-D block SUMMA driver: one large matrix polynomial over a pr x pc grid of
+GPUs, NCCL collectives through torch.distributed.
+
+Every rank owns block (I, J) of X, of each power X^k, of every coefficient
+block B_i and of every Horner iterate: rows [I n/pr, (I+1) n/pr), columns
+[J n/pc, (J+1) n/pc).  A product C = A B is formed block-locally as
+C_IJ = A_I: B_:J from two gathered panels:
+
+  * power chain X^k = X^{k-1} X (engine.py:151-153): the column panel X_:J is
+    gathered ONCE per evaluation (all-gather along the process column), the
+    row panel of X^{k-1} each step (all-gather along the process row);
+  * Horner Y phi_j (engine.py:249-251): the row panel Y_I: is gathered once
+    (at the working format, converted locally to each level format), the
+    column panel of phi_j each level -- in the level format, so fp32 levels
+    move 1/4 of the dd bytes;
+  * block assembly, the Horner add and all format conversions are local;
+  * planner norms: local column abs-sums (mpps_assemble_blocks_dist) ->
+    all-reduce(sum) along the process column -> column max -> all-reduce(max)
+    over the grid; every rank then runs the same deterministic planner and
+    rank 0's digits are broadcast so the schedule is identical everywhere.
+
+The arithmetic is the same C-ABI kernels as the single-GPU path (rectangular
+GEMM blocks with the fused Horner epilogue).  The ``ops`` object isolates the
+device calls so the collective plumbing is testable on CPU with gloo
+(tests/test_summa_gloo.py).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Tuple
+
+import numpy as np
+
+from .coefficients import CoefficientSeries, coeff_words
+from .planner import default_block_size, formats_of_digits, plan_digits_batch, plan_precisions
+from .precision import FP32, FP64, MatBatch, PrecisionCtx
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dist():
+    import torch.distributed as dist
+    return dist
+
+
+class ProcessGrid:
+    """pr x pc process grid over the default process group (row-major ranks)
+    with one communicator per process row and per process column."""
+
+    def __init__(self, pr: int, pc: int):
+        dist = _dist()
+        world = dist.get_world_size()
+        if pr * pc != world:
+            raise ValueError(f"grid {pr}x{pc} != world size {world}")
+        self.pr, self.pc = pr, pc
+        self.rank = dist.get_rank()
+        self.I, self.J = divmod(self.rank, pc)
+        # every rank must create every group, in the same order
+        rows = [dist.new_group([i * pc + j for j in range(pc)]) if pc > 1 else None for i in range(pr)]
+        cols = [dist.new_group([i * pc + j for i in range(pr)]) if pr > 1 else None for j in range(pc)]
+        self.row_group = rows[self.I]
+        self.col_group = cols[self.J]
+
+    @staticmethod
+    def for_world(world: int) -> Tuple[int, int]:
+        """1x1, 1x2, 2x2, 2x4, ... (pr <= pc, pr a power-of-two split)."""
+        pr = 1
+        while (pr * 2) * (pr * 2) <= world and world % (pr * 2) == 0:
+            pr *= 2
+        return pr, world // pr
+
+    def block(self, n: int):
+        if n % self.pr or n % self.pc:
+            raise ValueError(f"n={n} must be divisible by the grid {self.pr}x{self.pc}")
+        mr, nc = n // self.pr, n // self.pc
+        return self.I * mr, mr, self.J * nc, nc
+
+    # --- panels ------------------------------------------------------
+    def row_panel(self, A: MatBatch) -> MatBatch:
+        """A_I: = [A_I0 ... A_I(pc-1)] (all-gather along the process row)."""
+        if self.pc == 1:
+            return A
+        torch, dist = _torch(), _dist()
+        parts = [torch.empty_like(A.data) for _ in range(self.pc)]
+        dist.all_gather(parts, A.data.contiguous(), group=self.row_group)
+        return MatBatch(torch.cat(parts, dim=3), A.fmt)
+
+    def col_panel(self, A: MatBatch) -> MatBatch:
+        """A_:J = [A_0J; ...; A_(pr-1)J] (all-gather along the process column)."""
+        if self.pr == 1:
+            return A
+        torch, dist = _torch(), _dist()
+        parts = [torch.empty_like(A.data) for _ in range(self.pr)]
+        dist.all_gather(parts, A.data.contiguous(), group=self.col_group)
+        return MatBatch(torch.cat(parts, dim=2), A.fmt)
+
+    def sum_over_column(self, t):
+        if self.pr > 1:
+            _dist().all_reduce(t, op=_dist().ReduceOp.SUM, group=self.col_group)
+        return t
+
+    def max_over_grid(self, t):
+        if self.pr * self.pc > 1:
+            _dist().all_reduce(t, op=_dist().ReduceOp.MAX)
+        return t
+
+    def broadcast(self, t):
+        if self.pr * self.pc > 1:
+            _dist().broadcast(t, src=0)
+        return t
+
+    def gather_full(self, A: MatBatch, n: int) -> Optional[np.ndarray]:
+        """Assemble the global (words, n, n) matrix on every rank (checking
+        and tests only; not on the timed path)."""
+        torch, dist = _torch(), _dist()
+        if self.pr * self.pc == 1:
+            return A.data[:, 0].double().cpu().numpy()
+        parts = [torch.empty_like(A.data) for _ in range(self.pr * self.pc)]
+        dist.all_gather(parts, A.data.contiguous())
+        rows = []
+        for i in range(self.pr):
+            rows.append(torch.cat(parts[i * self.pc:(i + 1) * self.pc], dim=3))
+        return torch.cat(rows, dim=2)[:, 0].double().cpu().numpy()
+
+
+class DeviceOps:
+    """The C-ABI kernels, for SummaPS (one matrix per call, batch = 1)."""
+
+    def __init__(self, handle=None):
+        from . import _lib
+        self.h = handle or _lib.handle_for()
+        torch = _torch()
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    def empty(self, fmt, rows, cols):
+        return MatBatch.empty(fmt, 1, rows, cols, device=self.device)
+
+    def _e(self, e):
+        if not e:
+            return None
+        return _torch().tensor([int(e)], dtype=_torch().int32, device=self.device)
+
+    def convert(self, src, dst, exp=0):
+        self.h.convert(src, dst, None, self._e(exp))
+
+    def gemm(self, A, B, C):
+        self.h.gemm(A, B, C)
+
+    def coeffs(self, series, ctx):
+        return _torch().tensor(coeff_words(series, ctx), dtype=_torch().float64, device=self.device)
+
+    def assemble_dist(self, powers, m, coeffs, blocks, row0, col0):
+        torch = _torch()
+        r = len(blocks) - 1
+        colsums = torch.empty((1, r + 2, powers[0].cols), dtype=torch.float64, device=self.device)
+        self.h.assemble_blocks_dist(powers, m, coeffs, blocks, colsums, row0, col0)
+        return colsums
+
+    def colmax(self, colsums):
+        torch = _torch()
+        out = torch.empty((colsums.shape[0], colsums.shape[1]), dtype=torch.float64, device=self.device)
+        self.h.colmax(colsums, colsums.shape[1], colsums.shape[2], colsums.shape[0], out)
+        return out
+
+    def horner_step(self, Y, phi, Bprev, out, ey=0, ei=0, eo=0):
+        self.h.horner_step(Y, phi, Bprev, out, None, self._e(ey), self._e(ei), self._e(eo))
+
+    def scalar_top(self, bm_words, fmt_top, Y, Bprev, out, eo=0):
+        self.h.horner_scalar_top(bm_words, fmt_top, Y, Bprev, out, None, self._e(eo))
+
+
+@dataclass
+class DistResult:
+    block: MatBatch            # this rank's block of p(X) at the working format
+    digits: Tuple[int, ...]
+    nu: int
+    nilpotent: bool
+    norms: np.ndarray          # (r+2,) global ||B_0..B_r||, ||Y||
+    s: int
+    r: int
+
+    def plan(self, ctx: PrecisionCtx, delta: float = 10.0):
+        """The full EvaluationPlan (exact planner on the global norms)."""
+        return plan_precisions(tuple(float(x) for x in self.norms[:self.r + 1]), float(self.norms[self.r + 1]),
+                               ctx, delta, s=self.s)
+
+
+def _exp_for(v: float) -> int:
+    return -int(round(math.log2(v))) if v > 0 and math.isfinite(v) else 0
+
+
+def _working(ctx):
+    f = ctx.fmt
+    return FP64 if f == FP32 else f
+
+
+def cos_argument_dist(Xblk: MatBatch, ctx: PrecisionCtx, grid: ProcessGrid, ops) -> MatBatch:
+    """Z_IJ = X_I: X_:J at the working format (harness.py:100-101)."""
+    wf = _working(ctx)
+    Xw = Xblk
+    if Xblk.fmt != wf:
+        Xw = ops.empty(wf, Xblk.rows, Xblk.cols)
+        ops.convert(Xblk, Xw)
+    Z = ops.empty(wf, Xw.rows, Xw.cols)
+    ops.gemm(grid.row_panel(Xw), grid.col_panel(Xw), Z)
+    return Z
+
+
+def ps_mixed_dist(Xblk: MatBatch, series: CoefficientSeries, ctx: PrecisionCtx, grid: ProcessGrid,
+                  ops=None, delta: float = 10.0, fixed: bool = False) -> DistResult:
+    """ps_mixed_general (engine.py:348-387) -- or ps_fixed (304-345) with
+    ``fixed`` -- of one n x n matrix distributed over ``grid``; Xblk is this
+    rank's block (fp64 or working format)."""
+    torch = _torch()
+    ops = ops or DeviceOps()
+    m = series.degree
+    if m < 1:
+        raise ValueError("series degree must be >= 1")
+    d = ctx.decimal_digits
+    wf = _working(ctx)
+    s = default_block_size(m)
+    r = m // s
+    n = Xblk.rows * grid.pr
+    row0, mr, col0, nc = grid.block(n)
+    if (Xblk.rows, Xblk.cols) != (mr, nc):
+        raise ValueError(f"block shape {(Xblk.rows, Xblk.cols)} != {(mr, nc)} for n={n}")
+    # powers (engine.py:141-154): X^k = X^{k-1} X
+    P1 = Xblk
+    if Xblk.fmt != wf:
+        P1 = ops.empty(wf, mr, nc)
+        ops.convert(Xblk, P1)
+    powers = [P1]
+    if s > 1:
+        Xcol = grid.col_panel(P1)
+        for _ in range(1, s):
+            C = ops.empty(wf, mr, nc)
+            ops.gemm(grid.row_panel(powers[-1]), Xcol, C)
+            powers.append(C)
+    blocks = [ops.empty(wf, mr, nc) for _ in range(r + 1)]
+    coeffs = ops.coeffs(series, ctx)
+    colsums = ops.assemble_dist(powers, m, coeffs, blocks, row0, col0)
+    grid.sum_over_column(colsums)
+    norms_t = grid.max_over_grid(ops.colmax(colsums))
+    norms = norms_t.double().cpu().numpy()[0]
+    # planner (identical inputs on all ranks; rank 0's digits broadcast)
+    if fixed:
+        digits = np.full(r, d, dtype=np.int64)
+        nu, nil = r + 1, False
+    else:
+        dg, nv, nl = plan_digits_batch(norms[None, :r + 1], norms[None, r + 1], d, delta)
+        digits, nu, nil = dg[0], int(nv[0]), bool(nl[0])
+    pk = torch.tensor(list(digits) + [nu, int(nil)], dtype=torch.int64, device=norms_t.device)
+    grid.broadcast(pk)
+    pk = pk.cpu().numpy()
+    digits, nu, nil = tuple(int(x) for x in pk[:r]), int(pk[r]), bool(pk[r + 1])
+    if nil:
+        return DistResult(blocks[0], digits, nu, True, norms, s, r)
+    fm = (wf,) + formats_of_digits(digits)
+    ex = [(_exp_for(float(norms[j])) if fm[j] == FP32 else 0) for j in range(r + 1)]
+    ey = _exp_for(float(norms[r + 1]))
+    # Horner (engine.py:243-252)
+    Y = powers[s - 1]
+    Yrow_w = grid.row_panel(Y)
+    yrow = {wf: Yrow_w}
+    for f in sorted(set(fm[1:])):
+        if f not in yrow:
+            yf = ops.empty(f, Yrow_w.rows, Yrow_w.cols)
+            ops.convert(Yrow_w, yf, ey if f == FP32 else 0)
+            yrow[f] = yf
+    if m % s == 0:
+        out = ops.empty(fm[r - 1], mr, nc)
+        ops.scalar_top(coeff_words(series, ctx)[m], fm[r], Y, blocks[r - 1], out, ex[r - 1])
+        phi, j0 = out, r - 1
+    else:
+        phi = ops.empty(fm[r], mr, nc)
+        ops.convert(blocks[r], phi, ex[r])
+        j0 = r
+    for j in range(j0, 0, -1):
+        out = ops.empty(fm[j - 1], mr, nc)
+        ops.horner_step(yrow[fm[j]], grid.col_panel(phi), blocks[j - 1], out,
+                        ey if fm[j] == FP32 else 0, ex[j], ex[j - 1])
+        phi = out
+    return DistResult(phi, digits, nu, False, norms, s, r)

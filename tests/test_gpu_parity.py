@@ -263,3 +263,18 @@ def test_cfg2_full_size_properties(cuda):
     normP = np.abs(P.result.data[0].cpu().numpy()).sum(axis=1).max(axis=-1)
     assert (err <= 3 * tol(5, n, d) * normP ** 2).all(), err.max()
     assert P[0].diagnostics["level_formats"][0] == "dd"
+
+
+def test_pade_pair_shares_powers_bitwise(cuda):
+    """ps_mixed_pade forms the powers once; each polynomial equals its own
+    ps_mixed_general evaluation bit for bit (identical powers, kernels, plan)."""
+    m = mp()
+    X = synth(48, 2.0, 4)
+    for d, k in ((15, 13), (63, 26)):
+        ctx = m.PrecisionCtx(d)
+        num, den = m.ps_mixed_pade(X, k, ctx)
+        sn, sd = m.pade_exp_coeffs(k, k)
+        a = m.ps_mixed_general(X, sn, ctx)
+        b = m.ps_mixed_general(X, sd, ctx)
+        assert num.plan.level_digits == a.plan.level_digits and den.plan.level_digits == b.plan.level_digits
+        assert np.array_equal(words_of(num), words_of(a)) and np.array_equal(words_of(den), words_of(b))

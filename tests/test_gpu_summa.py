@@ -1,0 +1,59 @@
+"""SUMMA driver on the GPU over NCCL (one rank, 1x1 grid -- the box has one
+GPU; the multi-rank plumbing is covered by tests/test_summa_gloo.py): the
+distributed pipeline runs the same kernels in the same order as the
+single-GPU path, so its result and plan are bitwise identical."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from _util import synth, tol
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nccl1(cuda):
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    yield
+    dist.destroy_process_group()
+
+
+def test_summa_1x1_bitwise_equals_single_gpu(nccl1):
+    import torch
+    import paper_2312_17396_b200 as m
+    from paper_2312_17396_b200 import summa
+    from paper_2312_17396_b200.precision import MatBatch
+    n = 96
+    ctx = m.PrecisionCtx(31)
+    X = synth(n, 1.0, 0, cos=True)
+    grid = summa.ProcessGrid(1, 1)
+    blk = MatBatch(torch.from_numpy(X).cuda()[None, None], m.FP64)
+    Z = summa.cos_argument_dist(blk, ctx, grid, summa.DeviceOps())
+    res = summa.ps_mixed_dist(Z, m.taylor_cos_coeffs(24), ctx, grid)
+    ref = m.ps_mixed_general(m.cos_argument(X, ctx), m.taylor_cos_coeffs(24), ctx)
+    assert res.digits == ref.plan.level_digits and res.nu == ref.plan.nu
+    assert np.array_equal(res.block.data.cpu().numpy(), ref.result.data.cpu().numpy())
+    assert res.plan(ctx).to_dict() == ref.plan.to_dict()
+
+
+def test_summa_1x1_vs_oracle(nccl1, oracle_lib):
+    import torch
+    import paper_2312_17396_b200 as m
+    from paper_2312_17396_b200 import summa
+    from paper_2312_17396_b200.precision import MatBatch
+    n, d = 64, 31
+    X = synth(n, 1.0, 2)
+    grid = summa.ProcessGrid(1, 1)
+    res = summa.ps_mixed_dist(MatBatch(torch.from_numpy(X).cuda()[None, None], m.FP64),
+                              m.taylor_exp_coeffs(30), m.PrecisionCtx(d), grid)
+    ref = oracle_lib.ps_eval(X, m.taylor_exp_coeffs(30).coeffs, d)
+    assert res.digits == ref.digits
+    diff, refn = ref.compare(res.block.data[:, 0].cpu().numpy())
+    assert diff <= tol(res.r, n, d) * refn
