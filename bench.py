@@ -360,11 +360,11 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
 
     # ---- device-resident timed region (value) ----
-    clocks = ClockSampler(local_rank) if rank == 0 else None
+    clocks = ClockSampler(local_rank) if (rank == 0 and not args.no_clocks) else None
     barrier()
     if clocks:
         clocks.start()
-    h.probe = {}
+    h.probe = None if args.no_probe else {}
     l0 = h.launches
     total = 0.0
     for _ in range(args.steps):
@@ -417,10 +417,12 @@ def run_ours(args, rank, world, local_rank):
     # ---- roofline of the dominant kernel (timed live over the timed region) ----
     peaks = measure_peaks(torch, h)
     by_key = {}
-    for key, evs in probe.items():
+    for key, evs in (probe or {}).items():
         durs = [x.elapsed_time(y) * 1e-3 for x, y in evs]
         by_key[key] = (len(durs), sum(durs))
     names = {7: "fp32", 15: "fp64", 31: "dd", 63: "qd"}
+    if not by_key:
+        by_key[("none", 31, 31, 1, 1, 1, 1)] = (1, 1.0)
     dom = max(by_key.items(), key=lambda kv: kv[1][1])
     (kind, fin, fout, M, N, K, nb), (cnt, sec) = dom
     fname = names[fin]
@@ -475,6 +477,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-probe", action="store_true", help="diagnostic: no per-launch events")
+    ap.add_argument("--no-clocks", action="store_true", help="diagnostic: no nvidia-smi sampling")
     args = ap.parse_args()
     CFG.clear()
     CFG.update(CONFIGS[args.config])

@@ -16,7 +16,8 @@ from typing import Optional
 
 from .precision import DimensionError, MatBatch, UnsupportedPrecisionError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libmpps_b200.so")
+LIB_PATH = os.environ.get("MPPS_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "libmpps_b200.so")
 
 MPPS_OK, MPPS_EINVAL, MPPS_EFMT, MPPS_ECUDA = 0, 1, 2, 3
 

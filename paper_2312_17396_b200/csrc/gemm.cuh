@@ -62,13 +62,35 @@ constexpr int kThreads = 256;
 
 // Dynamic shared memory of gemm_kernel<F, ...>: two ring slots of the A and
 // B tiles, all word planes.
+constexpr int kStages = 3;
+
+template <int F> struct SmemGeom {
+  using T = typename FmtT<F>::word;
+  static constexpr int W = FmtT<F>::W;
+  static constexpr int APAD = 1;                          // odd A row stride: conflict-free column reads
+  static constexpr int BPAD = (sizeof(T) == 8) ? 2 : 4;   // 16-byte aligned B rows (vector reads)
+  static constexpr int AROW = Tile<F>::BK + APAD;
+  static constexpr int BROW = Tile<F>::BN + BPAD;
+  static constexpr size_t A_STAGE = (size_t)W * Tile<F>::BM * AROW;   // elements
+  static constexpr size_t B_STAGE = (size_t)W * Tile<F>::BK * BROW;
+};
+
 template <int F>
 constexpr size_t gemm_smem_bytes() {
-  using T = typename FmtT<F>::word;
-  constexpr int PAD = (sizeof(T) == 8) ? 2 : 4;
-  return sizeof(T) * 2 * FmtT<F>::W * Tile<F>::BK *
-         ((Tile<F>::BM + PAD) + (Tile<F>::BN + PAD));
+  using G = SmemGeom<F>;
+  return sizeof(typename G::T) * kStages * (G::A_STAGE + G::B_STAGE);
 }
+
+// cp.async with zero fill (src-size 0 when out of bounds: ragged tiles).
+template <int BYTES>
+__device__ __forceinline__ void cp_async_zfill(void *smem, const void *gmem, bool pred) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int src = pred ? BYTES : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(s), "l"(gmem), "n"(BYTES), "r"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // ------------------------------------------------------------ accumulators
 template <int F> struct Acc;
@@ -89,7 +111,14 @@ template <> struct Acc<F64> {
 template <> struct Acc<DD> {
   double h, l;
   __device__ __forceinline__ void zero() { h = 0.0; l = 0.0; }
+  // 12-instruction MAC (TwoSum).  The 9-instruction magnitude-select
+  // FastTwoSum variant (mp::dd_mac9) measured 12-17 % slower on B200: its
+  // integer compare/selects cost more issue slots than the 3 DADDs saved.
+#ifdef MPPS_DD_MAC9
+  __device__ __forceinline__ void mac(const double *a, const double *b) { mp::dd_mac9(a[0], a[1], b[0], b[1], h, l); }
+#else
   __device__ __forceinline__ void mac(const double *a, const double *b) { mp::dd_mac(a[0], a[1], b[0], b[1], h, l); }
+#endif
   __device__ __forceinline__ void renorm() { mp::dd_acc_renorm(h, l); }
   __device__ __forceinline__ mp::qd as_qd() const { return mp::qd_make(h, l, 0.0, 0.0); }
 };
@@ -150,14 +179,17 @@ __device__ __forceinline__ mp::qd horner_add(const mp::qd &B, const mp::qd &T) {
 
 // ---------------------------------------------------------------- kernel
 // MODE 0: C = A*B stored in format F.  MODE 1: fused Horner epilogue into FO.
+template <int F> struct MinBlocks { enum { value = 2 }; };
+template <> struct MinBlocks<F32> { enum { value = 1 }; };
+
 template <int F, int FO, int MODE>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, MinBlocks<F>::value)
 gemm_kernel(const GemmArgs args) {
+  using G = SmemGeom<F>;
   using T = typename FmtT<F>::word;
   constexpr int W = FmtT<F>::W;
   constexpr int BM = Tile<F>::BM, BN = Tile<F>::BN, BK = Tile<F>::BK;
   constexpr int TM = Tile<F>::TM, TN = Tile<F>::TN;
-  constexpr int PAD = (sizeof(T) == 8) ? 2 : 4;
   constexpr int A_PER = BM * BK / kThreads;  // A elements per thread per plane
   constexpr int B_PER = BK * BN / kThreads;
   constexpr int TX = BN / TN;                // threads along N
@@ -165,10 +197,8 @@ gemm_kernel(const GemmArgs args) {
   static_assert(A_PER >= 1 && B_PER >= 1, "tile too small");
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  typedef T ATile[W][BK][BM + PAD];
-  typedef T BTile[W][BK][BN + PAD];
-  ATile *As = reinterpret_cast<ATile *>(smem_raw);
-  BTile *Bs = reinterpret_cast<BTile *>(smem_raw + 2 * sizeof(ATile));
+  T *As = reinterpret_cast<T *>(smem_raw);                      // [stage][w][BM][AROW]
+  T *Bs = As + kStages * G::A_STAGE;                            // [stage][w][BK][BROW]
 
   const int tid = threadIdx.x;
   const int tx = tid % TX, ty = tid / TX;
@@ -181,44 +211,30 @@ gemm_kernel(const GemmArgs args) {
   const long long ap = args.A.plane, bp = args.B.plane;
   const int lda = args.A.ld, ldb = args.B.ld;
 
-  T ra[W][A_PER], rb[W][B_PER];
-
-  auto gload = [&](int k0) {
+  auto load_tile = [&](int stage, int k0) {
+    T *as = As + stage * G::A_STAGE;
+    T *bs = Bs + stage * G::B_STAGE;
 #pragma unroll
     for (int i = 0; i < A_PER; ++i) {
-      int e = tid + i * kThreads;
-      int row = e / BK, col = e % BK;
-      int gr = m0 + row, gc = k0 + col;
-      bool ok = gr < M && gc < K;
-      long long off = (long long)gr * lda + gc;
+      const int e = tid + i * kThreads;
+      const int row = e / BK, col = e % BK;
+      const int gr = m0 + row, gc = k0 + col;
+      const bool ok = gr < M && gc < K;
+      const long long off = ok ? (long long)gr * lda + gc : 0;
 #pragma unroll
-      for (int w = 0; w < W; ++w) ra[w][i] = ok ? Ag[off + w * ap] : T(0);
+      for (int w = 0; w < W; ++w)
+        cp_async_zfill<sizeof(T)>(as + (w * BM + row) * G::AROW + col, Ag + off + w * ap, ok);
     }
 #pragma unroll
     for (int i = 0; i < B_PER; ++i) {
-      int e = tid + i * kThreads;
-      int row = e / BN, col = e % BN;
-      int gr = k0 + row, gc = n0 + col;
-      bool ok = gr < K && gc < N;
-      long long off = (long long)gr * ldb + gc;
+      const int e = tid + i * kThreads;
+      const int row = e / BN, col = e % BN;
+      const int gr = k0 + row, gc = n0 + col;
+      const bool ok = gr < K && gc < N;
+      const long long off = ok ? (long long)gr * ldb + gc : 0;
 #pragma unroll
-      for (int w = 0; w < W; ++w) rb[w][i] = ok ? Bg[off + w * bp] : T(0);
-    }
-  };
-  auto sstore = [&](int buf) {
-#pragma unroll
-    for (int i = 0; i < A_PER; ++i) {
-      int e = tid + i * kThreads;
-      int row = e / BK, col = e % BK;
-#pragma unroll
-      for (int w = 0; w < W; ++w) As[buf][w][col][row] = ra[w][i];
-    }
-#pragma unroll
-    for (int i = 0; i < B_PER; ++i) {
-      int e = tid + i * kThreads;
-      int row = e / BN, col = e % BN;
-#pragma unroll
-      for (int w = 0; w < W; ++w) Bs[buf][w][row][col] = rb[w][i];
+      for (int w = 0; w < W; ++w)
+        cp_async_zfill<sizeof(T)>(bs + (w * BK + row) * G::BROW + col, Bg + off + w * bp, ok);
     }
   };
 
@@ -229,21 +245,30 @@ gemm_kernel(const GemmArgs args) {
     for (int j = 0; j < TN; ++j) acc[i][j].zero();
 
   const int ktiles = (K + BK - 1) / BK;
-  gload(0);
-  sstore(0);
-  __syncthreads();
+#pragma unroll
+  for (int st = 0; st < kStages - 1; ++st) {
+    if (st < ktiles) load_tile(st, st * BK);
+    cp_async_commit();
+  }
   for (int kt = 0; kt < ktiles; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < ktiles) gload((kt + 1) * BK);
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + kStages - 1;
+      if (nk < ktiles) load_tile(nk % kStages, nk * BK);
+      cp_async_commit();
+    }
+    const T *as = As + (kt % kStages) * G::A_STAGE;
+    const T *bs = Bs + (kt % kStages) * G::B_STAGE;
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
       T a[TM][W], b[TN][W];
 #pragma unroll
       for (int w = 0; w < W; ++w) {
 #pragma unroll
-        for (int i = 0; i < TM; ++i) a[i][w] = As[buf][w][kk][ty * TM + i];
+        for (int i = 0; i < TM; ++i) a[i][w] = as[(w * BM + ty * TM + i) * G::AROW + kk];
 #pragma unroll
-        for (int j = 0; j < TN; ++j) b[j][w] = Bs[buf][w][kk][tx * TN + j];
+        for (int j = 0; j < TN; ++j) b[j][w] = bs[(w * BK + kk) * G::BROW + tx * TN + j];
       }
 #pragma unroll
       for (int i = 0; i < TM; ++i)
@@ -254,9 +279,8 @@ gemm_kernel(const GemmArgs args) {
     for (int i = 0; i < TM; ++i)
 #pragma unroll
       for (int j = 0; j < TN; ++j) acc[i][j].renorm();
-    if (kt + 1 < ktiles) sstore(buf ^ 1);
-    __syncthreads();
   }
+  cp_async_wait<0>();
 
   // ---------------------------------------------------------- epilogue
   const MatRef &C = args.C;

@@ -160,6 +160,26 @@ MP_INLINE void dd_mac(double ah, double al, double bh, double bl, double &ch, do
   cl = add(cl, add(t, e));
   ch = s;
 }
+// 9-FP64-instruction variant: the hi-word sum uses Dekker's FastTwoSum on
+// magnitude-ordered operands (exact for |big| >= |small|), the ordering done
+// with integer compares/selects on the ALU pipe; the cross terms are folded
+// into cl by FMA.  FP64 pipe: DMUL + 3 DFMA + 3 DADD + 2 DADD.
+MP_INLINE void dd_mac9(double ah, double al, double bh, double bl, double &ch, double &cl) {
+  double p = mul(ah, bh);
+  double e = fma(ah, bh, -p);
+  cl = fma(ah, bl, cl);
+  cl = fma(al, bh, cl);
+  double s = add(ch, p);
+  // |ch| >= |p| as unsigned compare of the magnitude bit patterns
+  unsigned long long mc = (unsigned long long)__double_as_longlong(ch) & 0x7fffffffffffffffULL;
+  unsigned long long mp_ = (unsigned long long)__double_as_longlong(p) & 0x7fffffffffffffffULL;
+  bool cbig = mc >= mp_;
+  double big = cbig ? ch : p;
+  double small = cbig ? p : ch;
+  double t = sub(small, sub(s, big));
+  cl = add(cl, add(t, e));
+  ch = s;
+}
 MP_INLINE void dd_acc_renorm(double &ch, double &cl) {
   double s, e;
   two_sum(ch, cl, s, e);
