@@ -143,6 +143,45 @@ int mpps_horner_scalar_top(mpps_handle *h, const double *bm_words, int fmt_top,
                            mpps_mat *out, const int *sel, int nsel,
                            const int *exp_out);
 
+/* ------------------------------------------------------------------
+ * Tensor-core path (INT8 tcgen05 MMA, exact operand splitting).
+ * A multiword operand is split into signed 8-bit digit planes with one
+ * power-of-two scale per row (side 0, the left operand) or per column
+ * (side 1, the right operand, stored transposed); C = A B is then a sum of
+ * exact int32 tensor-core products recombined in the target format.
+ * Slices used per format: fp64 8, dd 16, qd 31 (first digits of a finer
+ * split are a valid coarser split, so one slicing serves every level).
+ */
+typedef struct {
+  void *digits;      /* device int8 [nslices][batch][rpad][kpad]            */
+  int *exps;         /* device int32 [batch][rpad] (row/column exponents)   */
+  int nslices, batch;
+  int rpad;          /* padded rows (side 0) / columns (side 1), % 128 == 0 */
+  int kpad;          /* padded inner dimension, % 32 == 0                   */
+} mpps_slices;
+
+/* Split src (side 0: by rows, side 1: by columns) into out->nslices digit
+ * planes (padding written as zero). */
+int mpps_slice(mpps_handle *h, const mpps_mat *src, int side, mpps_slices *out,
+               const int *sel, int nsel);
+
+/* mat_mul (precision.py:160-184) on the tensor cores: C (M x N, format of C)
+ * = A (sliced by rows) * B (sliced by columns), using nslices digit planes. */
+int mpps_gemm_sliced(mpps_handle *h, const mpps_slices *A, const mpps_slices *B,
+                     int nslices, int M, int N, int K, mpps_mat *C,
+                     const int *sel, int nsel);
+
+/* horner_mixed level (engine.py:249-251) on the tensor cores; same epilogue
+ * as mpps_horner_step. */
+int mpps_horner_step_sliced(mpps_handle *h, const mpps_slices *Y,
+                            const mpps_slices *phi, int nslices,
+                            const mpps_mat *Bprev, mpps_mat *out,
+                            const int *sel, int nsel, const int *exp_y,
+                            const int *exp_in, const int *exp_out);
+
+/* Digit planes the tensor-core path uses for a format (-1: not supported). */
+int mpps_oz_slices_for(int fmt);
+
 /* Diagnostic: pipe-peak probe used by bench.py for the per-precision
  * roofline denominators (not a reference operator).  Launches `blocks`
  * CTAs x 256 threads, each running 8 independent FMA chains of `iters`

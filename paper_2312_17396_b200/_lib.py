@@ -26,8 +26,39 @@ EXPORTED = (
     "mpps_last_error", "mpps_launch_count", "mpps_convert", "mpps_gemm",
     "mpps_axpy", "mpps_powers", "mpps_assemble_blocks", "mpps_one_norm",
     "mpps_horner_step", "mpps_horner_scalar_top", "mpps_probe_fma",
-    "mpps_assemble_blocks_dist", "mpps_colmax",
+    "mpps_assemble_blocks_dist", "mpps_colmax", "mpps_slice", "mpps_gemm_sliced",
+    "mpps_horner_step_sliced", "mpps_oz_slices_for",
 )
+
+
+class CSlices(ctypes.Structure):
+    _fields_ = [
+        ("digits", ctypes.c_void_p),
+        ("exps", ctypes.c_void_p),
+        ("nslices", ctypes.c_int),
+        ("batch", ctypes.c_int),
+        ("rpad", ctypes.c_int),
+        ("kpad", ctypes.c_int),
+    ]
+
+
+class Slices:
+    """Digit planes of one operand for the tensor-core path (torch buffers):
+    digits int8 (S, batch, rpad, kpad), exps int32 (batch, rpad)."""
+
+    __slots__ = ("digits", "exps", "S", "rows", "k")
+
+    def __init__(self, S: int, batch: int, rows: int, k: int, device):
+        import torch
+        rpad = -(-rows // 128) * 128
+        kpad = -(-k // 32) * 32
+        self.digits = torch.empty((S, batch, rpad, kpad), dtype=torch.int8, device=device)
+        self.exps = torch.empty((batch, rpad), dtype=torch.int32, device=device)
+        self.S, self.rows, self.k = S, rows, k
+
+    def c(self) -> CSlices:
+        d = self.digits
+        return CSlices(d.data_ptr(), self.exps.data_ptr(), d.shape[0], d.shape[1], d.shape[2], d.shape[3])
 
 
 class CMat(ctypes.Structure):
@@ -90,6 +121,11 @@ def load_library(path: Optional[str] = None):
         lib.mpps_probe_fma.argtypes = [vp, ip, ip, ip, vp]
         lib.mpps_assemble_blocks_dist.argtypes = [vp, mp, ip, ip, vp, mp, vp, ip, ip]
         lib.mpps_colmax.argtypes = [vp, vp, ip, ip, ip, vp]
+        sp = P(CSlices)
+        lib.mpps_slice.argtypes = [vp, mp, ip, sp, vp, ip]
+        lib.mpps_gemm_sliced.argtypes = [vp, sp, sp, ip, ip, ip, ip, mp, vp, ip]
+        lib.mpps_horner_step_sliced.argtypes = [vp, sp, sp, ip, mp, mp, vp, ip, vp, vp, vp]
+        lib.mpps_oz_slices_for.argtypes = [ip]
         for name in EXPORTED:
             getattr(lib, name).restype = getattr(lib, name).restype or ip
         if path is None:
@@ -203,6 +239,40 @@ class Handle:
     def colmax(self, colsums_dev, nvec: int, cols: int, batch: int, out_dev):
         self._check(self.lib.mpps_colmax(self.h, colsums_dev.data_ptr(), nvec, cols, batch, out_dev.data_ptr()),
                     "colmax")
+
+    # --- tensor-core path -------------------------------------------
+    def slices_for(self, fmt: int) -> int:
+        return int(self.lib.mpps_oz_slices_for(fmt))
+
+    def slice(self, src: MatBatch, side: int, S: int, sel=None) -> "Slices":
+        """side 0: split rows (left operand); side 1: split columns (right)."""
+        rows, k = (src.rows, src.cols) if side == 0 else (src.cols, src.rows)
+        out = Slices(S, src.batch, rows, k, src.device)
+        c_src, c_out = cmat(src), out.c()
+        nsel = 0 if sel is None else sel.numel()
+        self._check(self.lib.mpps_slice(self.h, ctypes.byref(c_src), side, ctypes.byref(c_out), _ptr(sel), nsel),
+                    "slice")
+        return out
+
+    def gemm_sliced(self, A: "Slices", B: "Slices", S: int, C: MatBatch, sel=None):
+        a, b, c = A.c(), B.c(), cmat(C)
+        nsel = 0 if sel is None else sel.numel()
+        end = self._ev(("gemm_tc", C.fmt, C.fmt, A.rows, B.rows, A.k, nsel or C.batch))
+        self._check(self.lib.mpps_gemm_sliced(self.h, ctypes.byref(a), ctypes.byref(b), S, A.rows, B.rows, A.k,
+                                              ctypes.byref(c), _ptr(sel), nsel), "mat_mul(tc)")
+        if end is not None:
+            end.record()
+
+    def horner_step_sliced(self, Y: "Slices", phi: "Slices", S: int, Bprev, out, sel=None, exp_y=None,
+                           exp_in=None, exp_out=None, fmt_in: int = 31):
+        y, p, b, o = Y.c(), phi.c(), cmat(Bprev), cmat(out)
+        nsel = 0 if sel is None else sel.numel()
+        end = self._ev(("horner_tc", fmt_in, out.fmt, Y.rows, phi.rows, Y.k, nsel or out.batch))
+        self._check(self.lib.mpps_horner_step_sliced(self.h, ctypes.byref(y), ctypes.byref(p), S, ctypes.byref(b),
+                                                     ctypes.byref(o), _ptr(sel), nsel, _ptr(exp_y), _ptr(exp_in),
+                                                     _ptr(exp_out)), "horner_step(tc)")
+        if end is not None:
+            end.record()
 
     def one_norm(self, A: MatBatch, norms_dev):
         a = cmat(A)

@@ -16,6 +16,7 @@
 
 #include "../../include/mpps_b200.h"
 #include "gemm.cuh"
+#include "ozaki.cuh"
 
 using namespace mpps;
 
@@ -673,5 +674,114 @@ int mpps_probe_fma(mpps_handle *h, int fmt, int blocks, int iters, void *scratch
     return set_err(h, MPPS_EFMT, "probe: fp32 or fp64 only");
   return after_launch(h, "fma_probe_kernel");
 }
+
+}  // extern "C"
+
+// ------------------------------------------------ tensor-core (Ozaki) path
+static int oz_slices_for(int fi) { return fi == QD ? 31 : fi == DD ? 16 : fi == F64 ? 8 : -1; }
+
+static oz::SliceRef sref(const mpps_slices *s) {
+  oz::SliceRef r;
+  r.digits = (int8_t *)s->digits; r.exps = s->exps; r.S = s->nslices; r.batch = s->batch;
+  r.rpad = s->rpad; r.kpad = s->kpad;
+  return r;
+}
+
+extern "C" int mpps_slice(mpps_handle *h, const mpps_mat *src, int side, mpps_slices *out, const int *sel, int nsel) {
+  int rc = check_mat(h, src, "slice.src");
+  if (rc) return rc;
+  if (!out || !out->digits || !out->exps) return set_err(h, MPPS_EINVAL, "slice: null output");
+  if (out->nslices < 1 || out->nslices > 31) return set_err(h, MPPS_EINVAL, "slice: 1..31 slices");
+  const int rows = side == 0 ? src->rows : src->cols;   // rows of the slice arrays
+  const int ks = side == 0 ? src->cols : src->rows;
+  if (out->rpad < rows || out->rpad % oz::kTileM || out->kpad < ks || out->kpad % oz::kKStep)
+    return set_err(h, MPPS_EINVAL, "slice: padding %dx%d too small or unaligned for %dx%d", out->rpad, out->kpad, rows, ks);
+  const int nb = sel ? nsel : src->batch;
+  if (!sel && out->batch != src->batch) return set_err(h, MPPS_EINVAL, "slice: batch mismatch");
+  if (nb == 0) return MPPS_OK;
+  oz::SliceRef o = sref(out);
+  const int fi = fmt_index(src->fmt);
+  if (side == 0) {
+    dim3 grid((out->rpad * 32 + 255) / 256, nb);
+    oz::slice_rows_kernel<<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel);
+    return after_launch(h, "slice_rows_kernel");
+  }
+  oz::col_exps_kernel<<<dim3((out->rpad + 127) / 128, nb), 128, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel);
+  rc = after_launch(h, "col_exps_kernel");
+  if (rc) return rc;
+  dim3 grid(out->rpad / 32, out->kpad / 32, nb);
+  oz::slice_cols_kernel<31><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel);
+  return after_launch(h, "slice_cols_kernel");
+}
+
+template <int S, int NT, int FO, int MODE>
+static int launch_oz(mpps_handle *h, const oz::OzArgs &a, int nb) {
+  constexpr size_t smem = oz::oz_smem_bytes<S, NT>();
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_kernel<S, NT, FO, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz attr: %s", cudaGetErrorString(e));
+    configured = true;
+  }
+  dim3 grid((a.N + NT - 1) / NT, (a.M + oz::kTileM - 1) / oz::kTileM, nb);
+  if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
+  oz::oz_gemm_kernel<S, NT, FO, MODE><<<grid, oz::kThreadsOz, smem, h->stream>>>(a);
+  return after_launch(h, "oz_gemm_kernel");
+}
+
+static int dispatch_oz(mpps_handle *h, int S, int fo, int mode, const oz::OzArgs &a, int nb) {
+#define OZ(SS, NT, FF, MM) if (S == SS && fo == FF && mode == MM) return launch_oz<SS, NT, FF, MM>(h, a, nb);
+  OZ(8, 32, F64, 0) OZ(8, 32, F64, 1) OZ(8, 32, DD, 1) OZ(8, 32, QD, 1)
+  OZ(16, 32, DD, 0) OZ(16, 32, DD, 1) OZ(16, 32, QD, 1)
+  OZ(31, 16, QD, 0) OZ(31, 16, QD, 1)
+#undef OZ
+  return set_err(h, MPPS_EFMT, "tensor-core GEMM: no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
+}
+
+static int check_sliced(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, int S, int M, int N, int K) {
+  if (!A || !B) return set_err(h, MPPS_EINVAL, "sliced gemm: null slices");
+  if (S > A->nslices || S > B->nslices) return set_err(h, MPPS_EINVAL, "sliced gemm: %d slices requested, %d/%d stored", S, A->nslices, B->nslices);
+  if (A->kpad != B->kpad || A->kpad < K) return set_err(h, MPPS_EINVAL, "sliced gemm: K padding mismatch");
+  if (A->rpad < M || B->rpad < N) return set_err(h, MPPS_EINVAL, "sliced gemm: row padding too small");
+  // int32 diagonal accumulators: |D| <= min(S,...) * 65^2 * K must stay below 2^31
+  if ((double)S * 4225.0 * (double)K >= 2147483648.0)
+    return set_err(h, MPPS_EINVAL, "sliced gemm: K=%d too large for exact int32 accumulation", K);
+  return MPPS_OK;
+}
+
+extern "C" {
+
+int mpps_gemm_sliced(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, int nslices, int M, int N, int K,
+                     mpps_mat *C, const int *sel, int nsel) {
+  int rc = check_mat(h, C, "gemm_sliced.C");
+  if (rc || (rc = check_sliced(h, A, B, nslices, M, N, K))) return rc;
+  if (C->rows != M || C->cols != N) return set_err(h, MPPS_EINVAL, "mat_mul: output shape");
+  oz::OzArgs a;
+  memset(&a, 0, sizeof(a));
+  a.A = sref(A); a.B = sref(B); a.M = M; a.N = N; a.K = K; a.S = nslices;
+  a.C = ref_of(C); a.sel = sel;
+  int nb = sel ? nsel : C->batch;
+  return dispatch_oz(h, nslices, fmt_index(C->fmt), 0, a, nb);
+}
+
+int mpps_horner_step_sliced(mpps_handle *h, const mpps_slices *Y, const mpps_slices *phi, int nslices,
+                            const mpps_mat *Bprev, mpps_mat *out, const int *sel, int nsel, const int *exp_y,
+                            const int *exp_in, const int *exp_out) {
+  int rc;
+  if ((rc = check_mat(h, Bprev, "horner_sliced.Bprev")) || (rc = check_mat(h, out, "horner_sliced.out"))) return rc;
+  const int M = out->rows, N = out->cols, K = Y ? Y->kpad : 0;
+  if ((rc = check_sliced(h, Y, phi, nslices, M, N, 0))) return rc;
+  if (Bprev->rows != M || Bprev->cols != N) return set_err(h, MPPS_EINVAL, "horner: operands must match the output");
+  oz::OzArgs a;
+  memset(&a, 0, sizeof(a));
+  a.A = sref(Y); a.B = sref(phi); a.M = M; a.N = N; a.K = K; a.S = nslices;
+  a.C = ref_of(out); a.sel = sel;
+  a.epi.Bprev = ref_of(Bprev); a.epi.exp_y = exp_y; a.epi.exp_in = exp_in; a.epi.exp_out = exp_out;
+  int nb = sel ? nsel : out->batch;
+  return dispatch_oz(h, nslices, fmt_index(out->fmt), 1, a, nb);
+}
+
+int mpps_oz_slices_for(int fmt) { return oz_slices_for(fmt_index(fmt)); }
 
 }  // extern "C"

@@ -1,0 +1,416 @@
+// Multiword GEMMs on the INT8 tensor cores (tcgen05.mma kind::i8) by exact
+// operand splitting (Ozaki scheme I).
+//
+//   A (rows scaled by 2^-ea_i) = sum_{s<S} a_s 2^-(6+7s),   a_s int8 in [-65, 65]
+//   B (cols scaled by 2^-eb_j) = sum_{t<S} b_t 2^-(6+7t)
+//   A B = 2^(ea_i+eb_j) sum_{d<S} 2^-(12+7d) D_d,   D_d = sum_{s+t=d} a_s b_t
+//
+// Every D_d is an exact int32 accumulation over K on the tensor cores (one
+// TMEM accumulator per diagonal d, all (s,t) pairs of the diagonal issued into
+// it); pairs with s+t >= S are dropped (their weight is below 2^-(12+7S),
+// i.e. below the target format's unit roundoff for S = 8 / 16 / 31 slices
+// -> fp64 / dd / qd).  The epilogue recombines the diagonals exactly (groups
+// of three fit a double), sums them in the target format, applies the
+// power-of-two row/column scales and then the same store / fused Horner
+// epilogue as the SIMT GEMM (gemm.cuh).
+//
+// Slices are stored K-major ([S][batch][rows_pad][K_pad] int8, rows_pad a
+// multiple of the tile, K_pad of 32, padding zero), B transposed (its columns
+// are the rows of the slice arrays).  Shared-memory operand tiles use the
+// canonical no-swizzle K-major UMMA layout: 8-row x 16-byte core matrices,
+// LBO = 128 B between the two 16-byte K chunks of one MMA-K step, SBO = 256 B
+// between 8-row groups.
+#pragma once
+#include "gemm.cuh"
+
+namespace mpps {
+namespace oz {
+
+constexpr int kTileM = 128;
+constexpr int kKStep = 32;      // int8 MMA K per instruction (32 bytes)
+constexpr int kThreadsOz = 128;
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+  return d;                // base offset 0, layout SWIZZLE_NONE (0)
+}
+
+// kind::i8 instruction descriptor: D s32, A/B signed int8, K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(mbar)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mbar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(mbar), "r"(phase)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+template <int NCOLS>
+__device__ __forceinline__ void tmem_alloc(uint32_t dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(dst_smem), "n"(NCOLS)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+template <int NCOLS>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "n"(NCOLS) : "memory");
+}
+
+// 8 consecutive 32-bit columns of this thread's TMEM lane.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t (&v)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, int32_t (&v)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+__device__ __forceinline__ void cp16(uint32_t dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+}
+
+__host__ __device__ constexpr int tmem_cols_for(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
+
+// ------------------------------------------------------------- slicing
+struct SliceRef {
+  int8_t *digits;   // [S][batch][rpad][kpad]
+  int *exps;        // [batch][rpad]
+  int S, batch, rpad, kpad;
+  __host__ __device__ long long plane() const { return (long long)batch * rpad * kpad; }
+};
+
+// Split one exact value (qd words, |v| < 1 after scaling) into S signed
+// digits: first 6 bits, then 7 bits each; the residual is kept exactly
+// (scaling by 2^k and subtracting the nearest integer are exact).
+__device__ __forceinline__ void split_digits(mp::qd v, int S, int8_t *out, long long stride) {
+  double x0 = v.x[0], x1 = v.x[1], x2 = v.x[2], x3 = v.x[3];
+  double sc = 64.0;
+  for (int s = 0; s < S; ++s) {
+    x0 *= sc; x1 *= sc; x2 *= sc; x3 *= sc;
+    double d = rint(x0);
+    double r = x0 - d;  // exact
+    // renormalise (r, x1, x2, x3) exactly
+    double s0, e0, s1, e1, s2, e2;
+    mp::two_sum(r, x1, s0, e0);
+    mp::two_sum(e0, x2, s1, e1);
+    mp::two_sum(e1, x3, s2, e2);
+    x0 = s0; x1 = s1; x2 = s2; x3 = e2;
+    out[s * stride] = (int8_t)(int)d;
+    sc = 128.0;
+  }
+}
+
+// Side A: rows scaled by their own max exponent; output [S][b][i][k].
+// One warp per row.
+__global__ void slice_rows_kernel(MatRef A, int rows, int cols, int fi, SliceRef out, const int *sel) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int bz = blockIdx.y;
+  const int b = sel ? sel[bz] : bz;
+  const int i = warp;
+  if (i >= out.rpad) return;
+  const long long base = (long long)b * A.bstride + (long long)i * A.ld;
+  double mx = 0.0;
+  if (i < rows)
+    for (int k = lane; k < cols; k += 32) {
+      double v = fi == F32 ? (double)((const float *)A.data)[base + k] : ((const double *)A.data)[base + k];
+      mx = fmax(mx, fabs(v));
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  int e = 0;
+  if (mx > 0.0) {
+    frexp(mx, &e);  // mx in [2^(e-1), 2^e)
+    // |value| <= mx (1 + 2^-52) < 2^e unless mx is the largest double below
+    // 2^e; one extra bit of headroom covers that corner.
+    if (ldexp(mx, -e) > 0.9999999999) e += 1;
+  }
+  if (lane == 0) out.exps[(long long)b * out.rpad + i] = e;
+  const long long plane = out.plane();
+  int8_t *o = out.digits + ((long long)b * out.rpad + i) * out.kpad;
+  for (int k = lane; k < out.kpad; k += 32) {
+    mp::qd v = mp::qd_make(0.0, 0.0, 0.0, 0.0);
+    if (i < rows && k < cols) {
+      v = fi == F32 ? mp::qd_from_d((double)((const float *)A.data)[base + k]) : load_qd(A, base + k);
+      v = mp::qd_ldexp(v, -e);
+    }
+    split_digits(v, out.S, o + k, plane);
+  }
+}
+
+// Side B: column exponents first (one thread per column, coalesced rows).
+__global__ void col_exps_kernel(MatRef B, int rows, int cols, int fi, SliceRef out, const int *sel) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int bz = blockIdx.y;
+  const int b = sel ? sel[bz] : bz;
+  if (j >= out.rpad) return;
+  double mx = 0.0;
+  if (j < cols)
+    for (int k = 0; k < rows; ++k) {
+      const long long off = (long long)b * B.bstride + (long long)k * B.ld + j;
+      double v = fi == F32 ? (double)((const float *)B.data)[off] : ((const double *)B.data)[off];
+      mx = fmax(mx, fabs(v));
+    }
+  int e = 0;
+  if (mx > 0.0) {
+    frexp(mx, &e);
+    if (ldexp(mx, -e) > 0.9999999999) e += 1;
+  }
+  out.exps[(long long)b * out.rpad + j] = e;
+}
+
+// Side B digits, transposed through shared memory: tile of 32 k x 32 j.
+template <int SMAX>
+__global__ void slice_cols_kernel(MatRef B, int rows, int cols, int fi, SliceRef out, const int *sel) {
+  __shared__ int8_t tile[SMAX][32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+  const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  const int bz = blockIdx.z;
+  const int b = sel ? sel[bz] : bz;
+  const int S = out.S;
+  for (int kk = ty; kk < 32; kk += 8) {
+    const int k = k0 + kk, j = j0 + tx;
+    mp::qd v = mp::qd_make(0.0, 0.0, 0.0, 0.0);
+    if (k < rows && j < cols) {
+      const long long off = (long long)b * B.bstride + (long long)k * B.ld + j;
+      v = fi == F32 ? mp::qd_from_d((double)((const float *)B.data)[off]) : load_qd(B, off);
+      v = mp::qd_ldexp(v, -out.exps[(long long)b * out.rpad + j]);
+    }
+    int8_t dg[SMAX];
+    split_digits(v, S, dg, 1);
+    for (int s = 0; s < S; ++s) tile[s][tx][kk] = dg[s];
+  }
+  __syncthreads();
+  const long long plane = out.plane();
+  for (int jj = ty; jj < 32; jj += 8) {
+    const int j = j0 + jj, k = k0 + tx;
+    if (j < out.rpad && k < out.kpad)
+      for (int s = 0; s < S; ++s)
+        out.digits[s * plane + ((long long)b * out.rpad + j) * out.kpad + k] = tile[s][jj][tx];
+  }
+}
+
+// -------------------------------------------------------------- GEMM
+struct OzArgs {
+  SliceRef A, B;   // A: rows = M (row-scaled); B: rows = N (transposed B, col-scaled)
+  int M, N, K;     // logical sizes
+  int S;           // slices used (<= A.S, B.S)
+  MatRef C;
+  const int *sel;
+  HornerEpi epi;
+};
+
+// Smem per stage: S slices of A (128 x 32 B) + S slices of B (NT x 32 B).
+template <int S, int NT>
+__host__ __device__ constexpr size_t oz_stage_bytes() { return (size_t)S * (kTileM + NT) * kKStep; }
+template <int S, int NT>
+__host__ __device__ constexpr int oz_stages() { return 2 * oz_stage_bytes<S, NT>() + 1024 <= 200 * 1024 ? 2 : 1; }
+template <int S, int NT>
+__host__ __device__ constexpr size_t oz_smem_bytes() { return oz_stages<S, NT>() * oz_stage_bytes<S, NT>() + 256; }
+
+// value of sum_d D_d 2^-(12+7d) as a qd (exact grouping in threes)
+template <int S>
+__device__ __forceinline__ mp::qd combine_diagonals(const int32_t *D) {
+  mp::qd acc = mp::qd_make(0.0, 0.0, 0.0, 0.0);
+  mp::dd accd = mp::dd_make(0.0, 0.0);
+#pragma unroll
+  for (int g = 0; g < (S + 2) / 3; ++g) {
+    const int d0 = 3 * g;
+    long long G = (long long)D[d0] << 14;
+    if (d0 + 1 < S) G += (long long)D[d0 + 1] << 7;
+    if (d0 + 2 < S) G += (long long)D[d0 + 2];
+    double gv = ldexp((double)G, -(12 + 7 * (d0 + 2)));  // exact
+    if constexpr (S > 16) acc = mp::qd_add(acc, mp::qd_from_d(gv));
+    else accd = mp::dd_add_d(accd, gv);
+  }
+  if constexpr (S > 16) return acc;
+  else return mp::qd_from_dd(accd);
+}
+
+template <int S, int NT, int FO, int MODE>
+__global__ void __launch_bounds__(kThreadsOz, 1) oz_gemm_kernel(const OzArgs args) {
+  constexpr int STAGES = oz_stages<S, NT>();
+  constexpr size_t STAGE = oz_stage_bytes<S, NT>();
+  constexpr int A_SLICE = kTileM * kKStep;   // bytes per A slice block
+  constexpr int B_SLICE = NT * kKStep;
+  constexpr int TCOLS = tmem_cols_for(S * NT);
+  constexpr uint32_t IDESC = idesc_i8(kTileM, NT);
+
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t *stage_base = smem;
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + STAGES * STAGE + 64);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int bz = blockIdx.z;
+  const int b = args.sel ? args.sel[bz] : bz;
+  const int m0 = blockIdx.y * kTileM, n0 = blockIdx.x * NT;
+  const int ksteps = args.A.kpad / kKStep;
+
+  if (warp == 0) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&mbar[s]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const long long aplane = args.A.plane(), bplane = args.B.plane();
+  const int8_t *Ab = args.A.digits + ((long long)b * args.A.rpad + m0) * args.A.kpad;
+  const int8_t *Bb = args.B.digits + ((long long)b * args.B.rpad + n0) * args.B.kpad;
+
+  auto load_stage = [&](int st, int kb) {
+    const uint32_t sa = smem_u32(stage_base + st * STAGE);
+    const uint32_t sb = sa + S * A_SLICE;
+    const int k0 = kb * kKStep;
+    // A: S slices x 128 rows x 2 chunks
+    for (int c = tid; c < S * kTileM * 2; c += kThreadsOz) {
+      const int s = c / (kTileM * 2), rem = c % (kTileM * 2);
+      const int row = rem >> 1, kc = rem & 1;
+      const uint32_t dst = sa + s * A_SLICE + (((row >> 3) * 2 + kc) << 7) + ((row & 7) << 4);
+      cp16(dst, Ab + s * aplane + (long long)row * args.A.kpad + k0 + kc * 16);
+    }
+    for (int c = tid; c < S * NT * 2; c += kThreadsOz) {
+      const int s = c / (NT * 2), rem = c % (NT * 2);
+      const int row = rem >> 1, kc = rem & 1;
+      const uint32_t dst = sb + s * B_SLICE + (((row >> 3) * 2 + kc) << 7) + ((row & 7) << 4);
+      cp16(dst, Bb + s * bplane + (long long)row * args.B.kpad + k0 + kc * 16);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+
+  uint32_t phase[2] = {0u, 0u};
+  load_stage(0, 0);
+  for (int kb = 0; kb < ksteps; ++kb) {
+    const int st = (STAGES == 2) ? (kb & 1) : 0;
+    if (STAGES == 2 && kb + 1 < ksteps) {
+      const int nst = st ^ 1;
+      if (kb >= 1) {  // stage nst was read by the MMAs of step kb-1
+        mbar_wait(smem_u32(&mbar[nst]), phase[nst]);
+        phase[nst] ^= 1u;
+      }
+      load_stage(nst, kb + 1);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      fence_after();
+      const uint32_t sa = smem_u32(stage_base + st * STAGE);
+      const uint32_t sb = sa + S * A_SLICE;
+#pragma unroll 1
+      for (int s = 0; s < S; ++s) {
+        const uint64_t ad = umma_desc(sa + s * A_SLICE, 128, 256);
+        for (int t = 0; t < S - s; ++t) {
+          const uint64_t bd = umma_desc(sb + t * B_SLICE, 128, 256);
+          mma_i8(tmem + (uint32_t)((s + t) * NT), ad, bd, IDESC, (kb > 0 || s > 0) ? 1u : 0u);
+        }
+      }
+      mma_commit(smem_u32(&mbar[st]));
+    }
+    if (STAGES == 1) {
+      mbar_wait(smem_u32(&mbar[0]), phase[0]);
+      phase[0] ^= 1u;
+      if (kb + 1 < ksteps) load_stage(0, kb + 1);
+    }
+  }
+  if (STAGES == 2) {
+    const int last = (ksteps - 1) & 1;
+    mbar_wait(smem_u32(&mbar[last]), phase[last]);
+  }
+  fence_after();
+
+  // ---------------------------------------------------------- epilogue
+  const int row = m0 + warp * 32 + lane;  // TMEM lane == tile row
+  const int ea = args.A.exps[(long long)b * args.A.rpad + m0 + warp * 32 + lane];
+  const MatRef &C = args.C;
+  int ey = 0, ei = 0, eo = 0;
+  if constexpr (MODE == 1) {
+    if (args.epi.exp_y) ey = args.epi.exp_y[b];
+    if (args.epi.exp_in) ei = args.epi.exp_in[b];
+    if (args.epi.exp_out) eo = args.epi.exp_out[b];
+  }
+  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+  constexpr int CW = (S > 16) ? 4 : 8;
+  for (int c0 = 0; c0 < NT; c0 += CW) {
+    int32_t D[S][CW];
+#pragma unroll
+    for (int d = 0; d < S; ++d) {
+      if constexpr (CW == 8) tmem_ld8(lane_base + (uint32_t)(d * NT + c0), D[d]);
+      else tmem_ld4(lane_base + (uint32_t)(d * NT + c0), D[d]);
+    }
+    tmem_ld_wait();
+#pragma unroll
+    for (int jj = 0; jj < CW; ++jj) {
+      const int col = n0 + c0 + jj;
+      if (row >= args.M || col >= args.N) continue;
+      int32_t Dj[S];
+#pragma unroll
+      for (int d = 0; d < S; ++d) Dj[d] = D[d][jj];
+      mp::qd v = combine_diagonals<S>(Dj);
+      const int eb = args.B.exps[(long long)b * args.B.rpad + col];
+      v = mp::qd_ldexp(v, ea + eb);
+      const long long off = (long long)b * C.bstride + (long long)row * C.ld + col;
+      if constexpr (MODE == 0) {
+        store_fmt<FO>(C, off, v, 0);
+      } else {
+        const int sh = -(ey + ei);
+        if (sh) v = mp::qd_ldexp(v, sh);
+        mp::qd bv = load_qd(args.epi.Bprev, (long long)b * args.epi.Bprev.bstride + (long long)row * args.epi.Bprev.ld + col);
+        store_fmt<FO>(C, off, horner_add<FO>(bv, v), eo);
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<TCOLS>(tmem);
+}
+
+}  // namespace oz
+}  // namespace mpps

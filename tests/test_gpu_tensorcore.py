@@ -1,0 +1,70 @@
+"""Tensor-core (INT8 tcgen05) multiword GEMM by exact operand splitting vs
+the SIMT error-free-transform GEMM and the MPFR oracle: same normwise
+accuracy class (c n u |A||B|), for fp64 (8 digit planes), dd (16), qd (31);
+square, ragged and rectangular shapes, batched."""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _words_of(fmt, A, rng):
+    if fmt == 15:
+        return A[None]
+    lo = A * 2.0 ** -60 * rng.standard_normal(A.shape)
+    w = [A, lo]
+    if fmt == 63:
+        w += [lo * 2.0 ** -60, lo * 2.0 ** -121]
+    return np.stack(w)
+
+
+@pytest.mark.parametrize("fmt,bits", [(15, 53), (31, 106), (63, 212)])
+@pytest.mark.parametrize("shape", [(64, 64, 64), (70, 45, 33), (256, 256, 256), (130, 96, 300)])
+def test_tc_gemm_vs_oracle(cuda, oracle_lib, fmt, bits, shape):
+    import torch
+    from paper_2312_17396_b200 import _lib, ops
+    M, N, K = shape
+    rng = np.random.default_rng(M + N + K + fmt)
+    A = rng.standard_normal((M, K)) * np.exp(rng.uniform(-3, 3, (M, 1)))
+    B = rng.standard_normal((K, N)) * np.exp(rng.uniform(-3, 3, (1, N)))
+    Aw, Bw = _words_of(fmt, A, rng), _words_of(fmt, B, rng)
+    h = _lib.handle_for()
+    Ad, Bd = ops.from_numpy(Aw, fmt), ops.from_numpy(Bw, fmt)
+    S = h.slices_for(fmt)
+    sa, sb = h.slice(Ad, 0, S), h.slice(Bd, 1, S)
+    from paper_2312_17396_b200.precision import MatBatch
+    C = MatBatch.empty(fmt, 1, M, N, device=cuda)
+    h.gemm_sliced(sa, sb, S, C)
+    got = C.data[:, 0].cpu().numpy()
+    # oracle on the square embedding (orc_matmul is square)
+    n = max(M, N, K)
+    Ap = np.zeros((Aw.shape[0], n, n)); Ap[:, :M, :K] = Aw
+    Bp = np.zeros((Bw.shape[0], n, n)); Bp[:, :K, :N] = Bw
+    Co = oracle_lib.matmul(Ap, Bp, bits)[:, :M, :N]
+    absAB = np.abs(A) @ np.abs(B)
+    u = Fraction(1, 2 ** bits)
+    for _ in range(200):
+        i, j = rng.integers(0, M), rng.integers(0, N)
+        g = sum(Fraction(float(x)) for x in got[:, i, j])
+        o = sum(Fraction(float(x)) for x in Co[:, i, j])
+        assert abs(g - o) <= 4 * K * u * Fraction(float(absAB[i, j])), (i, j, float(g - o), float(absAB[i, j]))
+
+
+def test_tc_gemm_batched_matches_simt(cuda):
+    import torch
+    from paper_2312_17396_b200 import _lib
+    from paper_2312_17396_b200.precision import MatBatch
+    h = _lib.handle_for()
+    B, n = 8, 200
+    X = MatBatch.empty(31, B, n, device=cuda)
+    X.data[0].normal_()
+    X.data[1] = X.data[0] * 2.0 ** -55
+    C1 = MatBatch.empty(31, B, n, device=cuda)
+    C2 = MatBatch.empty(31, B, n, device=cuda)
+    h.gemm(X, X, C1)
+    h.gemm_sliced(h.slice(X, 0, 16), h.slice(X, 1, 16), 16, C2)
+    d = (C1.data[0] - C2.data[0]) + (C1.data[1] - C2.data[1])
+    scale = X.data[0].abs() @ X.data[0].abs()
+    assert (d.abs() <= 8 * n * 2.0 ** -106 * scale).all()
