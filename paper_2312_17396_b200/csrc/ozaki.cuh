@@ -344,12 +344,22 @@ __global__ void __launch_bounds__(kThreadsOz, 1) oz_gemm_kernel(const OzArgs arg
       fence_after();
       const uint32_t sa = smem_u32(stage_base + st * STAGE);
       const uint32_t sb = sa + S * A_SLICE;
+      // A_s times the concatenated B slices [B_0 .. B_{S-1-s}] (stacked along
+      // N in smem, 8-row groups every 256 B) lands in the adjacent diagonal
+      // accumulators d = s .. S-1 (column offset s*NT): one wide MMA (split
+      // at the 256-column instruction limit) instead of S-s narrow ones.
 #pragma unroll 1
       for (int s = 0; s < S; ++s) {
         const uint64_t ad = umma_desc(sa + s * A_SLICE, 128, 256);
-        for (int t = 0; t < S - s; ++t) {
-          const uint64_t bd = umma_desc(sb + t * B_SLICE, 128, 256);
-          mma_i8(tmem + (uint32_t)((s + t) * NT), ad, bd, IDESC, (kb > 0 || s > 0) ? 1u : 0u);
+        int ncols = (S - s) * NT;
+        int t0 = 0;
+        while (ncols > 0) {
+          const int nn = ncols > 256 ? 256 : ncols;
+          const uint64_t bd = umma_desc(sb + t0 * B_SLICE, 128, 256);
+          const uint32_t idesc = idesc_i8(kTileM, nn);
+          mma_i8(tmem + (uint32_t)((s + t0) * NT), ad, bd, idesc, (kb > 0 || s > 0) ? 1u : 0u);
+          t0 += nn / NT;
+          ncols -= nn;
         }
       }
       mma_commit(smem_u32(&mbar[st]));

@@ -39,6 +39,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _lib
+from . import gemm_engine as ge
 from .bigfloat import MPF, exp_rn, fmt7, ln_rn, rn, to_fraction
 from .bounds import BoundInputs, thm21_bound, tau_sequence
 from .coefficients import (CoefficientSeries, coeff_words, eval_coeff,
@@ -279,8 +280,10 @@ def _form_powers(h, Xt, wf: int, s: int, timer: _Buckets, x_is_working: Optional
             h.convert(x_is_working, powers[0])
     else:
         h.convert(MatBatch(Xt.unsqueeze(0), FP64), powers[0])
-    for k in range(1, s):           # X^{k+1} = X^k X   (engine.py:151-153)
-        h.gemm(powers[k - 1], powers[0], powers[k])
+    if s > 1:
+        Xr = ge.prepare(h, powers[0], 1, wf)          # X: right operand of every step
+        for k in range(1, s):       # X^{k+1} = X^k X   (engine.py:151-153)
+            ge.gemm(h, ge.prepare(h, powers[k - 1], 0, wf), Xr, powers[k])
     timer.stop()
     return powers
 
@@ -364,12 +367,18 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
         def ex(j):
             return None if (exps is None or fm[j] != FP32) else exps[j]
 
-        ys: Dict[int, MatBatch] = {wf: Y}
+        # Y as the left operand of every level: one split at the finest
+        # tensor-core level format (coarser levels use a prefix of its digit
+        # planes); fp32 levels get a scaled fp32 copy (FFMA GEMM)
+        ys: Dict[int, ge.Operand] = {}
+        tc_fmts = [f for f in set(fm[1:]) if ge.uses_tc(f)]
+        if tc_fmts:
+            ytc = ge.prepare(h, Y, 0, max(tc_fmts), sel)
+            for f in tc_fmts:
+                ys[f] = ytc
         for f in sorted(set(fm[1:])):
             if f not in ys:
-                yf = MatBatch.empty(f, B, n, device=dev)
-                h.convert(Y, yf, sel, exp_y if f == FP32 else None)
-                ys[f] = yf
+                ys[f] = ge.prepare(h, Y, 0, f, sel, exp_y if f == FP32 else None)
         if scalar_top:
             out = result if r - 1 == 0 else ws.next(fm[r - 1])
             h.horner_scalar_top(bm_words, fm[r], Y, blocks[r - 1], out, sel, ex(r - 1))
@@ -380,8 +389,8 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
             j0 = r
         for j in range(j0, 0, -1):
             out = result if j - 1 == 0 else ws.next(fm[j - 1])
-            h.horner_step(ys[fm[j]], phi, blocks[j - 1], out, sel,
-                          exp_y if fm[j] == FP32 else None, ex(j), ex(j - 1))
+            ge.horner(h, ys[fm[j]], ge.prepare(h, phi, 1, fm[j], sel), fm[j], blocks[j - 1], out, sel,
+                      exp_y if fm[j] == FP32 else None, ex(j), ex(j - 1))
             phi = out
     timer.stop()
     return result
@@ -666,7 +675,7 @@ def cos_argument(X, ctx: PrecisionCtx) -> MatBatch:
         Xk = MatBatch.empty(wf, Xw.batch, Xw.rows, device=Xw.device)
         h.convert(Xw, Xk)
     Z = MatBatch.empty(wf, Xk.batch, Xk.rows, device=Xk.device)
-    h.gemm(Xk, Xk, Z)
+    ge.gemm(h, ge.prepare(h, Xk, 0, wf), ge.prepare(h, Xk, 1, wf), Z)
     return Z
 
 

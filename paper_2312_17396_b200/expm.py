@@ -25,6 +25,7 @@ from typing import List, Optional
 import numpy as np
 
 from . import _lib
+from . import gemm_engine as ge
 from .bounds import extra_squarings
 from .engine import BatchReport, _input, ps_mixed_exp
 from .planner import default_block_size
@@ -69,7 +70,7 @@ def expm_ss(A, ctx: PrecisionCtx, m: int = DEFAULT_M, delta: float = 10.0, timin
     for t in range(1, max(ells) + 1 if ells else 1):
         members = [b for b in range(B) if ells[b] >= t]
         sel = torch.tensor(members, dtype=torch.int32, device=P.device)
-        h.gemm(P, P, Q, sel)          # Q = P P for the selected members
+        ge.gemm(h, ge.prepare(h, P, 0, P.fmt, sel), ge.prepare(h, P, 1, P.fmt, sel), Q, sel)  # Q = P P
         h.convert(Q, P, sel)          # copy back (same format: exact)
     for b, r_ in enumerate(reps):
         r_._diag_extra = dict(r_._diag_extra or {}, squarings=int(ells[b]), degree=m,

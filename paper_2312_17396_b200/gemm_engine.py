@@ -1,0 +1,83 @@
+"""GEMM engine selection for the PS pipeline.
+
+Two sm_100a implementations of every multiword GEMM exist in
+libmpps_b200.so:
+
+* ``tc``   -- INT8 tensor cores (tcgen05.mma kind::i8) on exact digit-plane
+  splittings of the operands (csrc/ozaki.cuh): fp64 (8 planes), dd (16),
+  qd (31).  The operand that stays fixed across a chain (X in the power
+  chain, Y in the Horner chain) is split once per evaluation.
+* ``simt`` -- FP64-pipe error-free-transform GEMMs (csrc/gemm.cuh); also
+  the fp32 levels' FFMA GEMM in both engines.
+
+The default is ``tc``; ``MPPS_GEMM=simt`` (environment) or
+``set_engine("simt")`` selects the SIMT kernels (A/B evidence, tests).
+"""
+
+from __future__ import annotations
+
+import os
+
+from .precision import FP32, MatBatch
+
+_ENGINE = os.environ.get("MPPS_GEMM", "tc").lower()
+
+
+def set_engine(name: str) -> None:
+    global _ENGINE
+    if name not in ("tc", "simt"):
+        raise ValueError("engine must be 'tc' or 'simt'")
+    _ENGINE = name
+
+
+def engine() -> str:
+    return _ENGINE
+
+
+def uses_tc(fmt: int) -> bool:
+    return _ENGINE == "tc" and fmt != FP32
+
+
+class Operand:
+    """A GEMM operand prepared for one side: the MatBatch itself (SIMT) or
+    its digit planes (tensor cores).  ``fmt`` is the format it was prepared
+    at (for SIMT the data is converted to it)."""
+
+    __slots__ = ("mat", "slices", "fmt", "side")
+
+    def __init__(self, mat, slices, fmt, side):
+        self.mat, self.slices, self.fmt, self.side = mat, slices, fmt, side
+
+
+def prepare(h, A: MatBatch, side: int, fmt: int, sel=None, exp=None) -> Operand:
+    """Prepare A as the left (side 0) or right (side 1) operand of GEMMs at
+    ``fmt``.  For the tensor-core engine the split uses the planes of the
+    finest format any later use needs (the caller passes it as ``fmt``);
+    a coarser level uses a prefix of the planes."""
+    if uses_tc(fmt):
+        if exp is not None:
+            raise ValueError("power-of-two scaling applies to fp32 levels only")
+        return Operand(A, h.slice(A, side, h.slices_for(fmt), sel), fmt, side)
+    if A.fmt != fmt or exp is not None:
+        B = MatBatch.empty(fmt, A.batch, A.rows, A.cols, device=A.device)
+        h.convert(A, B, sel, exp)
+        A = B
+    return Operand(A, None, fmt, side)
+
+
+def gemm(h, L: Operand, R: Operand, C: MatBatch, sel=None) -> None:
+    """C = L R at C's format."""
+    if L.slices is not None and R.slices is not None:
+        h.gemm_sliced(L.slices, R.slices, h.slices_for(C.fmt), C, sel)
+    else:
+        h.gemm(L.mat, R.mat, C, sel)
+
+
+def horner(h, Y: Operand, phi: Operand, fmt_level: int, Bprev, out, sel=None, exp_y=None, exp_in=None,
+           exp_out=None) -> None:
+    """out = RN_out(2^eo (Bprev + 2^-(ey+ei) RN_level(Y phi)))."""
+    if Y.slices is not None and phi.slices is not None:
+        h.horner_step_sliced(Y.slices, phi.slices, h.slices_for(fmt_level), Bprev, out, sel, exp_y, exp_in,
+                             exp_out, fmt_in=fmt_level)
+    else:
+        h.horner_step(Y.mat, phi.mat, Bprev, out, sel, exp_y, exp_in, exp_out)

@@ -66,7 +66,9 @@ def mat_mul(A: MatBatch, B: MatBatch, ctx: PrecisionCtx) -> MatBatch:
         raise DimensionError(f"mat_mul: {A.shape} x {B.shape}")
     f = ctx.fmt
     C = MatBatch.empty(f, A.batch, A.rows, B.cols, device=A.device)
-    _lib.handle_for().gemm(_at(A, f), _at(B, f), C)
+    from . import gemm_engine as ge
+    h = _lib.handle_for()
+    ge.gemm(h, ge.prepare(h, _at(A, f), 0, f), ge.prepare(h, _at(B, f), 1, f), C)
     return C
 
 

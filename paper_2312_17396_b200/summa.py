@@ -149,7 +149,20 @@ class DeviceOps:
         self.h.convert(src, dst, None, self._e(exp))
 
     def gemm(self, A, B, C):
-        self.h.gemm(A, B, C)
+        self.gemm_op(self.prepare(A, 0, C.fmt), self.prepare(B, 1, C.fmt), C)
+
+    # prepared operands (tensor-core digit planes or SIMT matrices)
+    def prepare(self, A, side, fmt, exp=0):
+        from . import gemm_engine as ge
+        return ge.prepare(self.h, A, side, fmt, None, self._e(exp))
+
+    def gemm_op(self, L, R, C):
+        from . import gemm_engine as ge
+        ge.gemm(self.h, L, R, C)
+
+    def horner_op(self, Y, phi, fmt_level, Bprev, out, ey=0, ei=0, eo=0):
+        from . import gemm_engine as ge
+        ge.horner(self.h, Y, phi, fmt_level, Bprev, out, None, self._e(ey), self._e(ei), self._e(eo))
 
     def coeffs(self, series, ctx):
         return _torch().tensor(coeff_words(series, ctx), dtype=_torch().float64, device=self.device)
@@ -207,7 +220,7 @@ def cos_argument_dist(Xblk: MatBatch, ctx: PrecisionCtx, grid: ProcessGrid, ops)
         Xw = ops.empty(wf, Xblk.rows, Xblk.cols)
         ops.convert(Xblk, Xw)
     Z = ops.empty(wf, Xw.rows, Xw.cols)
-    ops.gemm(grid.row_panel(Xw), grid.col_panel(Xw), Z)
+    ops.gemm_op(ops.prepare(grid.row_panel(Xw), 0, wf), ops.prepare(grid.col_panel(Xw), 1, wf), Z)
     return Z
 
 
@@ -236,10 +249,10 @@ def ps_mixed_dist(Xblk: MatBatch, series: CoefficientSeries, ctx: PrecisionCtx, 
         ops.convert(Xblk, P1)
     powers = [P1]
     if s > 1:
-        Xcol = grid.col_panel(P1)
+        Xr = ops.prepare(grid.col_panel(P1), 1, wf)      # gathered and split once
         for _ in range(1, s):
             C = ops.empty(wf, mr, nc)
-            ops.gemm(grid.row_panel(powers[-1]), Xcol, C)
+            ops.gemm_op(ops.prepare(grid.row_panel(powers[-1]), 0, wf), Xr, C)
             powers.append(C)
     blocks = [ops.empty(wf, mr, nc) for _ in range(r + 1)]
     coeffs = ops.coeffs(series, ctx)
@@ -266,12 +279,16 @@ def ps_mixed_dist(Xblk: MatBatch, series: CoefficientSeries, ctx: PrecisionCtx, 
     # Horner (engine.py:243-252)
     Y = powers[s - 1]
     Yrow_w = grid.row_panel(Y)
-    yrow = {wf: Yrow_w}
+    from . import gemm_engine as ge
+    yrow = {}
+    tc_fmts = [f for f in set(fm[1:]) if ge.uses_tc(f) and not getattr(ops, "simt_only", False)]
+    if tc_fmts:
+        ytc = ops.prepare(Yrow_w, 0, max(tc_fmts))
+        for f in tc_fmts:
+            yrow[f] = ytc
     for f in sorted(set(fm[1:])):
         if f not in yrow:
-            yf = ops.empty(f, Yrow_w.rows, Yrow_w.cols)
-            ops.convert(Yrow_w, yf, ey if f == FP32 else 0)
-            yrow[f] = yf
+            yrow[f] = ops.prepare(Yrow_w, 0, f, ey if f == FP32 else 0)
     if m % s == 0:
         out = ops.empty(fm[r - 1], mr, nc)
         ops.scalar_top(coeff_words(series, ctx)[m], fm[r], Y, blocks[r - 1], out, ex[r - 1])
@@ -282,7 +299,7 @@ def ps_mixed_dist(Xblk: MatBatch, series: CoefficientSeries, ctx: PrecisionCtx, 
         j0 = r
     for j in range(j0, 0, -1):
         out = ops.empty(fm[j - 1], mr, nc)
-        ops.horner_step(yrow[fm[j]], grid.col_panel(phi), blocks[j - 1], out,
-                        ey if fm[j] == FP32 else 0, ex[j], ex[j - 1])
+        ops.horner_op(yrow[fm[j]], ops.prepare(grid.col_panel(phi), 1, fm[j]), fm[j], blocks[j - 1], out,
+                      ey if fm[j] == FP32 else 0, ex[j], ex[j - 1])
         phi = out
     return DistResult(phi, digits, nu, False, norms, s, r)

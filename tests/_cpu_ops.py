@@ -12,8 +12,27 @@ from paper_2312_17396_b200.coefficients import coeff_words
 from paper_2312_17396_b200.precision import FP32, MatBatch
 
 
+class _Op:
+    def __init__(self, mat):
+        self.mat = mat
+
+
 class CpuOps:
     device = torch.device("cpu")
+    simt_only = True
+
+    def prepare(self, A, side, fmt, exp=0):
+        if A.fmt == fmt and not exp:
+            return _Op(A)
+        B = self.empty(fmt, A.rows, A.cols)
+        self.convert(A, B, exp)
+        return _Op(B)
+
+    def gemm_op(self, L, R, C):
+        self.gemm(L.mat, R.mat, C)
+
+    def horner_op(self, Y, phi, fmt_level, Bprev, out, ey=0, ei=0, eo=0):
+        self.horner_step(Y.mat, phi.mat, Bprev, out, ey, ei, eo)
 
     def empty(self, fmt, rows, cols):
         m = MatBatch.empty(fmt, 1, rows, cols, device="cpu")
