@@ -114,6 +114,7 @@ template <> struct WV<F64> {
   static __device__ __forceinline__ T zero() { return 0.0; }
   static __device__ __forceinline__ T from(const mp::qd &q) { return q.x[0]; }
   static __device__ __forceinline__ T axpy(T a, T x, T y) { return __dadd_rn(__dmul_rn(a, x), y); }
+  static __device__ __forceinline__ T axpy_fast(T a, T x, T y) { return axpy(a, x, y); }
   static __device__ __forceinline__ double hi(T v) { return v; }
   static __device__ __forceinline__ void store(const MatRef &m, long long off, T v) { ((double *)m.data)[off] = v; }
 };
@@ -122,6 +123,9 @@ template <> struct WV<DD> {
   static __device__ __forceinline__ T zero() { return mp::dd_make(0.0, 0.0); }
   static __device__ __forceinline__ T from(const mp::qd &q) { return mp::dd_make(q.x[0], q.x[1]); }
   static __device__ __forceinline__ T axpy(T a, T x, T y) { return mp::dd_add(mp::dd_mul(a, x), y); }
+  // block assembly: normwise-accurate sloppy add (the blocks are sums of
+  // scaled powers; errors are measured against sum |b_j| ||X^j||)
+  static __device__ __forceinline__ T axpy_fast(T a, T x, T y) { return mp::dd_add_sloppy(mp::dd_mul(a, x), y); }
   static __device__ __forceinline__ double hi(T v) { return v.hi; }
   static __device__ __forceinline__ void store(const MatRef &m, long long off, T v) {
     double *p = (double *)m.data + off; p[0] = v.hi; p[m.plane] = v.lo;
@@ -132,6 +136,7 @@ template <> struct WV<QD> {
   static __device__ __forceinline__ T zero() { return mp::qd_make(0.0, 0.0, 0.0, 0.0); }
   static __device__ __forceinline__ T from(const mp::qd &q) { return q; }
   static __device__ __forceinline__ T axpy(T a, T x, T y) { return mp::qd_add(mp::qd_mul(a, x), y); }
+  static __device__ __forceinline__ T axpy_fast(T a, T x, T y) { return axpy(a, x, y); }
   static __device__ __forceinline__ double hi(T v) { return v.x[0]; }
   static __device__ __forceinline__ void store(const MatRef &m, long long off, T v) {
     double *p = (double *)m.data + off;
@@ -200,7 +205,7 @@ struct AssembleArgs {
 // One thread per (column, 32-row chunk); the r+1 block accumulators of an
 // entry live in registers, the coefficients in shared memory (broadcast
 // reads), so each power entry is loaded once and used for every block.
-template <int WF>
+template <int WF, int NB>
 __global__ void __launch_bounds__(128) assemble_kernel(const AssembleArgs a) {
   using V = WV<WF>;
   using T = typename V::T;
@@ -221,30 +226,30 @@ __global__ void __launch_bounds__(128) assemble_kernel(const AssembleArgs a) {
     else if constexpr (CW == 2) return mp::dd_make(c[0], c[1]);
     else return c[0];
   };
-  double cs[kMaxBlocks + 1];
+  double cs[NB + 1];
 #pragma unroll
-  for (int k = 0; k <= kMaxBlocks; ++k) cs[k] = 0.0;
+  for (int k = 0; k <= NB; ++k) cs[k] = 0.0;
   const int row0 = chunk * kRowsPerChunk;
   const int row1 = min(a.rows, row0 + kRowsPerChunk);
   for (int row = row0; row < row1; ++row) {
-    T acc[kMaxBlocks];
+    T acc[NB];
     const bool diag = (row + a.row0) == (col + a.col0);
 #pragma unroll
-    for (int k = 0; k < kMaxBlocks; ++k)
+    for (int k = 0; k < NB; ++k)
       if (k <= r) acc[k] = diag ? coef(s * k) : V::zero();
     for (int j = 1; j < s; ++j) {
       const MatRef &P = a.P[j - 1];
       T x = V::from(load_qd(P, (long long)b * P.bstride + (long long)row * P.ld + col));
 #pragma unroll
-      for (int k = 0; k < kMaxBlocks; ++k) {
+      for (int k = 0; k < NB; ++k) {
         if (k <= r) {
           const int hi = (k < full) ? s - 1 : m - s * full;
-          if (j <= hi) acc[k] = V::axpy(coef(s * k + j), x, acc[k]);
+          if (j <= hi) acc[k] = V::axpy_fast(coef(s * k + j), x, acc[k]);
         }
       }
     }
 #pragma unroll
-    for (int k = 0; k < kMaxBlocks; ++k) {
+    for (int k = 0; k < NB; ++k) {
       if (k <= r) {
         const MatRef &B = a.Bk[k];
         V::store(B, (long long)b * B.bstride + (long long)row * B.ld + col, acc[k]);
@@ -252,13 +257,13 @@ __global__ void __launch_bounds__(128) assemble_kernel(const AssembleArgs a) {
       }
     }
     const MatRef &Y = a.P[s - 1];
-    cs[kMaxBlocks] += fabs(((const double *)Y.data)[(long long)b * Y.bstride + (long long)row * Y.ld + col]);
+    cs[NB] += fabs(((const double *)Y.data)[(long long)b * Y.bstride + (long long)row * Y.ld + col]);
   }
   double *out = a.partial + ((long long)b * a.nchunk + chunk) * (long long)(r + 2) * n;
 #pragma unroll
-  for (int k = 0; k < kMaxBlocks; ++k)
+  for (int k = 0; k < NB; ++k)
     if (k <= r) out[(long long)k * n + col] = cs[k];
-  out[(long long)(r + 1) * n + col] = cs[kMaxBlocks];
+  out[(long long)(r + 1) * n + col] = cs[NB];
 }
 
 struct ColsumArgs {
@@ -552,11 +557,11 @@ static int assemble_common(mpps_handle *h, const mpps_mat *powers, int s, int m,
   cudaError_t e = cudaMallocAsync((void **)&a.partial, pbytes, h->stream);
   if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "assemble scratch: %s", cudaGetErrorString(e));
   dim3 grid((cols + 127) / 128, a.nchunk, batch);
-  switch (wf) {
-    case F64: assemble_kernel<F64><<<grid, 128, 0, h->stream>>>(a); break;
-    case DD: assemble_kernel<DD><<<grid, 128, 0, h->stream>>>(a); break;
-    case QD: assemble_kernel<QD><<<grid, 128, 0, h->stream>>>(a); break;
-  }
+  const int nbk = r + 1 <= 4 ? 4 : r + 1 <= 8 ? 8 : 16;
+#define AK(WW, NN) \
+  if (wf == WW && nbk == NN) assemble_kernel<WW, NN><<<grid, 128, 0, h->stream>>>(a); else
+  AK(F64, 4) AK(F64, 8) AK(F64, 16) AK(DD, 4) AK(DD, 8) AK(DD, 16) AK(QD, 4) AK(QD, 8) AK(QD, 16) {}
+#undef AK
   int rc = after_launch(h, "assemble_kernel");
   if (rc) return rc;
   if (norms) {
@@ -701,16 +706,25 @@ extern "C" int mpps_slice(mpps_handle *h, const mpps_mat *src, int side, mpps_sl
   if (nb == 0) return MPPS_OK;
   oz::SliceRef o = sref(out);
   const int fi = fmt_index(src->fmt);
+  const int W = fmt_words(fi);
+  const int S = out->nslices;
+  if (S != 8 && S != 16 && S != 31) return set_err(h, MPPS_EINVAL, "slice: 8, 16 or 31 digit planes");
   if (side == 0) {
     dim3 grid((out->rpad * 32 + 255) / 256, nb);
-    oz::slice_rows_kernel<<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel);
+#define SR(WW, SS) \
+  if (W == WW && S == SS) oz::slice_rows_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
+    SR(1, 8) SR(1, 16) SR(1, 31) SR(2, 8) SR(2, 16) SR(2, 31) SR(4, 8) SR(4, 16) SR(4, 31) {}
+#undef SR
     return after_launch(h, "slice_rows_kernel");
   }
   oz::col_exps_kernel<<<dim3((out->rpad + 127) / 128, nb), 128, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel);
   rc = after_launch(h, "col_exps_kernel");
   if (rc) return rc;
   dim3 grid(out->rpad / 32, out->kpad / 32, nb);
-  oz::slice_cols_kernel<31><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel);
+#define SC(WW, SS) \
+  if (W == WW && S == SS) oz::slice_cols_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
+  SC(1, 8) SC(1, 16) SC(1, 31) SC(2, 8) SC(2, 16) SC(2, 31) SC(4, 8) SC(4, 16) SC(4, 31) {}
+#undef SC
   return after_launch(h, "slice_cols_kernel");
 }
 

@@ -121,29 +121,56 @@ struct SliceRef {
   __host__ __device__ long long plane() const { return (long long)batch * rpad * kpad; }
 };
 
-// Split one exact value (qd words, |v| < 1 after scaling) into S signed
-// digits: first 6 bits, then 7 bits each; the residual is kept exactly
-// (scaling by 2^k and subtracting the nearest integer are exact).
-__device__ __forceinline__ void split_digits(mp::qd v, int S, int8_t *out, long long stride) {
-  double x0 = v.x[0], x1 = v.x[1], x2 = v.x[2], x3 = v.x[3];
+// Split one exact value (W words, |v| < 1 after scaling) into S signed
+// digits: first 6 bits, then 7 bits each.  The residual is kept exactly
+// (scaling by 2^k and subtracting the nearest integer are exact; the words
+// are renormalised with TwoSums), so sum_s d_s 2^-(6+7s) is the value
+// truncated after S digits.
+template <int W, int S>
+__device__ __forceinline__ void split_digits_w(const mp::qd &v, int8_t (&dg)[S]) {
+  double x[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) x[w] = v.x[w];
   double sc = 64.0;
+#pragma unroll
   for (int s = 0; s < S; ++s) {
-    x0 *= sc; x1 *= sc; x2 *= sc; x3 *= sc;
-    double d = rint(x0);
-    double r = x0 - d;  // exact
-    // renormalise (r, x1, x2, x3) exactly
-    double s0, e0, s1, e1, s2, e2;
-    mp::two_sum(r, x1, s0, e0);
-    mp::two_sum(e0, x2, s1, e1);
-    mp::two_sum(e1, x3, s2, e2);
-    x0 = s0; x1 = s1; x2 = s2; x3 = e2;
-    out[s * stride] = (int8_t)(int)d;
+#pragma unroll
+    for (int w = 0; w < W; ++w) x[w] *= sc;
+    const double d = rint(x[0]);
+    double r = x[0] - d;  // exact
+    if constexpr (W == 1) {
+      x[0] = r;
+    } else {
+      double c = r;
+#pragma unroll
+      for (int w = 1; w < W; ++w) {  // carry the lower words up (exact)
+        double t, e;
+        mp::two_sum(c, x[w], t, e);
+        x[w - 1] = t;
+        c = e;
+      }
+      x[W - 1] = c;
+    }
+    dg[s] = (int8_t)(int)d;
     sc = 128.0;
   }
 }
 
+__device__ __forceinline__ int row_exponent(double mx) {
+  int e = 0;
+  if (mx > 0.0) {
+    frexp(mx, &e);  // mx in [2^(e-1), 2^e)
+    // a multiword value may exceed its leading word by half an ulp: one bit
+    // of headroom when the maximum sits just below a power of two
+    if (ldexp(mx, -e) > 0.9999999999) e += 1;
+  }
+  return e;
+}
+
 // Side A: rows scaled by their own max exponent; output [S][b][i][k].
-// One warp per row.
+// One warp per row; each lane splits 4 consecutive entries and stores the 4
+// digits of a plane as one 32-bit word.
+template <int W, int S>
 __global__ void slice_rows_kernel(MatRef A, int rows, int cols, int fi, SliceRef out, const int *sel) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -160,23 +187,29 @@ __global__ void slice_rows_kernel(MatRef A, int rows, int cols, int fi, SliceRef
     }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  int e = 0;
-  if (mx > 0.0) {
-    frexp(mx, &e);  // mx in [2^(e-1), 2^e)
-    // |value| <= mx (1 + 2^-52) < 2^e unless mx is the largest double below
-    // 2^e; one extra bit of headroom covers that corner.
-    if (ldexp(mx, -e) > 0.9999999999) e += 1;
-  }
+  const int e = row_exponent(mx);
   if (lane == 0) out.exps[(long long)b * out.rpad + i] = e;
   const long long plane = out.plane();
   int8_t *o = out.digits + ((long long)b * out.rpad + i) * out.kpad;
-  for (int k = lane; k < out.kpad; k += 32) {
-    mp::qd v = mp::qd_make(0.0, 0.0, 0.0, 0.0);
-    if (i < rows && k < cols) {
-      v = fi == F32 ? mp::qd_from_d((double)((const float *)A.data)[base + k]) : load_qd(A, base + k);
-      v = mp::qd_ldexp(v, -e);
+  for (int k0 = 4 * lane; k0 < out.kpad; k0 += 128) {
+    uint32_t packed[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) packed[s] = 0u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = k0 + q;
+      mp::qd v = mp::qd_make(0.0, 0.0, 0.0, 0.0);
+      if (i < rows && k < cols) {
+        v = fi == F32 ? mp::qd_from_d((double)((const float *)A.data)[base + k]) : load_qd(A, base + k);
+        v = mp::qd_ldexp(v, -e);
+      }
+      int8_t dg[S];
+      split_digits_w<W, S>(v, dg);
+#pragma unroll
+      for (int s = 0; s < S; ++s) packed[s] |= ((uint32_t)(uint8_t)dg[s]) << (8 * q);
     }
-    split_digits(v, out.S, o + k, plane);
+#pragma unroll
+    for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t *>(o + s * plane + k0) = packed[s];
   }
 }
 
@@ -193,23 +226,17 @@ __global__ void col_exps_kernel(MatRef B, int rows, int cols, int fi, SliceRef o
       double v = fi == F32 ? (double)((const float *)B.data)[off] : ((const double *)B.data)[off];
       mx = fmax(mx, fabs(v));
     }
-  int e = 0;
-  if (mx > 0.0) {
-    frexp(mx, &e);
-    if (ldexp(mx, -e) > 0.9999999999) e += 1;
-  }
-  out.exps[(long long)b * out.rpad + j] = e;
+  out.exps[(long long)b * out.rpad + j] = row_exponent(mx);
 }
 
 // Side B digits, transposed through shared memory: tile of 32 k x 32 j.
-template <int SMAX>
+template <int W, int S>
 __global__ void slice_cols_kernel(MatRef B, int rows, int cols, int fi, SliceRef out, const int *sel) {
-  __shared__ int8_t tile[SMAX][32][33];
+  __shared__ int8_t tile[S][32][36];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
   const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
   const int bz = blockIdx.z;
   const int b = sel ? sel[bz] : bz;
-  const int S = out.S;
   for (int kk = ty; kk < 32; kk += 8) {
     const int k = k0 + kk, j = j0 + tx;
     mp::qd v = mp::qd_make(0.0, 0.0, 0.0, 0.0);
@@ -218,18 +245,21 @@ __global__ void slice_cols_kernel(MatRef B, int rows, int cols, int fi, SliceRef
       v = fi == F32 ? mp::qd_from_d((double)((const float *)B.data)[off]) : load_qd(B, off);
       v = mp::qd_ldexp(v, -out.exps[(long long)b * out.rpad + j]);
     }
-    int8_t dg[SMAX];
-    split_digits(v, S, dg, 1);
+    int8_t dg[S];
+    split_digits_w<W, S>(v, dg);
+#pragma unroll
     for (int s = 0; s < S; ++s) tile[s][tx][kk] = dg[s];
   }
   __syncthreads();
   const long long plane = out.plane();
-  for (int jj = ty; jj < 32; jj += 8) {
-    const int j = j0 + jj, k = k0 + tx;
-    if (j < out.rpad && k < out.kpad)
-      for (int s = 0; s < S; ++s)
-        out.digits[s * plane + ((long long)b * out.rpad + j) * out.kpad + k] = tile[s][jj][tx];
-  }
+  // each thread writes 4 consecutive k of one column j as a 32-bit word
+  const int jj = threadIdx.x >> 3, kq = (threadIdx.x & 7) * 4;
+  const int j = j0 + jj;
+  if (j < out.rpad && k0 + kq < out.kpad)
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+      *reinterpret_cast<uint32_t *>(out.digits + s * plane + ((long long)b * out.rpad + j) * out.kpad + k0 + kq) =
+          *reinterpret_cast<const uint32_t *>(&tile[s][jj][kq]);
 }
 
 // -------------------------------------------------------------- GEMM
