@@ -13,6 +13,7 @@
 #include <stdio.h>
 #include <stdarg.h>
 #include <string.h>
+#include <stdlib.h>
 
 #include "../../include/mpps_b200.h"
 #include "gemm.cuh"
@@ -728,6 +729,86 @@ extern "C" int mpps_slice(mpps_handle *h, const mpps_mat *src, int side, mpps_sl
   return after_launch(h, "slice_cols_kernel");
 }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// digit planes [S][batch][rpad][kpad] as a 3-D tensor (k, batch*rpad, S),
+// box {32, rows_box, S}, 32-byte swizzle
+static int make_slice_map(mpps_handle *h, CUtensorMap *map, const mpps_slices *s, int rows_box, int S) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return set_err(h, MPPS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)s->kpad, (cuuint64_t)s->batch * s->rpad, (cuuint64_t)s->nslices};
+  cuuint64_t strides[2] = {(cuuint64_t)s->kpad, (cuuint64_t)s->kpad * s->batch * s->rpad};
+  cuuint32_t box[3] = {32u, (cuuint32_t)rows_box, (cuuint32_t)S};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, s->digits, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(h, MPPS_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return MPPS_OK;
+}
+
+template <int S, int NT, int FO, int MODE>
+static int launch_oz_tma(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
+  constexpr size_t smem = oz::oz_tma_smem_bytes<S, NT>();
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_tma_kernel<S, NT, FO, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz tma attr: %s", cudaGetErrorString(e));
+    configured = true;
+  }
+  dim3 grid((a.N + NT - 1) / NT, (a.M + oz::kTileM - 1) / oz::kTileM, nb);
+  if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
+  oz::oz_gemm_tma_kernel<S, NT, FO, MODE><<<grid, oz::kThreadsOz, smem, h->stream>>>(a);
+  return after_launch(h, "oz_gemm_tma_kernel");
+}
+
+static int dispatch_oz_tma(mpps_handle *h, int S, int fo, int mode, const oz::OzTmaArgs &a, int nb) {
+#define OZ(SS, NT, FF, MM) if (S == SS && fo == FF && mode == MM) return launch_oz_tma<SS, NT, FF, MM>(h, a, nb);
+  OZ(8, 32, F64, 0) OZ(8, 32, F64, 1) OZ(8, 32, DD, 1) OZ(8, 32, QD, 1)
+  OZ(16, 32, DD, 0) OZ(16, 32, DD, 1) OZ(16, 32, QD, 1)
+  OZ(31, 16, QD, 0) OZ(31, 16, QD, 1)
+#undef OZ
+  return set_err(h, MPPS_EFMT, "tensor-core GEMM: no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
+}
+
+static int dispatch_oz(mpps_handle *h, int S, int fo, int mode, const oz::OzArgs &a, int nb);
+
+static bool use_tma() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MPPS_OZ_TMA");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, int S, int fo, int mode,
+                  const oz::OzArgs &a, int nb) {
+  if (!use_tma()) return dispatch_oz(h, S, fo, mode, a, nb);
+  oz::OzTmaArgs t;
+  memset(&t, 0, sizeof(t));
+  const int NT = (S > 16) ? 16 : 32;
+  int rc;
+  if ((rc = make_slice_map(h, &t.mapA, A, oz::kTileM, S)) || (rc = make_slice_map(h, &t.mapB, B, NT, S))) return rc;
+  t.A = a.A; t.B = a.B; t.M = a.M; t.N = a.N; t.K = a.K; t.S = a.S; t.C = a.C; t.sel = a.sel; t.epi = a.epi;
+  return dispatch_oz_tma(h, S, fo, mode, t, nb);
+}
+
 template <int S, int NT, int FO, int MODE>
 static int launch_oz(mpps_handle *h, const oz::OzArgs &a, int nb) {
   constexpr size_t smem = oz::oz_smem_bytes<S, NT>();
@@ -776,7 +857,7 @@ int mpps_gemm_sliced(mpps_handle *h, const mpps_slices *A, const mpps_slices *B,
   a.A = sref(A); a.B = sref(B); a.M = M; a.N = N; a.K = K; a.S = nslices;
   a.C = ref_of(C); a.sel = sel;
   int nb = sel ? nsel : C->batch;
-  return dispatch_oz(h, nslices, fmt_index(C->fmt), 0, a, nb);
+  return run_oz(h, A, B, nslices, fmt_index(C->fmt), 0, a, nb);
 }
 
 int mpps_horner_step_sliced(mpps_handle *h, const mpps_slices *Y, const mpps_slices *phi, int nslices,
@@ -793,7 +874,7 @@ int mpps_horner_step_sliced(mpps_handle *h, const mpps_slices *Y, const mpps_sli
   a.C = ref_of(out); a.sel = sel;
   a.epi.Bprev = ref_of(Bprev); a.epi.exp_y = exp_y; a.epi.exp_in = exp_in; a.epi.exp_out = exp_out;
   int nb = sel ? nsel : out->batch;
-  return dispatch_oz(h, nslices, fmt_index(out->fmt), 1, a, nb);
+  return run_oz(h, Y, phi, nslices, fmt_index(out->fmt), 1, a, nb);
 }
 
 int mpps_oz_slices_for(int fmt) { return oz_slices_for(fmt_index(fmt)); }

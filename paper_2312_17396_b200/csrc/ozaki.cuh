@@ -21,6 +21,7 @@
 // LBO = 128 B between the two 16-byte K chunks of one MMA-K step, SBO = 256 B
 // between 8-row groups.
 #pragma once
+#include <cuda.h>
 #include "gemm.cuh"
 
 namespace mpps {
@@ -33,13 +34,27 @@ constexpr int kThreadsOz = 128;
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout = 0) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
-  return d;                // base offset 0, layout SWIZZLE_NONE (0)
+  d |= (uint64_t)1 << 46;              // descriptor version (Blackwell)
+  d |= (uint64_t)(layout & 7) << 61;   // 0 = SWIZZLE_NONE, 6 = SWIZZLE_32B
+  return d;                            // base offset 0
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar), "r"(bytes) : "memory");
+}
+
+// 3-D TMA tile load into shared memory, completion counted on an mbarrier.
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                            uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(mbar)
+      : "memory");
 }
 
 // kind::i8 instruction descriptor: D s32, A/B signed int8, K-major, M x N.
@@ -408,6 +423,153 @@ __global__ void __launch_bounds__(kThreadsOz, 1) oz_gemm_kernel(const OzArgs arg
 
   // ---------------------------------------------------------- epilogue
   const int row = m0 + warp * 32 + lane;  // TMEM lane == tile row
+  const int ea = args.A.exps[(long long)b * args.A.rpad + m0 + warp * 32 + lane];
+  const MatRef &C = args.C;
+  int ey = 0, ei = 0, eo = 0;
+  if constexpr (MODE == 1) {
+    if (args.epi.exp_y) ey = args.epi.exp_y[b];
+    if (args.epi.exp_in) ei = args.epi.exp_in[b];
+    if (args.epi.exp_out) eo = args.epi.exp_out[b];
+  }
+  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+  constexpr int CW = (S > 16) ? 4 : 8;
+  for (int c0 = 0; c0 < NT; c0 += CW) {
+    int32_t D[S][CW];
+#pragma unroll
+    for (int d = 0; d < S; ++d) {
+      if constexpr (CW == 8) tmem_ld8(lane_base + (uint32_t)(d * NT + c0), D[d]);
+      else tmem_ld4(lane_base + (uint32_t)(d * NT + c0), D[d]);
+    }
+    tmem_ld_wait();
+#pragma unroll
+    for (int jj = 0; jj < CW; ++jj) {
+      const int col = n0 + c0 + jj;
+      if (row >= args.M || col >= args.N) continue;
+      int32_t Dj[S];
+#pragma unroll
+      for (int d = 0; d < S; ++d) Dj[d] = D[d][jj];
+      mp::qd v = combine_diagonals<S>(Dj);
+      const int eb = args.B.exps[(long long)b * args.B.rpad + col];
+      v = mp::qd_ldexp(v, ea + eb);
+      const long long off = (long long)b * C.bstride + (long long)row * C.ld + col;
+      if constexpr (MODE == 0) {
+        store_fmt<FO>(C, off, v, 0);
+      } else {
+        const int sh = -(ey + ei);
+        if (sh) v = mp::qd_ldexp(v, sh);
+        mp::qd bv = load_qd(args.epi.Bprev, (long long)b * args.epi.Bprev.bstride + (long long)row * args.epi.Bprev.ld + col);
+        store_fmt<FO>(C, off, horner_add<FO>(bv, v), eo);
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<TCOLS>(tmem);
+}
+
+// ------------------------------------------------- TMA-fed pipeline
+// Digit planes [S][batch][rpad][kpad] viewed by TMA as a 3-D tensor
+// (k, row, slice); one box = 32 B of K x R rows x all S planes, written
+// with the 32-byte swizzle that the UMMA SWIZZLE_32B K-major layout expects
+// (8-row groups every 256 B; plane s of A at +s*R*32 B; the B planes are
+// contiguous rows, so the concatenated-B MMAs see one N = (S-t0)*NT tile).
+struct OzTmaArgs {
+  CUtensorMap mapA;   // box {32, 128, S}
+  CUtensorMap mapB;   // box {32, NT, S}
+  SliceRef A, B;
+  int M, N, K, S;
+  MatRef C;
+  const int *sel;
+  HornerEpi epi;
+};
+
+template <int S, int NT>
+__host__ __device__ constexpr int oz_tma_stages() {
+  return (int)(((size_t)200 * 1024) / oz_stage_bytes<S, NT>()) >= 4 ? 4 : (int)(((size_t)200 * 1024) / oz_stage_bytes<S, NT>());
+}
+template <int S, int NT>
+__host__ __device__ constexpr size_t oz_tma_smem_bytes() { return oz_tma_stages<S, NT>() * oz_stage_bytes<S, NT>() + 2048; }
+
+template <int S, int NT, int FO, int MODE>
+__global__ void __launch_bounds__(kThreadsOz, 1) oz_gemm_tma_kernel(const __grid_constant__ OzTmaArgs args) {
+  constexpr int STAGES = oz_tma_stages<S, NT>();
+  static_assert(STAGES >= 1, "stage does not fit");
+  constexpr uint32_t STAGE = (uint32_t)oz_stage_bytes<S, NT>();
+  constexpr uint32_t A_SLICE = kTileM * kKStep;   // 4 KB
+  constexpr uint32_t B_SLICE = NT * kKStep;
+  constexpr int TCOLS = tmem_cols_for(S * NT);
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1 KB aligned stage ring (swizzle atoms must not straddle)
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE);
+  uint64_t *empty = full + STAGES;
+  uint64_t *done = empty + STAGES;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int bz = blockIdx.z;
+  const int b = args.sel ? args.sel[bz] : bz;
+  const int m0 = blockIdx.y * kTileM, n0 = blockIdx.x * NT;
+  const int ksteps = args.A.kpad / kKStep;
+
+  if (warp == 0) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
+  if (tid == 32) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    mbar_init(smem_u32(done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = smem_u32(smem);
+  const int rowA = b * args.A.rpad + m0, rowB = b * args.B.rpad + n0;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer
+    for (int kb = 0; kb < ksteps; ++kb) {
+      const int st = kb % STAGES;
+      if (kb >= STAGES) mbar_wait(smem_u32(&empty[st]), ((kb / STAGES) - 1) & 1);
+      const uint32_t sa = sbase + st * STAGE;
+      mbar_expect_tx(smem_u32(&full[st]), STAGE);
+      tma_load_3d(sa, &args.mapA, kb * kKStep, rowA, 0, smem_u32(&full[st]));
+      tma_load_3d(sa + S * A_SLICE, &args.mapB, kb * kKStep, rowB, 0, smem_u32(&full[st]));
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer
+    for (int kb = 0; kb < ksteps; ++kb) {
+      const int st = kb % STAGES;
+      mbar_wait(smem_u32(&full[st]), (kb / STAGES) & 1);
+      fence_after();
+      const uint32_t sa = sbase + st * STAGE;
+      const uint32_t sb = sa + S * A_SLICE;
+#pragma unroll 1
+      for (int s = 0; s < S; ++s) {
+        const uint64_t ad = umma_desc(sa + s * A_SLICE, 16, 256, 6);
+        int ncols = (S - s) * NT;
+        int t0 = 0;
+        while (ncols > 0) {
+          const int nn = ncols > 256 ? 256 : ncols;
+          const uint64_t bd = umma_desc(sb + t0 * B_SLICE, 16, 256, 6);
+          mma_i8(tmem + (uint32_t)((s + t0) * NT), ad, bd, idesc_i8(kTileM, nn), (kb > 0 || s > 0) ? 1u : 0u);
+          t0 += nn / NT;
+          ncols -= nn;
+        }
+      }
+      mma_commit(smem_u32(&empty[st]));
+    }
+    mma_commit(smem_u32(done));
+  }
+  __syncwarp();
+  mbar_wait(smem_u32(done), 0);
+  fence_after();
+
+  // ---------------------------------------------------------- epilogue
+  const int row = m0 + warp * 32 + lane;
   const int ea = args.A.exps[(long long)b * args.A.rpad + m0 + warp * 32 + lane];
   const MatRef &C = args.C;
   int ey = 0, ei = 0, eo = 0;
