@@ -140,6 +140,18 @@ def measure_peaks(torch, h):
         out[name] = best / 1e12
     out["dd"] = out["fp64"] / 15.0
     out["qd"] = out["fp64"] / 115.0
+    # INT8 tensor pipe (tcgen05 kind::i8), the bound of the tensor-core GEMMs
+    iters = 4096
+    h.probe_i8mma(sms, 64, scratch)
+    best = 0.0
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        h.probe_i8mma(sms, iters, scratch)
+        b.record()
+        torch.cuda.synchronize()
+        best = max(best, sms * 2.0 * 128 * 256 * 32 * iters / (a.elapsed_time(b) * 1e-3))
+    out["int8_tops"] = best / 1e12
     return out
 
 
@@ -426,12 +438,35 @@ def run_ours(args, rank, world, local_rank):
     dom = max(by_key.items(), key=lambda kv: kv[1][1])
     (kind, fin, fout, M, N, K, nb), (cnt, sec) = dom
     fname = names[fin]
-    achieved = 2.0 * M * N * K * nb / (sec / cnt) / 1e12
+    logical = 2.0 * M * N * K * nb / (sec / cnt) / 1e12       # logical TFLOP/s of the format
     step_time = total / args.steps
     fs = wl.flop_scale()
     t_ideal = sum(fs * c / (peaks[f] * 1e12) for f, c in gem.items())
     eff_gflops = sum(fs * c for c in gem.values()) * world * args.steps / total / 1e9
     plan0 = plans[0]
+    if kind.endswith("_tc"):
+        # INT8 tensor-core GEMM by exact digit-plane splitting: the hardware
+        # bound is the INT8 tensor pipe; algorithmic ops per launch =
+        # 2 M N K x (S(S+1)/2 plane pairs), S = 4/8/16/31 for fp32/fp64/dd/qd
+        S = {7: 4, 15: 8, 31: 16, 63: 31}[fin]
+        achieved = logical * S * (S + 1) / 2
+        roof = {"bound": "tensor (int8)", "achieved": achieved, "peak": peaks["int8_tops"],
+                "unit": "TOPS (int8)", "frac": achieved / peaks["int8_tops"],
+                "logical_tflops": logical, "logical_frac_of_format_peak": logical / peaks[fname],
+                "peak_source": f"tcgen05 kind::i8 probe in bench.py on this GPU ({peaks['int8_tops']:.0f} TOPS); "
+                               f"format peaks from DFMA/FFMA probes (fp64 {peaks['fp64']:.2f} TF/s, "
+                               f"Peak_dd = Peak_fp64/15, Peak_qd = Peak_fp64/115, SURVEY 8d); "
+                               "MEASURED_PEAKS.json holds only HBM and bf16"}
+    else:
+        roof = {"bound": "fp64-pipe" if fname != "fp32" else "fp32-pipe", "achieved": logical, "peak": peaks[fname],
+                "unit": "TFLOP/s (logical)", "frac": logical / peaks[fname],
+                "peak_source": "FMA pipe microbenchmark in bench.py on this GPU "
+                               f"(fp64 {peaks['fp64']:.2f} TF/s, fp32 {peaks['fp32']:.2f} TF/s); "
+                               "Peak_dd = Peak_fp64/15, Peak_qd = Peak_fp64/115 (SURVEY 8d); "
+                               "MEASURED_PEAKS.json holds only HBM and bf16"}
+    roof.update({"kernel": f"{kind} {fname}->{names[fout]} {M}x{N}x{K} x{nb}", "traffic": None,
+                 "share_of_step": sec / args.steps / step_time, "launches_per_step": cnt / args.steps,
+                 "eval_frac": t_ideal / step_time})
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * step_time, "higher_is_better": True,
@@ -441,19 +476,11 @@ def run_ours(args, rank, world, local_rank):
                    "n": wl.n, "m": wl.m, "digits": wl.cfg["digits"],
                    "schedule_digits": [list(p.level_digits) for p in plans],
                    "level_formats": wl.formats(rep), "gemms_per_step_per_gpu": gem,
+                   "gemm_engine": __import__("paper_2312_17396_b200.gemm_engine", fromlist=["x"]).engine(),
                    "parallelism": wl.parallelism,
                    "l2": "256 MiB buffer written between timed steps (L2 flushed)"},
         "gflops_effective": eff_gflops,
-        "roofline": {"bound": "fp64-pipe" if fname != "fp32" else "fp32-pipe",
-                     "kernel": f"{kind} {fname}->{names[fout]} {M}x{N}x{K} x{nb}",
-                     "achieved": achieved, "peak": peaks[fname], "unit": "TFLOP/s (logical)",
-                     "frac": achieved / peaks[fname], "traffic": None, "share_of_step": sec / args.steps / step_time,
-                     "launches_per_step": cnt / args.steps,
-                     "peak_source": "FMA pipe microbenchmark in bench.py on this GPU "
-                                    f"(fp64 {peaks['fp64']:.2f} TF/s, fp32 {peaks['fp32']:.2f} TF/s); "
-                                    "Peak_dd = Peak_fp64/15, Peak_qd = Peak_fp64/115 (SURVEY 8d); "
-                                    "MEASURED_PEAKS.json holds only HBM and bf16",
-                     "eval_frac": t_ideal / step_time},
+        "roofline": roof,
         "peaks_tflops": peaks,
         "e2e": {"value": e2e, "unit": "evals/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,

@@ -188,6 +188,10 @@ int mpps_oz_slices_for(int fmt);
  * steps in fmt (MPPS_FP32 / MPPS_FP64): 16 * iters flops per thread. */
 int mpps_probe_fma(mpps_handle *h, int fmt, int blocks, int iters, void *scratch);
 
+/* Diagnostic: INT8 tensor-pipe peak probe (tcgen05 kind::i8, 128x256x32
+ * MMAs back to back, one CTA per SM): 2*128*256*32*iters ops per CTA. */
+int mpps_probe_i8mma(mpps_handle *h, int blocks, int iters, void *scratch);
+
 #ifdef __cplusplus
 }
 #endif

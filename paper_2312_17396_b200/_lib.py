@@ -27,7 +27,7 @@ EXPORTED = (
     "mpps_axpy", "mpps_powers", "mpps_assemble_blocks", "mpps_one_norm",
     "mpps_horner_step", "mpps_horner_scalar_top", "mpps_probe_fma",
     "mpps_assemble_blocks_dist", "mpps_colmax", "mpps_slice", "mpps_gemm_sliced",
-    "mpps_horner_step_sliced", "mpps_oz_slices_for",
+    "mpps_horner_step_sliced", "mpps_oz_slices_for", "mpps_probe_i8mma",
 )
 
 
@@ -126,6 +126,7 @@ def load_library(path: Optional[str] = None):
         lib.mpps_gemm_sliced.argtypes = [vp, sp, sp, ip, ip, ip, ip, mp, vp, ip]
         lib.mpps_horner_step_sliced.argtypes = [vp, sp, sp, ip, mp, mp, vp, ip, vp, vp, vp]
         lib.mpps_oz_slices_for.argtypes = [ip]
+        lib.mpps_probe_i8mma.argtypes = [vp, ip, ip, vp]
         for name in EXPORTED:
             getattr(lib, name).restype = getattr(lib, name).restype or ip
         if path is None:
@@ -296,6 +297,9 @@ class Handle:
                                                     ctypes.byref(o), _ptr(sel), nsel, _ptr(exp_out)),
                     "horner_scalar_top")
 
+
+    def probe_i8mma(self, blocks: int, iters: int, scratch):
+        self._check(self.lib.mpps_probe_i8mma(self.h, blocks, iters, scratch.data_ptr()), "probe_i8mma")
 
     def probe_fma(self, fmt: int, blocks: int, iters: int, scratch):
         self._check(self.lib.mpps_probe_fma(self.h, fmt, blocks, iters, scratch.data_ptr()), "probe_fma")

@@ -684,7 +684,7 @@ int mpps_probe_fma(mpps_handle *h, int fmt, int blocks, int iters, void *scratch
 }  // extern "C"
 
 // ------------------------------------------------ tensor-core (Ozaki) path
-static int oz_slices_for(int fi) { return fi == QD ? 31 : fi == DD ? 16 : fi == F64 ? 8 : -1; }
+static int oz_slices_for(int fi) { return fi == QD ? 31 : fi == DD ? 16 : fi == F64 ? 8 : fi == F32 ? 4 : -1; }
 
 static oz::SliceRef sref(const mpps_slices *s) {
   oz::SliceRef r;
@@ -709,22 +709,22 @@ extern "C" int mpps_slice(mpps_handle *h, const mpps_mat *src, int side, mpps_sl
   const int fi = fmt_index(src->fmt);
   const int W = fmt_words(fi);
   const int S = out->nslices;
-  if (S != 8 && S != 16 && S != 31) return set_err(h, MPPS_EINVAL, "slice: 8, 16 or 31 digit planes");
+  if (S != 4 && S != 8 && S != 16 && S != 31) return set_err(h, MPPS_EINVAL, "slice: 4, 8, 16 or 31 digit planes");
   if (side == 0) {
     dim3 grid((out->rpad * 32 + 255) / 256, nb);
 #define SR(WW, SS) \
   if (W == WW && S == SS) oz::slice_rows_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
-    SR(1, 8) SR(1, 16) SR(1, 31) SR(2, 8) SR(2, 16) SR(2, 31) SR(4, 8) SR(4, 16) SR(4, 31) {}
+    SR(1, 4) SR(1, 8) SR(1, 16) SR(1, 31) SR(2, 4) SR(2, 8) SR(2, 16) SR(2, 31) SR(4, 4) SR(4, 8) SR(4, 16) SR(4, 31) {}
 #undef SR
     return after_launch(h, "slice_rows_kernel");
   }
-  oz::col_exps_kernel<<<dim3((out->rpad + 127) / 128, nb), 128, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel);
+  oz::col_exps_kernel<<<dim3(out->rpad / 32, nb), 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel);
   rc = after_launch(h, "col_exps_kernel");
   if (rc) return rc;
   dim3 grid(out->rpad / 32, out->kpad / 32, nb);
 #define SC(WW, SS) \
   if (W == WW && S == SS) oz::slice_cols_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
-  SC(1, 8) SC(1, 16) SC(1, 31) SC(2, 8) SC(2, 16) SC(2, 31) SC(4, 8) SC(4, 16) SC(4, 31) {}
+  SC(1, 4) SC(1, 8) SC(1, 16) SC(1, 31) SC(2, 4) SC(2, 8) SC(2, 16) SC(2, 31) SC(4, 4) SC(4, 8) SC(4, 16) SC(4, 31) {}
 #undef SC
   return after_launch(h, "slice_cols_kernel");
 }
@@ -779,6 +779,7 @@ static int launch_oz_tma(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
 
 static int dispatch_oz_tma(mpps_handle *h, int S, int fo, int mode, const oz::OzTmaArgs &a, int nb) {
 #define OZ(SS, NT, FF, MM) if (S == SS && fo == FF && mode == MM) return launch_oz_tma<SS, NT, FF, MM>(h, a, nb);
+  OZ(4, 32, F32, 0) OZ(4, 32, F32, 1) OZ(4, 32, F64, 1) OZ(4, 32, DD, 1) OZ(4, 32, QD, 1)
   OZ(8, 32, F64, 0) OZ(8, 32, F64, 1) OZ(8, 32, DD, 1) OZ(8, 32, QD, 1)
   OZ(16, 32, DD, 0) OZ(16, 32, DD, 1) OZ(16, 32, QD, 1)
   OZ(31, 16, QD, 0) OZ(31, 16, QD, 1)
@@ -878,5 +879,17 @@ int mpps_horner_step_sliced(mpps_handle *h, const mpps_slices *Y, const mpps_sli
 }
 
 int mpps_oz_slices_for(int fmt) { return oz_slices_for(fmt_index(fmt)); }
+
+int mpps_probe_i8mma(mpps_handle *h, int blocks, int iters, void *scratch) {
+  if (!scratch || blocks < 1 || iters < 1) return set_err(h, MPPS_EINVAL, "probe: bad arguments");
+  static bool configured = false;
+  const int smem = 40960 + 2048;
+  if (!configured) {
+    cudaFuncSetAttribute(oz::i8_mma_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  oz::i8_mma_probe_kernel<<<blocks, 128, smem, h->stream>>>(iters, (int *)scratch);
+  return after_launch(h, "i8_mma_probe_kernel");
+}
 
 }  // extern "C"

@@ -228,20 +228,29 @@ __global__ void slice_rows_kernel(MatRef A, int rows, int cols, int fi, SliceRef
   }
 }
 
-// Side B: column exponents first (one thread per column, coalesced rows).
+// Side B: column exponents.  Block = 32 columns x 8 row groups; each thread
+// scans every 8th row of its column (coalesced across the warp), then a
+// shared-memory max over the 8 groups.
 __global__ void col_exps_kernel(MatRef B, int rows, int cols, int fi, SliceRef out, const int *sel) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ double red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + tx;
   const int bz = blockIdx.y;
   const int b = sel ? sel[bz] : bz;
-  if (j >= out.rpad) return;
   double mx = 0.0;
   if (j < cols)
-    for (int k = 0; k < rows; ++k) {
+    for (int k = ty; k < rows; k += 8) {
       const long long off = (long long)b * B.bstride + (long long)k * B.ld + j;
       double v = fi == F32 ? (double)((const float *)B.data)[off] : ((const double *)B.data)[off];
       mx = fmax(mx, fabs(v));
     }
-  out.exps[(long long)b * out.rpad + j] = row_exponent(mx);
+  red[ty][tx] = mx;
+  __syncthreads();
+  if (ty == 0 && j < out.rpad) {
+#pragma unroll
+    for (int g = 1; g < 8; ++g) mx = fmax(mx, red[g][tx]);
+    out.exps[(long long)b * out.rpad + j] = row_exponent(mx);
+  }
 }
 
 // Side B digits, transposed through shared memory: tile of 32 k x 32 j.
@@ -612,6 +621,40 @@ __global__ void __launch_bounds__(kThreadsOz, 1) oz_gemm_tma_kernel(const __grid
   fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<TCOLS>(tmem);
+}
+
+// INT8 tensor-pipe peak probe: one CTA per SM issues back-to-back
+// 128x256x32 kind::i8 MMAs (operands: 40 KB of zeroed shared memory) into a
+// 256-column TMEM accumulator.  2*128*256*32 ops per MMA.
+__global__ void __launch_bounds__(128, 1) i8_mma_probe_kernel(int iters, int *out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t *done = reinterpret_cast<uint64_t *>(smem + 40960);
+  uint32_t *slot = reinterpret_cast<uint32_t *>(done + 1);
+  for (int i = threadIdx.x; i < 40960 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(smem)[i] = 0u;
+  if (threadIdx.x < 32) tmem_alloc<256>(smem_u32(slot));
+  if (threadIdx.x == 32) {
+    mbar_init(smem_u32(done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  fence_proxy_async();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *slot;
+  if (threadIdx.x == 0) {
+    const uint32_t sa = smem_u32(smem), sb = sa + 4096;
+    const uint64_t ad = umma_desc(sa, 16, 256, 6), bd = umma_desc(sb, 16, 256, 6);
+    for (int i = 0; i < iters; ++i) mma_i8(tmem, ad, bd, idesc_i8(128, 256), i > 0 ? 1u : 0u);
+    mma_commit(smem_u32(done));
+  }
+  __syncwarp();
+  mbar_wait(smem_u32(done), 0);
+  fence_after();
+  if (threadIdx.x == 0 && iters < 0) out[0] = 1;
+  fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc<256>(tmem);
 }
 
 }  // namespace oz

@@ -49,7 +49,8 @@ from .planner import (EvaluationPlan, cost_ratio, default_block_size,
                       matmul_counts, plan_digits_batch, plan_precisions,
                       snap_to_lattice)
 from .precision import (DD, FORMAT_NAME, FP32, FP64, NORM_CTX, QD,
-                        DimensionError, MatBatch, PrecisionCtx, as_fp64_batch)
+                        DimensionError, MatBatch, PrecisionCtx, as_fp64_batch,
+                        to_device_async)
 
 BUCKETS = ("power_formation", "norm_estimation", "mixed_horner", "coefficient_assembly")
 
@@ -301,7 +302,7 @@ def _assemble(h, powers: List[MatBatch], series: CoefficientSeries, ctx: Precisi
     key = (series.coeffs, ctx.binary_precision, str(dev))
     coeffs = _COEFF_DEV.get(key)
     if coeffs is None:
-        coeffs = torch.tensor(cw, dtype=torch.float64, device=dev)
+        coeffs = to_device_async(cw, torch.float64, dev)
         if len(_COEFF_DEV) > 64:
             _COEFF_DEV.clear()
         _COEFF_DEV[key] = coeffs
@@ -344,14 +345,14 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
             groups.setdefault(fm, []).append(b)
     if nil_idx:
         # p = B_0 (engine.py:378-379, 473-474)
-        ii = torch.tensor(nil_idx, device=dev)
+        ii = to_device_async(nil_idx, torch.int64, dev)
         result.data[:, ii] = blocks[0].data[:, ii]
     ws = _Workspace(B, n, dev)
     scalar_top = (m % s == 0)
     bm_words = prep.coeffs[m]
     whole = len(groups) == 1 and not nil_idx
     for fm, members in groups.items():
-        sel = None if whole else torch.tensor(members, dtype=torch.int32).to(dev, non_blocking=True)
+        sel = None if whole else to_device_async(members, torch.int32, dev)
         exps = exp_y = None
         if FP32 in fm:
             e = np.zeros((r + 1, B), dtype=np.int32)
@@ -361,8 +362,8 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
                 if fm[j] == FP32:
                     e[j, idx] = _exps_for(prep.norms[idx, j])
             ey[idx] = _exps_for(prep.norms[idx, r + 1])
-            exps = torch.from_numpy(e).to(dev, non_blocking=True)
-            exp_y = torch.from_numpy(ey).to(dev, non_blocking=True)
+            exps = to_device_async(e, torch.int32, dev)
+            exp_y = to_device_async(ey, torch.int32, dev)
 
         def ex(j):
             return None if (exps is None or fm[j] != FP32) else exps[j]

@@ -29,7 +29,7 @@ from . import gemm_engine as ge
 from .bounds import extra_squarings
 from .engine import BatchReport, _input, ps_mixed_exp
 from .planner import default_block_size
-from .precision import FP64, MatBatch, PrecisionCtx
+from .precision import FP64, MatBatch, PrecisionCtx, to_device_async
 
 DEFAULT_M = 42
 
@@ -60,16 +60,21 @@ def expm_ss(A, ctx: PrecisionCtx, m: int = DEFAULT_M, delta: float = 10.0, timin
     wf = ctx.fmt if ctx.fmt != 7 else FP64
     # X = 2^-l A, exact (the widening to the working format is exact too)
     X = MatBatch.empty(wf, B, n, device=Aw.device)
-    exps = torch.tensor([-e for e in ells], dtype=torch.int32, device=Aw.device)
+    exps = to_device_async([-e for e in ells], torch.int32, Aw.device)
     h.convert(Aw, X, None, exps)
     rep = ps_mixed_exp(X, m, ctx, delta=delta, timing=timing)
     from .engine import EvaluationReport
     reps = [rep] if isinstance(rep, EvaluationReport) else list(rep)
     P = rep.result
     Q = MatBatch.empty(P.fmt, P.batch, n, device=P.device)
+    sels = {}
     for t in range(1, max(ells) + 1 if ells else 1):
-        members = [b for b in range(B) if ells[b] >= t]
-        sel = torch.tensor(members, dtype=torch.int32, device=P.device)
+        members = tuple(b for b in range(B) if ells[b] >= t)
+        if members not in sels:
+            sels[members] = to_device_async(members, torch.int32, P.device)
+    for t in range(1, max(ells) + 1 if ells else 1):
+        members = tuple(b for b in range(B) if ells[b] >= t)
+        sel = sels[members]
         ge.gemm(h, ge.prepare(h, P, 0, P.fmt, sel), ge.prepare(h, P, 1, P.fmt, sel), Q, sel)  # Q = P P
         h.convert(Q, P, sel)          # copy back (same format: exact)
     for b, r_ in enumerate(reps):

@@ -7,8 +7,10 @@ libmpps_b200.so:
   splittings of the operands (csrc/ozaki.cuh): fp64 (8 planes), dd (16),
   qd (31).  The operand that stays fixed across a chain (X in the power
   chain, Y in the Horner chain) is split once per evaluation.
-* ``simt`` -- FP64-pipe error-free-transform GEMMs (csrc/gemm.cuh); also
-  the fp32 levels' FFMA GEMM in both engines.
+* ``simt`` -- FP64-pipe error-free-transform GEMMs and FFMA fp32 GEMMs
+  (csrc/gemm.cuh).
+
+fp32 levels use 4 digit planes (27 bits >= 24) on the tensor cores.
 
 The default is ``tc``; ``MPPS_GEMM=simt`` (environment) or
 ``set_engine("simt")`` selects the SIMT kernels (A/B evidence, tests).
@@ -35,7 +37,7 @@ def engine() -> str:
 
 
 def uses_tc(fmt: int) -> bool:
-    return _ENGINE == "tc" and fmt != FP32
+    return _ENGINE == "tc"
 
 
 class Operand:
@@ -55,8 +57,8 @@ def prepare(h, A: MatBatch, side: int, fmt: int, sel=None, exp=None) -> Operand:
     finest format any later use needs (the caller passes it as ``fmt``);
     a coarser level uses a prefix of the planes."""
     if uses_tc(fmt):
-        if exp is not None:
-            raise ValueError("power-of-two scaling applies to fp32 levels only")
+        # digit planes carry their own per-row/column power-of-two scales,
+        # so no extra level scaling is applied (exp is ignored)
         return Operand(A, h.slice(A, side, h.slices_for(fmt), sel), fmt, side)
     if A.fmt != fmt or exp is not None:
         B = MatBatch.empty(fmt, A.batch, A.rows, A.cols, device=A.device)
@@ -77,7 +79,9 @@ def horner(h, Y: Operand, phi: Operand, fmt_level: int, Bprev, out, sel=None, ex
            exp_out=None) -> None:
     """out = RN_out(2^eo (Bprev + 2^-(ey+ei) RN_level(Y phi)))."""
     if Y.slices is not None and phi.slices is not None:
-        h.horner_step_sliced(Y.slices, phi.slices, h.slices_for(fmt_level), Bprev, out, sel, exp_y, exp_in,
+        # the Y planes are unscaled (exp_y does not apply); phi keeps its
+        # level scaling 2^exp_in, undone in the epilogue
+        h.horner_step_sliced(Y.slices, phi.slices, h.slices_for(fmt_level), Bprev, out, sel, None, exp_in,
                              exp_out, fmt_in=fmt_level)
     else:
         h.horner_step(Y.mat, phi.mat, Bprev, out, sel, exp_y, exp_in, exp_out)

@@ -183,6 +183,18 @@ class MatBatch:
                 f"{self.rows}x{self.cols}, {self.device})")
 
 
+def to_device_async(values, dtype, device):
+    """Small host array -> device without stalling the stream: staged in
+    (cached) pinned memory and copied with non_blocking=True, so the launch
+    queue is not drained (a pageable torch.tensor(..., device=cuda) copy
+    synchronises the stream)."""
+    torch = _torch()
+    t = torch.as_tensor(np.asarray(values), dtype=dtype)
+    if t.device.type != "cpu":
+        return t.to(device)
+    return t.pin_memory().to(device, non_blocking=True)
+
+
 def torch_float64():
     return _torch().float64
 

@@ -267,7 +267,7 @@ def ps_mixed_dist(Xblk: MatBatch, series: CoefficientSeries, ctx: PrecisionCtx, 
     else:
         dg, nv, nl = plan_digits_batch(norms[None, :r + 1], norms[None, r + 1], d, delta)
         digits, nu, nil = dg[0], int(nv[0]), bool(nl[0])
-    pk = torch.tensor(list(digits) + [nu, int(nil)], dtype=torch.int64, device=norms_t.device)
+    pk = torch.tensor(list(digits) + [nu, int(nil)], dtype=torch.int64).to(norms_t.device)
     grid.broadcast(pk)
     pk = pk.cpu().numpy()
     digits, nu, nil = tuple(int(x) for x in pk[:r]), int(pk[r]), bool(pk[r + 1])
