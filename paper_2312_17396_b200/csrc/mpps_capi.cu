@@ -773,7 +773,7 @@ static int launch_oz_tma(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
   }
   dim3 grid((a.N + NT - 1) / NT, (a.M + oz::kTileM - 1) / oz::kTileM, nb);
   if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
-  oz::oz_gemm_tma_kernel<S, NT, FO, MODE><<<grid, oz::kThreadsOz, smem, h->stream>>>(a);
+  oz::oz_gemm_tma_kernel<S, NT, FO, MODE><<<grid, oz::kThreadsEpi, smem, h->stream>>>(a);
   return after_launch(h, "oz_gemm_tma_kernel");
 }
 
@@ -789,25 +789,54 @@ static int dispatch_oz_tma(mpps_handle *h, int S, int fo, int mode, const oz::Oz
 
 static int dispatch_oz(mpps_handle *h, int S, int fo, int mode, const oz::OzArgs &a, int nb);
 
-static bool use_tma() {
+template <int S, int NT, int FO, int MODE>
+static int launch_oz_ring(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
+  constexpr size_t smem = oz::OzRing<S, NT>::SMEM;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_ring_kernel<S, NT, FO, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz ring attr: %s", cudaGetErrorString(e));
+    configured = true;
+  }
+  dim3 grid((a.N + NT - 1) / NT, (a.M + oz::kTileM - 1) / oz::kTileM, nb);
+  if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
+  oz::oz_gemm_ring_kernel<S, NT, FO, MODE><<<grid, oz::kThreadsEpi, smem, h->stream>>>(a);
+  return after_launch(h, "oz_gemm_ring_kernel");
+}
+
+static int dispatch_oz_ring(mpps_handle *h, int S, int fo, int mode, const oz::OzTmaArgs &a, int nb) {
+#define OZ(SS, NT, FF, MM) if (S == SS && fo == FF && mode == MM) return launch_oz_ring<SS, NT, FF, MM>(h, a, nb);
+  OZ(4, 32, F32, 0) OZ(4, 32, F32, 1) OZ(4, 32, F64, 1) OZ(4, 32, DD, 1) OZ(4, 32, QD, 1)
+  OZ(8, 32, F64, 0) OZ(8, 32, F64, 1) OZ(8, 32, DD, 1) OZ(8, 32, QD, 1)
+  OZ(16, 32, DD, 0) OZ(16, 32, DD, 1) OZ(16, 32, QD, 1)
+  OZ(31, 16, QD, 0) OZ(31, 16, QD, 1)
+#undef OZ
+  return set_err(h, MPPS_EFMT, "tensor-core GEMM: no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
+}
+
+static int oz_mode() {   // 0 cp.async, 1 TMA two-stage, 2 TMA streamed planes, 3 (default) streamed for qd only
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("MPPS_OZ_TMA");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 3;
   }
-  return v == 1;
+  return v;
 }
+
 
 static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, int S, int fo, int mode,
                   const oz::OzArgs &a, int nb) {
-  if (!use_tma()) return dispatch_oz(h, S, fo, mode, a, nb);
+  if (oz_mode() == 0) return dispatch_oz(h, S, fo, mode, a, nb);
   oz::OzTmaArgs t;
   memset(&t, 0, sizeof(t));
   const int NT = (S > 16) ? 16 : 32;
+  const bool ring = oz_mode() == 2 || (oz_mode() == 3 && S > 16);
+  const int abox = ring ? (S < 4 ? S : 4) : S;
   int rc;
-  if ((rc = make_slice_map(h, &t.mapA, A, oz::kTileM, S)) || (rc = make_slice_map(h, &t.mapB, B, NT, S))) return rc;
+  if ((rc = make_slice_map(h, &t.mapA, A, oz::kTileM, abox)) || (rc = make_slice_map(h, &t.mapB, B, NT, S))) return rc;
   t.A = a.A; t.B = a.B; t.M = a.M; t.N = a.N; t.K = a.K; t.S = a.S; t.C = a.C; t.sel = a.sel; t.epi = a.epi;
-  return dispatch_oz_tma(h, S, fo, mode, t, nb);
+  return ring ? dispatch_oz_ring(h, S, fo, mode, t, nb) : dispatch_oz_tma(h, S, fo, mode, t, nb);
 }
 
 template <int S, int NT, int FO, int MODE>

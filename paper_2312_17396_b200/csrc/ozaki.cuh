@@ -30,6 +30,7 @@ namespace oz {
 constexpr int kTileM = 128;
 constexpr int kKStep = 32;      // int8 MMA K per instruction (32 bytes)
 constexpr int kThreadsOz = 128;
+constexpr int kThreadsEpi = 256;   // TMA/ring kernels: 8 warps (producer, MMA issuer, 8 epilogue)
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -476,6 +477,108 @@ __global__ void __launch_bounds__(kThreadsOz, 1) oz_gemm_kernel(const OzArgs arg
   if (warp == 0) tmem_dealloc<TCOLS>(tmem);
 }
 
+// ------------------------------------------------------ shared epilogue
+// 2^e as a double (exact); e within the normal range.
+__device__ __forceinline__ double pow2i(int e) {
+  if (e >= -1022 && e <= 1023) return __longlong_as_double((long long)(e + 1023) << 52);
+  return ldexp(1.0, e);
+}
+__host__ __device__ constexpr double pow2c(int e) {  // compile-time 2^e
+  double r = 1.0;
+  if (e >= 0) for (int i = 0; i < e; ++i) r *= 2.0;
+  else for (int i = 0; i < -e; ++i) r *= 0.5;
+  return r;
+}
+
+// sum_d D_d 2^-(12+7d) for S <= 16 as a dd (groups of three digits are
+// exact int64 -> double; group weights are compile-time constants).
+template <int S>
+__device__ __forceinline__ mp::dd combine_dd(const int32_t *D) {
+  mp::dd acc = mp::dd_make(0.0, 0.0);
+#pragma unroll
+  for (int g = 0; g < (S + 2) / 3; ++g) {
+    const int d0 = 3 * g;
+    long long G = (long long)D[d0] << 14;
+    if (d0 + 1 < S) G += (long long)D[d0 + 1] << 7;
+    if (d0 + 2 < S) G += (long long)D[d0 + 2];
+    const double gv = (double)G * pow2c(-(12 + 7 * (d0 + 2)));  // exact
+    if (g == 0) acc = mp::dd_make(gv, 0.0);
+    else acc = mp::dd_add_d(acc, gv);
+  }
+  return acc;
+}
+
+// Drain the S diagonal accumulators of this thread's TMEM lane for columns
+// [c_begin, c_end) and run the store / fused Horner epilogue.
+template <int S, int NT, int FO, int MODE, typename Args>
+__device__ __forceinline__ void oz_epilogue(const Args &args, uint32_t tmem, int quarter, int c_begin, int c_end,
+                                            int b, int m0, int n0, int lane) {
+  const int row = m0 + quarter * 32 + lane;
+  const int ea = args.A.exps[(long long)b * args.A.rpad + row];
+  const MatRef &C = args.C;
+  int ey = 0, ei = 0, eo = 0;
+  if constexpr (MODE == 1) {
+    if (args.epi.exp_y) ey = args.epi.exp_y[b];
+    if (args.epi.exp_in) ei = args.epi.exp_in[b];
+    if (args.epi.exp_out) eo = args.epi.exp_out[b];
+  }
+  const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+  constexpr int CW = (S > 16) ? 4 : 8;
+  for (int c0 = c_begin; c0 < c_end; c0 += CW) {
+    int32_t D[S][CW];
+#pragma unroll
+    for (int d = 0; d < S; ++d) {
+      if constexpr (CW == 8) tmem_ld8(lane_base + (uint32_t)(d * NT + c0), D[d]);
+      else tmem_ld4(lane_base + (uint32_t)(d * NT + c0), D[d]);
+    }
+    tmem_ld_wait();
+#pragma unroll
+    for (int jj = 0; jj < CW; ++jj) {
+      const int col = n0 + c0 + jj;
+      if (row >= args.M || col >= args.N) continue;
+      int32_t Dj[S];
+#pragma unroll
+      for (int d = 0; d < S; ++d) Dj[d] = D[d][jj];
+      const int eb = args.B.exps[(long long)b * args.B.rpad + col];
+      const long long off = (long long)b * C.bstride + (long long)row * C.ld + col;
+      if constexpr (S <= 16 && FO != QD) {
+        // dd-width epilogue (fp32 / fp64 / dd outputs)
+        mp::dd v = combine_dd<S>(Dj);
+        const double sc = pow2i(ea + eb - (MODE == 1 ? (ey + ei) : 0));
+        v = mp::dd_make(v.hi * sc, v.lo * sc);
+        if constexpr (MODE == 1) {
+          const MatRef &Bp = args.epi.Bprev;
+          const double *bp = (const double *)Bp.data + (long long)b * Bp.bstride + (long long)row * Bp.ld + col;
+          const mp::dd bv = mp::dd_make(bp[0], Bp.words > 1 ? bp[Bp.plane] : 0.0);
+          v = mp::dd_add(bv, v);
+        }
+        if constexpr (FO == DD) {
+          if (eo) { const double so = pow2i(eo); v = mp::dd_make(v.hi * so, v.lo * so); }
+          double *p = (double *)C.data + off;
+          p[0] = v.hi;
+          p[C.plane] = v.lo;
+        } else if constexpr (FO == F64) {
+          ((double *)C.data)[off] = eo ? v.hi * pow2i(eo) : v.hi;
+        } else {
+          if (eo) { const double so = pow2i(eo); v = mp::dd_make(v.hi * so, v.lo * so); }
+          ((float *)C.data)[off] = mp::dd_to_float(v.hi, v.lo);
+        }
+      } else {
+        mp::qd v = combine_diagonals<S>(Dj);
+        v = mp::qd_ldexp(v, ea + eb);
+        if constexpr (MODE == 0) {
+          store_fmt<FO>(C, off, v, 0);
+        } else {
+          const int sh = -(ey + ei);
+          if (sh) v = mp::qd_ldexp(v, sh);
+          mp::qd bv = load_qd(args.epi.Bprev, (long long)b * args.epi.Bprev.bstride + (long long)row * args.epi.Bprev.ld + col);
+          store_fmt<FO>(C, off, horner_add<FO>(bv, v), eo);
+        }
+      }
+    }
+  }
+}
+
 // ------------------------------------------------- TMA-fed pipeline
 // Digit planes [S][batch][rpad][kpad] viewed by TMA as a 3-D tensor
 // (k, row, slice); one box = 32 B of K x R rows x all S planes, written
@@ -500,7 +603,7 @@ template <int S, int NT>
 __host__ __device__ constexpr size_t oz_tma_smem_bytes() { return oz_tma_stages<S, NT>() * oz_stage_bytes<S, NT>() + 2048; }
 
 template <int S, int NT, int FO, int MODE>
-__global__ void __launch_bounds__(kThreadsOz, 1) oz_gemm_tma_kernel(const __grid_constant__ OzTmaArgs args) {
+__global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_tma_kernel(const __grid_constant__ OzTmaArgs args) {
   constexpr int STAGES = oz_tma_stages<S, NT>();
   static_assert(STAGES >= 1, "stage does not fit");
   constexpr uint32_t STAGE = (uint32_t)oz_stage_bytes<S, NT>();
@@ -578,45 +681,133 @@ __global__ void __launch_bounds__(kThreadsOz, 1) oz_gemm_tma_kernel(const __grid
   fence_after();
 
   // ---------------------------------------------------------- epilogue
-  const int row = m0 + warp * 32 + lane;
-  const int ea = args.A.exps[(long long)b * args.A.rpad + m0 + warp * 32 + lane];
-  const MatRef &C = args.C;
-  int ey = 0, ei = 0, eo = 0;
-  if constexpr (MODE == 1) {
-    if (args.epi.exp_y) ey = args.epi.exp_y[b];
-    if (args.epi.exp_in) ei = args.epi.exp_in[b];
-    if (args.epi.exp_out) eo = args.epi.exp_out[b];
+  // warps w and w+4 share TMEM lane quarter w % 4 and split the columns
+  {
+    const int quarter = warp & 3, half = warp >> 2;
+    constexpr int CW = (S > 16) ? 4 : 8;
+    constexpr int HALF = ((NT / 2 + CW - 1) / CW) * CW;
+    oz_epilogue<S, NT, FO, MODE>(args, tmem, quarter, half ? HALF : 0, half ? NT : HALF, b, m0, n0, lane);
   }
-  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-  constexpr int CW = (S > 16) ? 4 : 8;
-  for (int c0 = 0; c0 < NT; c0 += CW) {
-    int32_t D[S][CW];
-#pragma unroll
-    for (int d = 0; d < S; ++d) {
-      if constexpr (CW == 8) tmem_ld8(lane_base + (uint32_t)(d * NT + c0), D[d]);
-      else tmem_ld4(lane_base + (uint32_t)(d * NT + c0), D[d]);
-    }
-    tmem_ld_wait();
-#pragma unroll
-    for (int jj = 0; jj < CW; ++jj) {
-      const int col = n0 + c0 + jj;
-      if (row >= args.M || col >= args.N) continue;
-      int32_t Dj[S];
-#pragma unroll
-      for (int d = 0; d < S; ++d) Dj[d] = D[d][jj];
-      mp::qd v = combine_diagonals<S>(Dj);
-      const int eb = args.B.exps[(long long)b * args.B.rpad + col];
-      v = mp::qd_ldexp(v, ea + eb);
-      const long long off = (long long)b * C.bstride + (long long)row * C.ld + col;
-      if constexpr (MODE == 0) {
-        store_fmt<FO>(C, off, v, 0);
-      } else {
-        const int sh = -(ey + ei);
-        if (sh) v = mp::qd_ldexp(v, sh);
-        mp::qd bv = load_qd(args.epi.Bprev, (long long)b * args.epi.Bprev.bstride + (long long)row * args.epi.Bprev.ld + col);
-        store_fmt<FO>(C, off, horner_add<FO>(bv, v), eo);
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<TCOLS>(tmem);
+}
+
+// ----------------------------------------- TMA pipeline, streamed A planes
+// B (all S planes of one 32-byte K step, 16 KB for dd) sits in a 2-deep
+// ring; A planes stream through a deeper ring in groups of SG planes
+// (16 KB), so many loads are in flight while the wide MMAs of earlier
+// groups run.  Same MMA sequence and epilogue as oz_gemm_tma_kernel.
+template <int S, int NT>
+struct OzRing {
+  static constexpr int SG = S < 4 ? S : 4;                       // planes per A stage
+  static constexpr int NG = (S + SG - 1) / SG;                   // A stages per K step
+  static constexpr uint32_t A_BYTES = SG * kTileM * kKStep;      // 16 KB
+  static constexpr uint32_t B_BYTES = S * NT * kKStep;
+  static constexpr int NBS = 2;
+  static constexpr int NAS = (int)((160u * 1024u - NBS * ((B_BYTES + 1023) / 1024 * 1024)) / A_BYTES) > 8
+                                 ? 8
+                                 : (int)((160u * 1024u - NBS * ((B_BYTES + 1023) / 1024 * 1024)) / A_BYTES);
+  static constexpr uint32_t B_STRIDE = (B_BYTES + 1023) / 1024 * 1024;
+  static constexpr size_t SMEM = (size_t)NBS * B_STRIDE + (size_t)NAS * A_BYTES + 2048;
+};
+
+template <int S, int NT, int FO, int MODE>
+__global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_ring_kernel(const __grid_constant__ OzTmaArgs args) {
+  using R = OzRing<S, NT>;
+  constexpr uint32_t A_SLICE = kTileM * kKStep;
+  constexpr uint32_t B_SLICE = NT * kKStep;
+  constexpr int TCOLS = tmem_cols_for(S * NT);
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t *bring = smem;
+  uint8_t *aring = smem + R::NBS * R::B_STRIDE;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(aring + R::NAS * R::A_BYTES);
+  uint64_t *b_full = bar, *b_empty = bar + R::NBS;
+  uint64_t *a_full = bar + 2 * R::NBS, *a_empty = a_full + R::NAS;
+  uint64_t *done = a_empty + R::NAS;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int bz = blockIdx.z;
+  const int b = args.sel ? args.sel[bz] : bz;
+  const int m0 = blockIdx.y * kTileM, n0 = blockIdx.x * NT;
+  const int ksteps = args.A.kpad / kKStep;
+
+  if (warp == 0) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
+  if (tid == 32) {
+    for (int i = 0; i < R::NBS; ++i) { mbar_init(smem_u32(&b_full[i]), 1); mbar_init(smem_u32(&b_empty[i]), 1); }
+    for (int i = 0; i < R::NAS; ++i) { mbar_init(smem_u32(&a_full[i]), 1); mbar_init(smem_u32(&a_empty[i]), 1); }
+    mbar_init(smem_u32(done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int rowA = b * args.A.rpad + m0, rowB = b * args.B.rpad + n0;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer: B step, then the A plane groups of that step
+    int ai = 0;
+    for (int kb = 0; kb < ksteps; ++kb) {
+      const int bst = kb % R::NBS;
+      if (kb >= R::NBS) mbar_wait(smem_u32(&b_empty[bst]), ((kb / R::NBS) - 1) & 1);
+      mbar_expect_tx(smem_u32(&b_full[bst]), R::B_BYTES);
+      tma_load_3d(smem_u32(bring + bst * R::B_STRIDE), &args.mapB, kb * kKStep, rowB, 0, smem_u32(&b_full[bst]));
+      for (int g = 0; g < R::NG; ++g, ++ai) {
+        const int ast = ai % R::NAS;
+        if (ai >= R::NAS) mbar_wait(smem_u32(&a_empty[ast]), ((ai / R::NAS) - 1) & 1);
+        mbar_expect_tx(smem_u32(&a_full[ast]), R::A_BYTES);
+        tma_load_3d(smem_u32(aring + ast * R::A_BYTES), &args.mapA, kb * kKStep, rowA, g * R::SG,
+                    smem_u32(&a_full[ast]));
       }
     }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer
+    int ai = 0;
+    for (int kb = 0; kb < ksteps; ++kb) {
+      const int bst = kb % R::NBS;
+      mbar_wait(smem_u32(&b_full[bst]), (kb / R::NBS) & 1);
+      const uint32_t sb = smem_u32(bring + bst * R::B_STRIDE);
+      for (int g = 0; g < R::NG; ++g, ++ai) {
+        const int ast = ai % R::NAS;
+        mbar_wait(smem_u32(&a_full[ast]), (ai / R::NAS) & 1);
+        fence_after();
+        const uint32_t sa = smem_u32(aring + ast * R::A_BYTES);
+#pragma unroll 1
+        for (int q = 0; q < R::SG; ++q) {
+          const int s = g * R::SG + q;
+          if (s >= S) break;
+          const uint64_t ad = umma_desc(sa + q * A_SLICE, 16, 256, 6);
+          int ncols = (S - s) * NT;
+          int t0 = 0;
+          while (ncols > 0) {
+            const int nn = ncols > 256 ? 256 : ncols;
+            const uint64_t bd = umma_desc(sb + t0 * B_SLICE, 16, 256, 6);
+            mma_i8(tmem + (uint32_t)((s + t0) * NT), ad, bd, idesc_i8(kTileM, nn), (kb > 0 || s > 0) ? 1u : 0u);
+            t0 += nn / NT;
+            ncols -= nn;
+          }
+        }
+        mma_commit(smem_u32(&a_empty[ast]));
+      }
+      mma_commit(smem_u32(&b_empty[bst]));
+    }
+    mma_commit(smem_u32(done));
+  }
+  __syncwarp();
+  mbar_wait(smem_u32(done), 0);
+  fence_after();
+
+  // ---------------------------------------------------------- epilogue
+  // warps w and w+4 share TMEM lane quarter w % 4 and split the columns
+  {
+    const int quarter = warp & 3, half = warp >> 2;
+    constexpr int CW = (S > 16) ? 4 : 8;
+    constexpr int HALF = ((NT / 2 + CW - 1) / CW) * CW;
+    oz_epilogue<S, NT, FO, MODE>(args, tmem, quarter, half ? HALF : 0, half ? NT : HALF, b, m0, n0, lane);
   }
   fence_before();
   __syncthreads();
