@@ -376,8 +376,8 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     if clocks:
         clocks.start()
-    h.probe = None if args.no_probe else {}
-    l0 = h.launches
+    from paper_2312_17396_b200 import graphs as _graphs
+    l0 = _lib.total_launches()
     total = 0.0
     for _ in range(args.steps):
         flush.zero_()  # 256 MiB write between steps: L2 (126 MB) flushed
@@ -389,10 +389,29 @@ def run_ours(args, rank, world, local_rank):
         b.synchronize()
         total += a.elapsed_time(b) * 1e-3
     barrier()
-    launches = (h.launches - l0) / args.steps
-    probe = h.probe
-    h.probe = None
+    if _graphs.enabled() and _graphs.last_launches():
+        launches = float(_graphs.last_launches())      # kernels per graphed evaluation
+    else:
+        launches = (_lib.total_launches() - l0) / args.steps
     clk = clocks.stop() if clocks else None
+
+    # ---- roofline pass: the same K steps eagerly (graphs off) with a CUDA
+    # event pair around every GEMM launch on the launching stream ----
+    probe = None
+    if not args.no_probe:
+        was = _graphs.enabled()
+        _graphs.set_enabled(False)
+        h = _lib.handle_for()
+        wl.step(wl.Xd)
+        torch.cuda.synchronize()
+        h.probe = {}
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            wl.step(wl.Xd)
+        torch.cuda.synchronize()
+        probe, h.probe = h.probe, None
+        _graphs.set_enabled(was)
 
     # ---- end-to-end through the public API with host buffers ----
     outs = None
@@ -437,6 +456,7 @@ def run_ours(args, rank, world, local_rank):
         by_key[("none", 31, 31, 1, 1, 1, 1)] = (1, 1.0)
     dom = max(by_key.items(), key=lambda kv: kv[1][1])
     (kind, fin, fout, M, N, K, nb), (cnt, sec) = dom
+    eager_step = None
     fname = names[fin]
     logical = 2.0 * M * N * K * nb / (sec / cnt) / 1e12       # logical TFLOP/s of the format
     step_time = total / args.steps
@@ -466,7 +486,9 @@ def run_ours(args, rank, world, local_rank):
                                "MEASURED_PEAKS.json holds only HBM and bf16"}
     roof.update({"kernel": f"{kind} {fname}->{names[fout]} {M}x{N}x{K} x{nb}", "traffic": None,
                  "share_of_step": sec / args.steps / step_time, "launches_per_step": cnt / args.steps,
-                 "eval_frac": t_ideal / step_time})
+                 "eval_frac": t_ideal / step_time,
+                 "measured_in": "a second timed pass of the same K steps run eagerly (the value pass "
+                                "replays CUDA graphs, whose kernels cannot be bracketed by events)"})
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * step_time, "higher_is_better": True,

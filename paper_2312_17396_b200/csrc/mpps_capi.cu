@@ -430,6 +430,21 @@ int mpps_create(int device, void *stream, mpps_handle **out) {
     delete h;
     return MPPS_ECUDA;
   }
+  // keep stream-ordered scratch (norm partials) in the device pool across
+  // synchronisations instead of returning it to the OS after every sync.
+  // Done once per device and never while the stream is being captured into
+  // a CUDA graph (pool attribute calls would invalidate the capture).
+  static bool pool_done[64] = {false};
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (h->stream) cudaStreamIsCapturing(h->stream, &cap);
+  if (device >= 0 && device < 64 && !pool_done[device] && cap == cudaStreamCaptureStatusNone) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      unsigned long long thr = ~0ULL;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_done[device] = true;
+  }
   *out = h;
   return MPPS_OK;
 }

@@ -225,6 +225,22 @@ def _exp_for(norm: float) -> int:
     return -int(round(math.log2(norm)))
 
 
+_MASKS: Dict[tuple, object] = {}
+
+
+def _level_mask(fm, r, dev):
+    """Device int32 mask (r+2,) of the fp32 levels of a format tuple (cached,
+    so no host->device copy sits on the post-planner critical path)."""
+    key = (fm, r, str(dev))
+    t = _MASKS.get(key)
+    if t is None:
+        torch = _torch()
+        t = torch.tensor([1 if (0 < j <= r and fm[j] == FP32) else 0 for j in range(r + 2)],
+                         dtype=torch.int32, device=dev)
+        _MASKS[key] = t
+    return t
+
+
 def _exps_for(norms: np.ndarray) -> np.ndarray:
     """Vectorised _exp_for."""
     v = np.asarray(norms, dtype=np.float64)
@@ -265,6 +281,7 @@ class _Prepared:
     blocks: List[MatBatch]
     norms: np.ndarray          # (B, r+2) float64: ||B_0..B_r||, ||Y||
     coeffs: np.ndarray         # (m+1, 4) words at the working precision
+    norms_dev: object = None   # the same norms on the device (level scalings)
 
 
 def _form_powers(h, Xt, wf: int, s: int, timer: _Buckets, x_is_working: Optional[MatBatch] = None):
@@ -290,7 +307,7 @@ def _form_powers(h, Xt, wf: int, s: int, timer: _Buckets, x_is_working: Optional
 
 
 def _assemble(h, powers: List[MatBatch], series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: int,
-              timer: _Buckets) -> _Prepared:
+              timer: _Buckets, sync: bool = True) -> _Prepared:
     """assemble_block for every block + one_norm (engine.py:127-138,
     467-468), then the one host sync for the planner's norms."""
     torch = _torch()
@@ -311,21 +328,48 @@ def _assemble(h, powers: List[MatBatch], series: CoefficientSeries, ctx: Precisi
     norms = torch.empty((B, r + 2), dtype=torch.float64, device=dev)
     h.assemble_blocks(powers, m, coeffs, blocks, norms)
     timer.stop()
+    if not sync:
+        return _Prepared(wf, s, r, m, powers, blocks, None, cw, norms)
     timer.start("norm_estimation")
     norms_h = norms.cpu().numpy()   # the one host sync of the pipeline
     timer.stop()
-    return _Prepared(wf, s, r, m, powers, blocks, norms_h, cw)
+    return _Prepared(wf, s, r, m, powers, blocks, norms_h, cw, norms)
 
 
 def _prepare(h, Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: int,
-             timer: _Buckets, x_is_working: Optional[MatBatch] = None) -> _Prepared:
+             timer: _Buckets, x_is_working: Optional[MatBatch] = None, sync: bool = True) -> _Prepared:
     """eval_b0_and_power + assemble_block + one_norm (engine.py:141-154,
     127-138, 467-468) for the whole batch."""
     powers = _form_powers(h, Xt, wf, s, timer, x_is_working)
-    return _assemble(h, powers, series, ctx, wf, s, timer)
+    return _assemble(h, powers, series, ctx, wf, s, timer, sync)
 
 
-def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buckets) -> MatBatch:
+def _structure(prep: _Prepared, digits: np.ndarray, nil: np.ndarray):
+    """Batch members grouped by level-format tuple, plus the nilpotent ones."""
+    groups: Dict[Tuple[int, ...], List[int]] = {}
+    nil_idx = []
+    for b in range(len(digits)):
+        if nil[b]:
+            nil_idx.append(b)
+        else:
+            fm = (prep.wf,) + formats_of_digits(tuple(int(x) for x in digits[b]))
+            groups.setdefault(fm, []).append(b)
+    return tuple((fm, tuple(mem)) for fm, mem in groups.items()), tuple(nil_idx)
+
+
+def _selections(structure, dev):
+    """Device index tensors of a structure (created eagerly, outside any
+    graph capture)."""
+    torch = _torch()
+    groups, nil_idx = structure
+    whole = len(groups) == 1 and not nil_idx
+    sels = {fm: (None if whole else to_device_async(mem, torch.int32, dev)) for fm, mem in groups}
+    sels["nil"] = to_device_async(nil_idx, torch.int64, dev) if nil_idx else None
+    return sels
+
+
+def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buckets,
+            structure=None, sels=None) -> MatBatch:
     """horner_mixed (engine.py:243-252) for every matrix of the batch,
     grouped by level-format tuple (one launch per level per group)."""
     torch = _torch()
@@ -335,35 +379,44 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
     B, n, dev = Y.batch, Y.rows, Y.device
     result = MatBatch.empty(wf, B, n, device=dev)
     timer.start("mixed_horner")
-    groups: Dict[Tuple[int, ...], List[int]] = {}
-    nil_idx = []
-    for b in range(B):
-        if nil[b]:
-            nil_idx.append(b)
-        else:
-            fm = (wf,) + formats_of_digits(tuple(int(x) for x in digits[b]))
-            groups.setdefault(fm, []).append(b)
+    if structure is None:
+        structure = _structure(prep, digits, nil)
+    if sels is None:
+        sels = _selections(structure, dev)
+    group_list, nil_idx = structure
+    groups = {fm: list(mem) for fm, mem in group_list}
     if nil_idx:
         # p = B_0 (engine.py:378-379, 473-474)
-        ii = to_device_async(nil_idx, torch.int64, dev)
+        ii = sels["nil"]
         result.data[:, ii] = blocks[0].data[:, ii]
     ws = _Workspace(B, n, dev)
     scalar_top = (m % s == 0)
     bm_words = prep.coeffs[m]
-    whole = len(groups) == 1 and not nil_idx
     for fm, members in groups.items():
-        sel = None if whole else to_device_async(members, torch.int32, dev)
+        sel = sels[fm]
         exps = exp_y = None
         if FP32 in fm:
-            e = np.zeros((r + 1, B), dtype=np.int32)
-            ey = np.zeros(B, dtype=np.int32)
-            idx = np.asarray(members)
-            for j in range(1, r + 1):
-                if fm[j] == FP32:
-                    e[j, idx] = _exps_for(prep.norms[idx, j])
-            ey[idx] = _exps_for(prep.norms[idx, r + 1])
-            exps = to_device_async(e, torch.int32, dev)
-            exp_y = to_device_async(ey, torch.int32, dev)
+            # exact power-of-two level scalings, computed on the device from
+            # the device copy of the norms (no host round trip on the
+            # critical path): e = -round(log2 ||B_j||) for fp32 levels
+            if prep.norms_dev is not None:
+                nd = prep.norms_dev
+                ok = torch.isfinite(nd) & (nd > 0)
+                e_all = torch.where(ok, -torch.round(torch.log2(torch.where(ok, nd, torch.ones_like(nd)))),
+                                    torch.zeros_like(nd)).to(torch.int32)       # (B, r+2)
+                lvl = _level_mask(fm, r, dev)
+                exps = (e_all * lvl).t().contiguous()                              # (r+2, B)
+                exp_y = e_all[:, r + 1].contiguous()
+            else:
+                e = np.zeros((r + 1, B), dtype=np.int32)
+                ey = np.zeros(B, dtype=np.int32)
+                idx = np.asarray(members)
+                for j in range(1, r + 1):
+                    if fm[j] == FP32:
+                        e[j, idx] = _exps_for(prep.norms[idx, j])
+                ey[idx] = _exps_for(prep.norms[idx, r + 1])
+                exps = to_device_async(e, torch.int32, dev)
+                exp_y = to_device_async(ey, torch.int32, dev)
 
         def ex(j):
             return None if (exps is None or fm[j] != FP32) else exps[j]
@@ -449,6 +502,43 @@ def _plan_fn(norms_row, r, ctx, delta, s, apply_switch, fix_params):
 
 
 # ------------------------------------------------------------ evaluators
+def _graphed(Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: int, kind: str, delta: float,
+             apply_switch: bool, timer: _Buckets):
+    """The batched pipeline through cached CUDA graphs (graphs.py); returns
+    (prep, digits, nu, nil, result) or None (eager path)."""
+    from . import graphs
+    if Xt is None or not graphs.enabled():
+        return None
+    d = ctx.decimal_digits
+    key = (tuple(Xt.shape), str(Xt.device if Xt.is_cuda else "host"), series.coeffs, d, wf, s, kind, delta,
+           apply_switch, ge.engine())
+
+    def build_pre(xstatic, capture):
+        return _prepare(_lib.handle_for(), xstatic, series, ctx, wf, s, _Buckets(False), None, sync=False)
+
+    def run_post(prep, norms):
+        r = prep.r
+        if kind == "fixed":
+            digits = np.full((norms.shape[0], r), d, dtype=np.int64)
+            nu = np.full(norms.shape[0], r + 1, dtype=np.int64)
+            nil = np.zeros(norms.shape[0], dtype=bool)
+        else:
+            digits, nu, nil = plan_digits_batch(norms[:, :r + 1], norms[:, r + 1], d, delta, apply_switch)
+        structure = _structure(prep, digits, nil)
+        sels = _selections(structure, prep.norms_dev.device)
+
+        def post_fn(p):
+            return _horner(_lib.handle_for(), p, digits, nil, _Buckets(False), structure, sels)
+        return structure, post_fn, (digits, nu, nil)
+
+    out = graphs.run(key, Xt, build_pre, run_post, timer)
+    if out is None:
+        return None
+    prep, norms, result, info = out
+    digits, nu, nil = info
+    return prep, digits, nu, nil, result
+
+
 def ps_fixed(X, series: CoefficientSeries, ctx: PrecisionCtx, with_bound: bool = False,
              timing: bool = True):
     """Fixed-precision PS with s = ceil(sqrt(m)) (engine.py:304-345)."""
@@ -472,10 +562,15 @@ def ps_fixed(X, series: CoefficientSeries, ctx: PrecisionCtx, with_bound: bool =
                               tau_seq=(), norm_bs=(MPF(rn(c0, 54), 54),), norm_y=MPF(0, 64))
         return _reports(res, [lambda: plan] * B, None, "fixed", {}, False, single)
     s = default_block_size(m)
-    prep = _prepare(h, Xt, series, ctx, wf, s, timer, Xw)
-    r = prep.r
-    digits = np.full((B, r), d, dtype=np.int64)
-    result = _horner(h, prep, digits, np.zeros(B, dtype=bool), timer)
+    g = _graphed(Xt, series, ctx, wf, s, "fixed", 10.0, True, timer) if Xw is None else None
+    if g is not None:
+        prep, digits, _, _, result = g
+        r = prep.r
+    else:
+        prep = _prepare(h, Xt, series, ctx, wf, s, timer, Xw)
+        r = prep.r
+        digits = np.full((B, r), d, dtype=np.int64)
+        result = _horner(h, prep, digits, np.zeros(B, dtype=bool), timer)
     fns = []
     for b in range(B):
         nb = tuple(float(x) for x in prep.norms[b, :r + 1])
@@ -496,6 +591,9 @@ def ps_mixed_general(X, series: CoefficientSeries, ctx: PrecisionCtx, delta: flo
     timer = _Buckets(timing)
     wf = _working_format(ctx)
     s = default_block_size(m)
+    g = _graphed(Xt, series, ctx, wf, s, "mixed", delta, True, timer) if Xw is None else None
+    if g is not None:
+        return _graphed_reports(g, ctx, delta, True, True, with_bound, single, timer)
     prep = _prepare(h, Xt, series, ctx, wf, s, timer, Xw)
     return _mixed_tail(h, prep, ctx, delta, True, True, with_bound, single, timer)
 
@@ -510,6 +608,7 @@ def _mixed_tail(h, prep, ctx, delta, apply_switch, fix_params, with_bound, singl
     timer.stop()
     result = _horner(h, prep, digits, nil, timer)
     B = prep.norms.shape[0]
+    # built after the Horner launches so the GPU is not kept waiting
     fns = [_plan_fn(prep.norms[b], r, ctx, delta, s, apply_switch, fix_params) for b in range(B)]
     executed = [(tuple(int(x) for x in digits[b]), int(nu[b])) for b in range(B)]
     return _reports(result, fns, executed, "mixed", timer.seconds(), with_bound, single)
@@ -547,8 +646,20 @@ def ps_mixed_exp(X, m: int, ctx: PrecisionCtx, fix_params: bool = True, delta: f
     h = _lib.handle_for()
     timer = _Buckets(timing)
     wf = _working_format(ctx)
+    g = _graphed(Xt, series, ctx, wf, s, "mixed", delta, True, timer) if Xw is None else None
+    if g is not None:
+        return _graphed_reports(g, ctx, delta, True, fix_params, with_bound, single, timer)
     prep = _prepare(h, Xt, series, ctx, wf, s, timer, Xw)
     return _mixed_tail(h, prep, ctx, delta, True, fix_params, with_bound, single, timer)
+
+
+def _graphed_reports(g, ctx, delta, apply_switch, fix_params, with_bound, single, timer):
+    prep, digits, nu, nil, result = g
+    r, s = prep.r, prep.s
+    B = prep.norms.shape[0]
+    fns = [_plan_fn(prep.norms[b], r, ctx, delta, s, apply_switch, fix_params) for b in range(B)]
+    executed = [(tuple(int(x) for x in digits[b]), int(nu[b])) for b in range(B)]
+    return _reports(result, fns, executed, "mixed", timer.seconds(), with_bound, single)
 
 
 def _one_norms(Xt, Xw) -> np.ndarray:

@@ -1,0 +1,141 @@
+"""CUDA-graph execution of the batched PS pipeline.
+
+An evaluation has exactly one host synchronisation (the planner needs the
+block norms, engine.py:467-472).  The device work on either side of it is
+captured once per problem shape into two CUDA graphs and replayed:
+
+  pre graph   X -> working format, digit-plane splits, power chain,
+              fused block assembly + column norms, norms -> pinned host buffer
+  (host)      certified batched planner (planner.plan_digits_batch)
+  post graph  Horner chain for this plan structure (one graph per distinct
+              (level formats, members) grouping; cfg2's 64 matrices share one)
+
+Buffers live in the graphs' private memory pool and are reused across
+replays; inputs are copied into a static buffer and the result is cloned
+out, so every call returns independent tensors.  Any capture failure turns
+the graph path off for that shape (eager execution, same kernels).
+"""
+
+from __future__ import annotations
+
+import os
+from typing import Dict, Optional, Tuple
+
+import numpy as np
+
+from .precision import FP64, MatBatch
+
+_ENABLED = os.environ.get("MPPS_GRAPHS", "1") != "0"
+_CACHE: Dict[tuple, "_ShapeGraphs"] = {}
+_FAILED = set()
+
+
+def enabled() -> bool:
+    return _ENABLED
+
+
+def set_enabled(flag: bool) -> None:
+    global _ENABLED
+    _ENABLED = bool(flag)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class _ShapeGraphs:
+    def __init__(self):
+        self.pool = None
+        self.x_in = None
+        self.pre = None
+        self.prep = None
+        self.norms_pin = None
+        self.post: Dict[tuple, tuple] = {}
+        self.pre_launches = 0
+
+
+_LAST_LAUNCHES = 0
+
+
+def last_launches() -> int:
+    """Kernels of libmpps_b200.so executed by the last graphed evaluation
+    (counted when the graphs were captured)."""
+    return _LAST_LAUNCHES
+
+
+def run(key: tuple, Xsrc, build_pre, run_post, timer):
+    """Execute one evaluation through cached graphs.
+
+    key       hashable problem shape (batch, n, series, digits, engine, ...)
+    Xsrc      torch fp64 (B, n, n) tensor (device or pinned host)
+    build_pre(Xstatic) -> _Prepared   eager pre-planner pipeline (captured)
+    run_post(prep, norms) -> (post_key, post_fn, info)
+              post_fn(prep) launches the Horner chain and returns the result
+    Returns (prep, norms numpy, result MatBatch, info) or None when graphs
+    are off for this key (caller runs eagerly)."""
+    torch = _torch()
+    if not _ENABLED or key in _FAILED:
+        return None
+    g = _CACHE.get(key)
+    try:
+        if g is None:
+            g = _ShapeGraphs()
+            g.pool = torch.cuda.graph_pool_handle()
+            g.x_in = torch.empty(Xsrc.shape, dtype=torch.float64, device="cuda")
+            g.x_in.copy_(Xsrc, non_blocking=True)
+            # warm-up (kernel attributes, handles, lazy module state) then capture
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                build_pre(g.x_in, capture=False)
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            g.pre = torch.cuda.CUDAGraph()
+            from . import _lib
+            l0 = _lib.total_launches()
+            with torch.cuda.graph(g.pre, pool=g.pool):
+                g.prep = build_pre(g.x_in, capture=True)
+                g.norms_pin = torch.empty(g.prep.norms_dev.shape, dtype=torch.float64, pin_memory=True)
+                g.norms_pin.copy_(g.prep.norms_dev, non_blocking=True)
+            g.pre_launches = _lib.total_launches() - l0
+            _CACHE[key] = g
+        g.x_in.copy_(Xsrc, non_blocking=True)
+        timer.start("power_formation")
+        g.pre.replay()
+        timer.stop()
+        timer.start("norm_estimation")
+        torch.cuda.current_stream().synchronize()
+        norms = g.norms_pin.numpy().copy()
+        timer.stop()
+        g.prep.norms = norms
+        post_key, post_fn, info = run_post(g.prep, norms)
+        entry = g.post.get(post_key)
+        if entry is None:
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                post_fn(g.prep)                 # warm-up (new kernel instantiations)
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            from . import _lib
+            l0 = _lib.total_launches()
+            with torch.cuda.graph(graph, pool=g.pool):
+                res = post_fn(g.prep)
+            entry = (graph, res, post_fn, _lib.total_launches() - l0)  # post_fn keeps its index tensors alive
+            g.post[post_key] = entry
+        graph, res, _, post_launches = entry
+        global _LAST_LAUNCHES
+        _LAST_LAUNCHES = g.pre_launches + post_launches
+        timer.start("mixed_horner")
+        graph.replay()
+        out = MatBatch(res.data.clone(), res.fmt)
+        timer.stop()
+        return g.prep, norms, out, info
+    except Exception as exc:  # pragma: no cover - capture problems fall back to eager
+        _FAILED.add(key)
+        _CACHE.pop(key, None)
+        import warnings
+        warnings.warn(f"CUDA graph path disabled for this shape: {exc!r}")
+        return None

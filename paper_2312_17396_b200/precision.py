@@ -189,7 +189,10 @@ def to_device_async(values, dtype, device):
     queue is not drained (a pageable torch.tensor(..., device=cuda) copy
     synchronises the stream)."""
     torch = _torch()
-    t = torch.as_tensor(np.asarray(values), dtype=dtype)
+    a = np.asarray(values)
+    if isinstance(a, np.ndarray) and not a.flags.writeable:
+        a = a.copy()
+    t = torch.as_tensor(a, dtype=dtype)
     if t.device.type != "cpu":
         return t.to(device)
     return t.pin_memory().to(device, non_blocking=True)
