@@ -18,10 +18,11 @@ from .planner import (EvaluationPlan, cost_ratio, default_block_size,
 from .bounds import (BoundInputs, BoundInvalidError, extra_squarings, gamma,
                      tau_sequence, thm21_bound)
 from .engine import (BatchReport, EvaluationReport, cos_argument, horner_mixed, plan_only, ps_mixed_pade,
-                     ps_fixed, ps_mixed_exp, ps_mixed_general)
+                     ps_fixed, ps_mixed_exp, ps_mixed_general, submit_mixed_exp, submit_mixed_general,
+                     PendingEvaluation)
 
 from .expm import expm_ss
-from . import ops, summa
+from . import ops, summa, pipeline
 
 __version__ = "0.1.0"
 
@@ -32,7 +33,8 @@ __all__ = [
     "series_from_json", "series_to_json", "taylor_cos_coeffs", "taylor_exp_coeffs",
     "EvaluationPlan", "EvaluationReport", "BatchReport", "cost_ratio", "cos_argument",
     "default_block_size", "horner_mixed", "plan_only", "plan_precisions",
-    "ps_fixed", "ps_mixed_exp", "ps_mixed_general", "snap_to_lattice",
+    "ps_fixed", "ps_mixed_exp", "ps_mixed_general", "submit_mixed_exp", "submit_mixed_general",
+    "PendingEvaluation", "snap_to_lattice",
     "BoundInputs", "BoundInvalidError", "extra_squarings", "gamma",
     "tau_sequence", "thm21_bound", "expm_ss", "ops", "summa", "ps_mixed_pade",
 ]

@@ -118,6 +118,12 @@ template <> struct WV<F64> {
   static __device__ __forceinline__ T axpy_fast(T a, T x, T y) { return axpy(a, x, y); }
   static __device__ __forceinline__ double hi(T v) { return v; }
   static __device__ __forceinline__ void store(const MatRef &m, long long off, T v) { ((double *)m.data)[off] = v; }
+  static __device__ __forceinline__ T load(const MatRef &m, long long off) { return ((const double *)m.data)[off]; }
+  // block-assembly accumulator (engine.py:127-154): identical to axpy here
+  using Acc = T;
+  static __device__ __forceinline__ Acc acc_of(T v) { return v; }
+  static __device__ __forceinline__ Acc acc_mac(T c, T x, Acc a) { return axpy(c, x, a); }
+  static __device__ __forceinline__ T acc_final(Acc a) { return a; }
 };
 template <> struct WV<DD> {
   using T = mp::dd;
@@ -131,6 +137,30 @@ template <> struct WV<DD> {
   static __device__ __forceinline__ void store(const MatRef &m, long long off, T v) {
     double *p = (double *)m.data + off; p[0] = v.hi; p[m.plane] = v.lo;
   }
+  static __device__ __forceinline__ T load(const MatRef &m, long long off) {
+    const double *p = (const double *)m.data + off;
+    return mp::dd_make(p[0], p[m.plane]);
+  }
+  // Block-assembly accumulator: the high parts are summed with an exact
+  // TwoSum, every rounding error and the cross products go to an unnormalised
+  // low word, renormalised once per entry (12 FP64 instructions per term;
+  // normwise error <= (s + 2) u_dd sum_j |b_j| |X^j|, like dd_add_sloppy).
+  struct Acc { double hi, lo; };
+  static __device__ __forceinline__ Acc acc_of(T v) { return Acc{v.hi, v.lo}; }
+  static __device__ __forceinline__ Acc acc_mac(T c, T x, Acc a) {
+    const double p = __dmul_rn(c.hi, x.hi);
+    double e = __fma_rn(c.hi, x.hi, -p);
+    e = __fma_rn(c.hi, x.lo, e);
+    e = __fma_rn(c.lo, x.hi, e);
+    double sh, t;
+    mp::two_sum(a.hi, p, sh, t);
+    return Acc{sh, __dadd_rn(a.lo, __dadd_rn(t, e))};
+  }
+  static __device__ __forceinline__ T acc_final(Acc a) {
+    double h, l;
+    mp::quick_two_sum(a.hi, a.lo, h, l);
+    return mp::dd_make(h, l);
+  }
 };
 template <> struct WV<QD> {
   using T = mp::qd;
@@ -143,6 +173,14 @@ template <> struct WV<QD> {
     double *p = (double *)m.data + off;
     p[0] = v.x[0]; p[m.plane] = v.x[1]; p[2 * m.plane] = v.x[2]; p[3 * m.plane] = v.x[3];
   }
+  static __device__ __forceinline__ T load(const MatRef &m, long long off) {
+    const double *p = (const double *)m.data + off;
+    return mp::qd_make(p[0], p[m.plane], p[2 * m.plane], p[3 * m.plane]);
+  }
+  using Acc = T;
+  static __device__ __forceinline__ Acc acc_of(T v) { return v; }
+  static __device__ __forceinline__ Acc acc_mac(T c, T x, Acc a) { return axpy(c, x, a); }
+  static __device__ __forceinline__ T acc_final(Acc a) { return a; }
 };
 
 // ------------------------------------------------------------- kernels
@@ -203,13 +241,19 @@ struct AssembleArgs {
   int row0, col0;         // global offsets of this block (2-D distributed matrices)
 };
 
-// One thread per (column, 32-row chunk); the r+1 block accumulators of an
-// entry live in registers, the coefficients in shared memory (broadcast
-// reads), so each power entry is loaded once and used for every block.
+// One thread per (column, kAsmRows-row chunk); the NB = r+1 block
+// accumulators of an entry live in registers, the coefficients in shared
+// memory (broadcast reads), so each power entry is loaded once and used for
+// every block.  Power loads are issued in groups of kAsmLoads before use.
+constexpr int kAsmRows = 16;
+constexpr int kAsmLoads = 8;
+constexpr int kAsmLoads2 = 4;  // two-row path
+
 template <int WF, int NB>
-__global__ void __launch_bounds__(128) assemble_kernel(const AssembleArgs a) {
+__global__ void __launch_bounds__(128, (WF == QD || NB > 6) ? 1 : 4) assemble_kernel(const AssembleArgs a) {
   using V = WV<WF>;
   using T = typename V::T;
+  using Acc = typename V::Acc;
   constexpr int CW = (WF == QD) ? 4 : (WF == DD ? 2 : 1);
   __shared__ double sc[kMaxBlocks * kMaxPowers * CW];
   const int n = a.cols, s = a.s, m = a.m, r = a.r;
@@ -230,35 +274,119 @@ __global__ void __launch_bounds__(128) assemble_kernel(const AssembleArgs a) {
   double cs[NB + 1];
 #pragma unroll
   for (int k = 0; k <= NB; ++k) cs[k] = 0.0;
-  const int row0 = chunk * kRowsPerChunk;
-  const int row1 = min(a.rows, row0 + kRowsPerChunk);
-  for (int row = row0; row < row1; ++row) {
-    T acc[NB];
-    const bool diag = (row + a.row0) == (col + a.col0);
+  const int row0 = chunk * kAsmRows;
+  const int row1 = min(a.rows, row0 + kAsmRows);
+  auto load_row = [&](int row, int j0, T (&xs)[kAsmLoads]) {
 #pragma unroll
-    for (int k = 0; k < NB; ++k)
-      if (k <= r) acc[k] = diag ? coef(s * k) : V::zero();
-    for (int j = 1; j < s; ++j) {
-      const MatRef &P = a.P[j - 1];
-      T x = V::from(load_qd(P, (long long)b * P.bstride + (long long)row * P.ld + col));
+    for (int u = 0; u < kAsmLoads; ++u) {
+      const int j = j0 + u;
+      if (j < s) {
+        const MatRef &P = a.P[j - 1];
+        xs[u] = V::load(P, (long long)b * P.bstride + (long long)row * P.ld + col);
+      }
+    }
+  };
+  auto load_row2 = [&](int row, int j0, T (&xs)[kAsmLoads2]) {
 #pragma unroll
-      for (int k = 0; k < NB; ++k) {
-        if (k <= r) {
-          const int hi = (k < full) ? s - 1 : m - s * full;
-          if (j <= hi) acc[k] = V::axpy_fast(coef(s * k + j), x, acc[k]);
+    for (int u = 0; u < kAsmLoads2; ++u) {
+      const int j = j0 + u;
+      if (j < s) {
+        const MatRef &P = a.P[j - 1];
+        xs[u] = V::load(P, (long long)b * P.bstride + (long long)row * P.ld + col);
+      }
+    }
+  };
+  auto mac_group = [&](int j0, const T (&xs)[kAsmLoads], Acc (&acc)[NB]) {
+#pragma unroll
+    for (int u = 0; u < kAsmLoads; ++u) {
+      const int j = j0 + u;
+      if (j < s) {
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          if (k <= r) {
+            const int hi = (k < full) ? s - 1 : m - s * full;
+            if (j <= hi) acc[k] = V::acc_mac(coef(s * k + j), xs[u], acc[k]);
+          }
         }
       }
     }
+  };
+  auto finish_row = [&](int row, Acc (&acc)[NB], double ymag) {
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
       if (k <= r) {
         const MatRef &B = a.Bk[k];
-        V::store(B, (long long)b * B.bstride + (long long)row * B.ld + col, acc[k]);
-        cs[k] += fabs(V::hi(acc[k]));
+        const T v = V::acc_final(acc[k]);
+        V::store(B, (long long)b * B.bstride + (long long)row * B.ld + col, v);
+        cs[k] += fabs(V::hi(v));
       }
     }
-    const MatRef &Y = a.P[s - 1];
-    cs[NB] += fabs(((const double *)Y.data)[(long long)b * Y.bstride + (long long)row * Y.ld + col]);
+    cs[NB] += ymag;
+  };
+  auto init_acc = [&](int row, Acc (&acc)[NB]) {
+    const bool diag = (row + a.row0) == (col + a.col0);
+#pragma unroll
+    for (int k = 0; k < NB; ++k)
+      if (k <= r) acc[k] = V::acc_of(diag ? coef(s * k) : V::zero());
+  };
+  const MatRef &Y = a.P[s - 1];
+  auto y_at = [&](int row) {
+    return fabs(((const double *)Y.data)[(long long)b * Y.bstride + (long long)row * Y.ld + col]);
+  };
+  if (WF != QD) {
+    // two rows per iteration: twice the independent FP64 chains per warp and
+    // one shared-memory coefficient read per two MACs
+    int row = row0;
+    for (; row + 1 < row1; row += 2) {
+      Acc acc0[NB], acc1[NB];
+      init_acc(row, acc0);
+      init_acc(row + 1, acc1);
+      for (int j0 = 1; j0 < s; j0 += kAsmLoads2) {
+        T x0[kAsmLoads2], x1[kAsmLoads2];
+        load_row2(row, j0, x0);
+        load_row2(row + 1, j0, x1);
+#pragma unroll
+        for (int u = 0; u < kAsmLoads2; ++u) {
+          const int j = j0 + u;
+          if (j < s) {
+#pragma unroll
+            for (int k = 0; k < NB; ++k) {
+              if (k <= r) {
+                const int hi = (k < full) ? s - 1 : m - s * full;
+                if (j <= hi) {
+                  const T c = coef(s * k + j);
+                  acc0[k] = V::acc_mac(c, x0[u], acc0[k]);
+                  acc1[k] = V::acc_mac(c, x1[u], acc1[k]);
+                }
+              }
+            }
+          }
+        }
+      }
+      finish_row(row, acc0, y_at(row));
+      finish_row(row + 1, acc1, y_at(row + 1));
+    }
+    if (row < row1) {
+      Acc acc[NB];
+      init_acc(row, acc);
+      for (int j0 = 1; j0 < s; j0 += kAsmLoads) {
+        T xs[kAsmLoads];
+        load_row(row, j0, xs);
+        mac_group(j0, xs, acc);
+      }
+      finish_row(row, acc, y_at(row));
+    }
+  } else {
+    for (int row = row0; row < row1; ++row) {
+      Acc acc[NB];
+      init_acc(row, acc);
+      for (int j0 = 1; j0 < s; j0 += kAsmLoads) {
+        T xs[kAsmLoads];
+        load_row(row, j0, xs);
+        mac_group(j0, xs, acc);
+      }
+      finish_row(row, acc, y_at(row));
+    }
   }
   double *out = a.partial + ((long long)b * a.nchunk + chunk) * (long long)(r + 2) * n;
 #pragma unroll
@@ -568,15 +696,17 @@ static int assemble_common(mpps_handle *h, const mpps_mat *powers, int s, int m,
   if (rows == 0 || cols == 0 || batch == 0) return MPPS_OK;
   a.coeff = coeff; a.rows = rows; a.cols = cols; a.s = s; a.m = m; a.r = r;
   a.row0 = row0; a.col0 = col0;
-  a.nchunk = (rows + kRowsPerChunk - 1) / kRowsPerChunk;
+  a.nchunk = (rows + kAsmRows - 1) / kAsmRows;
   size_t pbytes = sizeof(double) * (size_t)batch * a.nchunk * (r + 2) * cols;
   cudaError_t e = cudaMallocAsync((void **)&a.partial, pbytes, h->stream);
   if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "assemble scratch: %s", cudaGetErrorString(e));
   dim3 grid((cols + 127) / 128, a.nchunk, batch);
-  const int nbk = r + 1 <= 4 ? 4 : r + 1 <= 8 ? 8 : 16;
+  const int nbk = r + 1 <= 8 ? r + 1 : 16;  // exact up to 8 blocks (registers)
 #define AK(WW, NN) \
   if (wf == WW && nbk == NN) assemble_kernel<WW, NN><<<grid, 128, 0, h->stream>>>(a); else
-  AK(F64, 4) AK(F64, 8) AK(F64, 16) AK(DD, 4) AK(DD, 8) AK(DD, 16) AK(QD, 4) AK(QD, 8) AK(QD, 16) {}
+#define AKW(WW) AK(WW, 1) AK(WW, 2) AK(WW, 3) AK(WW, 4) AK(WW, 5) AK(WW, 6) AK(WW, 7) AK(WW, 8) AK(WW, 16)
+  AKW(F64) AKW(DD) AKW(QD) {}
+#undef AKW
 #undef AK
   int rc = after_launch(h, "assemble_kernel");
   if (rc) return rc;

@@ -142,34 +142,73 @@ struct SliceRef {
 // (scaling by 2^k and subtracting the nearest integer are exact; the words
 // are renormalised with TwoSums), so sum_s d_s 2^-(6+7s) is the value
 // truncated after S digits.
+// 2^e as a double (exact); e within the normal range.
+__device__ __forceinline__ double pow2i(int e) {
+  if (e >= -1022 && e <= 1023) return __longlong_as_double((long long)(e + 1023) << 52);
+  return ldexp(1.0, e);
+}
+
+// v * 2^k on the first W words (exact power-of-two multiply; ldexp only
+// outside the normal range of 2^k)
+template <int W>
+__device__ __forceinline__ mp::qd scale_words(mp::qd v, int k) {
+  if (k >= -1022 && k <= 1023) {
+    const double p = __longlong_as_double((long long)(k + 1023) << 52);
+#pragma unroll
+    for (int w = 0; w < W; ++w) v.x[w] *= p;
+    return v;
+  }
+  return mp::qd_ldexp(v, k);
+}
+
 template <int W, int S>
-__device__ __forceinline__ void split_digits_w(const mp::qd &v, int8_t (&dg)[S]) {
+__device__ __forceinline__ void split_digits_wi(const mp::qd &v, int (&dg)[S]) {
+  // Digit s is the nearest integer to the running residual times 2^6 (s = 0)
+  // or 2^7.  Rounding uses the 1.5*2^52 shifter fused into the scaling FMA
+  // (FP64 pipe only; the digit is the low word of the shifted value), and
+  // the residual update x0 = x0*2^k - d is exact.  Lower words are carried
+  // lazily: they are rescaled and folded into x0 every kFold digits (exact
+  // two-sum chain), which keeps |x0| <= 0.5 + 2^-25 between folds, so every
+  // digit stays in [-65, 65] and sum_s d_s 2^-(6+7s) + residual == v exactly.
+  constexpr double kShift = 6755399441055744.0;  // 1.5 * 2^52
+  constexpr int kFold = 4;
   double x[W];
 #pragma unroll
   for (int w = 0; w < W; ++w) x[w] = v.x[w];
-  double sc = 64.0;
+  double pend = 1.0;  // scale owed to the lower words since the last fold
 #pragma unroll
   for (int s = 0; s < S; ++s) {
+    const double sc = (s == 0) ? 64.0 : 128.0;
+    if constexpr (W > 1) {
+      pend *= sc;
+      if (s > 0 && s % kFold == 0) {
 #pragma unroll
-    for (int w = 0; w < W; ++w) x[w] *= sc;
-    const double d = rint(x[0]);
-    double r = x[0] - d;  // exact
-    if constexpr (W == 1) {
-      x[0] = r;
-    } else {
-      double c = r;
+        for (int w = 1; w < W; ++w) x[w] *= pend / sc;  // lower words to x0's scale
+        double c = x[0];
 #pragma unroll
-      for (int w = 1; w < W; ++w) {  // carry the lower words up (exact)
-        double t, e;
-        mp::two_sum(c, x[w], t, e);
-        x[w - 1] = t;
-        c = e;
+        for (int w = 1; w < W; ++w) {
+          double t, e;
+          mp::two_sum(c, x[w], t, e);
+          x[w - 1] = t;
+          c = e;
+        }
+        x[W - 1] = c;
+        pend = sc;
       }
-      x[W - 1] = c;
     }
-    dg[s] = (int8_t)(int)d;
-    sc = 128.0;
+    const double t = fma(x[0], sc, kShift);
+    const double d = t - kShift;
+    x[0] = fma(x[0], sc, -d);  // exact
+    dg[s] = __double2loint(t);  // low byte = the digit (two's complement)
   }
+}
+
+template <int W, int S>
+__device__ __forceinline__ void split_digits_w(const mp::qd &v, int8_t (&dg)[S]) {
+  int di[S];
+  split_digits_wi<W, S>(v, di);
+#pragma unroll
+  for (int s = 0; s < S; ++s) dg[s] = (int8_t)di[s];
 }
 
 __device__ __forceinline__ int row_exponent(double mx) {
@@ -208,24 +247,23 @@ __global__ void slice_rows_kernel(MatRef A, int rows, int cols, int fi, SliceRef
   const long long plane = out.plane();
   int8_t *o = out.digits + ((long long)b * out.rpad + i) * out.kpad;
   for (int k0 = 4 * lane; k0 < out.kpad; k0 += 128) {
-    uint32_t packed[S];
-#pragma unroll
-    for (int s = 0; s < S; ++s) packed[s] = 0u;
+    int dq[4][S];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int k = k0 + q;
       mp::qd v = mp::qd_make(0.0, 0.0, 0.0, 0.0);
       if (i < rows && k < cols) {
         v = fi == F32 ? mp::qd_from_d((double)((const float *)A.data)[base + k]) : load_qd(A, base + k);
-        v = mp::qd_ldexp(v, -e);
+        v = scale_words<W>(v, -e);
       }
-      int8_t dg[S];
-      split_digits_w<W, S>(v, dg);
-#pragma unroll
-      for (int s = 0; s < S; ++s) packed[s] |= ((uint32_t)(uint8_t)dg[s]) << (8 * q);
+      split_digits_wi<W, S>(v, dq[q]);
     }
 #pragma unroll
-    for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t *>(o + s * plane + k0) = packed[s];
+    for (int s = 0; s < S; ++s) {  // bytes 0 of the four digits -> one word
+      const uint32_t lo = __byte_perm(dq[0][s], dq[1][s], 0x0040);
+      const uint32_t hi = __byte_perm(dq[2][s], dq[3][s], 0x0040);
+      *reinterpret_cast<uint32_t *>(o + s * plane + k0) = __byte_perm(lo, hi, 0x5410);
+    }
   }
 }
 
@@ -268,7 +306,7 @@ __global__ void slice_cols_kernel(MatRef B, int rows, int cols, int fi, SliceRef
     if (k < rows && j < cols) {
       const long long off = (long long)b * B.bstride + (long long)k * B.ld + j;
       v = fi == F32 ? mp::qd_from_d((double)((const float *)B.data)[off]) : load_qd(B, off);
-      v = mp::qd_ldexp(v, -out.exps[(long long)b * out.rpad + j]);
+      v = scale_words<W>(v, -out.exps[(long long)b * out.rpad + j]);
     }
     int8_t dg[S];
     split_digits_w<W, S>(v, dg);
@@ -478,11 +516,6 @@ __global__ void __launch_bounds__(kThreadsOz, 1) oz_gemm_kernel(const OzArgs arg
 }
 
 // ------------------------------------------------------ shared epilogue
-// 2^e as a double (exact); e within the normal range.
-__device__ __forceinline__ double pow2i(int e) {
-  if (e >= -1022 && e <= 1023) return __longlong_as_double((long long)(e + 1023) << 52);
-  return ldexp(1.0, e);
-}
 __host__ __device__ constexpr double pow2c(int e) {  // compile-time 2^e
   double r = 1.0;
   if (e >= 0) for (int i = 0; i < e; ++i) r *= 2.0;

@@ -502,13 +502,9 @@ def _plan_fn(norms_row, r, ctx, delta, s, apply_switch, fix_params):
 
 
 # ------------------------------------------------------------ evaluators
-def _graphed(Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: int, kind: str, delta: float,
-             apply_switch: bool, timer: _Buckets):
-    """The batched pipeline through cached CUDA graphs (graphs.py); returns
-    (prep, digits, nu, nil, result) or None (eager path)."""
-    from . import graphs
-    if Xt is None or not graphs.enabled():
-        return None
+def _graph_stages(Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: int, kind: str, delta: float,
+                  apply_switch: bool):
+    """(key, build_pre, run_post) of the graphed batched pipeline."""
     d = ctx.decimal_digits
     key = (tuple(Xt.shape), str(Xt.device if Xt.is_cuda else "host"), series.coeffs, d, wf, s, kind, delta,
            apply_switch, ge.engine())
@@ -530,13 +526,88 @@ def _graphed(Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: int, 
         def post_fn(p):
             return _horner(_lib.handle_for(), p, digits, nil, _Buckets(False), structure, sels)
         return structure, post_fn, (digits, nu, nil)
+    return key, build_pre, run_post
 
+
+def _graphed(Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: int, kind: str, delta: float,
+             apply_switch: bool, timer: _Buckets):
+    """The batched pipeline through cached CUDA graphs (graphs.py); returns
+    (prep, digits, nu, nil, result) or None (eager path)."""
+    from . import graphs
+    if Xt is None or not graphs.enabled():
+        return None
+    key, build_pre, run_post = _graph_stages(Xt, series, ctx, wf, s, kind, delta, apply_switch)
     out = graphs.run(key, Xt, build_pre, run_post, timer)
     if out is None:
         return None
     prep, norms, result, info = out
     digits, nu, nil = info
     return prep, digits, nu, nil, result
+
+
+class PendingEvaluation:
+    """A batched mixed-precision evaluation whose device work before the
+    planner is already enqueued (see submit_mixed_exp).  ``finish()`` waits
+    for this evaluation's block norms only, plans, enqueues the Horner chain
+    and returns the report exactly as the one-shot evaluator would."""
+
+    def __init__(self, finish):
+        self._finish = finish
+        self._report = None
+
+    def finish(self):
+        if self._report is None:
+            self._report = self._finish()
+            self._finish = None
+        return self._report
+
+
+def submit_mixed_general(X, series: CoefficientSeries, ctx: PrecisionCtx, delta: float = 10.0,
+                         with_bound: bool = False, timing: bool = True, slot: int = 0) -> PendingEvaluation:
+    """Two-phase ps_mixed_general: enqueue everything up to the block norms
+    now, plan and run the Horner phase at ``finish()``.  Submitting batch c+1
+    (another ``slot``) before finishing batch c keeps the GPU busy while the
+    host plans; results are bit-identical to ps_mixed_general."""
+    return _submit(X, series, ctx, delta, True, with_bound, timing, slot,
+                   lambda: ps_mixed_general(X, series, ctx, delta, with_bound, timing))
+
+
+def submit_mixed_exp(X, m: int, ctx: PrecisionCtx, delta: float = 10.0, with_bound: bool = False,
+                     timing: bool = True, slot: int = 0) -> PendingEvaluation:
+    """Two-phase ps_mixed_exp (fix_params=True; see submit_mixed_general)."""
+    if m < 1:
+        raise ValueError("m must be >= 1")
+    series = taylor_exp_coeffs(m)
+    if default_block_size(m) == m:
+        rep = ps_mixed_exp(X, m, ctx, True, delta, with_bound, timing)
+        return PendingEvaluation(lambda: rep)
+    return _submit(X, series, ctx, delta, True, with_bound, timing, slot,
+                   lambda: ps_mixed_exp(X, m, ctx, True, delta, with_bound, timing))
+
+
+def _submit(X, series, ctx, delta, fix_params, with_bound, timing, slot, eager):
+    from . import graphs
+    Xt, Xw, single = _input(X)
+    B, n = _check_square(Xt, Xw)
+    if series.degree < 1:
+        raise ValueError("series degree must be >= 1")
+    if Xt is None or not graphs.enabled():
+        rep = eager()
+        return PendingEvaluation(lambda: rep)
+    timer = _Buckets(timing)
+    wf = _working_format(ctx)
+    s = default_block_size(series.degree)
+    key, build_pre, run_post = _graph_stages(Xt, series, ctx, wf, s, "mixed", delta, True)
+    pend = graphs.submit(key, Xt, build_pre, timer, slot)
+    if pend is None:
+        rep = eager()
+        return PendingEvaluation(lambda: rep)
+
+    def fin():
+        prep, norms, result, (digits, nu, nil) = graphs.finish(pend, run_post)
+        return _graphed_reports((prep, digits, nu, nil, result), ctx, delta, True, fix_params, with_bound,
+                                single, timer)
+    return PendingEvaluation(fin)
 
 
 def ps_fixed(X, series: CoefficientSeries, ctx: PrecisionCtx, with_bound: bool = False,

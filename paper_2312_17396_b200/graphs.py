@@ -64,17 +64,24 @@ def last_launches() -> int:
     return _LAST_LAUNCHES
 
 
-def run(key: tuple, Xsrc, build_pre, run_post, timer):
-    """Execute one evaluation through cached graphs.
+class Pending:
+    """A submitted evaluation: the pre graph is enqueued and the norms are
+    on their way to pinned memory (``ready`` is recorded after the copy)."""
 
-    key       hashable problem shape (batch, n, series, digits, engine, ...)
-    Xsrc      torch fp64 (B, n, n) tensor (device or pinned host)
-    build_pre(Xstatic) -> _Prepared   eager pre-planner pipeline (captured)
-    run_post(prep, norms) -> (post_key, post_fn, info)
-              post_fn(prep) launches the Horner chain and returns the result
-    Returns (prep, norms numpy, result MatBatch, info) or None when graphs
-    are off for this key (caller runs eagerly)."""
+    __slots__ = ("g", "ready", "timer")
+
+    def __init__(self, g, ready, timer):
+        self.g, self.ready, self.timer = g, ready, timer
+
+
+def submit(key: tuple, Xsrc, build_pre, timer, slot: int = 0) -> Optional[Pending]:
+    """Enqueue the pre-planner graph of one evaluation (capturing it on first
+    use).  ``slot`` selects an independent set of static buffers, so two
+    evaluations of the same shape can be in flight (pre of chunk c+1 runs on
+    the GPU while the host plans chunk c).  Returns None when graphs are off
+    for this key (the caller runs eagerly)."""
     torch = _torch()
+    key = key + (("slot", slot),)
     if not _ENABLED or key in _FAILED:
         return None
     g = _CACHE.get(key)
@@ -103,39 +110,72 @@ def run(key: tuple, Xsrc, build_pre, run_post, timer):
         g.x_in.copy_(Xsrc, non_blocking=True)
         timer.start("power_formation")
         g.pre.replay()
+        ready = torch.cuda.Event()
+        ready.record()
         timer.stop()
-        timer.start("norm_estimation")
-        torch.cuda.current_stream().synchronize()
-        norms = g.norms_pin.numpy().copy()
-        timer.stop()
-        g.prep.norms = norms
-        post_key, post_fn, info = run_post(g.prep, norms)
-        entry = g.post.get(post_key)
-        if entry is None:
-            s = torch.cuda.Stream()
-            s.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(s):
-                post_fn(g.prep)                 # warm-up (new kernel instantiations)
-            torch.cuda.current_stream().wait_stream(s)
-            torch.cuda.synchronize()
-            graph = torch.cuda.CUDAGraph()
-            from . import _lib
-            l0 = _lib.total_launches()
-            with torch.cuda.graph(graph, pool=g.pool):
-                res = post_fn(g.prep)
-            entry = (graph, res, post_fn, _lib.total_launches() - l0)  # post_fn keeps its index tensors alive
-            g.post[post_key] = entry
-        graph, res, _, post_launches = entry
-        global _LAST_LAUNCHES
-        _LAST_LAUNCHES = g.pre_launches + post_launches
-        timer.start("mixed_horner")
-        graph.replay()
-        out = MatBatch(res.data.clone(), res.fmt)
-        timer.stop()
-        return g.prep, norms, out, info
+        return Pending(g, ready, timer)
     except Exception as exc:  # pragma: no cover - capture problems fall back to eager
         _FAILED.add(key)
         _CACHE.pop(key, None)
+        import warnings
+        warnings.warn(f"CUDA graph path disabled for this shape: {exc!r}")
+        return None
+
+
+def finish(p: Pending, run_post):
+    """Wait for the submitted evaluation's norms (its event only, not the
+    whole stream), plan on the host, enqueue the Horner graph for the plan
+    structure and return (prep, norms numpy, result MatBatch, info)."""
+    torch = _torch()
+    g, timer = p.g, p.timer
+    timer.start("norm_estimation")
+    p.ready.synchronize()
+    norms = g.norms_pin.numpy().copy()
+    timer.stop()
+    g.prep.norms = norms
+    post_key, post_fn, info = run_post(g.prep, norms)
+    entry = g.post.get(post_key)
+    if entry is None:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            post_fn(g.prep)                 # warm-up (new kernel instantiations)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        from . import _lib
+        l0 = _lib.total_launches()
+        with torch.cuda.graph(graph, pool=g.pool):
+            res = post_fn(g.prep)
+        entry = (graph, res, post_fn, _lib.total_launches() - l0)  # post_fn keeps its index tensors alive
+        g.post[post_key] = entry
+    graph, res, _, post_launches = entry
+    global _LAST_LAUNCHES
+    _LAST_LAUNCHES = g.pre_launches + post_launches
+    timer.start("mixed_horner")
+    graph.replay()
+    out = MatBatch(res.data.clone(), res.fmt)
+    timer.stop()
+    return g.prep, norms, out, info
+
+
+def run(key: tuple, Xsrc, build_pre, run_post, timer):
+    """Execute one evaluation through cached graphs: submit + finish.
+
+    key       hashable problem shape (batch, n, series, digits, engine, ...)
+    Xsrc      torch fp64 (B, n, n) tensor (device or pinned host)
+    build_pre(Xstatic) -> _Prepared   eager pre-planner pipeline (captured)
+    run_post(prep, norms) -> (post_key, post_fn, info)
+              post_fn(prep) launches the Horner chain and returns the result
+    Returns (prep, norms numpy, result MatBatch, info) or None when graphs
+    are off for this key (caller runs eagerly)."""
+    p = submit(key, Xsrc, build_pre, timer)
+    if p is None:
+        return None
+    try:
+        return finish(p, run_post)
+    except Exception as exc:  # pragma: no cover - capture problems fall back to eager
+        _FAILED.add(key + (("slot", 0),))
         import warnings
         warnings.warn(f"CUDA graph path disabled for this shape: {exc!r}")
         return None

@@ -1,0 +1,161 @@
+"""Host-resident batches: overlap host<->device copies, host planning and
+device evaluation.
+
+``evaluate_host(submit, X_host, out_host, chunks)`` splits a pinned host
+batch (B, n, n) into chunks and software-pipelines them:
+
+  upload stream    H2D of chunk c+1 (double-buffered device input)
+  compute stream   pre-planner graph of chunk c+1 is enqueued BEFORE the
+                   host plans chunk c, so the GPU works through the planner
+                   gap; then the Horner graph of chunk c
+  download stream  D2H of chunk c's result into ``out_host`` (words, B, n, n)
+
+PCIe is full duplex and the copies run on the copy engines, so for a
+multi-chunk batch only the first upload and the last download are exposed.
+``submit(x_dev, slot)`` returns an object with ``finish() -> report``
+(engine.submit_mixed_exp / submit_mixed_general, or ``eager(fn)`` for any
+one-shot evaluator).  Reports are returned in chunk order.
+"""
+
+from __future__ import annotations
+
+from typing import Callable, List
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def mixed_exp(m: int, ctx, **kw) -> Callable:
+    """submit callable for ps_mixed_exp (fix_params=True)."""
+    from .engine import submit_mixed_exp
+    return lambda x, slot: submit_mixed_exp(x, m, ctx, slot=slot, **kw)
+
+
+def mixed_general(series, ctx, **kw) -> Callable:
+    """submit callable for ps_mixed_general."""
+    from .engine import submit_mixed_general
+    return lambda x, slot: submit_mixed_general(x, series, ctx, slot=slot, **kw)
+
+
+def eager(fn: Callable) -> Callable:
+    """submit callable running a one-shot evaluator at submit time."""
+    from .engine import PendingEvaluation
+
+    def sub(x, slot):
+        rep = fn(x)
+        return PendingEvaluation(lambda: rep)
+    return sub
+
+
+_STATE = {}
+
+
+def _state(torch, dev):
+    """Copy streams and double-buffered device inputs, reused across calls
+    (creating streams/allocations per call costs ~0.4 ms of host time)."""
+    st = _STATE.get(dev)
+    if st is None:
+        st = {"up": torch.cuda.Stream(), "down": torch.cuda.Stream(), "bufs": {}}
+        _STATE[dev] = st
+    return st
+
+
+def split_sizes(B: int, chunks) -> List[int]:
+    """Chunk sizes: an explicit list, or ``chunks`` parts tapered so the last
+    chunk (whose download is exposed) is the smallest."""
+    if not isinstance(chunks, int):
+        sizes = [int(x) for x in chunks]
+        if sum(sizes) != B or min(sizes) < 1:
+            raise ValueError("chunk sizes must be positive and sum to the batch")
+        return sizes
+    k = max(1, min(int(chunks), B))
+    if k == 1:
+        return [B]
+    last = max(1, B // (2 * k - 1))            # the last chunk is about half the others
+    rest = B - last
+    sizes = [(rest * (i + 1)) // (k - 1) - (rest * i) // (k - 1) for i in range(k - 1)]
+    return sizes + [last]
+
+
+def evaluate_host(submit: Callable, X_host, out_host, chunks=3, trace=None) -> List[object]:
+    """``chunks``: a count (tapered split, see split_sizes) or explicit sizes.
+    ``trace``: optional list; timing events (label, event) are appended
+    (diagnostics, tools/e2e_chunks.py)."""
+    torch = _torch()
+
+    def mark(label, stream):
+        if trace is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            trace.append((label, e))
+    B = X_host.shape[0]
+    sizes = split_sizes(B, chunks)
+    chunks = len(sizes)
+    bounds = [0]
+    for z in sizes:
+        bounds.append(bounds[-1] + z)
+    comp = torch.cuda.current_stream()
+    st = _state(torch, comp.device)
+    up, down = st["up"], st["down"]
+    up.wait_stream(comp)
+    down.wait_stream(comp)
+    dev_in = [None, None]
+    ev_in = [torch.cuda.Event() for _ in range(chunks)]
+    ev_free = [torch.cuda.Event() for _ in range(chunks)]
+    pend = [None] * chunks
+    reps = []
+
+    def upload(c):
+        lo, hi = bounds[c], bounds[c + 1]
+        slot = c % 2
+        with torch.cuda.stream(up):
+            if c >= 2:
+                up.wait_event(ev_free[c - 2])        # slot consumed by chunk c-2's pre graph
+            shape = (hi - lo,) + tuple(X_host.shape[1:])
+            buf = st["bufs"].get((slot, shape))
+            if buf is None:
+                buf = torch.empty(shape, dtype=torch.float64, device=comp.device)
+                st["bufs"][(slot, shape)] = buf
+            dev_in[slot] = buf
+            mark(f"up{c}<", up)
+            dev_in[slot].copy_(X_host[lo:hi], non_blocking=True)
+            mark(f"up{c}>", up)
+            ev_in[c].record(up)
+
+    def start(c):
+        comp.wait_event(ev_in[c])
+        mark(f"pre{c}<", comp)
+        pend[c] = submit(dev_in[c % 2], c % 2)
+        mark(f"pre{c}>", comp)
+        ev_free[c].record(comp)
+
+    upload(0)
+    if chunks > 1:
+        upload(1)
+    start(0)
+    for c in range(chunks):
+        if c + 1 < chunks:
+            start(c + 1)                 # GPU: pre(c+1) runs while the host plans c
+            if c + 2 < chunks:
+                upload(c + 2)
+        mark(f"post{c}<", comp)
+        rep = pend[c].finish()
+        mark(f"post{c}>", comp)
+        pend[c] = None
+        done = torch.cuda.Event()
+        done.record(comp)
+        lo, hi = bounds[c], bounds[c + 1]
+        res = rep.result.data
+        with torch.cuda.stream(down):
+            down.wait_event(done)
+            mark(f"down{c}<", down)
+            for w in range(res.shape[0]):    # contiguous pinned destination per word
+                out_host[w, lo:hi].copy_(res[w], non_blocking=True)
+            res.record_stream(down)
+            mark(f"down{c}>", down)
+        reps.append(rep)
+    comp.wait_stream(down)
+    comp.wait_stream(up)
+    return reps

@@ -298,3 +298,20 @@ def test_graph_replay_matches_eager_bitwise(cuda):
     for a, b in zip(g, e):
         assert np.array_equal(a, b)
     assert not np.array_equal(g[0], g[1])
+
+
+def test_pipelined_host_evaluation_matches(cuda):
+    """pipeline.evaluate_host (chunked, copies overlapping compute) returns the
+    same bits as one device-resident batched call."""
+    import torch
+    from paper_2312_17396_b200 import pipeline
+    m = mp()
+    ctx = m.PrecisionCtx(31)
+    X = np.stack([synth(64, 1.0, b) for b in range(12)])
+    ref = m.ps_mixed_exp(X, 30, ctx).result.data.cpu().numpy()
+    Xh = torch.from_numpy(X).pin_memory()
+    out = torch.empty((2,) + X.shape, dtype=torch.float64).pin_memory()
+    reps = pipeline.evaluate_host(pipeline.mixed_exp(30, ctx), Xh, out, chunks=3)
+    torch.cuda.synchronize()
+    assert len(reps) == 3
+    assert np.array_equal(out.numpy(), ref)
