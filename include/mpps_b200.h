@@ -192,6 +192,21 @@ int mpps_probe_fma(mpps_handle *h, int fmt, int blocks, int iters, void *scratch
  * MMAs back to back, one CTA per SM): 2*128*256*32*iters ops per CTA. */
 int mpps_probe_i8mma(mpps_handle *h, int blocks, int iters, void *scratch);
 
+/* Diagnostic: while `buf` (device, 5 x uint64 per CTA) is set, the TMA-fed
+ * tensor-core GEMMs record per-CTA %globaltimer stamps (start, after
+ * setup, MMAs done, end) and the SM id; NULL turns it off.  Process-wide;
+ * for tools/cta_timeline.py only. */
+void mpps_debug_oz_trace(void *buf);
+
+/* Diagnostic: bit 0 skips the MMAs (operand feed only), bit 1 skips the
+ * TMA loads (MMAs on stale shared memory) of the TMA-fed GEMMs; results
+ * are garbage while set.  For tools/cta_timeline.py only. */
+void mpps_debug_oz_flags(int flags);
+
+/* Diagnostic: mpps_probe_i8mma with M = 128, N = n (16..256, multiple of
+ * 16), K = 32 MMAs back to back. */
+int mpps_debug_probe_i8mma_n(mpps_handle *h, int blocks, int iters, int n, void *scratch);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,8 @@ EXPORTED = (
     "mpps_axpy", "mpps_powers", "mpps_assemble_blocks", "mpps_one_norm",
     "mpps_horner_step", "mpps_horner_scalar_top", "mpps_probe_fma",
     "mpps_assemble_blocks_dist", "mpps_colmax", "mpps_slice", "mpps_gemm_sliced",
-    "mpps_horner_step_sliced", "mpps_oz_slices_for", "mpps_probe_i8mma",
+    "mpps_horner_step_sliced", "mpps_oz_slices_for", "mpps_probe_i8mma", "mpps_debug_oz_trace",
+    "mpps_debug_oz_flags", "mpps_debug_probe_i8mma_n",
 )
 
 
@@ -127,6 +128,11 @@ def load_library(path: Optional[str] = None):
         lib.mpps_horner_step_sliced.argtypes = [vp, sp, sp, ip, mp, mp, vp, ip, vp, vp, vp]
         lib.mpps_oz_slices_for.argtypes = [ip]
         lib.mpps_probe_i8mma.argtypes = [vp, ip, ip, vp]
+        lib.mpps_debug_oz_trace.argtypes = [vp]
+        lib.mpps_debug_oz_trace.restype = None
+        lib.mpps_debug_oz_flags.argtypes = [ip]
+        lib.mpps_debug_oz_flags.restype = None
+        lib.mpps_debug_probe_i8mma_n.argtypes = [vp, ip, ip, ip, vp]
         for name in EXPORTED:
             getattr(lib, name).restype = getattr(lib, name).restype or ip
         if path is None:

@@ -908,7 +908,7 @@ static int make_slice_map(mpps_handle *h, CUtensorMap *map, const mpps_slices *s
 
 template <int S, int NT, int FO, int MODE>
 static int launch_oz_tma(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
-  constexpr size_t smem = oz::oz_tma_smem_bytes<S, NT>();
+  constexpr size_t smem = oz::oz_tma_smem_bytes<S, NT, FO, MODE>();
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_tma_kernel<S, NT, FO, MODE>,
@@ -936,7 +936,7 @@ static int dispatch_oz(mpps_handle *h, int S, int fo, int mode, const oz::OzArgs
 
 template <int S, int NT, int FO, int MODE>
 static int launch_oz_ring(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
-  constexpr size_t smem = oz::OzRing<S, NT>::SMEM;
+  constexpr size_t smem = oz::oz_ring_smem_bytes<S, NT, FO, MODE>();
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_ring_kernel<S, NT, FO, MODE>,
@@ -960,7 +960,7 @@ static int dispatch_oz_ring(mpps_handle *h, int S, int fo, int mode, const oz::O
   return set_err(h, MPPS_EFMT, "tensor-core GEMM: no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
 }
 
-static int oz_mode() {   // 0 cp.async, 1 TMA two-stage, 2 TMA streamed planes, 3 (default) streamed for qd only
+static int oz_mode() {   // 0 cp.async, 1 TMA stage ring, 2 TMA streamed planes, 3 (default) streamed for S >= 16
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("MPPS_OZ_TMA");
@@ -970,17 +970,24 @@ static int oz_mode() {   // 0 cp.async, 1 TMA two-stage, 2 TMA streamed planes, 
 }
 
 
+// diagnostics: per-CTA phase timestamps of the next TMA-fed GEMMs
+static unsigned long long *g_oz_trace = nullptr;
+static int g_oz_dbg = 0;
+
 static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, int S, int fo, int mode,
                   const oz::OzArgs &a, int nb) {
   if (oz_mode() == 0) return dispatch_oz(h, S, fo, mode, a, nb);
   oz::OzTmaArgs t;
   memset(&t, 0, sizeof(t));
   const int NT = (S > 16) ? 16 : 32;
-  const bool ring = oz_mode() == 2 || (oz_mode() == 3 && S > 16);
+  // default: streamed-plane ring for dd / qd (S >= 16), 2-4 stage TMA ring below
+  const bool ring = oz_mode() == 2 || (oz_mode() == 3 && S >= 16);
   const int abox = ring ? (S < 4 ? S : 4) : S;
   int rc;
   if ((rc = make_slice_map(h, &t.mapA, A, oz::kTileM, abox)) || (rc = make_slice_map(h, &t.mapB, B, NT, S))) return rc;
   t.A = a.A; t.B = a.B; t.M = a.M; t.N = a.N; t.K = a.K; t.S = a.S; t.C = a.C; t.sel = a.sel; t.epi = a.epi;
+  t.trace = g_oz_trace;
+  t.dbg = g_oz_dbg;
   return ring ? dispatch_oz_ring(h, S, fo, mode, t, nb) : dispatch_oz_tma(h, S, fo, mode, t, nb);
 }
 
@@ -1043,6 +1050,7 @@ int mpps_horner_step_sliced(mpps_handle *h, const mpps_slices *Y, const mpps_sli
   const int M = out->rows, N = out->cols, K = Y ? Y->kpad : 0;
   if ((rc = check_sliced(h, Y, phi, nslices, M, N, 0))) return rc;
   if (Bprev->rows != M || Bprev->cols != N) return set_err(h, MPPS_EINVAL, "horner: operands must match the output");
+  if (fmt_index(Bprev->fmt) == F32) return set_err(h, MPPS_EFMT, "horner: B_{j-1} must be at the working format");
   oz::OzArgs a;
   memset(&a, 0, sizeof(a));
   a.A = sref(Y); a.B = sref(phi); a.M = M; a.N = N; a.K = K; a.S = nslices;
@@ -1054,6 +1062,9 @@ int mpps_horner_step_sliced(mpps_handle *h, const mpps_slices *Y, const mpps_sli
 
 int mpps_oz_slices_for(int fmt) { return oz_slices_for(fmt_index(fmt)); }
 
+void mpps_debug_oz_trace(void *buf) { g_oz_trace = (unsigned long long *)buf; }
+void mpps_debug_oz_flags(int flags) { g_oz_dbg = flags; }
+
 int mpps_probe_i8mma(mpps_handle *h, int blocks, int iters, void *scratch) {
   if (!scratch || blocks < 1 || iters < 1) return set_err(h, MPPS_EINVAL, "probe: bad arguments");
   static bool configured = false;
@@ -1063,6 +1074,15 @@ int mpps_probe_i8mma(mpps_handle *h, int blocks, int iters, void *scratch) {
     configured = true;
   }
   oz::i8_mma_probe_kernel<<<blocks, 128, smem, h->stream>>>(iters, (int *)scratch);
+  return after_launch(h, "i8_mma_probe_kernel");
+}
+
+int mpps_debug_probe_i8mma_n(mpps_handle *h, int blocks, int iters, int n, void *scratch) {
+  if (!scratch || blocks < 1 || iters < 1 || n < 16 || n > 256 || n % 16)
+    return set_err(h, MPPS_EINVAL, "probe: bad arguments");
+  int rc = mpps_probe_i8mma(h, blocks, 1, scratch);  // configures the kernel attribute
+  if (rc) return rc;
+  oz::i8_mma_probe_kernel<<<blocks, 128, 40960 + 2048, h->stream>>>(iters, (int *)scratch, n);
   return after_launch(h, "i8_mma_probe_kernel");
 }
 

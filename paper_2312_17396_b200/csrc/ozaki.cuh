@@ -541,11 +541,55 @@ __device__ __forceinline__ mp::dd combine_dd(const int32_t *D) {
   return acc;
 }
 
+// Column split of the epilogue: warps w and w+4 share TMEM lane quarter
+// w % 4; the first takes columns [0, HALF), the second [HALF, NT).
+template <int S, int NT>
+struct EpiCols {
+  static constexpr int CW = (S > 16) ? 4 : 8;                      // columns per TMEM load
+  static constexpr int HALF = ((NT / 2 + CW - 1) / CW) * CW;
+  static constexpr int MAXC = (NT - HALF > HALF) ? NT - HALF : HALF;
+};
+
+// Operands of the epilogue that do not depend on the MMAs (column
+// exponents; for the fused Horner step the previous block B_prev), loaded
+// by the epilogue warps while the mainloop runs instead of one dependent
+// global load per column afterwards.
+template <int S, int NT, int FO, int MODE>
+struct EpiPre {
+  static constexpr int MAXC = EpiCols<S, NT>::MAXC;
+  static constexpr bool BP = (MODE == 1) && (S <= 16) && (FO != QD);  // dd-width B_prev
+  int eb[MAXC];
+  double bp[BP ? MAXC : 1][2];
+};
+
+template <int S, int NT, int FO, int MODE, typename Args>
+__device__ __forceinline__ void oz_epi_prefetch(const Args &args, EpiPre<S, NT, FO, MODE> &pre, int quarter,
+                                                int c_begin, int c_end, int b, int m0, int n0, int lane) {
+  using P = EpiPre<S, NT, FO, MODE>;
+  const int row = m0 + quarter * 32 + lane;
+#pragma unroll
+  for (int i = 0; i < P::MAXC; ++i) {
+    const int col = n0 + c_begin + i;
+    const bool ok = (c_begin + i < c_end) && col < args.N;
+    pre.eb[i] = ok ? args.B.exps[(long long)b * args.B.rpad + col] : 0;
+    if constexpr (P::BP) {
+      pre.bp[i][0] = pre.bp[i][1] = 0.0;
+      if (ok && row < args.M) {
+        const MatRef &Bp = args.epi.Bprev;
+        const double *bp = (const double *)Bp.data + (long long)b * Bp.bstride + (long long)row * Bp.ld + col;
+        pre.bp[i][0] = bp[0];
+        if (Bp.words > 1) pre.bp[i][1] = bp[Bp.plane];
+      }
+    }
+  }
+}
+
 // Drain the S diagonal accumulators of this thread's TMEM lane for columns
 // [c_begin, c_end) and run the store / fused Horner epilogue.
 template <int S, int NT, int FO, int MODE, typename Args>
-__device__ __forceinline__ void oz_epilogue(const Args &args, uint32_t tmem, int quarter, int c_begin, int c_end,
-                                            int b, int m0, int n0, int lane) {
+__device__ __forceinline__ void oz_epilogue(const Args &args, const EpiPre<S, NT, FO, MODE> &pre, uint32_t tmem,
+                                            int quarter, int c_begin, int c_end, int b, int m0, int n0, int lane) {
+  using P = EpiPre<S, NT, FO, MODE>;
   const int row = m0 + quarter * 32 + lane;
   const int ea = args.A.exps[(long long)b * args.A.rpad + row];
   const MatRef &C = args.C;
@@ -556,8 +600,11 @@ __device__ __forceinline__ void oz_epilogue(const Args &args, uint32_t tmem, int
     if (args.epi.exp_out) eo = args.epi.exp_out[b];
   }
   const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-  constexpr int CW = (S > 16) ? 4 : 8;
-  for (int c0 = c_begin; c0 < c_end; c0 += CW) {
+  constexpr int CW = EpiCols<S, NT>::CW;
+#pragma unroll
+  for (int i0 = 0; i0 < P::MAXC; i0 += CW) {
+    const int c0 = c_begin + i0;
+    if (c0 >= c_end) break;
     int32_t D[S][CW];
 #pragma unroll
     for (int d = 0; d < S; ++d) {
@@ -572,19 +619,14 @@ __device__ __forceinline__ void oz_epilogue(const Args &args, uint32_t tmem, int
       int32_t Dj[S];
 #pragma unroll
       for (int d = 0; d < S; ++d) Dj[d] = D[d][jj];
-      const int eb = args.B.exps[(long long)b * args.B.rpad + col];
+      const int eb = pre.eb[i0 + jj];
       const long long off = (long long)b * C.bstride + (long long)row * C.ld + col;
       if constexpr (S <= 16 && FO != QD) {
         // dd-width epilogue (fp32 / fp64 / dd outputs)
         mp::dd v = combine_dd<S>(Dj);
         const double sc = pow2i(ea + eb - (MODE == 1 ? (ey + ei) : 0));
         v = mp::dd_make(v.hi * sc, v.lo * sc);
-        if constexpr (MODE == 1) {
-          const MatRef &Bp = args.epi.Bprev;
-          const double *bp = (const double *)Bp.data + (long long)b * Bp.bstride + (long long)row * Bp.ld + col;
-          const mp::dd bv = mp::dd_make(bp[0], Bp.words > 1 ? bp[Bp.plane] : 0.0);
-          v = mp::dd_add(bv, v);
-        }
+        if constexpr (MODE == 1) v = mp::dd_add(mp::dd_make(pre.bp[i0 + jj][0], pre.bp[i0 + jj][1]), v);
         if constexpr (FO == DD) {
           if (eo) { const double so = pow2i(eo); v = mp::dd_make(v.hi * so, v.lo * so); }
           double *p = (double *)C.data + off;
@@ -612,6 +654,29 @@ __device__ __forceinline__ void oz_epilogue(const Args &args, uint32_t tmem, int
   }
 }
 
+
+// All MMAs of one K step, fully unrolled: A_s x [B_0 .. B_{S-1-s}] (the B
+// planes are stacked along N) lands in diagonals s .. S-1 (TMEM column
+// offset s*NT), split at the 256-column instruction limit.  Descriptors are
+// compile-time offsets on two base descriptors (the 14-bit start-address
+// field cannot carry: shared addresses < 228 KB), so the issuing thread
+// spends a few instructions per MMA instead of ~150 cycles of descriptor
+// and loop arithmetic (which left the tensor pipe idle between MMAs).
+// acc0: accumulate flag of the K step's first write to every diagonal.
+template <int S, int NT, uint32_t A_SLICE, uint32_t B_SLICE>
+__device__ __forceinline__ void oz_issue_kstep(uint32_t tmem, uint64_t ad0, uint64_t bd0, uint32_t acc0) {
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+#pragma unroll
+    for (int t0 = 0; t0 < S - s; t0 += 256 / NT) {
+      constexpr int kMaxN = 256;
+      const int nn = ((S - s - t0) * NT > kMaxN) ? kMaxN : (S - s - t0) * NT;
+      mma_i8(tmem + (uint32_t)((s + t0) * NT), ad0 + (uint64_t)((s * A_SLICE) >> 4),
+             bd0 + (uint64_t)((t0 * B_SLICE) >> 4), idesc_i8(kTileM, nn), s > 0 ? 1u : acc0);
+    }
+  }
+}
+
 // ------------------------------------------------- TMA-fed pipeline
 // Digit planes [S][batch][rpad][kpad] viewed by TMA as a 3-D tensor
 // (k, row, slice); one box = 32 B of K x R rows x all S planes, written
@@ -626,37 +691,225 @@ struct OzTmaArgs {
   MatRef C;
   const int *sel;
   HornerEpi epi;
+  unsigned long long *trace;  // diagnostics (mpps_debug_oz_trace): per-CTA phase timestamps or null
+  int dbg;                     // diagnostics: bit 0 skip MMAs (feed only), bit 1 skip TMA (MMA only)
 };
 
-template <int S, int NT>
-__host__ __device__ constexpr int oz_tma_stages() {
-  return (int)(((size_t)200 * 1024) / oz_stage_bytes<S, NT>()) >= 4 ? 4 : (int)(((size_t)200 * 1024) / oz_stage_bytes<S, NT>());
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
-template <int S, int NT>
-__host__ __device__ constexpr size_t oz_tma_smem_bytes() { return oz_tma_stages<S, NT>() * oz_stage_bytes<S, NT>() + 2048; }
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+
+// Epilogue staging tile for the fused Horner step (dd-width outputs,
+// NT = 32): 2 words x 128 rows x NT columns of fp64, swizzled so that both
+// the per-row (thread = row) and the per-column (lane = column, coalesced
+// global access) passes are conflict-free.  B_prev is copied into it with
+// coalesced cp.async during the mainloop (a per-thread row-wise prefetch
+// competes with the TMA feed and slows the mainloop ~2.5x).
+template <int S, int NT, int FO, int MODE>
+__host__ __device__ constexpr bool oz_staged() { return S <= 16 && FO != QD && NT == 32 && MODE == 1; }
+template <int S, int NT, int FO, int MODE>
+__host__ __device__ constexpr uint32_t oz_ebuf_bytes() {
+  return oz_staged<S, NT, FO, MODE>() ? 2u * kTileM * NT * 8u : 0u;
+}
+// Co-resident CTAs per SM: one CTA's epilogue overlaps the other's
+// mainloop.  Needs <= 256 TMEM columns (S <= 8) and shared memory for two.
+template <int S, int MODE>
+__host__ __device__ constexpr int oz_ctas_per_sm() { return (MODE == 0 ? S <= 8 : S <= 4) ? 2 : 1; }
+template <int S, int NT, int FO = DD, int MODE = 0>
+__host__ __device__ constexpr int oz_tma_stages() {
+  constexpr size_t cap = (oz_ctas_per_sm<S, MODE>() == 2 ? (size_t)113 : (size_t)226) * 1024;
+  constexpr size_t ring = cap - oz_ebuf_bytes<S, NT, FO, MODE>() - 2048;
+  return (int)(ring / oz_stage_bytes<S, NT>()) >= 4 ? 4 : (int)(ring / oz_stage_bytes<S, NT>());
+}
+template <int S, int NT, int FO = DD, int MODE = 0>
+__host__ __device__ constexpr size_t oz_tma_smem_bytes() {
+  return oz_tma_stages<S, NT, FO, MODE>() * oz_stage_bytes<S, NT>() + oz_ebuf_bytes<S, NT, FO, MODE>() + 2048;
+}
+__device__ __forceinline__ int ebuf_idx(int w, int r, int c) { return ((w * kTileM + r) << 5) + (c ^ (r & 15)); }
+
+// Staged epilogue, phase 1 (epilogue warps 2..7, during the mainloop):
+// column exponents and, for the fused Horner step, the B_prev tile are
+// copied into shared memory with coalesced cp.async (lane = column).
+template <int S, int NT, int FO, int MODE, typename Args>
+__device__ __forceinline__ void oz_stage_load(const Args &args, double *ebuf, int *ebs, int b, int m0, int n0,
+                                              int wid, int nw, int lane) {
+  const int col = n0 + lane;
+  if (wid == 0) ebs[lane] = col < args.N ? args.B.exps[(long long)b * args.B.rpad + col] : 0;
+  if constexpr (MODE == 1) {
+    const MatRef &Bp = args.epi.Bprev;
+    const bool two = Bp.words > 1;
+    const double *base = (const double *)Bp.data + (long long)b * Bp.bstride;
+#pragma unroll 4
+    for (int r = wid; r < kTileM; r += nw) {
+      const int row = m0 + r;
+      const bool ok = row < args.M && col < args.N;
+      const double *src = ok ? base + (long long)row * Bp.ld + col : base;
+      cp_async_zfill<8>(ebuf + ebuf_idx(0, r, lane), src, ok);
+      cp_async_zfill<8>(ebuf + ebuf_idx(1, r, lane), ok && two ? src + Bp.plane : base, ok && two);
+    }
+    cp_async_commit();
+  }
+}
+
+// Phase 2 (all 8 warps, after the MMAs): thread = row; its columns are
+// combined from TMEM, the B_prev words read from (and the dd-width result
+// written back to) the staging tile.
+template <int S, int NT, int FO, int MODE, typename Args>
+__device__ __forceinline__ void oz_stage_compute(const Args &args, double *ebuf, const int *ebs, uint32_t tmem,
+                                                 int quarter, int c_begin, int c_end, int b, int m0, int lane) {
+  constexpr int CW = 8;
+  const int r = quarter * 32 + lane;
+  const int row = m0 + r;
+  const int ea = row < args.M ? args.A.exps[(long long)b * args.A.rpad + row] : 0;
+  int ey = 0, ei = 0, eo = 0;
+  if constexpr (MODE == 1) {
+    if (args.epi.exp_y) ey = args.epi.exp_y[b];
+    if (args.epi.exp_in) ei = args.epi.exp_in[b];
+    if (args.epi.exp_out) eo = args.epi.exp_out[b];
+  }
+  const double so = pow2i(eo);
+  const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+#pragma unroll
+  for (int i0 = 0; i0 < NT / 2; i0 += CW) {
+    const int c0 = c_begin + i0;
+    if (c0 >= c_end) break;
+    int32_t D[S][CW];
+#pragma unroll
+    for (int d = 0; d < S; ++d) tmem_ld8(lane_base + (uint32_t)(d * NT + c0), D[d]);
+    tmem_ld_wait();
+#pragma unroll
+    for (int jj = 0; jj < CW; ++jj) {
+      const int c = c0 + jj;
+      int32_t Dj[S];
+#pragma unroll
+      for (int d = 0; d < S; ++d) Dj[d] = D[d][jj];
+      mp::dd v = combine_dd<S>(Dj);
+      const double sc = pow2i(ea + ebs[c] - (MODE == 1 ? (ey + ei) : 0));
+      v = mp::dd_make(v.hi * sc, v.lo * sc);
+      const int i0w = ebuf_idx(0, r, c), i1w = ebuf_idx(1, r, c);
+      if constexpr (MODE == 1) v = mp::dd_add(mp::dd_make(ebuf[i0w], ebuf[i1w]), v);
+      if (eo) v = mp::dd_make(v.hi * so, v.lo * so);
+      if constexpr (FO == DD) {
+        ebuf[i0w] = v.hi;
+        ebuf[i1w] = v.lo;
+      } else if constexpr (FO == F64) {
+        ebuf[i0w] = v.hi;
+      } else {
+        ebuf[i0w] = (double)mp::dd_to_float(v.hi, v.lo);
+      }
+    }
+  }
+}
+
+// Phase 3 (all 8 warps): coalesced stores of the tile, lane = column.
+template <int FO>
+__device__ __forceinline__ void oz_stage_store(const MatRef &C, const double *ebuf, int M, int N, int b, int m0,
+                                               int n0, int warp, int lane) {
+  const int col = n0 + lane;
+  if (col >= N) return;
+#pragma unroll 4
+  for (int r = warp; r < kTileM; r += 8) {
+    const int row = m0 + r;
+    if (row >= M) break;
+    const long long off = (long long)b * C.bstride + (long long)row * C.ld + col;
+    const double w0 = ebuf[ebuf_idx(0, r, lane)];
+    if constexpr (FO == DD) {
+      double *p = (double *)C.data + off;
+      p[0] = w0;
+      p[C.plane] = ebuf[ebuf_idx(1, r, lane)];
+    } else if constexpr (FO == F64) {
+      ((double *)C.data)[off] = w0;
+    } else {
+      ((float *)C.data)[off] = (float)w0;  // exact: w0 holds an fp32 value
+    }
+  }
+}
+
+
+// Epilogue of the TMA / ring kernels (all 8 warps): operands that do not
+// depend on the MMAs are loaded while the mainloop runs (staged B_prev via
+// coalesced cp.async, or per-thread register prefetch), then the TMEM
+// diagonals are combined and stored.  Ends with every thread past its
+// TMEM reads (the caller deallocates).
+template <int S, int NT, int FO, int MODE, bool STAGED>
+__device__ __forceinline__ void oz_kernel_epilogue(const OzTmaArgs &args, double *ebuf, int *ebs, uint32_t tmem,
+                                                   uint64_t *done, int warp, int lane, int b, int m0, int n0,
+                                                   unsigned long long *tr) {
+  // warps w and w+4 share TMEM lane quarter w % 4 and split the columns
+  const int quarter = warp & 3, half = warp >> 2;
+  const int cb = half ? EpiCols<S, NT>::HALF : 0, ce = half ? NT : EpiCols<S, NT>::HALF;
+  if constexpr (STAGED) {
+    if (warp >= 2) {
+      oz_stage_load<S, NT, FO, MODE>(args, ebuf, ebs, b, m0, n0, warp - 2, 6, lane);
+      if constexpr (MODE == 1) cp_async_wait<0>();
+    }
+    __syncwarp();
+    mbar_wait(smem_u32(done), 0);
+    fence_after();
+    if (tr) tr[2] = globaltimer();
+    __syncthreads();  // staged B_prev / exponents visible to every warp
+    fence_after();
+    oz_stage_compute<S, NT, FO, MODE>(args, ebuf, ebs, tmem, quarter, cb, ce, b, m0, lane);
+    __syncthreads();
+    oz_stage_store<FO>(args.C, ebuf, args.M, args.N, b, m0, n0, warp, lane);
+  } else {
+    EpiPre<S, NT, FO, MODE> pre;
+    oz_epi_prefetch<S, NT, FO, MODE>(args, pre, quarter, cb, ce, b, m0, n0, lane);
+    __syncwarp();
+    mbar_wait(smem_u32(done), 0);
+    fence_after();
+    if (tr) tr[2] = globaltimer();
+    oz_epilogue<S, NT, FO, MODE>(args, pre, tmem, quarter, cb, ce, b, m0, n0, lane);
+  }
+  fence_before();
+  __syncthreads();
+  if (tr) tr[3] = globaltimer();
+}
+
+__device__ __forceinline__ unsigned long long *oz_trace_begin(const OzTmaArgs &args) {
+  if (!args.trace || threadIdx.x != 64) return nullptr;
+  unsigned long long *tr =
+      args.trace + 5ull * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+  tr[0] = globaltimer();
+  tr[4] = smid();
+  return tr;
+}
 
 template <int S, int NT, int FO, int MODE>
-__global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_tma_kernel(const __grid_constant__ OzTmaArgs args) {
-  constexpr int STAGES = oz_tma_stages<S, NT>();
-  static_assert(STAGES >= 1, "stage does not fit");
+__global__ void __launch_bounds__(kThreadsEpi, oz_ctas_per_sm<S, MODE>()) oz_gemm_tma_kernel(const __grid_constant__ OzTmaArgs args) {
+  constexpr int STAGES = oz_tma_stages<S, NT, FO, MODE>();
+  static_assert(STAGES >= 1, "stage ring does not fit");
   constexpr uint32_t STAGE = (uint32_t)oz_stage_bytes<S, NT>();
   constexpr uint32_t A_SLICE = kTileM * kKStep;   // 4 KB
   constexpr uint32_t B_SLICE = NT * kKStep;
   constexpr int TCOLS = tmem_cols_for(S * NT);
 
+  constexpr bool STAGED = oz_staged<S, NT, FO, MODE>();
+  constexpr uint32_t EBUF = oz_ebuf_bytes<S, NT, FO, MODE>();
+
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KB aligned stage ring (swizzle atoms must not straddle)
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE);
+  double *ebuf = reinterpret_cast<double *>(smem + STAGES * STAGE);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE + EBUF);
   uint64_t *empty = full + STAGES;
   uint64_t *done = empty + STAGES;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+  int *ebs = reinterpret_cast<int *>(tmem_slot + 4);  // NT column exponents
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int bz = blockIdx.z;
   const int b = args.sel ? args.sel[bz] : bz;
   const int m0 = blockIdx.y * kTileM, n0 = blockIdx.x * NT;
   const int ksteps = args.A.kpad / kKStep;
+  unsigned long long *tr = oz_trace_begin(args);
 
   if (warp == 0) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
   if (tid == 32) {
@@ -673,6 +926,7 @@ __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_tma_kernel(const __gri
   const uint32_t tmem = *tmem_slot;
   const uint32_t sbase = smem_u32(smem);
   const int rowA = b * args.A.rpad + m0, rowB = b * args.B.rpad + n0;
+  if (tr) tr[1] = globaltimer();
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer
@@ -680,9 +934,13 @@ __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_tma_kernel(const __gri
       const int st = kb % STAGES;
       if (kb >= STAGES) mbar_wait(smem_u32(&empty[st]), ((kb / STAGES) - 1) & 1);
       const uint32_t sa = sbase + st * STAGE;
-      mbar_expect_tx(smem_u32(&full[st]), STAGE);
-      tma_load_3d(sa, &args.mapA, kb * kKStep, rowA, 0, smem_u32(&full[st]));
-      tma_load_3d(sa + S * A_SLICE, &args.mapB, kb * kKStep, rowB, 0, smem_u32(&full[st]));
+      if (args.dbg & 2) {
+        mbar_expect_tx(smem_u32(&full[st]), 0);
+      } else {
+        mbar_expect_tx(smem_u32(&full[st]), STAGE);
+        tma_load_3d(sa, &args.mapA, kb * kKStep, rowA, 0, smem_u32(&full[st]));
+        tma_load_3d(sa + S * A_SLICE, &args.mapB, kb * kKStep, rowB, 0, smem_u32(&full[st]));
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer
@@ -692,37 +950,14 @@ __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_tma_kernel(const __gri
       fence_after();
       const uint32_t sa = sbase + st * STAGE;
       const uint32_t sb = sa + S * A_SLICE;
-#pragma unroll 1
-      for (int s = 0; s < S; ++s) {
-        const uint64_t ad = umma_desc(sa + s * A_SLICE, 16, 256, 6);
-        int ncols = (S - s) * NT;
-        int t0 = 0;
-        while (ncols > 0) {
-          const int nn = ncols > 256 ? 256 : ncols;
-          const uint64_t bd = umma_desc(sb + t0 * B_SLICE, 16, 256, 6);
-          mma_i8(tmem + (uint32_t)((s + t0) * NT), ad, bd, idesc_i8(kTileM, nn), (kb > 0 || s > 0) ? 1u : 0u);
-          t0 += nn / NT;
-          ncols -= nn;
-        }
-      }
+      if (!(args.dbg & 1))
+        oz_issue_kstep<S, NT, A_SLICE, B_SLICE>(tmem, umma_desc(sa, 16, 256, 6), umma_desc(sb, 16, 256, 6),
+                                                kb > 0 ? 1u : 0u);
       mma_commit(smem_u32(&empty[st]));
     }
     mma_commit(smem_u32(done));
   }
-  __syncwarp();
-  mbar_wait(smem_u32(done), 0);
-  fence_after();
-
-  // ---------------------------------------------------------- epilogue
-  // warps w and w+4 share TMEM lane quarter w % 4 and split the columns
-  {
-    const int quarter = warp & 3, half = warp >> 2;
-    constexpr int CW = (S > 16) ? 4 : 8;
-    constexpr int HALF = ((NT / 2 + CW - 1) / CW) * CW;
-    oz_epilogue<S, NT, FO, MODE>(args, tmem, quarter, half ? HALF : 0, half ? NT : HALF, b, m0, n0, lane);
-  }
-  fence_before();
-  __syncthreads();
+  oz_kernel_epilogue<S, NT, FO, MODE, STAGED>(args, ebuf, ebs, tmem, done, warp, lane, b, m0, n0, tr);
   if (warp == 0) tmem_dealloc<TCOLS>(tmem);
 }
 
@@ -731,6 +966,37 @@ __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_tma_kernel(const __gri
 // ring; A planes stream through a deeper ring in groups of SG planes
 // (16 KB), so many loads are in flight while the wide MMAs of earlier
 // groups run.  Same MMA sequence and epilogue as oz_gemm_tma_kernel.
+
+// The MMAs of planes s0 .. s0+SG-1 of one K step (A planes of a ring group
+// at ad0 + (s - s0) * A_SLICE), fully unrolled like oz_issue_kstep.
+template <int S, int NT, uint32_t A_SLICE, uint32_t B_SLICE, int S0, int SG>
+__device__ __forceinline__ void oz_issue_planes(uint32_t tmem, uint64_t ad0, uint64_t bd0, uint32_t acc0) {
+#pragma unroll
+  for (int s = S0; s < S0 + SG && s < S; ++s) {
+#pragma unroll
+    for (int t0 = 0; t0 < S - s; t0 += 256 / NT) {
+      const int nn = ((S - s - t0) * NT > 256) ? 256 : (S - s - t0) * NT;
+      mma_i8(tmem + (uint32_t)((s + t0) * NT), ad0 + (uint64_t)(((s - S0) * A_SLICE) >> 4),
+             bd0 + (uint64_t)((t0 * B_SLICE) >> 4), idesc_i8(kTileM, nn), s > 0 ? 1u : acc0);
+    }
+  }
+}
+
+template <int S, int NT, uint32_t A_SLICE, uint32_t B_SLICE, int SG, int G = 0>
+__device__ __forceinline__ void oz_ring_groups(uint32_t tmem, uint64_t bd0, uint32_t acc0, int &ai, uint8_t *aring,
+                                               uint64_t *a_full, uint64_t *a_empty, int nas, uint32_t a_bytes) {
+  if constexpr (G * SG < S) {
+    const int ast = ai % nas;
+    mbar_wait(smem_u32(&a_full[ast]), (ai / nas) & 1);
+    fence_after();
+    oz_issue_planes<S, NT, A_SLICE, B_SLICE, G * SG, SG>(tmem, umma_desc(smem_u32(aring + ast * a_bytes), 16, 256, 6),
+                                                         bd0, acc0);
+    mma_commit(smem_u32(&a_empty[ast]));
+    ++ai;
+    oz_ring_groups<S, NT, A_SLICE, B_SLICE, SG, G + 1>(tmem, bd0, acc0, ai, aring, a_full, a_empty, nas, a_bytes);
+  }
+}
+
 template <int S, int NT>
 struct OzRing {
   static constexpr int SG = S < 4 ? S : 4;                       // planes per A stage
@@ -744,6 +1010,8 @@ struct OzRing {
   static constexpr uint32_t B_STRIDE = (B_BYTES + 1023) / 1024 * 1024;
   static constexpr size_t SMEM = (size_t)NBS * B_STRIDE + (size_t)NAS * A_BYTES + 2048;
 };
+template <int S, int NT, int FO, int MODE>
+__host__ __device__ constexpr size_t oz_ring_smem_bytes() { return OzRing<S, NT>::SMEM + oz_ebuf_bytes<S, NT, FO, MODE>(); }
 
 template <int S, int NT, int FO, int MODE>
 __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_ring_kernel(const __grid_constant__ OzTmaArgs args) {
@@ -752,21 +1020,26 @@ __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_ring_kernel(const __gr
   constexpr uint32_t B_SLICE = NT * kKStep;
   constexpr int TCOLS = tmem_cols_for(S * NT);
 
+  constexpr bool STAGED = oz_staged<S, NT, FO, MODE>();
+  constexpr uint32_t EBUF = oz_ebuf_bytes<S, NT, FO, MODE>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t *bring = smem;
   uint8_t *aring = smem + R::NBS * R::B_STRIDE;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(aring + R::NAS * R::A_BYTES);
+  double *ebuf = reinterpret_cast<double *>(aring + R::NAS * R::A_BYTES);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(aring + R::NAS * R::A_BYTES + EBUF);
   uint64_t *b_full = bar, *b_empty = bar + R::NBS;
   uint64_t *a_full = bar + 2 * R::NBS, *a_empty = a_full + R::NAS;
   uint64_t *done = a_empty + R::NAS;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+  int *ebs = reinterpret_cast<int *>(tmem_slot + 4);  // NT column exponents
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int bz = blockIdx.z;
   const int b = args.sel ? args.sel[bz] : bz;
   const int m0 = blockIdx.y * kTileM, n0 = blockIdx.x * NT;
   const int ksteps = args.A.kpad / kKStep;
+  unsigned long long *tr = oz_trace_begin(args);
 
   if (warp == 0) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
   if (tid == 32) {
@@ -780,6 +1053,7 @@ __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_ring_kernel(const __gr
   fence_after();
   const uint32_t tmem = *tmem_slot;
   const int rowA = b * args.A.rpad + m0, rowB = b * args.B.rpad + n0;
+  if (tr) tr[1] = globaltimer();
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer: B step, then the A plane groups of that step
@@ -804,53 +1078,20 @@ __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_ring_kernel(const __gr
       const int bst = kb % R::NBS;
       mbar_wait(smem_u32(&b_full[bst]), (kb / R::NBS) & 1);
       const uint32_t sb = smem_u32(bring + bst * R::B_STRIDE);
-      for (int g = 0; g < R::NG; ++g, ++ai) {
-        const int ast = ai % R::NAS;
-        mbar_wait(smem_u32(&a_full[ast]), (ai / R::NAS) & 1);
-        fence_after();
-        const uint32_t sa = smem_u32(aring + ast * R::A_BYTES);
-#pragma unroll 1
-        for (int q = 0; q < R::SG; ++q) {
-          const int s = g * R::SG + q;
-          if (s >= S) break;
-          const uint64_t ad = umma_desc(sa + q * A_SLICE, 16, 256, 6);
-          int ncols = (S - s) * NT;
-          int t0 = 0;
-          while (ncols > 0) {
-            const int nn = ncols > 256 ? 256 : ncols;
-            const uint64_t bd = umma_desc(sb + t0 * B_SLICE, 16, 256, 6);
-            mma_i8(tmem + (uint32_t)((s + t0) * NT), ad, bd, idesc_i8(kTileM, nn), (kb > 0 || s > 0) ? 1u : 0u);
-            t0 += nn / NT;
-            ncols -= nn;
-          }
-        }
-        mma_commit(smem_u32(&a_empty[ast]));
-      }
+      oz_ring_groups<S, NT, A_SLICE, B_SLICE, R::SG>(tmem, umma_desc(sb, 16, 256, 6), kb > 0 ? 1u : 0u, ai, aring,
+                                                      a_full, a_empty, R::NAS, R::A_BYTES);
       mma_commit(smem_u32(&b_empty[bst]));
     }
     mma_commit(smem_u32(done));
   }
-  __syncwarp();
-  mbar_wait(smem_u32(done), 0);
-  fence_after();
-
-  // ---------------------------------------------------------- epilogue
-  // warps w and w+4 share TMEM lane quarter w % 4 and split the columns
-  {
-    const int quarter = warp & 3, half = warp >> 2;
-    constexpr int CW = (S > 16) ? 4 : 8;
-    constexpr int HALF = ((NT / 2 + CW - 1) / CW) * CW;
-    oz_epilogue<S, NT, FO, MODE>(args, tmem, quarter, half ? HALF : 0, half ? NT : HALF, b, m0, n0, lane);
-  }
-  fence_before();
-  __syncthreads();
+  oz_kernel_epilogue<S, NT, FO, MODE, STAGED>(args, ebuf, ebs, tmem, done, warp, lane, b, m0, n0, tr);
   if (warp == 0) tmem_dealloc<TCOLS>(tmem);
 }
 
 // INT8 tensor-pipe peak probe: one CTA per SM issues back-to-back
 // 128x256x32 kind::i8 MMAs (operands: 40 KB of zeroed shared memory) into a
 // 256-column TMEM accumulator.  2*128*256*32 ops per MMA.
-__global__ void __launch_bounds__(128, 1) i8_mma_probe_kernel(int iters, int *out) {
+__global__ void __launch_bounds__(128, 1) i8_mma_probe_kernel(int iters, int *out, int n = 256) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t *done = reinterpret_cast<uint64_t *>(smem + 40960);
@@ -869,7 +1110,8 @@ __global__ void __launch_bounds__(128, 1) i8_mma_probe_kernel(int iters, int *ou
   if (threadIdx.x == 0) {
     const uint32_t sa = smem_u32(smem), sb = sa + 4096;
     const uint64_t ad = umma_desc(sa, 16, 256, 6), bd = umma_desc(sb, 16, 256, 6);
-    for (int i = 0; i < iters; ++i) mma_i8(tmem, ad, bd, idesc_i8(128, 256), i > 0 ? 1u : 0u);
+    const uint32_t idesc = idesc_i8(128, n);
+    for (int i = 0; i < iters; ++i) mma_i8(tmem, ad, bd, idesc, i > 0 ? 1u : 0u);
     mma_commit(smem_u32(done));
   }
   __syncwarp();

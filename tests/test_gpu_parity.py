@@ -244,6 +244,24 @@ def test_errors_mirror_reference(cuda):
         m.ps_mixed_exp(np.zeros((3, 3)), 4, m.PrecisionCtx(64))
 
 
+def test_horner_rejects_fp32_previous_block(cuda):
+    """The fused Horner step reads B_{j-1} as fp64 words: an fp32 block is
+    rejected by both engines (blocks are assembled at >= fp64)."""
+    from paper_2312_17396_b200 import _lib
+    from paper_2312_17396_b200.precision import MatBatch
+    h = _lib.handle_for()
+    Y = MatBatch.zeros(15, 1, 8, device="cuda")
+    P = MatBatch.zeros(7, 1, 8, device="cuda")
+    Bp = MatBatch.zeros(7, 1, 8, device="cuda")
+    out = MatBatch.zeros(7, 1, 8, device="cuda")
+    ys, ps = h.slice(Y, 0, 4), h.slice(P, 1, 4)
+    err = mp().UnsupportedPrecisionError
+    with pytest.raises(err, match="working format"):
+        h.horner_step_sliced(ys, ps, 4, Bp, out, fmt_in=7)
+    with pytest.raises(err, match="working format"):
+        h.horner_step(P, P, Bp, out)
+
+
 def test_cfg2_full_size_properties(cuda):
     """Config 2 at full size (64 x n=256, dd): a size-independent check --
     p(X) p(-X) = I up to the Taylor truncation (1/31! ~ 1e-34) and the

@@ -73,3 +73,68 @@ if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "tc":
     for fmt, B, n in ((31, 64, 256), (31, 16, 1024), (31, 1, 2048), (31, 1, 8192), (15, 64, 256), (15, 1, 4096),
                       (63, 1, 1024), (63, 1, 2048)):
         bench_tc(fmt, B, n)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "sweep":
+    # fixed per-tile cost vs per-K-step cost of the TC kernels
+    for fmt in (7, 15, 31):
+        for B, n in ((64, 64), (64, 128), (64, 256), (64, 512), (16, 1024), (4, 2048)):
+            bench_tc(fmt, B, n)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "horner":
+    # fused Horner step vs plain GEMM on the same slices (cfg2 fp32 level)
+    h = _lib.handle_for()
+    B, n = 64, 256
+    Y = MatBatch.empty(31, B, n, device="cuda"); Y.data.normal_(); Y.data[1:] *= 1e-17
+    P = MatBatch.empty(7, B, n, device="cuda"); P.data.normal_()
+    Bp = MatBatch.empty(31, B, n, device="cuda"); Bp.data.normal_(); Bp.data[1:] *= 1e-17
+    out = MatBatch.empty(7, B, n, device="cuda")
+    for SA, fo in ((16, 7), (4, 7)):
+        ys = h.slice(Y, 0, SA)
+        ps = h.slice(P, 1, 4)
+        e_in = torch.zeros(B, dtype=torch.int32, device="cuda")
+        e_out = torch.zeros(B, dtype=torch.int32, device="cuda")
+
+        def t(fn, reps=10):
+            fn(); torch.cuda.synchronize()
+            best = 1e9
+            for _ in range(reps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(); fn(); b.record(); torch.cuda.synchronize()
+                best = min(best, a.elapsed_time(b))
+            return best * 1e3
+        print(f"Y planes {SA}: gemm_sliced S=4 {t(lambda: h.gemm_sliced(ys, ps, 4, out)):.1f} us; "
+              f"horner no exps {t(lambda: h.horner_step_sliced(ys, ps, 4, Bp, out, fmt_in=7)):.1f} us; "
+              f"horner exps {t(lambda: h.horner_step_sliced(ys, ps, 4, Bp, out, None, None, e_in, e_out, fmt_in=7)):.1f} us",
+              flush=True)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "horner32":
+    # fp32 Horner level: SIMT FFMA kernel vs INT8 tensor cores (S = 4)
+    h = _lib.handle_for()
+    B, n = 64, 256
+    Y = MatBatch.empty(31, B, n, device="cuda"); Y.data.normal_(); Y.data[1:] *= 1e-17
+    Y32 = MatBatch.empty(7, B, n, device="cuda"); h.convert(Y, Y32)
+    P = MatBatch.empty(7, B, n, device="cuda"); P.data.normal_()
+    Bp = MatBatch.empty(31, B, n, device="cuda"); Bp.data.normal_(); Bp.data[1:] *= 1e-17
+    out = MatBatch.empty(7, B, n, device="cuda")
+    ys, ps = h.slice(Y, 0, 16), h.slice(P, 1, 4)
+
+    def t(fn, reps=10):
+        fn(); torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(); fn(); b.record(); torch.cuda.synchronize()
+            best = min(best, a.elapsed_time(b))
+        return best * 1e3
+    print(f"fp32 level: simt horner {t(lambda: h.horner_step(Y32, P, Bp, out)):.1f} us "
+          f"(+ convert Y {t(lambda: h.convert(Y, Y32)):.1f} us); tc horner {t(lambda: h.horner_step_sliced(ys, ps, 4, Bp, out, fmt_in=7)):.1f} us "
+          f"(+ slice phi {t(lambda: h.slice(P, 1, 4)):.1f} us); simt gemm {t(lambda: h.gemm(Y32, P, out)):.1f} us", flush=True)
+    Y64 = MatBatch.empty(15, B, n, device="cuda"); h.convert(Y, Y64)
+    P64 = MatBatch.empty(15, B, n, device="cuda"); P64.data.normal_()
+    o64 = MatBatch.empty(15, B, n, device="cuda")
+    ps8 = h.slice(P64, 1, 8)
+    print(f"fp64 level: simt horner {t(lambda: h.horner_step(Y64, P64, Bp, o64)):.1f} us; "
+          f"tc horner {t(lambda: h.horner_step_sliced(ys, ps8, 8, Bp, o64, fmt_in=15)):.1f} us", flush=True)
