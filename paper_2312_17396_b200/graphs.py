@@ -10,6 +10,13 @@ captured once per problem shape into two CUDA graphs and replayed:
   post graph  Horner chain for this plan structure (one graph per distinct
               (level formats, members) grouping; cfg2's 64 matrices share one)
 
+The Horner graph depends on the plan only through its structure (the level
+scalings are computed on the device from the norms), so the graph of the
+previous evaluation's structure is replayed speculatively right after the
+pre graph and the host plans while it runs; if the new plan's structure
+differs, the right graph is replayed after it (same stream, overwriting
+the speculative result).  Results are identical either way.
+
 Buffers live in the graphs' private memory pool and are reused across
 replays; inputs are copied into a static buffer and the result is cloned
 out, so every call returns independent tensors.  Any capture failure turns
@@ -26,6 +33,7 @@ import numpy as np
 from .precision import FP64, MatBatch
 
 _ENABLED = os.environ.get("MPPS_GRAPHS", "1") != "0"
+_SPECULATE = os.environ.get("MPPS_SPECULATE", "1") != "0"
 _CACHE: Dict[tuple, "_ShapeGraphs"] = {}
 _FAILED = set()
 
@@ -53,9 +61,21 @@ class _ShapeGraphs:
         self.norms_pin = None
         self.post: Dict[tuple, tuple] = {}
         self.pre_launches = 0
+        self.last_post = None     # structure of the previous evaluation (speculation)
 
 
 _LAST_LAUNCHES = 0
+_SPEC_STATS = {"hit": 0, "miss": 0}
+
+
+def set_speculation(flag: bool) -> None:
+    global _SPECULATE
+    _SPECULATE = bool(flag)
+
+
+def speculation_stats() -> dict:
+    """Speculative Horner replays that matched / missed the plan."""
+    return dict(_SPEC_STATS)
 
 
 def last_launches() -> int:
@@ -68,10 +88,10 @@ class Pending:
     """A submitted evaluation: the pre graph is enqueued and the norms are
     on their way to pinned memory (``ready`` is recorded after the copy)."""
 
-    __slots__ = ("g", "ready", "timer")
+    __slots__ = ("g", "ready", "timer", "spec")
 
-    def __init__(self, g, ready, timer):
-        self.g, self.ready, self.timer = g, ready, timer
+    def __init__(self, g, ready, timer, spec=None):
+        self.g, self.ready, self.timer, self.spec = g, ready, timer, spec
 
 
 def submit(key: tuple, Xsrc, build_pre, timer, slot: int = 0) -> Optional[Pending]:
@@ -113,7 +133,10 @@ def submit(key: tuple, Xsrc, build_pre, timer, slot: int = 0) -> Optional[Pendin
         ready = torch.cuda.Event()
         ready.record()
         timer.stop()
-        return Pending(g, ready, timer)
+        spec = g.last_post if _SPECULATE else None
+        if spec is not None:
+            g.post[spec][0].replay()      # speculative Horner chain (checked in finish)
+        return Pending(g, ready, timer, spec)
     except Exception as exc:  # pragma: no cover - capture problems fall back to eager
         _FAILED.add(key)
         _CACHE.pop(key, None)
@@ -153,7 +176,14 @@ def finish(p: Pending, run_post):
     global _LAST_LAUNCHES
     _LAST_LAUNCHES = g.pre_launches + post_launches
     timer.start("mixed_horner")
-    graph.replay()
+    if p.spec is not None and p.spec == post_key:
+        _SPEC_STATS["hit"] += 1
+    else:
+        if p.spec is not None:
+            _SPEC_STATS["miss"] += 1
+            _LAST_LAUNCHES += g.post[p.spec][3]   # the speculative chain ran too
+        graph.replay()
+    g.last_post = post_key
     out = MatBatch(res.data.clone(), res.fmt)
     timer.stop()
     return g.prep, norms, out, info

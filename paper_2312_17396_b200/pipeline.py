@@ -5,9 +5,9 @@ device evaluation.
 batch (B, n, n) into chunks and software-pipelines them:
 
   upload stream    H2D of chunk c+1 (double-buffered device input)
-  compute stream   pre-planner graph of chunk c+1 is enqueued BEFORE the
-                   host plans chunk c, so the GPU works through the planner
-                   gap; then the Horner graph of chunk c
+  compute stream   pre-planner graph and (speculatively, graphs.py) Horner
+                   graph of each chunk; the host plans chunk c while its
+                   Horner chain runs
   download stream  D2H of chunk c's result into ``out_host`` (words, B, n, n)
 
 PCIe is full duplex and the copies run on the copy engines, so for a
@@ -136,16 +136,19 @@ def evaluate_host(submit: Callable, X_host, out_host, chunks=3, trace=None) -> L
         upload(1)
     start(0)
     for c in range(chunks):
-        if c + 1 < chunks:
-            start(c + 1)                 # GPU: pre(c+1) runs while the host plans c
-            if c + 2 < chunks:
-                upload(c + 2)
+        # submit() already enqueued chunk c's Horner chain speculatively
+        # (graphs.py), so finishing c before starting c+1 leaves no GPU gap
+        # and chunk c's download can begin as soon as its chain ends.
         mark(f"post{c}<", comp)
         rep = pend[c].finish()
         mark(f"post{c}>", comp)
         pend[c] = None
         done = torch.cuda.Event()
         done.record(comp)
+        if c + 1 < chunks:
+            start(c + 1)
+            if c + 2 < chunks:
+                upload(c + 2)
         lo, hi = bounds[c], bounds[c + 1]
         res = rep.result.data
         with torch.cuda.stream(down):

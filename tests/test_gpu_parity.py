@@ -318,6 +318,32 @@ def test_graph_replay_matches_eager_bitwise(cuda):
     assert not np.array_equal(g[0], g[1])
 
 
+def test_speculative_horner_miss_and_hit_bitwise(cuda):
+    """The Horner graph of the previous plan structure is replayed
+    speculatively; when the next batch's plan has a different structure
+    (here the level formats change with ||X||) the right graph runs after
+    it.  Hits and misses both give the eager path's bits."""
+    from paper_2312_17396_b200 import graphs
+    m = mp()
+    ctx = m.PrecisionCtx(31)
+    norms = (1.0, 1e-3, 1.0, 1.0, 1e-3)          # structures: A, B, A, A, B
+    Xs = [np.stack([synth(48, t, 7 * k + b) for b in range(2)]) for k, t in enumerate(norms)]
+    plans = [m.ps_mixed_exp(X, 30, ctx)[0].plan.level_digits for X in Xs[:2]]
+    assert plans[0] != plans[1]
+    graphs.set_enabled(True)
+    s0 = graphs.speculation_stats()
+    g = [m.ps_mixed_exp(X, 30, ctx).result.data.cpu().numpy() for X in Xs]
+    s1 = graphs.speculation_stats()
+    graphs.set_enabled(False)
+    try:
+        e = [m.ps_mixed_exp(X, 30, ctx).result.data.cpu().numpy() for X in Xs]
+    finally:
+        graphs.set_enabled(True)
+    for a, b in zip(g, e):
+        assert np.array_equal(a, b)
+    assert s1["miss"] - s0["miss"] >= 2 and s1["hit"] - s0["hit"] >= 1
+
+
 def test_pipelined_host_evaluation_matches(cuda):
     """pipeline.evaluate_host (chunked, copies overlapping compute) returns the
     same bits as one device-resident batched call."""
