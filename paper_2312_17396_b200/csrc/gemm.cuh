@@ -152,7 +152,7 @@ __device__ __forceinline__ void store_fmt(const MatRef &m, long long off, const 
     ((float *)m.data)[off] = mp::dd_to_float(d.hi, d.lo);
   } else if constexpr (FO == F64) {
     mp::dd d = mp::qd_to_dd(v);
-    ((double *)m.data)[off] = e ? ldexp(d.hi, e) : d.hi;
+    ((double *)m.data)[off] = e ? mp::dd_ldexp(d, e).hi : d.hi;
   } else if constexpr (FO == DD) {
     mp::dd d = mp::qd_to_dd(v);
     if (e) d = mp::dd_ldexp(d, e);

@@ -81,7 +81,15 @@ MP_INLINE dd dd_mul(dd a, dd b) {
   return dd_make(p, e);
 }
 MP_INLINE dd dd_neg(dd a) { return dd_make(-a.hi, -a.lo); }
-MP_INLINE dd dd_ldexp(dd a, int k) { return dd_make(ldexp(a.hi, k), ldexp(a.lo, k)); }
+MP_INLINE dd dd_ldexp(dd a, int k) {
+  // exact power-of-two multiply when 2^k is a normal double (same rounding
+  // as ldexp, which is much longer in SASS)
+  if (k >= -1022 && k <= 1023) {
+    const double p = __longlong_as_double((long long)(k + 1023) << 52);
+    return dd_make(a.hi * p, a.lo * p);
+  }
+  return dd_make(ldexp(a.hi, k), ldexp(a.lo, k));
+}
 
 // Correctly rounded dd -> fp32.  If hi is not an fp32 midpoint, hi+lo
 // rounds like hi (|lo| <= ulp_double(hi)/2 < distance to the midpoint);

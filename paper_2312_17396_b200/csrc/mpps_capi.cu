@@ -94,11 +94,14 @@ __device__ __forceinline__ mp::qd round_unbounded(const mp::qd &v) {
   if constexpr (FT == F32) {
     mp::dd d = mp::qd_to_dd(v);
     if (d.hi == 0.0 || !isfinite(d.hi)) return mp::qd_from_d((double)(float)d.hi);
+    // k with |hi| in [2^(k-1), 2^k) from the exponent field (normal hi)
+    const int ef = (int)((__double_as_longlong(d.hi) >> 52) & 0x7ff);
     int k = 0;
-    frexp(d.hi, &k);
+    if (ef != 0) k = ef - 1022;
+    else frexp(d.hi, &k);
     mp::dd s = mp::dd_ldexp(d, -k);         // |s| in [0.5, 1): fp32 normal range
     float f = mp::dd_to_float(s.hi, s.lo);
-    return mp::qd_from_d(ldexp((double)f, k));
+    return mp::qd_from_d(mp::dd_ldexp(mp::dd_make((double)f, 0.0), k).hi);
   } else if constexpr (FT == F64) {
     return mp::qd_from_d(mp::qd_to_dd(v).hi);
   } else if constexpr (FT == DD) {
@@ -459,12 +462,12 @@ struct ScalarTopArgs {
 template <int FT, int FO>
 __global__ void scalar_top_kernel(const ScalarTopArgs a) {
   const int b = a.sel ? a.sel[blockIdx.z] : (int)blockIdx.z;
-  const long long total = (long long)a.rows * a.cols;
   const int eo = a.exp_out ? a.exp_out[b] : 0;
   const mp::qd bm = mp::qd_make(a.bm[0], a.bm[1], a.bm[2], a.bm[3]);
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(t / a.cols), j = (int)(t % a.cols);
+  // 2-D grid: x = column blocks, y = rows (strided), z = batch members
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.cols) return;
+  for (int i = blockIdx.y; i < a.rows; i += gridDim.y) {
     mp::qd y = load_qd(a.Y, (long long)b * a.Y.bstride + (long long)i * a.Y.ld + j);
     mp::qd prod;
     if (a.wf == QD) {
@@ -475,6 +478,37 @@ __global__ void scalar_top_kernel(const ScalarTopArgs a) {
     mp::qd tv = round_unbounded<FT>(prod);
     mp::qd bv = load_qd(a.Bp, (long long)b * a.Bp.bstride + (long long)i * a.Bp.ld + j);
     store_fmt<FO>(a.out, (long long)b * a.out.bstride + (long long)i * a.out.ld + j, horner_add<FO>(bv, tv), eo);
+  }
+}
+
+// Same operation with the working format WF of Y and B_{r-1} known at
+// compile time (typed loads, no format branches): bit-identical to
+// scalar_top_kernel, which remains for mixed-format operands.
+template <int WF, int FT, int FO>
+__global__ void scalar_top_wf_kernel(const ScalarTopArgs a) {
+  using V = WV<WF>;
+  const int b = a.sel ? a.sel[blockIdx.z] : (int)blockIdx.z;
+  const int eo = a.exp_out ? a.exp_out[b] : 0;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.cols) return;
+  const long long yb = (long long)b * a.Y.bstride, bb = (long long)b * a.Bp.bstride,
+                  ob = (long long)b * a.out.bstride;
+  for (int i = blockIdx.y; i < a.rows; i += gridDim.y) {
+    const auto y = V::load(a.Y, yb + (long long)i * a.Y.ld + j);
+    const auto bp = V::load(a.Bp, bb + (long long)i * a.Bp.ld + j);
+    mp::qd prod, bv;
+    if constexpr (WF == QD) {
+      prod = mp::qd_mul(mp::qd_make(a.bm[0], a.bm[1], a.bm[2], a.bm[3]), y);
+      bv = bp;
+    } else if constexpr (WF == DD) {
+      prod = mp::qd_from_dd(mp::dd_mul(mp::dd_make(a.bm[0], a.bm[1]), y));
+      bv = mp::qd_from_dd(bp);
+    } else {
+      prod = mp::qd_from_dd(mp::dd_mul(mp::dd_make(a.bm[0], a.bm[1]), mp::dd_make(y, 0.0)));
+      bv = mp::qd_from_d(bp);
+    }
+    const mp::qd tv = round_unbounded<FT>(prod);
+    store_fmt<FO>(a.out, ob + (long long)i * a.out.ld + j, horner_add<FO>(bv, tv), eo);
   }
 }
 
@@ -806,9 +840,20 @@ int mpps_horner_scalar_top(mpps_handle *h, const double *bm, int fmt_top, const 
   a.sel = sel; a.exp_out = exp_out;
   int nb = sel ? nsel : out->batch;
   if (nb == 0 || a.rows == 0 || a.cols == 0) return MPPS_OK;
-  dim3 grid(ew_grid((long long)a.rows * a.cols / 4 + 1), 1, nb);
+  const int tpb = a.cols >= 256 ? 256 : 128;
+  dim3 grid((a.cols + tpb - 1) / tpb, a.rows < 65535 ? a.rows : 65535, nb);
+  if (fmt_index(Bprev->fmt) == wf && ft <= wf) {
+#define SW(W, A, B) \
+  if (wf == W && ft == A && fo == B) scalar_top_wf_kernel<W, A, B><<<grid, tpb, 0, h->stream>>>(a); else
+#define SWF(W) SW(W, F32, F32) SW(W, F32, F64) SW(W, F32, DD) SW(W, F32, QD) SW(W, F64, F64) SW(W, F64, DD) \
+  SW(W, F64, QD) SW(W, DD, DD) SW(W, DD, QD) SW(W, QD, QD)
+    SWF(F64) SWF(DD) SWF(QD) { return set_err(h, MPPS_EFMT, "scalar_top: formats"); }
+#undef SWF
+#undef SW
+    return after_launch(h, "scalar_top_kernel");
+  }
 #define ST(A, B) \
-  if (ft == A && fo == B) scalar_top_kernel<A, B><<<grid, 256, 0, h->stream>>>(a); else
+  if (ft == A && fo == B) scalar_top_kernel<A, B><<<grid, tpb, 0, h->stream>>>(a); else
   ST(F32, F32) ST(F32, F64) ST(F32, DD) ST(F32, QD) ST(F64, F64) ST(F64, DD) ST(F64, QD) ST(DD, DD) ST(DD, QD)
   ST(QD, QD) { return set_err(h, MPPS_EFMT, "scalar_top: formats"); }
 #undef ST
