@@ -64,18 +64,49 @@ def make_batch(rank, batch, n, norm):
 
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
+    region: an NVML polling thread (~0.5 ms period, so even a few-ms region
+    gets many samples); nvidia-smi -lms 200 when NVML is unavailable."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.proc = None
         self.lines = []
+        self.nvml = None
+        self.samples = []
+        self.running = False
 
     def start(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nvml = nv
+            self.hdl = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.smax = float(nv.nvmlDeviceGetMaxClockInfo(self.hdl, nv.NVML_CLOCK_SM))
+            get = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            self.bits = (nv.nvmlClocksThrottleReasonHwSlowdown, nv.nvmlClocksThrottleReasonHwThermalSlowdown,
+                         nv.nvmlClocksThrottleReasonSwThermalSlowdown, nv.nvmlClocksThrottleReasonSwPowerCap)
+            self.running = True
+
+            def poll():
+                while self.running:
+                    try:
+                        self.samples.append((float(nv.nvmlDeviceGetClockInfo(self.hdl, nv.NVML_CLOCK_SM)),
+                                             int(get(self.hdl))))
+                    except Exception:
+                        pass
+                    time.sleep(0.0005)
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -91,6 +122,13 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.nvml is not None:
+            self.running = False
+            self.thread.join(timeout=2)
+            sm = [c for c, _ in self.samples]
+            reasons = {nm for _, r in self.samples for nm, bit in zip(self.NAMES, self.bits) if r & bit}
+            return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.smax,
+                    "reasons": sorted(reasons), "samples": len(sm), "source": "nvml"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -99,7 +137,6 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
@@ -109,11 +146,11 @@ class ClockSampler:
                 smax = float(parts[1])
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[4:8]):
+            for nm, v in zip(self.NAMES, parts[4:8]):
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi"}
 
 
 # ------------------------------------------------------------- peaks
@@ -494,7 +531,16 @@ def run_ours(args, rank, world, local_rank):
                                f"(fp64 {peaks['fp64']:.2f} TF/s, fp32 {peaks['fp32']:.2f} TF/s); "
                                "Peak_dd = Peak_fp64/15, Peak_qd = Peak_fp64/115 (SURVEY 8d); "
                                "MEASURED_PEAKS.json holds only HBM and bf16"}
-    roof.update({"kernel": f"{kind} {fname}->{names[fout]} {M}x{N}x{K} x{nb}", "traffic": None,
+    kkey = f"{kind} {fname}->{names[fout]} {M}x{N}x{K} x{nb}"
+    traffic, tsrc = None, None
+    try:   # committed ncu --set full capture of this kernel at this shape (profiles/traffic.json)
+        tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")))
+        if kkey in tr:
+            traffic = tr[kkey]["dram_bytes_per_launch"]
+            tsrc = f"{tr[kkey]['capture']} ({tr[kkey]['kernel']}), bytes per launch"
+    except Exception:
+        pass
+    roof.update({"kernel": kkey, "traffic": traffic, "traffic_source": tsrc,
                  "share_of_step": sec / args.steps / step_time, "launches_per_step": cnt / args.steps,
                  "eval_frac": t_ideal / step_time,
                  "measured_in": "a second timed pass of the same K steps run eagerly (the value pass "

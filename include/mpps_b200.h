@@ -199,8 +199,9 @@ int mpps_probe_i8mma(mpps_handle *h, int blocks, int iters, void *scratch);
 void mpps_debug_oz_trace(void *buf);
 
 /* Diagnostic: bit 0 skips the MMAs (operand feed only), bit 1 skips the
- * TMA loads (MMAs on stale shared memory) of the TMA-fed GEMMs; results
- * are garbage while set.  For tools/cta_timeline.py only. */
+ * TMA loads (MMAs on stale shared memory) of the TMA-fed GEMMs (results
+ * are garbage while set); bits 8.. override the tile-raster group size
+ * (0 = default / MPPS_OZ_GROUP).  For tools/ only. */
 void mpps_debug_oz_flags(int flags);
 
 /* Diagnostic: mpps_probe_i8mma with M = 128, N = n (16..256, multiple of

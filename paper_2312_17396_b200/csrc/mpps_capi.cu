@@ -951,6 +951,18 @@ static int make_slice_map(mpps_handle *h, CUtensorMap *map, const mpps_slices *s
   return MPPS_OK;
 }
 
+// M tiles per raster group of the TMA / ring GEMMs (MPPS_OZ_GROUP, default 4)
+static int g_oz_group_override = 0;  // mpps_debug_oz_flags(flags): bits 8.. = group (0: default)
+static int oz_group() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MPPS_OZ_GROUP");
+    v = e ? atoi(e) : 4;
+    if (v < 1) v = 1;
+  }
+  return g_oz_group_override > 0 ? g_oz_group_override : v;
+}
+
 template <int S, int NT, int FO, int MODE>
 static int launch_oz_tma(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
   constexpr size_t smem = oz::oz_tma_smem_bytes<S, NT, FO, MODE>();
@@ -961,9 +973,13 @@ static int launch_oz_tma(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
     if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz tma attr: %s", cudaGetErrorString(e));
     configured = true;
   }
-  dim3 grid((a.N + NT - 1) / NT, (a.M + oz::kTileM - 1) / oz::kTileM, nb);
+  oz::OzTmaArgs t = a;
+  t.mtiles = (a.M + oz::kTileM - 1) / oz::kTileM;
+  t.ntiles = (a.N + NT - 1) / NT;
+  t.group = oz_group();
+  dim3 grid(t.mtiles * t.ntiles, 1, nb);
   if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
-  oz::oz_gemm_tma_kernel<S, NT, FO, MODE><<<grid, oz::kThreadsEpi, smem, h->stream>>>(a);
+  oz::oz_gemm_tma_kernel<S, NT, FO, MODE><<<grid, oz::kThreadsEpi, smem, h->stream>>>(t);
   return after_launch(h, "oz_gemm_tma_kernel");
 }
 
@@ -989,9 +1005,13 @@ static int launch_oz_ring(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
     if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz ring attr: %s", cudaGetErrorString(e));
     configured = true;
   }
-  dim3 grid((a.N + NT - 1) / NT, (a.M + oz::kTileM - 1) / oz::kTileM, nb);
+  oz::OzTmaArgs t = a;
+  t.mtiles = (a.M + oz::kTileM - 1) / oz::kTileM;
+  t.ntiles = (a.N + NT - 1) / NT;
+  t.group = oz_group();
+  dim3 grid(t.mtiles * t.ntiles, 1, nb);
   if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
-  oz::oz_gemm_ring_kernel<S, NT, FO, MODE><<<grid, oz::kThreadsEpi, smem, h->stream>>>(a);
+  oz::oz_gemm_ring_kernel<S, NT, FO, MODE><<<grid, oz::kThreadsEpi, smem, h->stream>>>(t);
   return after_launch(h, "oz_gemm_ring_kernel");
 }
 
@@ -1108,7 +1128,7 @@ int mpps_horner_step_sliced(mpps_handle *h, const mpps_slices *Y, const mpps_sli
 int mpps_oz_slices_for(int fmt) { return oz_slices_for(fmt_index(fmt)); }
 
 void mpps_debug_oz_trace(void *buf) { g_oz_trace = (unsigned long long *)buf; }
-void mpps_debug_oz_flags(int flags) { g_oz_dbg = flags; }
+void mpps_debug_oz_flags(int flags) { g_oz_dbg = flags & 0xff; g_oz_group_override = flags >> 8; }
 
 int mpps_probe_i8mma(mpps_handle *h, int blocks, int iters, void *scratch) {
   if (!scratch || blocks < 1 || iters < 1) return set_err(h, MPPS_EINVAL, "probe: bad arguments");

@@ -693,7 +693,23 @@ struct OzTmaArgs {
   HornerEpi epi;
   unsigned long long *trace;  // diagnostics (mpps_debug_oz_trace): per-CTA phase timestamps or null
   int dbg;                     // diagnostics: bit 0 skip MMAs (feed only), bit 1 skip TMA (MMA only)
+  int mtiles, ntiles, group;   // tile raster: blockIdx.x walks `group` M tiles fastest, then N
 };
+
+// Grouped raster: consecutive CTAs cover a group of up to `group` M tiles
+// (fastest) times successive N tiles, so a wave shares both its A row
+// panels and its B column panels in L2 (an N-fastest raster streams all of
+// B from DRAM once per M-tile row: 34x the operand bytes at n = 8192).
+__device__ __forceinline__ void oz_tile_of(const OzTmaArgs &a, int nt, int &m0, int &n0) {
+  const int id = blockIdx.x;
+  const int per_group = a.group * a.ntiles;
+  const int g = id / per_group;
+  const int first_m = g * a.group;
+  const int gm = min(a.group, a.mtiles - first_m);
+  const int r = id - g * per_group;
+  m0 = (first_m + r % gm) * kTileM;
+  n0 = (r / gm) * nt;
+}
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -907,7 +923,8 @@ __global__ void __launch_bounds__(kThreadsEpi, oz_ctas_per_sm<S, MODE>()) oz_gem
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int bz = blockIdx.z;
   const int b = args.sel ? args.sel[bz] : bz;
-  const int m0 = blockIdx.y * kTileM, n0 = blockIdx.x * NT;
+  int m0, n0;
+  oz_tile_of(args, NT, m0, n0);
   const int ksteps = args.A.kpad / kKStep;
   unsigned long long *tr = oz_trace_begin(args);
 
@@ -1037,7 +1054,8 @@ __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_ring_kernel(const __gr
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int bz = blockIdx.z;
   const int b = args.sel ? args.sel[bz] : bz;
-  const int m0 = blockIdx.y * kTileM, n0 = blockIdx.x * NT;
+  int m0, n0;
+  oz_tile_of(args, NT, m0, n0);
   const int ksteps = args.A.kpad / kKStep;
   unsigned long long *tr = oz_trace_begin(args);
 

@@ -138,3 +138,36 @@ if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "horner32":
     ps8 = h.slice(P64, 1, 8)
     print(f"fp64 level: simt horner {t(lambda: h.horner_step(Y64, P64, Bp, o64)):.1f} us; "
           f"tc horner {t(lambda: h.horner_step_sliced(ys, ps8, 8, Bp, o64, fmt_in=15)):.1f} us", flush=True)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "big":
+    for fmt, B, n in ((31, 1, 8192), (63, 1, 2048), (31, 16, 1024), (31, 64, 256)):
+        bench_tc(fmt, B, n, reps=3)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "group":
+    # raster group size, interleaved in one process (per-process variance)
+    import itertools
+    shapes = ((31, 1, 8192), (63, 1, 2048), (31, 16, 1024), (31, 64, 256))
+    G = (1, 2, 4, 8, 16)
+    h = _lib.handle_for()
+    res = {}
+    setups = {}
+    for fmt, B, n in shapes:
+        A = MatBatch.empty(fmt, B, n, device="cuda"); A.data.normal_()
+        if A.words > 1:
+            A.data[1:] *= 1e-17
+        C = MatBatch.empty(fmt, B, n, device="cuda")
+        S = h.slices_for(fmt)
+        setups[(fmt, B, n)] = (h.slice(A, 0, S), h.slice(A, 1, S), S, C)
+    for rep in range(3):
+        for g in G:
+            h.lib.mpps_debug_oz_flags(g << 8)
+            for key, (sa, sb, S, C) in setups.items():
+                h.gemm_sliced(sa, sb, S, C); torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(); h.gemm_sliced(sa, sb, S, C); b.record(); b.synchronize()
+                res.setdefault((key, g), []).append(a.elapsed_time(b))
+    h.lib.mpps_debug_oz_flags(0)
+    for key in setups:
+        print(key, " ".join(f"G={g}:{min(res[(key, g)]):.3f}ms" for g in G), flush=True)
