@@ -937,15 +937,17 @@ static EncodeTiledFn encode_fn() {
 
 // digit planes [S][batch][rpad][kpad] as a 3-D tensor (k, batch*rpad, S),
 // box {32, rows_box, S}, 32-byte swizzle
-static int make_slice_map(mpps_handle *h, CUtensorMap *map, const mpps_slices *s, int rows_box, int S) {
+static int make_slice_map(mpps_handle *h, CUtensorMap *map, const mpps_slices *s, int rows_box, int S,
+                          int kbox = 32) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return set_err(h, MPPS_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {(cuuint64_t)s->kpad, (cuuint64_t)s->batch * s->rpad, (cuuint64_t)s->nslices};
   cuuint64_t strides[2] = {(cuuint64_t)s->kpad, (cuuint64_t)s->kpad * s->batch * s->rpad};
-  cuuint32_t box[3] = {32u, (cuuint32_t)rows_box, (cuuint32_t)S};
+  cuuint32_t box[3] = {(cuuint32_t)kbox, (cuuint32_t)rows_box, (cuuint32_t)S};
   cuuint32_t estr[3] = {1u, 1u, 1u};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, s->digits, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, kbox == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_err(h, MPPS_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return MPPS_OK;
@@ -1025,6 +1027,101 @@ static int dispatch_oz_ring(mpps_handle *h, int S, int fo, int mode, const oz::O
   return set_err(h, MPPS_EFMT, "tensor-core GEMM: no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
 }
 
+template <int S, int NT, int FO, int MODE, int CL>
+static int launch_oz_pers(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
+  constexpr size_t smem = oz::OzPers<S, NT>::SMEM;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_pers_kernel<S, NT, FO, MODE, CL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz pers attr: %s", cudaGetErrorString(e));
+    configured = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  oz::OzTmaArgs t = a;
+  t.mtiles = (a.M + oz::kTileM - 1) / oz::kTileM;
+  t.ntiles = (a.N + NT - 1) / NT;
+  t.group = oz_group();
+  t.nbatch = nb;
+  if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
+  const long long groups = (long long)nb * t.mtiles * ((t.ntiles + CL - 1) / CL);
+  const long long maxg = sms / CL;
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)(CL * (groups < maxg ? groups : maxg)), 1, 1);
+  cfg.blockDim = dim3(oz::kThreadsPers, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = h->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, oz::oz_gemm_pers_kernel<S, NT, FO, MODE, CL>, t);
+  if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz pers launch: %s", cudaGetErrorString(e));
+  return after_launch(h, "oz_gemm_pers_kernel");
+}
+
+// persistent double-buffered kernel for the dd power-chain GEMMs:
+// MPPS_OZ_PERS = 0 (default) off, 1 single CTAs, 2 CTA pairs multicasting A (feed-bound: no gain measured)
+static int oz_pers_mode(int S, int fo, int mode) {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MPPS_OZ_PERS");
+    v = e ? atoi(e) : 0;
+  }
+  return (S == 16 && fo == DD && mode == 0) ? v : 0;
+}
+
+template <int S, int NT, int FO, int MODE>
+static int launch_oz_wide(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
+  constexpr size_t smem = oz::oz_wide_smem_bytes<S, NT, FO, MODE>();
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_wide_kernel<S, NT, FO, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz wide attr: %s", cudaGetErrorString(e));
+    configured = true;
+  }
+  oz::OzTmaArgs t = a;
+  t.mtiles = (a.M + oz::kTileM - 1) / oz::kTileM;
+  t.ntiles = (a.N + NT - 1) / NT;
+  t.group = oz_group();
+  dim3 grid(t.mtiles * t.ntiles, 1, nb);
+  if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
+  oz::oz_gemm_wide_kernel<S, NT, FO, MODE><<<grid, oz::kThreadsEpi, smem, h->stream>>>(t);
+  return after_launch(h, "oz_gemm_wide_kernel");
+}
+
+// 128-byte K boxes (MPPS_OZ_WIDE=0 disables, 2 forces every supported case):
+// measured faster for qd (n = 1024: 0.53 vs 0.63 ms; 2048: 3.56 vs 4.06 ms)
+// and for dd at K >= 4096 (n = 8192: 48.6 vs 50.8 ms); the 32-byte-box ring
+// kernel stays ahead for smaller dd products (n = 256: 0.167 vs 0.181 ms).
+static bool oz_wide_for(int S, int fo, int mode, int K) {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MPPS_OZ_WIDE");
+    v = e ? atoi(e) : 1;
+  }
+  if (!v) return false;
+  return (S == 16 && mode == 0 && fo == DD && (K >= 4096 || v == 2)) || (S == 31 && fo == QD);
+}
+
+static int dispatch_oz_wide(mpps_handle *h, int S, int fo, int mode, const oz::OzTmaArgs &a, int nb) {
+#define OZ(SS, NT, FF, MM) if (S == SS && fo == FF && mode == MM) return launch_oz_wide<SS, NT, FF, MM>(h, a, nb);
+  OZ(16, 32, DD, 0) OZ(31, 16, QD, 0) OZ(31, 16, QD, 1)
+#undef OZ
+  return set_err(h, MPPS_EFMT, "wide tensor-core GEMM: no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
+}
+
 static int oz_mode() {   // 0 cp.async, 1 TMA stage ring, 2 TMA streamed planes, 3 (default) streamed for S >= 16
   static int v = -1;
   if (v < 0) {
@@ -1044,15 +1141,26 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   if (oz_mode() == 0) return dispatch_oz(h, S, fo, mode, a, nb);
   oz::OzTmaArgs t;
   memset(&t, 0, sizeof(t));
-  const int NT = (S > 16) ? 16 : 32;
+  const bool wide = oz_wide_for(S, fo, mode, a.K);
+  const int pmode = wide ? 0 : oz_pers_mode(S, fo, mode);
+  const bool pers = pmode != 0;
+  const int NT = (S > 16 || pers) ? 16 : 32;
   // default: streamed-plane ring for dd / qd (S >= 16), 2-4 stage TMA ring below
-  const bool ring = oz_mode() == 2 || (oz_mode() == 3 && S >= 16);
+  const bool ring = pers || oz_mode() == 2 || (oz_mode() == 3 && S >= 16);
   const int abox = ring ? (S < 4 ? S : 4) : S;
   int rc;
-  if ((rc = make_slice_map(h, &t.mapA, A, oz::kTileM, abox)) || (rc = make_slice_map(h, &t.mapB, B, NT, S))) return rc;
+  if (wide) {
+    if ((rc = make_slice_map(h, &t.mapA, A, oz::kTileM, 1, 128)) || (rc = make_slice_map(h, &t.mapB, B, NT, S, 128)))
+      return rc;
+  } else if ((rc = make_slice_map(h, &t.mapA, A, oz::kTileM, abox)) || (rc = make_slice_map(h, &t.mapB, B, NT, S))) {
+    return rc;
+  }
   t.A = a.A; t.B = a.B; t.M = a.M; t.N = a.N; t.K = a.K; t.S = a.S; t.C = a.C; t.sel = a.sel; t.epi = a.epi;
   t.trace = g_oz_trace;
   t.dbg = g_oz_dbg;
+  if (wide) return dispatch_oz_wide(h, S, fo, mode, t, nb);
+  if (pmode == 1) return launch_oz_pers<16, 16, DD, 0, 1>(h, t, nb);
+  if (pmode == 2) return launch_oz_pers<16, 16, DD, 0, 2>(h, t, nb);
   return ring ? dispatch_oz_ring(h, S, fo, mode, t, nb) : dispatch_oz_tma(h, S, fo, mode, t, nb);
 }
 

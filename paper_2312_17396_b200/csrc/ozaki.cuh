@@ -94,6 +94,12 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
   }
 }
 
+__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(mbar) : "memory");
+}
+// named barrier among the `n` threads of the epilogue warps (id 1; 0 is __syncthreads)
+__device__ __forceinline__ void epi_bar_sync(int n) { asm volatile("bar.sync 1, %0;\n" ::"r"(n) : "memory"); }
+
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
@@ -694,14 +700,14 @@ struct OzTmaArgs {
   unsigned long long *trace;  // diagnostics (mpps_debug_oz_trace): per-CTA phase timestamps or null
   int dbg;                     // diagnostics: bit 0 skip MMAs (feed only), bit 1 skip TMA (MMA only)
   int mtiles, ntiles, group;   // tile raster: blockIdx.x walks `group` M tiles fastest, then N
+  int nbatch;                  // persistent kernels: batch members (tiles = nbatch * mtiles * ntiles)
 };
 
 // Grouped raster: consecutive CTAs cover a group of up to `group` M tiles
 // (fastest) times successive N tiles, so a wave shares both its A row
 // panels and its B column panels in L2 (an N-fastest raster streams all of
 // B from DRAM once per M-tile row: 34x the operand bytes at n = 8192).
-__device__ __forceinline__ void oz_tile_of(const OzTmaArgs &a, int nt, int &m0, int &n0) {
-  const int id = blockIdx.x;
+__device__ __forceinline__ void oz_tile_at(const OzTmaArgs &a, int id, int nt, int &m0, int &n0) {
   const int per_group = a.group * a.ntiles;
   const int g = id / per_group;
   const int first_m = g * a.group;
@@ -709,6 +715,9 @@ __device__ __forceinline__ void oz_tile_of(const OzTmaArgs &a, int nt, int &m0, 
   const int r = id - g * per_group;
   m0 = (first_m + r % gm) * kTileM;
   n0 = (r / gm) * nt;
+}
+__device__ __forceinline__ void oz_tile_of(const OzTmaArgs &a, int nt, int &m0, int &n0) {
+  oz_tile_at(a, blockIdx.x, nt, m0, n0);
 }
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -1104,6 +1113,352 @@ __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_ring_kernel(const __gr
   }
   oz_kernel_epilogue<S, NT, FO, MODE, STAGED>(args, ebuf, ebs, tmem, done, warp, lane, b, m0, n0, tr);
   if (warp == 0) tmem_dealloc<TCOLS>(tmem);
+}
+
+// ------------------------------------------- 128-byte K boxes (wide feed)
+// The 32-byte K boxes of the kernels above move one 32-byte sector per
+// tile row per TMA request, and the feed saturates at ~45-60 GB/s per SM
+// (the kernels run as fast with the MMAs switched off).  Here every TMA
+// box row is 128 bytes (4 MMA K steps; SWIZZLE_128B, the UMMA K-major
+// 128-byte-swizzle layout: 8-row x 128-byte atoms, SBO = 1024 B, the k-th
+// 32-byte K step selected by +32 B on the descriptor start address).
+// B: all S planes of NT rows x 128 B per stage (2 stages); A: one plane of
+// 128 rows x 128 B per ring slot, its 4 K steps of MMAs issued back to back.
+template <int S, int NT>
+struct OzWide {
+  static constexpr int KB = 128;                                  // K bytes per stage
+  static constexpr uint32_t A_BYTES = kTileM * KB;                // 16 KB: one plane
+  static constexpr uint32_t B_PLANE = NT * KB;                    // bytes per B plane
+  static constexpr uint32_t B_BYTES = S * B_PLANE;
+  static constexpr uint32_t B_STRIDE = (B_BYTES + 1023) / 1024 * 1024;
+  static constexpr int NBS = 2;
+  template <uint32_t EBUF>
+  __host__ __device__ static constexpr int nas() {
+    constexpr long long room = 225ll * 1024 - 2048 - (long long)EBUF - NBS * (long long)B_STRIDE;
+    return room / A_BYTES > 8 ? 8 : (int)(room / A_BYTES);
+  }
+};
+
+// MMAs of plane s for K step kk of a stage: A_s x [B_0 .. B_{S-1-s}]
+template <int S, int NT, int s>
+__device__ __forceinline__ void oz_wide_plane(uint32_t tmem, uint64_t ad, uint64_t bd0, uint32_t acc) {
+  constexpr uint32_t B_PLANE = OzWide<S, NT>::B_PLANE;
+#pragma unroll
+  for (int t0 = 0; t0 < S - s; t0 += 256 / NT) {
+    const int nn = ((S - s - t0) * NT > 256) ? 256 : (S - s - t0) * NT;
+    mma_i8(tmem + (uint32_t)((s + t0) * NT), ad, bd0 + (uint64_t)((t0 * B_PLANE) >> 4), idesc_i8(kTileM, nn),
+           s > 0 ? 1u : acc);
+  }
+}
+
+template <int S, int NT, int s = 0>
+__device__ __forceinline__ void oz_wide_stage(uint32_t tmem, uint32_t sb, int nk, uint32_t acc0, int &ai,
+                                              uint8_t *aring, uint64_t *a_full, uint64_t *a_empty, int nas) {
+  if constexpr (s < S) {
+    const int ast = ai % nas;
+    mbar_wait(smem_u32(&a_full[ast]), (ai / nas) & 1);
+    fence_after();
+    const uint32_t sa = smem_u32(aring + ast * OzWide<S, NT>::A_BYTES);
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+      if (kk < nk)
+        oz_wide_plane<S, NT, s>(tmem, umma_desc(sa + kk * 32, 16, 1024, 2), umma_desc(sb + kk * 32, 16, 1024, 2),
+                                kk > 0 ? 1u : acc0);
+    mma_commit(smem_u32(&a_empty[ast]));
+    ++ai;
+    oz_wide_stage<S, NT, s + 1>(tmem, sb, nk, acc0, ai, aring, a_full, a_empty, nas);
+  }
+}
+
+template <int S, int NT, int FO, int MODE>
+__host__ __device__ constexpr size_t oz_wide_smem_bytes() {
+  using W = OzWide<S, NT>;
+  constexpr uint32_t EBUF = oz_ebuf_bytes<S, NT, FO, MODE>();
+  return (size_t)W::NBS * W::B_STRIDE + (size_t)W::template nas<EBUF>() * W::A_BYTES + EBUF + 2048;
+}
+
+template <int S, int NT, int FO, int MODE>
+__global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_wide_kernel(const __grid_constant__ OzTmaArgs args) {
+  using W = OzWide<S, NT>;
+  constexpr int TCOLS = tmem_cols_for(S * NT);
+  constexpr bool STAGED = oz_staged<S, NT, FO, MODE>();
+  constexpr uint32_t EBUF = oz_ebuf_bytes<S, NT, FO, MODE>();
+  constexpr int NAS = W::template nas<EBUF>();
+  static_assert(NAS >= 2, "A ring does not fit");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t *bring = smem;
+  uint8_t *aring = smem + W::NBS * W::B_STRIDE;
+  double *ebuf = reinterpret_cast<double *>(aring + NAS * W::A_BYTES);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(aring + NAS * W::A_BYTES + EBUF);
+  uint64_t *b_full = bar, *b_empty = bar + W::NBS;
+  uint64_t *a_full = bar + 2 * W::NBS, *a_empty = a_full + NAS;
+  uint64_t *done = a_empty + NAS;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+  int *ebs = reinterpret_cast<int *>(tmem_slot + 4);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int bz = blockIdx.z;
+  const int b = args.sel ? args.sel[bz] : bz;
+  int m0, n0;
+  oz_tile_of(args, NT, m0, n0);
+  const int kpad = args.A.kpad;
+  const int kstages = (kpad + W::KB - 1) / W::KB;
+  unsigned long long *tr = oz_trace_begin(args);
+
+  if (warp == 0) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
+  if (tid == 32) {
+    for (int i = 0; i < W::NBS; ++i) { mbar_init(smem_u32(&b_full[i]), 1); mbar_init(smem_u32(&b_empty[i]), 1); }
+    for (int i = 0; i < NAS; ++i) { mbar_init(smem_u32(&a_full[i]), 1); mbar_init(smem_u32(&a_empty[i]), 1); }
+    mbar_init(smem_u32(done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int rowA = b * args.A.rpad + m0, rowB = b * args.B.rpad + n0;
+  if (tr) tr[1] = globaltimer();
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer: B stage (all planes), then the S A planes of that stage
+    int ai = 0;
+    for (int kb = 0; kb < kstages; ++kb) {
+      const int bst = kb % W::NBS;
+      if (kb >= W::NBS) mbar_wait(smem_u32(&b_empty[bst]), ((kb / W::NBS) - 1) & 1);
+      mbar_expect_tx(smem_u32(&b_full[bst]), W::B_BYTES);
+      tma_load_3d(smem_u32(bring + bst * W::B_STRIDE), &args.mapB, kb * W::KB, rowB, 0, smem_u32(&b_full[bst]));
+      for (int s = 0; s < S; ++s, ++ai) {
+        const int ast = ai % NAS;
+        if (ai >= NAS) mbar_wait(smem_u32(&a_empty[ast]), ((ai / NAS) - 1) & 1);
+        mbar_expect_tx(smem_u32(&a_full[ast]), W::A_BYTES);
+        tma_load_3d(smem_u32(aring + ast * W::A_BYTES), &args.mapA, kb * W::KB, rowA, s, smem_u32(&a_full[ast]));
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer
+    int ai = 0;
+    for (int kb = 0; kb < kstages; ++kb) {
+      const int bst = kb % W::NBS;
+      mbar_wait(smem_u32(&b_full[bst]), (kb / W::NBS) & 1);
+      fence_after();
+      const int left = (kpad - kb * W::KB) / kKStep;
+      const int nk = left < 4 ? left : 4;
+      oz_wide_stage<S, NT>(tmem, smem_u32(bring + bst * W::B_STRIDE), nk, kb > 0 ? 1u : 0u, ai, aring, a_full,
+                           a_empty, NAS);
+      mma_commit(smem_u32(&b_empty[bst]));
+    }
+    mma_commit(smem_u32(done));
+  }
+  oz_kernel_epilogue<S, NT, FO, MODE, STAGED>(args, ebuf, ebs, tmem, done, warp, lane, b, m0, n0, tr);
+  if (warp == 0) tmem_dealloc<TCOLS>(tmem);
+}
+
+// ------------------------------------- persistent, double-buffered TMEM
+// One CTA per SM walks the tiles of the whole batch; consecutive CTAs hold
+// consecutive tiles of the grouped raster.  Two accumulator sets of S*NT
+// TMEM columns (NT = 16 for dd: 2 x 256 columns) let the MMAs of tile i+1
+// run while the epilogue warps drain tile i, and the TMA producer streams
+// the next tile's planes during the epilogue instead of each CTA paying the
+// pipeline fill.
+//
+// CL = 2: CTA pairs (a 2-CTA cluster) take the two N tiles 2p, 2p+1 of one
+// M tile.  Both need the same A planes, so each CTA loads every other A
+// plane group and multicasts it into both CTAs' rings: the L2 -> SM traffic
+// of A (16 of the 18 KB per K step and 16 output columns) halves.  A ring
+// slot is refilled only after BOTH CTAs' MMAs have released it (the MMA
+// issuers' commits arrive on the a_empty barriers of both CTAs).
+//
+// Warp 0: TMA producer, warp 1: MMA issuer, warps 2..9: epilogue (warp w
+// reads TMEM lane quarter w % 4; warps 2..5 take the first half of the
+// columns, 6..9 the second).
+constexpr int kThreadsPers = 320;
+
+template <int S, int NT>
+struct OzPers {
+  // deeper rings than OzRing: a K step of 16 columns takes ~0.7 us of MMAs,
+  // shorter than a TMA round trip, so several B steps and A groups must be
+  // in flight
+  static constexpr int SG = OzRing<S, NT>::SG, NG = OzRing<S, NT>::NG;
+  static constexpr uint32_t A_BYTES = OzRing<S, NT>::A_BYTES, B_BYTES = OzRing<S, NT>::B_BYTES;
+  static constexpr uint32_t B_STRIDE = (B_BYTES + 1023) / 1024 * 1024;
+  static constexpr size_t kBudget = 212u * 1024u;
+  static constexpr int NBS = (B_STRIDE * 6 <= kBudget / 4) ? 6 : 2;
+  static constexpr int NAS_FIT = (int)((kBudget - NBS * (size_t)B_STRIDE) / A_BYTES);
+  static constexpr int NAS = NAS_FIT > 12 ? 12 : NAS_FIT;
+  static constexpr int ACC = S * NT;  // TMEM columns per accumulator set
+  static_assert(2 * ACC <= 512, "two accumulator sets must fit in TMEM");
+  static constexpr size_t SMEM = (size_t)NBS * B_STRIDE + (size_t)NAS * A_BYTES + 2048;
+};
+
+// tile t of a CL-CTA group: (batch member, M offset, N offset of this CTA)
+template <int CL>
+__device__ __forceinline__ void oz_pers_tile(const OzTmaArgs &a, int t, int nt, int rank, int &bz, int &m0, int &n0) {
+  const int npairs = (a.ntiles + CL - 1) / CL;
+  const int per = a.mtiles * npairs;
+  bz = t / per;
+  OzTmaArgs g = a;
+  g.ntiles = npairs;
+  oz_tile_at(g, t - bz * per, nt * CL, m0, n0);
+  n0 += rank * nt;
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                               uint32_t mbar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(mbar), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint32_t mbar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(mbar),
+      "h"(mask)
+      : "memory");
+}
+
+template <int S, int NT, uint32_t A_SLICE, uint32_t B_SLICE, int SG, int CL, int G = 0>
+__device__ __forceinline__ void oz_ring_groups_mc(uint32_t tmem, uint64_t bd0, uint32_t acc0, int &ai, uint8_t *aring,
+                                                  uint64_t *a_full, uint64_t *a_empty, int nas, uint32_t a_bytes,
+                                                  bool issue = true) {
+  if constexpr (G * SG < S) {
+    const int ast = ai % nas;
+    mbar_wait(smem_u32(&a_full[ast]), (ai / nas) & 1);
+    fence_after();
+    if (issue)
+      oz_issue_planes<S, NT, A_SLICE, B_SLICE, G * SG, SG>(tmem, umma_desc(smem_u32(aring + ast * a_bytes), 16, 256, 6),
+                                                           bd0, acc0);
+    if constexpr (CL == 1) mma_commit(smem_u32(&a_empty[ast]));
+    else mma_commit_mc(smem_u32(&a_empty[ast]), (uint16_t)((1u << CL) - 1u));
+    ++ai;
+    oz_ring_groups_mc<S, NT, A_SLICE, B_SLICE, SG, CL, G + 1>(tmem, bd0, acc0, ai, aring, a_full, a_empty, nas,
+                                                              a_bytes, issue);
+  }
+}
+
+template <int S, int NT, int FO, int MODE, int CL>
+__global__ void __launch_bounds__(kThreadsPers, 1) oz_gemm_pers_kernel(const __grid_constant__ OzTmaArgs args) {
+  using P = OzPers<S, NT>;
+  using R = P;
+  constexpr uint32_t A_SLICE = kTileM * kKStep;
+  constexpr uint32_t B_SLICE = NT * kKStep;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t *bring = smem;
+  uint8_t *aring = smem + R::NBS * R::B_STRIDE;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(aring + R::NAS * R::A_BYTES);
+  uint64_t *b_full = bar, *b_empty = bar + R::NBS;
+  uint64_t *a_full = bar + 2 * R::NBS, *a_empty = a_full + R::NAS;
+  uint64_t *acc_full = a_empty + R::NAS, *acc_empty = acc_full + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ksteps = args.A.kpad / kKStep;
+  const int rank = CL > 1 ? (int)cluster_rank() : 0;
+  const int group0 = blockIdx.x / CL, ngroups = gridDim.x / CL;
+  const int total = args.nbatch * args.mtiles * ((args.ntiles + CL - 1) / CL);
+
+  if (warp == 0) tmem_alloc<512>(smem_u32(tmem_slot));
+  if (tid == 32) {
+    for (int i = 0; i < R::NBS; ++i) { mbar_init(smem_u32(&b_full[i]), 1); mbar_init(smem_u32(&b_empty[i]), 1); }
+    for (int i = 0; i < R::NAS; ++i) { mbar_init(smem_u32(&a_full[i]), 1); mbar_init(smem_u32(&a_empty[i]), CL); }
+    for (int i = 0; i < 2; ++i) { mbar_init(smem_u32(&acc_full[i]), 1); mbar_init(smem_u32(&acc_empty[i]), 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  fence_before();
+  if constexpr (CL > 1) cluster_sync();   // peers' barriers initialised before any multicast
+  else __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer (ring positions continue across tiles)
+      int kg = 0, ai = 0;
+      for (int t = group0; t < total; t += ngroups) {
+        int bz, m0, n0;
+        oz_pers_tile<CL>(args, t, NT, rank, bz, m0, n0);
+        const int b = args.sel ? args.sel[bz] : bz;
+        const int rowA = b * args.A.rpad + m0, rowB = b * args.B.rpad + n0;
+        for (int kb = 0; kb < ksteps; ++kb, ++kg) {
+          const int bst = kg % R::NBS;
+          if (kg >= R::NBS) mbar_wait(smem_u32(&b_empty[bst]), ((kg / R::NBS) - 1) & 1);
+          mbar_expect_tx(smem_u32(&b_full[bst]), R::B_BYTES);
+          tma_load_3d(smem_u32(bring + bst * R::B_STRIDE), &args.mapB, kb * kKStep, rowB, 0, smem_u32(&b_full[bst]));
+          for (int g = 0; g < R::NG; ++g, ++ai) {
+            const int ast = ai % R::NAS;
+            // both CTAs' MMAs released the slot (CL arrivals)
+            if (ai >= R::NAS) mbar_wait(smem_u32(&a_empty[ast]), ((ai / R::NAS) - 1) & 1);
+            mbar_expect_tx(smem_u32(&a_full[ast]), R::A_BYTES);
+            if constexpr (CL == 1) {
+              tma_load_3d(smem_u32(aring + ast * R::A_BYTES), &args.mapA, kb * kKStep, rowA, g * R::SG,
+                          smem_u32(&a_full[ast]));
+            } else if (g % CL == rank) {
+              tma_load_3d_mc(smem_u32(aring + ast * R::A_BYTES), &args.mapA, kb * kKStep, rowA, g * R::SG,
+                             smem_u32(&a_full[ast]), (uint16_t)((1u << CL) - 1u));
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- MMA issuer: tile i accumulates into set i & 1
+      int kg = 0, ai = 0, i = 0;
+      for (int t = group0; t < total; t += ngroups, ++i) {
+        const int buf = i & 1;
+        if (i >= 2) mbar_wait(smem_u32(&acc_empty[buf]), ((i >> 1) - 1) & 1);
+        fence_after();
+        const uint32_t tacc = tmem + (uint32_t)(buf * P::ACC);
+        for (int kb = 0; kb < ksteps; ++kb, ++kg) {
+          const int bst = kg % R::NBS;
+          mbar_wait(smem_u32(&b_full[bst]), (kg / R::NBS) & 1);
+          fence_after();
+          const uint32_t sb = smem_u32(bring + bst * R::B_STRIDE);
+          oz_ring_groups_mc<S, NT, A_SLICE, B_SLICE, R::SG, CL>(tacc, umma_desc(sb, 16, 256, 6), kb > 0 ? 1u : 0u,
+                                                                ai, aring, a_full, a_empty, R::NAS, R::A_BYTES,
+                                                                !(args.dbg & 1));
+          mma_commit(smem_u32(&b_empty[bst]));
+        }
+        mma_commit(smem_u32(&acc_full[buf]));
+      }
+    }
+  } else {
+    // ---- epilogue warps
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int cb = half ? EpiCols<S, NT>::HALF : 0, ce = half ? NT : EpiCols<S, NT>::HALF;
+    int i = 0;
+    for (int t = group0; t < total; t += ngroups, ++i) {
+      int bz, m0, n0;
+      oz_pers_tile<CL>(args, t, NT, rank, bz, m0, n0);
+      const int b = args.sel ? args.sel[bz] : bz;
+      const int buf = i & 1;
+      EpiPre<S, NT, FO, MODE> pre;
+      oz_epi_prefetch<S, NT, FO, MODE>(args, pre, quarter, cb, ce, b, m0, n0, lane);
+      mbar_wait(smem_u32(&acc_full[buf]), (i >> 1) & 1);
+      fence_after();
+      if (!(args.dbg & 4))
+        oz_epilogue<S, NT, FO, MODE>(args, pre, tmem + (uint32_t)(buf * P::ACC), quarter, cb, ce, b, m0, n0, lane);
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&acc_empty[buf]));
+    }
+  }
+  fence_before();
+  // no CTA leaves while its peer may still multicast into its ring or barriers
+  if constexpr (CL > 1) cluster_sync();
+  else __syncthreads();
+  fence_after();
+  if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
 // INT8 tensor-pipe peak probe: one CTA per SM issues back-to-back

@@ -19,6 +19,7 @@ one-shot evaluator).  Reports are returned in chunk order.
 
 from __future__ import annotations
 
+import time
 from typing import Callable, List
 
 
@@ -79,8 +80,12 @@ def split_sizes(B: int, chunks) -> List[int]:
     return sizes + [last]
 
 
-def evaluate_host(submit: Callable, X_host, out_host, chunks=3, trace=None) -> List[object]:
+def evaluate_host(submit: Callable, X_host, out_host, chunks=3, trace=None, streams: int = 1) -> List[object]:
     """``chunks``: a count (tapered split, see split_sizes) or explicit sizes.
+    ``streams``: 1 runs the chunks one after another on the caller's stream;
+    2 alternates them over two compute streams (slot c % 2 on stream c % 2),
+    so chunk c+1's kernels fill the tails and gaps of chunk c's (a small
+    chunk alone leaves SMs idle in every kernel's last wave).
     ``trace``: optional list; timing events (label, event) are appended
     (diagnostics, tools/e2e_chunks.py)."""
     torch = _torch()
@@ -89,66 +94,78 @@ def evaluate_host(submit: Callable, X_host, out_host, chunks=3, trace=None) -> L
         if trace is not None:
             e = torch.cuda.Event(enable_timing=True)
             e.record(stream)
-            trace.append((label, e))
+            trace.append((label, e, time.perf_counter()))
     B = X_host.shape[0]
     sizes = split_sizes(B, chunks)
     chunks = len(sizes)
     bounds = [0]
     for z in sizes:
         bounds.append(bounds[-1] + z)
-    comp = torch.cuda.current_stream()
-    st = _state(torch, comp.device)
+    caller = torch.cuda.current_stream()
+    st = _state(torch, caller.device)
     up, down = st["up"], st["down"]
-    up.wait_stream(comp)
-    down.wait_stream(comp)
-    dev_in = [None, None]
+    if streams > 1:
+        comps = st.get("comps")
+        if comps is None:
+            comps = st["comps"] = [torch.cuda.Stream(), torch.cuda.Stream()]
+        for cs in comps:
+            cs.wait_stream(caller)
+    else:
+        comps = [caller, caller]
+    up.wait_stream(caller)
+    down.wait_stream(caller)
+    dev_in = [None] * chunks
     ev_in = [torch.cuda.Event() for _ in range(chunks)]
-    ev_free = [torch.cuda.Event() for _ in range(chunks)]
     pend = [None] * chunks
     reps = []
 
     def upload(c):
+        # one device input buffer per chunk position (cached across calls), so
+        # every upload is enqueued up front and never waits for a consumer
         lo, hi = bounds[c], bounds[c + 1]
-        slot = c % 2
         with torch.cuda.stream(up):
-            if c >= 2:
-                up.wait_event(ev_free[c - 2])        # slot consumed by chunk c-2's pre graph
             shape = (hi - lo,) + tuple(X_host.shape[1:])
-            buf = st["bufs"].get((slot, shape))
+            buf = st["bufs"].get((c, shape))
             if buf is None:
-                buf = torch.empty(shape, dtype=torch.float64, device=comp.device)
-                st["bufs"][(slot, shape)] = buf
-            dev_in[slot] = buf
+                buf = torch.empty(shape, dtype=torch.float64, device=caller.device)
+                st["bufs"][(c, shape)] = buf
+            dev_in[c] = buf
             mark(f"up{c}<", up)
-            dev_in[slot].copy_(X_host[lo:hi], non_blocking=True)
+            buf.copy_(X_host[lo:hi], non_blocking=True)
             mark(f"up{c}>", up)
             ev_in[c].record(up)
 
     def start(c):
-        comp.wait_event(ev_in[c])
-        mark(f"pre{c}<", comp)
-        pend[c] = submit(dev_in[c % 2], c % 2)
-        mark(f"pre{c}>", comp)
-        ev_free[c].record(comp)
+        comp = comps[c % 2]
+        with torch.cuda.stream(comp):
+            comp.wait_event(ev_in[c])
+            mark(f"pre{c}<", comp)
+            pend[c] = submit(dev_in[c], c % 2)
+            mark(f"pre{c}>", comp)
 
-    upload(0)
-    if chunks > 1:
-        upload(1)
+    for c in range(chunks):
+        upload(c)
     start(0)
+    if streams > 1 and chunks > 1:
+        start(1)
     for c in range(chunks):
         # submit() already enqueued chunk c's Horner chain speculatively
-        # (graphs.py), so finishing c before starting c+1 leaves no GPU gap
-        # and chunk c's download can begin as soon as its chain ends.
-        mark(f"post{c}<", comp)
-        rep = pend[c].finish()
-        mark(f"post{c}>", comp)
+        # (graphs.py), so finishing c before starting the next chunk leaves
+        # no GPU gap and chunk c's download can begin as soon as its chain
+        # ends.
+        comp = comps[c % 2]
+        with torch.cuda.stream(comp):
+            mark(f"post{c}<", comp)
+            rep = pend[c].finish()
+            mark(f"post{c}>", comp)
+            done = torch.cuda.Event()
+            done.record(comp)
         pend[c] = None
-        done = torch.cuda.Event()
-        done.record(comp)
-        if c + 1 < chunks:
-            start(c + 1)
+        if streams > 1:
             if c + 2 < chunks:
-                upload(c + 2)
+                start(c + 2)
+        elif c + 1 < chunks:
+            start(c + 1)
         lo, hi = bounds[c], bounds[c + 1]
         res = rep.result.data
         with torch.cuda.stream(down):
@@ -159,6 +176,9 @@ def evaluate_host(submit: Callable, X_host, out_host, chunks=3, trace=None) -> L
             res.record_stream(down)
             mark(f"down{c}>", down)
         reps.append(rep)
-    comp.wait_stream(down)
-    comp.wait_stream(up)
+    for cs in set(comps):
+        if cs is not caller:
+            caller.wait_stream(cs)
+    caller.wait_stream(down)
+    caller.wait_stream(up)
     return reps

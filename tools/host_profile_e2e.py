@@ -15,14 +15,15 @@ out = torch.empty((2, B, n, n), dtype=torch.float64).pin_memory()
 ctx = m.PrecisionCtx(31)
 fn = pipeline.mixed_exp(30, ctx, timing=False)
 chunks = [32, 32] if len(sys.argv) < 2 else eval(sys.argv[1])
+streams = 1 if len(sys.argv) < 3 else int(sys.argv[2])
 for _ in range(5):
-    pipeline.evaluate_host(fn, Xh, out, chunks)
+    pipeline.evaluate_host(fn, Xh, out, chunks, streams=streams)
 torch.cuda.synchronize()
 pr = cProfile.Profile()
 pr.enable()
 t0 = time.perf_counter()
 for _ in range(20):
-    pipeline.evaluate_host(fn, Xh, out, chunks)
+    pipeline.evaluate_host(fn, Xh, out, chunks, streams=streams)
     torch.cuda.synchronize()
 t1 = time.perf_counter()
 pr.disable()
