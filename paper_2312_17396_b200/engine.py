@@ -551,9 +551,16 @@ class PendingEvaluation:
     for this evaluation's block norms only, plans, enqueues the Horner chain
     and returns the report exactly as the one-shot evaluator would."""
 
-    def __init__(self, finish):
+    def __init__(self, finish, pending=None):
         self._finish = finish
         self._report = None
+        self._pending = pending     # graphs.Pending of a graphed evaluation
+
+    @property
+    def done_event(self):
+        """CUDA event after which the result is final (graphed evaluations
+        after finish(); None otherwise)."""
+        return self._pending.done if self._pending is not None else None
 
     def finish(self):
         if self._report is None:
@@ -563,17 +570,20 @@ class PendingEvaluation:
 
 
 def submit_mixed_general(X, series: CoefficientSeries, ctx: PrecisionCtx, delta: float = 10.0,
-                         with_bound: bool = False, timing: bool = True, slot: int = 0) -> PendingEvaluation:
+                         with_bound: bool = False, timing: bool = True, slot: int = 0,
+                         static_result: bool = False) -> PendingEvaluation:
     """Two-phase ps_mixed_general: enqueue everything up to the block norms
     now, plan and run the Horner phase at ``finish()``.  Submitting batch c+1
     (another ``slot``) before finishing batch c keeps the GPU busy while the
-    host plans; results are bit-identical to ps_mixed_general."""
+    host plans; results are bit-identical to ps_mixed_general.
+    ``static_result``: the report's result is the slot's graph buffer (no
+    device copy; valid until the slot is submitted again)."""
     return _submit(X, series, ctx, delta, True, with_bound, timing, slot,
-                   lambda: ps_mixed_general(X, series, ctx, delta, with_bound, timing))
+                   lambda: ps_mixed_general(X, series, ctx, delta, with_bound, timing), static_result)
 
 
 def submit_mixed_exp(X, m: int, ctx: PrecisionCtx, delta: float = 10.0, with_bound: bool = False,
-                     timing: bool = True, slot: int = 0) -> PendingEvaluation:
+                     timing: bool = True, slot: int = 0, static_result: bool = False) -> PendingEvaluation:
     """Two-phase ps_mixed_exp (fix_params=True; see submit_mixed_general)."""
     if m < 1:
         raise ValueError("m must be >= 1")
@@ -582,10 +592,10 @@ def submit_mixed_exp(X, m: int, ctx: PrecisionCtx, delta: float = 10.0, with_bou
         rep = ps_mixed_exp(X, m, ctx, True, delta, with_bound, timing)
         return PendingEvaluation(lambda: rep)
     return _submit(X, series, ctx, delta, True, with_bound, timing, slot,
-                   lambda: ps_mixed_exp(X, m, ctx, True, delta, with_bound, timing))
+                   lambda: ps_mixed_exp(X, m, ctx, True, delta, with_bound, timing), static_result)
 
 
-def _submit(X, series, ctx, delta, fix_params, with_bound, timing, slot, eager):
+def _submit(X, series, ctx, delta, fix_params, with_bound, timing, slot, eager, static_result=False):
     from . import graphs
     Xt, Xw, single = _input(X)
     B, n = _check_square(Xt, Xw)
@@ -604,10 +614,10 @@ def _submit(X, series, ctx, delta, fix_params, with_bound, timing, slot, eager):
         return PendingEvaluation(lambda: rep)
 
     def fin():
-        prep, norms, result, (digits, nu, nil) = graphs.finish(pend, run_post)
+        prep, norms, result, (digits, nu, nil) = graphs.finish(pend, run_post, clone=not static_result)
         return _graphed_reports((prep, digits, nu, nil, result), ctx, delta, True, fix_params, with_bound,
                                 single, timer)
-    return PendingEvaluation(fin)
+    return PendingEvaluation(fin, pend)
 
 
 def ps_fixed(X, series: CoefficientSeries, ctx: PrecisionCtx, with_bound: bool = False,

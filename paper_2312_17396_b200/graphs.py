@@ -88,10 +88,12 @@ class Pending:
     """A submitted evaluation: the pre graph is enqueued and the norms are
     on their way to pinned memory (``ready`` is recorded after the copy)."""
 
-    __slots__ = ("g", "ready", "timer", "spec")
+    __slots__ = ("g", "ready", "timer", "spec", "spec_done", "done")
 
-    def __init__(self, g, ready, timer, spec=None):
+    def __init__(self, g, ready, timer, spec=None, spec_done=None):
         self.g, self.ready, self.timer, self.spec = g, ready, timer, spec
+        self.spec_done = spec_done    # event after the speculative Horner chain
+        self.done = None              # event after the result is final (set by finish)
 
 
 def submit(key: tuple, Xsrc, build_pre, timer, slot: int = 0) -> Optional[Pending]:
@@ -134,9 +136,12 @@ def submit(key: tuple, Xsrc, build_pre, timer, slot: int = 0) -> Optional[Pendin
         ready.record()
         timer.stop()
         spec = g.last_post if _SPECULATE else None
+        spec_done = None
         if spec is not None:
             g.post[spec][0].replay()      # speculative Horner chain (checked in finish)
-        return Pending(g, ready, timer, spec)
+            spec_done = torch.cuda.Event()
+            spec_done.record()
+        return Pending(g, ready, timer, spec, spec_done)
     except Exception as exc:  # pragma: no cover - capture problems fall back to eager
         _FAILED.add(key)
         _CACHE.pop(key, None)
@@ -145,10 +150,13 @@ def submit(key: tuple, Xsrc, build_pre, timer, slot: int = 0) -> Optional[Pendin
         return None
 
 
-def finish(p: Pending, run_post):
+def finish(p: Pending, run_post, clone: bool = True):
     """Wait for the submitted evaluation's norms (its event only, not the
     whole stream), plan on the host, enqueue the Horner graph for the plan
-    structure and return (prep, norms numpy, result MatBatch, info)."""
+    structure and return (prep, norms numpy, result MatBatch, info).
+    ``clone=False`` returns the graph's static result buffer itself (valid
+    until this slot is submitted again; pipeline.evaluate_host downloads it
+    directly) and sets ``p.done``, the event after which it is final."""
     torch = _torch()
     g, timer = p.g, p.timer
     timer.start("norm_estimation")
@@ -178,13 +186,16 @@ def finish(p: Pending, run_post):
     timer.start("mixed_horner")
     if p.spec is not None and p.spec == post_key:
         _SPEC_STATS["hit"] += 1
+        p.done = p.spec_done
     else:
         if p.spec is not None:
             _SPEC_STATS["miss"] += 1
             _LAST_LAUNCHES += g.post[p.spec][3]   # the speculative chain ran too
         graph.replay()
+        p.done = torch.cuda.Event()
+        p.done.record()
     g.last_post = post_key
-    out = MatBatch(res.data.clone(), res.fmt)
+    out = MatBatch(res.data.clone(), res.fmt) if clone else MatBatch(res.data, res.fmt)
     timer.stop()
     return g.prep, norms, out, info
 

@@ -31,20 +31,26 @@ def _torch():
 def mixed_exp(m: int, ctx, **kw) -> Callable:
     """submit callable for ps_mixed_exp (fix_params=True)."""
     from .engine import submit_mixed_exp
-    return lambda x, slot: submit_mixed_exp(x, m, ctx, slot=slot, **kw)
+
+    def sub(x, slot, static_result=False):
+        return submit_mixed_exp(x, m, ctx, slot=slot, static_result=static_result, **kw)
+    return sub
 
 
 def mixed_general(series, ctx, **kw) -> Callable:
     """submit callable for ps_mixed_general."""
     from .engine import submit_mixed_general
-    return lambda x, slot: submit_mixed_general(x, series, ctx, slot=slot, **kw)
+
+    def sub(x, slot, static_result=False):
+        return submit_mixed_general(x, series, ctx, slot=slot, static_result=static_result, **kw)
+    return sub
 
 
 def eager(fn: Callable) -> Callable:
     """submit callable running a one-shot evaluator at submit time."""
     from .engine import PendingEvaluation
 
-    def sub(x, slot):
+    def sub(x, slot, static_result=False):
         rep = fn(x)
         return PendingEvaluation(lambda: rep)
     return sub
@@ -80,14 +86,23 @@ def split_sizes(B: int, chunks) -> List[int]:
     return sizes + [last]
 
 
-def evaluate_host(submit: Callable, X_host, out_host, chunks=3, trace=None, streams: int = 1) -> List[object]:
+def evaluate_host(submit: Callable, X_host, out_host, chunks=3, trace=None, streams: int = 1,
+                  ahead=None) -> List[object]:
     """``chunks``: a count (tapered split, see split_sizes) or explicit sizes.
-    ``streams``: 1 runs the chunks one after another on the caller's stream;
-    2 alternates them over two compute streams (slot c % 2 on stream c % 2),
-    so chunk c+1's kernels fill the tails and gaps of chunk c's (a small
-    chunk alone leaves SMs idle in every kernel's last wave).
-    ``trace``: optional list; timing events (label, event) are appended
-    (diagnostics, tools/e2e_chunks.py)."""
+
+    ``streams=1``: chunks run one after another on the caller's stream, the
+    next chunk submitted when the previous one is planned.
+    ``streams=2``: every chunk is submitted up front (its own graph slot,
+    chunk c on compute stream c % 2, the Horner chain replayed
+    speculatively, graphs.py), so the GPU never waits for the host planner;
+    the host then plans the chunks in order and each chunk's result is
+    downloaded straight from its slot's buffer once final.  Reports of this
+    mode reference those slot buffers: their ``result`` is valid until the
+    next call with the same shapes (``out_host`` holds the copy).
+    ``ahead`` (default: streams > 1) selects the submit-everything-up-front
+    mode independently of the stream count.
+    ``trace``: optional list; timing events (label, event, host time) are
+    appended (diagnostics, tools/e2e_chunks.py)."""
     torch = _torch()
 
     def mark(label, stream):
@@ -104,6 +119,8 @@ def evaluate_host(submit: Callable, X_host, out_host, chunks=3, trace=None, stre
     caller = torch.cuda.current_stream()
     st = _state(torch, caller.device)
     up, down = st["up"], st["down"]
+    if ahead is None:
+        ahead = streams > 1
     if streams > 1:
         comps = st.get("comps")
         if comps is None:
@@ -140,31 +157,33 @@ def evaluate_host(submit: Callable, X_host, out_host, chunks=3, trace=None, stre
         with torch.cuda.stream(comp):
             comp.wait_event(ev_in[c])
             mark(f"pre{c}<", comp)
-            pend[c] = submit(dev_in[c], c % 2)
+            if ahead:
+                pend[c] = submit(dev_in[c], c, static_result=True)
+            else:
+                pend[c] = submit(dev_in[c], c % 2)
             mark(f"pre{c}>", comp)
 
     for c in range(chunks):
         upload(c)
-    start(0)
-    if streams > 1 and chunks > 1:
-        start(1)
+    if ahead:
+        for c in range(chunks):
+            start(c)
+    else:
+        start(0)
     for c in range(chunks):
-        # submit() already enqueued chunk c's Horner chain speculatively
-        # (graphs.py), so finishing c before starting the next chunk leaves
-        # no GPU gap and chunk c's download can begin as soon as its chain
-        # ends.
         comp = comps[c % 2]
         with torch.cuda.stream(comp):
             mark(f"post{c}<", comp)
             rep = pend[c].finish()
             mark(f"post{c}>", comp)
-            done = torch.cuda.Event()
-            done.record(comp)
+            done = pend[c].done_event
+            if done is None:
+                done = torch.cuda.Event()
+                done.record(comp)
         pend[c] = None
-        if streams > 1:
-            if c + 2 < chunks:
-                start(c + 2)
-        elif c + 1 < chunks:
+        if not ahead and c + 1 < chunks:
+            # submitted after chunk c's planning: its speculative Horner
+            # chain follows chunk c's without a GPU gap
             start(c + 1)
         lo, hi = bounds[c], bounds[c + 1]
         res = rep.result.data

@@ -359,3 +359,11 @@ def test_pipelined_host_evaluation_matches(cuda):
     torch.cuda.synchronize()
     assert len(reps) == 3
     assert np.array_equal(out.numpy(), ref)
+    # every chunk submitted up front over two compute streams (static slot
+    # results downloaded directly), twice so the speculative Horner graphs hit
+    for _ in range(2):
+        out.zero_()
+        reps = pipeline.evaluate_host(pipeline.mixed_exp(30, ctx), Xh, out, chunks=[4, 4, 2, 2], streams=2)
+        torch.cuda.synchronize()
+        assert len(reps) == 4
+        assert np.array_equal(out.numpy(), ref)

@@ -14,26 +14,27 @@ Xh = torch.from_numpy(X).pin_memory()
 out = torch.empty((2, B, n, n), dtype=torch.float64).pin_memory()
 ctx = m.PrecisionCtx(31)
 fn = pipeline.mixed_exp(30, ctx, timing=False)
-cases = [(c, 1) for c in ([32, 32],)] + [(c, 2) for c in (4, [16] * 4, [24, 16, 16, 8], [20, 20, 16, 8], [12, 16, 16, 12, 8], [8] * 8)]
-for chunks, streams in cases:
+cases = [([32, 32], 1, False)] + [(c, 2, True) for c in ([16] * 4, [8, 16, 16, 16, 8], [8, 24, 24, 8])] + \
+    [(c, 1, True) for c in ([16] * 4, [8, 16, 16, 16, 8], [8, 12, 12, 12, 12, 8], [8] * 8, [8, 24, 24, 8])]
+for chunks, streams, ahead in cases:
     for _ in range(3):
-        pipeline.evaluate_host(fn, Xh, out, chunks, streams=streams)
+        pipeline.evaluate_host(fn, Xh, out, chunks, streams=streams, ahead=ahead)
     torch.cuda.synchronize()
     ts = []
     for _ in range(10):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(); pipeline.evaluate_host(fn, Xh, out, chunks, streams=streams); b.record(); b.synchronize()
+        a.record(); pipeline.evaluate_host(fn, Xh, out, chunks, streams=streams, ahead=ahead); b.record(); b.synchronize()
         ts.append(a.elapsed_time(b))
-    print(f"chunks={chunks} streams={streams} median {np.median(ts):.3f} ms  min {min(ts):.3f}  -> {B/np.median(ts)*1e3:.0f} evals/s", flush=True)
+    print(f"chunks={chunks} streams={streams} ahead={ahead} median {np.median(ts):.3f} ms  min {min(ts):.3f}  -> {B/np.median(ts)*1e3:.0f} evals/s", flush=True)
 
 import time as _t
-for chunks, streams in ((4, 2), ([8, 16, 16, 16, 8], 2)):
-    pipeline.evaluate_host(fn, Xh, out, chunks, streams=streams)
+for chunks, streams, ahead in (([16] * 4, 2, True), ([8, 16, 16, 16, 8], 1, True)):
+    pipeline.evaluate_host(fn, Xh, out, chunks, streams=streams, ahead=ahead)
     torch.cuda.synchronize()
     tr = []
     a = torch.cuda.Event(enable_timing=True); a.record()
     h0 = _t.perf_counter()
-    pipeline.evaluate_host(fn, Xh, out, chunks, trace=tr, streams=streams)
+    pipeline.evaluate_host(fn, Xh, out, chunks, trace=tr, streams=streams, ahead=ahead)
     h1 = _t.perf_counter()
     b = torch.cuda.Event(enable_timing=True); b.record(); b.synchronize()
     print(f"--- chunks={chunks} total {a.elapsed_time(b):.3f} ms, host returned at {(h1-h0)*1e3:.3f} ms")
@@ -45,8 +46,8 @@ ref = out.clone()
 pipeline.evaluate_host(fn, Xh, out, 1)
 torch.cuda.synchronize()
 ref = out.clone()
-for chunks, streams in cases:
+for chunks, streams, ahead in cases:
     out.zero_()
-    pipeline.evaluate_host(fn, Xh, out, chunks, streams=streams)
+    pipeline.evaluate_host(fn, Xh, out, chunks, streams=streams, ahead=ahead)
     torch.cuda.synchronize()
-    print(f"bitwise equal chunks={chunks} streams={streams}: {bool(torch.equal(out, ref))}")
+    print(f"bitwise equal chunks={chunks} streams={streams} ahead={ahead}: {bool(torch.equal(out, ref))}")
