@@ -124,6 +124,12 @@ int mpps_colmax(mpps_handle *h, const double *colsums, int nvec, int cols,
 /* one_norm (precision.py:235-249) of every batch member: norms[b]. */
 int mpps_one_norm(mpps_handle *h, const mpps_mat *A, double *norms);
 
+/* one_norm of complex matrices (precision.py:235-249 with mpc_abs, the
+ * reference's native element type, precision.py:78-105): A holds the real
+ * embeddings [[Re, -Im], [Im, Re]] (2nc x 2nc) on which the evaluators run
+ * complex inputs; norms[b * stride] = max_j sum_i |z_ij|, |z| = hypot(Re, Im). */
+int mpps_one_norm_complex(mpps_handle *h, const mpps_mat *A, int nc, double *norms, int stride);
+
 /* One fused matrix-Horner step of horner_mixed (engine.py:249-251):
  *   out = RN_out( 2^eo ( Bprev + 2^-(ey+ei) * RN_fmt(Y * phi) ) )
  * Y and phi share the level-j format, Bprev is the working-format block and

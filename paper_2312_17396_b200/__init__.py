@@ -21,6 +21,7 @@ from .engine import (BatchReport, EvaluationReport, cos_argument, horner_mixed, 
                      ps_fixed, ps_mixed_exp, ps_mixed_general, submit_mixed_exp, submit_mixed_general,
                      PendingEvaluation)
 
+from .complexmat import ComplexMatBatch
 from .expm import expm_ss
 from . import ops, summa, pipeline
 
@@ -37,4 +38,5 @@ __all__ = [
     "PendingEvaluation", "snap_to_lattice",
     "BoundInputs", "BoundInvalidError", "extra_squarings", "gamma",
     "tau_sequence", "thm21_bound", "expm_ss", "ops", "summa", "ps_mixed_pade",
+    "ComplexMatBatch",
 ]

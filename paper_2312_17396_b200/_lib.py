@@ -24,7 +24,7 @@ MPPS_OK, MPPS_EINVAL, MPPS_EFMT, MPPS_ECUDA = 0, 1, 2, 3
 EXPORTED = (
     "mpps_version", "mpps_create", "mpps_destroy", "mpps_set_stream",
     "mpps_last_error", "mpps_launch_count", "mpps_convert", "mpps_gemm",
-    "mpps_axpy", "mpps_powers", "mpps_assemble_blocks", "mpps_one_norm",
+    "mpps_axpy", "mpps_powers", "mpps_assemble_blocks", "mpps_one_norm", "mpps_one_norm_complex",
     "mpps_horner_step", "mpps_horner_scalar_top", "mpps_probe_fma",
     "mpps_assemble_blocks_dist", "mpps_colmax", "mpps_slice", "mpps_gemm_sliced",
     "mpps_horner_step_sliced", "mpps_oz_slices_for", "mpps_probe_i8mma", "mpps_debug_oz_trace",
@@ -117,6 +117,7 @@ def load_library(path: Optional[str] = None):
         lib.mpps_powers.argtypes = [vp, mp, ip]
         lib.mpps_assemble_blocks.argtypes = [vp, mp, ip, ip, vp, mp, vp]
         lib.mpps_one_norm.argtypes = [vp, mp, vp]
+        lib.mpps_one_norm_complex.argtypes = [vp, mp, ip, vp, ip]
         lib.mpps_horner_step.argtypes = [vp, mp, mp, mp, mp, vp, ip, vp, vp, vp]
         lib.mpps_horner_scalar_top.argtypes = [vp, P(ctypes.c_double), ip, mp, mp, mp, vp, ip, vp]
         lib.mpps_probe_fma.argtypes = [vp, ip, ip, ip, vp]
@@ -280,6 +281,14 @@ class Handle:
                                                      _ptr(exp_out)), "horner_step(tc)")
         if end is not None:
             end.record()
+
+    def one_norm_complex(self, A: MatBatch, nc: int, norms_dev, stride: int = 1):
+        """Complex one_norm of the 2nc x 2nc real embeddings in A into
+        norms_dev[b * stride] (norms_dev: a float64 device tensor view whose
+        first element receives batch member 0)."""
+        a = cmat(A)
+        self._check(self.lib.mpps_one_norm_complex(self.h, ctypes.byref(a), int(nc), norms_dev.data_ptr(), int(stride)),
+                    "one_norm_complex")
 
     def one_norm(self, A: MatBatch, norms_dev):
         a = cmat(A)

@@ -437,6 +437,50 @@ __global__ void norm_reduce_kernel(const double *partial, double *norms, int nbl
   if (threadIdx.x == 0) norms[(long long)b * nblk + k] = red[0];
 }
 
+// Complex one_norm on the real embedding [[Re, -Im], [Im, Re]] (2nc x 2nc):
+// partial[b][chunk][col] = sum over the chunk's rows i < nc of
+// |z_i,col| = hypot(Re, Im) (precision.py:235-249 with mpc_abs).
+__global__ void ccolsum_kernel(const ColsumArgs a, int nc) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  const int chunk = blockIdx.y, b = blockIdx.z;
+  if (col >= nc) return;
+  const int row0 = chunk * kRowsPerChunk, row1 = min(nc, row0 + kRowsPerChunk);
+  double s = 0.0;
+  for (int row = row0; row < row1; ++row) {
+    const long long off = (long long)b * a.A.bstride + (long long)row * a.A.ld + col;
+    const long long offi = off + (long long)nc * a.A.ld;
+    double re, im;
+    if (a.fi == F32) {
+      re = (double)((const float *)a.A.data)[off];
+      im = (double)((const float *)a.A.data)[offi];
+    } else {
+      re = ((const double *)a.A.data)[off];
+      im = ((const double *)a.A.data)[offi];
+    }
+    s += hypot(re, im);
+  }
+  a.partial[((long long)b * a.nchunk + chunk) * nc + col] = s;
+}
+
+// out[b * stride] = max_col sum_chunk partial[b][chunk][col]  (fixed order)
+__global__ void norm_reduce_strided_kernel(const double *partial, double *out, int nchunk, int cols, int stride) {
+  const int b = blockIdx.y;
+  double best = 0.0;
+  for (int col = threadIdx.x; col < cols; col += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < nchunk; ++c) s += partial[((long long)b * nchunk + c) * cols + col];
+    best = fmax(best, s);
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = best;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[(long long)b * stride] = red[0];
+}
+
 // colsums[b][k][col] = sum_chunk partial[b][chunk][k][col] (fixed order)
 __global__ void colsum_reduce_kernel(const double *partial, double *colsums, int nblk, int nchunk, int cols,
                                      int batch) {
@@ -794,6 +838,30 @@ int mpps_one_norm(mpps_handle *h, const mpps_mat *A, double *norms) {
   if (rc) return rc;
   norm_reduce_kernel<<<dim3(1, A->batch), 256, 0, h->stream>>>(a.partial, norms, 1, a.nchunk, A->cols);
   rc = after_launch(h, "norm_reduce_kernel");
+  cudaFreeAsync(a.partial, h->stream);
+  return rc;
+}
+
+int mpps_one_norm_complex(mpps_handle *h, const mpps_mat *A, int nc, double *norms, int stride) {
+  int rc = check_mat(h, A, "one_norm_complex.A");
+  if (rc) return rc;
+  if (!norms) return set_err(h, MPPS_EINVAL, "one_norm_complex: null output");
+  if (nc < 0 || A->rows != 2 * nc || A->cols != 2 * nc)
+    return set_err(h, MPPS_EINVAL, "one_norm_complex: A must be the %dx%d real embedding of a %dx%d complex matrix",
+                   2 * nc, 2 * nc, nc, nc);
+  if (stride < 1) return set_err(h, MPPS_EINVAL, "one_norm_complex: stride must be >= 1");
+  if (A->batch == 0 || nc == 0) return MPPS_OK;
+  ColsumArgs a;
+  a.A = ref_of(A); a.rows = nc; a.cols = nc; a.fi = fmt_index(A->fmt);
+  a.nchunk = (nc + kRowsPerChunk - 1) / kRowsPerChunk;
+  size_t pbytes = sizeof(double) * (size_t)A->batch * a.nchunk * nc;
+  cudaError_t e = cudaMallocAsync((void **)&a.partial, pbytes, h->stream);
+  if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "one_norm_complex scratch: %s", cudaGetErrorString(e));
+  ccolsum_kernel<<<dim3((nc + 127) / 128, a.nchunk, A->batch), 128, 0, h->stream>>>(a, nc);
+  rc = after_launch(h, "ccolsum_kernel");
+  if (rc) return rc;
+  norm_reduce_strided_kernel<<<dim3(1, A->batch), 256, 0, h->stream>>>(a.partial, norms, a.nchunk, nc, stride);
+  rc = after_launch(h, "norm_reduce_strided_kernel");
   cudaFreeAsync(a.partial, h->stream);
   return rc;
 }

@@ -39,6 +39,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _lib
+from . import complexmat
 from . import gemm_engine as ge
 from .bigfloat import MPF, exp_rn, fmt7, ln_rn, rn, to_fraction
 from .bounds import BoundInputs, thm21_bound, tau_sequence
@@ -86,11 +87,15 @@ class EvaluationReport:
         self._counts_mode = counts_mode
         self._executed = executed
 
+    _cplx_n = None      # n of a complex evaluation (result is a ComplexMatBatch)
+
     @property
     def result(self) -> MatBatch:
         if self._result is None:
             bm, i = self._batch_view
             self._result = bm.select(i)
+        if self._cplx_n is not None and not isinstance(self._result, complexmat.ComplexMatBatch):
+            self._result = complexmat.ComplexMatBatch(self._result, self._cplx_n)
         return self._result
 
     @property
@@ -327,6 +332,13 @@ def _assemble(h, powers: List[MatBatch], series: CoefficientSeries, ctx: Precisi
     blocks = [MatBatch.empty(wf, B, n, device=dev) for _ in range(r + 1)]
     norms = torch.empty((B, r + 2), dtype=torch.float64, device=dev)
     h.assemble_blocks(powers, m, coeffs, blocks, norms)
+    nc = complexmat.scope()
+    if nc is not None:
+        # complex inputs run on their real embeddings; the planner needs the
+        # complex one_norm (sum of |z|), not the embedding's abs-sums
+        for k in range(r + 1):
+            h.one_norm_complex(blocks[k], nc, norms[:, k], r + 2)
+        h.one_norm_complex(powers[s - 1], nc, norms[:, r + 1], r + 2)
     timer.stop()
     if not sync:
         return _Prepared(wf, s, r, m, powers, blocks, None, cw, norms)
@@ -507,7 +519,7 @@ def _graph_stages(Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: 
     """(key, build_pre, run_post) of the graphed batched pipeline."""
     d = ctx.decimal_digits
     key = (tuple(Xt.shape), str(Xt.device if Xt.is_cuda else "host"), series.coeffs, d, wf, s, kind, delta,
-           apply_switch, ge.engine())
+           apply_switch, ge.engine(), complexmat.scope())
 
     def build_pre(xstatic, capture):
         return _prepare(_lib.handle_for(), xstatic, series, ctx, wf, s, _Buckets(False), None, sync=False)
@@ -620,6 +632,7 @@ def _submit(X, series, ctx, delta, fix_params, with_bound, timing, slot, eager, 
     return PendingEvaluation(fin, pend)
 
 
+@complexmat.complex_aware
 def ps_fixed(X, series: CoefficientSeries, ctx: PrecisionCtx, with_bound: bool = False,
              timing: bool = True):
     """Fixed-precision PS with s = ceil(sqrt(m)) (engine.py:304-345)."""
@@ -660,6 +673,7 @@ def ps_fixed(X, series: CoefficientSeries, ctx: PrecisionCtx, with_bound: bool =
     return _reports(result, fns, None, "fixed", timer.seconds(), with_bound, single)
 
 
+@complexmat.complex_aware
 def ps_mixed_general(X, series: CoefficientSeries, ctx: PrecisionCtx, delta: float = 10.0,
                      with_bound: bool = False, timing: bool = True):
     """Mixed-precision PS for decaying coefficients (engine.py:348-387)."""
@@ -695,6 +709,7 @@ def _mixed_tail(h, prep, ctx, delta, apply_switch, fix_params, with_bound, singl
     return _reports(result, fns, executed, "mixed", timer.seconds(), with_bound, single)
 
 
+@complexmat.complex_aware
 def ps_mixed_exp(X, m: int, ctx: PrecisionCtx, fix_params: bool = True, delta: float = 10.0,
                  with_bound: bool = False, timing: bool = True):
     """Mixed-precision PS for the order-m Taylor approximant of exp
@@ -748,7 +763,11 @@ def _one_norms(Xt, Xw) -> np.ndarray:
     h = _lib.handle_for()
     A = Xw if Xw is not None else MatBatch(Xt.unsqueeze(0), FP64)
     out = torch.empty(A.batch, dtype=torch.float64, device=A.device)
-    h.one_norm(A, out)
+    nc = complexmat.scope()
+    if nc is not None:
+        h.one_norm_complex(A, nc, out, 1)
+    else:
+        h.one_norm(A, out)
     return out.cpu().numpy()
 
 
@@ -811,6 +830,7 @@ def _ps_mixed_exp_one(Xt, Xw, m, ctx, fix_params, delta, with_bound, timing, gro
     return _mixed_tail(h, prep, ctx, delta, False, fix_params, with_bound, True, timer)
 
 
+@complexmat.complex_aware
 def ps_mixed_pade(X, k: int, ctx: PrecisionCtx, delta: float = 10.0, with_bound: bool = False,
                   timing: bool = True):
     """Numerator and denominator of the diagonal [k/k] Pade approximant of
@@ -836,6 +856,7 @@ def ps_mixed_pade(X, k: int, ctx: PrecisionCtx, delta: float = 10.0, with_bound:
     return tuple(out)
 
 
+@complexmat.complex_aware
 def plan_only(X, series: CoefficientSeries, ctx: PrecisionCtx, delta: float = 10.0,
               fix_params: bool = True):
     """Planner only (engine.py:485-504).  The reference forms powers and
@@ -854,6 +875,7 @@ def plan_only(X, series: CoefficientSeries, ctx: PrecisionCtx, delta: float = 10
     return plans[0] if single else plans
 
 
+@complexmat.complex_aware
 def cos_argument(X, ctx: PrecisionCtx) -> MatBatch:
     """harness.py:100-101: the cosine polynomial variable Z = fl(X X) at the
     working precision (formed on device, returned as a working-format batch

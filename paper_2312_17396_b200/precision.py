@@ -234,8 +234,8 @@ def as_fp64_batch(X, device=None):
 
 def mpmatrix_to_float(A) -> np.ndarray:
     """Real fp64 values of a reference ``MPMatrix`` (complex entries with a
-    zero imaginary part); rejects complex inputs (complex support is a
-    SURVEY 8(f) 'next' row)."""
+    zero imaginary part); matrices with imaginary parts are routed to the
+    complex path (complexmat.py) by the entry points before reaching here."""
     out = np.empty((A.n_rows, A.n_cols))
     for i, row in enumerate(A.rows):
         for j, e in enumerate(row):
