@@ -23,7 +23,9 @@ from .engine import (BatchReport, EvaluationReport, cos_argument, horner_mixed, 
 
 from .complexmat import ComplexMatBatch
 from .expm import expm_ss
-from . import ops, summa, pipeline
+from . import ops, summa, pipeline, matio, harness
+from .harness import compare, reference_eval, relative_error
+from .matio import matrix_from_csv, matrix_from_json, matrix_to_csv, matrix_to_json
 
 __version__ = "0.1.0"
 
@@ -38,5 +40,5 @@ __all__ = [
     "PendingEvaluation", "snap_to_lattice",
     "BoundInputs", "BoundInvalidError", "extra_squarings", "gamma",
     "tau_sequence", "thm21_bound", "expm_ss", "ops", "summa", "ps_mixed_pade",
-    "ComplexMatBatch",
+    "ComplexMatBatch", "harness", "reference_eval", "relative_error", "compare", "matio", "matrix_to_json", "matrix_from_json", "matrix_to_csv", "matrix_from_csv",
 ]
