@@ -124,6 +124,14 @@ int mpps_colmax(mpps_handle *h, const double *colsums, int nvec, int cols,
 /* one_norm (precision.py:235-249) of every batch member: norms[b]. */
 int mpps_one_norm(mpps_handle *h, const mpps_mat *A, double *norms);
 
+/* Exact power-of-two scalings of fp32 Horner levels from the planner norms
+ * (device, no host round trip): norms is [batch][r+2]
+ * (||B_0..B_r||, ||Y||); e = -rint(log2 norm) (0 for zero / non-finite);
+ * exps[j][b] = e for the levels j whose bit is set in fp32_mask, else 0;
+ * exp_y[b] = e of ||Y||.  r + 2 <= 64. */
+int mpps_level_exps(mpps_handle *h, const double *norms, int batch, int r, unsigned long long fp32_mask,
+                    int *exps, int *exp_y);
+
 /* one_norm of complex matrices (precision.py:235-249 with mpc_abs, the
  * reference's native element type, precision.py:78-105): A holds the real
  * embeddings [[Re, -Im], [Im, Re]] (2nc x 2nc) on which the evaluators run

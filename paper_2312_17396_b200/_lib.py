@@ -24,7 +24,7 @@ MPPS_OK, MPPS_EINVAL, MPPS_EFMT, MPPS_ECUDA = 0, 1, 2, 3
 EXPORTED = (
     "mpps_version", "mpps_create", "mpps_destroy", "mpps_set_stream",
     "mpps_last_error", "mpps_launch_count", "mpps_convert", "mpps_gemm",
-    "mpps_axpy", "mpps_powers", "mpps_assemble_blocks", "mpps_one_norm", "mpps_one_norm_complex",
+    "mpps_axpy", "mpps_powers", "mpps_assemble_blocks", "mpps_one_norm", "mpps_one_norm_complex", "mpps_level_exps",
     "mpps_horner_step", "mpps_horner_scalar_top", "mpps_probe_fma",
     "mpps_assemble_blocks_dist", "mpps_colmax", "mpps_slice", "mpps_gemm_sliced",
     "mpps_horner_step_sliced", "mpps_oz_slices_for", "mpps_probe_i8mma", "mpps_debug_oz_trace",
@@ -118,6 +118,7 @@ def load_library(path: Optional[str] = None):
         lib.mpps_assemble_blocks.argtypes = [vp, mp, ip, ip, vp, mp, vp]
         lib.mpps_one_norm.argtypes = [vp, mp, vp]
         lib.mpps_one_norm_complex.argtypes = [vp, mp, ip, vp, ip]
+        lib.mpps_level_exps.argtypes = [vp, vp, ip, ip, ctypes.c_ulonglong, vp, vp]
         lib.mpps_horner_step.argtypes = [vp, mp, mp, mp, mp, vp, ip, vp, vp, vp]
         lib.mpps_horner_scalar_top.argtypes = [vp, P(ctypes.c_double), ip, mp, mp, mp, vp, ip, vp]
         lib.mpps_probe_fma.argtypes = [vp, ip, ip, ip, vp]
@@ -289,6 +290,12 @@ class Handle:
         a = cmat(A)
         self._check(self.lib.mpps_one_norm_complex(self.h, ctypes.byref(a), int(nc), norms_dev.data_ptr(), int(stride)),
                     "one_norm_complex")
+
+    def level_exps(self, norms_dev, r: int, fp32_mask: int, exps_dev, exp_y_dev):
+        """norms_dev (B, r+2) float64 -> exps_dev (r+2, B), exp_y_dev (B,) int32."""
+        self._check(self.lib.mpps_level_exps(self.h, norms_dev.data_ptr(), int(norms_dev.shape[0]), int(r),
+                                             int(fp32_mask), exps_dev.data_ptr(), exp_y_dev.data_ptr()),
+                    "level_exps")
 
     def one_norm(self, A: MatBatch, norms_dev):
         a = cmat(A)

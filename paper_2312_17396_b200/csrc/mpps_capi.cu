@@ -866,6 +866,33 @@ int mpps_one_norm_complex(mpps_handle *h, const mpps_mat *A, int nc, double *nor
   return rc;
 }
 
+// Exact power-of-two scalings of the fp32 Horner levels (DESIGN 2): for
+// every batch member b and level j, e = -rint(log2 ||B_j||) (0 for a zero or
+// non-finite norm); exps[j][b] = e where bit j of fp32_mask is set, else 0;
+// exp_y[b] = e of ||Y|| (norms column r+1).
+__global__ void level_exps_kernel(const double *norms, int batch, int r, unsigned long long fp32_mask, int *exps,
+                                  int *exp_y) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nl = r + 2;
+  if (t >= batch * nl) return;
+  const int b = t / nl, j = t % nl;
+  const double v = norms[(long long)b * nl + j];
+  int e = 0;
+  if (v > 0.0 && isfinite(v)) e = -(int)rint(log2(v));
+  exps[(long long)j * batch + b] = ((fp32_mask >> j) & 1ull) ? e : 0;
+  if (j == r + 1) exp_y[b] = e;
+}
+
+int mpps_level_exps(mpps_handle *h, const double *norms, int batch, int r, unsigned long long fp32_mask, int *exps,
+                    int *exp_y) {
+  if (!norms || !exps || !exp_y) return set_err(h, MPPS_EINVAL, "level_exps: null pointer");
+  if (batch < 0 || r < 0 || r + 2 > 64) return set_err(h, MPPS_EINVAL, "level_exps: bad batch %d / r %d", batch, r);
+  const long long n = (long long)batch * (r + 2);
+  if (n == 0) return MPPS_OK;
+  level_exps_kernel<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(norms, batch, r, fp32_mask, exps, exp_y);
+  return after_launch(h, "level_exps_kernel");
+}
+
 int mpps_horner_step(mpps_handle *h, const mpps_mat *Y, const mpps_mat *phi, const mpps_mat *Bprev, mpps_mat *out,
                      const int *sel, int nsel, const int *exp_y, const int *exp_in, const int *exp_out) {
   int rc;
@@ -1111,6 +1138,8 @@ static int launch_oz_pers(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
+    const char *cap = getenv("MPPS_OZ_SMS");   // diagnostics: cap the persistent grid
+    if (cap && atoi(cap) > 0 && atoi(cap) < sms) sms = atoi(cap);
   }
   oz::OzTmaArgs t = a;
   t.mtiles = (a.M + oz::kTileM - 1) / oz::kTileM;

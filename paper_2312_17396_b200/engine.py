@@ -230,22 +230,6 @@ def _exp_for(norm: float) -> int:
     return -int(round(math.log2(norm)))
 
 
-_MASKS: Dict[tuple, object] = {}
-
-
-def _level_mask(fm, r, dev):
-    """Device int32 mask (r+2,) of the fp32 levels of a format tuple (cached,
-    so no host->device copy sits on the post-planner critical path)."""
-    key = (fm, r, str(dev))
-    t = _MASKS.get(key)
-    if t is None:
-        torch = _torch()
-        t = torch.tensor([1 if (0 < j <= r and fm[j] == FP32) else 0 for j in range(r + 2)],
-                         dtype=torch.int32, device=dev)
-        _MASKS[key] = t
-    return t
-
-
 def _exps_for(norms: np.ndarray) -> np.ndarray:
     """Vectorised _exp_for."""
     v = np.asarray(norms, dtype=np.float64)
@@ -412,13 +396,10 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
             # the device copy of the norms (no host round trip on the
             # critical path): e = -round(log2 ||B_j||) for fp32 levels
             if prep.norms_dev is not None:
-                nd = prep.norms_dev
-                ok = torch.isfinite(nd) & (nd > 0)
-                e_all = torch.where(ok, -torch.round(torch.log2(torch.where(ok, nd, torch.ones_like(nd)))),
-                                    torch.zeros_like(nd)).to(torch.int32)       # (B, r+2)
-                lvl = _level_mask(fm, r, dev)
-                exps = (e_all * lvl).t().contiguous()                              # (r+2, B)
-                exp_y = e_all[:, r + 1].contiguous()
+                mask = sum(1 << j for j in range(1, r + 1) if fm[j] == FP32)
+                exps = torch.empty((r + 2, B), dtype=torch.int32, device=dev)
+                exp_y = torch.empty((B,), dtype=torch.int32, device=dev)
+                h.level_exps(prep.norms_dev, r, mask, exps, exp_y)
             else:
                 e = np.zeros((r + 1, B), dtype=np.int32)
                 ey = np.zeros(B, dtype=np.int32)
