@@ -218,6 +218,11 @@ void mpps_debug_oz_trace(void *buf);
  * (0 = default / MPPS_OZ_GROUP).  For tools/ only. */
 void mpps_debug_oz_flags(int flags);
 
+/* Peak probe: global -> shared ingest.  `blocks` CTAs (one per SM) each
+ * stream iters x 16 KB bulk copies (TMA engine, 8 in flight) from src
+ * (span_bytes, keep it L2-resident); bytes = blocks * iters * 16384. */
+int mpps_probe_ingest(mpps_handle *h, int blocks, int iters, const void *src, long long span_bytes);
+
 /* Diagnostic: mpps_probe_i8mma with M = 128, N = n (16..256, multiple of
  * 16), K = 32 MMAs back to back. */
 int mpps_debug_probe_i8mma_n(mpps_handle *h, int blocks, int iters, int n, void *scratch);

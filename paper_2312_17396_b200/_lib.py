@@ -28,7 +28,7 @@ EXPORTED = (
     "mpps_horner_step", "mpps_horner_scalar_top", "mpps_probe_fma",
     "mpps_assemble_blocks_dist", "mpps_colmax", "mpps_slice", "mpps_gemm_sliced",
     "mpps_horner_step_sliced", "mpps_oz_slices_for", "mpps_probe_i8mma", "mpps_debug_oz_trace",
-    "mpps_debug_oz_flags", "mpps_debug_probe_i8mma_n",
+    "mpps_debug_oz_flags", "mpps_debug_probe_i8mma_n", "mpps_probe_ingest",
 )
 
 
@@ -135,6 +135,7 @@ def load_library(path: Optional[str] = None):
         lib.mpps_debug_oz_flags.argtypes = [ip]
         lib.mpps_debug_oz_flags.restype = None
         lib.mpps_debug_probe_i8mma_n.argtypes = [vp, ip, ip, ip, vp]
+        lib.mpps_probe_ingest.argtypes = [vp, ip, ip, vp, ctypes.c_longlong]
         for name in EXPORTED:
             getattr(lib, name).restype = getattr(lib, name).restype or ip
         if path is None:
@@ -319,6 +320,10 @@ class Handle:
                                                     ctypes.byref(o), _ptr(sel), nsel, _ptr(exp_out)),
                     "horner_scalar_top")
 
+
+    def probe_ingest(self, blocks: int, iters: int, src):
+        self._check(self.lib.mpps_probe_ingest(self.h, blocks, iters, src.data_ptr(), src.numel() * src.element_size()),
+                    "probe_ingest")
 
     def probe_i8mma(self, blocks: int, iters: int, scratch):
         self._check(self.lib.mpps_probe_i8mma(self.h, blocks, iters, scratch.data_ptr()), "probe_i8mma")

@@ -1167,8 +1167,38 @@ static int launch_oz_pers(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
   return after_launch(h, "oz_gemm_pers_kernel");
 }
 
+template <int S, int NT, int FO, int MODE>
+static int launch_oz_pwide(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
+  constexpr size_t smem = oz::OzPWide<S, NT>::SMEM;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_pwide_kernel<S, NT, FO, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz pwide attr: %s", cudaGetErrorString(e));
+    configured = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  oz::OzTmaArgs t = a;
+  t.mtiles = (a.M + oz::kTileM - 1) / oz::kTileM;
+  t.ntiles = (a.N + NT - 1) / NT;
+  t.group = oz_group();
+  t.nbatch = nb;
+  if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
+  const long long tiles = (long long)nb * t.mtiles * t.ntiles;
+  oz::oz_gemm_pwide_kernel<S, NT, FO, MODE><<<(unsigned)(tiles < sms ? tiles : sms), oz::kThreadsPers, smem,
+                                              h->stream>>>(t);
+  return after_launch(h, "oz_gemm_pwide_kernel");
+}
+
 // persistent double-buffered kernel for the dd power-chain GEMMs:
-// MPPS_OZ_PERS = 0 (default) off, 1 single CTAs, 2 CTA pairs multicasting A (feed-bound: no gain measured)
+// MPPS_OZ_PERS = 0 (default) off, 1 single CTAs, 2 CTA pairs multicasting A, 3 persistent with 128-byte K
+// boxes (oz_gemm_pwide_kernel); measured no faster than the ring kernel (DESIGN 5.1)
 static int oz_pers_mode(int S, int fo, int mode) {
   static int v = -1;
   if (v < 0) {
@@ -1246,7 +1276,7 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   const bool ring = pers || oz_mode() == 2 || (oz_mode() == 3 && S >= 16);
   const int abox = ring ? (S < 4 ? S : 4) : S;
   int rc;
-  if (wide) {
+  if (wide || pmode == 3) {
     if ((rc = make_slice_map(h, &t.mapA, A, oz::kTileM, 1, 128)) || (rc = make_slice_map(h, &t.mapB, B, NT, S, 128)))
       return rc;
   } else if ((rc = make_slice_map(h, &t.mapA, A, oz::kTileM, abox)) || (rc = make_slice_map(h, &t.mapB, B, NT, S))) {
@@ -1256,6 +1286,7 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   t.trace = g_oz_trace;
   t.dbg = g_oz_dbg;
   if (wide) return dispatch_oz_wide(h, S, fo, mode, t, nb);
+  if (pmode == 3) return launch_oz_pwide<16, 16, DD, 0>(h, t, nb);
   if (pmode == 1) return launch_oz_pers<16, 16, DD, 0, 1>(h, t, nb);
   if (pmode == 2) return launch_oz_pers<16, 16, DD, 0, 2>(h, t, nb);
   return ring ? dispatch_oz_ring(h, S, fo, mode, t, nb) : dispatch_oz_tma(h, S, fo, mode, t, nb);
@@ -1345,6 +1376,18 @@ int mpps_probe_i8mma(mpps_handle *h, int blocks, int iters, void *scratch) {
   }
   oz::i8_mma_probe_kernel<<<blocks, 128, smem, h->stream>>>(iters, (int *)scratch);
   return after_launch(h, "i8_mma_probe_kernel");
+}
+
+int mpps_probe_ingest(mpps_handle *h, int blocks, int iters, const void *src, long long span_bytes) {
+  if (!src || blocks < 1 || iters < 1 || span_bytes < 16384) return set_err(h, MPPS_EINVAL, "probe: bad arguments");
+  const int smem = 8 * 16384 + 2048;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(oz::ingest_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  oz::ingest_probe_kernel<<<blocks, 32, smem, h->stream>>>((const uint8_t *)src, span_bytes, iters);
+  return after_launch(h, "ingest_probe_kernel");
 }
 
 int mpps_debug_probe_i8mma_n(mpps_handle *h, int blocks, int iters, int n, void *scratch) {

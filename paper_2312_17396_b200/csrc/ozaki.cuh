@@ -1023,7 +1023,10 @@ __device__ __forceinline__ void oz_ring_groups(uint32_t tmem, uint64_t bd0, uint
   }
 }
 
-template <int S, int NT>
+// Ring sizes (160 KB of stages next to the epilogue staging tile).  Larger
+// rings (4 B steps, 9-12 A groups, 210 KB) measured no faster: the feed
+// is not bound by the bytes in flight.
+template <int S, int NT, uint32_t EBUF = 0>
 struct OzRing {
   static constexpr int SG = S < 4 ? S : 4;                       // planes per A stage
   static constexpr int NG = (S + SG - 1) / SG;                   // A stages per K step
@@ -1037,17 +1040,19 @@ struct OzRing {
   static constexpr size_t SMEM = (size_t)NBS * B_STRIDE + (size_t)NAS * A_BYTES + 2048;
 };
 template <int S, int NT, int FO, int MODE>
-__host__ __device__ constexpr size_t oz_ring_smem_bytes() { return OzRing<S, NT>::SMEM + oz_ebuf_bytes<S, NT, FO, MODE>(); }
+__host__ __device__ constexpr size_t oz_ring_smem_bytes() {
+  return OzRing<S, NT, oz_ebuf_bytes<S, NT, FO, MODE>()>::SMEM + oz_ebuf_bytes<S, NT, FO, MODE>();
+}
 
 template <int S, int NT, int FO, int MODE>
 __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_ring_kernel(const __grid_constant__ OzTmaArgs args) {
-  using R = OzRing<S, NT>;
+  constexpr uint32_t EBUF = oz_ebuf_bytes<S, NT, FO, MODE>();
+  using R = OzRing<S, NT, EBUF>;
   constexpr uint32_t A_SLICE = kTileM * kKStep;
   constexpr uint32_t B_SLICE = NT * kKStep;
   constexpr int TCOLS = tmem_cols_for(S * NT);
 
   constexpr bool STAGED = oz_staged<S, NT, FO, MODE>();
-  constexpr uint32_t EBUF = oz_ebuf_bytes<S, NT, FO, MODE>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t *bring = smem;
@@ -1494,6 +1499,158 @@ __global__ void __launch_bounds__(128, 1) i8_mma_probe_kernel(int iters, int *ou
   fence_before();
   __syncthreads();
   if (threadIdx.x < 32) tmem_dealloc<256>(tmem);
+}
+
+// --------------------- persistent + double-buffered TMEM + 128-byte K boxes
+// The wide feed keeps the L2 slices at ~22 % (vs ~64 % for 32-byte boxes,
+// ncu lts__throughput at n = 1024), which leaves room for NT = 16 tiles:
+// two 256-column accumulator sets, the epilogue of tile i overlapping the
+// MMAs of tile i+1 and the producer streaming across tile boundaries.
+// Warp 0: TMA producer, warp 1: MMA issuer, warps 2..9: epilogue.
+template <int S, int NT>
+struct OzPWide {
+  using W = OzWide<S, NT>;
+  static constexpr int NBS = 2;
+  static constexpr int NAS_FIT = (int)((222ll * 1024 - 2048 - NBS * (long long)W::B_STRIDE) / W::A_BYTES);
+  static constexpr int NAS = NAS_FIT > 12 ? 12 : NAS_FIT;
+  static constexpr int ACC = S * NT;
+  static_assert(2 * ACC <= 512, "two accumulator sets must fit in TMEM");
+  static constexpr size_t SMEM = (size_t)NBS * W::B_STRIDE + (size_t)NAS * W::A_BYTES + 2048;
+};
+
+template <int S, int NT, int FO, int MODE>
+__global__ void __launch_bounds__(kThreadsPers, 1) oz_gemm_pwide_kernel(const __grid_constant__ OzTmaArgs args) {
+  using W = OzWide<S, NT>;
+  using P = OzPWide<S, NT>;
+  constexpr int NAS = P::NAS;
+  static_assert(NAS >= 3, "A ring does not fit");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t *bring = smem;
+  uint8_t *aring = smem + P::NBS * W::B_STRIDE;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(aring + NAS * W::A_BYTES);
+  uint64_t *b_full = bar, *b_empty = bar + P::NBS;
+  uint64_t *a_full = bar + 2 * P::NBS, *a_empty = a_full + NAS;
+  uint64_t *acc_full = a_empty + NAS, *acc_empty = acc_full + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int kpad = args.A.kpad;
+  const int kstages = (kpad + W::KB - 1) / W::KB;
+  const int total = args.nbatch * args.mtiles * args.ntiles;
+
+  if (warp == 0) tmem_alloc<512>(smem_u32(tmem_slot));
+  if (tid == 32) {
+    for (int i = 0; i < P::NBS; ++i) { mbar_init(smem_u32(&b_full[i]), 1); mbar_init(smem_u32(&b_empty[i]), 1); }
+    for (int i = 0; i < NAS; ++i) { mbar_init(smem_u32(&a_full[i]), 1); mbar_init(smem_u32(&a_empty[i]), 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(smem_u32(&acc_full[i]), 1); mbar_init(smem_u32(&acc_empty[i]), 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int kg = 0, ai = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        int bz, m0, n0;
+        oz_pers_tile<1>(args, t, NT, 0, bz, m0, n0);
+        const int b = args.sel ? args.sel[bz] : bz;
+        const int rowA = b * args.A.rpad + m0, rowB = b * args.B.rpad + n0;
+        for (int kb = 0; kb < kstages; ++kb, ++kg) {
+          const int bst = kg % P::NBS;
+          if (kg >= P::NBS) mbar_wait(smem_u32(&b_empty[bst]), ((kg / P::NBS) - 1) & 1);
+          mbar_expect_tx(smem_u32(&b_full[bst]), W::B_BYTES);
+          tma_load_3d(smem_u32(bring + bst * W::B_STRIDE), &args.mapB, kb * W::KB, rowB, 0, smem_u32(&b_full[bst]));
+          for (int s = 0; s < S; ++s, ++ai) {
+            const int ast = ai % NAS;
+            if (ai >= NAS) mbar_wait(smem_u32(&a_empty[ast]), ((ai / NAS) - 1) & 1);
+            mbar_expect_tx(smem_u32(&a_full[ast]), W::A_BYTES);
+            tma_load_3d(smem_u32(aring + ast * W::A_BYTES), &args.mapA, kb * W::KB, rowA, s, smem_u32(&a_full[ast]));
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int kg = 0, ai = 0, i = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
+        const int buf = i & 1;
+        if (i >= 2) mbar_wait(smem_u32(&acc_empty[buf]), ((i >> 1) - 1) & 1);
+        fence_after();
+        const uint32_t tacc = tmem + (uint32_t)(buf * P::ACC);
+        for (int kb = 0; kb < kstages; ++kb, ++kg) {
+          const int bst = kg % P::NBS;
+          mbar_wait(smem_u32(&b_full[bst]), (kg / P::NBS) & 1);
+          fence_after();
+          const int left = (kpad - kb * W::KB) / kKStep;
+          const int nk = left < 4 ? left : 4;
+          if (!(args.dbg & 1))
+            oz_wide_stage<S, NT>(tacc, smem_u32(bring + bst * W::B_STRIDE), nk, kb > 0 ? 1u : 0u, ai, aring, a_full,
+                                 a_empty, NAS);
+          else
+            for (int s = 0; s < S; ++s, ++ai) {   // diagnostics: feed only
+              mbar_wait(smem_u32(&a_full[ai % NAS]), (ai / NAS) & 1);
+              mma_commit(smem_u32(&a_empty[ai % NAS]));
+            }
+          mma_commit(smem_u32(&b_empty[bst]));
+        }
+        mma_commit(smem_u32(&acc_full[buf]));
+      }
+    }
+  } else {
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int cb = half ? EpiCols<S, NT>::HALF : 0, ce = half ? NT : EpiCols<S, NT>::HALF;
+    int i = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
+      int bz, m0, n0;
+      oz_pers_tile<1>(args, t, NT, 0, bz, m0, n0);
+      const int b = args.sel ? args.sel[bz] : bz;
+      const int buf = i & 1;
+      EpiPre<S, NT, FO, MODE> pre;
+      oz_epi_prefetch<S, NT, FO, MODE>(args, pre, quarter, cb, ce, b, m0, n0, lane);
+      mbar_wait(smem_u32(&acc_full[buf]), (i >> 1) & 1);
+      fence_after();
+      if (!(args.dbg & 4))
+        oz_epilogue<S, NT, FO, MODE>(args, pre, tmem + (uint32_t)(buf * P::ACC), quarter, cb, ce, b, m0, n0, lane);
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&acc_empty[buf]));
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+// Global -> shared ingest probe: one CTA per SM streams 16 KB bulk copies
+// (the TMA engine, 8 in flight) from an L2-resident buffer; the tensor-core
+// GEMMs are bound by this per-SM fill rate (~25 B/clk with every SM
+// loading), not by the MMAs (DESIGN 5.1).
+__global__ void __launch_bounds__(32, 1) ingest_probe_kernel(const uint8_t *src, long long span, int iters) {
+  constexpr int CH = 16384, NB = 8;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sm + NB * CH);
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < NB; ++i) mbar_init(smem_u32(&bar[i]), 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  const long long nchunks = span / CH;
+  const long long base = ((long long)blockIdx.x * 7919) % nchunks;
+  for (int it = 0; it < iters; ++it) {
+    const int st = it % NB;
+    if (it >= NB) mbar_wait(smem_u32(&bar[st]), ((it / NB) - 1) & 1);
+    mbar_expect_tx(smem_u32(&bar[st]), CH);
+    const uint8_t *g = src + ((base + it) % nchunks) * CH;
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(sm + st * CH)),
+                 "l"(g), "r"(CH), "r"(smem_u32(&bar[st]))
+                 : "memory");
+  }
+  for (int it = iters > NB ? iters - NB : 0; it < iters; ++it) mbar_wait(smem_u32(&bar[it % NB]), (it / NB) & 1);
 }
 
 }  // namespace oz
