@@ -565,9 +565,11 @@ def run_ours(args, rank, world, local_rank):
         ach = ingest / (sec / cnt) / 1e12
         roof["ingest"] = {"achieved": ach, "peak": peaks["ingest_tbps"], "unit": "TB/s", "frac": ach / peaks["ingest_tbps"],
                           "bytes_per_launch": ingest,
-                          "note": "the binding resource: digit planes moved global->shared per launch vs the "
-                                  "bulk-copy ingest probe (one CTA per SM) run in this bench; the INT8 MMAs "
-                                  "finish faster than the planes arrive (DESIGN 5.1)"}
+                          "note": "digit-plane bytes moved global->shared per launch (128-row x NT tiles, "
+                                  "all S planes of A and B over K) and their rate vs the bulk-copy ingest probe "
+                                  "(one CTA per SM, L2-resident 16 KB copies) run in this bench; with 32-byte K "
+                                  "boxes the L2 slices run at ~64% of peak (ncu lts__throughput, n=1024) and the "
+                                  "tensor pipe at ~62% -- DESIGN 5.1"}
     kkey = f"{kind} {fname}->{names[fout]} {M}x{N}x{K} x{nb}"
     traffic, tsrc = None, None
     try:   # committed ncu --set full capture of this kernel at this shape (profiles/traffic.json)

@@ -1229,9 +1229,11 @@ static int launch_oz_wide(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
 }
 
 // 128-byte K boxes (MPPS_OZ_WIDE=0 disables, 2 forces every supported case):
-// measured faster for qd (n = 1024: 0.53 vs 0.63 ms; 2048: 3.56 vs 4.06 ms)
-// and for dd at K >= 4096 (n = 8192: 48.6 vs 50.8 ms); the 32-byte-box ring
-// kernel stays ahead for smaller dd products (n = 256: 0.167 vs 0.181 ms).
+// default only for dd at K >= 4096 (n = 8192: 48.6 vs 50.8 ms).  The
+// 32-byte-box ring kernel stays ahead for smaller dd products (n = 256:
+// 0.167 vs 0.181 ms) and for qd inside the cfg4 evaluation (25.6 vs 24.0
+// evals/s, same-box A/B; an isolated qd GEMM microbenchmark had favoured
+// the wide kernel).
 static bool oz_wide_for(int S, int fo, int mode, int K) {
   static int v = -1;
   if (v < 0) {
@@ -1239,7 +1241,7 @@ static bool oz_wide_for(int S, int fo, int mode, int K) {
     v = e ? atoi(e) : 1;
   }
   if (!v) return false;
-  return (S == 16 && mode == 0 && fo == DD && (K >= 4096 || v == 2)) || (S == 31 && fo == QD);
+  return (S == 16 && mode == 0 && fo == DD && (K >= 4096 || v == 2)) || (S == 31 && fo == QD && v == 2);
 }
 
 static int dispatch_oz_wide(mpps_handle *h, int S, int fo, int mode, const oz::OzTmaArgs &a, int nb) {
