@@ -1292,7 +1292,10 @@ struct OzPers {
   static constexpr int NAS_FIT = (int)((kBudget - NBS * (size_t)B_STRIDE) / A_BYTES);
   static constexpr int NAS = NAS_FIT > 12 ? 12 : NAS_FIT;
   static constexpr int ACC = S * NT;  // TMEM columns per accumulator set
-  static_assert(2 * ACC <= 512, "two accumulator sets must fit in TMEM");
+  // two sets when they fit (epilogue overlaps the next tile's MMAs); one set
+  // otherwise (NT = 32 dd: only the feed runs ahead during the epilogue)
+  static constexpr int NACC = (2 * ACC <= 512) ? 2 : 1;
+  static_assert(NACC * ACC <= 512, "accumulators must fit in TMEM");
   static constexpr size_t SMEM = (size_t)NBS * B_STRIDE + (size_t)NAS * A_BYTES + 2048;
 };
 
@@ -1420,8 +1423,8 @@ __global__ void __launch_bounds__(kThreadsPers, 1) oz_gemm_pers_kernel(const __g
       // ---- MMA issuer: tile i accumulates into set i & 1
       int kg = 0, ai = 0, i = 0;
       for (int t = group0; t < total; t += ngroups, ++i) {
-        const int buf = i & 1;
-        if (i >= 2) mbar_wait(smem_u32(&acc_empty[buf]), ((i >> 1) - 1) & 1);
+        const int buf = i % P::NACC;
+        if (i >= P::NACC) mbar_wait(smem_u32(&acc_empty[buf]), ((i / P::NACC) - 1) & 1);
         fence_after();
         const uint32_t tacc = tmem + (uint32_t)(buf * P::ACC);
         for (int kb = 0; kb < ksteps; ++kb, ++kg) {
@@ -1446,10 +1449,10 @@ __global__ void __launch_bounds__(kThreadsPers, 1) oz_gemm_pers_kernel(const __g
       int bz, m0, n0;
       oz_pers_tile<CL>(args, t, NT, rank, bz, m0, n0);
       const int b = args.sel ? args.sel[bz] : bz;
-      const int buf = i & 1;
+      const int buf = i % P::NACC;
       EpiPre<S, NT, FO, MODE> pre;
       oz_epi_prefetch<S, NT, FO, MODE>(args, pre, quarter, cb, ce, b, m0, n0, lane);
-      mbar_wait(smem_u32(&acc_full[buf]), (i >> 1) & 1);
+      mbar_wait(smem_u32(&acc_full[buf]), (i / P::NACC) & 1);
       fence_after();
       if (!(args.dbg & 4))
         oz_epilogue<S, NT, FO, MODE>(args, pre, tmem + (uint32_t)(buf * P::ACC), quarter, cb, ce, b, m0, n0, lane);
