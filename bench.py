@@ -524,9 +524,9 @@ def run_ours(args, rank, world, local_rank):
         by_key[key] = (len(durs), sum(durs))
     names = {7: "fp32", 15: "fp64", 31: "dd", 63: "qd"}
     if not by_key:
-        by_key[("none", 31, 31, 1, 1, 1, 1)] = (1, 1.0)
+        by_key[("none", 31, 31, 1, 1, 1, 1, 0, 0)] = (1, 1.0)
     dom = max(by_key.items(), key=lambda kv: kv[1][1])
-    (kind, fin, fout, M, N, K, nb), (cnt, sec) = dom
+    (kind, fin, fout, M, N, K, nb, S_used, db_used), (cnt, sec) = dom
     eager_step = None
     fname = names[fin]
     logical = 2.0 * M * N * K * nb / (sec / cnt) / 1e12       # logical TFLOP/s of the format
@@ -538,8 +538,9 @@ def run_ours(args, rank, world, local_rank):
     if kind.endswith("_tc"):
         # INT8 tensor-core GEMM by exact digit-plane splitting: the hardware
         # bound is the INT8 tensor pipe; algorithmic ops per launch =
-        # 2 M N K x (S(S+1)/2 plane pairs), S = 4/8/16/31 for fp32/fp64/dd/qd
-        S = {7: 4, 15: 8, 31: 16, 63: 31}[fin]
+        # 2 M N K x (S(S+1)/2 plane pairs); S = 4/8/16/31 (7-bit digits) or
+        # 4/8/14/28 (8-bit) for fp32/fp64/dd/qd, recorded per launch
+        S = S_used or {7: 4, 15: 8, 31: 16, 63: 31}[fin]
         achieved = logical * S * (S + 1) / 2
         roof = {"bound": "tensor (int8)", "achieved": achieved, "peak": peaks["int8_tops"],
                 "unit": "TOPS (int8)", "frac": achieved / peaks["int8_tops"],
@@ -559,7 +560,7 @@ def run_ours(args, rank, world, local_rank):
         # global->shared bytes the kernel moves per launch: every 128-row x
         # NT-column output tile streams all S digit planes of its A rows and
         # B columns over K (NT = 32, 16 for qd)
-        NT = 16 if S > 16 else 32
+        NT = 16 if S > 16 else 32      # 14 planes (8-bit dd) still use NT = 32
         tiles = nb * (-(-M // 128)) * (-(-N // NT))
         ingest = tiles * (-(-K // 32)) * S * (128 + NT) * 32.0
         ach = ingest / (sec / cnt) / 1e12
@@ -571,6 +572,9 @@ def run_ours(args, rank, world, local_rank):
                                   "boxes the L2 slices run at ~64% of peak (ncu lts__throughput, n=1024) and the "
                                   "tensor pipe at ~62% -- DESIGN 5.1"}
     kkey = f"{kind} {fname}->{names[fout]} {M}x{N}x{K} x{nb}"
+    if kind.endswith("_tc"):
+        roof["digit_planes"] = S
+        roof["digit_bits"] = db_used
     traffic, tsrc = None, None
     try:   # committed ncu --set full capture of this kernel at this shape (profiles/traffic.json)
         tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")))

@@ -163,8 +163,9 @@ int mpps_horner_scalar_top(mpps_handle *h, const double *bm_words, int fmt_top,
  * power-of-two scale per row (side 0, the left operand) or per column
  * (side 1, the right operand, stored transposed); C = A B is then a sum of
  * exact int32 tensor-core products recombined in the target format.
- * Slices used per format: fp64 8, dd 16, qd 31 (first digits of a finer
- * split are a valid coarser split, so one slicing serves every level).
+ * Slices used per format: fp64 8, dd 16 (14 with 8-bit digits), qd 31 (28)
+ * (first digits of a finer split are a valid coarser split, so one slicing
+ * serves every level).
  */
 typedef struct {
   void *digits;      /* device int8 [nslices][batch][rpad][kpad]            */
@@ -172,6 +173,9 @@ typedef struct {
   int nslices, batch;
   int rpad;          /* padded rows (side 0) / columns (side 1), % 128 == 0 */
   int kpad;          /* padded inner dimension, % 32 == 0                   */
+  int digit_bits;    /* 7: digits in [-65, 65]; 8: [-128, 127] (first digit
+                        6 bits either way); 0 means 7.  Both operands of a
+                        product must use the same width.                    */
 } mpps_slices;
 
 /* Split src (side 0: by rows, side 1: by columns) into out->nslices digit
@@ -193,8 +197,15 @@ int mpps_horner_step_sliced(mpps_handle *h, const mpps_slices *Y,
                             const int *sel, int nsel, const int *exp_y,
                             const int *exp_in, const int *exp_out);
 
-/* Digit planes the tensor-core path uses for a format (-1: not supported). */
+/* Digit planes the tensor-core path uses for a format (-1: not supported):
+ * 7-bit digits fp32 4, fp64 8, dd 16, qd 31 (mpps_oz_slices_for); 8-bit
+ * digits fp32 4, fp64 8, dd 14, qd 28 (mpps_oz_slices_for_bits(fmt, 8)). */
 int mpps_oz_slices_for(int fmt);
+int mpps_oz_slices_for_bits(int fmt, int digit_bits);
+
+/* Largest inner dimension K for which 8-bit digits keep every int32
+ * diagonal accumulator exact at any format (qd: 28 planes). */
+int mpps_oz_max_k_8bit(void);
 
 /* Diagnostic: pipe-peak probe used by bench.py for the per-precision
  * roofline denominators (not a reference operator).  Launches `blocks`

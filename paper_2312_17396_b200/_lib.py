@@ -27,7 +27,7 @@ EXPORTED = (
     "mpps_axpy", "mpps_powers", "mpps_assemble_blocks", "mpps_one_norm", "mpps_one_norm_complex", "mpps_level_exps",
     "mpps_horner_step", "mpps_horner_scalar_top", "mpps_probe_fma",
     "mpps_assemble_blocks_dist", "mpps_colmax", "mpps_slice", "mpps_gemm_sliced",
-    "mpps_horner_step_sliced", "mpps_oz_slices_for", "mpps_probe_i8mma", "mpps_debug_oz_trace",
+    "mpps_horner_step_sliced", "mpps_oz_slices_for", "mpps_oz_slices_for_bits", "mpps_oz_max_k_8bit", "mpps_probe_i8mma", "mpps_debug_oz_trace",
     "mpps_debug_oz_flags", "mpps_debug_probe_i8mma_n", "mpps_probe_ingest",
 )
 
@@ -40,6 +40,7 @@ class CSlices(ctypes.Structure):
         ("batch", ctypes.c_int),
         ("rpad", ctypes.c_int),
         ("kpad", ctypes.c_int),
+        ("digit_bits", ctypes.c_int),
     ]
 
 
@@ -47,19 +48,19 @@ class Slices:
     """Digit planes of one operand for the tensor-core path (torch buffers):
     digits int8 (S, batch, rpad, kpad), exps int32 (batch, rpad)."""
 
-    __slots__ = ("digits", "exps", "S", "rows", "k")
+    __slots__ = ("digits", "exps", "S", "rows", "k", "db")
 
-    def __init__(self, S: int, batch: int, rows: int, k: int, device):
+    def __init__(self, S: int, batch: int, rows: int, k: int, device, db: int = 7):
         import torch
         rpad = -(-rows // 128) * 128
         kpad = -(-k // 32) * 32
         self.digits = torch.empty((S, batch, rpad, kpad), dtype=torch.int8, device=device)
         self.exps = torch.empty((batch, rpad), dtype=torch.int32, device=device)
-        self.S, self.rows, self.k = S, rows, k
+        self.S, self.rows, self.k, self.db = S, rows, k, db
 
     def c(self) -> CSlices:
         d = self.digits
-        return CSlices(d.data_ptr(), self.exps.data_ptr(), d.shape[0], d.shape[1], d.shape[2], d.shape[3])
+        return CSlices(d.data_ptr(), self.exps.data_ptr(), d.shape[0], d.shape[1], d.shape[2], d.shape[3], self.db)
 
 
 class CMat(ctypes.Structure):
@@ -129,6 +130,8 @@ def load_library(path: Optional[str] = None):
         lib.mpps_gemm_sliced.argtypes = [vp, sp, sp, ip, ip, ip, ip, mp, vp, ip]
         lib.mpps_horner_step_sliced.argtypes = [vp, sp, sp, ip, mp, mp, vp, ip, vp, vp, vp]
         lib.mpps_oz_slices_for.argtypes = [ip]
+        lib.mpps_oz_slices_for_bits.argtypes = [ip, ip]
+        lib.mpps_oz_max_k_8bit.argtypes = []
         lib.mpps_probe_i8mma.argtypes = [vp, ip, ip, vp]
         lib.mpps_debug_oz_trace.argtypes = [vp]
         lib.mpps_debug_oz_trace.restype = None
@@ -219,7 +222,7 @@ class Handle:
     def gemm(self, A: MatBatch, B: MatBatch, C: MatBatch, sel=None):
         a, b, c = cmat(A), cmat(B), cmat(C)
         nsel = 0 if sel is None else sel.numel()
-        end = self._ev(("gemm", A.fmt, C.fmt, A.rows, B.cols, A.cols, nsel or C.batch))
+        end = self._ev(("gemm", A.fmt, C.fmt, A.rows, B.cols, A.cols, nsel or C.batch, 0, 0))
         self._check(self.lib.mpps_gemm(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
                                        _ptr(sel), nsel), "mat_mul")
         if end is not None:
@@ -251,13 +254,17 @@ class Handle:
                     "colmax")
 
     # --- tensor-core path -------------------------------------------
-    def slices_for(self, fmt: int) -> int:
-        return int(self.lib.mpps_oz_slices_for(fmt))
+    def slices_for(self, fmt: int, db: int = 7) -> int:
+        return int(self.lib.mpps_oz_slices_for_bits(fmt, db))
 
-    def slice(self, src: MatBatch, side: int, S: int, sel=None) -> "Slices":
-        """side 0: split rows (left operand); side 1: split columns (right)."""
+    def max_k_8bit(self) -> int:
+        return int(self.lib.mpps_oz_max_k_8bit())
+
+    def slice(self, src: MatBatch, side: int, S: int, sel=None, db: int = 7) -> "Slices":
+        """side 0: split rows (left operand); side 1: split columns (right);
+        db: digit bits (7 or 8)."""
         rows, k = (src.rows, src.cols) if side == 0 else (src.cols, src.rows)
-        out = Slices(S, src.batch, rows, k, src.device)
+        out = Slices(S, src.batch, rows, k, src.device, db)
         c_src, c_out = cmat(src), out.c()
         nsel = 0 if sel is None else sel.numel()
         self._check(self.lib.mpps_slice(self.h, ctypes.byref(c_src), side, ctypes.byref(c_out), _ptr(sel), nsel),
@@ -267,7 +274,7 @@ class Handle:
     def gemm_sliced(self, A: "Slices", B: "Slices", S: int, C: MatBatch, sel=None):
         a, b, c = A.c(), B.c(), cmat(C)
         nsel = 0 if sel is None else sel.numel()
-        end = self._ev(("gemm_tc", C.fmt, C.fmt, A.rows, B.rows, A.k, nsel or C.batch))
+        end = self._ev(("gemm_tc", C.fmt, C.fmt, A.rows, B.rows, A.k, nsel or C.batch, S, A.db))
         self._check(self.lib.mpps_gemm_sliced(self.h, ctypes.byref(a), ctypes.byref(b), S, A.rows, B.rows, A.k,
                                               ctypes.byref(c), _ptr(sel), nsel), "mat_mul(tc)")
         if end is not None:
@@ -277,7 +284,7 @@ class Handle:
                            exp_in=None, exp_out=None, fmt_in: int = 31):
         y, p, b, o = Y.c(), phi.c(), cmat(Bprev), cmat(out)
         nsel = 0 if sel is None else sel.numel()
-        end = self._ev(("horner_tc", fmt_in, out.fmt, Y.rows, phi.rows, Y.k, nsel or out.batch))
+        end = self._ev(("horner_tc", fmt_in, out.fmt, Y.rows, phi.rows, Y.k, nsel or out.batch, S, Y.db))
         self._check(self.lib.mpps_horner_step_sliced(self.h, ctypes.byref(y), ctypes.byref(p), S, ctypes.byref(b),
                                                      ctypes.byref(o), _ptr(sel), nsel, _ptr(exp_y), _ptr(exp_in),
                                                      _ptr(exp_out)), "horner_step(tc)")
@@ -305,7 +312,7 @@ class Handle:
     def horner_step(self, Y, phi, Bprev, out, sel=None, exp_y=None, exp_in=None, exp_out=None):
         y, p, b, o = cmat(Y), cmat(phi), cmat(Bprev), cmat(out)
         nsel = 0 if sel is None else sel.numel()
-        end = self._ev(("horner", Y.fmt, out.fmt, Y.rows, Y.rows, Y.rows, nsel or out.batch))
+        end = self._ev(("horner", Y.fmt, out.fmt, Y.rows, Y.rows, Y.rows, nsel or out.batch, 0, 0))
         self._check(self.lib.mpps_horner_step(self.h, ctypes.byref(y), ctypes.byref(p), ctypes.byref(b),
                                               ctypes.byref(o), _ptr(sel), nsel, _ptr(exp_y), _ptr(exp_in),
                                               _ptr(exp_out)), "horner_step")

@@ -969,12 +969,25 @@ int mpps_probe_fma(mpps_handle *h, int fmt, int blocks, int iters, void *scratch
 }  // extern "C"
 
 // ------------------------------------------------ tensor-core (Ozaki) path
-static int oz_slices_for(int fi) { return fi == QD ? 31 : fi == DD ? 16 : fi == F64 ? 8 : fi == F32 ? 4 : -1; }
+static int oz_slices_for(int fi, int db = 7) {
+  if (db == 8) return fi == QD ? 28 : fi == DD ? 14 : fi == F64 ? 8 : fi == F32 ? 4 : -1;
+  return fi == QD ? 31 : fi == DD ? 16 : fi == F64 ? 8 : fi == F32 ? 4 : -1;
+}
+static int slice_db(const mpps_slices *s) { return s->digit_bits == 8 ? 8 : 7; }
+// |D_d| <= K * sum over the diagonal's pairs of |a_s b_t|: 7-bit digits
+// <= 65^2 each; 8-bit: <= 128^2, or 65 * 128 for the pairs with a 6-bit
+// first digit.  The bound must stay below 2^31.
+static double oz_diag_bound(int S, int db) {
+  if (db == 8) return (S >= 2 ? (S - 2) * 16384.0 + 2 * 8320.0 : 4225.0);
+  return S * 4225.0;
+}
+static const int kOzMaxK8 = 4800;   // 28 planes: 442624 * 4800 < 2^31
 
 static oz::SliceRef sref(const mpps_slices *s) {
   oz::SliceRef r;
   r.digits = (int8_t *)s->digits; r.exps = s->exps; r.S = s->nslices; r.batch = s->batch;
   r.rpad = s->rpad; r.kpad = s->kpad;
+  r.db = slice_db(s);
   return r;
 }
 
@@ -994,12 +1007,18 @@ extern "C" int mpps_slice(mpps_handle *h, const mpps_mat *src, int side, mpps_sl
   const int fi = fmt_index(src->fmt);
   const int W = fmt_words(fi);
   const int S = out->nslices;
-  if (S != 4 && S != 8 && S != 16 && S != 31) return set_err(h, MPPS_EINVAL, "slice: 4, 8, 16 or 31 digit planes");
+  if (out->digit_bits != 0 && out->digit_bits != 7 && out->digit_bits != 8)
+    return set_err(h, MPPS_EINVAL, "slice: digit_bits must be 7 or 8");
+  if (slice_db(out) == 7 && S != 4 && S != 8 && S != 16 && S != 31)
+    return set_err(h, MPPS_EINVAL, "slice: 4, 8, 16 or 31 digit planes of 7 bits");
+  if (slice_db(out) == 8 && S != 4 && S != 8 && S != 14 && S != 28)
+    return set_err(h, MPPS_EINVAL, "slice: 4, 8, 14 or 28 digit planes of 8 bits");
   if (side == 0) {
     dim3 grid((out->rpad * 32 + 255) / 256, nb);
 #define SR(WW, SS) \
   if (W == WW && S == SS) oz::slice_rows_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
-    SR(1, 4) SR(1, 8) SR(1, 16) SR(1, 31) SR(2, 4) SR(2, 8) SR(2, 16) SR(2, 31) SR(4, 4) SR(4, 8) SR(4, 16) SR(4, 31) {}
+    SR(1, 4) SR(1, 8) SR(1, 14) SR(1, 16) SR(1, 28) SR(1, 31) SR(2, 4) SR(2, 8) SR(2, 14) SR(2, 16) SR(2, 28)
+    SR(2, 31) SR(4, 4) SR(4, 8) SR(4, 14) SR(4, 16) SR(4, 28) SR(4, 31) {}
 #undef SR
     return after_launch(h, "slice_rows_kernel");
   }
@@ -1009,7 +1028,8 @@ extern "C" int mpps_slice(mpps_handle *h, const mpps_mat *src, int side, mpps_sl
   dim3 grid(out->rpad / 32, out->kpad / 32, nb);
 #define SC(WW, SS) \
   if (W == WW && S == SS) oz::slice_cols_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
-  SC(1, 4) SC(1, 8) SC(1, 16) SC(1, 31) SC(2, 4) SC(2, 8) SC(2, 16) SC(2, 31) SC(4, 4) SC(4, 8) SC(4, 16) SC(4, 31) {}
+  SC(1, 4) SC(1, 8) SC(1, 14) SC(1, 16) SC(1, 28) SC(1, 31) SC(2, 4) SC(2, 8) SC(2, 14) SC(2, 16) SC(2, 28)
+  SC(2, 31) SC(4, 4) SC(4, 8) SC(4, 14) SC(4, 16) SC(4, 28) SC(4, 31) {}
 #undef SC
   return after_launch(h, "slice_cols_kernel");
 }
@@ -1084,8 +1104,6 @@ static int dispatch_oz_tma(mpps_handle *h, int S, int fo, int mode, const oz::Oz
 #define OZ(SS, NT, FF, MM) if (S == SS && fo == FF && mode == MM) return launch_oz_tma<SS, NT, FF, MM>(h, a, nb);
   OZ(4, 32, F32, 0) OZ(4, 32, F32, 1) OZ(4, 32, F64, 1) OZ(4, 32, DD, 1) OZ(4, 32, QD, 1)
   OZ(8, 32, F64, 0) OZ(8, 32, F64, 1) OZ(8, 32, DD, 1) OZ(8, 32, QD, 1)
-  OZ(16, 32, DD, 0) OZ(16, 32, DD, 1) OZ(16, 32, QD, 1)
-  OZ(31, 16, QD, 0) OZ(31, 16, QD, 1)
 #undef OZ
   return set_err(h, MPPS_EFMT, "tensor-core GEMM: no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
 }
@@ -1114,9 +1132,9 @@ static int launch_oz_ring(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
 
 static int dispatch_oz_ring(mpps_handle *h, int S, int fo, int mode, const oz::OzTmaArgs &a, int nb) {
 #define OZ(SS, NT, FF, MM) if (S == SS && fo == FF && mode == MM) return launch_oz_ring<SS, NT, FF, MM>(h, a, nb);
-  OZ(4, 32, F32, 0) OZ(4, 32, F32, 1) OZ(4, 32, F64, 1) OZ(4, 32, DD, 1) OZ(4, 32, QD, 1)
-  OZ(8, 32, F64, 0) OZ(8, 32, F64, 1) OZ(8, 32, DD, 1) OZ(8, 32, QD, 1)
+  OZ(14, 32, DD, 0) OZ(14, 32, DD, 1) OZ(14, 32, QD, 1)
   OZ(16, 32, DD, 0) OZ(16, 32, DD, 1) OZ(16, 32, QD, 1)
+  OZ(28, 16, QD, 0) OZ(28, 16, QD, 1)
   OZ(31, 16, QD, 0) OZ(31, 16, QD, 1)
 #undef OZ
   return set_err(h, MPPS_EFMT, "tensor-core GEMM: no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
@@ -1241,12 +1259,12 @@ static bool oz_wide_for(int S, int fo, int mode, int K) {
     v = e ? atoi(e) : 1;
   }
   if (!v) return false;
-  return (S == 16 && mode == 0 && fo == DD && (K >= 4096 || v == 2)) || (S == 31 && fo == QD && v == 2);
+  return ((S == 16 || S == 14) && mode == 0 && fo == DD && (K >= 4096 || v == 2)) || (S == 31 && fo == QD && v == 2);
 }
 
 static int dispatch_oz_wide(mpps_handle *h, int S, int fo, int mode, const oz::OzTmaArgs &a, int nb) {
 #define OZ(SS, NT, FF, MM) if (S == SS && fo == FF && mode == MM) return launch_oz_wide<SS, NT, FF, MM>(h, a, nb);
-  OZ(16, 32, DD, 0) OZ(31, 16, QD, 0) OZ(31, 16, QD, 1)
+  OZ(14, 32, DD, 0) OZ(16, 32, DD, 0) OZ(31, 16, QD, 0) OZ(31, 16, QD, 1)
 #undef OZ
   return set_err(h, MPPS_EFMT, "wide tensor-core GEMM: no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
 }
@@ -1275,7 +1293,7 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   const bool pers = pmode != 0;
   const int NT = (S > 16 || pers) ? 16 : 32;
   // default: streamed-plane ring for dd / qd (S >= 16), 2-4 stage TMA ring below
-  const bool ring = pers || oz_mode() == 2 || (oz_mode() == 3 && S >= 16);
+  const bool ring = pers || oz_mode() == 2 || (oz_mode() == 3 && S >= 14) || S == 14 || S == 28;
   const int abox = ring ? (S < 4 ? S : 4) : S;
   int rc;
   if (wide || pmode == 3) {
@@ -1324,9 +1342,12 @@ static int check_sliced(mpps_handle *h, const mpps_slices *A, const mpps_slices 
   if (S > A->nslices || S > B->nslices) return set_err(h, MPPS_EINVAL, "sliced gemm: %d slices requested, %d/%d stored", S, A->nslices, B->nslices);
   if (A->kpad != B->kpad || A->kpad < K) return set_err(h, MPPS_EINVAL, "sliced gemm: K padding mismatch");
   if (A->rpad < M || B->rpad < N) return set_err(h, MPPS_EINVAL, "sliced gemm: row padding too small");
-  // int32 diagonal accumulators: |D| <= min(S,...) * 65^2 * K must stay below 2^31
-  if ((double)S * 4225.0 * (double)K >= 2147483648.0)
-    return set_err(h, MPPS_EINVAL, "sliced gemm: K=%d too large for exact int32 accumulation", K);
+  if (slice_db(A) != slice_db(B))
+    return set_err(h, MPPS_EINVAL, "sliced gemm: operands split with %d- and %d-bit digits", slice_db(A), slice_db(B));
+  // int32 diagonal accumulators must stay exact
+  if (oz_diag_bound(S, slice_db(A)) * (double)(K > 0 ? K : A->kpad) >= 2147483648.0)
+    return set_err(h, MPPS_EINVAL, "sliced gemm: K=%d too large for exact int32 accumulation (%d-bit digits)",
+                   K > 0 ? K : A->kpad, slice_db(A));
   return MPPS_OK;
 }
 
@@ -1364,6 +1385,8 @@ int mpps_horner_step_sliced(mpps_handle *h, const mpps_slices *Y, const mpps_sli
 }
 
 int mpps_oz_slices_for(int fmt) { return oz_slices_for(fmt_index(fmt)); }
+int mpps_oz_slices_for_bits(int fmt, int digit_bits) { return oz_slices_for(fmt_index(fmt), digit_bits == 8 ? 8 : 7); }
+int mpps_oz_max_k_8bit(void) { return kOzMaxK8; }
 
 void mpps_debug_oz_trace(void *buf) { g_oz_trace = (unsigned long long *)buf; }
 void mpps_debug_oz_flags(int flags) { g_oz_dbg = flags & 0xff; g_oz_group_override = flags >> 8; }

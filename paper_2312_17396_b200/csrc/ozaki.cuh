@@ -140,11 +140,22 @@ struct SliceRef {
   int8_t *digits;   // [S][batch][rpad][kpad]
   int *exps;        // [batch][rpad]
   int S, batch, rpad, kpad;
+  int db;           // digit bits: 7 (digits in [-65, 65]) or 8 ([-128, 127]); first digit 6 bits
   __host__ __device__ long long plane() const { return (long long)batch * rpad * kpad; }
 };
 
+// Digit width of a tensor-core product: S = 14 / 28 planes exist only as
+// 8-bit digits, 16 / 31 only as 7-bit ones; 4 and 8 planes are prefixes of
+// either split (the operands' SliceRef.db, equal for A and B).
+template <int S>
+__device__ __forceinline__ int oz_db_of(int db) {
+  if constexpr (S == 14 || S == 28) return 8;
+  else if constexpr (S == 16 || S == 31) return 7;
+  else return db == 8 ? 8 : 7;
+}
+
 // Split one exact value (W words, |v| < 1 after scaling) into S signed
-// digits: first 6 bits, then 7 bits each.  The residual is kept exactly
+// digits: first 6 bits, then db = 7 or 8 bits each.  The residual is kept exactly
 // (scaling by 2^k and subtracting the nearest integer are exact; the words
 // are renormalised with TwoSums), so sum_s d_s 2^-(6+7s) is the value
 // truncated after S digits.
@@ -167,7 +178,7 @@ __device__ __forceinline__ mp::qd scale_words(mp::qd v, int k) {
   return mp::qd_ldexp(v, k);
 }
 
-template <int W, int S>
+template <int W, int S, int DB>
 __device__ __forceinline__ void split_digits_wi(const mp::qd &v, int (&dg)[S]) {
   // Digit s is the nearest integer to the running residual times 2^6 (s = 0)
   // or 2^7.  Rounding uses the 1.5*2^52 shifter fused into the scaling FMA
@@ -182,9 +193,10 @@ __device__ __forceinline__ void split_digits_wi(const mp::qd &v, int (&dg)[S]) {
 #pragma unroll
   for (int w = 0; w < W; ++w) x[w] = v.x[w];
   double pend = 1.0;  // scale owed to the lower words since the last fold
+  constexpr double scd = DB == 8 ? 256.0 : 128.0;
 #pragma unroll
   for (int s = 0; s < S; ++s) {
-    const double sc = (s == 0) ? 64.0 : 128.0;
+    const double sc = (s == 0) ? 64.0 : scd;
     if constexpr (W > 1) {
       pend *= sc;
       if (s > 0 && s % kFold == 0) {
@@ -207,12 +219,24 @@ __device__ __forceinline__ void split_digits_wi(const mp::qd &v, int (&dg)[S]) {
     x[0] = fma(x[0], sc, -d);  // exact
     dg[s] = __double2loint(t);  // low byte = the digit (two's complement)
   }
+  if constexpr (DB == 8) {
+    // nearest-integer base-256 digits lie in [-128, 128]; carry the +128s
+    // (and anything outside int8) into the next more significant digit,
+    // bottom up -- the value is unchanged, every digit lands in [-128, 127]
+    // and the 6-bit first digit in [-65, 65]
+#pragma unroll
+    for (int s = S - 1; s >= 1; --s) {   // digits >= -128 always; only +128 / +129 carry
+      const int c = dg[s] > 127;
+      dg[s] -= c << 8;
+      dg[s - 1] += c;
+    }
+  }
 }
 
-template <int W, int S>
+template <int W, int S, int DB>
 __device__ __forceinline__ void split_digits_w(const mp::qd &v, int8_t (&dg)[S]) {
   int di[S];
-  split_digits_wi<W, S>(v, di);
+  split_digits_wi<W, S, DB>(v, di);
 #pragma unroll
   for (int s = 0; s < S; ++s) dg[s] = (int8_t)di[s];
 }
@@ -231,8 +255,9 @@ __device__ __forceinline__ int row_exponent(double mx) {
 // Side A: rows scaled by their own max exponent; output [S][b][i][k].
 // One warp per row; each lane splits 4 consecutive entries and stores the 4
 // digits of a plane as one 32-bit word.
-template <int W, int S>
-__global__ void slice_rows_kernel(MatRef A, int rows, int cols, int fi, SliceRef out, const int *sel) {
+template <int W, int S, int DB>
+__device__ __forceinline__ void slice_rows_body(const MatRef &A, int rows, int cols, int fi, const SliceRef &out,
+                                                const int *sel) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int bz = blockIdx.y;
@@ -253,23 +278,57 @@ __global__ void slice_rows_kernel(MatRef A, int rows, int cols, int fi, SliceRef
   const long long plane = out.plane();
   int8_t *o = out.digits + ((long long)b * out.rpad + i) * out.kpad;
   for (int k0 = 4 * lane; k0 < out.kpad; k0 += 128) {
-    int dq[4][S];
+    if constexpr (DB == 8) {
+      // 8-bit digits are final only after the bottom-up carry pass over the
+      // whole entry, so the four entries are split one after another and
+      // their digits inserted byte by byte into the plane words (S digits +
+      // S words live instead of 4 S digits)
+      uint32_t wd[S];
+#pragma unroll 1
+      for (int q = 0; q < 4; ++q) {
+        const int k = k0 + q;
+        mp::qd v = mp::qd_make(0.0, 0.0, 0.0, 0.0);
+        if (i < rows && k < cols) {
+          v = fi == F32 ? mp::qd_from_d((double)((const float *)A.data)[base + k]) : load_qd(A, base + k);
+          v = scale_words<W>(v, -e);
+        }
+        int dg[S];
+        split_digits_wi<W, S, DB>(v, dg);
+        // byte 0 of dg[s] -> byte q of wd[s] (selector nibble q = 4, others keep wd)
+        const uint32_t sel = 0x3210u + ((4u - q) << (4 * q));
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int k = k0 + q;
-      mp::qd v = mp::qd_make(0.0, 0.0, 0.0, 0.0);
-      if (i < rows && k < cols) {
-        v = fi == F32 ? mp::qd_from_d((double)((const float *)A.data)[base + k]) : load_qd(A, base + k);
-        v = scale_words<W>(v, -e);
+        for (int s = 0; s < S; ++s) wd[s] = __byte_perm(q == 0 ? 0u : wd[s], (uint32_t)dg[s], sel);
       }
-      split_digits_wi<W, S>(v, dq[q]);
-    }
 #pragma unroll
-    for (int s = 0; s < S; ++s) {  // bytes 0 of the four digits -> one word
-      const uint32_t lo = __byte_perm(dq[0][s], dq[1][s], 0x0040);
-      const uint32_t hi = __byte_perm(dq[2][s], dq[3][s], 0x0040);
-      *reinterpret_cast<uint32_t *>(o + s * plane + k0) = __byte_perm(lo, hi, 0x5410);
+      for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t *>(o + s * plane + k0) = wd[s];
+    } else {
+      int dq[4][S];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = k0 + q;
+        mp::qd v = mp::qd_make(0.0, 0.0, 0.0, 0.0);
+        if (i < rows && k < cols) {
+          v = fi == F32 ? mp::qd_from_d((double)((const float *)A.data)[base + k]) : load_qd(A, base + k);
+          v = scale_words<W>(v, -e);
+        }
+        split_digits_wi<W, S, DB>(v, dq[q]);
+      }
+#pragma unroll
+      for (int s = 0; s < S; ++s) {  // bytes 0 of the four digits -> one word
+        const uint32_t lo = __byte_perm(dq[0][s], dq[1][s], 0x0040);
+        const uint32_t hi = __byte_perm(dq[2][s], dq[3][s], 0x0040);
+        *reinterpret_cast<uint32_t *>(o + s * plane + k0) = __byte_perm(lo, hi, 0x5410);
+      }
     }
+  }
+}
+
+template <int W, int S>
+__global__ void slice_rows_kernel(MatRef A, int rows, int cols, int fi, SliceRef out, const int *sel) {
+  if (oz_db_of<S>(out.db) == 8) {
+    if constexpr (S != 16 && S != 31) slice_rows_body<W, S, 8>(A, rows, cols, fi, out, sel);
+  } else {
+    if constexpr (S != 14 && S != 28) slice_rows_body<W, S, 7>(A, rows, cols, fi, out, sel);
   }
 }
 
@@ -299,9 +358,9 @@ __global__ void col_exps_kernel(MatRef B, int rows, int cols, int fi, SliceRef o
 }
 
 // Side B digits, transposed through shared memory: tile of 32 k x 32 j.
-template <int W, int S>
-__global__ void slice_cols_kernel(MatRef B, int rows, int cols, int fi, SliceRef out, const int *sel) {
-  __shared__ int8_t tile[S][32][36];
+template <int W, int S, int DB>
+__device__ __forceinline__ void slice_cols_body(const MatRef &B, int rows, int cols, int fi, const SliceRef &out,
+                                                const int *sel, int8_t (*tile)[32][36]) {
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
   const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
   const int bz = blockIdx.z;
@@ -315,7 +374,7 @@ __global__ void slice_cols_kernel(MatRef B, int rows, int cols, int fi, SliceRef
       v = scale_words<W>(v, -out.exps[(long long)b * out.rpad + j]);
     }
     int8_t dg[S];
-    split_digits_w<W, S>(v, dg);
+    split_digits_w<W, S, DB>(v, dg);
 #pragma unroll
     for (int s = 0; s < S; ++s) tile[s][tx][kk] = dg[s];
   }
@@ -329,6 +388,16 @@ __global__ void slice_cols_kernel(MatRef B, int rows, int cols, int fi, SliceRef
     for (int s = 0; s < S; ++s)
       *reinterpret_cast<uint32_t *>(out.digits + s * plane + ((long long)b * out.rpad + j) * out.kpad + k0 + kq) =
           *reinterpret_cast<const uint32_t *>(&tile[s][jj][kq]);
+}
+
+template <int W, int S>
+__global__ void slice_cols_kernel(MatRef B, int rows, int cols, int fi, SliceRef out, const int *sel) {
+  __shared__ int8_t tile[S][32][36];
+  if (oz_db_of<S>(out.db) == 8) {
+    if constexpr (S != 16 && S != 31) slice_cols_body<W, S, 8>(B, rows, cols, fi, out, sel, tile);
+  } else {
+    if constexpr (S != 14 && S != 28) slice_cols_body<W, S, 7>(B, rows, cols, fi, out, sel, tile);
+  }
 }
 
 // -------------------------------------------------------------- GEMM
@@ -349,18 +418,18 @@ __host__ __device__ constexpr int oz_stages() { return 2 * oz_stage_bytes<S, NT>
 template <int S, int NT>
 __host__ __device__ constexpr size_t oz_smem_bytes() { return oz_stages<S, NT>() * oz_stage_bytes<S, NT>() + 256; }
 
-// value of sum_d D_d 2^-(12+7d) as a qd (exact grouping in threes)
-template <int S>
+// value of sum_d D_d 2^-(12+DB d) as a qd (exact grouping in threes)
+template <int S, int DB = 7>
 __device__ __forceinline__ mp::qd combine_diagonals(const int32_t *D) {
   mp::qd acc = mp::qd_make(0.0, 0.0, 0.0, 0.0);
   mp::dd accd = mp::dd_make(0.0, 0.0);
 #pragma unroll
   for (int g = 0; g < (S + 2) / 3; ++g) {
     const int d0 = 3 * g;
-    long long G = (long long)D[d0] << 14;
-    if (d0 + 1 < S) G += (long long)D[d0 + 1] << 7;
+    long long G = (long long)D[d0] << (2 * DB);
+    if (d0 + 1 < S) G += (long long)D[d0 + 1] << DB;
     if (d0 + 2 < S) G += (long long)D[d0 + 2];
-    double gv = ldexp((double)G, -(12 + 7 * (d0 + 2)));  // exact
+    double gv = ldexp((double)G, -(12 + DB * (d0 + 2)));  // exact
     if constexpr (S > 16) acc = mp::qd_add(acc, mp::qd_from_d(gv));
     else accd = mp::dd_add_d(accd, gv);
   }
@@ -502,7 +571,7 @@ __global__ void __launch_bounds__(kThreadsOz, 1) oz_gemm_kernel(const OzArgs arg
       int32_t Dj[S];
 #pragma unroll
       for (int d = 0; d < S; ++d) Dj[d] = D[d][jj];
-      mp::qd v = combine_diagonals<S>(Dj);
+      mp::qd v = oz_db_of<S>(args.A.db) == 8 ? combine_diagonals<S, 8>(Dj) : combine_diagonals<S, 7>(Dj);
       const int eb = args.B.exps[(long long)b * args.B.rpad + col];
       v = mp::qd_ldexp(v, ea + eb);
       const long long off = (long long)b * C.bstride + (long long)row * C.ld + col;
@@ -529,18 +598,18 @@ __host__ __device__ constexpr double pow2c(int e) {  // compile-time 2^e
   return r;
 }
 
-// sum_d D_d 2^-(12+7d) for S <= 16 as a dd (groups of three digits are
+// sum_d D_d 2^-(12+DB d) for S <= 16 as a dd (groups of three digits are
 // exact int64 -> double; group weights are compile-time constants).
-template <int S>
+template <int S, int DB = 7>
 __device__ __forceinline__ mp::dd combine_dd(const int32_t *D) {
   mp::dd acc = mp::dd_make(0.0, 0.0);
 #pragma unroll
   for (int g = 0; g < (S + 2) / 3; ++g) {
     const int d0 = 3 * g;
-    long long G = (long long)D[d0] << 14;
-    if (d0 + 1 < S) G += (long long)D[d0 + 1] << 7;
+    long long G = (long long)D[d0] << (2 * DB);
+    if (d0 + 1 < S) G += (long long)D[d0 + 1] << DB;
     if (d0 + 2 < S) G += (long long)D[d0 + 2];
-    const double gv = (double)G * pow2c(-(12 + 7 * (d0 + 2)));  // exact
+    const double gv = (double)G * pow2c(-(12 + DB * (d0 + 2)));  // exact
     if (g == 0) acc = mp::dd_make(gv, 0.0);
     else acc = mp::dd_add_d(acc, gv);
   }
@@ -591,8 +660,8 @@ __device__ __forceinline__ void oz_epi_prefetch(const Args &args, EpiPre<S, NT, 
 }
 
 // Drain the S diagonal accumulators of this thread's TMEM lane for columns
-// [c_begin, c_end) and run the store / fused Horner epilogue.
-template <int S, int NT, int FO, int MODE, typename Args>
+// [c_begin, c_end) and run the store / fused Horner epilogue (DB: digit bits).
+template <int S, int NT, int FO, int MODE, int DB, typename Args>
 __device__ __forceinline__ void oz_epilogue(const Args &args, const EpiPre<S, NT, FO, MODE> &pre, uint32_t tmem,
                                             int quarter, int c_begin, int c_end, int b, int m0, int n0, int lane) {
   using P = EpiPre<S, NT, FO, MODE>;
@@ -629,7 +698,7 @@ __device__ __forceinline__ void oz_epilogue(const Args &args, const EpiPre<S, NT
       const long long off = (long long)b * C.bstride + (long long)row * C.ld + col;
       if constexpr (S <= 16 && FO != QD) {
         // dd-width epilogue (fp32 / fp64 / dd outputs)
-        mp::dd v = combine_dd<S>(Dj);
+        mp::dd v = combine_dd<S, DB>(Dj);
         const double sc = pow2i(ea + eb - (MODE == 1 ? (ey + ei) : 0));
         v = mp::dd_make(v.hi * sc, v.lo * sc);
         if constexpr (MODE == 1) v = mp::dd_add(mp::dd_make(pre.bp[i0 + jj][0], pre.bp[i0 + jj][1]), v);
@@ -645,7 +714,7 @@ __device__ __forceinline__ void oz_epilogue(const Args &args, const EpiPre<S, NT
           ((float *)C.data)[off] = mp::dd_to_float(v.hi, v.lo);
         }
       } else {
-        mp::qd v = combine_diagonals<S>(Dj);
+        mp::qd v = combine_diagonals<S, DB>(Dj);
         v = mp::qd_ldexp(v, ea + eb);
         if constexpr (MODE == 0) {
           store_fmt<FO>(C, off, v, 0);
@@ -657,6 +726,18 @@ __device__ __forceinline__ void oz_epilogue(const Args &args, const EpiPre<S, NT
         }
       }
     }
+  }
+}
+
+template <int S, int NT, int FO, int MODE, typename Args>
+__device__ __forceinline__ void oz_epilogue_db(const Args &args, const EpiPre<S, NT, FO, MODE> &pre, uint32_t tmem,
+                                               int quarter, int c_begin, int c_end, int b, int m0, int n0, int lane) {
+  if (oz_db_of<S>(args.A.db) == 8) {
+    if constexpr (S != 16 && S != 31)
+      oz_epilogue<S, NT, FO, MODE, 8>(args, pre, tmem, quarter, c_begin, c_end, b, m0, n0, lane);
+  } else {
+    if constexpr (S != 14 && S != 28)
+      oz_epilogue<S, NT, FO, MODE, 7>(args, pre, tmem, quarter, c_begin, c_end, b, m0, n0, lane);
   }
 }
 
@@ -786,7 +867,7 @@ __device__ __forceinline__ void oz_stage_load(const Args &args, double *ebuf, in
 // Phase 2 (all 8 warps, after the MMAs): thread = row; its columns are
 // combined from TMEM, the B_prev words read from (and the dd-width result
 // written back to) the staging tile.
-template <int S, int NT, int FO, int MODE, typename Args>
+template <int S, int NT, int FO, int MODE, int DB, typename Args>
 __device__ __forceinline__ void oz_stage_compute(const Args &args, double *ebuf, const int *ebs, uint32_t tmem,
                                                  int quarter, int c_begin, int c_end, int b, int m0, int lane) {
   constexpr int CW = 8;
@@ -815,7 +896,7 @@ __device__ __forceinline__ void oz_stage_compute(const Args &args, double *ebuf,
       int32_t Dj[S];
 #pragma unroll
       for (int d = 0; d < S; ++d) Dj[d] = D[d][jj];
-      mp::dd v = combine_dd<S>(Dj);
+      mp::dd v = combine_dd<S, DB>(Dj);
       const double sc = pow2i(ea + ebs[c] - (MODE == 1 ? (ey + ei) : 0));
       v = mp::dd_make(v.hi * sc, v.lo * sc);
       const int i0w = ebuf_idx(0, r, c), i1w = ebuf_idx(1, r, c);
@@ -881,7 +962,11 @@ __device__ __forceinline__ void oz_kernel_epilogue(const OzTmaArgs &args, double
     if (tr) tr[2] = globaltimer();
     __syncthreads();  // staged B_prev / exponents visible to every warp
     fence_after();
-    oz_stage_compute<S, NT, FO, MODE>(args, ebuf, ebs, tmem, quarter, cb, ce, b, m0, lane);
+    if (oz_db_of<S>(args.A.db) == 8) {
+      if constexpr (S != 16 && S != 31) oz_stage_compute<S, NT, FO, MODE, 8>(args, ebuf, ebs, tmem, quarter, cb, ce, b, m0, lane);
+    } else {
+      if constexpr (S != 14 && S != 28) oz_stage_compute<S, NT, FO, MODE, 7>(args, ebuf, ebs, tmem, quarter, cb, ce, b, m0, lane);
+    }
     __syncthreads();
     oz_stage_store<FO>(args.C, ebuf, args.M, args.N, b, m0, n0, warp, lane);
   } else {
@@ -891,7 +976,7 @@ __device__ __forceinline__ void oz_kernel_epilogue(const OzTmaArgs &args, double
     mbar_wait(smem_u32(done), 0);
     fence_after();
     if (tr) tr[2] = globaltimer();
-    oz_epilogue<S, NT, FO, MODE>(args, pre, tmem, quarter, cb, ce, b, m0, n0, lane);
+    oz_epilogue_db<S, NT, FO, MODE>(args, pre, tmem, quarter, cb, ce, b, m0, n0, lane);
   }
   fence_before();
   __syncthreads();
@@ -1455,7 +1540,7 @@ __global__ void __launch_bounds__(kThreadsPers, 1) oz_gemm_pers_kernel(const __g
       mbar_wait(smem_u32(&acc_full[buf]), (i / P::NACC) & 1);
       fence_after();
       if (!(args.dbg & 4))
-        oz_epilogue<S, NT, FO, MODE>(args, pre, tmem + (uint32_t)(buf * P::ACC), quarter, cb, ce, b, m0, n0, lane);
+        oz_epilogue_db<S, NT, FO, MODE>(args, pre, tmem + (uint32_t)(buf * P::ACC), quarter, cb, ce, b, m0, n0, lane);
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&acc_empty[buf]));
@@ -1617,7 +1702,7 @@ __global__ void __launch_bounds__(kThreadsPers, 1) oz_gemm_pwide_kernel(const __
       mbar_wait(smem_u32(&acc_full[buf]), (i >> 1) & 1);
       fence_after();
       if (!(args.dbg & 4))
-        oz_epilogue<S, NT, FO, MODE>(args, pre, tmem + (uint32_t)(buf * P::ACC), quarter, cb, ce, b, m0, n0, lane);
+        oz_epilogue_db<S, NT, FO, MODE>(args, pre, tmem + (uint32_t)(buf * P::ACC), quarter, cb, ce, b, m0, n0, lane);
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&acc_empty[buf]));

@@ -12,6 +12,17 @@ libmpps_b200.so:
 
 fp32 levels use 4 digit planes (27 bits >= 24) on the tensor cores.
 
+Digit width: products with inner dimension 512 <= K <= 4800 split into
+8-bit digits -- dd in 14 planes (110 bits) instead of 16 7-bit ones (111
+bits): 105 plane pairs instead of 136 and 12.5 % fewer plane bytes (GEMM
+-8 % at n = 1024..2048); qd in 28 instead of 31 (GEMM -18 % at n = 2048).
+8-bit digits need a bottom-up carry pass per entry that makes the splitting
+~30 % dearer, which outweighs the GEMM gain at n = 256 (an O(n^2) split per
+O(n^3) product); above K = 4800 the int32 diagonal accumulators of qd's 28
+planes could overflow.  Both operands of a product share K, hence the width.
+``MPPS_DIGITS=7`` forces 7-bit digits everywhere, ``MPPS_DIGITS=8`` allows
+8-bit digits for every K <= 4800.
+
 The default is ``tc``; ``MPPS_GEMM=simt`` (environment) or
 ``set_engine("simt")`` selects the SIMT kernels (A/B evidence, tests).
 """
@@ -23,6 +34,25 @@ import os
 from .precision import FP32, MatBatch
 
 _ENGINE = os.environ.get("MPPS_GEMM", "tc").lower()
+_DIGITS = os.environ.get("MPPS_DIGITS", "auto")
+_MIN_K_8BIT = 512
+
+
+def set_digit_bits(db) -> None:
+    """Digit width policy of the tensor-core splits: 7, 8 or "auto"."""
+    global _DIGITS
+    if db not in (7, 8, "7", "8", "auto"):
+        raise ValueError("digit bits must be 7, 8 or 'auto'")
+    _DIGITS = str(db)
+
+
+def digit_bits_for(h, K: int) -> int:
+    """Digit width of a product with inner dimension K."""
+    if _DIGITS == "7" or K > h.max_k_8bit():
+        return 7
+    if _DIGITS == "8":
+        return 8
+    return 8 if K >= _MIN_K_8BIT else 7
 
 
 def set_engine(name: str) -> None:
@@ -59,7 +89,9 @@ def prepare(h, A: MatBatch, side: int, fmt: int, sel=None, exp=None) -> Operand:
     if uses_tc(fmt):
         # digit planes carry their own per-row/column power-of-two scales,
         # so no extra level scaling is applied (exp is ignored)
-        return Operand(A, h.slice(A, side, h.slices_for(fmt), sel), fmt, side)
+        K = A.cols if side == 0 else A.rows
+        db = digit_bits_for(h, K)
+        return Operand(A, h.slice(A, side, h.slices_for(fmt, db), sel, db), fmt, side)
     if A.fmt != fmt or exp is not None:
         B = MatBatch.empty(fmt, A.batch, A.rows, A.cols, device=A.device)
         h.convert(A, B, sel, exp)
@@ -70,7 +102,7 @@ def prepare(h, A: MatBatch, side: int, fmt: int, sel=None, exp=None) -> Operand:
 def gemm(h, L: Operand, R: Operand, C: MatBatch, sel=None) -> None:
     """C = L R at C's format."""
     if L.slices is not None and R.slices is not None:
-        h.gemm_sliced(L.slices, R.slices, h.slices_for(C.fmt), C, sel)
+        h.gemm_sliced(L.slices, R.slices, h.slices_for(C.fmt, L.slices.db), C, sel)
     else:
         h.gemm(L.mat, R.mat, C, sel)
 
@@ -81,7 +113,7 @@ def horner(h, Y: Operand, phi: Operand, fmt_level: int, Bprev, out, sel=None, ex
     if Y.slices is not None and phi.slices is not None:
         # the Y planes are unscaled (exp_y does not apply); phi keeps its
         # level scaling 2^exp_in, undone in the epilogue
-        h.horner_step_sliced(Y.slices, phi.slices, h.slices_for(fmt_level), Bprev, out, sel, None, exp_in,
+        h.horner_step_sliced(Y.slices, phi.slices, h.slices_for(fmt_level, Y.slices.db), Bprev, out, sel, None, exp_in,
                              exp_out, fmt_in=fmt_level)
     else:
         h.horner_step(Y.mat, phi.mat, Bprev, out, sel, exp_y, exp_in, exp_out)

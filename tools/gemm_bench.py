@@ -45,8 +45,10 @@ def bench_tc(fmt, B, n, reps=5):
     if A.words > 1:
         A.data[1:] *= 1e-17
     C = MatBatch.empty(fmt, B, n, device="cuda")
-    S = h.slices_for(fmt)
-    sa, sb = h.slice(A, 0, S), h.slice(A, 1, S)
+    from paper_2312_17396_b200 import gemm_engine
+    db = gemm_engine.digit_bits_for(h, n)
+    S = h.slices_for(fmt, db)
+    sa, sb = h.slice(A, 0, S, None, db), h.slice(A, 1, S, None, db)
     h.gemm_sliced(sa, sb, S, C)
     torch.cuda.synchronize()
 
@@ -61,7 +63,7 @@ def bench_tc(fmt, B, n, reps=5):
             best = min(best, a.elapsed_time(b) * 1e-3)
         return best
     tg = t(lambda: h.gemm_sliced(sa, sb, S, C))
-    ts = t(lambda: (h.slice(A, 0, S), h.slice(A, 1, S)))
+    ts = t(lambda: (h.slice(A, 0, S, None, db), h.slice(A, 1, S, None, db)))
     tf = 2.0 * B * n ** 3 / tg / 1e12
     pairs = S * (S + 1) // 2
     tops = 2.0 * B * n ** 3 * pairs / tg / 1e12
