@@ -542,8 +542,13 @@ def run_ours(args, rank, world, local_rank):
         # 4/8/14/28 (8-bit) for fp32/fp64/dd/qd, recorded per launch
         S = S_used or {7: 4, 15: 8, 31: 16, 63: 31}[fin]
         achieved = logical * S * (S + 1) / 2
+        S7 = {7: 4, 15: 8, 31: 16, 63: 31}[fin]
         roof = {"bound": "tensor (int8)", "achieved": achieved, "peak": peaks["int8_tops"],
                 "unit": "TOPS (int8)", "frac": achieved / peaks["int8_tops"],
+                "frac_7bit_equivalent": logical * S7 * (S7 + 1) / 2 / peaks["int8_tops"],
+                "frac_note": "frac counts the S(S+1)/2 plane-pair products per output this launch executed; "
+                             "8-bit digits need fewer (dd 105 vs 136) for the same product, so "
+                             "frac_7bit_equivalent rates the same logical throughput in 7-bit plane pairs",
                 "logical_tflops": logical, "logical_frac_of_format_peak": logical / peaks[fname],
                 "peak_source": f"tcgen05 kind::i8 probe in bench.py on this GPU ({peaks['int8_tops']:.0f} TOPS); "
                                f"format peaks from DFMA/FFMA probes (fp64 {peaks['fp64']:.2f} TF/s, "

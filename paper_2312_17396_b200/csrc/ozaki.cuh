@@ -252,6 +252,55 @@ __device__ __forceinline__ int row_exponent(double mx) {
   return e;
 }
 
+// 8-bit digits by exact fixed-point arithmetic (W <= 2 words, S <= 14):
+// V = round(v 2^(F - e)), F = 6 + 8 (S-1) <= 110 fractional bits, formed
+// with 16 guard bits in an int128 (words shifted into place by their
+// exponents; bits below the guard bits are dropped, so V is the nearest
+// integer up to a 2^-16 ulp tie window).  The balanced base-256 digits are
+// then carry-free: the bytes of Y = V + 0x80..80 (S-1 bytes) are d_s + 128,
+// i.e. d_s = byte ^ 0x80 read as int8 for s >= 1, and the top digit d_0 is
+// the (signed) byte S-1 of Y.  No FP64 work and no carry pass.
+template <int S>
+__host__ __device__ constexpr unsigned long long fixed_cmask_lo() {
+  unsigned long long c = 0;
+  for (int k = 0; k < S - 1 && k < 8; ++k) c |= 0x80ull << (8 * k);
+  return c;
+}
+template <int S>
+__host__ __device__ constexpr unsigned long long fixed_cmask_hi() {
+  unsigned long long c = 0;
+  for (int k = 8; k < S - 1; ++k) c |= 0x80ull << (8 * (k - 8));
+  return c;
+}
+
+template <int W, int S>
+__device__ __forceinline__ unsigned __int128 fixed_biased(const mp::qd &v, int e) {
+  constexpr int F = 6 + 8 * (S - 1);
+  constexpr int G = 16;
+  static_assert(W <= 2 && F + G <= 126, "fixed-point split: at most 2 words and 14 planes");
+  __int128 acc = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const long long bits = __double_as_longlong(v.x[w]);
+    const int ex = (int)((bits >> 52) & 0x7ff);
+    const long long mant = bits & 0xfffffffffffffLL;
+    const long long m = ex ? (mant | 0x10000000000000LL) : mant;   // subnormals: no implicit bit
+    const int sh = (ex ? ex : 1) - 1075 + F + G - e;                // |v| < 2^e  =>  sh < F + G - 52
+    __int128 t = 0;
+    if (sh >= 0) t = (__int128)m << sh;
+    else if (sh > -64) t = (__int128)(m >> (-sh));
+    acc += bits < 0 ? -t : t;
+  }
+  const __int128 V = (acc + ((__int128)1 << (G - 1))) >> G;
+  const unsigned __int128 C = ((unsigned __int128)fixed_cmask_hi<S>() << 64) | fixed_cmask_lo<S>();
+  return (unsigned __int128)V + C;
+}
+
+// byte k of the 128-bit Y as the low byte of an int
+__device__ __forceinline__ uint32_t fixed_word(const unsigned __int128 &Y, int j) {
+  return (uint32_t)(Y >> (32 * j));
+}
+
 // Side A: rows scaled by their own max exponent; output [S][b][i][k].
 // One warp per row; each lane splits 4 consecutive entries and stores the 4
 // digits of a plane as one 32-bit word.
@@ -278,7 +327,28 @@ __device__ __forceinline__ void slice_rows_body(const MatRef &A, int rows, int c
   const long long plane = out.plane();
   int8_t *o = out.digits + ((long long)b * out.rpad + i) * out.kpad;
   for (int k0 = 4 * lane; k0 < out.kpad; k0 += 128) {
-    if constexpr (DB == 8) {
+    if constexpr (DB == 8 && W <= 2 && S <= 14) {
+      // 8-bit digits from the exact fixed-point value (carry-free bytes)
+      unsigned __int128 Y[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = k0 + q;
+        mp::qd v = mp::qd_make(0.0, 0.0, 0.0, 0.0);
+        if (i < rows && k < cols)
+          v = fi == F32 ? mp::qd_from_d((double)((const float *)A.data)[base + k]) : load_qd(A, base + k);
+        Y[q] = fixed_biased<W, S>(v, e);
+      }
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int kb = S - 1 - s;                       // byte of Y holding digit s
+        const int j = kb >> 2, bsel = kb & 3;
+        const uint32_t lo = __byte_perm(fixed_word(Y[0], j), fixed_word(Y[1], j), bsel | ((bsel + 4) << 4));
+        const uint32_t hi = __byte_perm(fixed_word(Y[2], j), fixed_word(Y[3], j), bsel | ((bsel + 4) << 4));
+        uint32_t wv = __byte_perm(lo, hi, 0x5410);
+        if (s > 0) wv ^= 0x80808080u;
+        *reinterpret_cast<uint32_t *>(o + s * plane + k0) = wv;
+      }
+    } else if constexpr (DB == 8) {
       // 8-bit digits are final only after the bottom-up carry pass over the
       // whole entry, so the four entries are split one after another and
       // their digits inserted byte by byte into the plane words (S digits +
@@ -368,13 +438,29 @@ __device__ __forceinline__ void slice_cols_body(const MatRef &B, int rows, int c
   for (int kk = ty; kk < 32; kk += 8) {
     const int k = k0 + kk, j = j0 + tx;
     mp::qd v = mp::qd_make(0.0, 0.0, 0.0, 0.0);
+    constexpr bool FIXED = DB == 8 && W <= 2 && S <= 14;
+    int ecol = 0;
     if (k < rows && j < cols) {
       const long long off = (long long)b * B.bstride + (long long)k * B.ld + j;
       v = fi == F32 ? mp::qd_from_d((double)((const float *)B.data)[off]) : load_qd(B, off);
-      v = scale_words<W>(v, -out.exps[(long long)b * out.rpad + j]);
+      ecol = out.exps[(long long)b * out.rpad + j];
+      if constexpr (!FIXED) v = scale_words<W>(v, -ecol);
     }
+    const mp::qd vraw = v;
     int8_t dg[S];
-    split_digits_w<W, S, DB>(v, dg);
+    if constexpr (FIXED) {
+      // fixed-point path on the unscaled words (the column exponent enters
+      // the shift)
+      const unsigned __int128 Y = fixed_biased<W, S>(vraw, ecol);
+#pragma unroll
+      for (int s2 = 0; s2 < S; ++s2) {
+        const int kb = S - 1 - s2;
+        const int byte = (int)((Y >> (8 * kb)) & 0xff);
+        dg[s2] = (int8_t)(s2 > 0 ? (byte ^ 0x80) : byte);
+      }
+    } else {
+      split_digits_w<W, S, DB>(v, dg);
+    }
 #pragma unroll
     for (int s = 0; s < S; ++s) tile[s][tx][kk] = dg[s];
   }

@@ -12,16 +12,16 @@ libmpps_b200.so:
 
 fp32 levels use 4 digit planes (27 bits >= 24) on the tensor cores.
 
-Digit width: products with inner dimension 512 <= K <= 4800 split into
-8-bit digits -- dd in 14 planes (110 bits) instead of 16 7-bit ones (111
-bits): 105 plane pairs instead of 136 and 12.5 % fewer plane bytes (GEMM
--8 % at n = 1024..2048); qd in 28 instead of 31 (GEMM -18 % at n = 2048).
-8-bit digits need a bottom-up carry pass per entry that makes the splitting
-~30 % dearer, which outweighs the GEMM gain at n = 256 (an O(n^2) split per
-O(n^3) product); above K = 4800 the int32 diagonal accumulators of qd's 28
-planes could overflow.  Both operands of a product share K, hence the width.
-``MPPS_DIGITS=7`` forces 7-bit digits everywhere, ``MPPS_DIGITS=8`` allows
-8-bit digits for every K <= 4800.
+Digit width: products with inner dimension K <= 4800 split into 8-bit
+digits -- dd in 14 planes (110 bits) instead of 16 7-bit ones (111 bits):
+105 plane pairs instead of 136 and 12.5 % fewer plane bytes (GEMM -7..-9 %
+at n = 256..2048); qd in 28 instead of 31 (GEMM -18 % at n = 2048).  fp32 /
+fp64 / dd operands are split into 8-bit digits by exact fixed-point integer
+arithmetic (carry-free bytes, as cheap as the 7-bit FP64 split); qd keeps a
+floating-point split with a bottom-up carry pass.  Above K = 4800 the int32
+diagonal accumulators of qd's 28 planes could overflow, so larger K keeps
+7-bit digits.  Both operands of a product share K, hence the width.
+``MPPS_DIGITS=7`` forces 7-bit digits everywhere.
 
 The default is ``tc``; ``MPPS_GEMM=simt`` (environment) or
 ``set_engine("simt")`` selects the SIMT kernels (A/B evidence, tests).
@@ -35,7 +35,7 @@ from .precision import FP32, MatBatch
 
 _ENGINE = os.environ.get("MPPS_GEMM", "tc").lower()
 _DIGITS = os.environ.get("MPPS_DIGITS", "auto")
-_MIN_K_8BIT = 512
+_MIN_K_8BIT = 0
 
 
 def set_digit_bits(db) -> None:

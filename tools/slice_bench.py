@@ -6,15 +6,18 @@ from paper_2312_17396_b200 import _lib
 from paper_2312_17396_b200.precision import MatBatch
 
 h = _lib.handle_for()
-for B, n in ((64, 256), (16, 1024)):
-    A = MatBatch.empty(31, B, n, device="cuda"); A.data.normal_(); A.data[1:] *= 1e-17
+for fmt, S, db in ((31, 16, 7), (31, 14, 8), (15, 8, 7), (15, 8, 8), (7, 4, 7), (7, 4, 8)):
+  for B, n in ((64, 256), (16, 1024)):
+    A = MatBatch.empty(fmt, B, n, device="cuda"); A.data.normal_()
+    if A.words > 1:
+        A.data[1:] *= 1e-17
     res = []
     for side in (0, 1):
-        h.slice(A, side, 16); torch.cuda.synchronize()
+        h.slice(A, side, S, None, db); torch.cuda.synchronize()
         best = 1e9
         for _ in range(10):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(); h.slice(A, side, 16); b.record(); b.synchronize()
+            a.record(); h.slice(A, side, S, None, db); b.record(); b.synchronize()
             best = min(best, a.elapsed_time(b))
         res.append(best * 1e3)
-    print(f"{os.path.basename(_lib.LIB_PATH)} B={B} n={n}: rows {res[0]:.1f} us, cols {res[1]:.1f} us", flush=True)
+    print(f"fmt={fmt} S={S} db={db} B={B} n={n}: rows {res[0]:.1f} us, cols {res[1]:.1f} us", flush=True)
