@@ -94,6 +94,17 @@ int mpps_axpy(mpps_handle *h, const double *alpha_words, const mpps_mat *A,
  * with X^2..X^s, powers[k] = RN(powers[k-1] * X). */
 int mpps_powers(mpps_handle *h, mpps_mat *powers, int s);
 
+/* The same with the coefficient words on the HOST ((m+1) x 4 doubles),
+ * passed in the kernel's parameter space (compile-time coefficient
+ * offsets, no shared-memory coefficient traffic).  flags bit 0: when
+ * m mod s == 0, B_r = b_m I is not stored (blocks[r] may be unallocated;
+ * the K3 Horner step mpps_horner_scalar_top uses b_m directly) -- its norm
+ * is still written.  Supported shapes: mpps_assemble_hc_supported(fmt, s, m)
+ * (others: MPPS_EFMT, use mpps_assemble_blocks). */
+int mpps_assemble_blocks_hc(mpps_handle *h, const mpps_mat *powers, int s, int m,
+                            const double *coeff_host, mpps_mat *blocks, double *norms, int flags);
+int mpps_assemble_hc_supported(int fmt, int s, int m);
+
 /* assemble_block for i = 0..r plus one_norm of every block and of Y
  * (engine.py:127-138, 141-154; precision.py:235-249), fused into one pass
  * over the powers:  B_i = b_{si} I + sum_{j=1..hi_i} b_{si+j} X^j,

@@ -481,6 +481,87 @@ __global__ void norm_reduce_strided_kernel(const double *partial, double *out, i
   if (threadIdx.x == 0) out[(long long)b * stride] = red[0];
 }
 
+// Block assembly with the coefficients in the kernel's parameter space
+// (constant bank): every coefficient index s k + j is a compile-time
+// constant, so the FMAs take their coefficient operands straight from the
+// constant bank (no shared-memory loads, no coefficient registers).  One
+// row at a time with the next row's powers prefetched into registers, so
+// each thread keeps two rows of loads in flight at ~64 registers and the SM
+// runs 32+ warps.  `skip_top`: B_r = b_m I (m mod s == 0) is not stored --
+// the K3 Horner step uses b_m directly -- but its norm |b_m| is still
+// reported.  NP = s - 1 powers enter the blocks, NB = r + 1 blocks.
+template <int WF>
+__device__ __forceinline__ typename WV<WF>::T asmc_coef(const double (&c)[2]) {
+  if constexpr (WF == DD) return mp::dd_make(c[0], c[1]);
+  else return c[0];
+}
+
+template <int NB, int NP>
+struct AssembleCArgs {
+  MatRef P[NP + 1];        // X^1..X^s (X^s only for its norm)
+  MatRef Bk[NB];
+  double coef[NB * (NP + 1)][2];   // dd words of b_0..b_{NB (NP+1) - 1} (zero past m)
+  double *partial;         // [batch][nchunk][NB+1][cols]
+  int rows, cols, m, nchunk, skip_top;
+};
+
+template <int WF, int NB, int NP>
+#ifndef MPPS_ASMC_MINB
+#define MPPS_ASMC_MINB 8
+#endif
+__global__ void __launch_bounds__(128, MPPS_ASMC_MINB) assemble_c_kernel(const __grid_constant__ AssembleCArgs<NB, NP> a) {
+  using V = WV<WF>;
+  using T = typename V::T;
+  using Acc = typename V::Acc;
+  constexpr int S = NP + 1;
+  const int n = a.cols;
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  const int chunk = blockIdx.y, b = blockIdx.z;
+  if (col >= n) return;
+  const int full = a.m / S;
+  double cs[NB + 1];
+#pragma unroll
+  for (int k = 0; k <= NB; ++k) cs[k] = 0.0;
+  const int row0 = chunk * kAsmRows;
+  const int row1 = min(a.rows, row0 + kAsmRows);
+  T xc[NP], xn[NP];
+  double yc = 0.0, yn = 0.0;
+#define MPPS_ASMC_LOAD(ROW, X, Y_)                                                        \
+  {                                                                                       \
+    _Pragma("unroll") for (int j = 0; j < NP; ++j) {                                      \
+      X[j] = V::load(a.P[j], (long long)b * a.P[j].bstride + (long long)(ROW) * a.P[j].ld + col); \
+    }                                                                                     \
+    Y_ = ((const double *)a.P[NP].data)[(long long)b * a.P[NP].bstride + (long long)(ROW) * a.P[NP].ld + col]; \
+  }
+  if (row0 < row1) MPPS_ASMC_LOAD(row0, xc, yc)
+  for (int row = row0; row < row1; ++row) {
+    if (row + 1 < row1) MPPS_ASMC_LOAD(row + 1, xn, yn)
+    const bool diag = row == col;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      const int hi = (k < full) ? S - 1 : a.m - S * full;   // last power index of block k
+      Acc acc = V::acc_of(diag ? asmc_coef<WF>(a.coef[S * k]) : V::zero());
+#pragma unroll
+      for (int j = 1; j <= NP; ++j)
+        if (j <= hi) acc = V::acc_mac(asmc_coef<WF>(a.coef[S * k + j]), xc[j - 1], acc);
+      const T v = V::acc_final(acc);
+      cs[k] += fabs(V::hi(v));
+      if (!(a.skip_top && k == NB - 1)) {
+        const MatRef &B = a.Bk[k];
+        V::store(B, (long long)b * B.bstride + (long long)row * B.ld + col, v);
+      }
+    }
+    cs[NB] += fabs(yc);
+#pragma unroll
+    for (int j = 0; j < NP; ++j) xc[j] = xn[j];
+    yc = yn;
+  }
+#undef MPPS_ASMC_LOAD
+  double *out = a.partial + ((long long)b * a.nchunk + chunk) * (long long)(NB + 1) * n;
+#pragma unroll
+  for (int k = 0; k <= NB; ++k) out[(long long)k * n + col] = cs[k];
+}
+
 // colsums[b][k][col] = sum_chunk partial[b][chunk][k][col] (fixed order)
 __global__ void colsum_reduce_kernel(const double *partial, double *colsums, int nblk, int nchunk, int cols,
                                      int batch) {
@@ -620,6 +701,32 @@ int ew_grid(long long total) {
 }  // namespace
 
 // ===================================================================== ABI
+template <int WF, int NB, int NP>
+static int launch_assemble_c(mpps_handle *h, const mpps_mat *powers, int m, const double *coeff_host,
+                             mpps_mat *blocks, double *norms, int skip_top) {
+  AssembleCArgs<NB, NP> a;
+  memset(&a, 0, sizeof(a));
+  const int rows = powers[0].rows, cols = powers[0].cols, batch = powers[0].batch;
+  for (int k = 0; k <= NP; ++k) a.P[k] = ref_of(&powers[k]);
+  for (int k = 0; k < NB; ++k) a.Bk[k] = (skip_top && k == NB - 1) ? ref_of(&powers[0]) : ref_of(&blocks[k]);
+  for (int i = 0; i < NB * (NP + 1); ++i) {
+    a.coef[i][0] = i <= m ? coeff_host[4 * i] : 0.0;
+    a.coef[i][1] = i <= m ? coeff_host[4 * i + 1] : 0.0;
+  }
+  a.rows = rows; a.cols = cols; a.m = m; a.skip_top = skip_top;
+  a.nchunk = (rows + kAsmRows - 1) / kAsmRows;
+  size_t pbytes = sizeof(double) * (size_t)batch * a.nchunk * (NB + 1) * cols;
+  cudaError_t e = cudaMallocAsync((void **)&a.partial, pbytes, h->stream);
+  if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "assemble scratch: %s", cudaGetErrorString(e));
+  assemble_c_kernel<WF, NB, NP><<<dim3((cols + 127) / 128, a.nchunk, batch), 128, 0, h->stream>>>(a);
+  int rc = after_launch(h, "assemble_c_kernel");
+  if (rc) return rc;
+  norm_reduce_kernel<<<dim3(NB + 1, batch), 256, 0, h->stream>>>(a.partial, norms, NB + 1, a.nchunk, cols);
+  rc = after_launch(h, "norm_reduce_kernel");
+  cudaFreeAsync(a.partial, h->stream);
+  return rc;
+}
+
 extern "C" {
 
 int mpps_version(void) { return 100; }
@@ -798,6 +905,47 @@ static int assemble_common(mpps_handle *h, const mpps_mat *powers, int s, int m,
   }
   cudaFreeAsync(a.partial, h->stream);
   return rc;
+}
+
+int mpps_assemble_blocks_hc(mpps_handle *h, const mpps_mat *powers, int s, int m, const double *coeff_host,
+                            mpps_mat *blocks, double *norms, int flags) {
+  if (!powers || !blocks || !coeff_host || !norms) return set_err(h, MPPS_EINVAL, "assemble: null argument");
+  if (s < 1 || s > kMaxPowers || m < s) return set_err(h, MPPS_EINVAL, "need 1 <= s <= series degree (s=%d m=%d)", s, m);
+  if (powers[0].rows != powers[0].cols)
+    return set_err(h, MPPS_EINVAL, "assemble: square matrices expected (use mpps_assemble_blocks_dist)");
+  const int r = m / s;
+  const int skip_top = (flags & 1) && (m % s == 0);
+  const int wf = fmt_index(powers[0].fmt);
+  for (int k = 0; k < s; ++k) {
+    int rc = check_mat(h, &powers[k], "assemble.power");
+    if (rc) return rc;
+    if (powers[k].fmt != powers[0].fmt || powers[k].rows != powers[0].rows || powers[k].cols != powers[0].cols ||
+        powers[k].batch != powers[0].batch)
+      return set_err(h, MPPS_EINVAL, "assemble: powers must share format and shape");
+  }
+  for (int k = 0; k <= r; ++k) {
+    if (skip_top && k == r) continue;
+    int rc = check_mat(h, &blocks[k], "assemble.block");
+    if (rc) return rc;
+    if (blocks[k].fmt != powers[0].fmt || blocks[k].rows != powers[0].rows || blocks[k].cols != powers[0].cols ||
+        blocks[k].batch != powers[0].batch)
+      return set_err(h, MPPS_EINVAL, "assemble: blocks must match the powers");
+  }
+  if (powers[0].rows == 0 || powers[0].batch == 0) return MPPS_OK;
+#define AC(WW, NB_, NP_) \
+  if (wf == WW && r + 1 == NB_ && s - 1 == NP_) return launch_assemble_c<WW, NB_, NP_>(h, powers, m, coeff_host, blocks, norms, skip_top);
+  AC(DD, 6, 5) AC(DD, 7, 6) AC(DD, 5, 4) AC(DD, 4, 3) AC(DD, 5, 3) AC(F64, 5, 3) AC(F64, 4, 3)
+#undef AC
+  return set_err(h, MPPS_EFMT, "assemble_hc: no constant-coefficient kernel for r+1=%d, s=%d at format %d", r + 1, s,
+                 powers[0].fmt);
+}
+
+int mpps_assemble_hc_supported(int fmt, int s, int m) {
+  const int wf = fmt_index(fmt), r = m / s, nb = r + 1, np = s - 1;
+  if (wf == DD) return (nb == 6 && np == 5) || (nb == 7 && np == 6) || (nb == 5 && np == 4) || (nb == 4 && np == 3) ||
+                       (nb == 5 && np == 3);
+  if (wf == F64) return (nb == 5 && np == 3) || (nb == 4 && np == 3);
+  return 0;
 }
 
 int mpps_assemble_blocks(mpps_handle *h, const mpps_mat *powers, int s, int m, const double *coeff,

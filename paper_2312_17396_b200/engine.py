@@ -313,14 +313,23 @@ def _assemble(h, powers: List[MatBatch], series: CoefficientSeries, ctx: Precisi
             _COEFF_DEV.clear()
         _COEFF_DEV[key] = coeffs
     timer.start("coefficient_assembly")
-    blocks = [MatBatch.empty(wf, B, n, device=dev) for _ in range(r + 1)]
     norms = torch.empty((B, r + 2), dtype=torch.float64, device=dev)
-    h.assemble_blocks(powers, m, coeffs, blocks, norms)
+    hc = h.assemble_hc_supported(wf, s, m)
+    # B_r = b_m I when m mod s == 0: the K3 Horner step uses b_m itself, so
+    # the constant-coefficient kernel does not store it (norm still reported)
+    skip_top = hc and m % s == 0
+    blocks = [MatBatch.empty(wf, B, n, device=dev) if not (skip_top and k == r) else MatBatch.empty(wf, 1, 1, device=dev)
+              for k in range(r + 1)]
+    if hc:
+        h.assemble_blocks_hc(powers, m, cw, blocks, norms, skip_top)
+    else:
+        h.assemble_blocks(powers, m, coeffs, blocks, norms)
     nc = complexmat.scope()
     if nc is not None:
         # complex inputs run on their real embeddings; the planner needs the
-        # complex one_norm (sum of |z|), not the embedding's abs-sums
-        for k in range(r + 1):
+        # complex one_norm (sum of |z|), not the embedding's abs-sums (the
+        # unstored B_r = b_m I has the same norm either way)
+        for k in range(r + 1 - (1 if skip_top else 0)):
             h.one_norm_complex(blocks[k], nc, norms[:, k], r + 2)
         h.one_norm_complex(powers[s - 1], nc, norms[:, r + 1], r + 2)
     timer.stop()
