@@ -1442,7 +1442,7 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   const int NT = (S > 16 || pers) ? 16 : 32;
   // default: streamed-plane ring for dd / qd (S >= 16), 2-4 stage TMA ring below
   const bool ring = pers || oz_mode() == 2 || (oz_mode() == 3 && S >= 14) || S == 14 || S == 28;
-  const int abox = ring ? (S < 4 ? S : 4) : S;
+  const int abox = ring ? (S < 4 ? S : (S == 14 ? 7 : 4)) : S;   // OzRing<S, NT>::SG
   int rc;
   if (wide || pmode == 3) {
     if ((rc = make_slice_map(h, &t.mapA, A, oz::kTileM, 1, 128)) || (rc = make_slice_map(h, &t.mapB, B, NT, S, 128)))

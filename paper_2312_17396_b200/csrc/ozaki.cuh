@@ -1199,7 +1199,9 @@ __device__ __forceinline__ void oz_ring_groups(uint32_t tmem, uint64_t bd0, uint
 // is not bound by the bytes in flight.
 template <int S, int NT, uint32_t EBUF = 0>
 struct OzRing {
-  static constexpr int SG = S < 4 ? S : 4;                       // planes per A stage
+  // planes per A stage: groups of 4 (16 KB); 14 planes (8-bit dd) in two
+  // groups of 7 so that no stage carries out-of-range planes
+  static constexpr int SG = S < 4 ? S : (S == 14 ? 7 : 4);
   static constexpr int NG = (S + SG - 1) / SG;                   // A stages per K step
   static constexpr uint32_t A_BYTES = SG * kTileM * kKStep;      // 16 KB
   static constexpr uint32_t B_BYTES = S * NT * kKStep;

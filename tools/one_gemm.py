@@ -14,8 +14,10 @@ A.data.normal_()
 if A.words > 1:
     A.data[1:] *= 1e-17
 C = MatBatch.empty(fmt, B, n, device="cuda")
-S = h.slices_for(fmt)
-sa, sb = h.slice(A, 0, S), h.slice(A, 1, S)
+from paper_2312_17396_b200 import gemm_engine
+db = gemm_engine.digit_bits_for(h, n)       # the engine's digit width for this K
+S = h.slices_for(fmt, db)
+sa, sb = h.slice(A, 0, S, None, db), h.slice(A, 1, S, None, db)
 for _ in range(reps):
     h.gemm_sliced(sa, sb, S, C)
 torch.cuda.synchronize()
