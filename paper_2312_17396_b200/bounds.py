@@ -119,3 +119,29 @@ def extra_squarings(normX, s: int) -> int:
     if arg <= 1:
         return 0
     return int(math.ceil(log2_rn(arg, _P)))
+
+
+def alpha_m(X, m: int):
+    """bounds.py:193-213: the degree-selection norm surrogate
+    max(||X^d||^(1/d), ||X^(d+1)||^(1/(d+1))) at d = floor((1+sqrt(4m+5))/2)
+    (adjusted so d(d-1) <= m+1 < d(d+1)).  The powers are formed on the
+    device at fp64 (the reference forms them at the 16-digit NORM_CTX; this
+    is a magnitude diagnostic).  ``X``: a device MatBatch of batch 1.
+    Returns (alpha as float, d)."""
+    if m < 1:
+        raise ValueError("m must be >= 1")
+    from . import ops
+    from .precision import NORM_CTX
+    d_star = int((1 + math.isqrt(4 * m + 5)) // 2)
+    while (d_star + 1) * d_star <= m + 1:
+        d_star += 1
+    while d_star * (d_star - 1) > m + 1:
+        d_star -= 1
+    X = ops.round_to(X, NORM_CTX)
+    P = X
+    for _ in range(d_star - 1):
+        P = ops.mat_mul(P, X, NORM_CTX)
+    nd = float(ops.one_norm(P)[0])
+    P = ops.mat_mul(P, X, NORM_CTX)
+    nd1 = float(ops.one_norm(P)[0])
+    return max(nd ** (1.0 / d_star), nd1 ** (1.0 / (d_star + 1))), d_star

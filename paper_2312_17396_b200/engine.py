@@ -305,7 +305,7 @@ def _assemble(h, powers: List[MatBatch], series: CoefficientSeries, ctx: Precisi
     m = series.degree
     r = m // s
     cw = coeff_words(series, ctx)
-    key = (series.coeffs, ctx.binary_precision, str(dev))
+    key = (series.token, ctx.binary_precision, str(dev))
     coeffs = _COEFF_DEV.get(key)
     if coeffs is None:
         coeffs = to_device_async(cw, torch.float64, dev)
@@ -508,7 +508,7 @@ def _graph_stages(Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: 
                   apply_switch: bool):
     """(key, build_pre, run_post) of the graphed batched pipeline."""
     d = ctx.decimal_digits
-    key = (tuple(Xt.shape), str(Xt.device if Xt.is_cuda else "host"), series.coeffs, d, wf, s, kind, delta,
+    key = (tuple(Xt.shape), str(Xt.device if Xt.is_cuda else "host"), series.token, d, wf, s, kind, delta,
            apply_switch, ge.engine(), complexmat.scope())
 
     def build_pre(xstatic, capture):
@@ -859,10 +859,44 @@ def plan_only(X, series: CoefficientSeries, ctx: PrecisionCtx, delta: float = 10
     B, n = _check_square(Xt, Xw)
     s = default_block_size(m)
     h = _lib.handle_for()
-    prep = _prepare(h, Xt, series, NORM_CTX, FP64, s, _Buckets(False), Xw)
-    plans = [plan_precisions(prep.norms[b, :prep.r + 1], prep.norms[b, prep.r + 1], ctx, delta, s=s,
+    scaled, sig = _fp64_range_series(series, s)
+    prep = _prepare(h, Xt, scaled, NORM_CTX, FP64, s, _Buckets(False), Xw)
+    r = prep.r
+    if sig is None:
+        nbs = [prep.norms[b, :r + 1] for b in range(B)]
+    else:   # undo the exact per-block 2^sigma_i scalings on the norms
+        nbs = [[Fraction(float(prep.norms[b, i])) * Fraction(2) ** -sig[i] for i in range(r + 1)]
+               for b in range(B)]
+    plans = [plan_precisions(nbs[b], prep.norms[b, r + 1], ctx, delta, s=s,
                              apply_switch=True, fix_params=fix_params) for b in range(B)]
     return plans[0] if single else plans
+
+
+def _fp64_range_series(series: CoefficientSeries, s: int):
+    """(series, None) when every RN_54 coefficient is comfortably inside the
+    fp64 exponent range; otherwise (scaled series, sigma) with block i's
+    coefficients multiplied by 2^sigma_i so that its largest |b_k| is in
+    [1, 2).  The reference's MPFR exponents are unbounded (e.g. 1/182! for
+    Table 1's d = 256 row is below the fp64 range); power-of-two scaling
+    commutes exactly with RN_54 and with the block assembly, so
+    ||B_i|| = 2^-sigma_i ||B'_i|| exactly (barring fp64 range limits of the
+    scaled blocks themselves)."""
+    nz = [abs(Fraction(c)) for c in series.coeffs if c != 0]
+    if not nz or (min(nz) > Fraction(2) ** -900 and max(nz) < Fraction(2) ** 900):
+        return series, None
+    m = series.degree
+    r = m // s
+    sig = []
+    for i in range(r + 1):
+        hi = m if i == r else s * i + s - 1
+        blk = [abs(Fraction(c)) for c in series.coeffs[s * i:hi + 1] if c != 0]
+        if not blk:
+            sig.append(0)
+            continue
+        big = max(blk)
+        sig.append(-(big.numerator.bit_length() - big.denominator.bit_length()))
+    coeffs = tuple(Fraction(c) * Fraction(2) ** sig[min(k // s, r)] for k, c in enumerate(series.coeffs))
+    return CoefficientSeries(coeffs, series.family, series.variable_note), sig
 
 
 @complexmat.complex_aware

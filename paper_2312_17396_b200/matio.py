@@ -180,8 +180,8 @@ def _build(values, d: int, device):
     return ComplexMatBatch(MatBatch(torch.from_numpy(E).to(device), fmt), n)
 
 
-def matrix_from_json(text: str, device=None):
-    """precision.py:320-327."""
+def values_from_json(text: str):
+    """precision.py:320-327 on the host: (exact (re, im) entries at p bits, d)."""
     obj = json.loads(text)
     d = int(obj["decimal_digits"])
     p = PrecisionCtx(d).binary_precision
@@ -189,12 +189,11 @@ def matrix_from_json(text: str, device=None):
     ent = obj["entries"]
     if len(ent) != nr * nc:
         raise ValueError("entry count mismatch")
-    values = [[_entry_from_str(ent[i * nc + j], p) for j in range(nc)] for i in range(nr)]
-    return _build(values, d, device)
+    return [[_entry_from_str(ent[i * nc + j], p) for j in range(nc)] for i in range(nr)], d
 
 
-def matrix_from_csv(text: str, device=None):
-    """precision.py:340-346."""
+def values_from_csv(text: str):
+    """precision.py:340-346 on the host: (exact (re, im) entries at p bits, d)."""
     rows_in = [r for r in csv.reader(io.StringIO(text)) if r]
     if not rows_in or rows_in[0][0] != "digits":
         raise ValueError("missing digits header row")
@@ -203,4 +202,16 @@ def matrix_from_csv(text: str, device=None):
     values = [[_entry_from_str(s, p) for s in r] for r in rows_in[1:]]
     if any(len(r) != len(values[0]) for r in values):
         raise ValueError("ragged rows")
+    return values, d
+
+
+def matrix_from_json(text: str, device=None):
+    """precision.py:320-327."""
+    values, d = values_from_json(text)
+    return _build(values, d, device)
+
+
+def matrix_from_csv(text: str, device=None):
+    """precision.py:340-346."""
+    values, d = values_from_csv(text)
     return _build(values, d, device)
