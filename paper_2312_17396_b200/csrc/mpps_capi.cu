@@ -1256,6 +1256,26 @@ static int dispatch_oz_tma(mpps_handle *h, int S, int fo, int mode, const oz::Oz
   return set_err(h, MPPS_EFMT, "tensor-core GEMM: no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
 }
 
+// NT = 64 tiles for the fp32 / fp64 Horner levels (S = 4 / 8, one CTA per
+// SM): half the A-plane (Y) re-reads of NT = 32.  Measured slower at cfg2
+// (fp32 level 66 -> 93 us: the epilogue no longer overlaps a second CTA's
+// mainloop), so only MPPS_OZ_NT64=1 selects it.
+static bool oz_nt64_for(int S, int fo, int mode) {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MPPS_OZ_NT64");
+    v = e ? atoi(e) : 0;
+  }
+  return v != 0 && mode == 1 && (S == 4 || S == 8) && fo != QD;
+}
+
+static int dispatch_oz_tma64(mpps_handle *h, int S, int fo, int mode, const oz::OzTmaArgs &a, int nb) {
+#define OZ(SS, NT, FF, MM) if (S == SS && fo == FF && mode == MM) return launch_oz_tma<SS, NT, FF, MM>(h, a, nb);
+  OZ(4, 64, F32, 1) OZ(4, 64, F64, 1) OZ(4, 64, DD, 1) OZ(8, 64, F64, 1) OZ(8, 64, DD, 1)
+#undef OZ
+  return set_err(h, MPPS_EFMT, "tensor-core GEMM (NT=64): no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
+}
+
 static int dispatch_oz(mpps_handle *h, int S, int fo, int mode, const oz::OzArgs &a, int nb);
 
 template <int S, int NT, int FO, int MODE>
@@ -1439,9 +1459,10 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   const bool wide = oz_wide_for(S, fo, mode, a.K);
   const int pmode = wide ? 0 : oz_pers_mode(S, fo, mode);
   const bool pers = pmode != 0;
-  const int NT = (S > 16 || pers) ? 16 : 32;
   // default: streamed-plane ring for dd / qd (S >= 16), 2-4 stage TMA ring below
   const bool ring = pers || oz_mode() == 2 || (oz_mode() == 3 && S >= 14) || S == 14 || S == 28;
+  const bool nt64 = !wide && !ring && oz_nt64_for(S, fo, mode);
+  const int NT = (S > 16 || pers) ? 16 : (nt64 ? 64 : 32);
   const int abox = ring ? (S < 4 ? S : (S == 14 ? 7 : 4)) : S;   // OzRing<S, NT>::SG
   int rc;
   if (wide || pmode == 3) {
@@ -1457,6 +1478,7 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   if (pmode == 3) return launch_oz_pwide<16, 16, DD, 0>(h, t, nb);
   if (pmode == 1) return launch_oz_pers<16, 16, DD, 0, 1>(h, t, nb);
   if (pmode == 2) return launch_oz_pers<16, 16, DD, 0, 2>(h, t, nb);
+  if (nt64) return dispatch_oz_tma64(h, S, fo, mode, t, nb);
   return ring ? dispatch_oz_ring(h, S, fo, mode, t, nb) : dispatch_oz_tma(h, S, fo, mode, t, nb);
 }
 

@@ -702,6 +702,22 @@ __device__ __forceinline__ mp::dd combine_dd(const int32_t *D) {
   return acc;
 }
 
+// fp64 value of the recombined diagonals (one rounding per group beyond the
+// first; for fp32 / fp64 outputs)
+template <int S, int DB>
+__device__ __forceinline__ double combine_d(const int32_t *D) {
+  double acc = 0.0;
+#pragma unroll
+  for (int g = 0; g < (S + 2) / 3; ++g) {
+    const int d0 = 3 * g;
+    long long G = (long long)D[d0] << (2 * DB);
+    if (d0 + 1 < S) G += (long long)D[d0 + 1] << DB;
+    if (d0 + 2 < S) G += (long long)D[d0 + 2];
+    acc = fma((double)G, pow2c(-(12 + DB * (d0 + 2))), acc);
+  }
+  return acc;
+}
+
 // Column split of the epilogue: warps w and w+4 share TMEM lane quarter
 // w % 4; the first takes columns [0, HALF), the second [HALF, NT).
 template <int S, int NT>
@@ -905,18 +921,22 @@ __device__ __forceinline__ unsigned smid() {
 // coalesced cp.async during the mainloop (a per-thread row-wise prefetch
 // competes with the TMA feed and slows the mainloop ~2.5x).
 template <int S, int NT, int FO, int MODE>
-__host__ __device__ constexpr bool oz_staged() { return S <= 16 && FO != QD && NT == 32 && MODE == 1; }
+__host__ __device__ constexpr bool oz_staged() {
+  return S <= 16 && FO != QD && (NT == 32 || (NT == 64 && S <= 8)) && MODE == 1;
+}
 template <int S, int NT, int FO, int MODE>
 __host__ __device__ constexpr uint32_t oz_ebuf_bytes() {
   return oz_staged<S, NT, FO, MODE>() ? 2u * kTileM * NT * 8u : 0u;
 }
 // Co-resident CTAs per SM: one CTA's epilogue overlaps the other's
 // mainloop.  Needs <= 256 TMEM columns (S <= 8) and shared memory for two.
-template <int S, int MODE>
-__host__ __device__ constexpr int oz_ctas_per_sm() { return (MODE == 0 ? S <= 8 : S <= 4) ? 2 : 1; }
+// NT = 64 (fp32 / fp64 Horner levels: half the A-plane re-reads) runs one
+// CTA per SM: its 128 KB staging tile leaves no room for a second.
+template <int S, int MODE, int NT = 32>
+__host__ __device__ constexpr int oz_ctas_per_sm() { return NT == 32 && (MODE == 0 ? S <= 8 : S <= 4) ? 2 : 1; }
 template <int S, int NT, int FO = DD, int MODE = 0>
 __host__ __device__ constexpr int oz_tma_stages() {
-  constexpr size_t cap = (oz_ctas_per_sm<S, MODE>() == 2 ? (size_t)113 : (size_t)226) * 1024;
+  constexpr size_t cap = (oz_ctas_per_sm<S, MODE, NT>() == 2 ? (size_t)113 : (size_t)226) * 1024;
   constexpr size_t ring = cap - oz_ebuf_bytes<S, NT, FO, MODE>() - 2048;
   return (int)(ring / oz_stage_bytes<S, NT>()) >= 4 ? 4 : (int)(ring / oz_stage_bytes<S, NT>());
 }
@@ -924,7 +944,18 @@ template <int S, int NT, int FO = DD, int MODE = 0>
 __host__ __device__ constexpr size_t oz_tma_smem_bytes() {
   return oz_tma_stages<S, NT, FO, MODE>() * oz_stage_bytes<S, NT>() + oz_ebuf_bytes<S, NT, FO, MODE>() + 2048;
 }
-__device__ __forceinline__ int ebuf_idx(int w, int r, int c) { return ((w * kTileM + r) << 5) + (c ^ (r & 15)); }
+// The streamed-plane ring kernel also stages the plain dd GEMM's epilogue
+// (coalesced stores instead of one 64-byte row segment per thread)
+template <int S, int NT, int FO, int MODE>
+__host__ __device__ constexpr bool oz_ring_staged() {
+  return oz_staged<S, NT, FO, MODE>() || (MODE == 0 && FO == DD && NT == 32 && S >= 14 && S <= 16);
+}
+template <int S, int NT, int FO, int MODE>
+__host__ __device__ constexpr uint32_t oz_ring_ebuf() {
+  return oz_ring_staged<S, NT, FO, MODE>() ? 2u * kTileM * NT * 8u : 0u;
+}
+template <int NT = 32>
+__device__ __forceinline__ int ebuf_idx(int w, int r, int c) { return (w * kTileM + r) * NT + (c ^ (r & 15)); }
 
 // Staged epilogue, phase 1 (epilogue warps 2..7, during the mainloop):
 // column exponents and, for the fused Horner step, the B_prev tile are
@@ -932,8 +963,9 @@ __device__ __forceinline__ int ebuf_idx(int w, int r, int c) { return ((w * kTil
 template <int S, int NT, int FO, int MODE, typename Args>
 __device__ __forceinline__ void oz_stage_load(const Args &args, double *ebuf, int *ebs, int b, int m0, int n0,
                                               int wid, int nw, int lane) {
-  const int col = n0 + lane;
-  if (wid == 0) ebs[lane] = col < args.N ? args.B.exps[(long long)b * args.B.rpad + col] : 0;
+  if (wid == 0)
+#pragma unroll
+    for (int c = lane; c < NT; c += 32) ebs[c] = n0 + c < args.N ? args.B.exps[(long long)b * args.B.rpad + n0 + c] : 0;
   if constexpr (MODE == 1) {
     const MatRef &Bp = args.epi.Bprev;
     const bool two = Bp.words > 1;
@@ -941,10 +973,14 @@ __device__ __forceinline__ void oz_stage_load(const Args &args, double *ebuf, in
 #pragma unroll 4
     for (int r = wid; r < kTileM; r += nw) {
       const int row = m0 + r;
-      const bool ok = row < args.M && col < args.N;
-      const double *src = ok ? base + (long long)row * Bp.ld + col : base;
-      cp_async_zfill<8>(ebuf + ebuf_idx(0, r, lane), src, ok);
-      cp_async_zfill<8>(ebuf + ebuf_idx(1, r, lane), ok && two ? src + Bp.plane : base, ok && two);
+#pragma unroll
+      for (int c = lane; c < NT; c += 32) {
+        const int col = n0 + c;
+        const bool ok = row < args.M && col < args.N;
+        const double *src = ok ? base + (long long)row * Bp.ld + col : base;
+        cp_async_zfill<8>(ebuf + ebuf_idx<NT>(0, r, c), src, ok);
+        cp_async_zfill<8>(ebuf + ebuf_idx<NT>(1, r, c), ok && two ? src + Bp.plane : base, ok && two);
+      }
     }
     cp_async_commit();
   }
@@ -982,10 +1018,19 @@ __device__ __forceinline__ void oz_stage_compute(const Args &args, double *ebuf,
       int32_t Dj[S];
 #pragma unroll
       for (int d = 0; d < S; ++d) Dj[d] = D[d][jj];
-      mp::dd v = combine_dd<S, DB>(Dj);
       const double sc = pow2i(ea + ebs[c] - (MODE == 1 ? (ey + ei) : 0));
+      const int i0w = ebuf_idx<NT>(0, r, c), i1w = ebuf_idx<NT>(1, r, c);
+      if constexpr (FO != DD && S <= 8) {
+        // fp32 / fp64 outputs: the sum in fp64 (relative error ~2^-52
+        // before the final rounding to the output format) instead of dd
+        double v = combine_d<S, DB>(Dj) * sc;
+        if constexpr (MODE == 1) v = (ebuf[i0w] + v) + ebuf[i1w];
+        if (eo) v *= so;
+        ebuf[i0w] = FO == F64 ? v : (double)__double2float_rn(v);
+        continue;
+      }
+      mp::dd v = combine_dd<S, DB>(Dj);
       v = mp::dd_make(v.hi * sc, v.lo * sc);
-      const int i0w = ebuf_idx(0, r, c), i1w = ebuf_idx(1, r, c);
       if constexpr (MODE == 1) v = mp::dd_add(mp::dd_make(ebuf[i0w], ebuf[i1w]), v);
       if (eo) v = mp::dd_make(v.hi * so, v.lo * so);
       if constexpr (FO == DD) {
@@ -1001,25 +1046,28 @@ __device__ __forceinline__ void oz_stage_compute(const Args &args, double *ebuf,
 }
 
 // Phase 3 (all 8 warps): coalesced stores of the tile, lane = column.
-template <int FO>
+template <int FO, int NT = 32>
 __device__ __forceinline__ void oz_stage_store(const MatRef &C, const double *ebuf, int M, int N, int b, int m0,
                                                int n0, int warp, int lane) {
-  const int col = n0 + lane;
-  if (col >= N) return;
+#pragma unroll
+  for (int c = lane; c < NT; c += 32) {
+    const int col = n0 + c;
+    if (col >= N) return;
 #pragma unroll 4
-  for (int r = warp; r < kTileM; r += 8) {
-    const int row = m0 + r;
-    if (row >= M) break;
-    const long long off = (long long)b * C.bstride + (long long)row * C.ld + col;
-    const double w0 = ebuf[ebuf_idx(0, r, lane)];
-    if constexpr (FO == DD) {
-      double *p = (double *)C.data + off;
-      p[0] = w0;
-      p[C.plane] = ebuf[ebuf_idx(1, r, lane)];
-    } else if constexpr (FO == F64) {
-      ((double *)C.data)[off] = w0;
-    } else {
-      ((float *)C.data)[off] = (float)w0;  // exact: w0 holds an fp32 value
+    for (int r = warp; r < kTileM; r += 8) {
+      const int row = m0 + r;
+      if (row >= M) break;
+      const long long off = (long long)b * C.bstride + (long long)row * C.ld + col;
+      const double w0 = ebuf[ebuf_idx<NT>(0, r, c)];
+      if constexpr (FO == DD) {
+        double *p = (double *)C.data + off;
+        p[0] = w0;
+        p[C.plane] = ebuf[ebuf_idx<NT>(1, r, c)];
+      } else if constexpr (FO == F64) {
+        ((double *)C.data)[off] = w0;
+      } else {
+        ((float *)C.data)[off] = (float)w0;  // exact: w0 holds an fp32 value
+      }
     }
   }
 }
@@ -1054,7 +1102,7 @@ __device__ __forceinline__ void oz_kernel_epilogue(const OzTmaArgs &args, double
       if constexpr (S != 14 && S != 28) oz_stage_compute<S, NT, FO, MODE, 7>(args, ebuf, ebs, tmem, quarter, cb, ce, b, m0, lane);
     }
     __syncthreads();
-    oz_stage_store<FO>(args.C, ebuf, args.M, args.N, b, m0, n0, warp, lane);
+    oz_stage_store<FO, NT>(args.C, ebuf, args.M, args.N, b, m0, n0, warp, lane);
   } else {
     EpiPre<S, NT, FO, MODE> pre;
     oz_epi_prefetch<S, NT, FO, MODE>(args, pre, quarter, cb, ce, b, m0, n0, lane);
@@ -1079,7 +1127,7 @@ __device__ __forceinline__ unsigned long long *oz_trace_begin(const OzTmaArgs &a
 }
 
 template <int S, int NT, int FO, int MODE>
-__global__ void __launch_bounds__(kThreadsEpi, oz_ctas_per_sm<S, MODE>()) oz_gemm_tma_kernel(const __grid_constant__ OzTmaArgs args) {
+__global__ void __launch_bounds__(kThreadsEpi, oz_ctas_per_sm<S, MODE, NT>()) oz_gemm_tma_kernel(const __grid_constant__ OzTmaArgs args) {
   constexpr int STAGES = oz_tma_stages<S, NT, FO, MODE>();
   static_assert(STAGES >= 1, "stage ring does not fit");
   constexpr uint32_t STAGE = (uint32_t)oz_stage_bytes<S, NT>();
@@ -1214,18 +1262,18 @@ struct OzRing {
 };
 template <int S, int NT, int FO, int MODE>
 __host__ __device__ constexpr size_t oz_ring_smem_bytes() {
-  return OzRing<S, NT, oz_ebuf_bytes<S, NT, FO, MODE>()>::SMEM + oz_ebuf_bytes<S, NT, FO, MODE>();
+  return OzRing<S, NT, oz_ring_ebuf<S, NT, FO, MODE>()>::SMEM + oz_ring_ebuf<S, NT, FO, MODE>();
 }
 
 template <int S, int NT, int FO, int MODE>
 __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_ring_kernel(const __grid_constant__ OzTmaArgs args) {
-  constexpr uint32_t EBUF = oz_ebuf_bytes<S, NT, FO, MODE>();
+  constexpr uint32_t EBUF = oz_ring_ebuf<S, NT, FO, MODE>();
   using R = OzRing<S, NT, EBUF>;
   constexpr uint32_t A_SLICE = kTileM * kKStep;
   constexpr uint32_t B_SLICE = NT * kKStep;
   constexpr int TCOLS = tmem_cols_for(S * NT);
 
-  constexpr bool STAGED = oz_staged<S, NT, FO, MODE>();
+  constexpr bool STAGED = oz_ring_staged<S, NT, FO, MODE>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t *bring = smem;
