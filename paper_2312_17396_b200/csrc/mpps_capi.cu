@@ -1278,12 +1278,22 @@ static int dispatch_oz_tma64(mpps_handle *h, int S, int fo, int mode, const oz::
 
 static int dispatch_oz(mpps_handle *h, int S, int fo, int mode, const oz::OzArgs &a, int nb);
 
-template <int S, int NT, int FO, int MODE>
+// 16 epilogue warps for the staged dd ring kernels (MPPS_OZ_EW=8 selects 8)
+static int oz_ring_ew() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MPPS_OZ_EW");
+    v = (e && atoi(e) == 8) ? 8 : 16;
+  }
+  return v;
+}
+
+template <int S, int NT, int FO, int MODE, int EW = 8>
 static int launch_oz_ring(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
   constexpr size_t smem = oz::oz_ring_smem_bytes<S, NT, FO, MODE>();
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_ring_kernel<S, NT, FO, MODE>,
+    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_ring_kernel<S, NT, FO, MODE, EW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz ring attr: %s", cudaGetErrorString(e));
     configured = true;
@@ -1294,11 +1304,16 @@ static int launch_oz_ring(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
   t.group = oz_group();
   dim3 grid(t.mtiles * t.ntiles, 1, nb);
   if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
-  oz::oz_gemm_ring_kernel<S, NT, FO, MODE><<<grid, oz::kThreadsEpi, smem, h->stream>>>(t);
+  oz::oz_gemm_ring_kernel<S, NT, FO, MODE, EW><<<grid, 32 * EW, smem, h->stream>>>(t);
   return after_launch(h, "oz_gemm_ring_kernel");
 }
 
 static int dispatch_oz_ring(mpps_handle *h, int S, int fo, int mode, const oz::OzTmaArgs &a, int nb) {
+  if (oz_ring_ew() == 16) {
+#define OZ16(SS, NT, FF, MM) if (S == SS && fo == FF && mode == MM) return launch_oz_ring<SS, NT, FF, MM, 16>(h, a, nb);
+    OZ16(14, 32, DD, 0) OZ16(14, 32, DD, 1) OZ16(16, 32, DD, 0) OZ16(16, 32, DD, 1)
+#undef OZ16
+  }
 #define OZ(SS, NT, FF, MM) if (S == SS && fo == FF && mode == MM) return launch_oz_ring<SS, NT, FF, MM>(h, a, nb);
   OZ(14, 32, DD, 0) OZ(14, 32, DD, 1) OZ(14, 32, QD, 1)
   OZ(16, 32, DD, 0) OZ(16, 32, DD, 1) OZ(16, 32, QD, 1)

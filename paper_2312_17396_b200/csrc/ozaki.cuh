@@ -989,10 +989,9 @@ __device__ __forceinline__ void oz_stage_load(const Args &args, double *ebuf, in
 // Phase 2 (all 8 warps, after the MMAs): thread = row; its columns are
 // combined from TMEM, the B_prev words read from (and the dd-width result
 // written back to) the staging tile.
-template <int S, int NT, int FO, int MODE, int DB, typename Args>
+template <int S, int NT, int FO, int MODE, int DB, int CW = 8, typename Args>
 __device__ __forceinline__ void oz_stage_compute(const Args &args, double *ebuf, const int *ebs, uint32_t tmem,
                                                  int quarter, int c_begin, int c_end, int b, int m0, int lane) {
-  constexpr int CW = 8;
   const int r = quarter * 32 + lane;
   const int row = m0 + r;
   const int ea = row < args.M ? args.A.exps[(long long)b * args.A.rpad + row] : 0;
@@ -1010,7 +1009,10 @@ __device__ __forceinline__ void oz_stage_compute(const Args &args, double *ebuf,
     if (c0 >= c_end) break;
     int32_t D[S][CW];
 #pragma unroll
-    for (int d = 0; d < S; ++d) tmem_ld8(lane_base + (uint32_t)(d * NT + c0), D[d]);
+    for (int d = 0; d < S; ++d) {
+      if constexpr (CW == 8) tmem_ld8(lane_base + (uint32_t)(d * NT + c0), D[d]);
+      else tmem_ld4(lane_base + (uint32_t)(d * NT + c0), D[d]);
+    }
     tmem_ld_wait();
 #pragma unroll
     for (int jj = 0; jj < CW; ++jj) {
@@ -1046,7 +1048,7 @@ __device__ __forceinline__ void oz_stage_compute(const Args &args, double *ebuf,
 }
 
 // Phase 3 (all 8 warps): coalesced stores of the tile, lane = column.
-template <int FO, int NT = 32>
+template <int FO, int NT = 32, int EW = 8>
 __device__ __forceinline__ void oz_stage_store(const MatRef &C, const double *ebuf, int M, int N, int b, int m0,
                                                int n0, int warp, int lane) {
 #pragma unroll
@@ -1054,7 +1056,7 @@ __device__ __forceinline__ void oz_stage_store(const MatRef &C, const double *eb
     const int col = n0 + c;
     if (col >= N) return;
 #pragma unroll 4
-    for (int r = warp; r < kTileM; r += 8) {
+    for (int r = warp; r < kTileM; r += EW) {
       const int row = m0 + r;
       if (row >= M) break;
       const long long off = (long long)b * C.bstride + (long long)row * C.ld + col;
@@ -1078,16 +1080,19 @@ __device__ __forceinline__ void oz_stage_store(const MatRef &C, const double *eb
 // coalesced cp.async, or per-thread register prefetch), then the TMEM
 // diagonals are combined and stored.  Ends with every thread past its
 // TMEM reads (the caller deallocates).
-template <int S, int NT, int FO, int MODE, bool STAGED>
+template <int S, int NT, int FO, int MODE, bool STAGED, int EW = 8>
 __device__ __forceinline__ void oz_kernel_epilogue(const OzTmaArgs &args, double *ebuf, int *ebs, uint32_t tmem,
                                                    uint64_t *done, int warp, int lane, int b, int m0, int n0,
                                                    unsigned long long *tr) {
-  // warps w and w+4 share TMEM lane quarter w % 4 and split the columns
+  // warps w, w+4, ... share TMEM lane quarter w % 4 and split the columns
+  // (EW = 16, staged only: four column parts of NT/4, 4-column TMEM loads)
+  static_assert(EW == 8 || (EW == 16 && STAGED), "16 epilogue warps need the staged epilogue");
   const int quarter = warp & 3, half = warp >> 2;
-  const int cb = half ? EpiCols<S, NT>::HALF : 0, ce = half ? NT : EpiCols<S, NT>::HALF;
+  const int cb = EW == 16 ? half * (NT / 4) : (half ? EpiCols<S, NT>::HALF : 0);
+  const int ce = EW == 16 ? cb + NT / 4 : (half ? NT : EpiCols<S, NT>::HALF);
   if constexpr (STAGED) {
     if (warp >= 2) {
-      oz_stage_load<S, NT, FO, MODE>(args, ebuf, ebs, b, m0, n0, warp - 2, 6, lane);
+      oz_stage_load<S, NT, FO, MODE>(args, ebuf, ebs, b, m0, n0, warp - 2, EW - 2, lane);
       if constexpr (MODE == 1) cp_async_wait<0>();
     }
     __syncwarp();
@@ -1096,13 +1101,16 @@ __device__ __forceinline__ void oz_kernel_epilogue(const OzTmaArgs &args, double
     if (tr) tr[2] = globaltimer();
     __syncthreads();  // staged B_prev / exponents visible to every warp
     fence_after();
+    constexpr int SCW = EW == 16 ? 4 : 8;
     if (oz_db_of<S>(args.A.db) == 8) {
-      if constexpr (S != 16 && S != 31) oz_stage_compute<S, NT, FO, MODE, 8>(args, ebuf, ebs, tmem, quarter, cb, ce, b, m0, lane);
+      if constexpr (S != 16 && S != 31)
+        oz_stage_compute<S, NT, FO, MODE, 8, SCW>(args, ebuf, ebs, tmem, quarter, cb, ce, b, m0, lane);
     } else {
-      if constexpr (S != 14 && S != 28) oz_stage_compute<S, NT, FO, MODE, 7>(args, ebuf, ebs, tmem, quarter, cb, ce, b, m0, lane);
+      if constexpr (S != 14 && S != 28)
+        oz_stage_compute<S, NT, FO, MODE, 7, SCW>(args, ebuf, ebs, tmem, quarter, cb, ce, b, m0, lane);
     }
     __syncthreads();
-    oz_stage_store<FO, NT>(args.C, ebuf, args.M, args.N, b, m0, n0, warp, lane);
+    oz_stage_store<FO, NT, EW>(args.C, ebuf, args.M, args.N, b, m0, n0, warp, lane);
   } else {
     EpiPre<S, NT, FO, MODE> pre;
     oz_epi_prefetch<S, NT, FO, MODE>(args, pre, quarter, cb, ce, b, m0, n0, lane);
@@ -1265,8 +1273,8 @@ __host__ __device__ constexpr size_t oz_ring_smem_bytes() {
   return OzRing<S, NT, oz_ring_ebuf<S, NT, FO, MODE>()>::SMEM + oz_ring_ebuf<S, NT, FO, MODE>();
 }
 
-template <int S, int NT, int FO, int MODE>
-__global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_ring_kernel(const __grid_constant__ OzTmaArgs args) {
+template <int S, int NT, int FO, int MODE, int EW = 8>
+__global__ void __launch_bounds__(32 * EW, 1) oz_gemm_ring_kernel(const __grid_constant__ OzTmaArgs args) {
   constexpr uint32_t EBUF = oz_ring_ebuf<S, NT, FO, MODE>();
   using R = OzRing<S, NT, EBUF>;
   constexpr uint32_t A_SLICE = kTileM * kKStep;
@@ -1337,7 +1345,7 @@ __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_ring_kernel(const __gr
     }
     mma_commit(smem_u32(done));
   }
-  oz_kernel_epilogue<S, NT, FO, MODE, STAGED>(args, ebuf, ebs, tmem, done, warp, lane, b, m0, n0, tr);
+  oz_kernel_epilogue<S, NT, FO, MODE, STAGED, EW>(args, ebuf, ebs, tmem, done, warp, lane, b, m0, n0, tr);
   if (warp == 0) tmem_dealloc<TCOLS>(tmem);
 }
 
