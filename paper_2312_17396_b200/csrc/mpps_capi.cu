@@ -1228,12 +1228,12 @@ static int oz_group() {
   return g_oz_group_override > 0 ? g_oz_group_override : v;
 }
 
-template <int S, int NT, int FO, int MODE>
+template <int S, int NT, int FO, int MODE, int EW = 8>
 static int launch_oz_tma(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
   constexpr size_t smem = oz::oz_tma_smem_bytes<S, NT, FO, MODE>();
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_tma_kernel<S, NT, FO, MODE>,
+    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_tma_kernel<S, NT, FO, MODE, EW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz tma attr: %s", cudaGetErrorString(e));
     configured = true;
@@ -1244,11 +1244,17 @@ static int launch_oz_tma(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
   t.group = oz_group();
   dim3 grid(t.mtiles * t.ntiles, 1, nb);
   if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
-  oz::oz_gemm_tma_kernel<S, NT, FO, MODE><<<grid, oz::kThreadsEpi, smem, h->stream>>>(t);
+  oz::oz_gemm_tma_kernel<S, NT, FO, MODE, EW><<<grid, 32 * EW, smem, h->stream>>>(t);
   return after_launch(h, "oz_gemm_tma_kernel");
 }
 
+static int oz_ring_ew();
 static int dispatch_oz_tma(mpps_handle *h, int S, int fo, int mode, const oz::OzTmaArgs &a, int nb) {
+  // fp64 Horner levels (one CTA per SM): 16 epilogue warps like the dd ring
+  if (oz_ring_ew() == 16 && S == 8 && mode == 1) {
+    if (fo == DD) return launch_oz_tma<8, 32, DD, 1, 16>(h, a, nb);
+    if (fo == F64) return launch_oz_tma<8, 32, F64, 1, 16>(h, a, nb);
+  }
 #define OZ(SS, NT, FF, MM) if (S == SS && fo == FF && mode == MM) return launch_oz_tma<SS, NT, FF, MM>(h, a, nb);
   OZ(4, 32, F32, 0) OZ(4, 32, F32, 1) OZ(4, 32, F64, 1) OZ(4, 32, DD, 1) OZ(4, 32, QD, 1)
   OZ(8, 32, F64, 0) OZ(8, 32, F64, 1) OZ(8, 32, DD, 1) OZ(8, 32, QD, 1)

@@ -1134,8 +1134,8 @@ __device__ __forceinline__ unsigned long long *oz_trace_begin(const OzTmaArgs &a
   return tr;
 }
 
-template <int S, int NT, int FO, int MODE>
-__global__ void __launch_bounds__(kThreadsEpi, oz_ctas_per_sm<S, MODE, NT>()) oz_gemm_tma_kernel(const __grid_constant__ OzTmaArgs args) {
+template <int S, int NT, int FO, int MODE, int EW = 8>
+__global__ void __launch_bounds__(32 * EW, EW == 8 ? oz_ctas_per_sm<S, MODE, NT>() : 1) oz_gemm_tma_kernel(const __grid_constant__ OzTmaArgs args) {
   constexpr int STAGES = oz_tma_stages<S, NT, FO, MODE>();
   static_assert(STAGES >= 1, "stage ring does not fit");
   constexpr uint32_t STAGE = (uint32_t)oz_stage_bytes<S, NT>();
@@ -1210,7 +1210,7 @@ __global__ void __launch_bounds__(kThreadsEpi, oz_ctas_per_sm<S, MODE, NT>()) oz
     }
     mma_commit(smem_u32(done));
   }
-  oz_kernel_epilogue<S, NT, FO, MODE, STAGED>(args, ebuf, ebs, tmem, done, warp, lane, b, m0, n0, tr);
+  oz_kernel_epilogue<S, NT, FO, MODE, STAGED, EW>(args, ebuf, ebs, tmem, done, warp, lane, b, m0, n0, tr);
   if (warp == 0) tmem_dealloc<TCOLS>(tmem);
 }
 
