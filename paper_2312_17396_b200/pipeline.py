@@ -20,7 +20,7 @@ one-shot evaluator).  Reports are returned in chunk order.
 from __future__ import annotations
 
 import time
-from typing import Callable, List
+from typing import Callable, List, Optional
 
 
 def _torch():
@@ -87,7 +87,7 @@ def split_sizes(B: int, chunks) -> List[int]:
 
 
 def evaluate_host(submit: Callable, X_host, out_host, chunks=3, trace=None, streams: int = 1,
-                  ahead=None) -> List[object]:
+                  ahead=None, window: Optional[int] = None) -> List[object]:
     """``chunks``: a count (tapered split, see split_sizes) or explicit sizes.
 
     ``streams=1``: chunks run one after another on the caller's stream, the
@@ -101,6 +101,15 @@ def evaluate_host(submit: Callable, X_host, out_host, chunks=3, trace=None, stre
     next call with the same shapes (``out_host`` holds the copy).
     ``ahead`` (default: streams > 1) selects the submit-everything-up-front
     mode independently of the stream count.
+    ``window`` (ahead mode): at most this many chunks in flight, each in
+    graph slot ``c % window`` with its own device input buffer; chunk
+    c + window is uploaded and submitted once chunk c is planned, its
+    upload waiting on the GPU for chunk c's input copy and its evaluation
+    for chunk c's download.  A long host stream (many batches) then runs
+    through a bounded set of slots with the copies of one batch overlapping
+    the evaluation of the next; a report's ``result`` is then valid only
+    until chunk c + window is submitted (``out_host`` holds every result).
+    Default: every chunk in flight.
     ``trace``: optional list; timing events (label, event, host time) are
     appended (diagnostics, tools/e2e_chunks.py)."""
     torch = _torch()
@@ -131,21 +140,27 @@ def evaluate_host(submit: Callable, X_host, out_host, chunks=3, trace=None, stre
         comps = [caller, caller]
     up.wait_stream(caller)
     down.wait_stream(caller)
+    W = chunks if (window is None or not ahead) else max(1, min(int(window), chunks))
     dev_in = [None] * chunks
     ev_in = [torch.cuda.Event() for _ in range(chunks)]
+    consumed = [None] * chunks        # after chunk c's pre graph took its input
+    downed = [None] * chunks          # after chunk c's result left the device
     pend = [None] * chunks
     reps = []
 
     def upload(c):
         # one device input buffer per chunk position (cached across calls), so
         # every upload is enqueued up front and never waits for a consumer
+        # (with a window: per slot, after the previous chunk of the slot took it)
         lo, hi = bounds[c], bounds[c + 1]
         with torch.cuda.stream(up):
+            if c >= W:
+                up.wait_event(consumed[c - W])
             shape = (hi - lo,) + tuple(X_host.shape[1:])
-            buf = st["bufs"].get((c, shape))
+            buf = st["bufs"].get((c % W, shape))
             if buf is None:
                 buf = torch.empty(shape, dtype=torch.float64, device=caller.device)
-                st["bufs"][(c, shape)] = buf
+                st["bufs"][(c % W, shape)] = buf
             dev_in[c] = buf
             mark(f"up{c}<", up)
             buf.copy_(X_host[lo:hi], non_blocking=True)
@@ -156,17 +171,21 @@ def evaluate_host(submit: Callable, X_host, out_host, chunks=3, trace=None, stre
         comp = comps[c % 2]
         with torch.cuda.stream(comp):
             comp.wait_event(ev_in[c])
+            if c >= W:
+                comp.wait_event(downed[c - W])     # the slot's result buffer is free
             mark(f"pre{c}<", comp)
             if ahead:
-                pend[c] = submit(dev_in[c], c, static_result=True)
+                pend[c] = submit(dev_in[c], c % W, static_result=True)
             else:
                 pend[c] = submit(dev_in[c], c % 2)
+            consumed[c] = torch.cuda.Event()
+            consumed[c].record(comp)
             mark(f"pre{c}>", comp)
 
-    for c in range(chunks):
+    for c in range(W):
         upload(c)
     if ahead:
-        for c in range(chunks):
+        for c in range(W):
             start(c)
     else:
         start(0)
@@ -193,8 +212,13 @@ def evaluate_host(submit: Callable, X_host, out_host, chunks=3, trace=None, stre
             for w in range(res.shape[0]):    # contiguous pinned destination per word
                 out_host[w, lo:hi].copy_(res[w], non_blocking=True)
             res.record_stream(down)
+            downed[c] = torch.cuda.Event()
+            downed[c].record(down)
             mark(f"down{c}>", down)
         reps.append(rep)
+        if ahead and c + W < chunks:
+            upload(c + W)
+            start(c + W)
     for cs in set(comps):
         if cs is not caller:
             caller.wait_stream(cs)

@@ -367,3 +367,16 @@ def test_pipelined_host_evaluation_matches(cuda):
         torch.cuda.synchronize()
         assert len(reps) == 4
         assert np.array_equal(out.numpy(), ref)
+    # a host stream longer than the slot window: 6 chunks through 2 slots
+    # (uploads wait for the slot's previous input copy, evaluations for its
+    # previous download), distinct matrices per chunk
+    X2 = np.stack([synth(64, 1.0, 100 + b) for b in range(12)])
+    ref2 = m.ps_mixed_exp(X2, 30, ctx).result.data.cpu().numpy()
+    Xh2 = torch.from_numpy(X2).pin_memory()
+    for win in (2, 3):
+        out.zero_()
+        reps = pipeline.evaluate_host(pipeline.mixed_exp(30, ctx), Xh2, out, chunks=[2] * 6, streams=2,
+                                      window=win)
+        torch.cuda.synchronize()
+        assert len(reps) == 6
+        assert np.array_equal(out.numpy(), ref2)
