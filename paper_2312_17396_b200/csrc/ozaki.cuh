@@ -296,6 +296,58 @@ __device__ __forceinline__ unsigned __int128 fixed_biased(const mp::qd &v, int e
   return (unsigned __int128)V + C;
 }
 
+// Same V (up to the rounding of the low word, |V - v 2^(F-e)| <= 1) with
+// explicit 64-bit limbs instead of generic variable 128-bit shifts
+// (~3x fewer integer instructions per entry; the split is issue-bound):
+// hi = m_h 2^x_h with |hi| < 2^e gives s = x_h + F - e <= F - 53, i.e.
+// s < 64 for S <= 14, so m_h << s needs one funnel step; lo (<= half an ulp
+// of hi) lands at s - 53 <= 4 and is added as a rounded signed 64-bit value.
+__device__ __forceinline__ void dbl_int_parts(double x, long long &m, int &ex) {
+  const long long bits = __double_as_longlong(x);
+  const int eb = (int)((bits >> 52) & 0x7ff);
+  const long long mant = bits & 0xfffffffffffffLL;
+  const long long mm = eb ? (mant | 0x10000000000000LL) : mant;
+  m = bits < 0 ? -mm : mm;
+  ex = (eb ? eb : 1) - 1075;
+}
+// round(m 2^s) for s <= 4 (signed 64-bit; s < 0 rounds half up)
+__device__ __forceinline__ long long shift_round64(long long m, int s) {
+  if (s >= 0) return m << s;
+  const int t = -s > 62 ? 62 : -s;
+  return (m + (1LL << (t - 1))) >> t;
+}
+template <int W, int S>
+__device__ __forceinline__ unsigned __int128 fixed_biased_fast(const mp::qd &v, int e) {
+  constexpr int F = 6 + 8 * (S - 1);
+  static_assert(W <= 2 && F - 53 < 64, "fixed-point split: at most 2 words and 14 planes");
+  long long mh;
+  int xh;
+  dbl_int_parts(v.x[0], mh, xh);
+  const int sh = xh + F - e;
+  unsigned long long L;
+  long long H;
+  if (sh >= 0) {                       // m_h << sh, sh <= F - 53
+    L = (unsigned long long)mh << sh;
+    H = sh ? (mh >> (64 - sh)) : (mh >> 63);
+  } else {
+    const long long r = shift_round64(mh, sh);
+    L = (unsigned long long)r;
+    H = r >> 63;
+  }
+  if constexpr (W == 2) {
+    long long ml;
+    int xl;
+    dbl_int_parts(v.x[1], ml, xl);
+    const long long w = (ml == 0) ? 0 : shift_round64(ml, xl + F - e);
+    const unsigned long long L2 = L + (unsigned long long)w;
+    H += (w >> 63) + (L2 < L ? 1 : 0);
+    L = L2;
+  }
+  const unsigned __int128 V = ((unsigned __int128)(unsigned long long)H << 64) | L;
+  const unsigned __int128 C = ((unsigned __int128)fixed_cmask_hi<S>() << 64) | fixed_cmask_lo<S>();
+  return V + C;
+}
+
 // byte k of the 128-bit Y as the low byte of an int
 __device__ __forceinline__ uint32_t fixed_word(const unsigned __int128 &Y, int j) {
   return (uint32_t)(Y >> (32 * j));
@@ -336,7 +388,7 @@ __device__ __forceinline__ void slice_rows_body(const MatRef &A, int rows, int c
         mp::qd v = mp::qd_make(0.0, 0.0, 0.0, 0.0);
         if (i < rows && k < cols)
           v = fi == F32 ? mp::qd_from_d((double)((const float *)A.data)[base + k]) : load_qd(A, base + k);
-        Y[q] = fixed_biased<W, S>(v, e);
+        Y[q] = fixed_biased_fast<W, S>(v, e);
       }
 #pragma unroll
       for (int s = 0; s < S; ++s) {
@@ -451,7 +503,7 @@ __device__ __forceinline__ void slice_cols_body(const MatRef &B, int rows, int c
     if constexpr (FIXED) {
       // fixed-point path on the unscaled words (the column exponent enters
       // the shift)
-      const unsigned __int128 Y = fixed_biased<W, S>(vraw, ecol);
+      const unsigned __int128 Y = fixed_biased_fast<W, S>(vraw, ecol);
 #pragma unroll
       for (int s2 = 0; s2 < S; ++s2) {
         const int kb = S - 1 - s2;

@@ -95,3 +95,42 @@ def test_tc_digit_width_rules(cuda):
     d = (C.data[0] - A.data[0]) + (C.data[1] - A.data[1])
     assert (d.abs() <= 2.0 ** -104 * A.data[0].abs().amax(dim=-1, keepdim=True)).all()
     assert h.max_k_8bit() == 4800
+
+
+@pytest.mark.parametrize("side", [0, 1])
+@pytest.mark.parametrize("fmt,S", [(31, 14), (15, 8), (7, 4), (31, 8), (31, 4)])
+def test_fixed_point_split_exact(cuda, side, fmt, S):
+    """8-bit fixed-point split (fixed_biased_fast): every entry's digit planes
+    reproduce round(v 2^(F-e)) to within one unit of 2^(e-F), F = 6 + 8(S-1),
+    over entries spanning ~2^-200 .. 1 of their row/column maximum, signs,
+    zeros and normalised dd low words."""
+    import torch
+    from paper_2312_17396_b200 import _lib
+    from paper_2312_17396_b200.precision import MatBatch
+    h = _lib.handle_for()
+    rng = np.random.default_rng(7 + S + fmt + side)
+    n = 96
+    hi = rng.standard_normal((n, n)) * 2.0 ** rng.integers(-200, 1, (n, n)).astype(float)
+    hi[rng.random((n, n)) < 0.05] = 0.0
+    hi[:, 3] *= 2.0 ** 40          # a column / row with a large maximum
+    if fmt == 7:
+        hi = hi.astype(np.float32).astype(np.float64)
+    words = [hi]
+    if fmt == 31:
+        lo = np.where(hi != 0, hi * 2.0 ** -54 * rng.uniform(-1, 1, hi.shape), 0.0)
+        lo = (hi + lo) - hi            # representable, |lo| <= ulp(hi)/2
+        words = [hi, lo]
+    A = MatBatch.empty(fmt, 1, n, device=cuda)
+    for w, x in enumerate(words):
+        A.data[w, 0] = torch.from_numpy(x).to(A.data.dtype)
+    sl = h.slice(A, side, S, None, 8)
+    dig = sl.digits[:, 0].cpu().numpy().astype(np.int64)      # (S, rpad, kpad)
+    ex = sl.exps[0].cpu().numpy()
+    F = 6 + 8 * (S - 1)
+    for _ in range(300):
+        i, k = int(rng.integers(0, n)), int(rng.integers(0, n))
+        r, c = (i, k) if side == 0 else (k, i)     # row-split rows are A rows; col-split rows are A columns
+        v = sum(Fraction(float(words[w][r, c])) for w in range(len(words)))
+        V = sum(int(dig[s, i, k]) << (8 * (S - 1 - s)) for s in range(S))
+        exact = v * Fraction(2) ** (F - int(ex[i]))
+        assert abs(V - exact) <= 1, (side, i, k, float(V - exact))
