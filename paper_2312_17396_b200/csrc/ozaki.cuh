@@ -302,6 +302,12 @@ __device__ __forceinline__ unsigned __int128 fixed_biased(const mp::qd &v, int e
 // hi = m_h 2^x_h with |hi| < 2^e gives s = x_h + F - e <= F - 53, i.e.
 // s < 64 for S <= 14, so m_h << s needs one funnel step; lo (<= half an ulp
 // of hi) lands at s - 53 <= 4 and is added as a rounded signed 64-bit value.
+// the W stored words of a W-word source (W from the format: no run-time word count)
+template <int W>
+__device__ __forceinline__ mp::qd load_w(const MatRef &m, long long off) {
+  const double *p = (const double *)m.data + off;
+  return mp::qd_make(p[0], W > 1 ? p[m.plane] : 0.0, W > 2 ? p[2 * m.plane] : 0.0, W > 3 ? p[3 * m.plane] : 0.0);
+}
 __device__ __forceinline__ void dbl_int_parts(double x, long long &m, int &ex) {
   const long long bits = __double_as_longlong(x);
   const int eb = (int)((bits >> 52) & 0x7ff);
@@ -312,9 +318,9 @@ __device__ __forceinline__ void dbl_int_parts(double x, long long &m, int &ex) {
 }
 // round(m 2^s) for s <= 4 (signed 64-bit; s < 0 rounds half up)
 __device__ __forceinline__ long long shift_round64(long long m, int s) {
-  if (s >= 0) return m << s;
-  const int t = -s > 62 ? 62 : -s;
-  return (m + (1LL << (t - 1))) >> t;
+  const int t = min(max(-s, 1), 62);
+  const long long down = (m + (1LL << (t - 1))) >> t;
+  return s >= 0 ? (m << (s & 63)) : down;
 }
 template <int W, int S>
 __device__ __forceinline__ unsigned __int128 fixed_biased_fast(const mp::qd &v, int e) {
@@ -326,19 +332,18 @@ __device__ __forceinline__ unsigned __int128 fixed_biased_fast(const mp::qd &v, 
   const int sh = xh + F - e;
   unsigned long long L;
   long long H;
-  if (sh >= 0) {                       // m_h << sh, sh <= F - 53
-    L = (unsigned long long)mh << sh;
-    H = sh ? (mh >> (64 - sh)) : (mh >> 63);
-  } else {
+  {                                    // m_h << sh (sh <= F - 53 < 64) or rounded m_h 2^sh
+    const int sp = sh & 63;
     const long long r = shift_round64(mh, sh);
-    L = (unsigned long long)r;
-    H = r >> 63;
+    const long long hs = sp ? (mh >> (64 - sp)) : (mh >> 63);
+    L = sh >= 0 ? ((unsigned long long)mh << sp) : (unsigned long long)r;
+    H = sh >= 0 ? hs : (r >> 63);
   }
   if constexpr (W == 2) {
     long long ml;
     int xl;
     dbl_int_parts(v.x[1], ml, xl);
-    const long long w = (ml == 0) ? 0 : shift_round64(ml, xl + F - e);
+    const long long w = shift_round64(ml, xl + F - e);      // ml = 0 -> 0
     const unsigned long long L2 = L + (unsigned long long)w;
     H += (w >> 63) + (L2 < L ? 1 : 0);
     L = L2;
@@ -382,13 +387,25 @@ __device__ __forceinline__ void slice_rows_body(const MatRef &A, int rows, int c
     if constexpr (DB == 8 && W <= 2 && S <= 14) {
       // 8-bit digits from the exact fixed-point value (carry-free bytes)
       unsigned __int128 Y[4];
+      if (i < rows && k0 + 3 < cols && fi != F32) {
+        // interior: W words of four entries, no per-entry guards or format checks
+        const double *p = (const double *)A.data + base + k0;
+        double w0[4], w1[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int k = k0 + q;
-        mp::qd v = mp::qd_make(0.0, 0.0, 0.0, 0.0);
-        if (i < rows && k < cols)
-          v = fi == F32 ? mp::qd_from_d((double)((const float *)A.data)[base + k]) : load_qd(A, base + k);
-        Y[q] = fixed_biased_fast<W, S>(v, e);
+        for (int q = 0; q < 4; ++q) w0[q] = p[q];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w1[q] = W > 1 ? p[A.plane + q] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Y[q] = fixed_biased_fast<W, S>(mp::qd_make(w0[q], w1[q], 0.0, 0.0), e);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int k = k0 + q;
+          mp::qd v = mp::qd_make(0.0, 0.0, 0.0, 0.0);
+          if (i < rows && k < cols)
+            v = fi == F32 ? mp::qd_from_d((double)((const float *)A.data)[base + k]) : load_qd(A, base + k);
+          Y[q] = fixed_biased_fast<W, S>(v, e);
+        }
       }
 #pragma unroll
       for (int s = 0; s < S; ++s) {
@@ -494,7 +511,7 @@ __device__ __forceinline__ void slice_cols_body(const MatRef &B, int rows, int c
     int ecol = 0;
     if (k < rows && j < cols) {
       const long long off = (long long)b * B.bstride + (long long)k * B.ld + j;
-      v = fi == F32 ? mp::qd_from_d((double)((const float *)B.data)[off]) : load_qd(B, off);
+      v = fi == F32 ? mp::qd_from_d((double)((const float *)B.data)[off]) : load_w<W>(B, off);
       ecol = out.exps[(long long)b * out.rpad + j];
       if constexpr (!FIXED) v = scale_words<W>(v, -ecol);
     }
