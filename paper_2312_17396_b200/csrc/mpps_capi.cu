@@ -618,6 +618,27 @@ __global__ void scalar_top_wf_kernel(const ScalarTopArgs a) {
   if (j >= a.cols) return;
   const long long yb = (long long)b * a.Y.bstride, bb = (long long)b * a.Bp.bstride,
                   ob = (long long)b * a.out.bstride;
+  if constexpr (WF == DD && (FT == F32 || FT == F64) && (FO == F32 || FO == F64)) {
+    // fp32 / fp64 top level from dd operands in plain fp64: b_m Y to ~2^-53,
+    // RN_24 with an unbounded exponent by a Veltkamp split, the + B_{r-1}
+    // sum to ~2^-53 before the final rounding into FO
+    const double b0 = a.bm[0], b1 = a.bm[1], so = oz::pow2i(eo);
+    for (int i = blockIdx.y; i < a.rows; i += gridDim.y) {
+      const mp::dd y = V::load(a.Y, yb + (long long)i * a.Y.ld + j);
+      const mp::dd bp = V::load(a.Bp, bb + (long long)i * a.Bp.ld + j);
+      double tv = fma(b0, y.hi, fma(b0, y.lo, b1 * y.hi));
+      if constexpr (FT == F32) {
+        const double c = tv * 536870913.0;                 // 2^29 + 1
+        tv = c - (c - tv);                                 // 24 significant bits
+      }
+      double sum = (bp.hi + tv) + bp.lo;
+      if (eo) sum *= so;
+      const long long off = ob + (long long)i * a.out.ld + j;
+      if constexpr (FO == F32) ((float *)a.out.data)[off] = __double2float_rn(sum);
+      else ((double *)a.out.data)[off] = sum;
+    }
+    return;
+  }
   for (int i = blockIdx.y; i < a.rows; i += gridDim.y) {
     const auto y = V::load(a.Y, yb + (long long)i * a.Y.ld + j);
     const auto bp = V::load(a.Bp, bb + (long long)i * a.Bp.ld + j);
@@ -1139,6 +1160,18 @@ static oz::SliceRef sref(const mpps_slices *s) {
   return r;
 }
 
+// column split with the exponents in the same kernel (MPPS_OZ_COLS_FUSED=1).
+// Measured slower at cfg2 (dd split 37 + 8 -> 66 us: one CTA per 32-column
+// strip leaves too few CTAs in flight), so off by default.
+static bool oz_cols_fused() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MPPS_OZ_COLS_FUSED");
+    v = e ? atoi(e) : 0;
+  }
+  return v != 0;
+}
+
 extern "C" int mpps_slice(mpps_handle *h, const mpps_mat *src, int side, mpps_slices *out, const int *sel, int nsel) {
   int rc = check_mat(h, src, "slice.src");
   if (rc) return rc;
@@ -1169,6 +1202,15 @@ extern "C" int mpps_slice(mpps_handle *h, const mpps_mat *src, int side, mpps_sl
     SR(2, 31) SR(4, 4) SR(4, 8) SR(4, 14) SR(4, 16) SR(4, 28) SR(4, 31) {}
 #undef SR
     return after_launch(h, "slice_rows_kernel");
+  }
+  if (oz_cols_fused()) {
+    dim3 grid(out->rpad / 32, nb);
+#define SCF(WW, SS) \
+  if (W == WW && S == SS) oz::slice_cols_fused_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
+    SCF(1, 4) SCF(1, 8) SCF(1, 14) SCF(1, 16) SCF(1, 28) SCF(1, 31) SCF(2, 4) SCF(2, 8) SCF(2, 14) SCF(2, 16) SCF(2, 28)
+    SCF(2, 31) SCF(4, 4) SCF(4, 8) SCF(4, 14) SCF(4, 16) SCF(4, 28) SCF(4, 31) {}
+#undef SCF
+    return after_launch(h, "slice_cols_fused_kernel");
   }
   oz::col_exps_kernel<<<dim3(out->rpad / 32, nb), 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel);
   rc = after_launch(h, "col_exps_kernel");

@@ -499,10 +499,10 @@ __global__ void col_exps_kernel(MatRef B, int rows, int cols, int fi, SliceRef o
 // Side B digits, transposed through shared memory: tile of 32 k x 32 j.
 template <int W, int S, int DB>
 __device__ __forceinline__ void slice_cols_body(const MatRef &B, int rows, int cols, int fi, const SliceRef &out,
-                                                const int *sel, int8_t (*tile)[32][36]) {
+                                                const int *sel, int8_t (*tile)[32][36], int k0, int bz,
+                                                const int *ecs = nullptr) {
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
-  const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
-  const int bz = blockIdx.z;
+  const int j0 = blockIdx.x * 32;
   const int b = sel ? sel[bz] : bz;
   for (int kk = ty; kk < 32; kk += 8) {
     const int k = k0 + kk, j = j0 + tx;
@@ -512,7 +512,7 @@ __device__ __forceinline__ void slice_cols_body(const MatRef &B, int rows, int c
     if (k < rows && j < cols) {
       const long long off = (long long)b * B.bstride + (long long)k * B.ld + j;
       v = fi == F32 ? mp::qd_from_d((double)((const float *)B.data)[off]) : load_w<W>(B, off);
-      ecol = out.exps[(long long)b * out.rpad + j];
+      ecol = ecs ? ecs[tx] : out.exps[(long long)b * out.rpad + j];
       if constexpr (!FIXED) v = scale_words<W>(v, -ecol);
     }
     const mp::qd vraw = v;
@@ -549,9 +549,50 @@ template <int W, int S>
 __global__ void slice_cols_kernel(MatRef B, int rows, int cols, int fi, SliceRef out, const int *sel) {
   __shared__ int8_t tile[S][32][36];
   if (oz_db_of<S>(out.db) == 8) {
-    if constexpr (S != 16 && S != 31) slice_cols_body<W, S, 8>(B, rows, cols, fi, out, sel, tile);
+    if constexpr (S != 16 && S != 31)
+      slice_cols_body<W, S, 8>(B, rows, cols, fi, out, sel, tile, blockIdx.y * 32, blockIdx.z);
   } else {
-    if constexpr (S != 14 && S != 28) slice_cols_body<W, S, 7>(B, rows, cols, fi, out, sel, tile);
+    if constexpr (S != 14 && S != 28)
+      slice_cols_body<W, S, 7>(B, rows, cols, fi, out, sel, tile, blockIdx.y * 32, blockIdx.z);
+  }
+}
+
+// Column exponents and digits in one kernel: a CTA owns a strip of 32
+// columns over all K rows (its column maxima first, then the 32 x 32 tiles
+// of the strip; the second read of the strip hits L1/L2).  Saves the
+// separate col_exps pass over the matrix.
+template <int W, int S>
+__global__ void slice_cols_fused_kernel(MatRef B, int rows, int cols, int fi, SliceRef out, const int *sel) {
+  __shared__ int8_t tile[S][32][36];
+  __shared__ double red[8][33];
+  __shared__ int ecs[32];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + tx;
+  const int bz = blockIdx.y;
+  const int b = sel ? sel[bz] : bz;
+  double mx = 0.0;
+  if (j < cols)
+    for (int k = ty; k < rows; k += 8) {
+      const long long off = (long long)b * B.bstride + (long long)k * B.ld + j;
+      mx = fmax(mx, fabs(fi == F32 ? (double)((const float *)B.data)[off] : ((const double *)B.data)[off]));
+    }
+  red[ty][tx] = mx;
+  __syncthreads();
+  if (ty == 0) {
+#pragma unroll
+    for (int g = 1; g < 8; ++g) mx = fmax(mx, red[g][tx]);
+    const int e = row_exponent(mx);
+    ecs[tx] = e;
+    if (j < out.rpad) out.exps[(long long)b * out.rpad + j] = e;
+  }
+  __syncthreads();
+  for (int k0 = 0; k0 < out.kpad; k0 += 32) {
+    if (oz_db_of<S>(out.db) == 8) {
+      if constexpr (S != 16 && S != 31) slice_cols_body<W, S, 8>(B, rows, cols, fi, out, sel, tile, k0, bz, ecs);
+    } else {
+      if constexpr (S != 14 && S != 28) slice_cols_body<W, S, 7>(B, rows, cols, fi, out, sel, tile, k0, bz, ecs);
+    }
+    __syncthreads();    // the tile is rewritten by the next K step
   }
 }
 
