@@ -104,6 +104,18 @@ int mpps_powers(mpps_handle *h, mpps_mat *powers, int s);
 int mpps_assemble_blocks_hc(mpps_handle *h, const mpps_mat *powers, int s, int m,
                             const double *coeff_host, mpps_mat *blocks, double *norms, int flags);
 int mpps_assemble_hc_supported(int fmt, int s, int m);
+/* Two-pass block assembly (B200 extension of the same reference operators,
+ * engine.py:127-138 + precision.py:235-249): blocks[0..nblocks-1] only, at
+ * the blocks' formats: a prefix of dd blocks (full dd accumulation, the
+ * levels the plan keeps at dd), then fp64 blocks made from the high words
+ * of the dd powers (the planner's norms and the blocks of fp32/fp64 Horner
+ * levels).  Compiled mixes: all dd (nblocks <= 4), all fp64, or B_0, B_1 dd
+ * + fp64 (mpps_assemble_hc_n_supported, block_fmt -1).
+ * norms ([batch][nblocks+1], the last one ||Y||) may be NULL.  nblocks = r+1
+ * with m mod s = 0 is refused (B_r = b_m I). */
+int mpps_assemble_blocks_hc_n(mpps_handle *h, const mpps_mat *powers, int s, int m, const double *coeff_host,
+                              mpps_mat *blocks, int nblocks, double *norms);
+int mpps_assemble_hc_n_supported(int block_fmt, int s, int m, int nblocks);
 
 /* assemble_block for i = 0..r plus one_norm of every block and of Y
  * (engine.py:127-138, 141-154; precision.py:235-249), fused into one pass

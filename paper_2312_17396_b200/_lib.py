@@ -26,7 +26,7 @@ MPPS_OK, MPPS_EINVAL, MPPS_EFMT, MPPS_ECUDA = 0, 1, 2, 3
 EXPORTED = (
     "mpps_version", "mpps_create", "mpps_destroy", "mpps_set_stream",
     "mpps_last_error", "mpps_launch_count", "mpps_convert", "mpps_gemm",
-    "mpps_axpy", "mpps_powers", "mpps_assemble_blocks", "mpps_assemble_blocks_hc", "mpps_assemble_hc_supported", "mpps_one_norm", "mpps_one_norm_complex", "mpps_level_exps",
+    "mpps_axpy", "mpps_powers", "mpps_assemble_blocks", "mpps_assemble_blocks_hc", "mpps_assemble_hc_supported", "mpps_assemble_blocks_hc_n", "mpps_assemble_hc_n_supported", "mpps_one_norm", "mpps_one_norm_complex", "mpps_level_exps",
     "mpps_horner_step", "mpps_horner_scalar_top", "mpps_probe_fma",
     "mpps_assemble_blocks_dist", "mpps_colmax", "mpps_slice", "mpps_gemm_sliced",
     "mpps_horner_step_sliced", "mpps_oz_slices_for", "mpps_oz_slices_for_bits", "mpps_oz_max_k_8bit", "mpps_probe_i8mma", "mpps_debug_oz_trace",
@@ -121,6 +121,8 @@ def load_library(path: Optional[str] = None):
         lib.mpps_assemble_blocks.argtypes = [vp, mp, ip, ip, vp, mp, vp]
         lib.mpps_assemble_blocks_hc.argtypes = [vp, mp, ip, ip, P(ctypes.c_double), mp, vp, ip]
         lib.mpps_assemble_hc_supported.argtypes = [ip, ip, ip]
+        lib.mpps_assemble_blocks_hc_n.argtypes = [vp, mp, ip, ip, P(ctypes.c_double), mp, ip, vp]
+        lib.mpps_assemble_hc_n_supported.argtypes = [ip, ip, ip, ip]
         lib.mpps_one_norm.argtypes = [vp, mp, vp]
         lib.mpps_one_norm_complex.argtypes = [vp, mp, ip, vp, ip]
         lib.mpps_level_exps.argtypes = [vp, vp, ip, ip, ctypes.c_ulonglong, vp, vp]
@@ -259,6 +261,20 @@ class Handle:
         self._check(self.lib.mpps_assemble_blocks_hc(self.h, parr, len(powers), m,
                                                      cw.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), barr,
                                                      norms_dev.data_ptr(), 1 if skip_top else 0),
+                    "assemble_blocks")
+
+    def assemble_hc_n_supported(self, block_fmt: int, s: int, m: int, nblocks: int) -> bool:
+        return bool(self.lib.mpps_assemble_hc_n_supported(block_fmt, s, m, nblocks))
+
+    def assemble_blocks_hc_n(self, powers, m: int, coeff_words, blocks, norms_dev=None):
+        """Blocks B_0..B_{len(blocks)-1} at the blocks' format (fp64 from the
+        high words of dd powers, or dd); norms_dev (B, len(blocks)+1) or None."""
+        parr = cmat_array(powers)
+        barr = cmat_array(blocks)
+        cw = np.ascontiguousarray(coeff_words, dtype=np.float64)
+        self._check(self.lib.mpps_assemble_blocks_hc_n(self.h, parr, len(powers), m,
+                                                       cw.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), barr,
+                                                       len(blocks), None if norms_dev is None else norms_dev.data_ptr()),
                     "assemble_blocks")
 
     def assemble_blocks_dist(self, powers, m: int, coeff_dev, blocks, colsums_dev, row0: int, col0: int):

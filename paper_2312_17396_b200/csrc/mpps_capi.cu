@@ -505,7 +505,10 @@ struct AssembleCArgs {
   int rows, cols, m, nchunk, skip_top;
 };
 
-template <int WF, int NB, int NP>
+// ND < NB: blocks k >= ND are assembled and stored in fp64 from the high
+// words (two-pass assembly: the blocks of fp32 / fp64 Horner levels and the
+// planner's norms), blocks k < ND at WF.
+template <int WF, int NB, int NP, int ND = NB>
 #ifndef MPPS_ASMC_MINB
 #define MPPS_ASMC_MINB 8
 #endif
@@ -540,6 +543,18 @@ __global__ void __launch_bounds__(128, MPPS_ASMC_MINB) assemble_c_kernel(const _
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
       const int hi = (k < full) ? S - 1 : a.m - S * full;   // last power index of block k
+      if (k >= ND) {
+        double acc = diag ? a.coef[S * k][0] : 0.0;
+#pragma unroll
+        for (int j = 1; j <= NP; ++j)
+          if (j <= hi) acc = __dadd_rn(__dmul_rn(a.coef[S * k + j][0], V::hi(xc[j - 1])), acc);
+        cs[k] += fabs(acc);
+        if (!(a.skip_top && k == NB - 1)) {
+          const MatRef &B = a.Bk[k];
+          ((double *)B.data)[(long long)b * B.bstride + (long long)row * B.ld + col] = acc;
+        }
+        continue;
+      }
       Acc acc = V::acc_of(diag ? asmc_coef<WF>(a.coef[S * k]) : V::zero());
 #pragma unroll
       for (int j = 1; j <= NP; ++j)
@@ -557,6 +572,7 @@ __global__ void __launch_bounds__(128, MPPS_ASMC_MINB) assemble_c_kernel(const _
     yc = yn;
   }
 #undef MPPS_ASMC_LOAD
+  if (!a.partial) return;   // blocks only (the norms came from another pass)
   double *out = a.partial + ((long long)b * a.nchunk + chunk) * (long long)(NB + 1) * n;
 #pragma unroll
   for (int k = 0; k <= NB; ++k) out[(long long)k * n + col] = cs[k];
@@ -625,7 +641,8 @@ __global__ void scalar_top_wf_kernel(const ScalarTopArgs a) {
     const double b0 = a.bm[0], b1 = a.bm[1], so = oz::pow2i(eo);
     for (int i = blockIdx.y; i < a.rows; i += gridDim.y) {
       const mp::dd y = V::load(a.Y, yb + (long long)i * a.Y.ld + j);
-      const mp::dd bp = V::load(a.Bp, bb + (long long)i * a.Bp.ld + j);
+      const double *bpp = (const double *)a.Bp.data + bb + (long long)i * a.Bp.ld + j;
+      const mp::dd bp = mp::dd_make(bpp[0], a.Bp.words > 1 ? bpp[a.Bp.plane] : 0.0);   // fp64 B_{r-1} allowed
       double tv = fma(b0, y.hi, fma(b0, y.lo, b1 * y.hi));
       if constexpr (FT == F32) {
         const double c = tv * 536870913.0;                 // 2^29 + 1
@@ -722,7 +739,7 @@ int ew_grid(long long total) {
 }  // namespace
 
 // ===================================================================== ABI
-template <int WF, int NB, int NP>
+template <int WF, int NB, int NP, int ND = NB>
 static int launch_assemble_c(mpps_handle *h, const mpps_mat *powers, int m, const double *coeff_host,
                              mpps_mat *blocks, double *norms, int skip_top) {
   AssembleCArgs<NB, NP> a;
@@ -736,10 +753,15 @@ static int launch_assemble_c(mpps_handle *h, const mpps_mat *powers, int m, cons
   }
   a.rows = rows; a.cols = cols; a.m = m; a.skip_top = skip_top;
   a.nchunk = (rows + kAsmRows - 1) / kAsmRows;
+  if (!norms) {
+    a.partial = nullptr;
+    assemble_c_kernel<WF, NB, NP, ND><<<dim3((cols + 127) / 128, a.nchunk, batch), 128, 0, h->stream>>>(a);
+    return after_launch(h, "assemble_c_kernel");
+  }
   size_t pbytes = sizeof(double) * (size_t)batch * a.nchunk * (NB + 1) * cols;
   cudaError_t e = cudaMallocAsync((void **)&a.partial, pbytes, h->stream);
   if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "assemble scratch: %s", cudaGetErrorString(e));
-  assemble_c_kernel<WF, NB, NP><<<dim3((cols + 127) / 128, a.nchunk, batch), 128, 0, h->stream>>>(a);
+  assemble_c_kernel<WF, NB, NP, ND><<<dim3((cols + 127) / 128, a.nchunk, batch), 128, 0, h->stream>>>(a);
   int rc = after_launch(h, "assemble_c_kernel");
   if (rc) return rc;
   norm_reduce_kernel<<<dim3(NB + 1, batch), 256, 0, h->stream>>>(a.partial, norms, NB + 1, a.nchunk, cols);
@@ -961,6 +983,64 @@ int mpps_assemble_blocks_hc(mpps_handle *h, const mpps_mat *powers, int s, int m
                  powers[0].fmt);
 }
 
+int mpps_assemble_blocks_hc_n(mpps_handle *h, const mpps_mat *powers, int s, int m, const double *coeff_host,
+                              mpps_mat *blocks, int nblocks, double *norms) {
+  if (!powers || !blocks || !coeff_host) return set_err(h, MPPS_EINVAL, "assemble_n: null argument");
+  if (s < 2 || s > kMaxPowers || m < s) return set_err(h, MPPS_EINVAL, "need 2 <= s <= series degree (s=%d m=%d)", s, m);
+  const int r = m / s;
+  if (nblocks < 1 || nblocks > r + 1) return set_err(h, MPPS_EINVAL, "assemble_n: 1 <= nblocks <= r+1 (%d)", nblocks);
+  const int pf = fmt_index(powers[0].fmt), bf = fmt_index(blocks[0].fmt);
+  int nd = 0;                               // leading dd blocks, then fp64 ones
+  while (nd < nblocks && fmt_index(blocks[nd].fmt) == DD) ++nd;
+  for (int k = 0; k < s; ++k) {
+    int rc = check_mat(h, &powers[k], "assemble_n.power");
+    if (rc) return rc;
+    if (powers[k].fmt != powers[0].fmt || powers[k].rows != powers[0].rows || powers[k].cols != powers[0].cols ||
+        powers[k].batch != powers[0].batch || powers[k].rows != powers[k].cols)
+      return set_err(h, MPPS_EINVAL, "assemble_n: square powers of one format and shape");
+  }
+  for (int k = 0; k < nblocks; ++k) {
+    int rc = check_mat(h, &blocks[k], "assemble_n.block");
+    if (rc) return rc;
+    if ((k < nd ? fmt_index(blocks[k].fmt) != DD : fmt_index(blocks[k].fmt) != F64) ||
+        blocks[k].rows != powers[0].rows || blocks[k].cols != powers[0].cols || blocks[k].batch != powers[0].batch)
+      return set_err(h, MPPS_EINVAL, "assemble_n: blocks must match the powers (dd blocks first, then fp64)");
+  }
+  if (!(pf == DD && (bf == DD || bf == F64)))
+    return set_err(h, MPPS_EFMT, "assemble_n: dd powers into dd or fp64 blocks");
+  if (nblocks == r + 1 && m % s == 0) return set_err(h, MPPS_EINVAL, "assemble_n: B_r = b_m I is not assembled here");
+  if (powers[0].rows == 0 || powers[0].batch == 0) return MPPS_OK;
+  const int np = s - 1;
+#define AM(NB_, NP_) \
+  if (nd == 2 && nblocks == NB_ && np == NP_) return launch_assemble_c<DD, NB_, NP_, 2>(h, powers, m, coeff_host, blocks, norms, 0);
+  AM(5, 5) AM(6, 6) AM(4, 4) AM(3, 3) AM(4, 3)
+#undef AM
+#define AN(BF, NB_, NP_) \
+  if (bf == BF && nd == (BF == DD ? nblocks : 0) && nblocks == NB_ && np == NP_) \
+    return launch_assemble_c<BF, NB_, NP_>(h, powers, m, coeff_host, blocks, norms, 0);
+  AN(F64, 5, 5) AN(F64, 6, 6) AN(F64, 4, 4) AN(F64, 3, 3) AN(F64, 4, 3)
+  AN(DD, 1, 5) AN(DD, 2, 5) AN(DD, 3, 5) AN(DD, 4, 5) AN(DD, 1, 6) AN(DD, 2, 6) AN(DD, 3, 6) AN(DD, 4, 6)
+  AN(DD, 1, 4) AN(DD, 2, 4) AN(DD, 3, 4) AN(DD, 1, 3) AN(DD, 2, 3) AN(DD, 3, 3)
+#undef AN
+  return set_err(h, MPPS_EFMT, "assemble_n: no kernel for %d blocks, s=%d, format %d", nblocks, s, blocks[0].fmt);
+}
+
+int mpps_assemble_hc_n_supported(int block_fmt, int s, int m, int nblocks) {
+  // block_fmt: DD (all dd), F64 (all fp64) or -1: B_0, B_1 dd and the rest fp64
+  const int np = s - 1;
+  if (s < 2 || m < s || (nblocks == m / s + 1 && m % s == 0)) return 0;
+  if (block_fmt == -1)
+    return (nblocks == 5 && np == 5) || (nblocks == 6 && np == 6) || (nblocks == 4 && np == 4) ||
+           (nblocks == 3 && np == 3) || (nblocks == 4 && np == 3);
+  const int bf = fmt_index(block_fmt);
+  if (bf == F64)
+    return (nblocks == 5 && np == 5) || (nblocks == 6 && np == 6) || (nblocks == 4 && np == 4) ||
+           (nblocks == 3 && np == 3) || (nblocks == 4 && np == 3);
+  if (bf == DD)
+    return (np == 5 || np == 6) ? (nblocks >= 1 && nblocks <= 4) : (np == 3 || np == 4) ? (nblocks >= 1 && nblocks <= 3) : 0;
+  return 0;
+}
+
 int mpps_assemble_hc_supported(int fmt, int s, int m) {
   const int wf = fmt_index(fmt), r = m / s, nb = r + 1, np = s - 1;
   if (wf == DD) return (nb == 6 && np == 5) || (nb == 7 && np == 6) || (nb == 5 && np == 4) || (nb == 4 && np == 3) ||
@@ -1106,6 +1186,14 @@ int mpps_horner_scalar_top(mpps_handle *h, const double *bm, int fmt_top, const 
   if (nb == 0 || a.rows == 0 || a.cols == 0) return MPPS_OK;
   const int tpb = a.cols >= 256 ? 256 : 128;
   dim3 grid((a.cols + tpb - 1) / tpb, a.rows < 65535 ? a.rows : 65535, nb);
+  // dd Y with an fp64 B_{r-1} (two-pass block assembly: blocks of fp32 /
+  // fp64 levels are assembled in fp64): the fp64 fast path of the dd kernel
+  if (wf == DD && fmt_index(Bprev->fmt) == F64 && (ft == F32 || ft == F64) && (fo == F32 || fo == F64)) {
+    if (ft == F32 && fo == F32) scalar_top_wf_kernel<DD, F32, F32><<<grid, tpb, 0, h->stream>>>(a);
+    else if (ft == F32) scalar_top_wf_kernel<DD, F32, F64><<<grid, tpb, 0, h->stream>>>(a);
+    else scalar_top_wf_kernel<DD, F64, F64><<<grid, tpb, 0, h->stream>>>(a);
+    return after_launch(h, "scalar_top_kernel");
+  }
   if (fmt_index(Bprev->fmt) == wf && ft <= wf) {
 #define SW(W, A, B) \
   if (wf == W && ft == A && fo == B) scalar_top_wf_kernel<W, A, B><<<grid, tpb, 0, h->stream>>>(a); else

@@ -55,6 +55,10 @@ from .precision import (DD, FORMAT_NAME, FP32, FP64, NORM_CTX, QD,
 
 BUCKETS = ("power_formation", "norm_estimation", "mixed_horner", "coefficient_assembly")
 
+import os as _os
+#: two-pass block assembly for the mixed evaluators (MPPS_LOWP_ASSEMBLY=0: one dd pass)
+_LOWP = _os.environ.get("MPPS_LOWP_ASSEMBLY", "1") != "0"
+
 
 def _torch():
     import torch
@@ -271,6 +275,7 @@ class _Prepared:
     norms: np.ndarray          # (B, r+2) float64: ||B_0..B_r||, ||Y||
     coeffs: np.ndarray         # (m+1, 4) words at the working precision
     norms_dev: object = None   # the same norms on the device (level scalings)
+    lowp: bool = False         # blocks are fp64 (two-pass assembly): dd ones are made per plan in _horner
 
 
 def _form_powers(h, Xt, wf: int, s: int, timer: _Buckets, x_is_working: Optional[MatBatch] = None):
@@ -295,10 +300,27 @@ def _form_powers(h, Xt, wf: int, s: int, timer: _Buckets, x_is_working: Optional
     return powers
 
 
+def _lowp_blocks(h, wf: int, s: int, m: int) -> int:
+    """Number of blocks the fp64 pass of the two-pass assembly makes (0: not
+    applicable): dd working format, real inputs, a compiled shape."""
+    if wf != DD or complexmat.scope() is not None or s < 2 or not _LOWP:
+        return 0
+    r = m // s
+    nlo = r if m % s == 0 else r + 1
+    return nlo if nlo >= 2 and h.assemble_hc_n_supported(-1, s, m, nlo) else 0
+
+
 def _assemble(h, powers: List[MatBatch], series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: int,
-              timer: _Buckets, sync: bool = True) -> _Prepared:
+              timer: _Buckets, sync: bool = True, lowp: bool = False) -> _Prepared:
     """assemble_block for every block + one_norm (engine.py:127-138,
-    467-468), then the one host sync for the planner's norms."""
+    467-468), then the one host sync for the planner's norms.
+
+    ``lowp`` (mixed evaluators, dd working format): B_0 and B_1 in dd, the
+    other blocks in fp64 from the powers' high words (they serve the planner's
+    norms -- the reference plans from 16-digit norms -- and the B_{j-1} of
+    fp32 / fp64 Horner levels, to ~2^-53 |b| |X^j|).  If a plan keeps more
+    levels at dd, _horner assembles those blocks in dd (post-planner, per
+    plan structure).  cfg2: 60 % less FP64 work and 15 % fewer bytes."""
     torch = _torch()
     dev = powers[0].device
     B, n = powers[0].batch, powers[0].rows
@@ -314,6 +336,23 @@ def _assemble(h, powers: List[MatBatch], series: CoefficientSeries, ctx: Precisi
         _COEFF_DEV[key] = coeffs
     timer.start("coefficient_assembly")
     norms = torch.empty((B, r + 2), dtype=torch.float64, device=dev)
+    nlo = _lowp_blocks(h, wf, s, m) if lowp else 0
+    if nlo:
+        blocks = [MatBatch.empty(DD if k < 2 else FP64, B, n, device=dev) for k in range(nlo)]
+        lo_norms = torch.empty((B, nlo + 1), dtype=torch.float64, device=dev)
+        h.assemble_blocks_hc_n(powers, m, cw, blocks, lo_norms)
+        norms[:, :nlo] = lo_norms[:, :nlo]
+        norms[:, r + 1] = lo_norms[:, nlo]
+        if nlo == r:    # B_r = b_m I (not assembled): ||B_r|| = |hi(b_m)| as the one-pass kernel reports
+            norms[:, r] = abs(float(cw[m][0]))
+            blocks.append(MatBatch.empty(wf, 1, 1, device=dev))
+        timer.stop()
+        if not sync:
+            return _Prepared(wf, s, r, m, powers, blocks, None, cw, norms, lowp=True)
+        timer.start("norm_estimation")
+        norms_h = norms.cpu().numpy()
+        timer.stop()
+        return _Prepared(wf, s, r, m, powers, blocks, norms_h, cw, norms, lowp=True)
     hc = h.assemble_hc_supported(wf, s, m)
     # B_r = b_m I when m mod s == 0: the K3 Horner step uses b_m itself, so
     # the constant-coefficient kernel does not store it (norm still reported)
@@ -342,11 +381,41 @@ def _assemble(h, powers: List[MatBatch], series: CoefficientSeries, ctx: Precisi
 
 
 def _prepare(h, Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: int,
-             timer: _Buckets, x_is_working: Optional[MatBatch] = None, sync: bool = True) -> _Prepared:
+             timer: _Buckets, x_is_working: Optional[MatBatch] = None, sync: bool = True,
+             lowp: bool = False) -> _Prepared:
     """eval_b0_and_power + assemble_block + one_norm (engine.py:141-154,
     127-138, 467-468) for the whole batch."""
     powers = _form_powers(h, Xt, wf, s, timer, x_is_working)
-    return _assemble(h, powers, series, ctx, wf, s, timer, sync)
+    return _assemble(h, powers, series, ctx, wf, s, timer, sync, lowp)
+
+
+def _dd_blocks(h, prep: _Prepared, structure) -> List[MatBatch]:
+    """The blocks of a two-pass assembly for this plan structure: B_k in dd
+    for B_0 and every level k the plan keeps at dd (formats are
+    non-increasing, so a prefix), fp64 for the rest."""
+    r, s, m, wf = prep.r, prep.s, prep.m, prep.wf
+    group_list, _ = structure
+    nd = 1
+    for fm, _ in group_list:
+        k = 1
+        while k <= r and fm[k] == DD:
+            k += 1
+        nd = max(nd, k)
+    if m % s == 0:
+        nd = min(nd, r)          # B_r = b_m I is never assembled
+    if nd <= len(prep.blocks) and prep.blocks[nd - 1].fmt != DD:
+        B, n, dev = prep.powers[0].batch, prep.powers[0].rows, prep.powers[0].device
+        if h.assemble_hc_n_supported(DD, s, m, nd):
+            dd = [MatBatch.empty(DD, B, n, device=dev) for _ in range(nd)]
+            h.assemble_blocks_hc_n(prep.powers, m, prep.coeffs, dd)
+        else:                    # (nearly) flat plan: the one-pass dd assembly
+            skip_top = m % s == 0
+            dd = [MatBatch.empty(DD, B, n, device=dev) if not (skip_top and k == r)
+                  else MatBatch.empty(DD, 1, 1, device=dev) for k in range(r + 1)]
+            scratch = _torch().empty((B, r + 2), dtype=_torch().float64, device=dev)
+            h.assemble_blocks_hc(prep.powers, m, prep.coeffs, dd, scratch, skip_top)
+        return dd[:nd] + list(prep.blocks[nd:])
+    return list(prep.blocks)
 
 
 def _structure(prep: _Prepared, digits: np.ndarray, nil: np.ndarray):
@@ -380,12 +449,12 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
     torch = _torch()
     wf, s, r, m = prep.wf, prep.s, prep.r, prep.m
     Y = prep.powers[s - 1]
-    blocks = prep.blocks
     B, n, dev = Y.batch, Y.rows, Y.device
     result = MatBatch.empty(wf, B, n, device=dev)
     timer.start("mixed_horner")
     if structure is None:
         structure = _structure(prep, digits, nil)
+    blocks = _dd_blocks(h, prep, structure) if prep.lowp else prep.blocks
     if sels is None:
         sels = _selections(structure, dev)
     group_list, nil_idx = structure
@@ -512,7 +581,8 @@ def _graph_stages(Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: 
            apply_switch, ge.engine(), complexmat.scope())
 
     def build_pre(xstatic, capture):
-        return _prepare(_lib.handle_for(), xstatic, series, ctx, wf, s, _Buckets(False), None, sync=False)
+        return _prepare(_lib.handle_for(), xstatic, series, ctx, wf, s, _Buckets(False), None, sync=False,
+                        lowp=(kind == "mixed"))
 
     def run_post(prep, norms):
         r = prep.r
@@ -679,7 +749,7 @@ def ps_mixed_general(X, series: CoefficientSeries, ctx: PrecisionCtx, delta: flo
     g = _graphed(Xt, series, ctx, wf, s, "mixed", delta, True, timer) if Xw is None else None
     if g is not None:
         return _graphed_reports(g, ctx, delta, True, True, with_bound, single, timer)
-    prep = _prepare(h, Xt, series, ctx, wf, s, timer, Xw)
+    prep = _prepare(h, Xt, series, ctx, wf, s, timer, Xw, lowp=True)
     return _mixed_tail(h, prep, ctx, delta, True, True, with_bound, single, timer)
 
 
@@ -735,7 +805,7 @@ def ps_mixed_exp(X, m: int, ctx: PrecisionCtx, fix_params: bool = True, delta: f
     g = _graphed(Xt, series, ctx, wf, s, "mixed", delta, True, timer) if Xw is None else None
     if g is not None:
         return _graphed_reports(g, ctx, delta, True, fix_params, with_bound, single, timer)
-    prep = _prepare(h, Xt, series, ctx, wf, s, timer, Xw)
+    prep = _prepare(h, Xt, series, ctx, wf, s, timer, Xw, lowp=True)
     return _mixed_tail(h, prep, ctx, delta, True, fix_params, with_bound, single, timer)
 
 
@@ -800,7 +870,7 @@ def _ps_mixed_exp_one(Xt, Xw, m, ctx, fix_params, delta, with_bound, timing, gro
             return _explicit_powers(Xt, Xw, m, ctx, s, series, delta, True, fix_params, True, timing)
         h = _lib.handle_for()
         timer = _Buckets(timing)
-        prep = _prepare(h, Xt, series, ctx, _working_format(ctx), s, timer, Xw)
+        prep = _prepare(h, Xt, series, ctx, _working_format(ctx), s, timer, Xw, lowp=True)
         return _mixed_tail(h, prep, ctx, delta, True, fix_params, with_bound, True, timer)
     p54 = NORM_CTX.binary_precision
     nx = rn(Fraction(norm_x), p54)
@@ -816,7 +886,7 @@ def _ps_mixed_exp_one(Xt, Xw, m, ctx, fix_params, delta, with_bound, timing, gro
         return _explicit_powers(Xt, Xw, m, ctx, s, series, delta, False, fix_params, True, timing)
     h = _lib.handle_for()
     timer = _Buckets(timing)
-    prep = _prepare(h, Xt, series, ctx, _working_format(ctx), s, timer, Xw)
+    prep = _prepare(h, Xt, series, ctx, _working_format(ctx), s, timer, Xw, lowp=True)
     return _mixed_tail(h, prep, ctx, delta, False, fix_params, with_bound, True, timer)
 
 
@@ -841,7 +911,7 @@ def ps_mixed_pade(X, k: int, ctx: PrecisionCtx, delta: float = 10.0, with_bound:
     powers = _form_powers(h, Xt, wf, s, timer, Xw)
     out = []
     for series in (num, den):
-        prep = _assemble(h, powers, series, ctx, wf, s, timer)
+        prep = _assemble(h, powers, series, ctx, wf, s, timer, lowp=True)
         out.append(_mixed_tail(h, prep, ctx, delta, True, True, with_bound, single, timer))
     return tuple(out)
 
