@@ -1280,14 +1280,18 @@ extern "C" int mpps_slice(mpps_handle *h, const mpps_mat *src, int side, mpps_sl
     return set_err(h, MPPS_EINVAL, "slice: digit_bits must be 7 or 8");
   if (slice_db(out) == 7 && S != 4 && S != 8 && S != 16 && S != 31)
     return set_err(h, MPPS_EINVAL, "slice: 4, 8, 16 or 31 digit planes of 7 bits");
-  if (slice_db(out) == 8 && S != 4 && S != 8 && S != 14 && S != 28)
-    return set_err(h, MPPS_EINVAL, "slice: 4, 8, 14 or 28 digit planes of 8 bits");
+  if (slice_db(out) == 8 && S != 2 && S != 3 && S != 4 && S != 5 && S != 6 && S != 8 && S != 10 && S != 12 && S != 14 &&
+      S != 28)
+    return set_err(h, MPPS_EINVAL, "slice: 2, 3, 4, 5, 6, 8, 10, 12, 14 or 28 digit planes of 8 bits");
+  if (slice_db(out) == 7 && (S == 2 || S == 3 || S == 5 || S == 6 || S == 10 || S == 12))
+    return set_err(h, MPPS_EINVAL, "slice: %d planes exist only with 8-bit digits", S);
   if (side == 0) {
     dim3 grid((out->rpad * 32 + 255) / 256, nb);
 #define SR(WW, SS) \
   if (W == WW && S == SS) oz::slice_rows_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
     SR(1, 4) SR(1, 8) SR(1, 14) SR(1, 16) SR(1, 28) SR(1, 31) SR(2, 4) SR(2, 8) SR(2, 14) SR(2, 16) SR(2, 28)
     SR(2, 31) SR(4, 4) SR(4, 8) SR(4, 14) SR(4, 16) SR(4, 28) SR(4, 31) {}
+    // per-level plane counts are column-side (phi) only
 #undef SR
     return after_launch(h, "slice_rows_kernel");
   }
@@ -1307,7 +1311,8 @@ extern "C" int mpps_slice(mpps_handle *h, const mpps_mat *src, int side, mpps_sl
 #define SC(WW, SS) \
   if (W == WW && S == SS) oz::slice_cols_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
   SC(1, 4) SC(1, 8) SC(1, 14) SC(1, 16) SC(1, 28) SC(1, 31) SC(2, 4) SC(2, 8) SC(2, 14) SC(2, 16) SC(2, 28)
-  SC(2, 31) SC(4, 4) SC(4, 8) SC(4, 14) SC(4, 16) SC(4, 28) SC(4, 31) {}
+  SC(2, 31) SC(4, 4) SC(4, 8) SC(4, 14) SC(4, 16) SC(4, 28) SC(4, 31)
+  SC(1, 2) SC(1, 3) SC(1, 5) SC(1, 6) SC(2, 2) SC(2, 3) SC(2, 5) SC(2, 6) SC(2, 10) SC(2, 12) {}
 #undef SC
   return after_launch(h, "slice_cols_kernel");
 }
@@ -1384,6 +1389,14 @@ static int dispatch_oz_tma(mpps_handle *h, int S, int fo, int mode, const oz::Oz
   if (oz_ring_ew() == 16 && S == 8 && mode == 1) {
     if (fo == DD) return launch_oz_tma<8, 32, DD, 1, 16>(h, a, nb);
     if (fo == F64) return launch_oz_tma<8, 32, F64, 1, 16>(h, a, nb);
+  }
+  // per-level plane counts of the Horner chain (8-bit digits): S <= 3 two
+  // CTAs per SM, larger S one CTA per SM with 16 epilogue warps
+  if (mode == 1) {
+#define OZL(SS, FF, EWW) if (S == SS && fo == FF) return launch_oz_tma<SS, 32, FF, 1, EWW>(h, a, nb);
+    OZL(2, F32, 8) OZL(2, F64, 8) OZL(2, DD, 8) OZL(3, F32, 8) OZL(3, F64, 8) OZL(3, DD, 8)
+    OZL(5, F64, 16) OZL(5, DD, 16) OZL(6, F64, 16) OZL(6, DD, 16) OZL(10, DD, 16) OZL(12, DD, 16)
+#undef OZL
   }
 #define OZ(SS, NT, FF, MM) if (S == SS && fo == FF && mode == MM) return launch_oz_tma<SS, NT, FF, MM>(h, a, nb);
   OZ(4, 32, F32, 0) OZ(4, 32, F32, 1) OZ(4, 32, F64, 1) OZ(4, 32, DD, 1) OZ(4, 32, QD, 1)

@@ -148,8 +148,14 @@ struct SliceRef {
 // 8-bit digits, 16 / 31 only as 7-bit ones; 4 and 8 planes are prefixes of
 // either split (the operands' SliceRef.db, equal for A and B).
 template <int S>
+__host__ __device__ constexpr bool oz_has7() {   // a 7-bit variant exists
+  return !(S == 14 || S == 28 || S == 2 || S == 3 || S == 5 || S == 6 || S == 10 || S == 12);
+}
+template <int S>
 __device__ __forceinline__ int oz_db_of(int db) {
-  if constexpr (S == 14 || S == 28) return 8;
+  // 14 / 28 and the per-level plane counts of the 8-bit split (2, 3, 5, 6,
+  // 10, 12) exist only with 8-bit digits
+  if constexpr (S == 14 || S == 28 || S == 2 || S == 3 || S == 5 || S == 6 || S == 10 || S == 12) return 8;
   else if constexpr (S == 16 || S == 31) return 7;
   else return db == 8 ? 8 : 7;
 }
@@ -467,7 +473,7 @@ __global__ void slice_rows_kernel(MatRef A, int rows, int cols, int fi, SliceRef
   if (oz_db_of<S>(out.db) == 8) {
     if constexpr (S != 16 && S != 31) slice_rows_body<W, S, 8>(A, rows, cols, fi, out, sel);
   } else {
-    if constexpr (S != 14 && S != 28) slice_rows_body<W, S, 7>(A, rows, cols, fi, out, sel);
+    if constexpr (oz_has7<S>()) slice_rows_body<W, S, 7>(A, rows, cols, fi, out, sel);
   }
 }
 
@@ -552,7 +558,7 @@ __global__ void slice_cols_kernel(MatRef B, int rows, int cols, int fi, SliceRef
     if constexpr (S != 16 && S != 31)
       slice_cols_body<W, S, 8>(B, rows, cols, fi, out, sel, tile, blockIdx.y * 32, blockIdx.z);
   } else {
-    if constexpr (S != 14 && S != 28)
+    if constexpr (oz_has7<S>())
       slice_cols_body<W, S, 7>(B, rows, cols, fi, out, sel, tile, blockIdx.y * 32, blockIdx.z);
   }
 }
@@ -590,7 +596,7 @@ __global__ void slice_cols_fused_kernel(MatRef B, int rows, int cols, int fi, Sl
     if (oz_db_of<S>(out.db) == 8) {
       if constexpr (S != 16 && S != 31) slice_cols_body<W, S, 8>(B, rows, cols, fi, out, sel, tile, k0, bz, ecs);
     } else {
-      if constexpr (S != 14 && S != 28) slice_cols_body<W, S, 7>(B, rows, cols, fi, out, sel, tile, k0, bz, ecs);
+      if constexpr (oz_has7<S>()) slice_cols_body<W, S, 7>(B, rows, cols, fi, out, sel, tile, k0, bz, ecs);
     }
     __syncthreads();    // the tile is rewritten by the next K step
   }
@@ -948,7 +954,7 @@ __device__ __forceinline__ void oz_epilogue_db(const Args &args, const EpiPre<S,
     if constexpr (S != 16 && S != 31)
       oz_epilogue<S, NT, FO, MODE, 8>(args, pre, tmem, quarter, c_begin, c_end, b, m0, n0, lane);
   } else {
-    if constexpr (S != 14 && S != 28)
+    if constexpr (oz_has7<S>())
       oz_epilogue<S, NT, FO, MODE, 7>(args, pre, tmem, quarter, c_begin, c_end, b, m0, n0, lane);
   }
 }
@@ -1216,7 +1222,7 @@ __device__ __forceinline__ void oz_kernel_epilogue(const OzTmaArgs &args, double
       if constexpr (S != 16 && S != 31)
         oz_stage_compute<S, NT, FO, MODE, 8, SCW>(args, ebuf, ebs, tmem, quarter, cb, ce, b, m0, lane);
     } else {
-      if constexpr (S != 14 && S != 28)
+      if constexpr (oz_has7<S>())
         oz_stage_compute<S, NT, FO, MODE, 7, SCW>(args, ebuf, ebs, tmem, quarter, cb, ce, b, m0, lane);
     }
     __syncthreads();

@@ -396,7 +396,7 @@ def _dd_blocks(h, prep: _Prepared, structure) -> List[MatBatch]:
     r, s, m, wf = prep.r, prep.s, prep.m, prep.wf
     group_list, _ = structure
     nd = 1
-    for fm, _ in group_list:
+    for (fm, _st), _ in group_list:
         k = 1
         while k <= r and fm[k] == DD:
             k += 1
@@ -419,16 +419,28 @@ def _dd_blocks(h, prep: _Prepared, structure) -> List[MatBatch]:
 
 
 def _structure(prep: _Prepared, digits: np.ndarray, nil: np.ndarray):
-    """Batch members grouped by level-format tuple, plus the nilpotent ones."""
-    groups: Dict[Tuple[int, ...], List[int]] = {}
+    """Batch members grouped by (level formats, level digit planes), plus the
+    nilpotent ones.  The planes of every level's tensor-core GEMM follow the
+    member's own planned digits (gemm_engine.planes_for_digits), so a matrix
+    gets the same bits alone or inside any batch (batch invariance)."""
+    groups: Dict[Tuple, List[int]] = {}
     nil_idx = []
-    for b in range(len(digits)):
-        if nil[b]:
+    tc = prep.wf in (FP64, DD) and ge.uses_tc(prep.wf)
+    h = _lib.handle_for() if tc else None
+    db = ge.digit_bits_for(h, prep.powers[0].rows) if tc else None
+    memo = {}
+    nil_l = np.asarray(nil, dtype=bool).tolist()
+    for b, dg in enumerate(map(tuple, np.asarray(digits).tolist())):
+        if nil_l[b]:
             nil_idx.append(b)
-        else:
-            fm = (prep.wf,) + formats_of_digits(tuple(int(x) for x in digits[b]))
-            groups.setdefault(fm, []).append(b)
-    return tuple((fm, tuple(mem)) for fm, mem in groups.items()), tuple(nil_idx)
+            continue
+        key = memo.get(dg)
+        if key is None:
+            fm = (prep.wf,) + formats_of_digits(dg)
+            st = tuple(ge.planes_for_digits(h, fm[j], dg[j - 1], db) for j in range(1, prep.r + 1)) if tc else ()
+            key = memo[dg] = (fm, st)
+        groups.setdefault(key, []).append(b)
+    return tuple((key, tuple(mem)) for key, mem in groups.items()), tuple(nil_idx)
 
 
 def _selections(structure, dev):
@@ -437,7 +449,7 @@ def _selections(structure, dev):
     torch = _torch()
     groups, nil_idx = structure
     whole = len(groups) == 1 and not nil_idx
-    sels = {fm: (None if whole else to_device_async(mem, torch.int32, dev)) for fm, mem in groups}
+    sels = {key: (None if whole else to_device_async(mem, torch.int32, dev)) for key, mem in groups}
     sels["nil"] = to_device_async(nil_idx, torch.int64, dev) if nil_idx else None
     return sels
 
@@ -466,8 +478,9 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
     ws = _Workspace(B, n, dev)
     scalar_top = (m % s == 0)
     bm_words = prep.coeffs[m]
-    for fm, members in groups.items():
-        sel = sels[fm]
+    for key, members in groups.items():
+        fm, st = key
+        sel = sels[key]
         exps = exp_y = None
         if FP32 in fm:
             # exact power-of-two level scalings, computed on the device from
@@ -514,8 +527,9 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
             j0 = r
         for j in range(j0, 0, -1):
             out = result if j - 1 == 0 else ws.next(fm[j - 1])
-            ge.horner(h, ys[fm[j]], ge.prepare(h, phi, 1, fm[j], sel), fm[j], blocks[j - 1], out, sel,
-                      exp_y if fm[j] == FP32 else None, ex(j), ex(j - 1))
+            ns = st[j - 1] if st else None       # this level's digit planes
+            ge.horner(h, ys[fm[j]], ge.prepare(h, phi, 1, fm[j], sel, nslices=ns), fm[j], blocks[j - 1], out, sel,
+                      exp_y if fm[j] == FP32 else None, ex(j), ex(j - 1), nslices=ns)
             phi = out
     timer.stop()
     return result
@@ -563,6 +577,12 @@ def _reports(result: MatBatch, plan_fns, executed, counts_mode, sec, with_bound,
     if single:
         return reps[0]
     return BatchReport(reps, result, sec)
+
+
+def _plan_fn_list(row, r, ctx, delta, s, apply_switch, fix_params):
+    """_plan_fn for a row of python floats."""
+    nb, ny = tuple(row[:r + 1]), row[r + 1]
+    return lambda: plan_precisions(nb, ny, ctx, delta, s=s, apply_switch=apply_switch, fix_params=fix_params)
 
 
 def _plan_fn(norms_row, r, ctx, delta, s, apply_switch, fix_params):
@@ -812,9 +832,12 @@ def ps_mixed_exp(X, m: int, ctx: PrecisionCtx, fix_params: bool = True, delta: f
 def _graphed_reports(g, ctx, delta, apply_switch, fix_params, with_bound, single, timer):
     prep, digits, nu, nil, result = g
     r, s = prep.r, prep.s
-    B = prep.norms.shape[0]
-    fns = [_plan_fn(prep.norms[b], r, ctx, delta, s, apply_switch, fix_params) for b in range(B)]
-    executed = [(tuple(int(x) for x in digits[b]), int(nu[b])) for b in range(B)]
+    # one tolist() per array instead of per-element conversions: this runs
+    # on the host between the Horner graph launch and the caller's next
+    # step (64 reports at cfg2)
+    rows = prep.norms.tolist()
+    fns = [_plan_fn_list(row, r, ctx, delta, s, apply_switch, fix_params) for row in rows]
+    executed = [(tuple(dg), n) for dg, n in zip(digits.tolist(), nu.tolist())]
     return _reports(result, fns, executed, "mixed", timer.seconds(), with_bound, single)
 
 

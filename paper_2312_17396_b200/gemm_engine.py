@@ -81,7 +81,31 @@ class Operand:
         self.mat, self.slices, self.fmt, self.side = mat, slices, fmt, side
 
 
-def prepare(h, A: MatBatch, side: int, fmt: int, sel=None, exp=None) -> Operand:
+#: plane counts with an 8-bit-digit kernel set (csrc: 2, 3, 5, 6, 10, 12
+#: exist for the Horner chain's column operand only)
+_PLANES_8 = (2, 3, 4, 5, 6, 8, 10, 12, 14)
+_PER_LEVEL = os.environ.get("MPPS_LEVEL_PLANES", "1") != "0"
+
+
+def planes_for_digits(h, fmt: int, digits: int, db: int) -> int:
+    """Digit planes for a Horner level planned at ``digits`` decimal digits
+    (engine.py:184-215) stored in ``fmt``: the level's GEMM needs the
+    reference's p = ceil(d log2 10) bits (its mat_mul runs at ctx_j,
+    engine.py:249-251), not the full storage format.  8-bit planes carry
+    6 + 8 (S-1) bits; S is the smallest compiled count with >= p + 4 bits,
+    capped at the format's own count (the snapped-lattice kernels)."""
+    full = h.slices_for(fmt, db)
+    if db != 8 or not _PER_LEVEL or fmt not in (7, 15, 31):
+        return full
+    import math
+    p = math.ceil(digits * math.log2(10))
+    for S in _PLANES_8:
+        if 6 + 8 * (S - 1) >= p + 4:
+            return min(S, full)
+    return full
+
+
+def prepare(h, A: MatBatch, side: int, fmt: int, sel=None, exp=None, nslices=None) -> Operand:
     """Prepare A as the left (side 0) or right (side 1) operand of GEMMs at
     ``fmt``.  For the tensor-core engine the split uses the planes of the
     finest format any later use needs (the caller passes it as ``fmt``);
@@ -91,7 +115,7 @@ def prepare(h, A: MatBatch, side: int, fmt: int, sel=None, exp=None) -> Operand:
         # so no extra level scaling is applied (exp is ignored)
         K = A.cols if side == 0 else A.rows
         db = digit_bits_for(h, K)
-        return Operand(A, h.slice(A, side, h.slices_for(fmt, db), sel, db), fmt, side)
+        return Operand(A, h.slice(A, side, nslices or h.slices_for(fmt, db), sel, db), fmt, side)
     if A.fmt != fmt or exp is not None:
         B = MatBatch.empty(fmt, A.batch, A.rows, A.cols, device=A.device)
         h.convert(A, B, sel, exp)
@@ -108,12 +132,12 @@ def gemm(h, L: Operand, R: Operand, C: MatBatch, sel=None) -> None:
 
 
 def horner(h, Y: Operand, phi: Operand, fmt_level: int, Bprev, out, sel=None, exp_y=None, exp_in=None,
-           exp_out=None) -> None:
+           exp_out=None, nslices=None) -> None:
     """out = RN_out(2^eo (Bprev + 2^-(ey+ei) RN_level(Y phi)))."""
     if Y.slices is not None and phi.slices is not None:
         # the Y planes are unscaled (exp_y does not apply); phi keeps its
         # level scaling 2^exp_in, undone in the epilogue
-        h.horner_step_sliced(Y.slices, phi.slices, h.slices_for(fmt_level, Y.slices.db), Bprev, out, sel, None, exp_in,
-                             exp_out, fmt_in=fmt_level)
+        h.horner_step_sliced(Y.slices, phi.slices, nslices or h.slices_for(fmt_level, Y.slices.db), Bprev, out, sel,
+                             None, exp_in, exp_out, fmt_in=fmt_level)
     else:
         h.horner_step(Y.mat, phi.mat, Bprev, out, sel, exp_y, exp_in, exp_out)
