@@ -205,6 +205,10 @@ typedef struct {
  * planes (padding written as zero). */
 int mpps_slice(mpps_handle *h, const mpps_mat *src, int side, mpps_slices *out,
                const int *sel, int nsel);
+/* Column split of src into slice rows [row0, row0 + src->cols) of out: the
+ * right operand [P_0 | P_1] of one GEMM over several matrices (the power
+ * chain's [X | X^2]); other rows are untouched. */
+int mpps_slice_into(mpps_handle *h, const mpps_mat *src, mpps_slices *out, int row0, const int *sel, int nsel);
 
 /* mat_mul (precision.py:160-184) on the tensor cores: C (M x N, format of C)
  * = A (sliced by rows) * B (sliced by columns), using nslices digit planes. */

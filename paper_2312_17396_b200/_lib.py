@@ -26,7 +26,7 @@ MPPS_OK, MPPS_EINVAL, MPPS_EFMT, MPPS_ECUDA = 0, 1, 2, 3
 EXPORTED = (
     "mpps_version", "mpps_create", "mpps_destroy", "mpps_set_stream",
     "mpps_last_error", "mpps_launch_count", "mpps_convert", "mpps_gemm",
-    "mpps_axpy", "mpps_powers", "mpps_assemble_blocks", "mpps_assemble_blocks_hc", "mpps_assemble_hc_supported", "mpps_assemble_blocks_hc_n", "mpps_assemble_hc_n_supported", "mpps_one_norm", "mpps_one_norm_complex", "mpps_level_exps",
+    "mpps_axpy", "mpps_powers", "mpps_slice_into", "mpps_assemble_blocks", "mpps_assemble_blocks_hc", "mpps_assemble_hc_supported", "mpps_assemble_blocks_hc_n", "mpps_assemble_hc_n_supported", "mpps_one_norm", "mpps_one_norm_complex", "mpps_level_exps",
     "mpps_horner_step", "mpps_horner_scalar_top", "mpps_probe_fma",
     "mpps_assemble_blocks_dist", "mpps_colmax", "mpps_slice", "mpps_gemm_sliced",
     "mpps_horner_step_sliced", "mpps_oz_slices_for", "mpps_oz_slices_for_bits", "mpps_oz_max_k_8bit", "mpps_probe_i8mma", "mpps_debug_oz_trace",
@@ -133,6 +133,7 @@ def load_library(path: Optional[str] = None):
         lib.mpps_colmax.argtypes = [vp, vp, ip, ip, ip, vp]
         sp = P(CSlices)
         lib.mpps_slice.argtypes = [vp, mp, ip, sp, vp, ip]
+        lib.mpps_slice_into.argtypes = [vp, mp, sp, ip, vp, ip]
         lib.mpps_gemm_sliced.argtypes = [vp, sp, sp, ip, ip, ip, ip, mp, vp, ip]
         lib.mpps_horner_step_sliced.argtypes = [vp, sp, sp, ip, mp, mp, vp, ip, vp, vp, vp]
         lib.mpps_oz_slices_for.argtypes = [ip]
@@ -305,11 +306,20 @@ class Handle:
                     "slice")
         return out
 
+    def slice_into(self, src: MatBatch, out: "Slices", row0: int, sel=None):
+        """Column split of src into slice rows [row0, row0 + src.cols) of out."""
+        c_src, c_out = cmat(src), out.c()
+        nsel = 0 if sel is None else sel.numel()
+        self._check(self.lib.mpps_slice_into(self.h, ctypes.byref(c_src), ctypes.byref(c_out), int(row0), _ptr(sel),
+                                             nsel), "slice_into")
+
     def gemm_sliced(self, A: "Slices", B: "Slices", S: int, C: MatBatch, sel=None):
         a, b, c = A.c(), B.c(), cmat(C)
         nsel = 0 if sel is None else sel.numel()
         end = self._ev(("gemm_tc", C.fmt, C.fmt, A.rows, B.rows, A.k, nsel or C.batch, S, A.db))
-        self._check(self.lib.mpps_gemm_sliced(self.h, ctypes.byref(a), ctypes.byref(b), S, A.rows, B.rows, A.k,
+        # N from C: B may hold more column slices than this product uses
+        # (the power chain's [X | X^2] operand)
+        self._check(self.lib.mpps_gemm_sliced(self.h, ctypes.byref(a), ctypes.byref(b), S, A.rows, C.cols, A.k,
                                               ctypes.byref(c), _ptr(sel), nsel), "mat_mul(tc)")
         if end is not None:
             end.record()

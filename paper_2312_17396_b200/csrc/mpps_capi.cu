@@ -1260,19 +1260,43 @@ static bool oz_cols_fused() {
   return v != 0;
 }
 
+static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices *out, const int *sel, int nsel,
+                      int row0, int nrows);
+
 extern "C" int mpps_slice(mpps_handle *h, const mpps_mat *src, int side, mpps_slices *out, const int *sel, int nsel) {
+  return slice_impl(h, src, side, out, sel, nsel, 0, -1);
+}
+
+/* Column split of src into slice rows [row0, row0 + src->cols) of out (the
+ * right operand [P_0 | P_1 | ...] of a GEMM whose N spans several matrices:
+ * the power chain's [X | X^2]); rows outside are left untouched. */
+extern "C" int mpps_slice_into(mpps_handle *h, const mpps_mat *src, mpps_slices *out, int row0, const int *sel,
+                               int nsel) {
+  if (row0 < 0 || !src || !out || row0 + src->cols > out->rpad)
+    return set_err(h, MPPS_EINVAL, "slice_into: rows [%d, %d) outside the %d slice rows", row0,
+                   row0 + (src ? src->cols : 0), out ? out->rpad : 0);
+  return slice_impl(h, src, 1, out, sel, nsel, row0, src->cols);
+}
+
+static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices *out, const int *sel, int nsel,
+                      int row0, int nrows) {
   int rc = check_mat(h, src, "slice.src");
   if (rc) return rc;
   if (!out || !out->digits || !out->exps) return set_err(h, MPPS_EINVAL, "slice: null output");
   if (out->nslices < 1 || out->nslices > 31) return set_err(h, MPPS_EINVAL, "slice: 1..31 slices");
   const int rows = side == 0 ? src->rows : src->cols;   // rows of the slice arrays
   const int ks = side == 0 ? src->cols : src->rows;
-  if (out->rpad < rows || out->rpad % oz::kTileM || out->kpad < ks || out->kpad % oz::kKStep)
+  if (out->rpad < row0 + rows || out->rpad % oz::kTileM || out->kpad < ks || out->kpad % oz::kKStep)
     return set_err(h, MPPS_EINVAL, "slice: padding %dx%d too small or unaligned for %dx%d", out->rpad, out->kpad, rows, ks);
   const int nb = sel ? nsel : src->batch;
   if (!sel && out->batch != src->batch) return set_err(h, MPPS_EINVAL, "slice: batch mismatch");
   if (nb == 0) return MPPS_OK;
   oz::SliceRef o = sref(out);
+  if (nrows >= 0) {
+    o.row0 = row0;
+    o.nrows = nrows;
+  }
+  const int gx = nrows >= 0 ? (nrows + 31) / 32 : out->rpad / 32;   // column-side CTAs
   const int fi = fmt_index(src->fmt);
   const int W = fmt_words(fi);
   const int S = out->nslices;
@@ -1295,7 +1319,7 @@ extern "C" int mpps_slice(mpps_handle *h, const mpps_mat *src, int side, mpps_sl
 #undef SR
     return after_launch(h, "slice_rows_kernel");
   }
-  if (oz_cols_fused()) {
+  if (oz_cols_fused() && nrows < 0) {
     dim3 grid(out->rpad / 32, nb);
 #define SCF(WW, SS) \
   if (W == WW && S == SS) oz::slice_cols_fused_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
@@ -1304,10 +1328,10 @@ extern "C" int mpps_slice(mpps_handle *h, const mpps_mat *src, int side, mpps_sl
 #undef SCF
     return after_launch(h, "slice_cols_fused_kernel");
   }
-  oz::col_exps_kernel<<<dim3(out->rpad / 32, nb), 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel);
+  oz::col_exps_kernel<<<dim3(gx, nb), 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel);
   rc = after_launch(h, "col_exps_kernel");
   if (rc) return rc;
-  dim3 grid(out->rpad / 32, out->kpad / 32, nb);
+  dim3 grid(gx, out->kpad / 32, nb);
 #define SC(WW, SS) \
   if (W == WW && S == SS) oz::slice_cols_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
   SC(1, 4) SC(1, 8) SC(1, 14) SC(1, 16) SC(1, 28) SC(1, 31) SC(2, 4) SC(2, 8) SC(2, 14) SC(2, 16) SC(2, 28)

@@ -141,6 +141,8 @@ struct SliceRef {
   int *exps;        // [batch][rpad]
   int S, batch, rpad, kpad;
   int db;           // digit bits: 7 (digits in [-65, 65]) or 8 ([-128, 127]); first digit 6 bits
+  int row0 = 0;     // column splits: first slice row written (mpps_slice_into)
+  int nrows = 1 << 30;   // and the number of rows written (default: through rpad)
   __host__ __device__ long long plane() const { return (long long)batch * rpad * kpad; }
 };
 
@@ -495,10 +497,10 @@ __global__ void col_exps_kernel(MatRef B, int rows, int cols, int fi, SliceRef o
     }
   red[ty][tx] = mx;
   __syncthreads();
-  if (ty == 0 && j < out.rpad) {
+  if (ty == 0 && out.row0 + j < out.rpad && j < out.nrows) {
 #pragma unroll
     for (int g = 1; g < 8; ++g) mx = fmax(mx, red[g][tx]);
-    out.exps[(long long)b * out.rpad + j] = row_exponent(mx);
+    out.exps[(long long)b * out.rpad + out.row0 + j] = row_exponent(mx);
   }
 }
 
@@ -518,7 +520,7 @@ __device__ __forceinline__ void slice_cols_body(const MatRef &B, int rows, int c
     if (k < rows && j < cols) {
       const long long off = (long long)b * B.bstride + (long long)k * B.ld + j;
       v = fi == F32 ? mp::qd_from_d((double)((const float *)B.data)[off]) : load_w<W>(B, off);
-      ecol = ecs ? ecs[tx] : out.exps[(long long)b * out.rpad + j];
+      ecol = ecs ? ecs[tx] : out.exps[(long long)b * out.rpad + out.row0 + j];
       if constexpr (!FIXED) v = scale_words<W>(v, -ecol);
     }
     const mp::qd vraw = v;
@@ -544,11 +546,11 @@ __device__ __forceinline__ void slice_cols_body(const MatRef &B, int rows, int c
   // each thread writes 4 consecutive k of one column j as a 32-bit word
   const int jj = threadIdx.x >> 3, kq = (threadIdx.x & 7) * 4;
   const int j = j0 + jj;
-  if (j < out.rpad && k0 + kq < out.kpad)
+  if (out.row0 + j < out.rpad && j < out.nrows && k0 + kq < out.kpad)
 #pragma unroll
     for (int s = 0; s < S; ++s)
-      *reinterpret_cast<uint32_t *>(out.digits + s * plane + ((long long)b * out.rpad + j) * out.kpad + k0 + kq) =
-          *reinterpret_cast<const uint32_t *>(&tile[s][jj][kq]);
+      *reinterpret_cast<uint32_t *>(out.digits + s * plane + ((long long)b * out.rpad + out.row0 + j) * out.kpad +
+                                    k0 + kq) = *reinterpret_cast<const uint32_t *>(&tile[s][jj][kq]);
 }
 
 template <int W, int S>

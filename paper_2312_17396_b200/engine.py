@@ -58,6 +58,8 @@ BUCKETS = ("power_formation", "norm_estimation", "mixed_horner", "coefficient_as
 import os as _os
 #: two-pass block assembly for the mixed evaluators (MPPS_LOWP_ASSEMBLY=0: one dd pass)
 _LOWP = _os.environ.get("MPPS_LOWP_ASSEMBLY", "1") != "0"
+#: two powers per power-chain GEMM (MPPS_PAIRED_POWERS=0: X^{k+1} = X^k X one by one)
+_PAIRED = _os.environ.get("MPPS_PAIRED_POWERS", "1") != "0"
 
 
 def _torch():
@@ -292,12 +294,45 @@ def _form_powers(h, Xt, wf: int, s: int, timer: _Buckets, x_is_working: Optional
             h.convert(x_is_working, powers[0])
     else:
         h.convert(MatBatch(Xt.unsqueeze(0), FP64), powers[0])
-    if s > 1:
+    if s > 1 and _PAIRED and ge.uses_tc(wf) and s >= 4:
+        powers = _paired_powers(h, powers[0], wf, s)
+    elif s > 1:
         Xr = ge.prepare(h, powers[0], 1, wf)          # X: right operand of every step
         for k in range(1, s):       # X^{k+1} = X^k X   (engine.py:151-153)
             ge.gemm(h, ge.prepare(h, powers[k - 1], 0, wf), Xr, powers[k])
     timer.stop()
     return powers
+
+
+def _paired_powers(h, X: MatBatch, wf: int, s: int) -> List[MatBatch]:
+    """X, X^2..X^s with two powers per tensor-core GEMM: the right operand
+    is the column split of [X | X^2] (one slice buffer, 2n columns), so
+    [X^{k+1} | X^{k+2}] = X^k [X | X^2] is one product of N = 2n.  s = 6:
+    3 GEMMs and 3 row splits instead of 5 and 5 (powers are the same
+    working-precision products, associated differently than the
+    reference's X^{k+1} = X^k X; engine.py:151-153)."""
+    B, n, dev = X.batch, X.rows, X.device
+    db = ge.digit_bits_for(h, n)
+    S = h.slices_for(wf, db)
+    SP = _lib.Slices(S, B, 2 * n, n, dev, db)
+    h.slice_into(X, SP, 0)
+    X2 = MatBatch.empty(wf, B, n, device=dev)
+    h.gemm_sliced(h.slice(X, 0, S, None, db), SP, S, X2)        # X^2 = X X (first n slice rows)
+    h.slice_into(X2, SP, n)
+    out = [X, X2]
+    A = X2
+    while len(out) < s:
+        if s - len(out) >= 2:
+            Q = MatBatch.empty(wf, B, n, 2 * n, device=dev)
+            h.gemm_sliced(h.slice(A, 0, S, None, db), SP, S, Q)  # [A X | A X^2]
+            lo, hi = MatBatch(Q.data[..., :n], wf), MatBatch(Q.data[..., n:], wf)
+            out += [lo, hi]
+            A = hi
+        else:
+            C = MatBatch.empty(wf, B, n, device=dev)
+            h.gemm_sliced(h.slice(A, 0, S, None, db), SP, S, C)
+            out.append(C)
+    return out
 
 
 def _lowp_blocks(h, wf: int, s: int, m: int) -> int:
