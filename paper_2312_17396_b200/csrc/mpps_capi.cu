@@ -1314,8 +1314,8 @@ static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices
 #define SR(WW, SS) \
   if (W == WW && S == SS) oz::slice_rows_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
     SR(1, 4) SR(1, 8) SR(1, 14) SR(1, 16) SR(1, 28) SR(1, 31) SR(2, 4) SR(2, 8) SR(2, 14) SR(2, 16) SR(2, 28)
-    SR(2, 31) SR(4, 4) SR(4, 8) SR(4, 14) SR(4, 16) SR(4, 28) SR(4, 31) {}
-    // per-level plane counts are column-side (phi) only
+    SR(2, 31) SR(4, 4) SR(4, 8) SR(4, 14) SR(4, 16) SR(4, 28) SR(4, 31)
+    SR(1, 2) SR(1, 3) SR(1, 5) SR(1, 6) SR(2, 2) SR(2, 3) SR(2, 5) SR(2, 6) SR(2, 10) SR(2, 12) {}
 #undef SR
     return after_launch(h, "slice_rows_kernel");
   }

@@ -546,7 +546,11 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
         ys: Dict[int, ge.Operand] = {}
         tc_fmts = [f for f in set(fm[1:]) if ge.uses_tc(f)]
         if tc_fmts:
-            ytc = ge.prepare(h, Y, 0, max(tc_fmts), sel)
+            # tensor cores: the level products run as phi_j Y (Y and phi_j
+            # commute: both are polynomials in X), so each phi_j is split by
+            # rows (one pass, no column-exponent pre-pass) and Y by columns
+            # once, at the finest level's planes
+            ytc = ge.prepare(h, Y, 1, max(tc_fmts), sel)
             for f in tc_fmts:
                 ys[f] = ytc
         for f in sorted(set(fm[1:])):
@@ -563,8 +567,13 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
         for j in range(j0, 0, -1):
             out = result if j - 1 == 0 else ws.next(fm[j - 1])
             ns = st[j - 1] if st else None       # this level's digit planes
-            ge.horner(h, ys[fm[j]], ge.prepare(h, phi, 1, fm[j], sel, nslices=ns), fm[j], blocks[j - 1], out, sel,
-                      exp_y if fm[j] == FP32 else None, ex(j), ex(j - 1), nslices=ns)
+            if ge.uses_tc(fm[j]):
+                # phi_j (rows) x Y (columns): left operand first
+                ge.horner(h, ge.prepare(h, phi, 0, fm[j], sel, nslices=ns), ys[fm[j]], fm[j], blocks[j - 1], out,
+                          sel, None, ex(j), ex(j - 1), nslices=ns)
+            else:
+                ge.horner(h, ys[fm[j]], ge.prepare(h, phi, 1, fm[j], sel), fm[j], blocks[j - 1], out, sel,
+                          exp_y if fm[j] == FP32 else None, ex(j), ex(j - 1))
             phi = out
     timer.stop()
     return result

@@ -1,7 +1,10 @@
 """SUMMA driver on the GPU over NCCL (one rank, 1x1 grid -- the box has one
-GPU; the multi-rank plumbing is covered by tests/test_summa_gloo.py): the
-distributed pipeline runs the same kernels in the same order as the
-single-GPU path, so its result and plan are bitwise identical."""
+GPU; the multi-rank plumbing is covered by tests/test_summa_gloo.py).  The
+distributed pipeline keeps the reference's association (X^k = X^{k-1} X,
+Y phi), format plane counts and an all-dd block assembly, while the
+single-GPU engine pairs powers, runs phi Y with per-level planes and
+assembles fp32/fp64-level blocks in fp64: same schedule, values within the
+c n u tolerance of each other and of the oracle."""
 import os
 import socket
 
@@ -25,7 +28,7 @@ def nccl1(cuda):
     dist.destroy_process_group()
 
 
-def test_summa_1x1_bitwise_equals_single_gpu(nccl1):
+def test_summa_1x1_matches_single_gpu(nccl1):
     import torch
     import paper_2312_17396_b200 as m
     from paper_2312_17396_b200 import summa
@@ -39,8 +42,14 @@ def test_summa_1x1_bitwise_equals_single_gpu(nccl1):
     res = summa.ps_mixed_dist(Z, m.taylor_cos_coeffs(24), ctx, grid)
     ref = m.ps_mixed_general(m.cos_argument(X, ctx), m.taylor_cos_coeffs(24), ctx)
     assert res.digits == ref.plan.level_digits and res.nu == ref.plan.nu
-    assert np.array_equal(res.block.data.cpu().numpy(), ref.result.data.cpu().numpy())
-    assert res.plan(ctx).to_dict() == ref.plan.to_dict()
+    a = res.block.data.cpu().numpy()
+    b = ref.result.data.cpu().numpy()
+    va, vb = a[0, 0] + a[1, 0], b[0, 0] + b[1, 0]
+    d = np.abs((a[0, 0] - b[0, 0]) + (a[1, 0] - b[1, 0])).sum(axis=0).max()
+    assert d <= tol(ref.plan.r, n, 31) * np.abs(vb).sum(axis=0).max()
+    pa, pb = res.plan(ctx).to_dict(), ref.plan.to_dict()
+    for k in ("s", "r", "nu", "working_digits", "digits", "roundoffs", "nilpotent"):
+        assert pa[k] == pb[k], k
 
 
 def test_summa_1x1_vs_oracle(nccl1, oracle_lib):
