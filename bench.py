@@ -442,6 +442,11 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     gem = wl.gemms(rep)
     plans = wl.plans(rep)
+    # long-lived objects (graphs, buffers, the workload) out of the collector's
+    # generations: no multi-ms gen-2 pause inside a timed region
+    import gc
+    gc.collect()
+    gc.freeze()
 
     def barrier():
         if dist is not None:

@@ -112,6 +112,17 @@ def evaluate_host(submit: Callable, X_host, out_host, chunks=3, trace=None, stre
     Default: every chunk in flight.
     ``trace``: optional list; timing events (label, event, host time) are
     appended (diagnostics, tools/e2e_chunks.py)."""
+    import gc
+    gc_was = gc.isenabled()
+    gc.disable()    # a gen-2 collection (~30 ms) would idle the GPU waiting on the host planner
+    try:
+        return _evaluate_host(submit, X_host, out_host, chunks, trace, streams, ahead, window)
+    finally:
+        if gc_was:
+            gc.enable()
+
+
+def _evaluate_host(submit, X_host, out_host, chunks, trace, streams, ahead, window):
     torch = _torch()
 
     def mark(label, stream):

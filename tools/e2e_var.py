@@ -18,7 +18,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "freeze":
     gc.collect()
     gc.freeze()
 vals = []
-for _ in range(12):
+for _ in range(20):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     pl.evaluate_host(sub, Xbig, out, sizes, streams=2, window=6)
