@@ -550,7 +550,7 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
             # commute: both are polynomials in X), so each phi_j is split by
             # rows (one pass, no column-exponent pre-pass) and Y by columns
             # once, at the finest level's planes
-            ytc = ge.prepare(h, Y, 1, max(tc_fmts), sel)
+            ytc = ge.prepare(h, Y, 1, max(tc_fmts), sel, nslices=max(st) if st else None)
             for f in tc_fmts:
                 ys[f] = ytc
         for f in sorted(set(fm[1:])):
