@@ -141,8 +141,10 @@ template <> struct WV<DD> {
     double *p = (double *)m.data + off; p[0] = v.hi; p[m.plane] = v.lo;
   }
   static __device__ __forceinline__ T load(const MatRef &m, long long off) {
+    // an fp64 matrix reads as a dd with a zero low word (the power chain's
+    // X stays in its fp64 input format)
     const double *p = (const double *)m.data + off;
-    return mp::dd_make(p[0], p[m.plane]);
+    return mp::dd_make(p[0], m.words > 1 ? p[m.plane] : 0.0);
   }
   // Block-assembly accumulator: the high parts are summed with an exact
   // TwoSum, every rounding error and the cross products go to an unnormalised
@@ -958,19 +960,20 @@ int mpps_assemble_blocks_hc(mpps_handle *h, const mpps_mat *powers, int s, int m
     return set_err(h, MPPS_EINVAL, "assemble: square matrices expected (use mpps_assemble_blocks_dist)");
   const int r = m / s;
   const int skip_top = (flags & 1) && (m % s == 0);
-  const int wf = fmt_index(powers[0].fmt);
+  const int wf = fmt_index(powers[s - 1].fmt);
   for (int k = 0; k < s; ++k) {
     int rc = check_mat(h, &powers[k], "assemble.power");
     if (rc) return rc;
-    if (powers[k].fmt != powers[0].fmt || powers[k].rows != powers[0].rows || powers[k].cols != powers[0].cols ||
-        powers[k].batch != powers[0].batch)
+    const bool x64 = k == 0 && wf == DD && fmt_index(powers[0].fmt) == F64;   // fp64 X under a dd chain
+    if ((powers[k].fmt != powers[s - 1].fmt && !x64) || powers[k].rows != powers[0].rows ||
+        powers[k].cols != powers[0].cols || powers[k].batch != powers[0].batch)
       return set_err(h, MPPS_EINVAL, "assemble: powers must share format and shape");
   }
   for (int k = 0; k <= r; ++k) {
     if (skip_top && k == r) continue;
     int rc = check_mat(h, &blocks[k], "assemble.block");
     if (rc) return rc;
-    if (blocks[k].fmt != powers[0].fmt || blocks[k].rows != powers[0].rows || blocks[k].cols != powers[0].cols ||
+    if (fmt_index(blocks[k].fmt) != wf || blocks[k].rows != powers[0].rows || blocks[k].cols != powers[0].cols ||
         blocks[k].batch != powers[0].batch)
       return set_err(h, MPPS_EINVAL, "assemble: blocks must match the powers");
   }
@@ -980,7 +983,7 @@ int mpps_assemble_blocks_hc(mpps_handle *h, const mpps_mat *powers, int s, int m
   AC(DD, 6, 5) AC(DD, 7, 6) AC(DD, 5, 4) AC(DD, 4, 3) AC(DD, 5, 3) AC(F64, 5, 3) AC(F64, 4, 3)
 #undef AC
   return set_err(h, MPPS_EFMT, "assemble_hc: no constant-coefficient kernel for r+1=%d, s=%d at format %d", r + 1, s,
-                 powers[0].fmt);
+                 powers[s - 1].fmt);
 }
 
 int mpps_assemble_blocks_hc_n(mpps_handle *h, const mpps_mat *powers, int s, int m, const double *coeff_host,
@@ -989,14 +992,15 @@ int mpps_assemble_blocks_hc_n(mpps_handle *h, const mpps_mat *powers, int s, int
   if (s < 2 || s > kMaxPowers || m < s) return set_err(h, MPPS_EINVAL, "need 2 <= s <= series degree (s=%d m=%d)", s, m);
   const int r = m / s;
   if (nblocks < 1 || nblocks > r + 1) return set_err(h, MPPS_EINVAL, "assemble_n: 1 <= nblocks <= r+1 (%d)", nblocks);
-  const int pf = fmt_index(powers[0].fmt), bf = fmt_index(blocks[0].fmt);
+  const int pf = fmt_index(powers[s - 1].fmt), bf = fmt_index(blocks[0].fmt);
   int nd = 0;                               // leading dd blocks, then fp64 ones
   while (nd < nblocks && fmt_index(blocks[nd].fmt) == DD) ++nd;
   for (int k = 0; k < s; ++k) {
     int rc = check_mat(h, &powers[k], "assemble_n.power");
     if (rc) return rc;
-    if (powers[k].fmt != powers[0].fmt || powers[k].rows != powers[0].rows || powers[k].cols != powers[0].cols ||
-        powers[k].batch != powers[0].batch || powers[k].rows != powers[k].cols)
+    const bool x64 = k == 0 && fmt_index(powers[0].fmt) == F64;   // fp64 X under a dd chain
+    if ((powers[k].fmt != powers[s - 1].fmt && !x64) || powers[k].rows != powers[0].rows ||
+        powers[k].cols != powers[0].cols || powers[k].batch != powers[0].batch || powers[k].rows != powers[k].cols)
       return set_err(h, MPPS_EINVAL, "assemble_n: square powers of one format and shape");
   }
   for (int k = 0; k < nblocks; ++k) {

@@ -280,8 +280,12 @@ class _Prepared:
     lowp: bool = False         # blocks are fp64 (two-pass assembly): dd ones are made per plan in _horner
 
 
-def _form_powers(h, Xt, wf: int, s: int, timer: _Buckets, x_is_working: Optional[MatBatch] = None):
-    """X, X^2..X^s at the working format (engine.py:141-154 power chain)."""
+def _form_powers(h, Xt, wf: int, s: int, timer: _Buckets, x_is_working: Optional[MatBatch] = None,
+                 x_fp64_ok: bool = False):
+    """X, X^2..X^s at the working format (engine.py:141-154 power chain).
+    ``x_fp64_ok``: an fp64 input X under a dd chain on the tensor cores
+    stays fp64 (its digit split and the block assembly read it directly:
+    widening it to dd is exact and changes no value)."""
     dev = Xt.device if Xt is not None else x_is_working.device
     B = Xt.shape[0] if Xt is not None else x_is_working.batch
     n = Xt.shape[1] if Xt is not None else x_is_working.rows
@@ -292,6 +296,8 @@ def _form_powers(h, Xt, wf: int, s: int, timer: _Buckets, x_is_working: Optional
             powers[0] = x_is_working
         else:
             h.convert(x_is_working, powers[0])
+    elif x_fp64_ok and wf == DD and s >= 4 and _PAIRED and ge.uses_tc(wf):
+        powers[0] = MatBatch(Xt.unsqueeze(0), FP64)
     else:
         h.convert(MatBatch(Xt.unsqueeze(0), FP64), powers[0])
     if s > 1 and _PAIRED and ge.uses_tc(wf) and s >= 4:
@@ -420,7 +426,12 @@ def _prepare(h, Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: in
              lowp: bool = False) -> _Prepared:
     """eval_b0_and_power + assemble_block + one_norm (engine.py:141-154,
     127-138, 467-468) for the whole batch."""
-    powers = _form_powers(h, Xt, wf, s, timer, x_is_working)
+    m = series.degree
+    # fp64 X may stay unwidened when the assembly runs the constant-coefficient
+    # kernels (both the mixed and the all-dd ones read an fp64 X^1)
+    x64 = (wf == DD and complexmat.scope() is None and h.assemble_hc_supported(wf, s, m)
+           and (not lowp or _lowp_blocks(h, wf, s, m) > 0))
+    powers = _form_powers(h, Xt, wf, s, timer, x_is_working, x_fp64_ok=x64)
     return _assemble(h, powers, series, ctx, wf, s, timer, sync, lowp)
 
 
