@@ -173,3 +173,25 @@ def test_batched_planner_certified_equals_exact():
         for b in range(len(rows)):
             p = plan_precisions(nb[b], ny[b], PrecisionCtx(d), s=2)
             assert tuple(dig[b]) == p.level_digits and nu[b] == p.nu and nil[b] == p.nilpotent
+
+
+def test_level_planes_from_planned_digits():
+    """gemm_engine.planes_for_digits: the smallest compiled 8-bit plane count
+    with 6 + 8 (S-1) >= ceil(d log2 10) + 4 bits, capped at the format's
+    plane count; 7-bit digits keep the format's count."""
+    import math
+    from paper_2312_17396_b200 import gemm_engine as ge
+
+    class H:
+        def slices_for(self, fmt, db):
+            return {8: {7: 4, 15: 8, 31: 14, 63: 28}, 7: {7: 4, 15: 8, 31: 16, 63: 31}}[db][fmt]
+
+    h = H()
+    assert [ge.planes_for_digits(h, 31, d, 8) for d in (22, 31, 16)] == [10, 14, 8]
+    assert [ge.planes_for_digits(h, 15, d, 8) for d in (10, 15, 8)] == [5, 8, 5]
+    assert [ge.planes_for_digits(h, 7, d, 8) for d in (1, 3, 4, 7)] == [2, 2, 3, 4]
+    assert ge.planes_for_digits(h, 31, 22, 7) == 16
+    for fmt, dmax in ((7, 7), (15, 15), (31, 31)):
+        for d in range(1, dmax + 1):
+            S = ge.planes_for_digits(h, fmt, d, 8)
+            assert 6 + 8 * (S - 1) >= min(math.ceil(d * math.log2(10)) + 4, 6 + 8 * (h.slices_for(fmt, 8) - 1))
