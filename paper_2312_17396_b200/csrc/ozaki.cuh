@@ -361,6 +361,56 @@ __device__ __forceinline__ unsigned __int128 fixed_biased_fast(const mp::qd &v, 
   return V + C;
 }
 
+// The same V as fixed_biased_fast, with the alignment done on the FP64 pipe
+// (the split is ALU-bound: ncu on slice_rows_kernel<2,14> at cfg2 showed the
+// ALU pipe 73 % busy at ~150 instructions per entry, ~100 of them integer
+// shifts/selects of the 128-bit alignment above).  The row's 2^(F-e) comes
+// as two normal factors p1 p2 (F - e spans [-1015, 1183]); w 2^(F-e) is then
+// exact wherever it can round to a nonzero integer (an intermediate below
+// 2^-1022 only arises when the result is < 2^-1022 as well), the half-up
+// rounding is floor(a + 1/2) below 2^52 (exact there; above, a is already an
+// integer), and the 128-bit two's complement comes from |r| = q 2^64 + rem
+// (q, rem exact doubles) converted with F2I and negated.
+__device__ __forceinline__ double pow2_normal(int k) {   // k in [-1022, 1023]
+  return __longlong_as_double((long long)(k + 1023) << 52);
+}
+template <int S>
+__device__ __forceinline__ void fixed_scale(int e, double &p1, double &p2) {
+  constexpr int F = 6 + 8 * (S - 1);
+  const int k = F - e, k1 = k >> 1;
+  p1 = pow2_normal(k1);
+  p2 = pow2_normal(k - k1);
+}
+__device__ __forceinline__ double round_half_up_scaled(double w, double p1, double p2) {
+  const double a = __dmul_rn(__dmul_rn(w, p1), p2);
+  return fabs(a) < 0x1p52 ? floor(__dadd_rn(a, 0.5)) : a;
+}
+template <int W, int S>
+__device__ __forceinline__ unsigned __int128 fixed_biased_fp(double h, double l, double p1, double p2) {
+  static_assert(W <= 2 && 6 + 8 * (S - 1) - 53 < 64, "fixed-point split: at most 2 words and 14 planes");
+  const double r = round_half_up_scaled(h, p1, p2);
+  const double m = fabs(r);
+  const double q = trunc(__dmul_rn(m, 0x1p-64));
+  const double rem = __fma_rn(-q, 0x1p64, m);
+  unsigned long long L = __double2ull_rz(rem);
+  unsigned long long H = __double2ull_rz(q);
+  {                                    // branch-free 128-bit negate for r < 0
+    const bool neg = r < 0.0;
+    const unsigned long long nH = ~H + (L == 0ull ? 1ull : 0ull), nL = 0ull - L;
+    H = neg ? nH : H;
+    L = neg ? nL : L;
+  }
+  if constexpr (W == 2) {
+    const long long w = __double2ll_rz(round_half_up_scaled(l, p1, p2));
+    const unsigned long long L2 = L + (unsigned long long)w;
+    H += (unsigned long long)(w >> 63) + (L2 < L ? 1ull : 0ull);
+    L = L2;
+  }
+  const unsigned __int128 V = ((unsigned __int128)H << 64) | L;
+  const unsigned __int128 C = ((unsigned __int128)fixed_cmask_hi<S>() << 64) | fixed_cmask_lo<S>();
+  return V + C;
+}
+
 // byte k of the 128-bit Y as the low byte of an int
 __device__ __forceinline__ uint32_t fixed_word(const unsigned __int128 &Y, int j) {
   return (uint32_t)(Y >> (32 * j));
@@ -389,6 +439,8 @@ __device__ __forceinline__ void slice_rows_body(const MatRef &A, int rows, int c
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   const int e = row_exponent(mx);
   if (lane == 0) out.exps[(long long)b * out.rpad + i] = e;
+  double p1 = 1.0, p2 = 1.0;
+  if constexpr (DB == 8 && W <= 2 && S <= 14) fixed_scale<S>(e, p1, p2);
   const long long plane = out.plane();
   int8_t *o = out.digits + ((long long)b * out.rpad + i) * out.kpad;
   for (int k0 = 4 * lane; k0 < out.kpad; k0 += 128) {
@@ -404,7 +456,7 @@ __device__ __forceinline__ void slice_rows_body(const MatRef &A, int rows, int c
 #pragma unroll
         for (int q = 0; q < 4; ++q) w1[q] = W > 1 ? p[A.plane + q] : 0.0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) Y[q] = fixed_biased_fast<W, S>(mp::qd_make(w0[q], w1[q], 0.0, 0.0), e);
+        for (int q = 0; q < 4; ++q) Y[q] = fixed_biased_fp<W, S>(w0[q], w1[q], p1, p2);
       } else {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -528,7 +580,9 @@ __device__ __forceinline__ void slice_cols_body(const MatRef &B, int rows, int c
     if constexpr (FIXED) {
       // fixed-point path on the unscaled words (the column exponent enters
       // the shift)
-      const unsigned __int128 Y = fixed_biased_fast<W, S>(vraw, ecol);
+      double p1, p2;
+      fixed_scale<S>(ecol, p1, p2);
+      const unsigned __int128 Y = fixed_biased_fp<W, S>(vraw.x[0], W > 1 ? vraw.x[1] : 0.0, p1, p2);
 #pragma unroll
       for (int s2 = 0; s2 < S; ++s2) {
         const int kb = S - 1 - s2;
