@@ -457,6 +457,14 @@ __device__ __forceinline__ void slice_rows_body(const MatRef &A, int rows, int c
         for (int q = 0; q < 4; ++q) w1[q] = W > 1 ? p[A.plane + q] : 0.0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) Y[q] = fixed_biased_fp<W, S>(w0[q], w1[q], p1, p2);
+      } else if (W == 1 && i < rows && k0 + 3 < cols) {
+        // interior of an fp32 source (one word; widening to fp64 is exact)
+        const float *p = (const float *)A.data + base + k0;
+        float w0[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w0[q] = p[q];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Y[q] = fixed_biased_fp<1, S>((double)w0[q], 0.0, p1, p2);
       } else {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
