@@ -572,6 +572,53 @@ __device__ __forceinline__ void slice_cols_body(const MatRef &B, int rows, int c
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
   const int j0 = blockIdx.x * 32;
   const int b = sel ? sel[bz] : bz;
+  if constexpr (DB == 8 && W <= 2 && S <= 14) {
+    // fixed-point path: each thread splits 4 consecutive k (rows 4 ty .. 4 ty + 3,
+    // coalesced over the warp's 32 columns) of column j0 + tx and packs each
+    // plane's 4 digits into one word (3 PRMT), staged as words in the tile
+    // (one STS per plane instead of four byte stores)
+    uint32_t(*tw)[32][9] = reinterpret_cast<uint32_t(*)[32][9]>(tile);
+    const int j = j0 + tx, kb0 = k0 + 4 * ty;
+    int ecol = 0;
+    if (j < cols) ecol = ecs ? ecs[tx] : out.exps[(long long)b * out.rpad + out.row0 + j];
+    double p1, p2;
+    fixed_scale<S>(ecol, p1, p2);
+    unsigned __int128 Y[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = kb0 + q;
+      double h = 0.0, l = 0.0;
+      if (k < rows && j < cols) {
+        const long long off = (long long)b * B.bstride + (long long)k * B.ld + j;
+        if (fi == F32) {
+          h = (double)((const float *)B.data)[off];
+        } else {
+          h = ((const double *)B.data)[off];
+          if constexpr (W > 1) l = ((const double *)B.data)[off + B.plane];
+        }
+      }
+      Y[q] = fixed_biased_fp<W, S>(h, l, p1, p2);
+    }
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int kb = S - 1 - s, wj = kb >> 2, bsel = kb & 3;
+      const uint32_t lo = __byte_perm(fixed_word(Y[0], wj), fixed_word(Y[1], wj), bsel | ((bsel + 4) << 4));
+      const uint32_t hi = __byte_perm(fixed_word(Y[2], wj), fixed_word(Y[3], wj), bsel | ((bsel + 4) << 4));
+      uint32_t wv = __byte_perm(lo, hi, 0x5410);
+      if (s > 0) wv ^= 0x80808080u;
+      tw[s][tx][ty] = wv;
+    }
+    __syncthreads();
+    const long long plane = out.plane();
+    const int jj = threadIdx.x >> 3, kq = threadIdx.x & 7;
+    const int jo = j0 + jj;
+    if (out.row0 + jo < out.rpad && jo < out.nrows && k0 + 4 * kq < out.kpad)
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+        *reinterpret_cast<uint32_t *>(out.digits + s * plane + ((long long)b * out.rpad + out.row0 + jo) * out.kpad +
+                                      k0 + 4 * kq) = tw[s][jj][kq];
+    return;
+  }
   for (int kk = ty; kk < 32; kk += 8) {
     const int k = k0 + kk, j = j0 + tx;
     mp::qd v = mp::qd_make(0.0, 0.0, 0.0, 0.0);
@@ -617,7 +664,7 @@ __device__ __forceinline__ void slice_cols_body(const MatRef &B, int rows, int c
 
 template <int W, int S>
 __global__ void slice_cols_kernel(MatRef B, int rows, int cols, int fi, SliceRef out, const int *sel) {
-  __shared__ int8_t tile[S][32][36];
+  __shared__ __align__(16) int8_t tile[S][32][36];
   if (oz_db_of<S>(out.db) == 8) {
     if constexpr (S != 16 && S != 31)
       slice_cols_body<W, S, 8>(B, rows, cols, fi, out, sel, tile, blockIdx.y * 32, blockIdx.z);
@@ -633,7 +680,7 @@ __global__ void slice_cols_kernel(MatRef B, int rows, int cols, int fi, SliceRef
 // separate col_exps pass over the matrix.
 template <int W, int S>
 __global__ void slice_cols_fused_kernel(MatRef B, int rows, int cols, int fi, SliceRef out, const int *sel) {
-  __shared__ int8_t tile[S][32][36];
+  __shared__ __align__(16) int8_t tile[S][32][36];
   __shared__ double red[8][33];
   __shared__ int ecs[32];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
