@@ -416,6 +416,74 @@ __device__ __forceinline__ uint32_t fixed_word(const unsigned __int128 &Y, int j
   return (uint32_t)(Y >> (32 * j));
 }
 
+// The S plane words of four consecutive entries (digit s = byte S-1-s of Y;
+// bytes below the top one are offset by 0x80) stored at k0 of each plane.
+template <int S>
+__device__ __forceinline__ void store_plane_words(const unsigned __int128 (&Y)[4], int8_t *o, long long plane, int k0) {
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int kb = S - 1 - s, j = kb >> 2, bsel = kb & 3;
+    const uint32_t lo = __byte_perm(fixed_word(Y[0], j), fixed_word(Y[1], j), bsel | ((bsel + 4) << 4));
+    const uint32_t hi = __byte_perm(fixed_word(Y[2], j), fixed_word(Y[3], j), bsel | ((bsel + 4) << 4));
+    uint32_t wv = __byte_perm(lo, hi, 0x5410);
+    if (s > 0) wv ^= 0x80808080u;
+    *reinterpret_cast<uint32_t *>(o + s * plane + k0) = wv;
+  }
+}
+
+// Register-resident row split for rows of 128 or 256 fp64/dd entries (the
+// cfg2 shapes): every lane loads its entries' words (4 consecutive per 128
+// columns, 16-byte loads) before the row maximum, so one DRAM latency covers
+// the row instead of a max pass followed by a second, dependent load pass.
+template <int W, int S>
+__device__ __forceinline__ void slice_rows_regs(const MatRef &A, long long base, int cols, const SliceRef &out, int b,
+                                                int i, int lane) {
+  constexpr int NIT = 2;
+  double h[NIT][4], l[NIT][4];
+  const double *p = (const double *)A.data + base + 4 * lane;
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    if (it * 128 < cols) {
+      const double2 a0 = *reinterpret_cast<const double2 *>(p + 128 * it);
+      const double2 a1 = *reinterpret_cast<const double2 *>(p + 128 * it + 2);
+      h[it][0] = a0.x; h[it][1] = a0.y; h[it][2] = a1.x; h[it][3] = a1.y;
+      if constexpr (W > 1) {
+        const double2 b0 = *reinterpret_cast<const double2 *>(p + A.plane + 128 * it);
+        const double2 b1 = *reinterpret_cast<const double2 *>(p + A.plane + 128 * it + 2);
+        l[it][0] = b0.x; l[it][1] = b0.y; l[it][2] = b1.x; l[it][3] = b1.y;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) l[it][q] = 0.0;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) h[it][q] = l[it][q] = 0.0;
+    }
+  }
+  double mx = 0.0;
+#pragma unroll
+  for (int it = 0; it < NIT; ++it)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) mx = fmax(mx, fabs(h[it][q]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const int e = row_exponent(mx);
+  if (lane == 0) out.exps[(long long)b * out.rpad + i] = e;
+  double p1, p2;
+  fixed_scale<S>(e, p1, p2);
+  const long long plane = out.plane();
+  int8_t *o = out.digits + ((long long)b * out.rpad + i) * out.kpad;
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    if (it * 128 < cols) {
+      unsigned __int128 Y[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Y[q] = fixed_biased_fp<W, S>(h[it][q], l[it][q], p1, p2);
+      store_plane_words<S>(Y, o, plane, 4 * lane + 128 * it);
+    }
+  }
+}
+
 // Side A: rows scaled by their own max exponent; output [S][b][i][k].
 // One warp per row; each lane splits 4 consecutive entries and stores the 4
 // digits of a plane as one 32-bit word.
@@ -429,6 +497,14 @@ __device__ __forceinline__ void slice_rows_body(const MatRef &A, int rows, int c
   const int i = warp;
   if (i >= out.rpad) return;
   const long long base = (long long)b * A.bstride + (long long)i * A.ld;
+  if constexpr (DB == 8 && W <= 2 && S <= 14) {
+    // warp-uniform: the whole row is interior and 16-byte aligned
+    if (i < rows && fi != F32 && cols == out.kpad && (cols == 128 || cols == 256) && (A.plane & 1) == 0 &&
+        ((reinterpret_cast<uintptr_t>((const double *)A.data + base)) & 15) == 0) {
+      slice_rows_regs<W, S>(A, base, cols, out, b, i, lane);
+      return;
+    }
+  }
   double mx = 0.0;
   if (i < rows)
     for (int k = lane; k < cols; k += 32) {

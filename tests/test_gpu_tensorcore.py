@@ -97,19 +97,20 @@ def test_tc_digit_width_rules(cuda):
     assert h.max_k_8bit() == 4800
 
 
+@pytest.mark.parametrize("n", [96, 256])
 @pytest.mark.parametrize("side", [0, 1])
 @pytest.mark.parametrize("fmt,S", [(31, 14), (15, 8), (7, 4), (31, 8), (31, 4)])
-def test_fixed_point_split_exact(cuda, side, fmt, S):
+def test_fixed_point_split_exact(cuda, side, fmt, S, n):
     """8-bit fixed-point split (fixed_biased_fast): every entry's digit planes
     reproduce round(v 2^(F-e)) to within one unit of 2^(e-F), F = 6 + 8(S-1),
     over entries spanning ~2^-200 .. 1 of their row/column maximum, signs,
-    zeros and normalised dd low words."""
+    zeros and normalised dd low words.  n = 256 takes the register-resident
+    row split (whole 16-byte-aligned rows of 128/256 entries)."""
     import torch
     from paper_2312_17396_b200 import _lib
     from paper_2312_17396_b200.precision import MatBatch
     h = _lib.handle_for()
-    rng = np.random.default_rng(7 + S + fmt + side)
-    n = 96
+    rng = np.random.default_rng(7 + S + fmt + side + n)
     hi = rng.standard_normal((n, n)) * 2.0 ** rng.integers(-200, 1, (n, n)).astype(float)
     hi[rng.random((n, n)) < 0.05] = 0.0
     hi[:, 3] *= 2.0 ** 40          # a column / row with a large maximum
