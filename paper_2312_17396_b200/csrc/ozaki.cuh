@@ -436,14 +436,19 @@ __device__ __forceinline__ void store_plane_words(const unsigned __int128 (&Y)[4
 // columns, 16-byte loads) before the row maximum, so one DRAM latency covers
 // the row instead of a max pass followed by a second, dependent load pass.
 template <int W, int S>
-__device__ __forceinline__ void slice_rows_regs(const MatRef &A, long long base, int cols, const SliceRef &out, int b,
-                                                int i, int lane) {
+__device__ __forceinline__ void slice_rows_regs(const MatRef &A, long long base, int cols, int fi, const SliceRef &out,
+                                                int b, int i, int lane) {
   constexpr int NIT = 2;
   double h[NIT][4], l[NIT][4];
   const double *p = (const double *)A.data + base + 4 * lane;
 #pragma unroll
   for (int it = 0; it < NIT; ++it) {
-    if (it * 128 < cols) {
+    if (W == 1 && fi == F32 && it * 128 < cols) {     // fp32 source: one 16-byte load, exact widening
+      const float4 a = *reinterpret_cast<const float4 *>((const float *)A.data + base + 4 * lane + 128 * it);
+      h[it][0] = a.x; h[it][1] = a.y; h[it][2] = a.z; h[it][3] = a.w;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) l[it][q] = 0.0;
+    } else if (it * 128 < cols) {
       const double2 a0 = *reinterpret_cast<const double2 *>(p + 128 * it);
       const double2 a1 = *reinterpret_cast<const double2 *>(p + 128 * it + 2);
       h[it][0] = a0.x; h[it][1] = a0.y; h[it][2] = a1.x; h[it][3] = a1.y;
@@ -499,9 +504,11 @@ __device__ __forceinline__ void slice_rows_body(const MatRef &A, int rows, int c
   const long long base = (long long)b * A.bstride + (long long)i * A.ld;
   if constexpr (DB == 8 && W <= 2 && S <= 14) {
     // warp-uniform: the whole row is interior and 16-byte aligned
-    if (i < rows && fi != F32 && cols == out.kpad && (cols == 128 || cols == 256) && (A.plane & 1) == 0 &&
-        ((reinterpret_cast<uintptr_t>((const double *)A.data + base)) & 15) == 0) {
-      slice_rows_regs<W, S>(A, base, cols, out, b, i, lane);
+    const bool f32 = fi == F32;
+    if (i < rows && (W == 1 || !f32) && cols == out.kpad && (cols == 128 || cols == 256) && (f32 || (A.plane & 1) == 0) &&
+        ((f32 ? reinterpret_cast<uintptr_t>((const float *)A.data + base)
+              : reinterpret_cast<uintptr_t>((const double *)A.data + base)) & 15) == 0) {
+      slice_rows_regs<W, S>(A, base, cols, fi, out, b, i, lane);
       return;
     }
   }
@@ -607,7 +614,7 @@ __device__ __forceinline__ void slice_rows_body(const MatRef &A, int rows, int c
 }
 
 template <int W, int S>
-__global__ void slice_rows_kernel(MatRef A, int rows, int cols, int fi, SliceRef out, const int *sel) {
+__global__ void __launch_bounds__(256, (W <= 2 && S <= 14) ? 3 : 1) slice_rows_kernel(MatRef A, int rows, int cols, int fi, SliceRef out, const int *sel) {
   if (oz_db_of<S>(out.db) == 8) {
     if constexpr (S != 16 && S != 31) slice_rows_body<W, S, 8>(A, rows, cols, fi, out, sel);
   } else {
