@@ -1319,7 +1319,8 @@ static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices
   if (W == WW && S == SS) oz::slice_rows_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
     SR(1, 4) SR(1, 8) SR(1, 14) SR(1, 16) SR(1, 28) SR(1, 31) SR(2, 4) SR(2, 8) SR(2, 14) SR(2, 16) SR(2, 28)
     SR(2, 31) SR(4, 4) SR(4, 8) SR(4, 14) SR(4, 16) SR(4, 28) SR(4, 31)
-    SR(1, 2) SR(1, 3) SR(1, 5) SR(1, 6) SR(2, 2) SR(2, 3) SR(2, 5) SR(2, 6) SR(2, 10) SR(2, 12) {}
+    SR(1, 2) SR(1, 3) SR(1, 5) SR(1, 6) SR(2, 2) SR(2, 3) SR(2, 5) SR(2, 6) SR(2, 10) SR(2, 12)
+    return set_err(h, MPPS_EINVAL, "slice: no row kernel for %d words x %d planes", W, S);
 #undef SR
     return after_launch(h, "slice_rows_kernel");
   }
@@ -1328,7 +1329,9 @@ static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices
 #define SCF(WW, SS) \
   if (W == WW && S == SS) oz::slice_cols_fused_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
     SCF(1, 4) SCF(1, 8) SCF(1, 14) SCF(1, 16) SCF(1, 28) SCF(1, 31) SCF(2, 4) SCF(2, 8) SCF(2, 14) SCF(2, 16) SCF(2, 28)
-    SCF(2, 31) SCF(4, 4) SCF(4, 8) SCF(4, 14) SCF(4, 16) SCF(4, 28) SCF(4, 31) {}
+    SCF(2, 31) SCF(4, 4) SCF(4, 8) SCF(4, 14) SCF(4, 16) SCF(4, 28) SCF(4, 31)
+    SCF(1, 2) SCF(1, 3) SCF(1, 5) SCF(1, 6) SCF(2, 2) SCF(2, 3) SCF(2, 5) SCF(2, 6) SCF(2, 10) SCF(2, 12)
+    return set_err(h, MPPS_EINVAL, "slice: no column kernel for %d words x %d planes", W, S);
 #undef SCF
     return after_launch(h, "slice_cols_fused_kernel");
   }
@@ -1340,7 +1343,8 @@ static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices
   if (W == WW && S == SS) oz::slice_cols_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
   SC(1, 4) SC(1, 8) SC(1, 14) SC(1, 16) SC(1, 28) SC(1, 31) SC(2, 4) SC(2, 8) SC(2, 14) SC(2, 16) SC(2, 28)
   SC(2, 31) SC(4, 4) SC(4, 8) SC(4, 14) SC(4, 16) SC(4, 28) SC(4, 31)
-  SC(1, 2) SC(1, 3) SC(1, 5) SC(1, 6) SC(2, 2) SC(2, 3) SC(2, 5) SC(2, 6) SC(2, 10) SC(2, 12) {}
+  SC(1, 2) SC(1, 3) SC(1, 5) SC(1, 6) SC(2, 2) SC(2, 3) SC(2, 5) SC(2, 6) SC(2, 10) SC(2, 12)
+  return set_err(h, MPPS_EINVAL, "slice: no column kernel for %d words x %d planes", W, S);
 #undef SC
   return after_launch(h, "slice_cols_kernel");
 }
