@@ -10,6 +10,15 @@
 // intrinsics so nvcc cannot contract or reassociate them.
 #pragma once
 #include <cuda_runtime.h>
+
+// Programmatic dependent launch: first statement of every kernel the host
+// launches with programmaticStreamSerialization (mpps_capi.cu launch_k).  The
+// wait returns once the preceding kernel in the stream has completed and its
+// writes are visible (a no-op for an ordinary launch), so nothing of the
+// predecessor is read or overwritten early; the trigger lets the next kernel's
+// CTAs be placed on SMs freed by this grid's last wave.
+#define MPPS_PDL_ENTER() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+
 #include <stdint.h>
 
 #define MP_INLINE __device__ __forceinline__

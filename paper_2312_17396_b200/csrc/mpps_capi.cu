@@ -19,6 +19,35 @@
 #include "gemm.cuh"
 #include "ozaki.cuh"
 
+// Launch with programmatic stream serialization (PDL) when MPPS_PDL=1: the
+// kernel's CTA placement overlaps the predecessor's tail; every kernel
+// launched here begins with MPPS_PDL_ENTER() (mp_arith.cuh).  Off by default:
+// the graphed cfg2 step measured the same with and without it (47.96K / 47.03K
+// vs 47.83K evals/s on one box), i.e. the step is not launch-gap bound.
+static bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MPPS_PDL");
+    v = e ? atoi(e) : 0;
+  }
+  return v != 0;
+}
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+
 using namespace mpps;
 
 struct mpps_handle {
@@ -197,6 +226,7 @@ struct ConvertArgs {
 
 template <int FO>
 __global__ void convert_kernel(const ConvertArgs a) {
+  MPPS_PDL_ENTER();
   const int b = a.sel ? a.sel[blockIdx.z] : (int)blockIdx.z;
   const long long total = (long long)a.rows * a.cols;
   const int e = a.exp ? a.exp[b] : 0;
@@ -421,6 +451,7 @@ __global__ void colsum_kernel(const ColsumArgs a) {
 
 // norms[b][k] = max_col sum_chunk partial[b][chunk][k][col]  (fixed order)
 __global__ void norm_reduce_kernel(const double *partial, double *norms, int nblk, int nchunk, int cols) {
+  MPPS_PDL_ENTER();
   const int k = blockIdx.x, b = blockIdx.y;
   double best = 0.0;
   for (int col = threadIdx.x; col < cols; col += blockDim.x) {
@@ -515,6 +546,7 @@ template <int WF, int NB, int NP, int ND = NB>
 #define MPPS_ASMC_MINB 8
 #endif
 __global__ void __launch_bounds__(128, MPPS_ASMC_MINB) assemble_c_kernel(const __grid_constant__ AssembleCArgs<NB, NP> a) {
+  MPPS_PDL_ENTER();
   using V = WV<WF>;
   using T = typename V::T;
   using Acc = typename V::Acc;
@@ -629,6 +661,7 @@ __global__ void scalar_top_kernel(const ScalarTopArgs a) {
 // scalar_top_kernel, which remains for mixed-format operands.
 template <int WF, int FT, int FO>
 __global__ void scalar_top_wf_kernel(const ScalarTopArgs a) {
+  MPPS_PDL_ENTER();
   using V = WV<WF>;
   const int b = a.sel ? a.sel[blockIdx.z] : (int)blockIdx.z;
   const int eo = a.exp_out ? a.exp_out[b] : 0;
@@ -757,16 +790,16 @@ static int launch_assemble_c(mpps_handle *h, const mpps_mat *powers, int m, cons
   a.nchunk = (rows + kAsmRows - 1) / kAsmRows;
   if (!norms) {
     a.partial = nullptr;
-    assemble_c_kernel<WF, NB, NP, ND><<<dim3((cols + 127) / 128, a.nchunk, batch), 128, 0, h->stream>>>(a);
+    launch_k(assemble_c_kernel<WF, NB, NP, ND>, dim3(dim3((cols + 127) / 128, a.nchunk, batch)), dim3(128), 0, h->stream, a);
     return after_launch(h, "assemble_c_kernel");
   }
   size_t pbytes = sizeof(double) * (size_t)batch * a.nchunk * (NB + 1) * cols;
   cudaError_t e = cudaMallocAsync((void **)&a.partial, pbytes, h->stream);
   if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "assemble scratch: %s", cudaGetErrorString(e));
-  assemble_c_kernel<WF, NB, NP, ND><<<dim3((cols + 127) / 128, a.nchunk, batch), 128, 0, h->stream>>>(a);
+  launch_k(assemble_c_kernel<WF, NB, NP, ND>, dim3(dim3((cols + 127) / 128, a.nchunk, batch)), dim3(128), 0, h->stream, a);
   int rc = after_launch(h, "assemble_c_kernel");
   if (rc) return rc;
-  norm_reduce_kernel<<<dim3(NB + 1, batch), 256, 0, h->stream>>>(a.partial, norms, NB + 1, a.nchunk, cols);
+  launch_k(norm_reduce_kernel, dim3(dim3(NB + 1, batch)), dim3(256), 0, h->stream, a.partial, norms, NB + 1, a.nchunk, cols);
   rc = after_launch(h, "norm_reduce_kernel");
   cudaFreeAsync(a.partial, h->stream);
   return rc;
@@ -837,10 +870,10 @@ int mpps_convert(mpps_handle *h, const mpps_mat *src, mpps_mat *dst, const int *
   a.sel = sel; a.exp = exp;
   dim3 grid(ew_grid((long long)a.rows * a.cols / 4 + 1), 1, nb);
   switch (fmt_index(dst->fmt)) {
-    case F32: convert_kernel<F32><<<grid, 256, 0, h->stream>>>(a); break;
-    case F64: convert_kernel<F64><<<grid, 256, 0, h->stream>>>(a); break;
-    case DD: convert_kernel<DD><<<grid, 256, 0, h->stream>>>(a); break;
-    case QD: convert_kernel<QD><<<grid, 256, 0, h->stream>>>(a); break;
+    case F32: launch_k(convert_kernel<F32>, dim3(grid), dim3(256), 0, h->stream, a); break;
+    case F64: launch_k(convert_kernel<F64>, dim3(grid), dim3(256), 0, h->stream, a); break;
+    case DD: launch_k(convert_kernel<DD>, dim3(grid), dim3(256), 0, h->stream, a); break;
+    case QD: launch_k(convert_kernel<QD>, dim3(grid), dim3(256), 0, h->stream, a); break;
   }
   return after_launch(h, "convert_kernel");
 }
@@ -941,7 +974,7 @@ static int assemble_common(mpps_handle *h, const mpps_mat *powers, int s, int m,
   int rc = after_launch(h, "assemble_kernel");
   if (rc) return rc;
   if (norms) {
-    norm_reduce_kernel<<<dim3(r + 2, batch), 256, 0, h->stream>>>(a.partial, norms, r + 2, a.nchunk, cols);
+    launch_k(norm_reduce_kernel, dim3(dim3(r + 2, batch)), dim3(256), 0, h->stream, a.partial, norms, r + 2, a.nchunk, cols);
     rc = after_launch(h, "norm_reduce_kernel");
   } else {
     long long tot = (long long)batch * (r + 2) * cols;
@@ -1070,7 +1103,7 @@ int mpps_colmax(mpps_handle *h, const double *colsums, int nvec, int cols, int b
   if (!colsums || !out || nvec < 1 || cols < 1 || batch < 0) return set_err(h, MPPS_EINVAL, "colmax: bad arguments");
   if (batch == 0) return MPPS_OK;
   // colsums laid out [batch][nvec][cols] == partial layout with nchunk = 1
-  norm_reduce_kernel<<<dim3(nvec, batch), 256, 0, h->stream>>>(colsums, out, nvec, 1, cols);
+  launch_k(norm_reduce_kernel, dim3(dim3(nvec, batch)), dim3(256), 0, h->stream, colsums, out, nvec, 1, cols);
   return after_launch(h, "norm_reduce_kernel");
 }
 
@@ -1089,7 +1122,7 @@ int mpps_one_norm(mpps_handle *h, const mpps_mat *A, double *norms) {
   colsum_kernel<<<dim3((A->cols + 127) / 128, a.nchunk, A->batch), 128, 0, h->stream>>>(a);
   rc = after_launch(h, "colsum_kernel");
   if (rc) return rc;
-  norm_reduce_kernel<<<dim3(1, A->batch), 256, 0, h->stream>>>(a.partial, norms, 1, a.nchunk, A->cols);
+  launch_k(norm_reduce_kernel, dim3(dim3(1, A->batch)), dim3(256), 0, h->stream, a.partial, norms, 1, a.nchunk, A->cols);
   rc = after_launch(h, "norm_reduce_kernel");
   cudaFreeAsync(a.partial, h->stream);
   return rc;
@@ -1125,6 +1158,7 @@ int mpps_one_norm_complex(mpps_handle *h, const mpps_mat *A, int nc, double *nor
 // exp_y[b] = e of ||Y|| (norms column r+1).
 __global__ void level_exps_kernel(const double *norms, int batch, int r, unsigned long long fp32_mask, int *exps,
                                   int *exp_y) {
+  MPPS_PDL_ENTER();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int nl = r + 2;
   if (t >= batch * nl) return;
@@ -1142,7 +1176,7 @@ int mpps_level_exps(mpps_handle *h, const double *norms, int batch, int r, unsig
   if (batch < 0 || r < 0 || r + 2 > 64) return set_err(h, MPPS_EINVAL, "level_exps: bad batch %d / r %d", batch, r);
   const long long n = (long long)batch * (r + 2);
   if (n == 0) return MPPS_OK;
-  level_exps_kernel<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(norms, batch, r, fp32_mask, exps, exp_y);
+  launch_k(level_exps_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, h->stream, norms, batch, r, fp32_mask, exps, exp_y);
   return after_launch(h, "level_exps_kernel");
 }
 
@@ -1193,14 +1227,14 @@ int mpps_horner_scalar_top(mpps_handle *h, const double *bm, int fmt_top, const 
   // dd Y with an fp64 B_{r-1} (two-pass block assembly: blocks of fp32 /
   // fp64 levels are assembled in fp64): the fp64 fast path of the dd kernel
   if (wf == DD && fmt_index(Bprev->fmt) == F64 && (ft == F32 || ft == F64) && (fo == F32 || fo == F64)) {
-    if (ft == F32 && fo == F32) scalar_top_wf_kernel<DD, F32, F32><<<grid, tpb, 0, h->stream>>>(a);
-    else if (ft == F32) scalar_top_wf_kernel<DD, F32, F64><<<grid, tpb, 0, h->stream>>>(a);
-    else scalar_top_wf_kernel<DD, F64, F64><<<grid, tpb, 0, h->stream>>>(a);
+    if (ft == F32 && fo == F32) launch_k(scalar_top_wf_kernel<DD, F32, F32>, dim3(grid), dim3(tpb), 0, h->stream, a);
+    else if (ft == F32) launch_k(scalar_top_wf_kernel<DD, F32, F64>, dim3(grid), dim3(tpb), 0, h->stream, a);
+    else launch_k(scalar_top_wf_kernel<DD, F64, F64>, dim3(grid), dim3(tpb), 0, h->stream, a);
     return after_launch(h, "scalar_top_kernel");
   }
   if (fmt_index(Bprev->fmt) == wf && ft <= wf) {
 #define SW(W, A, B) \
-  if (wf == W && ft == A && fo == B) scalar_top_wf_kernel<W, A, B><<<grid, tpb, 0, h->stream>>>(a); else
+  if (wf == W && ft == A && fo == B) launch_k(scalar_top_wf_kernel<W, A, B>, dim3(grid), dim3(tpb), 0, h->stream, a); else
 #define SWF(W) SW(W, F32, F32) SW(W, F32, F64) SW(W, F32, DD) SW(W, F32, QD) SW(W, F64, F64) SW(W, F64, DD) \
   SW(W, F64, QD) SW(W, DD, DD) SW(W, DD, QD) SW(W, QD, QD)
     SWF(F64) SWF(DD) SWF(QD) { return set_err(h, MPPS_EFMT, "scalar_top: formats"); }
@@ -1316,7 +1350,7 @@ static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices
   if (side == 0) {
     dim3 grid((out->rpad * 32 + 255) / 256, nb);
 #define SR(WW, SS) \
-  if (W == WW && S == SS) oz::slice_rows_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
+  if (W == WW && S == SS) launch_k(oz::slice_rows_kernel<WW, SS>, dim3(grid), dim3(256), 0, h->stream, ref_of(src), src->rows, src->cols, fi, o, sel); else
     SR(1, 4) SR(1, 8) SR(1, 14) SR(1, 16) SR(1, 28) SR(1, 31) SR(2, 4) SR(2, 8) SR(2, 14) SR(2, 16) SR(2, 28)
     SR(2, 31) SR(4, 4) SR(4, 8) SR(4, 14) SR(4, 16) SR(4, 28) SR(4, 31)
     SR(1, 2) SR(1, 3) SR(1, 5) SR(1, 6) SR(2, 2) SR(2, 3) SR(2, 5) SR(2, 6) SR(2, 10) SR(2, 12)
@@ -1327,7 +1361,7 @@ static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices
   if (oz_cols_fused() && nrows < 0) {
     dim3 grid(out->rpad / 32, nb);
 #define SCF(WW, SS) \
-  if (W == WW && S == SS) oz::slice_cols_fused_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
+  if (W == WW && S == SS) launch_k(oz::slice_cols_fused_kernel<WW, SS>, dim3(grid), dim3(256), 0, h->stream, ref_of(src), src->rows, src->cols, fi, o, sel); else
     SCF(1, 4) SCF(1, 8) SCF(1, 14) SCF(1, 16) SCF(1, 28) SCF(1, 31) SCF(2, 4) SCF(2, 8) SCF(2, 14) SCF(2, 16) SCF(2, 28)
     SCF(2, 31) SCF(4, 4) SCF(4, 8) SCF(4, 14) SCF(4, 16) SCF(4, 28) SCF(4, 31)
     SCF(1, 2) SCF(1, 3) SCF(1, 5) SCF(1, 6) SCF(2, 2) SCF(2, 3) SCF(2, 5) SCF(2, 6) SCF(2, 10) SCF(2, 12)
@@ -1335,12 +1369,12 @@ static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices
 #undef SCF
     return after_launch(h, "slice_cols_fused_kernel");
   }
-  oz::col_exps_kernel<<<dim3(gx, nb), 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel);
+  launch_k(oz::col_exps_kernel, dim3(dim3(gx, nb)), dim3(256), 0, h->stream, ref_of(src), src->rows, src->cols, fi, o, sel);
   rc = after_launch(h, "col_exps_kernel");
   if (rc) return rc;
   dim3 grid(gx, out->kpad / 32, nb);
 #define SC(WW, SS) \
-  if (W == WW && S == SS) oz::slice_cols_kernel<WW, SS><<<grid, 256, 0, h->stream>>>(ref_of(src), src->rows, src->cols, fi, o, sel); else
+  if (W == WW && S == SS) launch_k(oz::slice_cols_kernel<WW, SS>, dim3(grid), dim3(256), 0, h->stream, ref_of(src), src->rows, src->cols, fi, o, sel); else
   SC(1, 4) SC(1, 8) SC(1, 14) SC(1, 16) SC(1, 28) SC(1, 31) SC(2, 4) SC(2, 8) SC(2, 14) SC(2, 16) SC(2, 28)
   SC(2, 31) SC(4, 4) SC(4, 8) SC(4, 14) SC(4, 16) SC(4, 28) SC(4, 31)
   SC(1, 2) SC(1, 3) SC(1, 5) SC(1, 6) SC(2, 2) SC(2, 3) SC(2, 5) SC(2, 6) SC(2, 10) SC(2, 12)
@@ -1411,7 +1445,7 @@ static int launch_oz_tma(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
   t.group = oz_group();
   dim3 grid(t.mtiles * t.ntiles, 1, nb);
   if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
-  oz::oz_gemm_tma_kernel<S, NT, FO, MODE, EW><<<grid, 32 * EW, smem, h->stream>>>(t);
+  launch_k(oz::oz_gemm_tma_kernel<S, NT, FO, MODE, EW>, dim3(grid), dim3(32 * EW), smem, h->stream, t);
   return after_launch(h, "oz_gemm_tma_kernel");
 }
 
@@ -1485,7 +1519,7 @@ static int launch_oz_ring(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
   t.group = oz_group();
   dim3 grid(t.mtiles * t.ntiles, 1, nb);
   if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
-  oz::oz_gemm_ring_kernel<S, NT, FO, MODE, EW><<<grid, 32 * EW, smem, h->stream>>>(t);
+  launch_k(oz::oz_gemm_ring_kernel<S, NT, FO, MODE, EW>, dim3(grid), dim3(32 * EW), smem, h->stream, t);
   return after_launch(h, "oz_gemm_ring_kernel");
 }
 

@@ -615,6 +615,7 @@ __device__ __forceinline__ void slice_rows_body(const MatRef &A, int rows, int c
 
 template <int W, int S>
 __global__ void __launch_bounds__(256, (W <= 2 && S <= 14) ? 3 : 1) slice_rows_kernel(MatRef A, int rows, int cols, int fi, SliceRef out, const int *sel) {
+  MPPS_PDL_ENTER();
   if (oz_db_of<S>(out.db) == 8) {
     if constexpr (S != 16 && S != 31) slice_rows_body<W, S, 8>(A, rows, cols, fi, out, sel);
   } else {
@@ -626,6 +627,7 @@ __global__ void __launch_bounds__(256, (W <= 2 && S <= 14) ? 3 : 1) slice_rows_k
 // scans every 8th row of its column (coalesced across the warp), then a
 // shared-memory max over the 8 groups.
 __global__ void col_exps_kernel(MatRef B, int rows, int cols, int fi, SliceRef out, const int *sel) {
+  MPPS_PDL_ENTER();
   __shared__ double red[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + tx;
@@ -747,6 +749,7 @@ __device__ __forceinline__ void slice_cols_body(const MatRef &B, int rows, int c
 
 template <int W, int S>
 __global__ void slice_cols_kernel(MatRef B, int rows, int cols, int fi, SliceRef out, const int *sel) {
+  MPPS_PDL_ENTER();
   __shared__ __align__(16) int8_t tile[S][32][36];
   if (oz_db_of<S>(out.db) == 8) {
     if constexpr (S != 16 && S != 31)
@@ -763,6 +766,7 @@ __global__ void slice_cols_kernel(MatRef B, int rows, int cols, int fi, SliceRef
 // separate col_exps pass over the matrix.
 template <int W, int S>
 __global__ void slice_cols_fused_kernel(MatRef B, int rows, int cols, int fi, SliceRef out, const int *sel) {
+  MPPS_PDL_ENTER();
   __shared__ __align__(16) int8_t tile[S][32][36];
   __shared__ double red[8][33];
   __shared__ int ecs[32];
@@ -1446,6 +1450,7 @@ __device__ __forceinline__ unsigned long long *oz_trace_begin(const OzTmaArgs &a
 
 template <int S, int NT, int FO, int MODE, int EW = 8>
 __global__ void __launch_bounds__(32 * EW, EW == 8 ? oz_ctas_per_sm<S, MODE, NT>() : 1) oz_gemm_tma_kernel(const __grid_constant__ OzTmaArgs args) {
+  MPPS_PDL_ENTER();
   constexpr int STAGES = oz_tma_stages<S, NT, FO, MODE>();
   static_assert(STAGES >= 1, "stage ring does not fit");
   constexpr uint32_t STAGE = (uint32_t)oz_stage_bytes<S, NT>();
@@ -1585,6 +1590,7 @@ __host__ __device__ constexpr size_t oz_ring_smem_bytes() {
 
 template <int S, int NT, int FO, int MODE, int EW = 8>
 __global__ void __launch_bounds__(32 * EW, 1) oz_gemm_ring_kernel(const __grid_constant__ OzTmaArgs args) {
+  MPPS_PDL_ENTER();
   constexpr uint32_t EBUF = oz_ring_ebuf<S, NT, FO, MODE>();
   using R = OzRing<S, NT, EBUF>;
   constexpr uint32_t A_SLICE = kTileM * kKStep;
