@@ -1289,6 +1289,18 @@ static oz::SliceRef sref(const mpps_slices *s) {
 // column split with the exponents in the same kernel (MPPS_OZ_COLS_FUSED=1).
 // Measured slower at cfg2 (dd split 37 + 8 -> 66 us: one CTA per 32-column
 // strip leaves too few CTAs in flight), so off by default.
+// MPPS_OZ_COLS_CLUSTER=1: one-pass cluster column split for K <= 256.  Off by
+// default: at cfg2 it measured 40.5 / 36.7 / 36.3 us for <2,14> / <2,10> /
+// <1,14> against 39.5 / 35.9 / 33.0 for col_exps_kernel + slice_cols_kernel
+// (the cluster barrier between the loads and the split serialises them)
+static bool oz_cols_cluster() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MPPS_OZ_COLS_CLUSTER");
+    v = e ? atoi(e) : 0;
+  }
+  return v != 0;
+}
 static bool oz_cols_fused() {
   static int v = -1;
   if (v < 0) {
@@ -1368,6 +1380,30 @@ static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices
     return set_err(h, MPPS_EINVAL, "slice: no column kernel for %d words x %d planes", W, S);
 #undef SCF
     return after_launch(h, "slice_cols_fused_kernel");
+  }
+  if (slice_db(out) == 8 && W <= 2 && S <= 14 && out->kpad / 32 <= 8 && oz_cols_cluster()) {
+    // one cluster of kpad/32 CTAs per 32-column strip: exponents and digits in one pass
+    const unsigned ky = (unsigned)(out->kpad / 32);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(gx, ky, nb);
+    cfg.blockDim = dim3(256);
+    cfg.stream = h->stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 1;
+    at[0].val.clusterDim.y = ky;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+#define SCC(WW, SS) \
+  if (W == WW && S == SS) cudaLaunchKernelEx(&cfg, oz::slice_cols_cluster_kernel<WW, SS>, ref_of(src), src->rows, src->cols, fi, o, sel); else
+    SCC(1, 2) SCC(1, 3) SCC(1, 4) SCC(1, 5) SCC(1, 6) SCC(1, 8) SCC(1, 10) SCC(1, 12) SCC(1, 14)
+    SCC(2, 2) SCC(2, 3) SCC(2, 4) SCC(2, 5) SCC(2, 6) SCC(2, 8) SCC(2, 10) SCC(2, 12) SCC(2, 14)
+    return set_err(h, MPPS_EINVAL, "slice: no cluster column kernel for %d words x %d planes", W, S);
+#undef SCC
+    return after_launch(h, "slice_cols_cluster_kernel");
   }
   launch_k(oz::col_exps_kernel, dim3(dim3(gx, nb)), dim3(256), 0, h->stream, ref_of(src), src->rows, src->cols, fi, o, sel);
   rc = after_launch(h, "col_exps_kernel");

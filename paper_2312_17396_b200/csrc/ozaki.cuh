@@ -22,6 +22,7 @@
 // between 8-row groups.
 #pragma once
 #include <cuda.h>
+#include <cooperative_groups.h>
 #include "gemm.cuh"
 
 namespace mpps {
@@ -758,6 +759,87 @@ __global__ void slice_cols_kernel(MatRef B, int rows, int cols, int fi, SliceRef
     if constexpr (oz_has7<S>())
       slice_cols_body<W, S, 7>(B, rows, cols, fi, out, sel, tile, blockIdx.y * 32, blockIdx.z);
   }
+}
+
+// Column exponents and digits in one pass for K <= 256 (8-bit digits, <= 14
+// planes): the kpad/32 CTAs of a 32-column strip form one thread-block
+// cluster; each CTA loads its 32 x 32 tile once (4 consecutive k per thread),
+// publishes its partial column maxima in shared memory, reads the other CTAs'
+// over DSMEM, and splits the registers it already holds.  Replaces
+// col_exps_kernel's separate pass over the matrix (3 launches per cfg2 step).
+template <int W, int S>
+__global__ void __launch_bounds__(256) slice_cols_cluster_kernel(MatRef B, int rows, int cols, int fi, SliceRef out,
+                                                                 const int *sel) {
+  MPPS_PDL_ENTER();
+  namespace cg = cooperative_groups;
+  static_assert(W <= 2 && S <= 14, "fixed-point column split");
+  __shared__ __align__(16) uint32_t tw[S][32][9];
+  __shared__ double red[8][33];
+  __shared__ double cmax[32];
+  __shared__ int ecs[32];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int j0 = blockIdx.x * 32, j = j0 + tx;
+  const int k0 = blockIdx.y * 32, kb0 = k0 + 4 * ty;
+  const int b = sel ? sel[blockIdx.z] : (int)blockIdx.z;
+  double h[4], l[4];
+  double mx = 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int k = kb0 + q;
+    h[q] = 0.0;
+    l[q] = 0.0;
+    if (k < rows && j < cols) {
+      const long long off = (long long)b * B.bstride + (long long)k * B.ld + j;
+      if (fi == F32) {
+        h[q] = (double)((const float *)B.data)[off];
+      } else {
+        h[q] = ((const double *)B.data)[off];
+        if constexpr (W > 1) l[q] = ((const double *)B.data)[off + B.plane];
+      }
+    }
+    mx = fmax(mx, fabs(h[q]));
+  }
+  red[ty][tx] = mx;
+  __syncthreads();
+  if (ty == 0) {
+#pragma unroll
+    for (int g = 1; g < 8; ++g) mx = fmax(mx, red[g][tx]);
+    cmax[tx] = mx;
+  }
+  cluster.sync();                                   // every CTA's partial maxima visible
+  if (ty == 0) {
+    const int nr = (int)cluster.num_blocks();
+    double m = 0.0;
+    for (int r = 0; r < nr; ++r) m = fmax(m, cluster.map_shared_rank(cmax, r)[tx]);
+    const int e = row_exponent(m);
+    ecs[tx] = e;
+    if (blockIdx.y == 0 && out.row0 + j < out.rpad && j < out.nrows) out.exps[(long long)b * out.rpad + out.row0 + j] = e;
+  }
+  cluster.sync();                                   // remote reads done (no CTA exits early); ecs visible
+  double p1, p2;
+  fixed_scale<S>(j < cols ? ecs[tx] : 0, p1, p2);
+  unsigned __int128 Y[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) Y[q] = fixed_biased_fp<W, S>(h[q], l[q], p1, p2);
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int kb = S - 1 - s, wj = kb >> 2, bsel = kb & 3;
+    const uint32_t lo = __byte_perm(fixed_word(Y[0], wj), fixed_word(Y[1], wj), bsel | ((bsel + 4) << 4));
+    const uint32_t hi = __byte_perm(fixed_word(Y[2], wj), fixed_word(Y[3], wj), bsel | ((bsel + 4) << 4));
+    uint32_t wv = __byte_perm(lo, hi, 0x5410);
+    if (s > 0) wv ^= 0x80808080u;
+    tw[s][tx][ty] = wv;
+  }
+  __syncthreads();
+  const long long plane = out.plane();
+  const int jj = threadIdx.x >> 3, kq = threadIdx.x & 7;
+  const int jo = j0 + jj;
+  if (out.row0 + jo < out.rpad && jo < out.nrows && k0 + 4 * kq < out.kpad)
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+      *reinterpret_cast<uint32_t *>(out.digits + s * plane + ((long long)b * out.rpad + out.row0 + jo) * out.kpad + k0 +
+                                    4 * kq) = tw[s][jj][kq];
 }
 
 // Column exponents and digits in one kernel: a CTA owns a strip of 32
