@@ -1289,6 +1289,15 @@ static oz::SliceRef sref(const mpps_slices *s) {
 // column split with the exponents in the same kernel (MPPS_OZ_COLS_FUSED=1).
 // Measured slower at cfg2 (dd split 37 + 8 -> 66 us: one CTA per 32-column
 // strip leaves too few CTAs in flight), so off by default.
+// MPPS_OZ_COLS_FIXED=0 restores slice_cols_kernel (32 x 32 tiles) for 8-bit splits
+static bool oz_cols_fixed() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MPPS_OZ_COLS_FIXED");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
 // MPPS_OZ_COLS_CLUSTER=1: one-pass cluster column split for K <= 256.  Off by
 // default: at cfg2 it measured 40.5 / 36.7 / 36.3 us for <2,14> / <2,10> /
 // <1,14> against 39.5 / 35.9 / 33.0 for col_exps_kernel + slice_cols_kernel
@@ -1408,6 +1417,16 @@ static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices
   launch_k(oz::col_exps_kernel, dim3(dim3(gx, nb)), dim3(256), 0, h->stream, ref_of(src), src->rows, src->cols, fi, o, sel);
   rc = after_launch(h, "col_exps_kernel");
   if (rc) return rc;
+  if (slice_db(out) == 8 && W <= 2 && S <= 14 && oz_cols_fixed()) {
+    dim3 gridf(gx, (out->kpad + 63) / 64, nb);
+#define SCX(WW, SS) \
+  if (W == WW && S == SS) launch_k(oz::slice_cols_fixed_kernel<WW, SS>, gridf, dim3(256), 0, h->stream, ref_of(src), src->rows, src->cols, fi, o, sel); else
+    SCX(1, 2) SCX(1, 3) SCX(1, 4) SCX(1, 5) SCX(1, 6) SCX(1, 8) SCX(1, 10) SCX(1, 12) SCX(1, 14)
+    SCX(2, 2) SCX(2, 3) SCX(2, 4) SCX(2, 5) SCX(2, 6) SCX(2, 8) SCX(2, 10) SCX(2, 12) SCX(2, 14)
+    return set_err(h, MPPS_EINVAL, "slice: no fixed column kernel for %d words x %d planes", W, S);
+#undef SCX
+    return after_launch(h, "slice_cols_fixed_kernel");
+  }
   dim3 grid(gx, out->kpad / 32, nb);
 #define SC(WW, SS) \
   if (W == WW && S == SS) launch_k(oz::slice_cols_kernel<WW, SS>, dim3(grid), dim3(256), 0, h->stream, ref_of(src), src->rows, src->cols, fi, o, sel); else

@@ -748,6 +748,72 @@ __device__ __forceinline__ void slice_cols_body(const MatRef &B, int rows, int c
                                     k0 + kq) = *reinterpret_cast<const uint32_t *>(&tile[s][jj][kq]);
 }
 
+// Fixed-point column split (8-bit digits, <= 14 planes), 32 columns x 64 k per
+// CTA: each thread splits 2 x 4 consecutive k of its column (8 loads in
+// flight), packs plane words and stages them in a [S][32 j][16 k-words] tile
+// for coalesced 32-byte row segments.  Column exponents from col_exps_kernel.
+template <int W, int S>
+__global__ void __launch_bounds__(256) slice_cols_fixed_kernel(MatRef B, int rows, int cols, int fi, SliceRef out,
+                                                               const int *sel) {
+  MPPS_PDL_ENTER();
+  static_assert(W <= 2 && S <= 14, "fixed-point column split");
+  __shared__ __align__(16) uint32_t tw[S][32][17];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int j0 = blockIdx.x * 32, j = j0 + tx;
+  const int k0 = blockIdx.y * 64;
+  const int b = sel ? sel[blockIdx.z] : (int)blockIdx.z;
+  int ecol = 0;
+  if (j < cols) ecol = out.exps[(long long)b * out.rpad + out.row0 + j];
+  double h[2][4], l[2][4];
+#pragma unroll
+  for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = k0 + 32 * hf + 4 * ty + q;
+      h[hf][q] = 0.0;
+      l[hf][q] = 0.0;
+      if (k < rows && j < cols) {
+        const long long off = (long long)b * B.bstride + (long long)k * B.ld + j;
+        if (fi == F32) {
+          h[hf][q] = (double)((const float *)B.data)[off];
+        } else {
+          h[hf][q] = ((const double *)B.data)[off];
+          if constexpr (W > 1) l[hf][q] = ((const double *)B.data)[off + B.plane];
+        }
+      }
+    }
+  double p1, p2;
+  fixed_scale<S>(ecol, p1, p2);
+#pragma unroll
+  for (int hf = 0; hf < 2; ++hf) {
+    unsigned __int128 Y[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) Y[q] = fixed_biased_fp<W, S>(h[hf][q], l[hf][q], p1, p2);
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int kb = S - 1 - s, wj = kb >> 2, bsel = kb & 3;
+      const uint32_t lo = __byte_perm(fixed_word(Y[0], wj), fixed_word(Y[1], wj), bsel | ((bsel + 4) << 4));
+      const uint32_t hi = __byte_perm(fixed_word(Y[2], wj), fixed_word(Y[3], wj), bsel | ((bsel + 4) << 4));
+      uint32_t wv = __byte_perm(lo, hi, 0x5410);
+      if (s > 0) wv ^= 0x80808080u;
+      tw[s][tx][8 * hf + ty] = wv;
+    }
+  }
+  __syncthreads();
+  const long long plane = out.plane();
+  // 16 words (64 k) per column: thread -> (column jj, word kq), two passes of 16 columns
+#pragma unroll
+  for (int ps = 0; ps < 2; ++ps) {
+    const int jj = 16 * ps + (threadIdx.x >> 4), kq = threadIdx.x & 15;
+    const int jo = j0 + jj;
+    if (out.row0 + jo < out.rpad && jo < out.nrows && k0 + 4 * kq < out.kpad)
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+        *reinterpret_cast<uint32_t *>(out.digits + s * plane + ((long long)b * out.rpad + out.row0 + jo) * out.kpad +
+                                      k0 + 4 * kq) = tw[s][jj][kq];
+  }
+}
+
 template <int W, int S>
 __global__ void slice_cols_kernel(MatRef B, int rows, int cols, int fi, SliceRef out, const int *sel) {
   MPPS_PDL_ENTER();
