@@ -1,22 +1,36 @@
 """Benchmark of the B200 mixed-precision Paterson-Stockmeyer hot path.
 
-Default workload (BASELINE.json configs[1], the metric's single-GPU
-config): Taylor approximant of exp, m=30, s=6, a batch of 64 real matrices
-n=256, X ~ N(0,1) rescaled to ||X||_1 = 1 (seeded), double-double working
-precision with the planner's lower-precision levels.  One step = one
-mixed-precision PS evaluation of the whole batch (powers, blocks + norms,
-host planner, mixed Horner) through the public API.
-
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfgX ...] [--scaling weak|strong]
 
-Multi-GPU (torchrun): every rank evaluates its own 64-matrix batch (batch
-sharding, no data-path collective) -> weak scaling; the JSON line reports
-the whole-job evals/s with the max-over-ranks device time.
+With no --config the run prints two JSON lines: cfg2 (BASELINE configs[1],
+64 x n=256 Taylor exp at dd) and then, LAST, the headline cfg5 (the largest
+single-GPU config: Taylor cosine of degree 24 in Z = X^2, one n=8192 matrix,
+dd working).  One step = one mixed-precision PS evaluation of the config's
+unit (the whole batch, or the one matrix) through the public API: powers,
+blocks + norms, host planner, mixed Horner.
 
-``--impl reference`` times the reference algorithm's CPU implementation
-(the oracle port in oracle/, a C restatement of the reference's MPFR
-arithmetic; the reference itself is pure Python over gmpy2, absent from this
-image) on the host cores, on one matrix of the same workload per step.
+Inputs: seeded synthetic matrices of the BASELINE shapes (the
+configs have no dataset).  Every timed step reads a different input batch
+(a pool of distinct seeded batches, cycled when one step's input is larger
+than ~1 GB), so the speculative Horner graph can miss; the line reports
+graphs.speculation_stats().
+
+Multi-GPU: ``--gpus N`` without torchrun re-executes itself under
+``torch.distributed.run`` (one rank per GPU, NCCL).  Batched configs shard
+their matrices over the ranks with no data-path collective (``--scaling
+weak``: every rank evaluates its own B matrices, the default; ``strong``:
+one B-matrix batch split B/N per rank); cfg5 at N > 1 runs the 2-D block
+SUMMA (summa.py).  Device time is the max over ranks.
+
+``--impl reference`` times the reference algorithm's CPU path (the oracle
+port: the C MPFR restatement of the reference's arithmetic in oracle/; the
+reference itself is pure Python over gmpy2, absent from this image) on all
+host cores, on the same config dicts: cfg1/cfg2 run whole evaluations of
+one matrix per step; cfg3/4/5 cannot finish on a CPU (hours to weeks), so
+each step times the port's mat_mul at every precision the config's GEMM
+list needs on an n=256 sample and extrapolates the evaluation as
+sum_g n^3 t_MAC(bits_g), labelled "extrapolated".
 """
 
 from __future__ import annotations
@@ -46,20 +60,42 @@ CONFIGS = {
     "cfg4": dict(workload="cfg4: Pade [26/26] numerator+denominator by mixed PS at qd, one n=2048 matrix, ||X||_1=2",
                  batch=1, n=2048, m=26, digits=63, norm=2.0, kind="pade"),
     "cfg5": dict(workload="cfg5: cos Taylor deg 24 in Z=X^2 (s=5), one n=8192 matrix, ||X||_1=1 (X~N(0,1)/sqrt(n)), "
-                          "dd working, 2-D block SUMMA over NCCL",
-                 batch=1, n=8192, m=24, digits=31, norm=1.0, kind="summa_cos"),
+                          "dd working; 2-D block SUMMA over NCCL at N>1",
+                 batch=1, n=8192, m=24, digits=31, norm=1.0, kind="cos"),
 }
-CFG = dict(CONFIGS["cfg2"])
+DEFAULT_CONFIGS = ("cfg2", "cfg5")      # the last line is the headline
 METRIC = "matrix-polynomial evals/sec"
+POOL_BYTES = 1 << 30                    # distinct inputs kept per run (device + pinned host)
 
 
-def synth(n, target, seed):
+def synth(n, target, seed, cos=False):
+    """SURVEY 8d generator (tests/_util.synth): X = G target/||G||_1,
+    G ~ N(0,1) from default_rng(seed) (/sqrt(n) first for the cosine)."""
     G = np.random.default_rng(seed).standard_normal((n, n))
+    if cos:
+        G = G / np.sqrt(n)
     return G * (target / np.abs(G).sum(axis=0).max())
 
 
-def make_batch(rank, batch, n, norm):
-    return np.stack([synth(n, norm, rank * batch + i) for i in range(batch)])
+def config_dict(name, world, scaling):
+    """The `config` object of BOTH arms (identical for the same run)."""
+    c = CONFIGS[name]
+    if c["kind"] == "cos":
+        par = "single GPU" if world == 1 else "2-D block SUMMA over %dx%d ranks" % _grid_shape(world)
+    elif world == 1:
+        par = "single GPU"
+    elif scaling == "strong":
+        par = f"batch-sharded {c['batch']}/{world} matrices per GPU (strong)"
+    else:
+        par = f"batch-sharded, {c['batch']} matrices per GPU (weak)"
+    return {"workload": c["workload"], "name": name, "batch": c["batch"], "n": c["n"], "m": c["m"],
+            "digits": c["digits"], "parallelism": par,
+            "l2": "256 MiB buffer written between timed steps (L2 flushed); inputs distinct per step"}
+
+
+def _grid_shape(world):
+    from paper_2312_17396_b200 import summa
+    return summa.ProcessGrid.for_world(world)
 
 
 # ----------------------------------------------------------------- clocks
@@ -158,7 +194,9 @@ def measure_peaks(torch, h):
     """FP64 / FP32 FMA pipe peaks on this GPU (2 flops per FMA): the
     per-precision roofline denominators (MEASURED_PEAKS.json has only HBM and
     bf16).  Peak_dd / Peak_qd follow SURVEY 8(d): Peak_fp64 / k with
-    k_dd = 15 and k_qd = 115 FP64-pipe instructions per canonical MAC."""
+    k_dd = 15 and k_qd = 115 FP64-pipe instructions per canonical MAC.
+    Plus the INT8 tcgen05 pipe (the tensor-core GEMMs' bound) and the
+    global->shared ingest rate."""
     out = {}
     scratch = torch.zeros(16, dtype=torch.float64, device="cuda")
     sms = torch.cuda.get_device_properties(0).multi_processor_count
@@ -177,7 +215,6 @@ def measure_peaks(torch, h):
         out[name] = best / 1e12
     out["dd"] = out["fp64"] / 15.0
     out["qd"] = out["fp64"] / 115.0
-    # INT8 tensor pipe (tcgen05 kind::i8), the bound of the tensor-core GEMMs
     iters = 4096
     h.probe_i8mma(sms, 64, scratch)
     best = 0.0
@@ -189,8 +226,6 @@ def measure_peaks(torch, h):
         torch.cuda.synchronize()
         best = max(best, sms * 2.0 * 128 * 256 * 32 * iters / (a.elapsed_time(b) * 1e-3))
     out["int8_tops"] = best / 1e12
-    # global -> shared ingest (TMA bulk copies, one CTA per SM, L2-resident
-    # 48 MiB source): the per-SM fill rate that bounds the tensor-core GEMMs
     src = torch.zeros(48 << 20, dtype=torch.uint8, device="cuda")
     iters = 2048
     h.probe_ingest(sms, 64, src)
@@ -206,66 +241,141 @@ def measure_peaks(torch, h):
     return out
 
 
-def honest_gemms(plan):
-    """GEMMs the device executes per evaluation, by lattice format: s-1
-    powers at the working format + one per Horner level, except the K3 top
-    level when m mod s == 0 (B_r = b_m I -> elementwise)."""
-    from paper_2312_17396_b200.precision import FORMAT_NAME
-    fm = plan.level_formats
+# ---------------------------------------------------------- reference arm
+def _all_cores():
+    if _ORIG_AFFINITY:      # the CPU baseline uses every host core, not the GPU-local ones
+        os.sched_setaffinity(0, _ORIG_AFFINITY)
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    os.environ["OMP_NUM_THREADS"] = str(cores)
+    return cores
+
+
+def _ref_gemm_list(name):
+    """(bits, count) per evaluation of the oracle composition (SURVEY 8c:
+    powers/blocks at the working bits, Horner levels at the snapped digits'
+    bits) for the configs the port cannot finish, from the committed
+    full-size plan fixture (tests/golden/fullsize_plans.json, written by
+    oracle/make_fullsize_plans.py with the oracle's planner)."""
+    import oracle
+    c = CONFIGS[name]
+    fx = json.load(open(os.path.join(ROOT, "tests", "golden", "fullsize_plans.json")))[name]
+    wb = oracle.bits_of(c["digits"])
     counts = {}
-    w = FORMAT_NAME[fm[0]]
-    counts[w] = counts.get(w, 0) + plan.s - 1
-    top_scalar = (CFG["m"] % plan.s == 0)
-    for j in range(1, plan.r + 1):
-        if j == plan.r and top_scalar:
-            continue
-        f = FORMAT_NAME[fm[j]]
-        counts[f] = counts.get(f, 0) + 1
-    return counts
+
+    def add(bits, k):
+        counts[bits] = counts.get(bits, 0) + k
+    for ent in fx["plans"]:
+        s, r, m = ent["s"], ent["r"], ent["m"]
+        if not ent.get("shared_powers_with_previous"):
+            add(wb, s - 1)                       # X^2..X^s (form_powers; shared by the Pade pair)
+        for j, dj in enumerate(ent["snapped"], start=1):
+            if j == r and m % s == 0:
+                continue                         # B_r = b_m I: no product
+            add(oracle.bits_of(dj), 1)
+        add(wb, ent.get("squarings", 0))
+        add(wb, ent.get("argument_gemms", 0))    # cosine Z = X X
+    per_unit = fx.get("units", 1)
+    return counts, per_unit
 
 
-# ---------------------------------------------------------- reference
-def run_reference(args, rank, world):
-    """The reference algorithm's CPU path (oracle port) on host cores."""
-    if rank != 0:
-        return
+def reference_step_extrapolated(name, n_s=256):
+    """One bounded step of the reference arm for cfg3/4/5: the port's
+    mat_mul timed at each precision of the GEMM list on an n_s sample (all
+    cores); returns (extrapolated seconds per unit, detail)."""
+    import oracle
+    c = CONFIGS[name]
+    counts, units = _ref_gemm_list(name)
+    A = synth(n_s, 1.0, 7)
+    Bm = synth(n_s, 1.0, 8)
+    t_mac = {}
+    for bits in sorted(counts):
+        t0 = time.perf_counter()
+        oracle.matmul(A, Bm, bits)
+        t_mac[bits] = (time.perf_counter() - t0) / n_s ** 3
+    total = sum(c["n"] ** 3 * t_mac[b] * k for b, k in counts.items())
+    return total / units, {"t_mac_ns": {str(b): 1e9 * t for b, t in t_mac.items()},
+                           "gemms_per_unit": {str(b): k / units for b, k in counts.items()}}
+
+
+def reference_step_full(name, seed):
+    """One bounded step for cfg1/cfg2: a whole mixed evaluation of one
+    matrix of the config in the port; returns seconds."""
     import oracle
     from paper_2312_17396_b200.coefficients import taylor_exp_coeffs
-    oracle.build()
-    cores = os.cpu_count() or 1
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
-    n, m, d = CFG["n"], CFG["m"], CFG["digits"]
-    coeffs = taylor_exp_coeffs(m).coeffs
-    X = [synth(n, CFG["norm"], i) for i in range(args.warmup + args.steps)]
-    for i in range(args.warmup):
-        oracle.ps_eval(X[i], coeffs, d)
+    c = CONFIGS[name]
+    X = synth(c["n"], c["norm"], seed)
     t0 = time.perf_counter()
-    for i in range(args.steps):
-        oracle.ps_eval(X[args.warmup + i], coeffs, d)
-    sec = time.perf_counter() - t0
-    v = args.steps / sec
+    oracle.ps_eval(X, taylor_exp_coeffs(c["m"]).coeffs, c["digits"])
+    return time.perf_counter() - t0
+
+
+def reference_sample(name, steps, warmup):
+    """(value evals/s, cpu_baseline dict) of the port on this config."""
+    import oracle
+    oracle.build()
+    cores = _all_cores()
+    kind = CONFIGS[name]["kind"]
+    full = kind == "exp"
+    for i in range(warmup):
+        (reference_step_full(name, 10_000 + i) if full else reference_step_extrapolated(name))
+    total, detail = 0.0, None
+    t0 = time.perf_counter()
+    for i in range(steps):
+        if full:
+            total += reference_step_full(name, i)
+        else:
+            sec, detail = reference_step_extrapolated(name)
+            total += sec
+    wall = time.perf_counter() - t0
+    v = steps / total
+    n = CONFIGS[name]["n"]
+    if full:
+        sample = (f"{steps} whole mixed PS evaluations of one n={n} matrix each (seeds 0..{steps - 1}) in the C "
+                  f"MPFR restatement of the reference (oracle/), OpenMP over GEMM rows, {wall:.1f} s")
+    else:
+        sample = (f"extrapolated: each of {steps} steps times the port's mat_mul (precision.py:160-184 "
+                  f"restated) at every precision of the config's GEMM list on an n=256 sample "
+                  f"(t_MAC ns per precision bits {({k: round(x, 2) for k, x in detail['t_mac_ns'].items()})}), "
+                  f"evaluation = sum_g n^3 t_MAC(bits_g) over {detail['gemms_per_unit']} GEMMs per unit; "
+                  f"O(n^2) terms omitted; {wall:.1f} s of CPU time")
+    cb = {"value": v, "unit": "evals/s", "cores": cores, "kind": "port", "sample": sample}
+    if not full:
+        cb["extrapolated"] = True
+    return v, cb
+
+
+def run_reference(name, args, rank, world):
+    if rank != 0:
+        return
+    v, cb = reference_sample(name, args.steps, args.warmup)
     line = {"metric": METRIC, "value": v, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "mpfr-103bit (per-op rounded, reference semantics)",
-            "data": "synthetic (seeded N(0,1), ||X||_1=1)", "impl": "reference",
-            "config": {"workload": CFG["workload"], "batch": CFG["batch"], "n": n, "m": m, "digits": d},
-            "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": "port",
-                             "sample": f"1 matrix (n={n}) of the 64-matrix batch per step, full mixed PS "
-                                       "evaluation in the C MPFR restatement (oracle/mpfr_oracle.c), "
-                                       "OpenMP over GEMM rows"},
+            "warmup": args.warmup, "ms_per_step": 1e3 / v, "higher_is_better": True,
+            "scaling": _scaling(name, args), "vs_baseline": None,
+            "dtype": f"mpfr {_bits_note(name)} (per-op rounded, reference semantics)",
+            "data": "synthetic (seeded N(0,1) rescaled to the config's ||X||_1; BASELINE configs have no dataset)",
+            "impl": "reference", "config": config_dict(name, world, args.scaling),
+            "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def _bits_note(name):
+    import oracle
+    return f"{oracle.bits_of(CONFIGS[name]['digits'])}-bit working"
+
+
+def _scaling(name, args):
+    return "strong" if (CONFIGS[name]["kind"] == "cos" or args.scaling == "strong") else "weak"
+
+
 def pcie_rates(torch, h2d_bytes: int, d2h_bytes: int, reps: int = 5):
     """Plain pinned-host <-> device copy rates of one step's input / result
-    sizes in this process (the ceiling of the e2e stream; the host memory
-    placement of a VM makes it differ between processes)."""
+    sizes in this process (the ceiling of the e2e stream)."""
     try:
         hb = torch.empty(max(h2d_bytes, d2h_bytes) // 8, dtype=torch.float64).pin_memory()
         db = torch.empty_like(hb, device="cuda")
         out = {}
-        for name, nbytes, dst, src in (("h2d", h2d_bytes, db, hb), ("d2h", d2h_bytes, hb, db)):
+        for nm, nbytes, dst, src in (("h2d", h2d_bytes, db, hb), ("d2h", d2h_bytes, hb, db)):
             k = nbytes // 8
             dst[:k].copy_(src[:k], non_blocking=True)
             torch.cuda.synchronize()
@@ -275,84 +385,73 @@ def pcie_rates(torch, h2d_bytes: int, d2h_bytes: int, reps: int = 5):
                 dst[:k].copy_(src[:k], non_blocking=True)
             b.record()
             b.synchronize()
-            out[name] = reps * nbytes / (a.elapsed_time(b) * 1e-3) / 1e9
+            out[nm] = reps * nbytes / (a.elapsed_time(b) * 1e-3) / 1e9
         return out
     except Exception as e:  # diagnostics only
         return {"error": str(e)[:120]}
 
 
-def cpu_baseline_sample(cores_hint=None):
-    if _ORIG_AFFINITY:      # the CPU baseline uses every host core, not the GPU-local ones
-        os.sched_setaffinity(0, _ORIG_AFFINITY)
-    import oracle
-    from paper_2312_17396_b200.coefficients import taylor_exp_coeffs
-    oracle.build()
-    n, m, d = CFG["n"], CFG["m"], CFG["digits"]
-    X = synth(n, CFG["norm"], 0)
-    t0 = time.perf_counter()
-    oracle.ps_eval(X, taylor_exp_coeffs(m).coeffs, d)
-    sec = time.perf_counter() - t0
-    return {"value": 1.0 / sec, "unit": "evals/s", "cores": os.cpu_count() or 1, "kind": "port",
-            "sample": f"1 matrix (n={n}, seed 0) of the cfg2 batch, full mixed PS in the C MPFR "
-                      f"restatement of the reference (oracle/), OpenMP over GEMM rows, {sec:.1f} s"}
-
-
 # ---------------------------------------------------------------- ours
 class Workload:
-    """One benchmark config: device-resident inputs, a step through the
-    public API, an end-to-end step from pinned host buffers, and the honest
+    """One benchmark config on this rank: a pool of distinct device-resident
+    (and pinned host) inputs, a step through the public API, and the honest
     GEMM count per unit."""
 
-    def __init__(self, name, rank, world, torch, mp):
+    def __init__(self, name, rank, world, torch, mp, scaling, steps, warmup):
         self.name, self.cfg = name, CONFIGS[name]
         self.rank, self.world, self.torch, self.mp = rank, world, torch, mp
         c = self.cfg
         self.ctx = mp.PrecisionCtx(c["digits"])
-        self.n, self.B, self.m = c["n"], c["batch"], c["m"]
+        self.n, self.m = c["n"], c["m"]
         self.kind = c["kind"]
-        self.scaling = "strong" if self.kind == "summa_cos" else "weak"
+        self.scaling = "strong" if (self.kind == "cos" or scaling == "strong") else "weak"
         self.grid = None
-        if self.kind == "expm":
-            rng = np.random.default_rng(1000 + rank)
-            targets = 10.0 ** rng.uniform(-2, 3, size=self.B)
-            self.Xh = np.stack([synth(self.n, t, rank * self.B + i) for i, t in enumerate(targets)])
-        elif self.kind == "summa_cos":
+        if self.kind == "cos" and world > 1:
             from paper_2312_17396_b200 import summa
             pr, pc = summa.ProcessGrid.for_world(world)
-            self.grid = summa.ProcessGrid(pr, pc) if world > 1 else None
-            X = np.random.default_rng(0).standard_normal((self.n, self.n)) / np.sqrt(self.n)
-            X *= c["norm"] / np.abs(X).sum(axis=0).max()
-            if self.grid is None:
-                self.Xh = X
-            else:
-                r0, mr, c0, nc = self.grid.block(self.n)
-                self.Xh = np.ascontiguousarray(X[r0:r0 + mr, c0:c0 + nc])
-            self.parallelism = f"SUMMA {pr}x{pc}"
+            self.grid = summa.ProcessGrid(pr, pc)
+        B = c["batch"]
+        if self.kind in ("exp", "expm") and self.scaling == "strong" and world > 1:
+            lo, hi = rank * B // world, (rank + 1) * B // world
+            self.members = list(range(lo, hi))
         else:
-            self.Xh = make_batch(rank, self.B, self.n, c["norm"])
-            if self.B == 1:
-                self.Xh = self.Xh[0]
-        if self.kind != "summa_cos":
-            self.parallelism = f"batch-sharded x{world}" if world > 1 else "single GPU"
-        self.Xd = torch.from_numpy(self.Xh).cuda()
-        self.Xpin = torch.from_numpy(self.Xh).pin_memory()
+            self.members = list(range(B))
+        self.B = len(self.members)
+        step_bytes = self.B * self.n * self.n * 8
+        self.pool = max(2, min(steps + warmup + 1, POOL_BYTES // step_bytes))
+        self.Xh = [self._make(t) for t in range(self.pool)]
+        self.Xd = [torch.from_numpy(x).cuda() for x in self.Xh]
+        self.Xpin = [torch.from_numpy(x).pin_memory() for x in self.Xh]
+
+    def _make(self, t):
+        """Input of pool slot t on this rank: seeds never repeat across
+        slots or ranks (slot 0 of rank 0 is the parity tests' seed set)."""
+        c, n, B = self.cfg, self.n, self.cfg["batch"]
+        gid = t * max(self.world, 1) + (0 if self.scaling == "strong" else self.rank)
+        if self.kind == "exp":
+            X = np.stack([synth(n, c["norm"], gid * B + i) for i in self.members])
+            return X[0] if c["batch"] == 1 else X
+        if self.kind == "expm":
+            rng = np.random.default_rng(1000 + gid)
+            targets = 10.0 ** rng.uniform(-2, 3, size=B)
+            return np.stack([synth(n, targets[i], gid * B + i) for i in self.members])
+        if self.kind == "pade":
+            return synth(n, c["norm"], gid)
+        X = synth(n, c["norm"], t, cos=True)                    # cosine: one matrix per step
+        if self.grid is not None:
+            r0, mr, c0, nc = self.grid.block(n)
+            X = np.ascontiguousarray(X[r0:r0 + mr, c0:c0 + nc])
+        return X
 
     def _summa(self, X):
         from paper_2312_17396_b200 import summa
         from paper_2312_17396_b200.precision import MatBatch
-        torch = self.torch
-        grid = self.grid
-        if grid is None:
-            grid = summa.ProcessGrid.__new__(summa.ProcessGrid)
-            grid.pr = grid.pc = 1
-            grid.rank = grid.I = grid.J = 0
-            grid.row_group = grid.col_group = None
         if X.device.type == "cpu":
             X = X.to("cuda", non_blocking=True)
         blk = MatBatch(X.reshape(1, 1, *X.shape), 15)
         ops = summa.DeviceOps()
-        Z = summa.cos_argument_dist(blk, self.ctx, grid, ops)
-        return summa.ps_mixed_dist(Z, self.mp.taylor_cos_coeffs(self.m), self.ctx, grid, ops)
+        Z = summa.cos_argument_dist(blk, self.ctx, self.grid, ops)
+        return summa.ps_mixed_dist(Z, self.mp.taylor_cos_coeffs(self.m), self.ctx, self.grid, ops)
 
     def step(self, X):
         mp, ctx, m = self.mp, self.ctx, self.m
@@ -362,42 +461,41 @@ class Workload:
             return mp.expm_ss(X, ctx, m, timing=False)
         if self.kind == "pade":
             return mp.ps_mixed_pade(X, m, ctx, timing=False)
-        return self._summa(X)
+        if self.grid is not None:
+            return self._summa(X)
+        Z = mp.cos_argument(X, ctx)
+        return mp.ps_mixed_general(Z, mp.taylor_cos_coeffs(m), ctx, timing=False)
 
     def results(self, rep):
         """Device tensors holding the step's result(s)."""
         if self.kind == "pade":
             return [r.result.data for r in rep]
-        if self.kind == "summa_cos":
+        if self.grid is not None:
             return [rep.block.data]
         return [rep.result.data]
 
     def plans(self, rep):
         if self.kind == "pade":
             return [rep[0].plan, rep[1].plan]
-        if self.kind == "summa_cos":
+        if self.grid is not None:
             return [rep.plan(self.ctx)]
         if hasattr(rep, "plan"):
             return [rep.plan]
-        return [rep[0].plan]
+        return [r.plan for r in rep]
 
     def formats(self, rep):
-        if self.kind == "summa_cos":
-            from paper_2312_17396_b200.precision import FORMAT_NAME
-            return [FORMAT_NAME[f] for f in self.plans(rep)[0].level_formats]
-        r0 = rep[0] if self.kind == "pade" or not hasattr(rep, "diagnostics") else rep
-        return r0.diagnostics["level_formats"]
+        from paper_2312_17396_b200.precision import FORMAT_NAME
+        return [[FORMAT_NAME[f] for f in p.level_formats] for p in self.plans(rep)[:4]]
 
     def gemms(self, rep):
-        """Honest device GEMMs per step, by format (whole local step)."""
+        """Honest device GEMMs per step on this rank, by format."""
         from paper_2312_17396_b200.precision import FORMAT_NAME
         counts = {}
 
         def add(f, c):
             counts[f] = counts.get(f, 0) + c
 
-        plans = self.plans(rep)
-        for i, p in enumerate(plans):
+        for i, p in enumerate(self.plans(rep)):
             fm = p.level_formats
             if not (self.kind == "pade" and i > 0):
                 add(FORMAT_NAME[fm[0]], p.s - 1)           # powers (shared by the Pade pair)
@@ -405,13 +503,11 @@ class Workload:
                 if j == p.r and self.m % p.s == 0:
                     continue                                # K3: elementwise
                 add(FORMAT_NAME[fm[j]], 1)
-        mult = self.B if self.kind in ("exp", "expm") else 1
-        counts = {k: v * mult for k, v in counts.items()}
-        if self.kind == "summa_cos":
+        if self.kind == "cos":
             add("dd", 1)                                    # Z = X X
         if self.kind == "expm":
-            ells = [r.diagnostics["squarings"] for r in (rep if not hasattr(rep, "plan") else [rep])]
-            add("dd", sum(ells))
+            reps = rep if not hasattr(rep, "plan") else [rep]
+            add("dd", sum(r.diagnostics["squarings"] for r in reps))
         return counts
 
     def units(self):
@@ -420,30 +516,22 @@ class Workload:
     def flop_scale(self):
         """GEMM flops are 2 n^3 per (global) GEMM; for SUMMA each rank does
         1/world of every GEMM."""
-        return 2.0 * self.n ** 3 / (self.world if self.kind == "summa_cos" else 1)
+        return 2.0 * self.n ** 3 / (self.world if self.grid is not None else 1)
 
 
-def run_ours(args, rank, world, local_rank):
+def run_ours(name, args, rank, world, local_rank, dist):
     import torch
     import paper_2312_17396_b200 as mp
-    from paper_2312_17396_b200 import _lib
+    from paper_2312_17396_b200 import _lib, graphs as _graphs
 
-    torch.cuda.set_device(local_rank)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    wl = Workload(args.config, rank, world, torch, mp)
+    wl = Workload(name, rank, world, torch, mp, args.scaling, args.steps, args.warmup)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     h = _lib.handle_for()
+    P = wl.pool
 
-    for _ in range(args.warmup):
-        rep = wl.step(wl.Xd)
+    for i in range(args.warmup):
+        rep = wl.step(wl.Xd[(args.steps + i) % P])
     torch.cuda.synchronize()
-    gem = wl.gemms(rep)
-    plans = wl.plans(rep)
-    # long-lived objects (graphs, buffers, the workload) out of the collector's
-    # generations: no multi-ms gen-2 pause inside a timed region
     import gc
     gc.collect()
     gc.freeze()
@@ -453,29 +541,39 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ---- device-resident timed region (value) ----
+    # ---- device-resident timed region (value): step t reads input t ----
     clocks = ClockSampler(local_rank) if (rank == 0 and not args.no_clocks) else None
+    spec0 = _graphs.speculation_stats()
     barrier()
     if clocks:
         clocks.start()
-    from paper_2312_17396_b200 import graphs as _graphs
     l0 = _lib.total_launches()
     total = 0.0
-    for _ in range(args.steps):
+    gem, plans, fmts = {}, [], []
+    for t in range(args.steps):
         flush.zero_()  # 256 MiB write between steps: L2 (126 MB) flushed
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        rep = wl.step(wl.Xd)
+        rep = wl.step(wl.Xd[t % P])
         b.record()
         b.synchronize()
         total += a.elapsed_time(b) * 1e-3
+        for f, c in wl.gemms(rep).items():
+            gem[f] = gem.get(f, 0) + c
+        if t == 0:
+            plans, fmts = wl.plans(rep), wl.formats(rep)
     barrier()
-    if _graphs.enabled() and _graphs.last_launches():
-        launches = float(_graphs.last_launches())      # kernels per graphed evaluation
-    else:
-        launches = (_lib.total_launches() - l0) / args.steps
     clk = clocks.stop() if clocks else None
+    spec1 = _graphs.speculation_stats()
+    eager_launches = _lib.total_launches() - l0
+    if _graphs.enabled() and _graphs.last_launches() and wl.kind == "exp":
+        per_step = float(_graphs.last_launches())      # kernels per graphed evaluation (captured count)
+        launches = per_step * args.steps
+    else:
+        launches = float(eager_launches)
+        per_step = launches / args.steps
+    gem = {k: v / args.steps for k, v in gem.items()}
 
     # ---- roofline pass: the same K steps eagerly (graphs off) with a CUDA
     # event pair around every GEMM launch on the launching stream ----
@@ -484,93 +582,85 @@ def run_ours(args, rank, world, local_rank):
         was = _graphs.enabled()
         _graphs.set_enabled(False)
         h = _lib.handle_for()
-        wl.step(wl.Xd)
+        wl.step(wl.Xd[0])
         torch.cuda.synchronize()
         h.probe = {}
-        for _ in range(args.steps):
+        for t in range(args.steps):
             flush.zero_()
             barrier()
-            wl.step(wl.Xd)
+            wl.step(wl.Xd[t % P])
         torch.cuda.synchronize()
         probe, h.probe = h.probe, None
         _graphs.set_enabled(was)
 
     # ---- end-to-end through the public API with host buffers ----
-    # batched exp configs: paper_2312_17396_b200.pipeline.evaluate_host (H2D of
-    # chunk c+1 and D2H of chunk c-1 overlap the evaluation of chunk c)
     from paper_2312_17396_b200 import pipeline as _pl
-    outs = None
+    W = {15: 1, 31: 2, 63: 4}[wl.cfg["digits"]]
     e2e_total = 0.0
-    # 4 chunks alternating over two compute streams (pipeline.evaluate_host):
-    # each chunk's kernels fill the other's tails; its copies and host
-    # planning overlap the other chunks' evaluation
     if wl.kind == "exp" and wl.B >= 16:
+        # the K steps' batches as one pinned host stream through
+        # pipeline.evaluate_host: chunks of every step flow through a window
+        # of graph slots, so the copies of step t overlap the evaluation of
+        # step t+1; every step's H2D and D2H stay inside the timed region
         chunks = [wl.B // 2, wl.B - wl.B // 2]
-    else:
-        chunks = 1
-    e2e_streams = 2 if chunks != 1 else 1
-    e2e_mode = "per step"
-    if chunks != 1:
-        # the K steps as one host stream (K x B matrices, pinned): chunks of
-        # every step flow through a window of graph slots, so the copies
-        # of step i overlap the evaluation of step i+1; every step's H2D
-        # and D2H stay inside the one timed region
-        W = {15: 1, 31: 2, 63: 4}[wl.cfg["digits"]]
-        Xbig = wl.Xpin.repeat(args.steps, 1, 1).pin_memory()
-        outs = [torch.empty((W,) + tuple(Xbig.shape), dtype=torch.float64).pin_memory()]
+        Xbig = torch.cat([wl.Xpin[t % P] for t in range(args.steps)]).pin_memory()
+        out = torch.empty((W,) + tuple(Xbig.shape), dtype=torch.float64).pin_memory()
         sizes = list(chunks) * args.steps
         sub = _pl.mixed_exp(wl.m, wl.ctx, timing=False)
         win = 6    # tools/e2e_sweep.py: [32, 32] x window 6 ~ [16]*4 x 12 > [16]*4 x 8 > [64] x 3
-        _pl.evaluate_host(sub, Xbig, outs[0], sizes, streams=e2e_streams, window=win)   # warm-up / capture
+        Xwarm = torch.cat([wl.Xpin[(args.steps + t) % P] for t in range(args.steps)]).pin_memory()
+        _pl.evaluate_host(sub, Xwarm, out, sizes, streams=2, window=win)   # warm-up / capture
+        del Xwarm
         flush.zero_()
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        _pl.evaluate_host(sub, Xbig, outs[0], sizes, streams=e2e_streams, window=win)
+        _pl.evaluate_host(sub, Xbig, out, sizes, streams=2, window=win)
         b.record()
         b.synchronize()
         e2e_total = a.elapsed_time(b) * 1e-3
-        e2e_mode = f"{args.steps} steps streamed in one call (window {win} chunk slots)"
-        # per-step bytes: one step's input and result
-        outs = [torch.empty((W,) + tuple(wl.Xpin.shape), dtype=torch.float64)]
-    for i in range(args.steps + 1 if chunks == 1 else 0):
-        flush.zero_()
-        barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        if chunks != 1:
-            if outs is None:
-                W = {15: 1, 31: 2, 63: 4}[wl.cfg["digits"]]
-                outs = [torch.empty((W,) + tuple(wl.Xpin.shape), dtype=torch.float64).pin_memory()]
-            _pl.evaluate_host(_pl.mixed_exp(wl.m, wl.ctx, timing=False), wl.Xpin, outs[0], chunks,
-                              streams=e2e_streams)
-        else:
-            rep = wl.step(wl.Xpin)
+        e2e_path = ("paper_2312_17396_b200.pipeline.evaluate_host(ps_mixed_exp, pinned host stream of the "
+                    f"{args.steps} steps' distinct batches, chunks {chunks} per step over 2 compute streams, a "
+                    f"window of {win} chunk slots: copies and host planning overlap compute, also across steps; "
+                    "no L2 flush inside the stream, per-step working set ~1 GB > L2)")
+        h2d = wl.Xh[0].nbytes
+        d2h = W * wl.Xh[0].nbytes
+    else:
+        outs = None
+        for i in range(args.steps + 1):
+            X = wl.Xpin[(i + P - 1) % P]
+            flush.zero_()
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            rep = wl.step(X)
             res = wl.results(rep)
             if outs is None:
                 outs = [torch.empty(r.shape, dtype=r.dtype).pin_memory() for r in res]
             for o, r in zip(outs, res):
                 o.copy_(r, non_blocking=True)
-        b.record()
-        b.synchronize()
-        if i > 0:
-            e2e_total += a.elapsed_time(b) * 1e-3
-    h2d = wl.Xh.nbytes
-    d2h = sum(o.numel() * o.element_size() for o in outs)
+            b.record()
+            b.synchronize()
+            if i > 0:            # the first call is a warm-up of the host-input path
+                e2e_total += a.elapsed_time(b) * 1e-3
+        e2e_path = "public API on a pinned host input, result copied back to pinned host memory, per step"
+        h2d = wl.Xh[0].nbytes
+        d2h = sum(o.numel() * o.element_size() for o in outs)
     link = pcie_rates(torch, h2d, d2h)
 
-    t = torch.tensor([total, e2e_total], dtype=torch.float64, device="cuda")
+    tt = torch.tensor([total, e2e_total], dtype=torch.float64, device="cuda")
     if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total, e2e_total = float(t[0]), float(t[1])
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    total, e2e_total = float(tt[0]), float(tt[1])
     if rank != 0:
-        dist.destroy_process_group()
         return
     per_step_units = wl.units() * (world if wl.scaling == "weak" else 1)
+    if wl.scaling == "strong" and wl.kind in ("exp", "expm"):
+        per_step_units = wl.cfg["batch"]
     value = per_step_units * args.steps / total
     e2e = per_step_units * args.steps / e2e_total
 
-    # ---- roofline of the dominant kernel (timed live over the timed region) ----
+    # ---- roofline of the dominant kernel (timed live over the K steps) ----
     peaks = measure_peaks(torch, h)
     by_key = {}
     for key, evs in (probe or {}).items():
@@ -581,62 +671,49 @@ def run_ours(args, rank, world, local_rank):
         by_key[("none", 31, 31, 1, 1, 1, 1, 0, 0)] = (1, 1.0)
     dom = max(by_key.items(), key=lambda kv: kv[1][1])
     (kind, fin, fout, M, N, K, nb, S_used, db_used), (cnt, sec) = dom
-    eager_step = None
     fname = names[fin]
     logical = 2.0 * M * N * K * nb / (sec / cnt) / 1e12       # logical TFLOP/s of the format
     step_time = total / args.steps
     fs = wl.flop_scale()
     t_ideal = sum(fs * c / (peaks[f] * 1e12) for f, c in gem.items())
-    eff_gflops = sum(fs * c for c in gem.values()) * world * args.steps / total / 1e9
-    plan0 = plans[0]
+    eff_gflops = sum(fs * c for c in gem.values()) * (world if wl.scaling == "weak" or wl.grid is not None else 1) \
+        * args.steps / total / 1e9
     if kind.endswith("_tc"):
-        # INT8 tensor-core GEMM by exact digit-plane splitting: the hardware
-        # bound is the INT8 tensor pipe; algorithmic ops per launch =
-        # 2 M N K x (S(S+1)/2 plane pairs); S = 4/8/16/31 (7-bit digits) or
-        # 4/8/14/28 (8-bit) for fp32/fp64/dd/qd, recorded per launch
+        # INT8 tensor-core GEMM by exact digit-plane splitting: algorithmic
+        # ops per launch = 2 M N K x S(S+1)/2 plane-pair products (S planes
+        # recorded per launch: 4/8/14/28 for fp32/fp64/dd/qd with 8-bit
+        # digits, 4/8/16/31 with 7-bit)
         S = S_used or {7: 4, 15: 8, 31: 16, 63: 31}[fin]
-        achieved = logical * S * (S + 1) / 2
+        pairs = S * (S + 1) / 2
+        achieved = logical * pairs
         S7 = {7: 4, 15: 8, 31: 16, 63: 31}[fin]
-        roof = {"bound": "tensor (int8)", "achieved": achieved, "peak": peaks["int8_tops"],
-                "unit": "TOPS (int8)", "frac": achieved / peaks["int8_tops"],
+        roof = {"bound": "tensor", "pipe": "int8 (tcgen05.mma kind::i8)", "achieved": achieved,
+                "peak": peaks["int8_tops"], "unit": "TOPS (int8)", "frac": achieved / peaks["int8_tops"],
                 "frac_7bit_equivalent": logical * S7 * (S7 + 1) / 2 / peaks["int8_tops"],
+                "algorithmic_ops_per_launch": 2.0 * M * N * K * nb * pairs,
+                "mean_launch_s": sec / cnt,
                 "frac_note": "frac counts the S(S+1)/2 plane-pair products per output this launch executed; "
-                             "8-bit digits need fewer (dd 105 vs 136) for the same product, so "
                              "frac_7bit_equivalent rates the same logical throughput in 7-bit plane pairs",
                 "logical_tflops": logical, "logical_frac_of_format_peak": logical / peaks[fname],
-                "peak_source": f"tcgen05 kind::i8 probe in bench.py on this GPU ({peaks['int8_tops']:.0f} TOPS); "
-                               f"format peaks from DFMA/FFMA probes (fp64 {peaks['fp64']:.2f} TF/s, "
-                               f"Peak_dd = Peak_fp64/15, Peak_qd = Peak_fp64/115, SURVEY 8d); "
-                               "MEASURED_PEAKS.json holds only HBM and bf16"}
-    else:
-        roof = {"bound": "fp64-pipe" if fname != "fp32" else "fp32-pipe", "achieved": logical, "peak": peaks[fname],
-                "unit": "TFLOP/s (logical)", "frac": logical / peaks[fname],
-                "peak_source": "FMA pipe microbenchmark in bench.py on this GPU "
-                               f"(fp64 {peaks['fp64']:.2f} TF/s, fp32 {peaks['fp32']:.2f} TF/s); "
-                               "Peak_dd = Peak_fp64/15, Peak_qd = Peak_fp64/115 (SURVEY 8d); "
-                               "MEASURED_PEAKS.json holds only HBM and bf16"}
-    if kind.endswith("_tc"):
-        # global->shared bytes the kernel moves per launch: every 128-row x
-        # NT-column output tile streams all S digit planes of its A rows and
-        # B columns over K (NT = 32, 16 for qd)
-        NT = 16 if S > 16 else 32      # 14 planes (8-bit dd) still use NT = 32
+                "peak_source": f"tcgen05 kind::i8 probe in bench.py on this GPU ({peaks['int8_tops']:.0f} TOPS; "
+                               "MEASURED_PEAKS.json has no INT8 figure); format peaks from DFMA/FFMA probes "
+                               f"(fp64 {peaks['fp64']:.2f} TF/s, Peak_dd = Peak_fp64/15, SURVEY 8d)"}
+        NT = 16 if S > 16 else 32
         tiles = nb * (-(-M // 128)) * (-(-N // NT))
         ingest = tiles * (-(-K // 32)) * S * (128 + NT) * 32.0
         ach = ingest / (sec / cnt) / 1e12
-        roof["ingest"] = {"achieved": ach, "peak": peaks["ingest_tbps"], "unit": "TB/s", "frac": ach / peaks["ingest_tbps"],
-                          "bytes_per_launch": ingest,
-                          "note": "digit-plane bytes moved global->shared per launch (128-row x NT tiles, "
-                                  "all S planes of A and B over K) and their rate vs the bulk-copy ingest probe "
-                                  "(one CTA per SM, L2-resident 16 KB copies) run in this bench; with 32-byte K "
-                                  "boxes the L2 slices run at ~64% of peak (ncu lts__throughput, n=1024) and the "
-                                  "tensor pipe at ~62% -- DESIGN 5.1"}
-    kkey = f"{kind} {fname}->{names[fout]} {M}x{N}x{K} x{nb}"
-    if kind.endswith("_tc"):
+        roof["ingest"] = {"achieved": ach, "peak": peaks["ingest_tbps"], "unit": "TB/s",
+                          "frac": ach / peaks["ingest_tbps"], "bytes_per_launch": ingest}
         roof["digit_planes"] = S
         roof["digit_bits"] = db_used
+    else:
+        roof = {"bound": "fp64-pipe" if fname != "fp32" else "fp32-pipe", "achieved": logical, "peak": peaks[fname],
+                "unit": "TFLOP/s (logical)", "frac": logical / peaks[fname], "mean_launch_s": sec / cnt,
+                "peak_source": "FMA pipe microbenchmark in bench.py on this GPU"}
+    kkey = f"{kind} {fname}->{names[fout]} {M}x{N}x{K} x{nb}"
     traffic, tsrc = None, None
     try:   # committed ncu --set full capture of this kernel at this shape (profiles/traffic.json)
-        tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")))
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
         if kkey in tr:
             traffic = tr[kkey]["dram_bytes_per_launch"]
             tsrc = f"{tr[kkey]['capture']} ({tr[kkey]['kernel']}), bytes per launch"
@@ -647,52 +724,51 @@ def run_ours(args, rank, world, local_rank):
                  "eval_frac": t_ideal / step_time,
                  "measured_in": "a second timed pass of the same K steps run eagerly (the value pass "
                                 "replays CUDA graphs, whose kernels cannot be bracketed by events)"})
+    spec = {k: spec1[k] - spec0[k] for k in spec1}
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * step_time, "higher_is_better": True,
-        "scaling": wl.scaling, "vs_baseline": None, "dtype": names[plan0.level_formats[0]],
+        "scaling": wl.scaling, "vs_baseline": None, "dtype": names[plans[0].level_formats[0]],
         "data": "synthetic (seeded N(0,1) rescaled to the config's ||X||_1; BASELINE configs have no dataset)",
-        "config": {"workload": wl.cfg["workload"], "name": args.config, "units_per_gpu_step": wl.units(),
-                   "n": wl.n, "m": wl.m, "digits": wl.cfg["digits"],
-                   "schedule_digits": [list(p.level_digits) for p in plans],
-                   "level_formats": wl.formats(rep), "gemms_per_step_per_gpu": gem,
-                   "gemm_engine": __import__("paper_2312_17396_b200.gemm_engine", fromlist=["x"]).engine(),
-                   "parallelism": wl.parallelism,
-                   "host_affinity": (f"{len(CFG['numa_cpus'])} GPU-local CPUs (NVML affinity)"
-                                     if CFG.get("numa_cpus") else "unbound"),
-                   "l2": "256 MiB buffer written between timed steps (L2 flushed)"},
+        "config": config_dict(name, world, args.scaling),
+        "inputs": f"{P} distinct seeded input batches in HBM, step t reads batch t mod {P}",
+        "plan": {"schedule_digits": [list(p.level_digits) for p in plans[:4]], "level_formats": fmts,
+                 "gemms_per_step_per_gpu": gem, "speculation": spec,
+                 "host_affinity": (f"{len(_NUMA_CPUS)} GPU-local CPUs (NVML affinity)" if _NUMA_CPUS else "unbound")},
         "gflops_effective": eff_gflops,
         "roofline": roof,
         "peaks_tflops": peaks,
         "e2e": {"value": e2e, "unit": "evals/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": ("paper_2312_17396_b200.pipeline.evaluate_host(ps_mixed_exp, pinned host stream of the "
-                         f"{args.steps} steps' batches, chunks {chunks} per step over {e2e_streams} compute streams, "
-                         "a window of 6 chunk slots: copies and host planning overlap compute, also across steps; "
-                         "no L2 flush inside the stream, per-step working set ~1 GB > L2)") if chunks != 1 else
-                        "public API on a pinned host batch, result copied back to pinned host memory",
-                "mode": e2e_mode,
-                "link_gbs": link},
+                "path": e2e_path, "link_gbs": link},
         "gpu_launches": launches,
+        "gpu_launches_per_step": per_step,
         "clocks": clk,
     }
-    if world == 1 and not args.no_cpu_baseline and args.config == "cfg2":
+    if world == 1 and not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = cpu_baseline_sample()
+            _, line["cpu_baseline"] = reference_sample(name, 1, 0)
         except Exception as e:  # the baseline is reported, never required
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+        finally:
+            if _NUMA_CPUS:
+                os.sched_setaffinity(0, _NUMA_CPUS)
     print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
+    # release this config's pools before the next config
+    del wl, rep
+    gc.unfreeze()
+    gc.collect()
+    torch.cuda.empty_cache()
 
 
 _ORIG_AFFINITY = []
+_NUMA_CPUS = []
 
 
 def bind_to_gpu_numa(local_rank: int):
     """Pin this rank's host threads to the CPUs NVML reports as local to its
     GPU, so the pinned host buffers of the e2e stream are first-touched on
     the GPU's NUMA node (a far node measured 20-25K instead of 35K evals/s
-    on the cfg2 host stream).  Returns the CPU list or None."""
+    on the cfg2 host stream)."""
     try:
         import pynvml as nv
         nv.nvmlInit()
@@ -703,10 +779,20 @@ def bind_to_gpu_numa(local_rank: int):
         if cpus:
             _ORIG_AFFINITY[:] = sorted(os.sched_getaffinity(0))
             os.sched_setaffinity(0, cpus)
-            return cpus
+            _NUMA_CPUS[:] = cpus
     except Exception:
-        return None
-    return None
+        pass
+
+
+def _relaunch_under_torchrun(gpus: int) -> int:
+    """`bench.py --gpus N` outside torchrun: one rank per GPU on this node."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -715,22 +801,42 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", action="append", choices=sorted(CONFIGS),
+                    help="config(s) to run, in order (default: cfg2 then the headline cfg5)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="batched configs at N>1: B matrices per rank (weak) or B/N (strong)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-probe", action="store_true", help="diagnostic: no per-launch events")
     ap.add_argument("--no-clocks", action="store_true", help="diagnostic: no nvidia-smi sampling")
     args = ap.parse_args()
-    CFG.clear()
-    CFG.update(CONFIGS[args.config])
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0 and args.gpus > 1:
+        sys.exit(_relaunch_under_torchrun(args.gpus))
+    world = max(world, 1)
+    if world != args.gpus:
+        ap.error(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl != "reference":
-        CFG["numa_cpus"] = bind_to_gpu_numa(local_rank)
+    names = args.config or list(DEFAULT_CONFIGS)
     if args.impl == "reference":
-        run_reference(args, rank, world)
-    else:
-        run_ours(args, rank, world, local_rank)
+        for name in names:
+            run_reference(name, args, rank, world)
+        return
+    bind_to_gpu_numa(local_rank)
+    import torch
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")          # communicator rank counts in the log
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    for name in names:
+        run_ours(name, args, rank, world, local_rank, dist)
+    if dist is not None:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -72,6 +72,10 @@ def lib():
         L.orc_compare.argtypes = [ctypes.c_void_p, dp, ctypes.c_int, dp, dp]
         L.orc_matmul.argtypes = [ctypes.c_int, dp, ctypes.c_int, dp, ctypes.c_int, ctypes.c_long, dp]
         L.orc_result_from_block.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        L.orc_poly_cols.argtypes = [ctypes.c_int, dp, ctypes.c_int, ctypes.c_int, P(ctypes.c_char_p),
+                                    P(ctypes.c_char_p), ctypes.c_long, ctypes.c_int, P(ctypes.c_int), ctypes.c_int, dp]
+        L.orc_matpow_cols.argtypes = [ctypes.c_int, dp, ctypes.c_int, ctypes.c_int, ctypes.c_long, P(ctypes.c_int),
+                                      ctypes.c_int, dp]
         L.orc_plan.argtypes = [dp, dp, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int,
                                P(ctypes.c_int), P(ctypes.c_int), dp]
         _lib = L
@@ -211,7 +215,7 @@ def ps_eval(X_words, coeffs: Sequence[Fraction], d_w: int, *, mode: str = "mixed
         # p = B_0 (engine.py:378-379, 473-474)
         lib().orc_result_from_block(ps.h, 0)
         return OracleResult(ps, norms2, digits, nu, True, tuple(digits), [wb] + [bits_of(1)] * r)
-    snapped = snap(digits, d_w) if snap_levels else tuple(digits)
+    snapped = snap(digits, d_w) if (snap_levels and mode != "fixed") else tuple(digits)
     level_bits = [wb] + [bits_of(x) for x in snapped]
     ps.horner(level_bits)
     return OracleResult(ps, norms2, digits, nu, False, snapped, level_bits)
@@ -221,3 +225,53 @@ def reference_eval_words(X_words, coeffs: Sequence[Fraction], d: int) -> np.ndar
     """harness.py:105-109: ps_fixed at 2d digits (returned unrounded, 4 words)."""
     res = ps_eval(X_words, coeffs, 2 * d, mode="fixed")
     return res.ps.result_words(4)
+
+
+def _cols_arg(cols):
+    cols = [int(c) for c in cols]
+    return (ctypes.c_int * len(cols))(*cols), len(cols)
+
+
+def poly_columns(X_words, coeffs: Sequence[Fraction], bits: int, cols, squares: bool = False) -> np.ndarray:
+    """Tier C: columns ``cols`` of p(X) -- or of p(X^2) with
+    ``squares`` (the cosine's Z = X X, harness.py:100-101) -- by
+    matrix-vector Horner at ``bits`` (use 2x the working digits' bits, as
+    reference_eval does, harness.py:105-109).  Returns (4, len(cols), n)
+    exact word planes."""
+    Xw = _words(X_words)
+    n = Xw.shape[1]
+    m = len(coeffs) - 1
+    nums = (ctypes.c_char_p * (m + 1))(*[str(Fraction(c).numerator).encode() for c in coeffs])
+    dens = (ctypes.c_char_p * (m + 1))(*[str(Fraction(c).denominator).encode() for c in coeffs])
+    ca, nc = _cols_arg(cols)
+    out = np.zeros((4, nc, n))
+    if lib().orc_poly_cols(n, _dp(Xw), Xw.shape[0], m, nums, dens, bits, int(bool(squares)), ca, nc, _dp(out)):
+        raise ValueError("bad column index")
+    return out
+
+
+def power_columns(P_words, count: int, bits: int, cols) -> np.ndarray:
+    """Columns ``cols`` of P^count at ``bits`` (repeated matrix-vector
+    products); (4, len(cols), n) word planes."""
+    Pw = _words(P_words)
+    n = Pw.shape[1]
+    ca, nc = _cols_arg(cols)
+    out = np.zeros((4, nc, n))
+    if lib().orc_matpow_cols(n, _dp(Pw), Pw.shape[0], int(count), bits, ca, nc, _dp(out)):
+        raise ValueError("bad column index")
+    return out
+
+
+def column_diff(gpu_cols: np.ndarray, ref_cols: np.ndarray) -> np.ndarray:
+    """Per column ||g - r||_1, every entry's difference of word expansions
+    formed exactly (rationals): gpu_cols (W, ncols, n), ref_cols (4, ncols, n)."""
+    g = np.asarray(gpu_cols, dtype=np.float64)
+    r = np.asarray(ref_cols, dtype=np.float64)
+    out = np.zeros(g.shape[1])
+    for c in range(g.shape[1]):
+        tot = Fraction(0)
+        for i in range(g.shape[2]):
+            d = sum(Fraction(float(x)) for x in g[:, c, i]) - sum(Fraction(float(x)) for x in r[:, c, i])
+            tot += abs(d)
+        out[c] = float(tot)
+    return out

@@ -20,6 +20,11 @@
  *                             engine.py:127-138 (assemble_block), 467-468 (norms)
  *   orc_horner                engine.py:243-252 (horner_mixed)
  *   orc_plan                  engine.py:184-215 (the digit rule of plan_precisions)
+ *   orc_poly_cols             Tier C of SURVEY 8(c): sampled columns of p(X) (or
+ *                             p(X^2)) by matrix-vector Horner at high precision --
+ *                             the ground truth of harness.py:105-109 (reference_eval,
+ *                             2x digits) for sizes whose n^3 MPFR GEMMs cannot finish
+ *   orc_matpow_cols           sampled columns of P^k (the squaring phase of cfg3)
  *
  * MPFR 4.2.1 is present as a runtime library only (no headers), so the few
  * prototypes needed are declared here against the documented ABI
@@ -60,6 +65,7 @@ extern int mpfr_log10(mpfr_ptr, mpfr_srcptr, int);
 extern int mpfr_cmp(mpfr_srcptr, mpfr_srcptr);
 extern int mpfr_sgn(mpfr_srcptr);
 extern int mpfr_zero_p(mpfr_srcptr);
+extern int mpfr_mul_d(mpfr_ptr, mpfr_srcptr, double, int);
 
 #define NORM_BITS 54  /* NORM_CTX = 16 digits (precision.py:72) */
 #define BOUND_BITS 107 /* BOUND_CTX = 32 digits (precision.py:75) */
@@ -481,5 +487,102 @@ int orc_result_from_block(orc_ps *p, int which) {
     mpfr_set(&p->result.v[i], &p->blocks[which].v[i], RNDN);
   }
   p->have_result = 1;
+  return 0;
+}
+
+/* ---------------------------------------------------------------- Tier C
+ * y = RN_bits(A w) for a dense A given as aw word planes of n*n doubles (the
+ * exact sum of the planes is the matrix): per row, acc = sum_k sum_w
+ * RN(a_ik^(w) w_k) added sequentially at `bits`.  At twice the working digits
+ * this is far below the parity tolerance (c n u_work), like reference_eval. */
+static void matvec_words(int n, const double *A, int aw, const mpfr_struct *w, mpfr_struct *y, long bits) {
+  long nn = (long)n * n;
+#pragma omp parallel
+  {
+    mpfr_struct t;
+    mpfr_init2(&t, bits);
+#pragma omp for schedule(static)
+    for (int i = 0; i < n; ++i) {
+      mpfr_ptr acc = &y[i];
+      mpfr_set_si(acc, 0, RNDN);
+      for (int k = 0; k < n; ++k) {
+        for (int q = 0; q < aw; ++q) {
+          double a = A[q * nn + (long)i * n + k];
+          if (a == 0.0) continue;
+          mpfr_mul_d(&t, &w[k], a, RNDN);
+          mpfr_add(acc, acc, &t, RNDN);
+        }
+      }
+    }
+    mpfr_clear(&t);
+  }
+}
+
+static mpfr_struct *vec_new(int n, long bits) {
+  mpfr_struct *v = (mpfr_struct *)malloc(sizeof(mpfr_struct) * (size_t)n);
+  for (int i = 0; i < n; ++i) {
+    mpfr_init2(&v[i], bits);
+    mpfr_set_si(&v[i], 0, RNDN);
+  }
+  return v;
+}
+static void vec_free(mpfr_struct *v, int n) {
+  for (int i = 0; i < n; ++i) mpfr_clear(&v[i]);
+  free(v);
+}
+
+/* Columns cols[0..ncols) of p(A), A = X (squares = 0) or A = X X (squares =
+ * 1, the cosine's Z, harness.py:100-101, applied as X (X w)), p = sum_k b_k
+ * A^k with b_k = RN_bits(nums[k]/dens[k]): w = b_m e_j, then
+ * w = A w + b_k e_j for k = m-1..0.  out: (4, ncols, n) exact word planes. */
+int orc_poly_cols(int n, const double *X, int xw, int m, const char **nums, const char **dens, long bits,
+                  int squares, const int *cols, int ncols, double *out) {
+  mpfr_struct *coef = (mpfr_struct *)malloc(sizeof(mpfr_struct) * (m + 1));
+  for (int k = 0; k <= m; ++k) {
+    mpfr_init2(&coef[k], bits);
+    set_rational(&coef[k], nums[k], dens[k], bits);
+  }
+  mpfr_struct *w = vec_new(n, bits), *y = vec_new(n, bits);
+  long plane = (long)ncols * n;
+  for (int c = 0; c < ncols; ++c) {
+    int j = cols[c];
+    if (j < 0 || j >= n) return 1;
+    for (int i = 0; i < n; ++i) mpfr_set_si(&w[i], 0, RNDN);
+    mpfr_set(&w[j], &coef[m], RNDN);
+    for (int k = m - 1; k >= 0; --k) {
+      matvec_words(n, X, xw, w, y, bits);
+      if (squares) {
+        mpfr_struct *tmp = w; w = y; y = tmp;
+        matvec_words(n, X, xw, w, y, bits);
+      }
+      mpfr_add(&y[j], &y[j], &coef[k], RNDN);
+      mpfr_struct *tmp = w; w = y; y = tmp;
+    }
+    for (int i = 0; i < n; ++i) split(&w[i], out + (long)c * n + i, 4, plane);
+  }
+  vec_free(w, n);
+  vec_free(y, n);
+  for (int k = 0; k <= m; ++k) mpfr_clear(&coef[k]);
+  free(coef);
+  return 0;
+}
+
+/* Columns of P^count (P given as pw word planes) at `bits`: out (4, ncols, n). */
+int orc_matpow_cols(int n, const double *P, int pw, int count, long bits, const int *cols, int ncols,
+                    double *out) {
+  mpfr_struct *w = vec_new(n, bits), *y = vec_new(n, bits);
+  long plane = (long)ncols * n;
+  for (int c = 0; c < ncols; ++c) {
+    int j = cols[c];
+    if (j < 0 || j >= n) return 1;
+    for (int i = 0; i < n; ++i) mpfr_set_si(&w[i], i == j ? 1 : 0, RNDN);
+    for (int k = 0; k < count; ++k) {
+      matvec_words(n, P, pw, w, y, bits);
+      mpfr_struct *tmp = w; w = y; y = tmp;
+    }
+    for (int i = 0; i < n; ++i) split(&w[i], out + (long)c * n + i, 4, plane);
+  }
+  vec_free(w, n);
+  vec_free(y, n);
   return 0;
 }

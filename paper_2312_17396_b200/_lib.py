@@ -316,9 +316,10 @@ class Handle:
     def gemm_sliced(self, A: "Slices", B: "Slices", S: int, C: MatBatch, sel=None):
         a, b, c = A.c(), B.c(), cmat(C)
         nsel = 0 if sel is None else sel.numel()
-        end = self._ev(("gemm_tc", C.fmt, C.fmt, A.rows, B.rows, A.k, nsel or C.batch, S, A.db))
-        # N from C: B may hold more column slices than this product uses
-        # (the power chain's [X | X^2] operand)
+        # the probe key and the launch both take N from C: B may hold more
+        # column slices than this product uses (the power chain's [X | X^2]
+        # operand feeds the N = n launch of X^2 and the N = 2n paired ones)
+        end = self._ev(("gemm_tc", C.fmt, C.fmt, A.rows, C.cols, A.k, nsel or C.batch, S, A.db))
         self._check(self.lib.mpps_gemm_sliced(self.h, ctypes.byref(a), ctypes.byref(b), S, A.rows, C.cols, A.k,
                                               ctypes.byref(c), _ptr(sel), nsel), "mat_mul(tc)")
         if end is not None:

@@ -44,10 +44,13 @@ def scaling_of(norms: np.ndarray, m: int = DEFAULT_M) -> List[int]:
     return [extra_squarings(float(v), s) if v > 0 else 0 for v in norms]
 
 
-def expm_ss(A, ctx: PrecisionCtx, m: int = DEFAULT_M, delta: float = 10.0, timing: bool = True):
+def expm_ss(A, ctx: PrecisionCtx, m: int = DEFAULT_M, delta: float = 10.0, timing: bool = True,
+            return_stage: bool = False):
     """exp(A) for an (n, n) or (B, n, n) batch.  Returns a BatchReport (or a
     single report) whose ``diagnostics['squarings']`` holds l per matrix and
-    whose ``result`` is exp(A) at the working format."""
+    whose ``result`` is exp(A) at the working format.  ``return_stage``
+    returns (report, P) with P a copy of the PS stage p_m(2^-l A) before the
+    squarings (full-size parity tests check the two phases separately)."""
     torch = _torch()
     h = _lib.handle_for()
     At, Aw, single = _input(A)
@@ -66,6 +69,7 @@ def expm_ss(A, ctx: PrecisionCtx, m: int = DEFAULT_M, delta: float = 10.0, timin
     from .engine import EvaluationReport
     reps = [rep] if isinstance(rep, EvaluationReport) else list(rep)
     P = rep.result
+    stage = MatBatch(P.data.clone(), P.fmt) if return_stage else None
     Q = MatBatch.empty(P.fmt, P.batch, n, device=P.device)
     sels = {}
     for t in range(1, max(ells) + 1 if ells else 1):
@@ -80,4 +84,4 @@ def expm_ss(A, ctx: PrecisionCtx, m: int = DEFAULT_M, delta: float = 10.0, timin
     for b, r_ in enumerate(reps):
         r_._diag_extra = dict(r_._diag_extra or {}, squarings=int(ells[b]), degree=m,
                               norm_A=float(normsA[b]))
-    return rep
+    return (rep, stage) if return_stage else rep

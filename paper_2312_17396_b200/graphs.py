@@ -18,8 +18,11 @@ differs, the right graph is replayed after it (same stream, overwriting
 the speculative result).  Results are identical either way.
 
 Buffers live in the graphs' private memory pool and are reused across
-replays; inputs are copied into a static buffer and the result is cloned
-out, so every call returns independent tensors.  Any capture failure turns
+replays; inputs are always copied into the graph's static input buffer
+(stream-ordered at submit, so the caller may reuse its tensor afterwards and
+the post graph, which can re-read X^1 = the static input when a plan keeps
+extra dd levels, never sees a later upload), and the result is cloned out, so
+every call returns independent tensors.  Any capture failure turns
 the graph path off for that shape (eager execution, same kernels).
 """
 
@@ -35,8 +38,6 @@ from .precision import FP64, MatBatch
 _ENABLED = os.environ.get("MPPS_GRAPHS", "1") != "0"
 _SPECULATE = os.environ.get("MPPS_SPECULATE", "1") != "0"
 _CACHE: Dict[tuple, "_ShapeGraphs"] = {}
-_LAST_PTR: Dict[tuple, int] = {}
-_ZERO_COPY = os.environ.get("MPPS_GRAPH_ZERO_COPY", "1") != "0"
 _FAILED = set()
 
 
@@ -108,31 +109,13 @@ def submit(key: tuple, Xsrc, build_pre, timer, slot: int = 0) -> Optional[Pendin
     key = key + (("slot", slot),)
     if not _ENABLED or key in _FAILED:
         return None
-    # zero-copy input: a device tensor passed again at the same address is
-    # read by its own pre graph in place (no copy into the static input).
-    # The graph reads whatever that address holds at replay, so this is
-    # exact for any caller; one such graph per shape (slot 0 only)
-    zkey = None
-    if slot == 0 and _ZERO_COPY and Xsrc.is_cuda and Xsrc.is_contiguous():
-        ptr = Xsrc.data_ptr()
-        zkey = key + (("xptr", ptr),)
-        if zkey not in _CACHE and _LAST_PTR.get(key) != ptr:
-            zkey = None                      # first sighting of this address: copy path
-        _LAST_PTR[key] = ptr
-        if zkey is not None and zkey not in _CACHE and any(k[:-1] == key for k in _CACHE if k[-1][0] == "xptr"):
-            zkey = None                      # one pointer-bound graph per shape
-    if zkey is not None and zkey not in _FAILED:
-        key = zkey
     g = _CACHE.get(key)
     try:
         if g is None:
             g = _ShapeGraphs()
             g.pool = torch.cuda.graph_pool_handle()
-            if key[-1][0] == "xptr":
-                g.x_in = Xsrc                    # read in place (see above)
-            else:
-                g.x_in = torch.empty(Xsrc.shape, dtype=torch.float64, device="cuda")
-                g.x_in.copy_(Xsrc, non_blocking=True)
+            g.x_in = torch.empty(Xsrc.shape, dtype=torch.float64, device="cuda")
+            g.x_in.copy_(Xsrc, non_blocking=True)
             # warm-up (kernel attributes, handles, lazy module state) then capture
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
@@ -149,8 +132,7 @@ def submit(key: tuple, Xsrc, build_pre, timer, slot: int = 0) -> Optional[Pendin
                 g.norms_pin.copy_(g.prep.norms_dev, non_blocking=True)
             g.pre_launches = _lib.total_launches() - l0
             _CACHE[key] = g
-        if g.x_in.data_ptr() != Xsrc.data_ptr():
-            g.x_in.copy_(Xsrc, non_blocking=True)
+        g.x_in.copy_(Xsrc, non_blocking=True)
         timer.start("power_formation")
         g.pre.replay()
         ready = torch.cuda.Event()

@@ -66,6 +66,15 @@ class ProcessGrid:
         self.row_group = rows[self.I]
         self.col_group = cols[self.J]
 
+    @classmethod
+    def single(cls) -> "ProcessGrid":
+        """A 1x1 grid without a process group (one GPU, no collectives)."""
+        g = cls.__new__(cls)
+        g.pr = g.pc = 1
+        g.rank = g.I = g.J = 0
+        g.row_group = g.col_group = None
+        return g
+
     @staticmethod
     def for_world(world: int) -> Tuple[int, int]:
         """1x1, 1x2, 2x2, 2x4, ... (pr <= pc, pr a power-of-two split)."""

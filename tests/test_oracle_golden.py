@@ -124,3 +124,49 @@ def test_table1_reference_schedules_vs_planner(oracle_lib):
         r = m // s
         p = plan_precisions(fr[:r + 1], fr[r + 1], PrecisionCtx(d), s=s)
         assert p.to_dict() == row["plan"]
+
+
+def test_tier_c_columns_pinned_to_full_oracle(oracle_lib):
+    """The Tier-C ground truth (oracle.poly_columns: matrix-vector Horner at
+    2x digits) equals the full 2x-digit reference_eval (harness.py:105-109,
+    fixed PS in MPFR) column by column, for exp and for the cosine's
+    p(X^2); power_columns equals mat_mul products."""
+    from _util import synth
+    from paper_2312_17396_b200 import taylor_exp_coeffs, taylor_cos_coeffs
+    n, d = 20, 31
+    cols = [0, 7, 19]
+    X = synth(n, 1.0, 3)
+    co = taylor_exp_coeffs(30).coeffs
+    ref = oracle_lib.reference_eval_words(X, co, d)
+    pc = oracle_lib.poly_columns(X, co, oracle_lib.bits_of(2 * d), cols)
+    nrm = np.abs(ref[0]).sum(0).max()
+    assert (oracle_lib.column_diff(pc, ref[:, :, cols].transpose(0, 2, 1)) <= 1e-58 * nrm).all()
+    Xc = synth(n, 1.0, 4, cos=True)
+    cc = taylor_cos_coeffs(24).coeffs
+    Z = oracle_lib.matmul(Xc, Xc, 2 * oracle_lib.bits_of(2 * d))
+    ref = oracle_lib.reference_eval_words(Z, cc, d)
+    pc = oracle_lib.poly_columns(Xc, cc, oracle_lib.bits_of(2 * d), cols, squares=True)
+    assert (oracle_lib.column_diff(pc, ref[:, :, cols].transpose(0, 2, 1)) <= 1e-58).all()
+    P = np.stack([X, X * 2.0 ** -60])
+    P3 = oracle_lib.matmul(oracle_lib.matmul(P, P, 400), P, 400)
+    pw = oracle_lib.power_columns(P, 3, 400, cols)
+    assert (oracle_lib.column_diff(pw, P3[:, :, cols].transpose(0, 2, 1)) <= 1e-60).all()   # 4 output words ~ 212 bits
+
+
+def test_fullsize_fixtures_consistent():
+    """tests/golden/fullsize_*: one record (and truth columns) per cfg3 matrix,
+    per cfg4 polynomial and for cfg5; snapped formats follow the digits."""
+    import json
+    import os
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    fx = json.load(open(os.path.join(here, "fullsize_plans.json")))
+    cols = np.load(os.path.join(here, "fullsize_cols.npz"))
+    assert len(fx["cfg3"]["plans"]) == 16 and len(fx["cfg4"]["plans"]) == 2 and len(fx["cfg5"]["plans"]) == 1
+    lat = (7, 15, 31, 63)
+    recs = fx["cfg3"]["plans"] + fx["cfg4"]["plans"] + fx["cfg4"]["fp64_pade13"] + fx["cfg5"]["plans"]
+    for rec in recs:
+        assert rec["snapped"] == [min(x for x in lat if x >= dd) for dd in rec["digits"]]
+        assert rec["margin_integer"] > 1e-9 and rec["margin_delta"] > 1e-9
+    for b in range(16):
+        assert cols[f"cfg3_{b}"].shape == (4, 2, 1024)
+    assert cols["cfg5"].shape == (4, 2, 8192)
