@@ -512,7 +512,10 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
     timer.start("mixed_horner")
     if structure is None:
         structure = _structure(prep, digits, nil)
-    blocks = _dd_blocks(h, prep, structure) if prep.lowp else prep.blocks
+    # two-pass assembly: dd blocks exist for the longest dd prefix of any
+    # group; each group takes B_k in dd only where its own level k is dd
+    # (fp64 block otherwise), so a matrix gets the same bits in any batch
+    dd_blocks = _dd_blocks(h, prep, structure) if prep.lowp else prep.blocks
     if sels is None:
         sels = _selections(structure, dev)
     group_list, nil_idx = structure
@@ -520,13 +523,14 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
     if nil_idx:
         # p = B_0 (engine.py:378-379, 473-474)
         ii = sels["nil"]
-        result.data[:, ii] = blocks[0].data[:, ii]
+        result.data[:, ii] = dd_blocks[0].data[:, ii]
     ws = _Workspace(B, n, dev)
     scalar_top = (m % s == 0)
     bm_words = prep.coeffs[m]
     for key, members in groups.items():
         fm, st = key
         sel = sels[key]
+        blocks = [dd_blocks[k] if fm[k] == DD else prep.blocks[k] for k in range(r + 1)]
         exps = exp_y = None
         if FP32 in fm:
             # exact power-of-two level scalings, computed on the device from

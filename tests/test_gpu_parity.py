@@ -185,6 +185,21 @@ def test_batch_invariance_bitwise(cuda):
         assert np.array_equal(words_of(one), rep.result.data[:, b].cpu().numpy())
 
 
+def test_batch_invariance_heterogeneous_plans_bitwise(cuda):
+    """Batch members whose plans keep different numbers of dd levels (the
+    post-planner dd re-assembly covers the longest prefix in the batch):
+    every member still equals its solo evaluation bit for bit."""
+    m = mp()
+    ctx = m.PrecisionCtx(31)
+    norms = [1.0, 6.0, 0.01, 8.0, 3.0]
+    X = np.stack([synth(40, t, 20 + b) for b, t in enumerate(norms)])
+    rep = m.ps_mixed_exp(X, 30, ctx)
+    assert len({tuple(r.diagnostics["level_formats"]) for r in rep}) >= 3
+    for b in range(len(norms)):
+        one = m.ps_mixed_exp(X[b], 30, ctx)
+        assert np.array_equal(words_of(one), rep.result.data[:, b].cpu().numpy()), b
+
+
 @pytest.mark.parametrize("fmt,bits", [(7, 24), (15, 53), (31, 106), (63, 212)])
 def test_gemm_operator_parity(cuda, oracle_lib, fmt, bits):
     """mat_mul per format vs the oracle's mat_mul at the format's bits:
