@@ -501,9 +501,12 @@ def _selections(structure, dev):
 
 
 def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buckets,
-            structure=None, sels=None) -> MatBatch:
+            structure=None, sels=None, commute: bool = True) -> MatBatch:
     """horner_mixed (engine.py:243-252) for every matrix of the batch,
-    grouped by level-format tuple (one launch per level per group)."""
+    grouped by level-format tuple (one launch per level per group).
+    ``commute``: Y and the blocks are polynomials in one X (every evaluator),
+    so the tensor-core levels may run phi_j Y; the public horner_mixed on
+    arbitrary blocks passes False and gets Y phi_j as the reference computes."""
     torch = _torch()
     wf, s, r, m = prep.wf, prep.s, prep.r, prep.m
     Y = prep.powers[s - 1]
@@ -559,7 +562,7 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
         # tensor-core level format (coarser levels use a prefix of its digit
         # planes); fp32 levels get a scaled fp32 copy (FFMA GEMM)
         ys: Dict[int, ge.Operand] = {}
-        tc_fmts = [f for f in set(fm[1:]) if ge.uses_tc(f)]
+        tc_fmts = [f for f in set(fm[1:]) if ge.uses_tc(f)] if commute else []
         if tc_fmts:
             # tensor cores: the level products run as phi_j Y (Y and phi_j
             # commute: both are polynomials in X), so each phi_j is split by
@@ -582,7 +585,7 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
         for j in range(j0, 0, -1):
             out = result if j - 1 == 0 else ws.next(fm[j - 1])
             ns = st[j - 1] if st else None       # this level's digit planes
-            if ge.uses_tc(fm[j]):
+            if ge.uses_tc(fm[j]) and commute:
                 # phi_j (rows) x Y (columns): left operand first
                 ge.horner(h, ge.prepare(h, phi, 0, fm[j], sel, nslices=ns), ys[fm[j]], fm[j], blocks[j - 1], out,
                           sel, None, ex(j), ex(j - 1), nslices=ns)
@@ -1082,4 +1085,4 @@ def horner_mixed(Bs: Sequence[MatBatch], Y: MatBatch, plan: EvaluationPlan) -> M
     m = plan.r * plan.s + 1       # m mod s != 0: B_r is a general block here
     prep = _Prepared(Y.fmt, plan.s, plan.r, m, [Y] * plan.s, list(Bs), norms, np.zeros((m + 1, 4)))
     digits = np.array([plan.level_digits] * Y.batch, dtype=np.int64)
-    return _horner(h, prep, digits, np.zeros(Y.batch, dtype=bool), _Buckets(False))
+    return _horner(h, prep, digits, np.zeros(Y.batch, dtype=bool), _Buckets(False), commute=False)
