@@ -14,6 +14,13 @@ C_IJ = A_I: B_:J from two gathered panels:
     column panel of phi_j each level -- in the level format, so fp32 levels
     move 1/4 of the dd bytes;
   * block assembly, the Horner add and all format conversions are local;
+  * overlap: every product is issued in row chunks (power chain) or column
+    chunks (Horner) and each finished chunk's panel all-gather is started
+    at once (async collective on NCCL's stream), so the gather of chunk t
+    runs while chunk t+1 is computed, and the next product's chunk t waits
+    only for its own gathered rows/columns.  Rows of a left operand and
+    columns of a right operand are split independently (per-row / per-column
+    digit scales), so chunking changes no bit of the result;
   * planner norms: local column abs-sums (mpps_assemble_blocks_dist) ->
     all-reduce(sum) along the process column -> column max -> all-reduce(max)
     over the grid; every rank then runs the same deterministic planner and
@@ -108,6 +115,28 @@ class ProcessGrid:
         dist.all_gather(parts, A.data.contiguous(), group=self.col_group)
         return MatBatch(torch.cat(parts, dim=2), A.fmt)
 
+    # --- chunked, asynchronous panels (compute/communication overlap) ---
+    def row_panel_start(self, A: MatBatch):
+        """Start the all-gather of A's rows along the process row; the
+        returned handle's panel_finish() gives [A_I0 ... A_I(pc-1)]."""
+        if self.pc == 1:
+            return _Done(A)
+        torch, dist = _torch(), _dist()
+        src = A.data.contiguous()
+        parts = [torch.empty_like(src) for _ in range(self.pc)]
+        work = dist.all_gather(parts, src, group=self.row_group, async_op=True)
+        return _Pending(work, parts, 3, A.fmt)
+
+    def col_panel_start(self, A: MatBatch):
+        """Start the all-gather of A's columns along the process column."""
+        if self.pr == 1:
+            return _Done(A)
+        torch, dist = _torch(), _dist()
+        src = A.data.contiguous()
+        parts = [torch.empty_like(src) for _ in range(self.pr)]
+        work = dist.all_gather(parts, src, group=self.col_group, async_op=True)
+        return _Pending(work, parts, 2, A.fmt)
+
     def sum_over_column(self, t):
         if self.pr > 1:
             _dist().all_reduce(t, op=_dist().ReduceOp.SUM, group=self.col_group)
@@ -135,6 +164,57 @@ class ProcessGrid:
         for i in range(self.pr):
             rows.append(torch.cat(parts[i * self.pc:(i + 1) * self.pc], dim=3))
         return torch.cat(rows, dim=2)[:, 0].double().cpu().numpy()
+
+
+class _Done:
+    __slots__ = ("A",)
+
+    def __init__(self, A):
+        self.A = A
+
+    def panel_finish(self) -> MatBatch:
+        return self.A
+
+
+class _Pending:
+    """An in-flight panel all-gather; panel_finish() makes the caller's
+    stream wait for it (no host block on NCCL) and concatenates the parts."""
+    __slots__ = ("work", "parts", "dim", "fmt")
+
+    def __init__(self, work, parts, dim, fmt):
+        self.work, self.parts, self.dim, self.fmt = work, parts, dim, fmt
+
+    def panel_finish(self) -> MatBatch:
+        self.work.wait()
+        return MatBatch(_torch().cat(self.parts, dim=self.dim), self.fmt)
+
+
+def chunk_bounds(extent: int, chunks: int, align: int = 128) -> List[Tuple[int, int]]:
+    """[lo, hi) pieces of ``extent`` for chunked products: at most
+    ``chunks`` pieces, interior boundaries on multiples of ``align`` (the
+    tensor-core row tile) where the extent allows."""
+    chunks = max(1, int(chunks))
+    if chunks == 1 or extent <= align:
+        return [(0, extent)]
+    step = -(-extent // chunks)
+    step = -(-step // align) * align
+    out, lo = [], 0
+    while lo < extent:
+        hi = min(extent, lo + step)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def rows_of(A: MatBatch, lo: int, hi: int) -> MatBatch:
+    return MatBatch(A.data[:, :, lo:hi, :], A.fmt)
+
+
+def cols_of(A: MatBatch, lo: int, hi: int) -> MatBatch:
+    return MatBatch(A.data[:, :, :, lo:hi], A.fmt)
+
+
+DEFAULT_CHUNKS = 4
 
 
 class DeviceOps:
@@ -234,12 +314,17 @@ def cos_argument_dist(Xblk: MatBatch, ctx: PrecisionCtx, grid: ProcessGrid, ops)
 
 
 def ps_mixed_dist(Xblk: MatBatch, series: CoefficientSeries, ctx: PrecisionCtx, grid: ProcessGrid,
-                  ops=None, delta: float = 10.0, fixed: bool = False) -> DistResult:
+                  ops=None, delta: float = 10.0, fixed: bool = False, chunks: Optional[int] = None,
+                  chunk_align: int = 128) -> DistResult:
     """ps_mixed_general (engine.py:348-387) -- or ps_fixed (304-345) with
     ``fixed`` -- of one n x n matrix distributed over ``grid``; Xblk is this
-    rank's block (fp64 or working format)."""
+    rank's block (fp64 or working format).  ``chunks``: row / column pieces
+    per product for communication overlap (default DEFAULT_CHUNKS on a
+    multi-rank grid, 1 on 1x1); the result does not depend on it."""
     torch = _torch()
     ops = ops or DeviceOps()
+    if chunks is None:
+        chunks = 1 if grid.pr * grid.pc == 1 else DEFAULT_CHUNKS
     m = series.degree
     if m < 1:
         raise ValueError("series degree must be >= 1")
@@ -257,11 +342,20 @@ def ps_mixed_dist(Xblk: MatBatch, series: CoefficientSeries, ctx: PrecisionCtx, 
         P1 = ops.empty(wf, mr, nc)
         ops.convert(Xblk, P1)
     powers = [P1]
+    rch = chunk_bounds(mr, chunks, chunk_align)
+    # row-panel gathers of the newest power, one per row chunk, in flight
+    # while the chunks after it are computed (and, for Y = X^s, while the
+    # blocks are assembled and the norms reduced)
+    pend = [grid.row_panel_start(rows_of(P1, lo, hi)) for lo, hi in rch]
     if s > 1:
         Xr = ops.prepare(grid.col_panel(P1), 1, wf)      # gathered and split once
         for _ in range(1, s):
             C = ops.empty(wf, mr, nc)
-            ops.gemm_op(ops.prepare(grid.row_panel(powers[-1]), 0, wf), Xr, C)
+            nxt = []
+            for (lo, hi), pnd in zip(rch, pend):
+                ops.gemm_op(ops.prepare(pnd.panel_finish(), 0, wf), Xr, rows_of(C, lo, hi))
+                nxt.append(grid.row_panel_start(rows_of(C, lo, hi)))
+            pend = nxt
             powers.append(C)
     blocks = [ops.empty(wf, mr, nc) for _ in range(r + 1)]
     coeffs = ops.coeffs(series, ctx)
@@ -287,7 +381,8 @@ def ps_mixed_dist(Xblk: MatBatch, series: CoefficientSeries, ctx: PrecisionCtx, 
     ey = _exp_for(float(norms[r + 1]))
     # Horner (engine.py:243-252)
     Y = powers[s - 1]
-    Yrow_w = grid.row_panel(Y)
+    ypanels = [p.panel_finish() for p in pend]
+    Yrow_w = ypanels[0] if len(ypanels) == 1 else MatBatch(torch.cat([p.data for p in ypanels], dim=2), wf)
     from . import gemm_engine as ge
     yrow = {}
     tc_fmts = [f for f in set(fm[1:]) if ge.uses_tc(f) and not getattr(ops, "simt_only", False)]
@@ -306,9 +401,20 @@ def ps_mixed_dist(Xblk: MatBatch, series: CoefficientSeries, ctx: PrecisionCtx, 
         phi = ops.empty(fm[r], mr, nc)
         ops.convert(blocks[r], phi, ex[r])
         j0 = r
+    # Horner levels in column chunks: chunk t of level j-1 needs only the
+    # gathered column chunk t of phi_j; its own gather starts as soon as it
+    # is written
+    cch = chunk_bounds(nc, chunks, chunk_align)
+    pend = [grid.col_panel_start(cols_of(phi, lo, hi)) for lo, hi in cch] if j0 > 0 else []
     for j in range(j0, 0, -1):
         out = ops.empty(fm[j - 1], mr, nc)
-        ops.horner_op(yrow[fm[j]], ops.prepare(grid.col_panel(phi), 1, fm[j]), fm[j], blocks[j - 1], out,
-                      ey if fm[j] == FP32 else 0, ex[j], ex[j - 1])
+        nxt = []
+        for (lo, hi), pnd in zip(cch, pend):
+            ops.horner_op(yrow[fm[j]], ops.prepare(pnd.panel_finish(), 1, fm[j]), fm[j],
+                          cols_of(blocks[j - 1], lo, hi), cols_of(out, lo, hi),
+                          ey if fm[j] == FP32 else 0, ex[j], ex[j - 1])
+            if j > 1:
+                nxt.append(grid.col_panel_start(cols_of(out, lo, hi)))
+        pend = nxt
         phi = out
     return DistResult(phi, digits, nu, False, norms, s, r)

@@ -66,3 +66,29 @@ def test_summa_1x1_vs_oracle(nccl1, oracle_lib):
     assert res.digits == ref.digits
     diff, refn = ref.compare(res.block.data[:, 0].cpu().numpy())
     assert diff <= tol(res.r, n, d) * refn
+
+
+def test_summa_chunked_overlap_is_bitwise_invisible(cuda):
+    """The chunked (overlapped) power and Horner chains give exactly the
+    unchunked result: row chunks of a left operand and column chunks of a
+    right operand (ragged last chunk, strided views into the block) are
+    split and multiplied independently of the rest."""
+    import torch
+    import paper_2312_17396_b200 as m
+    from paper_2312_17396_b200 import summa
+    from paper_2312_17396_b200.precision import MatBatch
+    n = 640
+    ctx = m.PrecisionCtx(31)
+    grid = summa.ProcessGrid.single()
+    for family, X in (("exp", synth(n, 1.0, 5)), ("cos", synth(n, 1.0, 6, cos=True))):
+        blk = MatBatch(torch.from_numpy(X).cuda()[None, None], m.FP64)
+        ops = summa.DeviceOps()
+        if family == "cos":
+            blk = summa.cos_argument_dist(blk, ctx, grid, ops)
+            series = m.taylor_cos_coeffs(24)
+        else:
+            series = m.taylor_exp_coeffs(30)
+        a = summa.ps_mixed_dist(blk, series, ctx, grid, ops, chunks=1)
+        b = summa.ps_mixed_dist(blk, series, ctx, grid, ops, chunks=3)
+        assert a.digits == b.digits
+        assert torch.equal(a.block.data, b.block.data), family
