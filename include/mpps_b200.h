@@ -233,6 +233,10 @@ int mpps_oz_slices_for_bits(int fmt, int digit_bits);
 /* Largest inner dimension K for which 8-bit digits keep every int32
  * diagonal accumulator exact at any format (qd: 28 planes). */
 int mpps_oz_max_k_8bit(void);
+/* Largest inner dimension K for which a product of format fmt's full plane
+ * count with digit_bits-bit digits keeps its int32 diagonal accumulators
+ * exact (dd: 10070 with 8-bit digits, 31770 with 7-bit; qd: 4851 / 16443). */
+int mpps_oz_max_k(int fmt, int digit_bits);
 
 /* Diagnostic: pipe-peak probe used by bench.py for the per-precision
  * roofline denominators (not a reference operator).  Launches `blocks`

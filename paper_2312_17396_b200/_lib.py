@@ -29,7 +29,7 @@ EXPORTED = (
     "mpps_axpy", "mpps_powers", "mpps_slice_into", "mpps_assemble_blocks", "mpps_assemble_blocks_hc", "mpps_assemble_hc_supported", "mpps_assemble_blocks_hc_n", "mpps_assemble_hc_n_supported", "mpps_one_norm", "mpps_one_norm_complex", "mpps_level_exps",
     "mpps_horner_step", "mpps_horner_scalar_top", "mpps_probe_fma",
     "mpps_assemble_blocks_dist", "mpps_colmax", "mpps_slice", "mpps_gemm_sliced",
-    "mpps_horner_step_sliced", "mpps_oz_slices_for", "mpps_oz_slices_for_bits", "mpps_oz_max_k_8bit", "mpps_probe_i8mma", "mpps_debug_oz_trace",
+    "mpps_horner_step_sliced", "mpps_oz_slices_for", "mpps_oz_slices_for_bits", "mpps_oz_max_k_8bit", "mpps_oz_max_k", "mpps_probe_i8mma", "mpps_debug_oz_trace",
     "mpps_debug_oz_flags", "mpps_debug_probe_i8mma_n", "mpps_probe_ingest",
 )
 
@@ -139,6 +139,7 @@ def load_library(path: Optional[str] = None):
         lib.mpps_oz_slices_for.argtypes = [ip]
         lib.mpps_oz_slices_for_bits.argtypes = [ip, ip]
         lib.mpps_oz_max_k_8bit.argtypes = []
+        lib.mpps_oz_max_k.argtypes = [ip, ip]
         lib.mpps_probe_i8mma.argtypes = [vp, ip, ip, vp]
         lib.mpps_debug_oz_trace.argtypes = [vp]
         lib.mpps_debug_oz_trace.restype = None
@@ -294,6 +295,10 @@ class Handle:
 
     def max_k_8bit(self) -> int:
         return int(self.lib.mpps_oz_max_k_8bit())
+
+    def max_k(self, fmt: int, db: int) -> int:
+        """Largest exact K for fmt's full plane count at db-bit digits."""
+        return int(self.lib.mpps_oz_max_k(int(fmt), int(db)))
 
     def slice(self, src: MatBatch, side: int, S: int, sel=None, db: int = 7) -> "Slices":
         """side 0: split rows (left operand); side 1: split columns (right);

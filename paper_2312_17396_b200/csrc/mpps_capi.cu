@@ -1,7 +1,7 @@
 // C-ABI implementation of include/mpps_b200.h: kernel launches for the
 // mixed-precision Paterson-Stockmeyer hot path on sm_100a.
 //
-// Kernels in this file (GEMMs are in gemm.cuh):
+// Kernels in this file (the tensor-core GEMMs and digit splits are in ozaki.cuh):
 //   convert_kernel      round_to / format conversion      precision.py:153-157
 //   axpy_kernel         mat_axpy                          precision.py:187-197
 //   assemble_kernel     assemble_block x (r+1) + column   engine.py:127-154,
@@ -16,7 +16,7 @@
 #include <stdlib.h>
 
 #include "../../include/mpps_b200.h"
-#include "gemm.cuh"
+#include "formats.cuh"
 #include "ozaki.cuh"
 
 // Launch with programmatic stream serialization (PDL) when MPPS_PDL=1: the
@@ -470,6 +470,18 @@ __global__ void norm_reduce_kernel(const double *partial, double *norms, int nbl
   if (threadIdx.x == 0) norms[(long long)b * nblk + k] = red[0];
 }
 
+// Stage 1 of the two-stage reduction for few (batch x block) pairs and many
+// chunks (one large matrix): colsum[b][k][col] = sum_chunk partial (the same
+// fixed chunk order as norm_reduce_kernel, so the norms are bitwise equal).
+__global__ void chunk_sum_kernel(const double *partial, double *colsum, int nblk, int nchunk, int cols) {
+  MPPS_PDL_ENTER();
+  const int col = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y, b = blockIdx.z;
+  if (col >= cols) return;
+  double s = 0.0;
+  for (int c = 0; c < nchunk; ++c) s += partial[(((long long)b * nchunk + c) * nblk + k) * cols + col];
+  colsum[((long long)b * nblk + k) * cols + col] = s;
+}
+
 // Complex one_norm on the real embedding [[Re, -Im], [Im, Re]] (2nc x 2nc):
 // partial[b][chunk][col] = sum over the chunk's rows i < nc of
 // |z_i,col| = hypot(Re, Im) (precision.py:235-249 with mpc_abs).
@@ -710,43 +722,6 @@ __global__ void scalar_top_wf_kernel(const ScalarTopArgs a) {
   }
 }
 
-// --------------------------------------------------------- GEMM launches
-template <int F, int FO, int MODE>
-int launch_gemm(mpps_handle *h, const GemmArgs &g, int nb) {
-  constexpr size_t smem = gemm_smem_bytes<F>();
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<F, FO, MODE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "gemm attr: %s", cudaGetErrorString(e));
-    configured = true;
-  }
-  dim3 grid((g.N + Tile<F>::BN - 1) / Tile<F>::BN, (g.M + Tile<F>::BM - 1) / Tile<F>::BM, nb);
-  if (grid.x == 0 || grid.y == 0 || nb == 0) return MPPS_OK;
-  gemm_kernel<F, FO, MODE><<<grid, kThreads, smem, h->stream>>>(g);
-  return after_launch(h, "gemm_kernel");
-}
-
-int dispatch_gemm(mpps_handle *h, int fi, int fo, int mode, const GemmArgs &g, int nb) {
-  if (mode == 0) {
-    switch (fi) {
-      case F32: return launch_gemm<F32, F32, 0>(h, g, nb);
-      case F64: return launch_gemm<F64, F64, 0>(h, g, nb);
-      case DD: return launch_gemm<DD, DD, 0>(h, g, nb);
-      case QD: return launch_gemm<QD, QD, 0>(h, g, nb);
-    }
-  } else {
-#define CASE(A, B) \
-  if (fi == A && fo == B) return launch_gemm<A, B, 1>(h, g, nb);
-    CASE(F32, F32) CASE(F32, F64) CASE(F32, DD) CASE(F32, QD)
-    CASE(F64, F64) CASE(F64, DD) CASE(F64, QD)
-    CASE(DD, DD) CASE(DD, QD)
-    CASE(QD, QD)
-#undef CASE
-  }
-  return set_err(h, MPPS_EFMT, "no GEMM for level formats %d -> %d (output must be at least as wide)", fi, fo);
-}
-
 // Pipe-peak probes (bench.py roofline denominators): 8 independent FMA
 // chains per thread, full-chip grid.  2 flops per FMA.
 template <typename T>
@@ -769,6 +744,31 @@ int ew_grid(long long total) {
   if (g > 148 * 8) g = 148 * 8;
   if (g < 1) g = 1;
   return (int)g;
+}
+
+// norms[b][k] = max_col sum_chunk partial[b][chunk][k][col].  One CTA per
+// (b, k) when there are enough of them; otherwise (one large matrix: e.g.
+// 6 CTAs reading 512 chunks x 8192 columns at cfg5) the chunk sums first run
+// column-parallel into stream-ordered scratch.
+int launch_norm_reduce(mpps_handle *h, const double *partial, double *norms, int nblk, int nchunk, int cols,
+                       int batch) {
+  if (nblk * batch >= 148 || nchunk <= 4) {
+    launch_k(norm_reduce_kernel, dim3(nblk, batch), dim3(256), 0, h->stream, partial, norms, nblk, nchunk, cols);
+    return after_launch(h, "norm_reduce_kernel");
+  }
+  double *colsum = nullptr;
+  cudaError_t e = cudaMallocAsync((void **)&colsum, sizeof(double) * (size_t)batch * nblk * cols, h->stream);
+  if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "norm scratch: %s", cudaGetErrorString(e));
+  launch_k(chunk_sum_kernel, dim3((cols + 255) / 256, nblk, batch), dim3(256), 0, h->stream, (const double *)partial,
+           colsum, nblk, nchunk, cols);
+  int rc = after_launch(h, "chunk_sum_kernel");
+  if (!rc) {
+    launch_k(norm_reduce_kernel, dim3(nblk, batch), dim3(256), 0, h->stream, (const double *)colsum, norms, nblk, 1,
+             cols);
+    rc = after_launch(h, "norm_reduce_kernel");
+  }
+  cudaFreeAsync(colsum, h->stream);
+  return rc;
 }
 
 }  // namespace
@@ -799,8 +799,7 @@ static int launch_assemble_c(mpps_handle *h, const mpps_mat *powers, int m, cons
   launch_k(assemble_c_kernel<WF, NB, NP, ND>, dim3(dim3((cols + 127) / 128, a.nchunk, batch)), dim3(128), 0, h->stream, a);
   int rc = after_launch(h, "assemble_c_kernel");
   if (rc) return rc;
-  launch_k(norm_reduce_kernel, dim3(dim3(NB + 1, batch)), dim3(256), 0, h->stream, a.partial, norms, NB + 1, a.nchunk, cols);
-  rc = after_launch(h, "norm_reduce_kernel");
+  rc = launch_norm_reduce(h, a.partial, norms, NB + 1, a.nchunk, cols, batch);
   cudaFreeAsync(a.partial, h->stream);
   return rc;
 }
@@ -876,25 +875,6 @@ int mpps_convert(mpps_handle *h, const mpps_mat *src, mpps_mat *dst, const int *
     case QD: launch_k(convert_kernel<QD>, dim3(grid), dim3(256), 0, h->stream, a); break;
   }
   return after_launch(h, "convert_kernel");
-}
-
-int mpps_gemm(mpps_handle *h, const mpps_mat *A, const mpps_mat *B, mpps_mat *C, const int *sel, int nsel) {
-  int rc;
-  if ((rc = check_mat(h, A, "gemm.A")) || (rc = check_mat(h, B, "gemm.B")) || (rc = check_mat(h, C, "gemm.C")))
-    return rc;
-  if (A->fmt != B->fmt || A->fmt != C->fmt)
-    return set_err(h, MPPS_EFMT, "gemm: operand formats %d,%d,%d differ", A->fmt, B->fmt, C->fmt);
-  if (A->cols != B->rows || C->rows != A->rows || C->cols != B->cols)
-    return set_err(h, MPPS_EINVAL, "mat_mul: (%d, %d) x (%d, %d) -> (%d, %d)", A->rows, A->cols, B->rows, B->cols,
-                   C->rows, C->cols);
-  GemmArgs g;
-  memset(&g, 0, sizeof(g));
-  g.M = A->rows; g.N = B->cols; g.K = A->cols;
-  g.A = ref_of(A); g.B = ref_of(B); g.C = ref_of(C);
-  g.sel = sel;
-  int nb = sel ? nsel : C->batch;
-  int fi = fmt_index(A->fmt);
-  return dispatch_gemm(h, fi, fi, 0, g, nb);
 }
 
 int mpps_axpy(mpps_handle *h, const double *alpha, const mpps_mat *A, const mpps_mat *B, mpps_mat *C) {
@@ -974,8 +954,7 @@ static int assemble_common(mpps_handle *h, const mpps_mat *powers, int s, int m,
   int rc = after_launch(h, "assemble_kernel");
   if (rc) return rc;
   if (norms) {
-    launch_k(norm_reduce_kernel, dim3(dim3(r + 2, batch)), dim3(256), 0, h->stream, a.partial, norms, r + 2, a.nchunk, cols);
-    rc = after_launch(h, "norm_reduce_kernel");
+    rc = launch_norm_reduce(h, a.partial, norms, r + 2, a.nchunk, cols, batch);
   } else {
     long long tot = (long long)batch * (r + 2) * cols;
     colsum_reduce_kernel<<<ew_grid(tot), 256, 0, h->stream>>>(a.partial, colsums, r + 2, a.nchunk, cols, batch);
@@ -1122,8 +1101,7 @@ int mpps_one_norm(mpps_handle *h, const mpps_mat *A, double *norms) {
   colsum_kernel<<<dim3((A->cols + 127) / 128, a.nchunk, A->batch), 128, 0, h->stream>>>(a);
   rc = after_launch(h, "colsum_kernel");
   if (rc) return rc;
-  launch_k(norm_reduce_kernel, dim3(dim3(1, A->batch)), dim3(256), 0, h->stream, a.partial, norms, 1, a.nchunk, A->cols);
-  rc = after_launch(h, "norm_reduce_kernel");
+  rc = launch_norm_reduce(h, a.partial, norms, 1, a.nchunk, A->cols, A->batch);
   cudaFreeAsync(a.partial, h->stream);
   return rc;
 }
@@ -1178,28 +1156,6 @@ int mpps_level_exps(mpps_handle *h, const double *norms, int batch, int r, unsig
   if (n == 0) return MPPS_OK;
   launch_k(level_exps_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, h->stream, norms, batch, r, fp32_mask, exps, exp_y);
   return after_launch(h, "level_exps_kernel");
-}
-
-int mpps_horner_step(mpps_handle *h, const mpps_mat *Y, const mpps_mat *phi, const mpps_mat *Bprev, mpps_mat *out,
-                     const int *sel, int nsel, const int *exp_y, const int *exp_in, const int *exp_out) {
-  int rc;
-  if ((rc = check_mat(h, Y, "horner.Y")) || (rc = check_mat(h, phi, "horner.phi")) ||
-      (rc = check_mat(h, Bprev, "horner.Bprev")) || (rc = check_mat(h, out, "horner.out")))
-    return rc;
-  if (Y->fmt != phi->fmt) return set_err(h, MPPS_EFMT, "horner: Y and phi formats differ (%d, %d)", Y->fmt, phi->fmt);
-  if (fmt_index(Bprev->fmt) == F32) return set_err(h, MPPS_EFMT, "horner: B_{j-1} must be at the working format");
-  const int M = Y->rows, K = Y->cols, N = phi->cols;
-  if (phi->rows != K || Bprev->rows != M || Bprev->cols != N || out->rows != M || out->cols != N)
-    return set_err(h, MPPS_EINVAL, "horner: operands must be Y %dx%d, phi %dx%d, B/out %dx%d", M, K, K, N, M, N);
-  GemmArgs g;
-  memset(&g, 0, sizeof(g));
-  g.M = M; g.N = N; g.K = K;
-  g.A = ref_of(Y); g.B = ref_of(phi); g.C = ref_of(out);
-  g.sel = sel;
-  g.epi.Bprev = ref_of(Bprev);
-  g.epi.exp_y = exp_y; g.epi.exp_in = exp_in; g.epi.exp_out = exp_out;
-  int nb = sel ? nsel : out->batch;
-  return dispatch_gemm(h, fmt_index(Y->fmt), fmt_index(out->fmt), 1, g, nb);
 }
 
 int mpps_horner_scalar_top(mpps_handle *h, const double *bm, int fmt_top, const mpps_mat *Y, const mpps_mat *Bprev,
@@ -1808,6 +1764,79 @@ static int check_sliced(mpps_handle *h, const mpps_slices *A, const mpps_slices 
 
 extern "C" {
 
+// mat_mul / Horner step on plain matrices (precision.py:160-184,
+// engine.py:249-251): both operands are split into digit planes in
+// stream-ordered scratch and multiplied on the tensor cores -- the same
+// kernels the evaluators drive through mpps_slice + mpps_*_sliced.  8-bit
+// digits while the format's plane count stays exact at K (mpps_oz_max_k),
+// 7-bit above; the format's full plane count.
+static int tc_split_pair(mpps_handle *h, const mpps_mat *L, const mpps_mat *R, int fmt, int K, const int *sel,
+                         int nsel, mpps_slices *sl, mpps_slices *sr, void **mem) {
+  const int db = K <= mpps_oz_max_k(fmt, 8) ? 8 : 7;
+  const int S = oz_slices_for(fmt_index(fmt), db);
+  const int batch = L->batch;
+  mpps_slices *sides[2] = {sl, sr};
+  const int rows[2] = {L->rows, R->cols};
+  size_t off[3] = {0, 0, 0};
+  for (int i = 0; i < 2; ++i) {
+    mpps_slices *o = sides[i];
+    o->nslices = S; o->batch = batch; o->digit_bits = db;
+    o->rpad = (rows[i] + oz::kTileM - 1) / oz::kTileM * oz::kTileM;
+    o->kpad = (K + oz::kKStep - 1) / oz::kKStep * oz::kKStep;
+    size_t d = (size_t)S * batch * o->rpad * o->kpad, e = sizeof(int) * (size_t)batch * o->rpad;
+    off[i + 1] = off[i] + ((d + 255) & ~(size_t)255) + ((e + 255) & ~(size_t)255);
+  }
+  cudaError_t e = cudaMallocAsync(mem, off[2], h->stream);
+  if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "digit-plane scratch: %s", cudaGetErrorString(e));
+  for (int i = 0; i < 2; ++i) {
+    mpps_slices *o = sides[i];
+    size_t d = (size_t)S * batch * o->rpad * o->kpad;
+    o->digits = (char *)*mem + off[i];
+    o->exps = (int *)((char *)*mem + off[i] + ((d + 255) & ~(size_t)255));
+  }
+  int rc = mpps_slice(h, L, 0, sl, sel, nsel);
+  if (!rc) rc = mpps_slice(h, R, 1, sr, sel, nsel);
+  return rc;
+}
+
+int mpps_gemm(mpps_handle *h, const mpps_mat *A, const mpps_mat *B, mpps_mat *C, const int *sel, int nsel) {
+  int rc;
+  if ((rc = check_mat(h, A, "gemm.A")) || (rc = check_mat(h, B, "gemm.B")) || (rc = check_mat(h, C, "gemm.C")))
+    return rc;
+  if (A->fmt != B->fmt || A->fmt != C->fmt)
+    return set_err(h, MPPS_EFMT, "gemm: operand formats %d,%d,%d differ", A->fmt, B->fmt, C->fmt);
+  if (A->cols != B->rows || C->rows != A->rows || C->cols != B->cols)
+    return set_err(h, MPPS_EINVAL, "mat_mul: (%d, %d) x (%d, %d) -> (%d, %d)", A->rows, A->cols, B->rows, B->cols,
+                   C->rows, C->cols);
+  if (A->batch != B->batch || A->batch != C->batch) return set_err(h, MPPS_EINVAL, "mat_mul: batch mismatch");
+  mpps_slices sa, sb;
+  void *mem = nullptr;
+  rc = tc_split_pair(h, A, B, C->fmt, A->cols, sel, nsel, &sa, &sb, &mem);
+  if (!rc) rc = mpps_gemm_sliced(h, &sa, &sb, sa.nslices, A->rows, B->cols, A->cols, C, sel, nsel);
+  if (mem) cudaFreeAsync(mem, h->stream);
+  return rc;
+}
+
+int mpps_horner_step(mpps_handle *h, const mpps_mat *Y, const mpps_mat *phi, const mpps_mat *Bprev, mpps_mat *out,
+                     const int *sel, int nsel, const int *exp_y, const int *exp_in, const int *exp_out) {
+  int rc;
+  if ((rc = check_mat(h, Y, "horner.Y")) || (rc = check_mat(h, phi, "horner.phi")) ||
+      (rc = check_mat(h, Bprev, "horner.Bprev")) || (rc = check_mat(h, out, "horner.out")))
+    return rc;
+  if (Y->fmt != phi->fmt) return set_err(h, MPPS_EFMT, "horner: Y and phi formats differ (%d, %d)", Y->fmt, phi->fmt);
+  if (fmt_index(Bprev->fmt) == F32) return set_err(h, MPPS_EFMT, "horner: B_{j-1} must be at the working format");
+  const int M = Y->rows, K = Y->cols, N = phi->cols;
+  if (phi->rows != K || Bprev->rows != M || Bprev->cols != N || out->rows != M || out->cols != N)
+    return set_err(h, MPPS_EINVAL, "horner: operands must be Y %dx%d, phi %dx%d, B/out %dx%d", M, K, K, N, M, N);
+  if (Y->batch != phi->batch) return set_err(h, MPPS_EINVAL, "horner: batch mismatch");
+  mpps_slices sy, sp;
+  void *mem = nullptr;
+  rc = tc_split_pair(h, Y, phi, Y->fmt, K, sel, nsel, &sy, &sp, &mem);
+  if (!rc) rc = mpps_horner_step_sliced(h, &sy, &sp, sy.nslices, Bprev, out, sel, nsel, exp_y, exp_in, exp_out);
+  if (mem) cudaFreeAsync(mem, h->stream);
+  return rc;
+}
+
 int mpps_gemm_sliced(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, int nslices, int M, int N, int K,
                      mpps_mat *C, const int *sel, int nsel) {
   int rc = check_mat(h, C, "gemm_sliced.C");
@@ -1842,6 +1871,12 @@ int mpps_horner_step_sliced(mpps_handle *h, const mpps_slices *Y, const mpps_sli
 int mpps_oz_slices_for(int fmt) { return oz_slices_for(fmt_index(fmt)); }
 int mpps_oz_slices_for_bits(int fmt, int digit_bits) { return oz_slices_for(fmt_index(fmt), digit_bits == 8 ? 8 : 7); }
 int mpps_oz_max_k_8bit(void) { return kOzMaxK8; }
+int mpps_oz_max_k(int fmt, int digit_bits) {
+  const int db = digit_bits == 8 ? 8 : 7;
+  const int S = oz_slices_for(fmt_index(fmt), db);
+  if (S < 1) return 0;
+  return (int)(2147483647.0 / oz_diag_bound(S, db));
+}
 
 void mpps_debug_oz_trace(void *buf) { g_oz_trace = (unsigned long long *)buf; }
 void mpps_debug_oz_flags(int flags) { g_oz_dbg = flags & 0xff; g_oz_group_override = flags >> 8; }

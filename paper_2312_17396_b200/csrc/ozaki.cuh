@@ -12,7 +12,7 @@
 // -> fp64 / dd / qd).  The epilogue recombines the diagonals exactly (groups
 // of three fit a double), sums them in the target format, applies the
 // power-of-two row/column scales and then the same store / fused Horner
-// epilogue as the SIMT GEMM (gemm.cuh).
+// epilogue helpers (formats.cuh).
 //
 // Slices are stored K-major ([S][batch][rows_pad][K_pad] int8, rows_pad a
 // multiple of the tile, K_pad of 32, padding zero), B transposed (its columns
@@ -23,7 +23,7 @@
 #pragma once
 #include <cuda.h>
 #include <cooperative_groups.h>
-#include "gemm.cuh"
+#include "formats.cuh"
 
 namespace mpps {
 namespace oz {

@@ -318,7 +318,7 @@ def _paired_powers(h, X: MatBatch, wf: int, s: int) -> List[MatBatch]:
     working-precision products, associated differently than the
     reference's X^{k+1} = X^k X; engine.py:151-153)."""
     B, n, dev = X.batch, X.rows, X.device
-    db = ge.digit_bits_for(h, n)
+    db = ge.digit_bits_for(h, n, wf)
     S = h.slices_for(wf, db)
     SP = _lib.Slices(S, B, 2 * n, n, dev, db)
     h.slice_into(X, SP, 0)
@@ -473,7 +473,7 @@ def _structure(prep: _Prepared, digits: np.ndarray, nil: np.ndarray):
     nil_idx = []
     tc = prep.wf in (FP64, DD) and ge.uses_tc(prep.wf)
     h = _lib.handle_for() if tc else None
-    db = ge.digit_bits_for(h, prep.powers[0].rows) if tc else None
+    db = ge.digit_bits_for(h, prep.powers[0].rows, prep.wf) if tc else None
     memo = {}
     nil_l = np.asarray(nil, dtype=bool).tolist()
     for b, dg in enumerate(map(tuple, np.asarray(digits).tolist())):
@@ -568,12 +568,12 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
             # commute: both are polynomials in X), so each phi_j is split by
             # rows (one pass, no column-exponent pre-pass) and Y by columns
             # once, at the finest level's planes
-            ytc = ge.prepare(h, Y, 1, max(tc_fmts), sel, nslices=max(st) if st else None)
+            ytc = ge.prepare(h, Y, 1, max(tc_fmts), sel, nslices=max(st) if st else None, wf=wf)
             for f in tc_fmts:
                 ys[f] = ytc
         for f in sorted(set(fm[1:])):
             if f not in ys:
-                ys[f] = ge.prepare(h, Y, 0, f, sel, exp_y if f == FP32 else None)
+                ys[f] = ge.prepare(h, Y, 0, f, sel, exp_y if f == FP32 else None, wf=wf)
         if scalar_top:
             out = result if r - 1 == 0 else ws.next(fm[r - 1])
             h.horner_scalar_top(bm_words, fm[r], Y, blocks[r - 1], out, sel, ex(r - 1))
@@ -587,10 +587,10 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
             ns = st[j - 1] if st else None       # this level's digit planes
             if ge.uses_tc(fm[j]) and commute:
                 # phi_j (rows) x Y (columns): left operand first
-                ge.horner(h, ge.prepare(h, phi, 0, fm[j], sel, nslices=ns), ys[fm[j]], fm[j], blocks[j - 1], out,
+                ge.horner(h, ge.prepare(h, phi, 0, fm[j], sel, nslices=ns, wf=wf), ys[fm[j]], fm[j], blocks[j - 1], out,
                           sel, None, ex(j), ex(j - 1), nslices=ns)
             else:
-                ge.horner(h, ys[fm[j]], ge.prepare(h, phi, 1, fm[j], sel), fm[j], blocks[j - 1], out, sel,
+                ge.horner(h, ys[fm[j]], ge.prepare(h, phi, 1, fm[j], sel, wf=wf), fm[j], blocks[j - 1], out, sel,
                           exp_y if fm[j] == FP32 else None, ex(j), ex(j - 1))
             phi = out
     timer.stop()

@@ -1,16 +1,10 @@
-"""GEMM engine selection for the PS pipeline.
-
-Two sm_100a implementations of every multiword GEMM exist in
-libmpps_b200.so:
-
-* ``tc``   -- INT8 tensor cores (tcgen05.mma kind::i8) on exact digit-plane
-  splittings of the operands (csrc/ozaki.cuh): fp64 (8 planes), dd (16),
-  qd (31).  The operand that stays fixed across a chain (X in the power
-  chain, Y in the Horner chain) is split once per evaluation.
-* ``simt`` -- FP64-pipe error-free-transform GEMMs and FFMA fp32 GEMMs
-  (csrc/gemm.cuh).
-
-fp32 levels use 4 digit planes (27 bits >= 24) on the tensor cores.
+"""The GEMMs of the PS pipeline: every product (power chain, Horner levels,
+squarings, SUMMA blocks, the operator-level mat_mul) runs on the INT8
+tensor cores (tcgen05.mma kind::i8) on exact digit-plane splittings of the
+operands (csrc/ozaki.cuh): fp32 (4 planes), fp64 (8), dd (14 / 16), qd
+(28 / 31).  The operand that stays fixed across a chain (X in the power
+chain, Y in the Horner chain) is split once per evaluation.  (Round 1 also
+kept a SIMT DFMA engine behind MPPS_GEMM=simt; it was retired in round 2.)
 
 Digit width: products with inner dimension K <= 4800 split into 8-bit
 digits -- dd in 14 planes (110 bits) instead of 16 7-bit ones (111 bits):
@@ -22,9 +16,6 @@ floating-point split with a bottom-up carry pass.  Above K = 4800 the int32
 diagonal accumulators of qd's 28 planes could overflow, so larger K keeps
 7-bit digits.  Both operands of a product share K, hence the width.
 ``MPPS_DIGITS=7`` forces 7-bit digits everywhere.
-
-The default is ``tc``; ``MPPS_GEMM=simt`` (environment) or
-``set_engine("simt")`` selects the SIMT kernels (A/B evidence, tests).
 """
 
 from __future__ import annotations
@@ -33,7 +24,6 @@ import os
 
 from .precision import FP32, MatBatch
 
-_ENGINE = os.environ.get("MPPS_GEMM", "tc").lower()
 _DIGITS = os.environ.get("MPPS_DIGITS", "auto")
 _MIN_K_8BIT = 0
 
@@ -46,34 +36,34 @@ def set_digit_bits(db) -> None:
     _DIGITS = str(db)
 
 
-def digit_bits_for(h, K: int) -> int:
-    """Digit width of a product with inner dimension K."""
-    if _DIGITS == "7" or K > h.max_k_8bit():
+def digit_bits_for(h, K: int, fmt: int = 63) -> int:
+    """Digit width of the products of an evaluation at working format
+    ``fmt`` with inner dimension K: 8-bit while fmt's full plane count keeps
+    the int32 diagonal accumulators exact at K (dd up to K = 10070, qd up to
+    4851; mpps_oz_max_k), 7-bit above.  Every split of one evaluation must
+    pass the same (K, fmt) -- the working format, also for the coarser
+    levels' operands -- so both operands of every product share the width.
+    The default fmt (qd) is the conservative bound for any format."""
+    if _DIGITS == "7" or K > h.max_k(fmt, 8):
         return 7
     if _DIGITS == "8":
         return 8
     return 8 if K >= _MIN_K_8BIT else 7
 
 
-def set_engine(name: str) -> None:
-    global _ENGINE
-    if name not in ("tc", "simt"):
-        raise ValueError("engine must be 'tc' or 'simt'")
-    _ENGINE = name
-
-
 def engine() -> str:
-    return _ENGINE
+    return "tc"
 
 
 def uses_tc(fmt: int) -> bool:
-    return _ENGINE == "tc"
+    return True
 
 
 class Operand:
-    """A GEMM operand prepared for one side: the MatBatch itself (SIMT) or
-    its digit planes (tensor cores).  ``fmt`` is the format it was prepared
-    at (for SIMT the data is converted to it)."""
+    """A GEMM operand prepared for one side: its digit planes (``slices``)
+    plus the source matrix; ``fmt`` is the format it was prepared at.  The
+    host test double of the SUMMA driver (tests/_cpu_ops.py) builds
+    Operands without planes."""
 
     __slots__ = ("mat", "slices", "fmt", "side")
 
@@ -105,39 +95,28 @@ def planes_for_digits(h, fmt: int, digits: int, db: int) -> int:
     return full
 
 
-def prepare(h, A: MatBatch, side: int, fmt: int, sel=None, exp=None, nslices=None) -> Operand:
+def prepare(h, A: MatBatch, side: int, fmt: int, sel=None, exp=None, nslices=None, wf=None) -> Operand:
     """Prepare A as the left (side 0) or right (side 1) operand of GEMMs at
-    ``fmt``.  For the tensor-core engine the split uses the planes of the
-    finest format any later use needs (the caller passes it as ``fmt``);
-    a coarser level uses a prefix of the planes."""
-    if uses_tc(fmt):
-        # digit planes carry their own per-row/column power-of-two scales,
-        # so no extra level scaling is applied (exp is ignored)
-        K = A.cols if side == 0 else A.rows
-        db = digit_bits_for(h, K)
-        return Operand(A, h.slice(A, side, nslices or h.slices_for(fmt, db), sel, db), fmt, side)
-    if A.fmt != fmt or exp is not None:
-        B = MatBatch.empty(fmt, A.batch, A.rows, A.cols, device=A.device)
-        h.convert(A, B, sel, exp)
-        A = B
-    return Operand(A, None, fmt, side)
+    ``fmt``: its digit planes at the finest format any later use needs (the
+    caller passes it as ``fmt``); a coarser level uses a prefix of the
+    planes.  The planes carry their own per-row/column power-of-two scales,
+    so no extra level scaling applies (``exp`` is accepted and ignored).
+    ``wf``: the evaluation's working format, which fixes the digit width
+    (digit_bits_for); default ``fmt``."""
+    K = A.cols if side == 0 else A.rows
+    db = digit_bits_for(h, K, wf if wf is not None else fmt)
+    return Operand(A, h.slice(A, side, nslices or h.slices_for(fmt, db), sel, db), fmt, side)
 
 
 def gemm(h, L: Operand, R: Operand, C: MatBatch, sel=None) -> None:
-    """C = L R at C's format."""
-    if L.slices is not None and R.slices is not None:
-        h.gemm_sliced(L.slices, R.slices, h.slices_for(C.fmt, L.slices.db), C, sel)
-    else:
-        h.gemm(L.mat, R.mat, C, sel)
+    """C = L R at C's format on the tensor cores."""
+    h.gemm_sliced(L.slices, R.slices, h.slices_for(C.fmt, L.slices.db), C, sel)
 
 
 def horner(h, Y: Operand, phi: Operand, fmt_level: int, Bprev, out, sel=None, exp_y=None, exp_in=None,
            exp_out=None, nslices=None) -> None:
-    """out = RN_out(2^eo (Bprev + 2^-(ey+ei) RN_level(Y phi)))."""
-    if Y.slices is not None and phi.slices is not None:
-        # the Y planes are unscaled (exp_y does not apply); phi keeps its
-        # level scaling 2^exp_in, undone in the epilogue
-        h.horner_step_sliced(Y.slices, phi.slices, nslices or h.slices_for(fmt_level, Y.slices.db), Bprev, out, sel,
-                             None, exp_in, exp_out, fmt_in=fmt_level)
-    else:
-        h.horner_step(Y.mat, phi.mat, Bprev, out, sel, exp_y, exp_in, exp_out)
+    """out = RN_out(2^eo (Bprev + 2^-ei RN_level(Y phi))): the Y planes are
+    unscaled (exp_y does not apply); phi keeps its level scaling 2^exp_in,
+    undone in the epilogue."""
+    h.horner_step_sliced(Y.slices, phi.slices, nslices or h.slices_for(fmt_level, Y.slices.db), Bprev, out, sel,
+                         None, exp_in, exp_out, fmt_in=fmt_level)

@@ -243,7 +243,9 @@ class DeviceOps:
     # prepared operands (tensor-core digit planes or SIMT matrices)
     def prepare(self, A, side, fmt, exp=0):
         from . import gemm_engine as ge
-        return ge.prepare(self.h, A, side, fmt, None, self._e(exp))
+        # the digit width follows the evaluation's working format (set by
+        # the drivers below), so every product's operands share it
+        return ge.prepare(self.h, A, side, fmt, None, self._e(exp), wf=getattr(self, "wf", None))
 
     def gemm_op(self, L, R, C):
         from . import gemm_engine as ge
@@ -304,6 +306,7 @@ def _working(ctx):
 def cos_argument_dist(Xblk: MatBatch, ctx: PrecisionCtx, grid: ProcessGrid, ops) -> MatBatch:
     """Z_IJ = X_I: X_:J at the working format (harness.py:100-101)."""
     wf = _working(ctx)
+    ops.wf = wf
     Xw = Xblk
     if Xblk.fmt != wf:
         Xw = ops.empty(wf, Xblk.rows, Xblk.cols)
@@ -330,6 +333,7 @@ def ps_mixed_dist(Xblk: MatBatch, series: CoefficientSeries, ctx: PrecisionCtx, 
         raise ValueError("series degree must be >= 1")
     d = ctx.decimal_digits
     wf = _working(ctx)
+    ops.wf = wf
     s = default_block_size(m)
     r = m // s
     n = Xblk.rows * grid.pr
@@ -385,7 +389,7 @@ def ps_mixed_dist(Xblk: MatBatch, series: CoefficientSeries, ctx: PrecisionCtx, 
     Yrow_w = ypanels[0] if len(ypanels) == 1 else MatBatch(torch.cat([p.data for p in ypanels], dim=2), wf)
     from . import gemm_engine as ge
     yrow = {}
-    tc_fmts = [f for f in set(fm[1:]) if ge.uses_tc(f) and not getattr(ops, "simt_only", False)]
+    tc_fmts = [f for f in set(fm[1:]) if not getattr(ops, "host_double", False)]
     if tc_fmts:
         ytc = ops.prepare(Yrow_w, 0, max(tc_fmts))
         for f in tc_fmts:

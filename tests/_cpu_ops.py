@@ -19,7 +19,7 @@ class _Op:
 
 class CpuOps:
     device = torch.device("cpu")
-    simt_only = True
+    host_double = True     # no digit planes: one prepared Y per level format
 
     def prepare(self, A, side, fmt, exp=0):
         if A.fmt == fmt and not exp:

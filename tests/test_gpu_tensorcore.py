@@ -54,7 +54,10 @@ def test_tc_gemm_vs_oracle(cuda, oracle_lib, fmt, bits, shape, db):
         assert abs(g - o) <= 4 * K * u * Fraction(float(absAB[i, j])), (i, j, float(g - o), float(absAB[i, j]))
 
 
-def test_tc_gemm_batched_matches_simt(cuda):
+def test_abi_gemm_and_horner_step_on_plain_matrices(cuda):
+    """mpps_gemm / mpps_horner_step (the C-ABI operator entry points on plain
+    matrices: the library splits into stream-ordered scratch itself) equal
+    the explicit split + sliced-kernel path bit for bit, with a selection."""
     import torch
     from paper_2312_17396_b200 import _lib
     from paper_2312_17396_b200.precision import MatBatch
@@ -63,13 +66,25 @@ def test_tc_gemm_batched_matches_simt(cuda):
     X = MatBatch.empty(31, B, n, device=cuda)
     X.data[0].normal_()
     X.data[1] = X.data[0] * 2.0 ** -55
-    C1 = MatBatch.empty(31, B, n, device=cuda)
-    C2 = MatBatch.empty(31, B, n, device=cuda)
-    h.gemm(X, X, C1)
-    h.gemm_sliced(h.slice(X, 0, 16), h.slice(X, 1, 16), 16, C2)
-    d = (C1.data[0] - C2.data[0]) + (C1.data[1] - C2.data[1])
-    scale = X.data[0].abs() @ X.data[0].abs()
-    assert (d.abs() <= 8 * n * 2.0 ** -106 * scale).all()
+    C1 = MatBatch.zeros(31, B, n, device=cuda)
+    C2 = MatBatch.zeros(31, B, n, device=cuda)
+    sel = torch.tensor([5, 1, 2], dtype=torch.int32, device=cuda)
+    h.gemm(X, X, C1, sel)
+    S = h.slices_for(31, 8)
+    h.gemm_sliced(h.slice(X, 0, S, sel, 8), h.slice(X, 1, S, sel, 8), S, C2, sel)
+    assert torch.equal(C1.data, C2.data)
+    assert C1.data[:, 0].abs().sum() == 0 and C1.data[:, 5].abs().sum() > 0
+    P = MatBatch.empty(15, B, n, device=cuda)
+    P.data.normal_()
+    Bp = MatBatch.empty(31, B, n, device=cuda)
+    Bp.data.normal_()
+    O1 = MatBatch.zeros(15, B, n, device=cuda)
+    O2 = MatBatch.zeros(15, B, n, device=cuda)
+    Xf = MatBatch(X.data[:1].clone(), 15)
+    h.horner_step(Xf, P, Bp, O1)
+    S = h.slices_for(15, 8)
+    h.horner_step_sliced(h.slice(Xf, 0, S, None, 8), h.slice(P, 1, S, None, 8), S, Bp, O2, fmt_in=15)
+    assert torch.equal(O1.data, O2.data)
 
 
 def test_tc_digit_width_rules(cuda):
