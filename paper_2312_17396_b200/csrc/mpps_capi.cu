@@ -1461,6 +1461,28 @@ static int launch_oz_tma(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
 }
 
 static int oz_ring_ew();
+// smallest K that takes the NT = 128 few-plane Horner tiles (MPPS_OZ_NT128_K;
+// 0 disables them)
+static int oz_nt128_min_k() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MPPS_OZ_NT128_K");
+    v = e ? atoi(e) : 2048;
+    if (v <= 0) v = 1 << 30;
+  }
+  return v;
+}
+// few-plane Horner levels at large K (e.g. cfg5's fp32 levels, K = 8192):
+// 128-column tiles, the epilogue amortised over the long mainloop
+static bool oz_nt128_for(int S, int fo, int mode, int K, int db) {
+  return mode == 1 && db == 8 && S <= 4 && fo != QD && K >= oz_nt128_min_k();
+}
+static int dispatch_oz_tma128(mpps_handle *h, int S, int fo, const oz::OzTmaArgs &a, int nb) {
+#define OZW(SS, FF) if (S == SS && fo == FF) return launch_oz_tma<SS, 128, FF, 1, 8>(h, a, nb);
+  OZW(2, F32) OZW(2, F64) OZW(2, DD) OZW(3, F32) OZW(3, F64) OZW(3, DD) OZW(4, F32) OZW(4, F64) OZW(4, DD)
+#undef OZW
+  return set_err(h, MPPS_EFMT, "tensor-core GEMM (NT=128): no kernel for %d slices -> format %d", S, fo);
+}
 static int dispatch_oz_tma(mpps_handle *h, int S, int fo, int mode, const oz::OzTmaArgs &a, int nb) {
   // fp64 Horner levels (one CTA per SM): 16 epilogue warps like the dd ring
   if (oz_ring_ew() == 16 && S == 8 && mode == 1) {
@@ -1702,8 +1724,9 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   const bool pers = pmode != 0;
   // default: streamed-plane ring for dd / qd (S >= 16), 2-4 stage TMA ring below
   const bool ring = pers || oz_mode() == 2 || (oz_mode() == 3 && S >= 14) || S == 14 || S == 28;
-  const bool nt64 = !wide && !ring && oz_nt64_for(S, fo, mode);
-  const int NT = (S > 16 || pers) ? 16 : (nt64 ? 64 : 32);
+  const bool nt128 = !wide && !ring && oz_nt128_for(S, fo, mode, a.K, slice_db(A));
+  const bool nt64 = !wide && !ring && !nt128 && oz_nt64_for(S, fo, mode);
+  const int NT = (S > 16 || pers) ? 16 : (nt128 ? 128 : nt64 ? 64 : 32);
   const int abox = ring ? (S < 4 ? S : (S == 14 ? 7 : 4)) : S;   // OzRing<S, NT>::SG
   int rc;
   if (wide || pmode == 3) {
@@ -1719,6 +1742,7 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   if (pmode == 3) return launch_oz_pwide<16, 16, DD, 0>(h, t, nb);
   if (pmode == 1) return launch_oz_pers<16, 16, DD, 0, 1>(h, t, nb);
   if (pmode == 2) return launch_oz_pers<16, 16, DD, 0, 2>(h, t, nb);
+  if (nt128) return dispatch_oz_tma128(h, S, fo, t, nb);
   if (nt64) return dispatch_oz_tma64(h, S, fo, mode, t, nb);
   return ring ? dispatch_oz_ring(h, S, fo, mode, t, nb) : dispatch_oz_tma(h, S, fo, mode, t, nb);
 }

@@ -1386,9 +1386,18 @@ template <int S, int NT, int FO, int MODE>
 __host__ __device__ constexpr bool oz_staged() {
   return S <= 16 && FO != QD && (NT == 32 || (NT == 64 && S <= 8)) && MODE == 1;
 }
+// NT = 128 tiles for the few-plane Horner levels at large K (8-bit S <= 4:
+// fp32 levels, S * 128 <= 512 TMEM columns): 4x fewer A-plane re-reads and
+// N = 256 MMAs; the epilogue stages 32-column chunks of the tile in turn.
+template <int S, int NT, int FO, int MODE>
+__host__ __device__ constexpr bool oz_chunked() {
+  return NT == 128 && S <= 4 && FO != QD && MODE == 1;
+}
+constexpr int kEpiChunk = 32;
 template <int S, int NT, int FO, int MODE>
 __host__ __device__ constexpr uint32_t oz_ebuf_bytes() {
-  return oz_staged<S, NT, FO, MODE>() ? 2u * kTileM * NT * 8u : 0u;
+  return oz_chunked<S, NT, FO, MODE>() ? 2u * kTileM * kEpiChunk * 8u
+         : oz_staged<S, NT, FO, MODE>() ? 2u * kTileM * NT * 8u : 0u;
 }
 // Co-resident CTAs per SM: one CTA's epilogue overlaps the other's
 // mainloop.  Needs <= 256 TMEM columns (S <= 8) and shared memory for two.
@@ -1451,9 +1460,10 @@ __device__ __forceinline__ void oz_stage_load(const Args &args, double *ebuf, in
 // Phase 2 (all 8 warps, after the MMAs): thread = row; its columns are
 // combined from TMEM, the B_prev words read from (and the dd-width result
 // written back to) the staging tile.
-template <int S, int NT, int FO, int MODE, int DB, int CW = 8, typename Args>
+template <int S, int NT, int FO, int MODE, int DB, int CW = 8, int TS = NT, typename Args>
 __device__ __forceinline__ void oz_stage_compute(const Args &args, double *ebuf, const int *ebs, uint32_t tmem,
-                                                 int quarter, int c_begin, int c_end, int b, int m0, int lane) {
+                                                 int quarter, int c_begin, int c_end, int b, int m0, int lane,
+                                                 int toff = 0) {
   const int r = quarter * 32 + lane;
   const int row = m0 + r;
   const int ea = row < args.M ? args.A.exps[(long long)b * args.A.rpad + row] : 0;
@@ -1472,8 +1482,8 @@ __device__ __forceinline__ void oz_stage_compute(const Args &args, double *ebuf,
     int32_t D[S][CW];
 #pragma unroll
     for (int d = 0; d < S; ++d) {
-      if constexpr (CW == 8) tmem_ld8(lane_base + (uint32_t)(d * NT + c0), D[d]);
-      else tmem_ld4(lane_base + (uint32_t)(d * NT + c0), D[d]);
+      if constexpr (CW == 8) tmem_ld8(lane_base + (uint32_t)(d * TS + toff + c0), D[d]);
+      else tmem_ld4(lane_base + (uint32_t)(d * TS + toff + c0), D[d]);
     }
     tmem_ld_wait();
 #pragma unroll
@@ -1587,6 +1597,49 @@ __device__ __forceinline__ void oz_kernel_epilogue(const OzTmaArgs &args, double
   if (tr) tr[3] = globaltimer();
 }
 
+// Epilogue of the NT = 128 few-plane Horner tiles: the tile's columns are
+// staged, combined and stored in 32-column chunks through one 64 KB staging
+// tile (B_prev of chunk 0 is copied during the mainloop, the later chunks'
+// after it); TMEM diagonal d of column c sits at d * NT + c.
+template <int S, int NT, int FO, int MODE, int EW = 8>
+__device__ __forceinline__ void oz_kernel_epilogue_chunked(const OzTmaArgs &args, double *ebuf, int *ebs,
+                                                           uint32_t tmem, uint64_t *done, int warp, int lane, int b,
+                                                           int m0, int n0, unsigned long long *tr) {
+  static_assert(EW == 8, "chunked epilogue: 8 warps");
+  constexpr int C = kEpiChunk;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int cb = half ? EpiCols<S, C>::HALF : 0, ce = half ? C : EpiCols<S, C>::HALF;
+  if (warp >= 2) oz_stage_load<S, C, FO, MODE>(args, ebuf, ebs, b, m0, n0, warp - 2, EW - 2, lane);
+  __syncwarp();
+  mbar_wait(smem_u32(done), 0);
+  fence_after();
+  if (tr) tr[2] = globaltimer();
+#pragma unroll 1
+  for (int q = 0; q < NT / C; ++q) {
+    const int nq = n0 + q * C;
+    if (q > 0) {
+      if (nq >= args.N) break;
+      oz_stage_load<S, C, FO, MODE>(args, ebuf, ebs, b, m0, nq, warp, EW, lane);
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // staged B_prev / exponents visible to every warp
+    fence_after();
+    if (oz_db_of<S>(args.A.db) == 8) {
+      if constexpr (S != 16 && S != 31)
+        oz_stage_compute<S, C, FO, MODE, 8, 8, NT>(args, ebuf, ebs, tmem, quarter, cb, ce, b, m0, lane, q * C);
+    } else {
+      if constexpr (oz_has7<S>())
+        oz_stage_compute<S, C, FO, MODE, 7, 8, NT>(args, ebuf, ebs, tmem, quarter, cb, ce, b, m0, lane, q * C);
+    }
+    __syncthreads();
+    oz_stage_store<FO, C, EW>(args.C, ebuf, args.M, args.N, b, m0, nq, warp, lane);
+    __syncthreads();  // the staging tile is refilled by the next chunk
+  }
+  fence_before();
+  __syncthreads();
+  if (tr) tr[3] = globaltimer();
+}
+
 __device__ __forceinline__ unsigned long long *oz_trace_begin(const OzTmaArgs &args) {
   if (!args.trace || threadIdx.x != 64) return nullptr;
   unsigned long long *tr =
@@ -1673,7 +1726,10 @@ __global__ void __launch_bounds__(32 * EW, EW == 8 ? oz_ctas_per_sm<S, MODE, NT>
     }
     mma_commit(smem_u32(done));
   }
-  oz_kernel_epilogue<S, NT, FO, MODE, STAGED, EW>(args, ebuf, ebs, tmem, done, warp, lane, b, m0, n0, tr);
+  if constexpr (oz_chunked<S, NT, FO, MODE>())
+    oz_kernel_epilogue_chunked<S, NT, FO, MODE, EW>(args, ebuf, ebs, tmem, done, warp, lane, b, m0, n0, tr);
+  else
+    oz_kernel_epilogue<S, NT, FO, MODE, STAGED, EW>(args, ebuf, ebs, tmem, done, warp, lane, b, m0, n0, tr);
   if (warp == 0) tmem_dealloc<TCOLS>(tmem);
 }
 

@@ -150,3 +150,47 @@ def test_fixed_point_split_exact(cuda, side, fmt, S, n):
         V = sum(int(dig[s, i, k]) << (8 * (S - 1 - s)) for s in range(S))
         exact = v * Fraction(2) ** (F - int(ex[i]))
         assert abs(V - exact) <= 1, (side, i, k, float(V - exact))
+
+
+_NT128_SCRIPT = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2312_17396_b200 import _lib
+from paper_2312_17396_b200.precision import MatBatch
+h = _lib.handle_for()
+rng = np.random.default_rng(3)
+B, M, K, N = 3, 200, 2080, 300
+out = {}
+for S, fo in ((2, 7), (3, 15), (4, 31), (2, 31)):
+    Y = MatBatch(torch.from_numpy(rng.standard_normal((1, B, M, K))).cuda(), 15)
+    P = MatBatch(torch.from_numpy(rng.standard_normal((1, B, K, N))).cuda(), 15)
+    Bp = MatBatch(torch.from_numpy(rng.standard_normal((2, B, M, N)) * np.array([1, 2.0 ** -60])[:, None, None, None]).cuda(), 31)
+    o = MatBatch.zeros(fo, B, M, N, device="cuda")
+    sel = torch.tensor([2, 0], dtype=torch.int32, device="cuda")
+    ei = torch.tensor([3, -1, 2], dtype=torch.int32, device="cuda")
+    eo = torch.tensor([-2, 0, 1], dtype=torch.int32, device="cuda")
+    h.horner_step_sliced(h.slice(Y, 0, S, None, 8), h.slice(P, 1, S, None, 8), S, Bp, o, sel, None, ei, eo, fmt_in=fo)
+    out[f"{S}_{fo}"] = o.data.double().cpu().numpy()
+np.savez(sys.argv[2], **out)
+'''
+
+
+def test_nt128_few_plane_horner_matches_nt32(cuda, tmp_path):
+    """The 128-column few-plane Horner tiles (K >= 2048, S <= 4, chunked
+    staged epilogue) give the same bits as the 32-column tiles
+    (MPPS_OZ_NT128_K=0), with ragged M / N / K, a selection and level
+    exponents; run in two processes (the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "nt.py"
+    script.write_text(_NT128_SCRIPT)
+    res = {}
+    for tag, env in (("wide", {}), ("narrow", {"MPPS_OZ_NT128_K": "0"})):
+        f = tmp_path / f"{tag}.npz"
+        subprocess.check_call([sys.executable, str(script), root, str(f)], env=dict(os.environ, **env))
+        res[tag] = dict(np.load(f))
+    for k in res["wide"]:
+        assert np.array_equal(res["wide"][k], res["narrow"][k]), k
+        assert np.abs(res["wide"][k][:, 1]).sum() == 0 and np.abs(res["wide"][k][:, 0]).sum() > 0
