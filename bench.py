@@ -567,7 +567,7 @@ def run_ours(name, args, rank, world, local_rank, dist):
     clk = clocks.stop() if clocks else None
     spec1 = _graphs.speculation_stats()
     eager_launches = _lib.total_launches() - l0
-    if _graphs.enabled() and _graphs.last_launches() and wl.kind == "exp":
+    if eager_launches == 0 and _graphs.enabled() and _graphs.last_launches() and wl.kind == "exp":
         per_step = float(_graphs.last_launches())      # kernels per graphed evaluation (captured count)
         launches = per_step * args.steps
     else:

@@ -238,6 +238,24 @@ int mpps_oz_max_k_8bit(void);
  * exact (dd: 10070 with 8-bit digits, 31770 with 7-bit; qd: 4851 / 16443). */
 int mpps_oz_max_k(int fmt, int digit_bits);
 
+/* K5: the whole mixed PS evaluation of small matrices (n <= 32, fp64
+ * working format) in two launches around the host planner, one
+ * CTA per matrix, operands in shared memory.
+ *   mpps_small_ps_prepare: powers X^2..X^s, blocks B_0..B_r and the planner
+ *     norms (eval_b0_and_power + assemble_block + one_norm, engine.py:127-154,
+ *     467-468).  coeff: m+1 fp64 RN_p(b_k); blocks: device (r+1, B, n, n)
+ *     fp64 (block r not written when m mod s == 0: B_r = b_m I); Y: device
+ *     (B, n, n); norms: device (B, r+2) = ||B_0..B_r||, ||Y||.
+ *   mpps_small_ps_horner: horner_mixed (engine.py:243-252) with per-matrix
+ *     level formats level_fmt: HOST (B, r+1) int8, 0 = fp32, 1 = fp64 (copied
+ *     into the launch; the call returns once it is enqueued);
+ *     out: contiguous fp64 (B, n, n).  bm = RN_p(b_m). */
+int mpps_small_ps_supported(int n, int m, int fmt);
+int mpps_small_ps_prepare(mpps_handle *h, const mpps_mat *X, int m, int s, const double *coeff,
+                          double *blocks, double *Y, double *norms);
+int mpps_small_ps_horner(mpps_handle *h, const double *Y, const double *blocks, const signed char *level_fmt,
+                         int m, int s, double bm, mpps_mat *out);
+
 /* Diagnostic: pipe-peak probe used by bench.py for the per-precision
  * roofline denominators (not a reference operator).  Launches `blocks`
  * CTAs x 256 threads, each running 8 independent FMA chains of `iters`

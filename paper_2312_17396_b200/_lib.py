@@ -31,6 +31,7 @@ EXPORTED = (
     "mpps_assemble_blocks_dist", "mpps_colmax", "mpps_slice", "mpps_gemm_sliced",
     "mpps_horner_step_sliced", "mpps_oz_slices_for", "mpps_oz_slices_for_bits", "mpps_oz_max_k_8bit", "mpps_oz_max_k", "mpps_probe_i8mma", "mpps_debug_oz_trace",
     "mpps_debug_oz_flags", "mpps_debug_probe_i8mma_n", "mpps_probe_ingest",
+    "mpps_small_ps_supported", "mpps_small_ps_prepare", "mpps_small_ps_horner",
 )
 
 
@@ -147,6 +148,9 @@ def load_library(path: Optional[str] = None):
         lib.mpps_debug_oz_flags.restype = None
         lib.mpps_debug_probe_i8mma_n.argtypes = [vp, ip, ip, ip, vp]
         lib.mpps_probe_ingest.argtypes = [vp, ip, ip, vp, ctypes.c_longlong]
+        lib.mpps_small_ps_supported.argtypes = [ip, ip, ip]
+        lib.mpps_small_ps_prepare.argtypes = [vp, mp, ip, ip, P(ctypes.c_double), vp, vp, vp]
+        lib.mpps_small_ps_horner.argtypes = [vp, vp, vp, vp, ip, ip, ctypes.c_double, mp]
         for name in EXPORTED:
             getattr(lib, name).restype = getattr(lib, name).restype or ip
         if path is None:
@@ -378,6 +382,26 @@ class Handle:
                     "horner_scalar_top")
 
 
+    # --- K5: small matrices ------------------------------------------
+    def small_ps_supported(self, n: int, m: int, fmt: int) -> bool:
+        return bool(self.lib.mpps_small_ps_supported(int(n), int(m), int(fmt)))
+
+    def small_ps_prepare(self, X: MatBatch, m: int, s: int, coeff, blocks, Y, norms):
+        """X fp64 (1, B, n, n); coeff (m+1,) float64 host; blocks / Y / norms
+        device float64 tensors (see include/mpps_b200.h)."""
+        c = np.ascontiguousarray(coeff, dtype=np.float64)
+        x = cmat(X)
+        self._check(self.lib.mpps_small_ps_prepare(self.h, ctypes.byref(x), int(m), int(s),
+                                                   c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                                   blocks.data_ptr(), Y.data_ptr(), norms.data_ptr()), "small_ps")
+
+    def small_ps_horner(self, Y, blocks, level_fmt: np.ndarray, m: int, s: int, bm: float, out: MatBatch):
+        """level_fmt: host (B, r+1) int8 numpy array (0 fp32, 1 fp64)."""
+        o = cmat(out)
+        f = np.ascontiguousarray(level_fmt, dtype=np.int8)
+        self._check(self.lib.mpps_small_ps_horner(self.h, Y.data_ptr(), blocks.data_ptr(), f.ctypes.data,
+                                                  int(m), int(s), float(bm), ctypes.byref(o)), "small_ps")
+
     def probe_ingest(self, blocks: int, iters: int, src):
         self._check(self.lib.mpps_probe_ingest(self.h, blocks, iters, src.data_ptr(), src.numel() * src.element_size()),
                     "probe_ingest")
@@ -390,13 +414,17 @@ class Handle:
 
 
 _handles = {}
+_cuda_ok = False
 
 
 def handle_for(device=None) -> Handle:
     """The handle bound to torch's current stream on ``device``."""
     import torch
-    if not torch.cuda.is_available():
-        raise MppsCudaError("no CUDA device: the B200 path has no CPU fallback")
+    global _cuda_ok
+    if not _cuda_ok:
+        if not torch.cuda.is_available():
+            raise MppsCudaError("no CUDA device: the B200 path has no CPU fallback")
+        _cuda_ok = True
     dev = torch.cuda.current_device() if device is None else (
         device.index if hasattr(device, "index") and device.index is not None else int(device)
         if not hasattr(device, "type") else torch.cuda.current_device())

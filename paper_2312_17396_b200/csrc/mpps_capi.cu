@@ -18,6 +18,7 @@
 #include "../../include/mpps_b200.h"
 #include "formats.cuh"
 #include "ozaki.cuh"
+#include "small_ps.cuh"
 
 // Launch with programmatic stream serialization (PDL) when MPPS_PDL=1: the
 // kernel's CTA placement overlaps the predecessor's tail; every kernel
@@ -1204,6 +1205,79 @@ int mpps_horner_scalar_top(mpps_handle *h, const double *bm, int fmt_top, const 
   ST(QD, QD) { return set_err(h, MPPS_EFMT, "scalar_top: formats"); }
 #undef ST
   return after_launch(h, "scalar_top_kernel");
+}
+
+// ---------------------------------------------------- K5: small matrices
+int mpps_small_ps_supported(int n, int m, int fmt) {
+  if (fmt != MPPS_FP64 || n < 1 || n > mpps::small::kMaxN || m < 2) return 0;
+  int s = 1;
+  while (s * s < m) ++s;                       // ceil(sqrt(m)) (planner.default_block_size)
+  if (s >= m || s > mpps::small::kMaxS || m / s + 1 > mpps::small::kMaxBlocks || m + 1 > mpps::small::kMaxCoef)
+    return 0;
+  return 1;
+}
+
+static size_t small_prep_smem(int n, int s, int r) { return sizeof(double) * (size_t)n * n * (s + r + 1); }
+
+int mpps_small_ps_prepare(mpps_handle *h, const mpps_mat *X, int m, int s, const double *coeff, double *blocks,
+                          double *Y, double *norms) {
+  int rc = check_mat(h, X, "small_ps.X");
+  if (rc) return rc;
+  if (!coeff || !blocks || !Y || !norms) return set_err(h, MPPS_EINVAL, "small_ps: null argument");
+  if (X->rows != X->cols) return set_err(h, MPPS_EINVAL, "small_ps: X must be square");
+  if (X->fmt != MPPS_FP64) return set_err(h, MPPS_EFMT, "small_ps: X must be fp64");
+  if (!mpps_small_ps_supported(X->rows, m, MPPS_FP64)) return set_err(h, MPPS_EINVAL, "small_ps: unsupported n=%d m=%d", X->rows, m);
+  int sd = 1;
+  while (sd * sd < m) ++sd;
+  if (s != sd) return set_err(h, MPPS_EINVAL, "small_ps: s must be ceil(sqrt(m)) = %d", sd);
+  mpps::small::PrepArgs a;
+  memset(&a, 0, sizeof(a));
+  a.X = (const double *)X->data; a.xbs = X->batch_stride; a.ldx = X->ld;
+  a.n = X->rows; a.m = m; a.s = s; a.r = m / s; a.top_scalar = (m % s) == 0;
+  for (int k = 0; k <= m; ++k) a.coef[k] = coeff[k];
+  a.blocks = blocks; a.Y = Y; a.norms = norms; a.batch = X->batch;
+  if (X->batch == 0) return MPPS_OK;
+  const size_t smem = small_prep_smem(a.n, s, a.r);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(mpps::small::small_prepare_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)small_prep_smem(mpps::small::kMaxN, mpps::small::kMaxS, mpps::small::kMaxBlocks - 1));
+    if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "small_ps attr: %s", cudaGetErrorString(e));
+    configured = true;
+  }
+  launch_k(mpps::small::small_prepare_kernel, dim3(X->batch), dim3(mpps::small::kThreads), smem, h->stream, a);
+  return after_launch(h, "small_prepare_kernel");
+}
+
+int mpps_small_ps_horner(mpps_handle *h, const double *Y, const double *blocks, const signed char *level_fmt,
+                         int m, int s, double bm, mpps_mat *out) {
+  int rc = check_mat(h, out, "small_ps.out");
+  if (rc) return rc;
+  if (!Y || !blocks || !level_fmt) return set_err(h, MPPS_EINVAL, "small_ps: null argument");
+  if (out->fmt != MPPS_FP64) return set_err(h, MPPS_EFMT, "small_ps: the result is at the fp64 working format");
+  const int n = out->rows;
+  if (out->cols != n || out->ld != n || out->batch_stride != (long long)n * n)
+    return set_err(h, MPPS_EINVAL, "small_ps: contiguous square output expected");
+  if (!mpps_small_ps_supported(n, m, MPPS_FP64)) return set_err(h, MPPS_EINVAL, "small_ps: unsupported n=%d m=%d", n, m);
+  static thread_local mpps::small::HornerArgs a;      // ~4 KB: kept off the stack
+  a.Y = Y; a.blocks = blocks; a.fmt = nullptr; a.out = (double *)out->data; a.bm = bm;
+  a.n = n; a.r = m / s; a.top_scalar = (m % s) == 0; a.batch = out->batch;
+  if (out->batch == 0) return MPPS_OK;
+  const size_t nf = (size_t)out->batch * (a.r + 1);
+  signed char *dfmt = nullptr;
+  if (nf <= (size_t)mpps::small::kInlineFmt) {
+    memcpy(a.fmt_inline, level_fmt, nf);   // host formats ride in the kernel parameters
+  } else {
+    cudaError_t e = cudaMallocAsync((void **)&dfmt, nf, h->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dfmt, level_fmt, nf, cudaMemcpyHostToDevice, h->stream);
+    if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "small_ps formats: %s", cudaGetErrorString(e));
+    a.fmt = dfmt;
+  }
+  launch_k(mpps::small::small_horner_kernel, dim3(out->batch), dim3(mpps::small::kThreads),
+           sizeof(double) * 3 * (size_t)n * n, h->stream, a);
+  int rc2 = after_launch(h, "small_horner_kernel");
+  if (dfmt) cudaFreeAsync(dfmt, h->stream);
+  return rc2;
 }
 
 int mpps_probe_fma(mpps_handle *h, int fmt, int blocks, int iters, void *scratch) {

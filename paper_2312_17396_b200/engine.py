@@ -60,6 +60,8 @@ import os as _os
 _LOWP = _os.environ.get("MPPS_LOWP_ASSEMBLY", "1") != "0"
 #: two powers per power-chain GEMM (MPPS_PAIRED_POWERS=0: X^{k+1} = X^k X one by one)
 _PAIRED = _os.environ.get("MPPS_PAIRED_POWERS", "1") != "0"
+#: K5 fused small-matrix evaluation (n <= 32, fp64 working; MPPS_SMALL=0: general pipeline)
+_SMALL = _os.environ.get("MPPS_SMALL", "1") != "0"
 
 
 def _torch():
@@ -654,6 +656,92 @@ def _plan_fn(norms_row, r, ctx, delta, s, apply_switch, fix_params):
                                    fix_params=fix_params)
 
 
+# ------------------------------------------------- K5: small matrices
+_SMALL_OK: Dict[tuple, bool] = {}
+
+
+def _small_ok(X, series: CoefficientSeries, ctx: PrecisionCtx) -> bool:
+    """Whether the two-kernel small-matrix path (csrc/small_ps.cuh) runs
+    this evaluation: fp64 working format, real n <= 32, s < m, coefficients
+    well inside the fp64 range (the kernels keep fp32 levels as 24-bit
+    roundings in fp64, whose exponent range must hold every level)."""
+    if not _SMALL or complexmat.scope() is not None or _working_format(ctx) != FP64:
+        return False
+    shp = X.data.shape[2:] if isinstance(X, MatBatch) else getattr(X, "shape", None)
+    key = (series.token, ctx.binary_precision, tuple(shp) if shp is not None else None,
+           X.fmt if isinstance(X, MatBatch) else None)
+    ok = _SMALL_OK.get(key)
+    if ok is None:
+        ok = _SMALL_OK[key] = _small_ok_uncached(X, series, ctx)
+    return ok
+
+
+def _small_ok_uncached(X, series: CoefficientSeries, ctx: PrecisionCtx) -> bool:
+    if isinstance(X, MatBatch):
+        if X.fmt != FP64 or X.rows != X.cols:
+            return False
+        n = X.rows
+    else:
+        shp = getattr(X, "shape", None)
+        if shp is None or len(shp) not in (2, 3) or shp[-1] != shp[-2]:
+            return False
+        n = shp[-1]
+    m = series.degree
+    if not _lib.handle_for().small_ps_supported(n, m, FP64):
+        return False
+    c = np.abs(coeff_words(series, ctx)[:, 0])
+    nz = c[c != 0]
+    return bool(nz.size == 0 or (nz.min() > 2.0 ** -900 and nz.max() < 2.0 ** 900))
+
+
+def _small_eval(X, series: CoefficientSeries, ctx: PrecisionCtx, kind: str, delta: float, apply_switch: bool,
+                fix_params: bool, with_bound: bool, timing: bool):
+    """K5: powers, blocks and norms in one launch, the host
+    planner, the mixed Horner chain in a second launch (one CTA per matrix,
+    operands in shared memory) -- engine.py:141-154, 127-138, 157-215,
+    243-252.  kind: "mixed" or "fixed"."""
+    torch = _torch()
+    Xt, Xw, single = _input(X)
+    B, n = _check_square(Xt, Xw)
+    Xm = Xw if Xw is not None else MatBatch(Xt.unsqueeze(0), FP64)
+    h = _lib.handle_for()
+    m = series.degree
+    s = default_block_size(m)
+    r = m // s
+    d = ctx.decimal_digits
+    cw = np.ascontiguousarray(coeff_words(series, ctx)[:, 0])     # fp64 working: one word each
+    dev = Xm.device
+    timer = _Buckets(timing)
+    blocks = torch.empty((r + 1, B, n, n), dtype=torch.float64, device=dev)
+    Y = torch.empty((B, n, n), dtype=torch.float64, device=dev)
+    norms_d = torch.empty((B, r + 2), dtype=torch.float64, device=dev)
+    timer.start("power_formation")
+    h.small_ps_prepare(Xm, m, s, cw, blocks, Y, norms_d)
+    timer.stop()
+    timer.start("norm_estimation")
+    norms = norms_d.cpu().numpy()              # the one host sync
+    if kind == "fixed":
+        digits = np.full((B, r), d, dtype=np.int64)
+        nu = np.full(B, r + 1, dtype=np.int64)
+    else:
+        digits, nu, _ = plan_digits_batch(norms[:, :r + 1], norms[:, r + 1], d, delta, apply_switch)
+    timer.stop()
+    fm = np.ones((B, r + 1), dtype=np.int8)
+    for b, dg in enumerate(np.asarray(digits).tolist()):
+        fm[b, 1:] = [0 if f == FP32 else 1 for f in formats_of_digits(dg)]
+    result = MatBatch.empty(FP64, B, n, device=dev)
+    timer.start("mixed_horner")
+    h.small_ps_horner(Y, blocks, fm, m, s, float(cw[m]), result)
+    timer.stop()
+    if kind == "fixed":
+        fns = [(lambda nb=tuple(float(x) for x in norms[b, :r + 1]), ny=float(norms[b, r + 1]):
+                fixed_plan(nb, ny, ctx, s)) for b in range(B)]
+        return _reports(result, fns, None, "fixed", timer.seconds(), with_bound, single)
+    fns = [_plan_fn(norms[b], r, ctx, delta, s, apply_switch, fix_params) for b in range(B)]
+    executed = [(tuple(int(x) for x in digits[b]), int(nu[b])) for b in range(B)]
+    return _reports(result, fns, executed, "mixed", timer.seconds(), with_bound, single)
+
+
 # ------------------------------------------------------------ evaluators
 def _graph_stages(Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: int, kind: str, delta: float,
                   apply_switch: bool):
@@ -755,7 +843,7 @@ def _submit(X, series, ctx, delta, fix_params, with_bound, timing, slot, eager, 
     B, n = _check_square(Xt, Xw)
     if series.degree < 1:
         raise ValueError("series degree must be >= 1")
-    if Xt is None or not graphs.enabled():
+    if Xt is None or not graphs.enabled() or _small_ok(Xt, series, ctx):
         rep = eager()
         return PendingEvaluation(lambda: rep)
     timer = _Buckets(timing)
@@ -798,6 +886,8 @@ def ps_fixed(X, series: CoefficientSeries, ctx: PrecisionCtx, with_bound: bool =
                               tau_seq=(), norm_bs=(MPF(rn(c0, 54), 54),), norm_y=MPF(0, 64))
         return _reports(res, [lambda: plan] * B, None, "fixed", {}, False, single)
     s = default_block_size(m)
+    if _small_ok(X, series, ctx):
+        return _small_eval(X, series, ctx, "fixed", 10.0, True, True, with_bound, timing)
     g = _graphed(Xt, series, ctx, wf, s, "fixed", 10.0, True, timer) if Xw is None else None
     if g is not None:
         prep, digits, _, _, result = g
@@ -824,6 +914,8 @@ def ps_mixed_general(X, series: CoefficientSeries, ctx: PrecisionCtx, delta: flo
     m = series.degree
     if m < 1:
         raise ValueError("series degree must be >= 1")
+    if _small_ok(X, series, ctx):
+        return _small_eval(X, series, ctx, "mixed", delta, True, True, with_bound, timing)
     h = _lib.handle_for()
     timer = _Buckets(timing)
     wf = _working_format(ctx)
@@ -881,6 +973,8 @@ def ps_mixed_exp(X, m: int, ctx: PrecisionCtx, fix_params: bool = True, delta: f
             return BatchReport(reps, res, {})
     if s == m:
         return _explicit_powers(Xt, Xw, m, ctx, s, series, delta, True, fix_params, single, timing)
+    if _small_ok(X, series, ctx):
+        return _small_eval(X, series, ctx, "mixed", delta, True, fix_params, with_bound, timing)
     h = _lib.handle_for()
     timer = _Buckets(timing)
     wf = _working_format(ctx)
@@ -989,6 +1083,9 @@ def ps_mixed_pade(X, k: int, ctx: PrecisionCtx, delta: float = 10.0, with_bound:
     if k < 1:
         raise ValueError("series degree must be >= 1")
     num, den = pade_exp_coeffs(k, k)
+    if _small_ok(X, num, ctx):      # K5: two launches per polynomial, nothing to share
+        return (ps_mixed_general(X, num, ctx, delta, with_bound, timing),
+                ps_mixed_general(X, den, ctx, delta, with_bound, timing))
     h = _lib.handle_for()
     timer = _Buckets(timing)
     wf = _working_format(ctx)

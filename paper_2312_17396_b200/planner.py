@@ -175,6 +175,8 @@ def plan_digits_batch(norm_bs, norm_y, d: int, delta: float = 10.0, apply_switch
     nb = np.asarray(norm_bs, dtype=np.float64)
     ny = np.asarray(norm_y, dtype=np.float64)
     B, r1 = nb.shape
+    if B <= 4:
+        return _plan_rows_small(nb, ny, d, delta, apply_switch)
     r = r1 - 1
     digits = np.ones((B, r), dtype=np.int64)
     nu = np.full(B, r + 1, dtype=np.int64)
@@ -207,6 +209,56 @@ def plan_digits_batch(norm_bs, norm_y, d: int, delta: float = 10.0, apply_switch
         digits[b] = p.level_digits
         nu[b] = p.nu
         nil[b] = p.nilpotent
+    return digits, nu, nil
+
+
+def _plan_rows_small(nb, ny, d: int, delta: float, apply_switch: bool):
+    """plan_digits_batch for a few rows in scalar Python (numpy's per-call
+    overhead dominates a one-matrix evaluation): the same certified float64
+    rule -- digits exact away from integers and the delta threshold, the
+    exact plan_precisions otherwise -- so the result is identical."""
+    import numpy as np
+    B, r1 = nb.shape
+    r = r1 - 1
+    lim = d - math.log10(delta)
+    digits = np.ones((B, r), dtype=np.int64)
+    nu = np.full(B, r + 1, dtype=np.int64)
+    nil = np.zeros(B, dtype=bool)
+    for b in range(B):
+        row = [float(x) for x in nb[b]]
+        y = float(ny[b])
+        if y == 0:
+            nil[b], nu[b] = True, 1
+            continue
+        risky = not (all(math.isfinite(x) for x in row) and math.isfinite(y))
+        dig, qual = [], []
+        if not risky:
+            lb0 = math.log10(row[0]) if row[0] > 0 else 0.0
+            ly = math.log10(y)
+            for i in range(1, r + 1):
+                if row[i] == 0 or row[0] == 0:
+                    dig.append(1)
+                    qual.append(True)
+                    continue
+                e = (d - lb0) + (math.log10(row[i]) + i * ly) + 1e-9
+                if abs(e - round(e)) < _CERT_MARGIN or abs(e - lim) < _CERT_MARGIN:
+                    risky = True
+                    break
+                dig.append(min(max(math.floor(e), 1), d))
+                qual.append(e <= lim)
+        if risky:
+            p = plan_precisions(nb[b], ny[b], PrecisionCtx(d), delta, s=1, apply_switch=apply_switch)
+            digits[b], nu[b], nil[b] = p.level_digits, p.nu, p.nilpotent
+            continue
+        first = next((i + 1 for i, q in enumerate(qual) if q), r + 1)
+        if apply_switch:
+            for i in range(first - 1):
+                dig[i] = d
+        for i in range(r - 2, -1, -1):
+            if dig[i + 1] > dig[i]:
+                dig[i] = dig[i + 1]
+        digits[b] = dig
+        nu[b] = first
     return digits, nu, nil
 
 

@@ -419,3 +419,42 @@ def test_windowed_host_stream_with_dd_reassembly(cuda):
             pipeline.evaluate_host(pipeline.mixed_exp(30, ctx), Xh, out, chunks=[2] * 8, streams=2, window=win)
             torch.cuda.synchronize()
             assert np.array_equal(out.numpy(), ref)
+
+
+def test_small_fused_path_vs_oracle_and_invariance(cuda, oracle_lib):
+    """K5 (n <= 32, fp64 working: two launches around the planner) against
+    the oracle for mixed exp, fixed PS and Pade 13 at ragged n, batch
+    members bitwise equal to solo runs, and the same schedule as the general
+    pipeline (MPPS_SMALL=0 in-process switch)."""
+    from paper_2312_17396_b200 import engine
+    m = mp()
+    ctx = m.PrecisionCtx(15)
+    for n, seed in ((32, 3), (17, 4), (5, 6)):
+        X = synth(n, 0.5, seed)
+        assert engine._small_ok(X, m.taylor_exp_coeffs(16), ctx)
+        rep = m.ps_mixed_exp(X, 16, ctx)
+        _check(rep, oracle_lib.ps_eval(X, m.taylor_exp_coeffs(16).coeffs, 15), n, 15)
+        s = m.taylor_exp_coeffs(20)
+        fx = m.ps_fixed(X, s, ctx)
+        ref = oracle_lib.ps_eval(X, s.coeffs, 15, mode="fixed")
+        diff, refn = ref.compare(words_of(fx))
+        assert diff <= tol(fx.plan.r, n, 15) * refn
+        X2 = synth(n, 2.0, seed)
+        num, den = m.ps_mixed_pade(X2, 13, ctx)
+        sn, sd = m.pade_exp_coeffs(13, 13)
+        _check(num, oracle_lib.ps_eval(X2, sn.coeffs, 15), n, 15)
+        _check(den, oracle_lib.ps_eval(X2, sd.coeffs, 15), n, 15)
+    Xb = np.stack([synth(24, t, 80 + b) for b, t in enumerate((0.5, 3.0, 0.01, 1.5))])
+    rep = m.ps_mixed_exp(Xb, 16, ctx)
+    for b in range(4):
+        one = m.ps_mixed_exp(Xb[b], 16, ctx)
+        assert np.array_equal(words_of(one), rep.result.data[:, b].cpu().numpy())
+    engine._SMALL = False
+    try:
+        gen = m.ps_mixed_exp(Xb, 16, ctx)
+    finally:
+        engine._SMALL = True
+    for b in range(4):
+        assert gen[b].plan.level_digits == rep[b].plan.level_digits
+        g, k = gen.result.data[0, b].cpu().numpy(), rep.result.data[0, b].cpu().numpy()
+        assert np.abs(g - k).sum(0).max() <= tol(4, 24, 15) * np.abs(g).sum(0).max()

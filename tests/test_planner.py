@@ -228,3 +228,32 @@ def test_execution_planner_vs_mpfr_oracle_1e5(oracle_lib):
                 assert tuple(dig[i]) == od and nu[i] == onu and bool(nil[i]) == onil, (nb[i], y[i], d)
             total += B
     assert total >= 100_000
+
+
+def test_small_batch_planner_rows_vs_mpfr_oracle(oracle_lib):
+    """plan_digits_batch's scalar path for batches of <= 4 rows (one-matrix
+    evaluations) against the C MPFR digit rule, boundary rows included."""
+    from paper_2312_17396_b200.planner import plan_digits_batch
+    rng = np.random.default_rng(12)
+    for r in (1, 4, 6):
+        for d in (15, 31, 63):
+            for _ in range(400):
+                B = int(rng.integers(1, 5))
+                y = 10 ** rng.uniform(-3, 2, B)
+                b0 = 10 ** rng.uniform(-2, 4, B)
+                nb = np.concatenate([b0[:, None], b0[:, None] * np.cumprod(10 ** rng.uniform(-12, 0.5, (B, r)), axis=1)],
+                                    axis=1)
+                if rng.random() < 0.2:
+                    k = int(rng.integers(1, d))
+                    nb[0, 1] = nb[0, 0] * 10.0 ** (k - d - 1e-9) / y[0]
+                if rng.random() < 0.05:
+                    y[0] = 0.0
+                if rng.random() < 0.05:
+                    nb[-1, -1] = 0.0
+                dig, nu, nil = plan_digits_batch(nb, y, d)
+                for i in range(B):
+                    n2 = np.zeros((r + 2, 2))
+                    n2[:r + 1, 0] = nb[i]
+                    n2[r + 1, 0] = y[i]
+                    od, onu, onil, _ = oracle_lib.plan_digits(n2, d)
+                    assert tuple(dig[i]) == od and nu[i] == onu and bool(nil[i]) == onil
