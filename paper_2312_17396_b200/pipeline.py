@@ -236,3 +236,65 @@ def _evaluate_host(submit, X_host, out_host, chunks, trace, streams, ahead, wind
     caller.wait_stream(down)
     caller.wait_stream(up)
     return reps
+
+
+def evaluate_stream(fn: Callable, X_host: List, out_host: List, results_of: Optional[Callable] = None,
+                    keep_reports: bool = True) -> List[object]:
+    """A stream of host-resident inputs through any one-shot evaluator
+    ``fn(x_dev) -> report`` (e.g. ``lambda x: ps_mixed_general(cos_argument(x,
+    ctx), series, ctx)`` for one large matrix per step), software-pipelined:
+
+      upload stream    H2D of input t+1 (two device input slots)
+      caller stream    fn(input t)
+      download stream  D2H of result t into ``out_host[t]`` (pinned), while
+                       input t+1 is evaluated
+
+    ``results_of(report) -> [device tensors]`` (default: ``report.result.data``)
+    names the tensors copied into the matching ``out_host[t]`` list entries.
+    Inputs are pinned host tensors of one shape; returns the reports
+    (``keep_reports=False``: none are kept, so each step's device result is
+    released as soon as its download is done -- a long stream then runs in
+    constant device memory)."""
+    torch = _torch()
+    caller = torch.cuda.current_stream()
+    st = _state(torch, caller.device)
+    up, down = st["up"], st["down"]
+    up.wait_stream(caller)
+    down.wait_stream(caller)
+    results_of = results_of or (lambda rep: [rep.result.data])
+    T = len(X_host)
+    shape = tuple(X_host[0].shape)
+    slots = st["bufs"].get(("stream", shape))
+    if slots is None:
+        slots = st["bufs"][("stream", shape)] = [torch.empty(shape, dtype=torch.float64, device=caller.device)
+                                                 for _ in range(2)]
+    ev_in = [torch.cuda.Event() for _ in range(T)]
+    consumed = [None] * T
+
+    def upload(t):
+        with torch.cuda.stream(up):
+            if t >= 2:
+                up.wait_event(consumed[t - 2])       # the slot's previous input was taken
+            slots[t % 2].copy_(X_host[t], non_blocking=True)
+            ev_in[t].record(up)
+
+    reps = []
+    upload(0)
+    for t in range(T):
+        if t + 1 < T:
+            upload(t + 1)
+        caller.wait_event(ev_in[t])
+        rep = fn(slots[t % 2])
+        consumed[t] = torch.cuda.Event()
+        consumed[t].record(caller)
+        with torch.cuda.stream(down):
+            down.wait_event(consumed[t])
+            for dst, src in zip(out_host[t], results_of(rep)):
+                dst.copy_(src, non_blocking=True)
+                src.record_stream(down)
+        if keep_reports:
+            reps.append(rep)
+        del rep
+    caller.wait_stream(down)
+    caller.wait_stream(up)
+    return reps

@@ -458,3 +458,25 @@ def test_small_fused_path_vs_oracle_and_invariance(cuda, oracle_lib):
         assert gen[b].plan.level_digits == rep[b].plan.level_digits
         g, k = gen.result.data[0, b].cpu().numpy(), rep.result.data[0, b].cpu().numpy()
         assert np.abs(g - k).sum(0).max() <= tol(4, 24, 15) * np.abs(g).sum(0).max()
+
+
+def test_evaluate_stream_matches_direct_calls(cuda):
+    """pipeline.evaluate_stream (H2D of step t+1 and D2H of step t-1
+    overlapping step t, two device input slots) returns each step's result
+    bit for bit as a direct call on the same input."""
+    import torch
+    from paper_2312_17396_b200 import pipeline
+    m = mp()
+    ctx = m.PrecisionCtx(31)
+    series = m.taylor_cos_coeffs(24)
+    Xs = [synth(300, 1.0, 90 + t, cos=True) for t in range(4)]
+
+    def fn(x):
+        return m.ps_mixed_general(m.cos_argument(x, ctx), series, ctx)
+    ref = [fn(X).result.data.cpu().numpy() for X in Xs]
+    Xh = [torch.from_numpy(X).pin_memory() for X in Xs]
+    outs = [[torch.empty((2, 1, 300, 300), dtype=torch.float64).pin_memory()] for _ in Xs]
+    pipeline.evaluate_stream(fn, Xh, outs)
+    torch.cuda.synchronize()
+    for o, r in zip(outs, ref):
+        assert np.array_equal(o[0].numpy(), r)
