@@ -412,7 +412,8 @@ class Workload:
             self.grid = summa.ProcessGrid(pr, pc)
         B = c["batch"]
         if self.kind in ("exp", "expm") and self.scaling == "strong" and world > 1:
-            lo, hi = rank * B // world, (rank + 1) * B // world
+            from paper_2312_17396_b200.sharding import shard_bounds
+            lo, hi = shard_bounds(B, world, rank)
             self.members = list(range(lo, hi))
         else:
             self.members = list(range(B))
@@ -427,7 +428,8 @@ class Workload:
         """Input of pool slot t on this rank: seeds never repeat across
         slots or ranks (slot 0 of rank 0 is the parity tests' seed set)."""
         c, n, B = self.cfg, self.n, self.cfg["batch"]
-        gid = t * max(self.world, 1) + (0 if self.scaling == "strong" else self.rank)
+        from paper_2312_17396_b200.sharding import batch_id
+        gid = batch_id(t, self.world, self.rank, self.scaling == "strong")
         if self.kind == "exp":
             X = np.stack([synth(n, c["norm"], gid * B + i) for i in self.members])
             return X[0] if c["batch"] == 1 else X
