@@ -783,7 +783,7 @@ def run_ours(name, args, rank, world, local_rank, dist):
                 os.sched_setaffinity(0, _NUMA_CPUS)
     print(json.dumps(line), flush=True)
     # release this config's pools before the next config
-    del wl, rep
+    wl = rep = None
     gc.unfreeze()
     gc.collect()
     torch.cuda.empty_cache()

@@ -973,12 +973,15 @@ int mpps_assemble_blocks_hc(mpps_handle *h, const mpps_mat *powers, int s, int m
     return set_err(h, MPPS_EINVAL, "assemble: square matrices expected (use mpps_assemble_blocks_dist)");
   const int r = m / s;
   const int skip_top = (flags & 1) && (m % s == 0);
-  const int wf = fmt_index(powers[s - 1].fmt);
+  const int pref = s > 1 ? 1 : 0;            // X^2: always at the working format
+  const int wf = fmt_index(powers[pref].fmt);
   for (int k = 0; k < s; ++k) {
     int rc = check_mat(h, &powers[k], "assemble.power");
     if (rc) return rc;
     const bool x64 = k == 0 && wf == DD && fmt_index(powers[0].fmt) == F64;   // fp64 X under a dd chain
-    if ((powers[k].fmt != powers[s - 1].fmt && !x64) || powers[k].rows != powers[0].rows ||
+    // Y = X^s at fp64 precision under a dd chain: only its norm is read (high word)
+    const bool y64 = k == s - 1 && k > 0 && wf == DD && fmt_index(powers[k].fmt) == F64;
+    if ((powers[k].fmt != powers[pref].fmt && !x64 && !y64) || powers[k].rows != powers[0].rows ||
         powers[k].cols != powers[0].cols || powers[k].batch != powers[0].batch)
       return set_err(h, MPPS_EINVAL, "assemble: powers must share format and shape");
   }
@@ -996,7 +999,7 @@ int mpps_assemble_blocks_hc(mpps_handle *h, const mpps_mat *powers, int s, int m
   AC(DD, 6, 5) AC(DD, 7, 6) AC(DD, 5, 4) AC(DD, 4, 3) AC(DD, 5, 3) AC(F64, 5, 3) AC(F64, 4, 3)
 #undef AC
   return set_err(h, MPPS_EFMT, "assemble_hc: no constant-coefficient kernel for r+1=%d, s=%d at format %d", r + 1, s,
-                 powers[s - 1].fmt);
+                 powers[pref].fmt);
 }
 
 int mpps_assemble_blocks_hc_n(mpps_handle *h, const mpps_mat *powers, int s, int m, const double *coeff_host,
@@ -1005,14 +1008,16 @@ int mpps_assemble_blocks_hc_n(mpps_handle *h, const mpps_mat *powers, int s, int
   if (s < 2 || s > kMaxPowers || m < s) return set_err(h, MPPS_EINVAL, "need 2 <= s <= series degree (s=%d m=%d)", s, m);
   const int r = m / s;
   if (nblocks < 1 || nblocks > r + 1) return set_err(h, MPPS_EINVAL, "assemble_n: 1 <= nblocks <= r+1 (%d)", nblocks);
-  const int pf = fmt_index(powers[s - 1].fmt), bf = fmt_index(blocks[0].fmt);
+  const int pf = fmt_index(powers[1].fmt), bf = fmt_index(blocks[0].fmt);   // X^2: the working format
   int nd = 0;                               // leading dd blocks, then fp64 ones
   while (nd < nblocks && fmt_index(blocks[nd].fmt) == DD) ++nd;
   for (int k = 0; k < s; ++k) {
     int rc = check_mat(h, &powers[k], "assemble_n.power");
     if (rc) return rc;
     const bool x64 = k == 0 && fmt_index(powers[0].fmt) == F64;   // fp64 X under a dd chain
-    if ((powers[k].fmt != powers[s - 1].fmt && !x64) || powers[k].rows != powers[0].rows ||
+    // Y = X^s at fp64 precision: only its norm is read (high word)
+    const bool y64 = k == s - 1 && fmt_index(powers[k].fmt) == F64;
+    if ((powers[k].fmt != powers[1].fmt && !x64 && !y64) || powers[k].rows != powers[0].rows ||
         powers[k].cols != powers[0].cols || powers[k].batch != powers[0].batch || powers[k].rows != powers[k].cols)
       return set_err(h, MPPS_EINVAL, "assemble_n: square powers of one format and shape");
   }

@@ -62,6 +62,9 @@ _LOWP = _os.environ.get("MPPS_LOWP_ASSEMBLY", "1") != "0"
 _PAIRED = _os.environ.get("MPPS_PAIRED_POWERS", "1") != "0"
 #: K5 fused small-matrix evaluation (n <= 32, fp64 working; MPPS_SMALL=0: general pipeline)
 _SMALL = _os.environ.get("MPPS_SMALL", "1") != "0"
+#: mixed evaluators with an odd s >= 5 form Y = X^s at fp64 precision and at dd only for the
+#: matrices whose plan keeps a Horner level at dd (MPPS_Y_LOW=0: Y always at dd)
+_Y_LOW = _os.environ.get("MPPS_Y_LOW", "1") != "0"
 
 
 def _torch():
@@ -280,10 +283,11 @@ class _Prepared:
     coeffs: np.ndarray         # (m+1, 4) words at the working precision
     norms_dev: object = None   # the same norms on the device (level scalings)
     lowp: bool = False         # blocks are fp64 (two-pass assembly): dd ones are made per plan in _horner
+    y_low: bool = False        # Y = X^s is at fp64 precision: groups with a dd level get a dd Y in _horner
 
 
 def _form_powers(h, Xt, wf: int, s: int, timer: _Buckets, x_is_working: Optional[MatBatch] = None,
-                 x_fp64_ok: bool = False):
+                 x_fp64_ok: bool = False, y_low: bool = False):
     """X, X^2..X^s at the working format (engine.py:141-154 power chain).
     ``x_fp64_ok``: an fp64 input X under a dd chain on the tensor cores
     stays fp64 (its digit split and the block assembly read it directly:
@@ -303,7 +307,7 @@ def _form_powers(h, Xt, wf: int, s: int, timer: _Buckets, x_is_working: Optional
     else:
         h.convert(MatBatch(Xt.unsqueeze(0), FP64), powers[0])
     if s > 1 and _PAIRED and ge.uses_tc(wf) and s >= 4:
-        powers = _paired_powers(h, powers[0], wf, s)
+        powers = _paired_powers(h, powers[0], wf, s, y_low)
     elif s > 1:
         Xr = ge.prepare(h, powers[0], 1, wf)          # X: right operand of every step
         for k in range(1, s):       # X^{k+1} = X^k X   (engine.py:151-153)
@@ -312,7 +316,14 @@ def _form_powers(h, Xt, wf: int, s: int, timer: _Buckets, x_is_working: Optional
     return powers
 
 
-def _paired_powers(h, X: MatBatch, wf: int, s: int) -> List[MatBatch]:
+def _y_low_ok(wf: int, s: int, lowp: bool) -> bool:
+    """Y = X^s at fp64 precision first (see _paired_powers): mixed evaluators
+    on the dd tensor-core chain whose last power is a single GEMM (odd s)."""
+    return (_Y_LOW and lowp and wf == DD and s >= 5 and s % 2 == 1 and _PAIRED
+            and complexmat.scope() is None)
+
+
+def _paired_powers(h, X: MatBatch, wf: int, s: int, y_low: bool = False) -> List[MatBatch]:
     """X, X^2..X^s with two powers per tensor-core GEMM: the right operand
     is the column split of [X | X^2] (one slice buffer, 2n columns), so
     [X^{k+1} | X^{k+2}] = X^k [X | X^2] is one product of N = 2n.  s = 6:
@@ -336,6 +347,15 @@ def _paired_powers(h, X: MatBatch, wf: int, s: int) -> List[MatBatch]:
             lo, hi = MatBatch(Q.data[..., :n], wf), MatBatch(Q.data[..., n:], wf)
             out += [lo, hi]
             A = hi
+        elif y_low:
+            # Y = X^s, the last (single) product, at fp64 precision: it enters
+            # only the Horner products, which use a level's digit planes of it,
+            # and ||Y||.  Plans that keep a level at dd get Y at dd in _horner
+            # (the same product as below, so their bits are unchanged).
+            S64 = h.slices_for(FP64, db)
+            C = MatBatch.empty(FP64, B, n, device=dev)
+            h.gemm_sliced(h.slice(A, 0, S64, None, db), SP, S64, C)
+            out.append(C)
         else:
             C = MatBatch.empty(wf, B, n, device=dev)
             h.gemm_sliced(h.slice(A, 0, S, None, db), SP, S, C)
@@ -433,8 +453,11 @@ def _prepare(h, Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: in
     # kernels (both the mixed and the all-dd ones read an fp64 X^1)
     x64 = (wf == DD and complexmat.scope() is None and h.assemble_hc_supported(wf, s, m)
            and (not lowp or _lowp_blocks(h, wf, s, m) > 0))
-    powers = _form_powers(h, Xt, wf, s, timer, x_is_working, x_fp64_ok=x64)
-    return _assemble(h, powers, series, ctx, wf, s, timer, sync, lowp)
+    y_low = _y_low_ok(wf, s, lowp)
+    powers = _form_powers(h, Xt, wf, s, timer, x_is_working, x_fp64_ok=x64, y_low=y_low)
+    prep = _assemble(h, powers, series, ctx, wf, s, timer, sync, lowp)
+    prep.y_low = y_low and powers[s - 1].fmt != wf
+    return prep
 
 
 def _dd_blocks(h, prep: _Prepared, structure) -> List[MatBatch]:
@@ -491,6 +514,21 @@ def _structure(prep: _Prepared, digits: np.ndarray, nil: np.ndarray):
     return tuple((key, tuple(mem)) for key, mem in groups.items()), tuple(nil_idx)
 
 
+_SEL_CACHE: Dict[tuple, object] = {}
+
+
+def _selection_of(members, dev):
+    """Device index tensor of a member list (cached: created outside graph
+    captures on first use, reused by the replays)."""
+    key = (tuple(members), str(dev))
+    t = _SEL_CACHE.get(key)
+    if t is None:
+        if len(_SEL_CACHE) > 256:
+            _SEL_CACHE.clear()
+        t = _SEL_CACHE[key] = to_device_async(list(members), _torch().int32, dev)
+    return t
+
+
 def _selections(structure, dev):
     """Device index tensors of a structure (created eagerly, outside any
     graph capture)."""
@@ -525,6 +563,15 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
         sels = _selections(structure, dev)
     group_list, nil_idx = structure
     groups = {fm: list(mem) for fm, mem in group_list}
+    Y_dd = None
+    if prep.y_low and any(DD in key[0][1:] for key, _ in group_list):
+        # groups with a dd level need Y at dd: the chain's last product again
+        # at the working planes (X^s = X^(s-1) X), for those members only
+        dd_mem = sorted(b for key, mem in group_list if DD in key[0][1:] for b in mem)
+        sel_dd = None if len(dd_mem) == B else _selection_of(dd_mem, dev)
+        Y_dd = MatBatch.empty(DD, B, n, device=dev)
+        ge.gemm(h, ge.prepare(h, prep.powers[s - 2], 0, wf, sel_dd, wf=wf),
+                ge.prepare(h, prep.powers[0], 1, wf, sel_dd, wf=wf), Y_dd, sel_dd)
     if nil_idx:
         # p = B_0 (engine.py:378-379, 473-474)
         ii = sels["nil"]
@@ -536,6 +583,7 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
         fm, st = key
         sel = sels[key]
         blocks = [dd_blocks[k] if fm[k] == DD else prep.blocks[k] for k in range(r + 1)]
+        Y = Y_dd if (Y_dd is not None and DD in fm[1:]) else prep.powers[s - 1]
         exps = exp_y = None
         if FP32 in fm:
             # exact power-of-two level scalings, computed on the device from

@@ -480,3 +480,38 @@ def test_evaluate_stream_matches_direct_calls(cuda):
     torch.cuda.synchronize()
     for o, r in zip(outs, ref):
         assert np.array_equal(o[0].numpy(), r)
+
+
+def test_y_low_precision_rule(cuda, oracle_lib):
+    """Odd s (m = 42, s = 7): Y = X^s is formed at fp64 precision and at dd
+    only for the matrices whose plan keeps a Horner level at dd.  Members
+    with a dd level get exactly the bits of the always-dd chain
+    (MPPS_Y_LOW=0); the others stay within the oracle tolerance; every
+    member equals its solo evaluation bit for bit (the choice depends on the
+    matrix's own plan only)."""
+    from paper_2312_17396_b200 import engine
+    m = mp()
+    n, d = 40, 31
+    ctx = m.PrecisionCtx(d)
+    norms = [2.5, 0.01, 2.0, 0.02]
+    X = np.stack([synth(n, t, 60 + b) for b, t in enumerate(norms)])
+    rep = m.ps_mixed_exp(X, 42, ctx)
+    fm = [r.diagnostics["level_formats"] for r in rep]
+    has_dd = [("dd" in f[1:]) for f in fm]
+    assert any(has_dd) and not all(has_dd), fm
+    engine._Y_LOW = False
+    try:
+        full = m.ps_mixed_exp(X, 42, ctx).result.data.cpu().numpy()
+    finally:
+        engine._Y_LOW = True
+    got = rep.result.data.cpu().numpy()
+    coeffs = m.taylor_exp_coeffs(42).coeffs
+    for b in range(len(norms)):
+        solo = m.ps_mixed_exp(X[b], 42, ctx)
+        assert np.array_equal(words_of(solo), got[:, b]), b
+        if has_dd[b]:
+            assert np.array_equal(got[:, b], full[:, b]), b
+        ref = oracle_lib.ps_eval(X[b], coeffs, d)
+        assert rep[b].plan.level_digits == ref.digits
+        diff, refn = ref.compare(got[:, b])
+        assert diff <= tol(rep[b].plan.r, n, d) * refn, (b, diff / refn)
