@@ -226,6 +226,22 @@ def measure_peaks(torch, h):
         torch.cuda.synchronize()
         best = max(best, sms * 2.0 * 128 * 256 * 32 * iters / (a.elapsed_time(b) * 1e-3))
     out["int8_tops"] = best / 1e12
+    # sustained: the same probe (pseudo-random operands) back to back for
+    # ~3 s -- the clock settles under the power cap, as in a long step; the
+    # rate of the last second
+    one = sms * 2.0 * 128 * 256 * 32 * iters
+    t_end = time.perf_counter() + 3.0
+    evs = []
+    while time.perf_counter() < t_end:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(8):
+            h.probe_i8mma(sms, iters, scratch)
+        b.record()
+        b.synchronize()
+        evs.append((time.perf_counter(), a.elapsed_time(b) * 1e-3))
+    tail = [sec for t, sec in evs if t >= evs[-1][0] - 1.0] or [evs[-1][1]]
+    out["int8_tops_sustained"] = 8 * one * len(tail) / sum(tail) / 1e12
     src = torch.zeros(48 << 20, dtype=torch.uint8, device="cuda")
     iters = 2048
     h.probe_ingest(sms, 64, src)
@@ -716,15 +732,23 @@ def run_ours(name, args, rank, world, local_rank, dist):
         pairs = S * (S + 1) / 2
         achieved = logical * pairs
         S7 = {7: 4, 15: 8, 31: 16, 63: 31}[fin]
+        # the sustained probe peak for a kernel timed inside a long run (the
+        # K steps last >= 1 s: the clock sits under the power cap, as in the
+        # sustained probe); the burst peak otherwise (B200_PROFILING rule)
+        long_run = total >= 1.0
+        pk = peaks["int8_tops_sustained"] if long_run else peaks["int8_tops"]
         roof = {"bound": "tensor", "pipe": "int8 (tcgen05.mma kind::i8)", "achieved": achieved,
-                "peak": peaks["int8_tops"], "unit": "TOPS (int8)", "frac": achieved / peaks["int8_tops"],
-                "frac_7bit_equivalent": logical * S7 * (S7 + 1) / 2 / peaks["int8_tops"],
+                "peak": pk, "peak_kind": "sustained (3 s back-to-back probe)" if long_run else "burst",
+                "unit": "TOPS (int8)", "frac": achieved / pk,
+                "frac_of_burst_peak": achieved / peaks["int8_tops"],
+                "frac_7bit_equivalent": logical * S7 * (S7 + 1) / 2 / pk,
                 "algorithmic_ops_per_launch": 2.0 * M * N * K * nb * pairs,
                 "mean_launch_s": sec / cnt,
                 "frac_note": "frac counts the S(S+1)/2 plane-pair products per output this launch executed; "
                              "frac_7bit_equivalent rates the same logical throughput in 7-bit plane pairs",
                 "logical_tflops": logical, "logical_frac_of_format_peak": logical / peaks[fname],
-                "peak_source": f"tcgen05 kind::i8 probe in bench.py on this GPU ({peaks['int8_tops']:.0f} TOPS; "
+                "peak_source": f"tcgen05 kind::i8 probe in bench.py on this GPU (burst {peaks['int8_tops']:.0f}, "
+                               f"sustained {peaks['int8_tops_sustained']:.0f} TOPS; "
                                "MEASURED_PEAKS.json has no INT8 figure); format peaks from DFMA/FFMA probes "
                                f"(fp64 {peaks['fp64']:.2f} TF/s, Peak_dd = Peak_fp64/15, SURVEY 8d)"}
         NT = 16 if S > 16 else 32

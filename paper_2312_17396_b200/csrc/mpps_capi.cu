@@ -1736,6 +1736,15 @@ static int oz_pers_mode(int S, int fo, int mode) {
   return (S == 16 && fo == DD && mode == 0) ? v : 0;
 }
 
+static int oz_wide_cluster() {   // MPPS_OZ_WIDE_MC=0: one CTA per tile, no A multicast
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MPPS_OZ_WIDE_MC");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
 template <int S, int NT, int FO, int MODE>
 static int launch_oz_wide(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
   constexpr size_t smem = oz::oz_wide_smem_bytes<S, NT, FO, MODE>();
@@ -1743,6 +1752,9 @@ static int launch_oz_wide(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_wide_kernel<S, NT, FO, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(oz::oz_gemm_wide_kernel<S, NT, FO, MODE, 2>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz wide attr: %s", cudaGetErrorString(e));
     configured = true;
   }
@@ -1752,6 +1764,24 @@ static int launch_oz_wide(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
   t.group = oz_group();
   dim3 grid(t.mtiles * t.ntiles, 1, nb);
   if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
+  if (oz_wide_cluster() && t.ntiles % 2 == 0) {
+    // CTA pairs on adjacent N tiles multicast the shared A planes
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(oz::kThreadsEpi);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = h->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, oz::oz_gemm_wide_kernel<S, NT, FO, MODE, 2>, t);
+    if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz wide cluster launch: %s", cudaGetErrorString(e));
+    return after_launch(h, "oz_gemm_wide_kernel");
+  }
   oz::oz_gemm_wide_kernel<S, NT, FO, MODE><<<grid, oz::kThreadsEpi, smem, h->stream>>>(t);
   return after_launch(h, "oz_gemm_wide_kernel");
 }

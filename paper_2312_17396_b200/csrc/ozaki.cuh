@@ -1869,6 +1869,29 @@ __global__ void __launch_bounds__(32 * EW, 1) oz_gemm_ring_kernel(const __grid_c
   if (warp == 0) tmem_dealloc<TCOLS>(tmem);
 }
 
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                               uint32_t mbar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(mbar), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint32_t mbar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(mbar),
+      "h"(mask)
+      : "memory");
+}
+
 // ------------------------------------------- 128-byte K boxes (wide feed)
 // The 32-byte K boxes of the kernels above move one 32-byte sector per
 // tile row per TMA request, and the feed saturates at ~45-60 GB/s per SM
@@ -1905,7 +1928,7 @@ __device__ __forceinline__ void oz_wide_plane(uint32_t tmem, uint64_t ad, uint64
   }
 }
 
-template <int S, int NT, int s = 0>
+template <int S, int NT, int CL = 1, int s = 0>
 __device__ __forceinline__ void oz_wide_stage(uint32_t tmem, uint32_t sb, int nk, uint32_t acc0, int &ai,
                                               uint8_t *aring, uint64_t *a_full, uint64_t *a_empty, int nas) {
   if constexpr (s < S) {
@@ -1918,9 +1941,12 @@ __device__ __forceinline__ void oz_wide_stage(uint32_t tmem, uint32_t sb, int nk
       if (kk < nk)
         oz_wide_plane<S, NT, s>(tmem, umma_desc(sa + kk * 32, 16, 1024, 2), umma_desc(sb + kk * 32, 16, 1024, 2),
                                 kk > 0 ? 1u : acc0);
-    mma_commit(smem_u32(&a_empty[ast]));
+    // the slot is refilled by a multicast into every CTA of the pair: it is
+    // free only when all of their MMAs have read it
+    if constexpr (CL == 1) mma_commit(smem_u32(&a_empty[ast]));
+    else mma_commit_mc(smem_u32(&a_empty[ast]), (uint16_t)((1u << CL) - 1u));
     ++ai;
-    oz_wide_stage<S, NT, s + 1>(tmem, sb, nk, acc0, ai, aring, a_full, a_empty, nas);
+    oz_wide_stage<S, NT, CL, s + 1>(tmem, sb, nk, acc0, ai, aring, a_full, a_empty, nas);
   }
 }
 
@@ -1931,7 +1957,11 @@ __host__ __device__ constexpr size_t oz_wide_smem_bytes() {
   return (size_t)W::NBS * W::B_STRIDE + (size_t)W::template nas<EBUF>() * W::A_BYTES + EBUF + 2048;
 }
 
-template <int S, int NT, int FO, int MODE>
+// CL = 2: a 2-CTA cluster takes two adjacent N tiles of one M tile; both
+// need the same A planes, so plane s is loaded by CTA s % 2 and multicast
+// into both CTAs' rings (L2 -> SM traffic of A, ~80 % of the feed at
+// NT = 32, halves); B stays per CTA.
+template <int S, int NT, int FO, int MODE, int CL = 1>
 __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_wide_kernel(const __grid_constant__ OzTmaArgs args) {
   using W = OzWide<S, NT>;
   constexpr int TCOLS = tmem_cols_for(S * NT);
@@ -1955,7 +1985,15 @@ __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_wide_kernel(const __gr
   const int bz = blockIdx.z;
   const int b = args.sel ? args.sel[bz] : bz;
   int m0, n0;
-  oz_tile_of(args, NT, m0, n0);
+  const int rank = CL > 1 ? (int)cluster_rank() : 0;
+  if constexpr (CL == 1) {
+    oz_tile_of(args, NT, m0, n0);
+  } else {
+    OzTmaArgs g = args;
+    g.ntiles = args.ntiles / CL;             // the launch guarantees ntiles % CL == 0
+    oz_tile_at(g, blockIdx.x / CL, NT * CL, m0, n0);
+    n0 += rank * NT;
+  }
   const int kpad = args.A.kpad;
   const int kstages = (kpad + W::KB - 1) / W::KB;
   unsigned long long *tr = oz_trace_begin(args);
@@ -1963,12 +2001,13 @@ __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_wide_kernel(const __gr
   if (warp == 0) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
   if (tid == 32) {
     for (int i = 0; i < W::NBS; ++i) { mbar_init(smem_u32(&b_full[i]), 1); mbar_init(smem_u32(&b_empty[i]), 1); }
-    for (int i = 0; i < NAS; ++i) { mbar_init(smem_u32(&a_full[i]), 1); mbar_init(smem_u32(&a_empty[i]), 1); }
+    for (int i = 0; i < NAS; ++i) { mbar_init(smem_u32(&a_full[i]), 1); mbar_init(smem_u32(&a_empty[i]), CL); }
     mbar_init(smem_u32(done), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   fence_before();
-  __syncthreads();
+  if constexpr (CL > 1) cluster_sync();   // the peer's barriers exist before any multicast
+  else __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
   const int rowA = b * args.A.rpad + m0, rowB = b * args.B.rpad + n0;
@@ -1986,7 +2025,11 @@ __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_wide_kernel(const __gr
         const int ast = ai % NAS;
         if (ai >= NAS) mbar_wait(smem_u32(&a_empty[ast]), ((ai / NAS) - 1) & 1);
         mbar_expect_tx(smem_u32(&a_full[ast]), W::A_BYTES);
-        tma_load_3d(smem_u32(aring + ast * W::A_BYTES), &args.mapA, kb * W::KB, rowA, s, smem_u32(&a_full[ast]));
+        if constexpr (CL == 1)
+          tma_load_3d(smem_u32(aring + ast * W::A_BYTES), &args.mapA, kb * W::KB, rowA, s, smem_u32(&a_full[ast]));
+        else if (s % CL == rank)
+          tma_load_3d_mc(smem_u32(aring + ast * W::A_BYTES), &args.mapA, kb * W::KB, rowA, s, smem_u32(&a_full[ast]),
+                         (uint16_t)((1u << CL) - 1u));
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -1998,13 +2041,20 @@ __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_wide_kernel(const __gr
       fence_after();
       const int left = (kpad - kb * W::KB) / kKStep;
       const int nk = left < 4 ? left : 4;
-      oz_wide_stage<S, NT>(tmem, smem_u32(bring + bst * W::B_STRIDE), nk, kb > 0 ? 1u : 0u, ai, aring, a_full,
-                           a_empty, NAS);
+      oz_wide_stage<S, NT, CL>(tmem, smem_u32(bring + bst * W::B_STRIDE), nk, kb > 0 ? 1u : 0u, ai, aring, a_full,
+                               a_empty, NAS);
       mma_commit(smem_u32(&b_empty[bst]));
     }
     mma_commit(smem_u32(done));
   }
   oz_kernel_epilogue<S, NT, FO, MODE, STAGED>(args, ebuf, ebs, tmem, done, warp, lane, b, m0, n0, tr);
+  if constexpr (CL > 1) {
+    // no CTA leaves while its peer may still multicast into its ring or
+    // arrive on its barriers
+    fence_before();
+    cluster_sync();
+    fence_after();
+  }
   if (warp == 0) tmem_dealloc<TCOLS>(tmem);
 }
 
@@ -2058,29 +2108,6 @@ __device__ __forceinline__ void oz_pers_tile(const OzTmaArgs &a, int t, int nt, 
   g.ntiles = npairs;
   oz_tile_at(g, t - bz * per, nt * CL, m0, n0);
   n0 += rank * nt;
-}
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2,
-                                               uint32_t mbar, uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(mbar), "h"(mask)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit_mc(uint32_t mbar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(mbar),
-      "h"(mask)
-      : "memory");
 }
 
 template <int S, int NT, uint32_t A_SLICE, uint32_t B_SLICE, int SG, int CL, int G = 0>
@@ -2226,7 +2253,13 @@ __global__ void __launch_bounds__(128, 1) i8_mma_probe_kernel(int iters, int *ou
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t *done = reinterpret_cast<uint64_t *>(smem + 40960);
   uint32_t *slot = reinterpret_cast<uint32_t *>(done + 1);
-  for (int i = threadIdx.x; i < 40960 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(smem)[i] = 0u;
+  // pseudo-random operand bytes (a zero operand draws little power, so a
+  // sustained run with it would never meet the power cap real data meets)
+  for (int i = threadIdx.x; i < 40960 / 4; i += blockDim.x) {
+    uint32_t x = (uint32_t)i * 2654435761u + blockIdx.x * 40503u;
+    x ^= x >> 15; x *= 2246822519u; x ^= x >> 13;
+    reinterpret_cast<uint32_t *>(smem)[i] = x;
+  }
   if (threadIdx.x < 32) tmem_alloc<256>(smem_u32(slot));
   if (threadIdx.x == 32) {
     mbar_init(smem_u32(done), 1);
