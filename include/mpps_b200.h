@@ -205,6 +205,15 @@ typedef struct {
  * planes (padding written as zero). */
 int mpps_slice(mpps_handle *h, const mpps_mat *src, int side, mpps_slices *out,
                const int *sel, int nsel);
+/* mpps_slice in two halves, for operands whose row / column scales span
+ * more than the caller's block (the SUMMA driver splits its own block and
+ * gathers digit planes): mode 1 writes only out->exps (each row's -- side 0
+ * -- or column's -- side 1 -- power-of-two scale); mode 2 splits with the
+ * scales already in out->exps (which may be larger than the block's own, e.g.
+ * the max over a process row), giving exactly the digits the split of the
+ * whole panel would give; mode 0 = mpps_slice. */
+int mpps_slice_ex(mpps_handle *h, const mpps_mat *src, int side, mpps_slices *out,
+                  const int *sel, int nsel, int mode);
 /* Column split of src into slice rows [row0, row0 + src->cols) of out: the
  * right operand [P_0 | P_1] of one GEMM over several matrices (the power
  * chain's [X | X^2]); other rows are untouched. */

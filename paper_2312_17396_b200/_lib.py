@@ -31,7 +31,7 @@ EXPORTED = (
     "mpps_assemble_blocks_dist", "mpps_colmax", "mpps_slice", "mpps_gemm_sliced",
     "mpps_horner_step_sliced", "mpps_oz_slices_for", "mpps_oz_slices_for_bits", "mpps_oz_max_k_8bit", "mpps_oz_max_k", "mpps_probe_i8mma", "mpps_debug_oz_trace",
     "mpps_debug_oz_flags", "mpps_debug_probe_i8mma_n", "mpps_probe_ingest",
-    "mpps_small_ps_supported", "mpps_small_ps_prepare", "mpps_small_ps_horner",
+    "mpps_small_ps_supported", "mpps_small_ps_prepare", "mpps_small_ps_horner", "mpps_slice_ex",
 )
 
 
@@ -135,6 +135,7 @@ def load_library(path: Optional[str] = None):
         sp = P(CSlices)
         lib.mpps_slice.argtypes = [vp, mp, ip, sp, vp, ip]
         lib.mpps_slice_into.argtypes = [vp, mp, sp, ip, vp, ip]
+        lib.mpps_slice_ex.argtypes = [vp, mp, ip, sp, vp, ip, ip]
         lib.mpps_gemm_sliced.argtypes = [vp, sp, sp, ip, ip, ip, ip, mp, vp, ip]
         lib.mpps_horner_step_sliced.argtypes = [vp, sp, sp, ip, mp, mp, vp, ip, vp, vp, vp]
         lib.mpps_oz_slices_for.argtypes = [ip]
@@ -314,6 +315,14 @@ class Handle:
         self._check(self.lib.mpps_slice(self.h, ctypes.byref(c_src), side, ctypes.byref(c_out), _ptr(sel), nsel),
                     "slice")
         return out
+
+    def slice_ex(self, src: MatBatch, side: int, out: "Slices", mode: int, sel=None):
+        """mode 1: only out.exps (row / column scales); mode 2: split with
+        the scales already in out.exps (include/mpps_b200.h)."""
+        c_src, c_out = cmat(src), out.c()
+        nsel = 0 if sel is None else sel.numel()
+        self._check(self.lib.mpps_slice_ex(self.h, ctypes.byref(c_src), side, ctypes.byref(c_out), _ptr(sel), nsel,
+                                           int(mode)), "slice_ex")
 
     def slice_into(self, src: MatBatch, out: "Slices", row0: int, sel=None):
         """Column split of src into slice rows [row0, row0 + src.cols) of out."""

@@ -1355,10 +1355,16 @@ static bool oz_cols_fused() {
 }
 
 static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices *out, const int *sel, int nsel,
-                      int row0, int nrows);
+                      int row0, int nrows, int mode = 0);
 
 extern "C" int mpps_slice(mpps_handle *h, const mpps_mat *src, int side, mpps_slices *out, const int *sel, int nsel) {
   return slice_impl(h, src, side, out, sel, nsel, 0, -1);
+}
+
+extern "C" int mpps_slice_ex(mpps_handle *h, const mpps_mat *src, int side, mpps_slices *out, const int *sel, int nsel,
+                             int mode) {
+  if (mode < 0 || mode > 2) return set_err(h, MPPS_EINVAL, "slice_ex: mode 0, 1 or 2");
+  return slice_impl(h, src, side, out, sel, nsel, 0, -1, mode);
 }
 
 /* Column split of src into slice rows [row0, row0 + src->cols) of out (the
@@ -1373,7 +1379,7 @@ extern "C" int mpps_slice_into(mpps_handle *h, const mpps_mat *src, mpps_slices 
 }
 
 static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices *out, const int *sel, int nsel,
-                      int row0, int nrows) {
+                      int row0, int nrows, int mode) {
   int rc = check_mat(h, src, "slice.src");
   if (rc) return rc;
   if (!out || !out->digits || !out->exps) return set_err(h, MPPS_EINVAL, "slice: null output");
@@ -1403,6 +1409,16 @@ static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices
     return set_err(h, MPPS_EINVAL, "slice: 2, 3, 4, 5, 6, 8, 10, 12, 14 or 28 digit planes of 8 bits");
   if (slice_db(out) == 7 && (S == 2 || S == 3 || S == 5 || S == 6 || S == 10 || S == 12))
     return set_err(h, MPPS_EINVAL, "slice: %d planes exist only with 8-bit digits", S);
+  if (mode == 1) {          // exponents only
+    if (side == 0)
+      launch_k(oz::row_exps_kernel, dim3((out->rpad * 32 + 255) / 256, nb), dim3(256), 0, h->stream, ref_of(src),
+               src->rows, src->cols, fi, o, sel);
+    else
+      launch_k(oz::col_exps_kernel, dim3(dim3(gx, nb)), dim3(256), 0, h->stream, ref_of(src), src->rows, src->cols, fi,
+               o, sel);
+    return after_launch(h, side == 0 ? "row_exps_kernel" : "col_exps_kernel");
+  }
+  o.given = mode == 2;
   if (side == 0) {
     dim3 grid((out->rpad * 32 + 255) / 256, nb);
 #define SR(WW, SS) \
@@ -1414,7 +1430,7 @@ static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices
 #undef SR
     return after_launch(h, "slice_rows_kernel");
   }
-  if (oz_cols_fused() && nrows < 0) {
+  if (oz_cols_fused() && nrows < 0 && mode == 0) {
     dim3 grid(out->rpad / 32, nb);
 #define SCF(WW, SS) \
   if (W == WW && S == SS) launch_k(oz::slice_cols_fused_kernel<WW, SS>, dim3(grid), dim3(256), 0, h->stream, ref_of(src), src->rows, src->cols, fi, o, sel); else
@@ -1425,7 +1441,7 @@ static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices
 #undef SCF
     return after_launch(h, "slice_cols_fused_kernel");
   }
-  if (slice_db(out) == 8 && W <= 2 && S <= 14 && out->kpad / 32 <= 8 && oz_cols_cluster()) {
+  if (slice_db(out) == 8 && W <= 2 && S <= 14 && out->kpad / 32 <= 8 && oz_cols_cluster() && mode == 0) {
     // one cluster of kpad/32 CTAs per 32-column strip: exponents and digits in one pass
     const unsigned ky = (unsigned)(out->kpad / 32);
     cudaLaunchConfig_t cfg = {};
@@ -1449,9 +1465,12 @@ static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices
 #undef SCC
     return after_launch(h, "slice_cols_cluster_kernel");
   }
-  launch_k(oz::col_exps_kernel, dim3(dim3(gx, nb)), dim3(256), 0, h->stream, ref_of(src), src->rows, src->cols, fi, o, sel);
-  rc = after_launch(h, "col_exps_kernel");
-  if (rc) return rc;
+  if (mode == 0) {
+    launch_k(oz::col_exps_kernel, dim3(dim3(gx, nb)), dim3(256), 0, h->stream, ref_of(src), src->rows, src->cols, fi, o,
+             sel);
+    rc = after_launch(h, "col_exps_kernel");
+    if (rc) return rc;
+  }
   if (slice_db(out) == 8 && W <= 2 && S <= 14 && oz_cols_fixed()) {
     dim3 gridf(gx, (out->kpad + 63) / 64, nb);
 #define SCX(WW, SS) \

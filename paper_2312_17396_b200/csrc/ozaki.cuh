@@ -144,6 +144,7 @@ struct SliceRef {
   int db;           // digit bits: 7 (digits in [-65, 65]) or 8 ([-128, 127]); first digit 6 bits
   int row0 = 0;     // column splits: first slice row written (mpps_slice_into)
   int nrows = 1 << 30;   // and the number of rows written (default: through rpad)
+  int given = 0;    // exps already hold the row / column exponents (mpps_slice_ex mode 2)
   __host__ __device__ long long plane() const { return (long long)batch * rpad * kpad; }
 };
 
@@ -506,23 +507,30 @@ __device__ __forceinline__ void slice_rows_body(const MatRef &A, int rows, int c
   if constexpr (DB == 8 && W <= 2 && S <= 14) {
     // warp-uniform: the whole row is interior and 16-byte aligned
     const bool f32 = fi == F32;
-    if (i < rows && (W == 1 || !f32) && cols == out.kpad && (cols == 128 || cols == 256) && (f32 || (A.plane & 1) == 0) &&
+    if (!out.given && i < rows && (W == 1 || !f32) && cols == out.kpad && (cols == 128 || cols == 256) && (f32 || (A.plane & 1) == 0) &&
         ((f32 ? reinterpret_cast<uintptr_t>((const float *)A.data + base)
               : reinterpret_cast<uintptr_t>((const double *)A.data + base)) & 15) == 0) {
       slice_rows_regs<W, S>(A, base, cols, fi, out, b, i, lane);
       return;
     }
   }
-  double mx = 0.0;
-  if (i < rows)
-    for (int k = lane; k < cols; k += 32) {
-      double v = fi == F32 ? (double)((const float *)A.data)[base + k] : ((const double *)A.data)[base + k];
-      mx = fmax(mx, fabs(v));
-    }
+  int e;
+  if (out.given) {
+    // the row exponent of the whole panel row (SUMMA: max over the process
+    // row), so this block's digits are exactly those of the gathered panel
+    e = out.exps[(long long)b * out.rpad + i];
+  } else {
+    double mx = 0.0;
+    if (i < rows)
+      for (int k = lane; k < cols; k += 32) {
+        double v = fi == F32 ? (double)((const float *)A.data)[base + k] : ((const double *)A.data)[base + k];
+        mx = fmax(mx, fabs(v));
+      }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  const int e = row_exponent(mx);
-  if (lane == 0) out.exps[(long long)b * out.rpad + i] = e;
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    e = row_exponent(mx);
+    if (lane == 0) out.exps[(long long)b * out.rpad + i] = e;
+  }
   double p1 = 1.0, p2 = 1.0;
   if constexpr (DB == 8 && W <= 2 && S <= 14) fixed_scale<S>(e, p1, p2);
   const long long plane = out.plane();
@@ -622,6 +630,23 @@ __global__ void __launch_bounds__(256, (W <= 2 && S <= 14) ? 3 : 1) slice_rows_k
   } else {
     if constexpr (oz_has7<S>()) slice_rows_body<W, S, 7>(A, rows, cols, fi, out, sel);
   }
+}
+
+// Side A exponents only (mpps_slice_ex mode 1): one warp per row.
+__global__ void row_exps_kernel(MatRef A, int rows, int cols, int fi, SliceRef out, const int *sel) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int b = sel ? sel[blockIdx.y] : (int)blockIdx.y;
+  if (i >= out.rpad) return;
+  double mx = 0.0;
+  const long long base = (long long)b * A.bstride + (long long)i * A.ld;
+  if (i < rows)
+    for (int k = lane; k < cols; k += 32) {
+      double v = fi == F32 ? (double)((const float *)A.data)[base + k] : ((const double *)A.data)[base + k];
+      mx = fmax(mx, fabs(v));
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) out.exps[(long long)b * out.rpad + i] = row_exponent(mx);
 }
 
 // Side B: column exponents.  Block = 32 columns x 8 row groups; each thread

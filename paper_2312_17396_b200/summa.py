@@ -10,9 +10,13 @@ C_IJ = A_I: B_:J from two gathered panels:
     gathered ONCE per evaluation (all-gather along the process column), the
     row panel of X^{k-1} each step (all-gather along the process row);
   * Horner Y phi_j (engine.py:249-251): the row panel Y_I: is gathered once
-    (at the working format, converted locally to each level format), the
-    column panel of phi_j each level -- in the level format, so fp32 levels
-    move 1/4 of the dd bytes;
+    (at the working planes; each level uses a prefix), the column panel of
+    phi_j each level -- at the level format's planes;
+  * panels move as digit planes: each rank reduces the row (column) scales
+    of its block over the process row (column), splits only its own block
+    with them and all-gathers the planes -- exactly the split of the whole
+    panel, without splitting it pc (pr) times over, and S bytes per entry
+    instead of the dd words' 16;
   * block assembly, the Horner add and all format conversions are local;
   * overlap: every product is issued in row chunks (power chain) or column
     chunks (Horner) and each finished chunk's panel all-gather is started
@@ -217,6 +221,27 @@ def cols_of(A: MatBatch, lo: int, hi: int) -> MatBatch:
 DEFAULT_CHUNKS = 4
 
 
+class _PlanePending:
+    """An in-flight digit-plane panel (DeviceOps.panel_start); finish()
+    makes the caller's stream wait for the gather and returns the operand."""
+    __slots__ = ("work", "parts", "sl", "rows", "k", "db", "fmt", "side")
+
+    def __init__(self, work, parts, sl, rows, k, db, fmt, side):
+        self.work, self.parts, self.sl, self.rows, self.k = work, parts, sl, rows, k
+        self.db, self.fmt, self.side = db, fmt, side
+
+    def finish(self):
+        from . import _lib
+        from . import gemm_engine as ge
+        if self.work is not None:
+            self.work.wait()
+        sl = _lib.Slices.__new__(_lib.Slices)
+        sl.digits = self.parts[0] if len(self.parts) == 1 else _torch().cat(self.parts, dim=3)
+        sl.exps = self.sl.exps
+        sl.S, sl.rows, sl.k, sl.db = self.sl.S, self.rows, self.k, self.db
+        return ge.Operand(None, sl, self.fmt, self.side)
+
+
 class DeviceOps:
     """The C-ABI kernels, for SummaPS (one matrix per call, batch = 1)."""
 
@@ -250,6 +275,49 @@ class DeviceOps:
     def gemm_op(self, L, R, C):
         from . import gemm_engine as ge
         ge.gemm(self.h, L, R, C)
+
+    def panel_start(self, grid: "ProcessGrid", A: MatBatch, side: int, fmt: int, k_total: int):
+        """Start the digit-plane panel of this rank's block A: side 0, the row
+        panel A_I: (the blocks of the process row concatenated along K); side
+        1, the column panel A_:J (along the process column).  Each rank
+        splits only its own block, with the row / column scales reduced
+        (max) over the panel first, so the gathered planes are exactly the
+        split of the whole panel; the planes (S bytes per entry instead of
+        the dd words' 16) are all-gathered asynchronously."""
+        from . import _lib
+        from . import gemm_engine as ge
+        torch, dist = _torch(), _dist()
+        h = self.h
+        db = ge.digit_bits_for(h, k_total, getattr(self, "wf", None) or fmt)
+        S = h.slices_for(fmt, db)
+        rows, k = (A.rows, A.cols) if side == 0 else (A.cols, A.rows)
+        parts_n, group = (grid.pc, grid.row_group) if side == 0 else (grid.pr, grid.col_group)
+        sl = _lib.Slices(S, 1, rows, k, self.device, db)
+        if parts_n == 1:
+            h.slice_ex(A, side, sl, 0)
+            return _PlanePending(None, [sl.digits], sl, rows, k, db, fmt, side)
+        if k % 32:
+            raise ValueError(f"SUMMA plane gathers need block extents divisible by 32 (got {k})")
+        h.slice_ex(A, side, sl, 1)                                   # this block's scales
+        dist.all_reduce(sl.exps, op=dist.ReduceOp.MAX, group=group)  # the panel's scales
+        h.slice_ex(A, side, sl, 2)                                   # split with them
+        parts = [torch.empty_like(sl.digits) for _ in range(parts_n)]
+        work = dist.all_gather(parts, sl.digits, group=group, async_op=True)
+        return _PlanePending(work, parts, sl, rows, k * parts_n, db, fmt, side)
+
+    def concat_rows(self, ops_):
+        """One row-split operand from row chunks (digit planes and scales)."""
+        from . import _lib
+        from . import gemm_engine as ge
+        if len(ops_) == 1:
+            return ops_[0]
+        torch = _torch()
+        s0 = ops_[0].slices
+        sl = _lib.Slices.__new__(_lib.Slices)
+        sl.digits = torch.cat([o.slices.digits for o in ops_], dim=2)
+        sl.exps = torch.cat([o.slices.exps for o in ops_], dim=1)
+        sl.S, sl.rows, sl.k, sl.db = s0.S, sl.digits.shape[2], s0.k, s0.db
+        return ge.Operand(None, sl, ops_[0].fmt, 0)
 
     def horner_op(self, Y, phi, fmt_level, Bprev, out, ey=0, ei=0, eo=0):
         from . import gemm_engine as ge
@@ -312,7 +380,10 @@ def cos_argument_dist(Xblk: MatBatch, ctx: PrecisionCtx, grid: ProcessGrid, ops)
         Xw = ops.empty(wf, Xblk.rows, Xblk.cols)
         ops.convert(Xblk, Xw)
     Z = ops.empty(wf, Xw.rows, Xw.cols)
-    ops.gemm_op(ops.prepare(grid.row_panel(Xw), 0, wf), ops.prepare(grid.col_panel(Xw), 1, wf), Z)
+    n = Xw.rows * grid.pr
+    rp = ops.panel_start(grid, Xw, 0, wf, n)
+    cp = ops.panel_start(grid, Xw, 1, wf, n)
+    ops.gemm_op(rp.finish(), cp.finish(), Z)
     return Z
 
 
@@ -350,15 +421,15 @@ def ps_mixed_dist(Xblk: MatBatch, series: CoefficientSeries, ctx: PrecisionCtx, 
     # row-panel gathers of the newest power, one per row chunk, in flight
     # while the chunks after it are computed (and, for Y = X^s, while the
     # blocks are assembled and the norms reduced)
-    pend = [grid.row_panel_start(rows_of(P1, lo, hi)) for lo, hi in rch]
+    pend = [ops.panel_start(grid, rows_of(P1, lo, hi), 0, wf, n) for lo, hi in rch]
     if s > 1:
-        Xr = ops.prepare(grid.col_panel(P1), 1, wf)      # gathered and split once
+        Xr = ops.panel_start(grid, P1, 1, wf, n).finish()      # gathered and split once
         for _ in range(1, s):
             C = ops.empty(wf, mr, nc)
             nxt = []
             for (lo, hi), pnd in zip(rch, pend):
-                ops.gemm_op(ops.prepare(pnd.panel_finish(), 0, wf), Xr, rows_of(C, lo, hi))
-                nxt.append(grid.row_panel_start(rows_of(C, lo, hi)))
+                ops.gemm_op(pnd.finish(), Xr, rows_of(C, lo, hi))
+                nxt.append(ops.panel_start(grid, rows_of(C, lo, hi), 0, wf, n))
             pend = nxt
             powers.append(C)
     blocks = [ops.empty(wf, mr, nc) for _ in range(r + 1)]
@@ -385,18 +456,13 @@ def ps_mixed_dist(Xblk: MatBatch, series: CoefficientSeries, ctx: PrecisionCtx, 
     ey = _exp_for(float(norms[r + 1]))
     # Horner (engine.py:243-252)
     Y = powers[s - 1]
-    ypanels = [p.panel_finish() for p in pend]
-    Yrow_w = ypanels[0] if len(ypanels) == 1 else MatBatch(torch.cat([p.data for p in ypanels], dim=2), wf)
-    from . import gemm_engine as ge
+    # Y's row panel: the row chunks gathered during the assembly / norm
+    # reduction, at the working planes (each level uses a prefix)
+    Yrow = ops.concat_rows([p.finish() for p in pend])
     yrow = {}
-    tc_fmts = [f for f in set(fm[1:]) if not getattr(ops, "host_double", False)]
-    if tc_fmts:
-        ytc = ops.prepare(Yrow_w, 0, max(tc_fmts))
-        for f in tc_fmts:
-            yrow[f] = ytc
     for f in sorted(set(fm[1:])):
-        if f not in yrow:
-            yrow[f] = ops.prepare(Yrow_w, 0, f, ey if f == FP32 else 0)
+        yrow[f] = (ops.prepare(Yrow.mat, 0, f, ey if f == FP32 else 0) if getattr(ops, "host_double", False)
+                   else Yrow)
     if m % s == 0:
         out = ops.empty(fm[r - 1], mr, nc)
         ops.scalar_top(coeff_words(series, ctx)[m], fm[r], Y, blocks[r - 1], out, ex[r - 1])
@@ -409,16 +475,16 @@ def ps_mixed_dist(Xblk: MatBatch, series: CoefficientSeries, ctx: PrecisionCtx, 
     # gathered column chunk t of phi_j; its own gather starts as soon as it
     # is written
     cch = chunk_bounds(nc, chunks, chunk_align)
-    pend = [grid.col_panel_start(cols_of(phi, lo, hi)) for lo, hi in cch] if j0 > 0 else []
+    pend = [ops.panel_start(grid, cols_of(phi, lo, hi), 1, fm[j0], n) for lo, hi in cch] if j0 > 0 else []
     for j in range(j0, 0, -1):
         out = ops.empty(fm[j - 1], mr, nc)
         nxt = []
         for (lo, hi), pnd in zip(cch, pend):
-            ops.horner_op(yrow[fm[j]], ops.prepare(pnd.panel_finish(), 1, fm[j]), fm[j],
+            ops.horner_op(yrow[fm[j]], pnd.finish(), fm[j],
                           cols_of(blocks[j - 1], lo, hi), cols_of(out, lo, hi),
                           ey if fm[j] == FP32 else 0, ex[j], ex[j - 1])
             if j > 1:
-                nxt.append(grid.col_panel_start(cols_of(out, lo, hi)))
+                nxt.append(ops.panel_start(grid, cols_of(out, lo, hi), 1, fm[j - 1], n))
         pend = nxt
         phi = out
     return DistResult(phi, digits, nu, False, norms, s, r)

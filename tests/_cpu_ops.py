@@ -31,6 +31,19 @@ class CpuOps:
     def gemm_op(self, L, R, C):
         self.gemm(L.mat, R.mat, C)
 
+    def panel_start(self, grid, A, side, fmt, k_total):
+        """The dd panel gathered by the grid (no digit planes on the host)."""
+        pend = grid.row_panel_start(A) if side == 0 else grid.col_panel_start(A)
+        ops = self
+
+        class _P:
+            def finish(self_):
+                return ops.prepare(pend.panel_finish(), side, fmt)
+        return _P()
+
+    def concat_rows(self, ops_):
+        return _Op(MatBatch(torch.cat([o.mat.data for o in ops_], dim=2), ops_[0].mat.fmt))
+
     def horner_op(self, Y, phi, fmt_level, Bprev, out, ey=0, ei=0, eo=0):
         self.horner_step(Y.mat, phi.mat, Bprev, out, ey, ei, eo)
 

@@ -92,3 +92,42 @@ def test_summa_chunked_overlap_is_bitwise_invisible(cuda):
         b = summa.ps_mixed_dist(blk, series, ctx, grid, ops, chunks=3)
         assert a.digits == b.digits
         assert torch.equal(a.block.data, b.block.data), family
+
+
+@pytest.mark.parametrize("db,fmt", [(8, 31), (7, 31), (8, 15)])
+def test_plane_panel_equals_split_of_the_panel(cuda, db, fmt):
+    """SUMMA panels move as digit planes: a block split with the panel's
+    scales (mpps_slice_ex: mode 1 scales of each block, max over the blocks,
+    mode 2 split) and concatenated along K gives exactly the planes and
+    scales of the split of the whole panel -- row panels (side 0, blocks
+    along columns) and column panels (side 1, blocks along rows)."""
+    import torch
+    from paper_2312_17396_b200 import _lib
+    from paper_2312_17396_b200.precision import MatBatch
+    h = _lib.handle_for()
+    rng = np.random.default_rng(12)
+    rows, K, parts = 200, 384, 3            # blocks of K/parts = 128
+    W = 2 if fmt == 31 else 1
+    A = rng.standard_normal((W, 1, rows, K)) * np.logspace(0, -9, K)[None, None, None, :]
+    if W == 2:
+        A[1] *= 2.0 ** -57
+    S = h.slices_for(fmt, db)
+    for side in (0, 1):
+        src = A if side == 0 else A.transpose(0, 1, 3, 2).copy()
+        M = MatBatch(torch.from_numpy(src).cuda(), fmt)
+        whole = h.slice(M, side, S, None, db)
+        kb = K // parts
+        blocks = []
+        for p in range(parts):
+            sub = src[..., :, p * kb:(p + 1) * kb] if side == 0 else src[..., p * kb:(p + 1) * kb, :]
+            B = MatBatch(torch.from_numpy(np.ascontiguousarray(sub)).cuda(), fmt)
+            sl = _lib.Slices(S, 1, rows, kb, "cuda", db)
+            h.slice_ex(B, side, sl, 1)
+            blocks.append((B, sl))
+        ex = torch.stack([sl.exps for _, sl in blocks]).amax(dim=0)
+        for B, sl in blocks:
+            sl.exps.copy_(ex)
+            h.slice_ex(B, side, sl, 2)
+        digits = torch.cat([sl.digits for _, sl in blocks], dim=3)
+        assert torch.equal(ex[:, :rows], whole.exps[:, :rows]), side
+        assert torch.equal(digits[:, :, :rows], whole.digits[:, :, :rows]), side
