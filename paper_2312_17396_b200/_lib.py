@@ -31,7 +31,7 @@ EXPORTED = (
     "mpps_assemble_blocks_dist", "mpps_colmax", "mpps_slice", "mpps_gemm_sliced",
     "mpps_horner_step_sliced", "mpps_oz_slices_for", "mpps_oz_slices_for_bits", "mpps_oz_max_k_8bit", "mpps_oz_max_k", "mpps_probe_i8mma", "mpps_debug_oz_trace",
     "mpps_debug_oz_flags", "mpps_debug_probe_i8mma_n", "mpps_probe_ingest",
-    "mpps_small_ps_supported", "mpps_small_ps_prepare", "mpps_small_ps_horner", "mpps_slice_ex",
+    "mpps_small_ps_supported", "mpps_small_ps_prepare", "mpps_small_ps_horner", "mpps_slice_ex", "mpps_small_ps_eval",
 )
 
 
@@ -152,6 +152,7 @@ def load_library(path: Optional[str] = None):
         lib.mpps_small_ps_supported.argtypes = [ip, ip, ip]
         lib.mpps_small_ps_prepare.argtypes = [vp, mp, ip, ip, P(ctypes.c_double), vp, vp, vp]
         lib.mpps_small_ps_horner.argtypes = [vp, vp, vp, vp, ip, ip, ctypes.c_double, mp]
+        lib.mpps_small_ps_eval.argtypes = [vp, mp, ip, ip, vp, ip, ctypes.c_double, ip, ip, vp, vp, vp, vp, vp, vp, mp]
         for name in EXPORTED:
             getattr(lib, name).restype = getattr(lib, name).restype or ip
         if path is None:
@@ -410,6 +411,26 @@ class Handle:
         f = np.ascontiguousarray(level_fmt, dtype=np.int8)
         self._check(self.lib.mpps_small_ps_horner(self.h, Y.data_ptr(), blocks.data_ptr(), f.ctypes.data,
                                                   int(m), int(s), float(bm), ctypes.byref(o)), "small_ps")
+
+    def small_ps_eval(self, X: MatBatch, m: int, s: int, coeff: np.ndarray, d: int, delta: float,
+                      apply_switch: bool, fixed: bool, blocks, Y, norms_dev, out: MatBatch):
+        """One call: prepare, host norms, certified digit rule, Horner.
+        Returns (norms (B, r+2), digits (B, r), nu (B,), planned): planned is
+        False when the certified rule declined (the caller plans exactly and
+        runs small_ps_horner)."""
+        B, r = X.batch, m // s
+        norms = np.empty((B, r + 2), dtype=np.float64)
+        digits = np.empty((B, max(r, 1)), dtype=np.int32)
+        nu = np.empty(B, dtype=np.int32)
+        x, o = cmat(X), cmat(out)
+        rc = self.lib.mpps_small_ps_eval(self.h, ctypes.byref(x), int(m), int(s), coeff.ctypes.data, int(d),
+                                         float(delta), int(bool(apply_switch)), int(bool(fixed)), blocks.data_ptr(),
+                                         Y.data_ptr(), norms_dev.data_ptr(), norms.ctypes.data, digits.ctypes.data,
+                                         nu.ctypes.data, ctypes.byref(o))
+        if rc == 4:
+            return norms, None, None, False
+        self._check(rc, "small_ps")
+        return norms, digits[:, :r], nu, True
 
     def probe_ingest(self, blocks: int, iters: int, src):
         self._check(self.lib.mpps_probe_ingest(self.h, blocks, iters, src.data_ptr(), src.numel() * src.element_size()),

@@ -1285,6 +1285,81 @@ int mpps_small_ps_horner(mpps_handle *h, const double *Y, const double *blocks, 
   return rc2;
 }
 
+// The planner's digit rule (engine.py:184-215) in certified float64 for one
+// matrix: exact digits unless some e_i lies within 1e-8 of an integer or of
+// the delta threshold (float64 evaluation error < 1e-11) -- then returns 1
+// and the caller plans exactly (planner.plan_precisions).
+static int small_plan_row(const double *nb, double y, int r, int d, double delta, int apply_switch, int *digits,
+                          int *nu_out) {
+  const double M = 1e-8, lim = d - log10(delta);
+  if (y == 0.0) {
+    for (int i = 0; i < r; ++i) digits[i] = 1;
+    *nu_out = 1;
+    return 0;
+  }
+  if (!isfinite(y)) return 1;
+  for (int i = 0; i <= r; ++i)
+    if (!isfinite(nb[i])) return 1;
+  const double lb0 = nb[0] > 0 ? log10(nb[0]) : 0.0, ly = log10(y);
+  int qual[64];
+  for (int i = 1; i <= r; ++i) {
+    if (nb[i] == 0.0 || nb[0] == 0.0) {
+      digits[i - 1] = 1;
+      qual[i - 1] = 1;
+      continue;
+    }
+    const double e = (d - lb0) + (log10(nb[i]) + i * ly) + 1e-9;
+    if (fabs(e - nearbyint(e)) < M || fabs(e - lim) < M) return 1;
+    int di = (int)floor(e);
+    digits[i - 1] = di < 1 ? 1 : (di > d ? d : di);
+    qual[i - 1] = e <= lim;
+  }
+  int nu = r + 1;
+  for (int i = 1; i <= r; ++i)
+    if (qual[i - 1]) { nu = i; break; }
+  if (apply_switch)
+    for (int i = 1; i < nu; ++i) digits[i - 1] = d;
+  for (int i = r - 2; i >= 0; --i)
+    if (digits[i + 1] > digits[i]) digits[i] = digits[i + 1];
+  *nu_out = nu;
+  return 0;
+}
+
+int mpps_small_ps_eval(mpps_handle *h, const mpps_mat *X, int m, int s, const double *coeff, int d, double delta,
+                       int apply_switch, int fixed, double *blocks, double *Y, double *norms_dev, double *norms_host,
+                       int *digits_host, int *nu_host, mpps_mat *out) {
+  int rc = mpps_small_ps_prepare(h, X, m, s, coeff, blocks, Y, norms_dev);
+  if (rc) return rc;
+  const int B = X->batch, r = m / s;
+  if (r > 63) return set_err(h, MPPS_EINVAL, "small_ps_eval: r too large");
+  cudaError_t e = cudaMemcpyAsync(norms_host, norms_dev, sizeof(double) * (size_t)B * (r + 2), cudaMemcpyDeviceToHost,
+                                  h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);     // the one host sync (planner norms)
+  if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "small_ps_eval norms: %s", cudaGetErrorString(e));
+  static thread_local signed char fmts[mpps::small::kInlineFmt];
+  signed char *fm = (size_t)B * (r + 1) <= sizeof(fmts) ? fmts : (signed char *)malloc((size_t)B * (r + 1));
+  int uncertain = 0;
+  for (int b = 0; b < B && !uncertain; ++b) {
+    int *dg = digits_host + (long long)b * r;
+    if (fixed) {
+      for (int i = 0; i < r; ++i) dg[i] = d;
+      nu_host[b] = r + 1;
+    } else {
+      uncertain = small_plan_row(norms_host + (long long)b * (r + 2), norms_host[(long long)b * (r + 2) + r + 1], r, d,
+                                 delta, apply_switch, dg, &nu_host[b]);
+    }
+    fm[(long long)b * (r + 1)] = 1;                            // level 0: the fp64 working format
+    for (int i = 0; i < r; ++i) fm[(long long)b * (r + 1) + 1 + i] = dg[i] <= 7 ? 0 : 1;
+  }
+  if (uncertain) {
+    if (fm != fmts) free(fm);
+    return 4;   // MPPS_NEED_PLAN: the caller plans exactly and calls mpps_small_ps_horner
+  }
+  rc = mpps_small_ps_horner(h, Y, blocks, fm, m, s, coeff[m], out);
+  if (fm != fmts) free(fm);
+  return rc;
+}
+
 int mpps_probe_fma(mpps_handle *h, int fmt, int blocks, int iters, void *scratch) {
   if (!scratch || blocks < 1 || iters < 1) return set_err(h, MPPS_EINVAL, "probe: bad arguments");
   if (fmt == MPPS_FP64)

@@ -744,10 +744,13 @@ def _small_ok_uncached(X, series: CoefficientSeries, ctx: PrecisionCtx) -> bool:
 
 def _small_eval(X, series: CoefficientSeries, ctx: PrecisionCtx, kind: str, delta: float, apply_switch: bool,
                 fix_params: bool, with_bound: bool, timing: bool):
-    """K5: powers, blocks and norms in one launch, the host
-    planner, the mixed Horner chain in a second launch (one CTA per matrix,
-    operands in shared memory) -- engine.py:141-154, 127-138, 157-215,
-    243-252.  kind: "mixed" or "fixed"."""
+    """K5: powers, blocks and norms in one launch, the planner's
+    digit rule in certified float64 inside the library (mpps_small_ps_eval:
+    no Python between the two launches), the mixed Horner chain in a second
+    launch -- engine.py:141-154, 127-138, 157-215, 243-252.  When the
+    certified rule declines (an e_i within 1e-8 of a digit boundary) the
+    exact planner runs here and the Horner launch follows.  kind: "mixed" or
+    "fixed"."""
     torch = _torch()
     Xt, Xw, single = _input(X)
     B, n = _check_square(Xt, Xw)
@@ -757,37 +760,46 @@ def _small_eval(X, series: CoefficientSeries, ctx: PrecisionCtx, kind: str, delt
     s = default_block_size(m)
     r = m // s
     d = ctx.decimal_digits
-    cw = np.ascontiguousarray(coeff_words(series, ctx)[:, 0])     # fp64 working: one word each
+    cw = _small_coeffs(series, ctx)
     dev = Xm.device
     timer = _Buckets(timing)
     blocks = torch.empty((r + 1, B, n, n), dtype=torch.float64, device=dev)
     Y = torch.empty((B, n, n), dtype=torch.float64, device=dev)
     norms_d = torch.empty((B, r + 2), dtype=torch.float64, device=dev)
-    timer.start("power_formation")
-    h.small_ps_prepare(Xm, m, s, cw, blocks, Y, norms_d)
-    timer.stop()
-    timer.start("norm_estimation")
-    norms = norms_d.cpu().numpy()              # the one host sync
-    if kind == "fixed":
-        digits = np.full((B, r), d, dtype=np.int64)
-        nu = np.full(B, r + 1, dtype=np.int64)
-    else:
-        digits, nu, _ = plan_digits_batch(norms[:, :r + 1], norms[:, r + 1], d, delta, apply_switch)
-    timer.stop()
-    fm = np.ones((B, r + 1), dtype=np.int8)
-    for b, dg in enumerate(np.asarray(digits).tolist()):
-        fm[b, 1:] = [0 if f == FP32 else 1 for f in formats_of_digits(dg)]
     result = MatBatch.empty(FP64, B, n, device=dev)
-    timer.start("mixed_horner")
-    h.small_ps_horner(Y, blocks, fm, m, s, float(cw[m]), result)
+    timer.start("power_formation")
+    norms, digits, nu, planned = h.small_ps_eval(Xm, m, s, cw, d, delta, apply_switch, kind == "fixed", blocks, Y,
+                                                 norms_d, result)
     timer.stop()
+    if not planned:
+        digits, nu, _ = plan_digits_batch(norms[:, :r + 1], norms[:, r + 1], d, delta, apply_switch)
+        fm = np.ones((B, r + 1), dtype=np.int8)
+        for b, dg in enumerate(np.asarray(digits).tolist()):
+            fm[b, 1:] = [0 if f == FP32 else 1 for f in formats_of_digits(dg)]
+        timer.start("mixed_horner")
+        h.small_ps_horner(Y, blocks, fm, m, s, float(cw[m]), result)
+        timer.stop()
     if kind == "fixed":
         fns = [(lambda nb=tuple(float(x) for x in norms[b, :r + 1]), ny=float(norms[b, r + 1]):
                 fixed_plan(nb, ny, ctx, s)) for b in range(B)]
         return _reports(result, fns, None, "fixed", timer.seconds(), with_bound, single)
     fns = [_plan_fn(norms[b], r, ctx, delta, s, apply_switch, fix_params) for b in range(B)]
-    executed = [(tuple(int(x) for x in digits[b]), int(nu[b])) for b in range(B)]
+    dl, nl = np.asarray(digits).tolist(), np.asarray(nu).tolist()
+    executed = [(tuple(dl[b]), int(nl[b])) for b in range(B)]
     return _reports(result, fns, executed, "mixed", timer.seconds(), with_bound, single)
+
+
+_SMALL_COEFFS: Dict[tuple, np.ndarray] = {}
+
+
+def _small_coeffs(series: CoefficientSeries, ctx: PrecisionCtx) -> np.ndarray:
+    key = (series.token, ctx.binary_precision)
+    c = _SMALL_COEFFS.get(key)
+    if c is None:
+        if len(_SMALL_COEFFS) > 64:
+            _SMALL_COEFFS.clear()
+        c = _SMALL_COEFFS[key] = np.ascontiguousarray(coeff_words(series, ctx)[:, 0])   # fp64: one word each
+    return c
 
 
 # ------------------------------------------------------------ evaluators

