@@ -668,9 +668,11 @@ def run_ours(name, args, rank, world, local_rank, dist):
                     "no L2 flush inside the stream, per-step working set ~1 GB > L2)")
         h2d = wl.Xh[0].nbytes
         d2h = W * wl.Xh[0].nbytes
-    elif wl.Xh[0].nbytes < (64 << 20):
-        # small steps (cfg1): one call per step through the public API, the
-        # result copied back to pinned memory, each step synchronised
+    elif wl.kind != "cos" or os.environ.get("MPPS_BENCH_E2E_STREAM") == "0":
+        # one call per step through the public API, the result copied back
+        # to pinned memory, each step synchronised.  (A host stream measured
+        # slower for cfg3, whose mid-step host syncs queue behind the
+        # previous step's D2H on the copy engine, and equal for cfg4.)
         outs = None
         for i in range(args.steps + 1):
             X = wl.Xpin[(i + P - 1) % P]
