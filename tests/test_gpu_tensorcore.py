@@ -204,21 +204,22 @@ from paper_2312_17396_b200.precision import MatBatch
 h = _lib.handle_for()
 rng = np.random.default_rng(4)
 out = {}
-for (M, K, N, db) in ((384, 4160, 512, 8), (256, 4096, 320, 7)):
+for (M, K, N, db, fmt) in ((384, 4160, 512, 8, 31), (256, 4096, 320, 7, 31), (200, 4160, 384, 8, 15)):
     A = MatBatch(torch.from_numpy(rng.standard_normal((2, 2, M, K)) * np.array([1, 2.0 ** -55])[:, None, None, None]).cuda(), 31)
     Bm = MatBatch(torch.from_numpy(rng.standard_normal((2, 2, K, N)) * np.array([1, 2.0 ** -57])[:, None, None, None]).cuda(), 31)
-    S = h.slices_for(31, db)
-    C = MatBatch.zeros(31, 2, M, N, device="cuda")
+    S = h.slices_for(fmt, db)
+    C = MatBatch.zeros(fmt, 2, M, N, device="cuda")
     h.gemm_sliced(h.slice(A, 0, S, None, db), h.slice(Bm, 1, S, None, db), S, C)
-    out[f"{M}_{db}"] = C.data.cpu().numpy()
+    out[f"{M}_{db}_{fmt}"] = C.data.cpu().numpy()
 np.savez(sys.argv[2], **out)
 '''
 
 
 def test_wide_kernel_cluster_multicast_matches(cuda, tmp_path):
-    """The 128-byte-box dd GEMM (K >= 4096) with 2-CTA clusters multicasting
-    the A planes gives the same bits as one CTA per tile (MPPS_OZ_WIDE_MC=0),
-    8- and 7-bit digits, batch 2, ragged K."""
+    """The 128-byte-box GEMMs (K >= 4096: dd, and the 8-plane fp64 product
+    with 64-column tiles) with 2-CTA clusters multicasting the A planes give
+    the same bits as one CTA per tile (MPPS_OZ_WIDE_MC=0) and as the 32-byte
+    box kernels (MPPS_OZ_WIDE=0); 8- and 7-bit digits, batch 2, ragged K."""
     import os
     import subprocess
     import sys
@@ -226,10 +227,11 @@ def test_wide_kernel_cluster_multicast_matches(cuda, tmp_path):
     script = tmp_path / "w.py"
     script.write_text(_WIDE_SCRIPT)
     res = {}
-    for tag, env in (("mc", {}), ("solo", {"MPPS_OZ_WIDE_MC": "0"})):
+    for tag, env in (("mc", {}), ("solo", {"MPPS_OZ_WIDE_MC": "0"}), ("tma", {"MPPS_OZ_WIDE": "0"})):
         f = tmp_path / f"{tag}.npz"
         subprocess.check_call([sys.executable, str(script), root, str(f)], env=dict(os.environ, **env))
         res[tag] = dict(np.load(f))
     for k in res["mc"]:
         assert np.array_equal(res["mc"][k], res["solo"][k]), k
+        assert np.array_equal(res["mc"][k], res["tma"][k]), k
         assert np.abs(res["mc"][k]).sum() > 0
