@@ -1894,14 +1894,17 @@ static bool oz_wide_for(int S, int fo, int mode, int K) {
   }
   if (!v) return false;
   return ((S == 16 || S == 14) && mode == 0 && fo == DD && (K >= 4096 || v == 2)) || (S == 31 && fo == QD && v == 2) ||
-         (S == 8 && mode == 0 && fo == F64 && K >= 4096);     // Y = X^s at fp64 precision (64-column tiles)
+         (S == 8 && mode == 0 && fo == F64 && K >= 4096) ||   // Y = X^s at fp64 precision (64-column tiles)
+         ((S == 2 || S == 3) && mode == 1 && fo != QD && K >= 4096);   // few-plane Horner levels (128 columns)
 }
-// N tile of the wide kernel: 8-plane fp64 products fill TMEM with 64 columns
-static int oz_wide_nt(int S) { return S == 8 ? 64 : S > 16 ? 16 : 32; }
+// N tile of the wide kernel: 8-plane fp64 products fill TMEM with 64 columns,
+// 2-3-plane Horner levels with 128 (chunked staged epilogue)
+static int oz_wide_nt(int S, int mode) { return (mode == 1 && S <= 4) ? 128 : S == 8 ? 64 : S > 16 ? 16 : 32; }
 
 static int dispatch_oz_wide(mpps_handle *h, int S, int fo, int mode, const oz::OzTmaArgs &a, int nb) {
 #define OZ(SS, NT, FF, MM) if (S == SS && fo == FF && mode == MM) return launch_oz_wide<SS, NT, FF, MM>(h, a, nb);
   OZ(14, 32, DD, 0) OZ(16, 32, DD, 0) OZ(31, 16, QD, 0) OZ(31, 16, QD, 1) OZ(8, 64, F64, 0)
+  OZ(2, 128, F32, 1) OZ(2, 128, F64, 1) OZ(2, 128, DD, 1) OZ(3, 128, F32, 1) OZ(3, 128, F64, 1) OZ(3, 128, DD, 1)
 #undef OZ
   return set_err(h, MPPS_EFMT, "wide tensor-core GEMM: no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
 }
@@ -1932,7 +1935,7 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   const bool ring = pers || oz_mode() == 2 || (oz_mode() == 3 && S >= 14) || S == 14 || S == 28;
   const bool nt128 = !wide && !ring && oz_nt128_for(S, fo, mode, a.K, slice_db(A));
   const bool nt64 = !wide && !ring && !nt128 && oz_nt64_for(S, fo, mode);
-  const int NT = wide ? oz_wide_nt(S) : (S > 16 || pers) ? 16 : (nt128 ? 128 : nt64 ? 64 : 32);
+  const int NT = wide ? oz_wide_nt(S, mode) : (S > 16 || pers) ? 16 : (nt128 ? 128 : nt64 ? 64 : 32);
   const int abox = ring ? (S < 4 ? S : (S == 14 ? 7 : 4)) : S;   // OzRing<S, NT>::SG
   int rc;
   if (wide || pmode == 3) {

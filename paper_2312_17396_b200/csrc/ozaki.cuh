@@ -2072,7 +2072,10 @@ __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_wide_kernel(const __gr
     }
     mma_commit(smem_u32(done));
   }
-  oz_kernel_epilogue<S, NT, FO, MODE, STAGED>(args, ebuf, ebs, tmem, done, warp, lane, b, m0, n0, tr);
+  if constexpr (oz_chunked<S, NT, FO, MODE>())
+    oz_kernel_epilogue_chunked<S, NT, FO, MODE>(args, ebuf, ebs, tmem, done, warp, lane, b, m0, n0, tr);
+  else
+    oz_kernel_epilogue<S, NT, FO, MODE, STAGED>(args, ebuf, ebs, tmem, done, warp, lane, b, m0, n0, tr);
   if constexpr (CL > 1) {
     // no CTA leaves while its peer may still multicast into its ring or
     // arrive on its barriers

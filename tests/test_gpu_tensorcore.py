@@ -159,9 +159,9 @@ from paper_2312_17396_b200 import _lib
 from paper_2312_17396_b200.precision import MatBatch
 h = _lib.handle_for()
 rng = np.random.default_rng(3)
-B, M, K, N = 3, 200, 2080, 300
+B, M, N = 3, 200, 300
 out = {}
-for S, fo in ((2, 7), (3, 15), (4, 31), (2, 31)):
+for K, S, fo in ((2080, 2, 7), (2080, 3, 15), (2080, 4, 31), (2080, 2, 31), (4160, 2, 7), (4160, 3, 31)):
     Y = MatBatch(torch.from_numpy(rng.standard_normal((1, B, M, K))).cuda(), 15)
     P = MatBatch(torch.from_numpy(rng.standard_normal((1, B, K, N))).cuda(), 15)
     Bp = MatBatch(torch.from_numpy(rng.standard_normal((2, B, M, N)) * np.array([1, 2.0 ** -60])[:, None, None, None]).cuda(), 31)
@@ -170,16 +170,17 @@ for S, fo in ((2, 7), (3, 15), (4, 31), (2, 31)):
     ei = torch.tensor([3, -1, 2], dtype=torch.int32, device="cuda")
     eo = torch.tensor([-2, 0, 1], dtype=torch.int32, device="cuda")
     h.horner_step_sliced(h.slice(Y, 0, S, None, 8), h.slice(P, 1, S, None, 8), S, Bp, o, sel, None, ei, eo, fmt_in=fo)
-    out[f"{S}_{fo}"] = o.data.double().cpu().numpy()
+    out[f"{K}_{S}_{fo}"] = o.data.double().cpu().numpy()
 np.savez(sys.argv[2], **out)
 '''
 
 
 def test_nt128_few_plane_horner_matches_nt32(cuda, tmp_path):
     """The 128-column few-plane Horner tiles (K >= 2048, S <= 4, chunked
-    staged epilogue) give the same bits as the 32-column tiles
-    (MPPS_OZ_NT128_K=0), with ragged M / N / K, a selection and level
-    exponents; run in two processes (the switch is read once)."""
+    staged epilogue; 128-byte K boxes for S <= 3 at K >= 4096) give the same
+    bits as the 32-column tiles (MPPS_OZ_NT128_K=0) and as the 32-byte-box
+    128-column kernel (MPPS_OZ_WIDE=0), with ragged M / N / K, a selection
+    and level exponents; separate processes (the switches are read once)."""
     import os
     import subprocess
     import sys
@@ -187,12 +188,14 @@ def test_nt128_few_plane_horner_matches_nt32(cuda, tmp_path):
     script = tmp_path / "nt.py"
     script.write_text(_NT128_SCRIPT)
     res = {}
-    for tag, env in (("wide", {}), ("narrow", {"MPPS_OZ_NT128_K": "0"})):
+    for tag, env in (("wide", {}), ("narrow", {"MPPS_OZ_NT128_K": "0", "MPPS_OZ_WIDE": "0"}),
+                     ("tma128", {"MPPS_OZ_WIDE": "0"})):
         f = tmp_path / f"{tag}.npz"
         subprocess.check_call([sys.executable, str(script), root, str(f)], env=dict(os.environ, **env))
         res[tag] = dict(np.load(f))
     for k in res["wide"]:
         assert np.array_equal(res["wide"][k], res["narrow"][k]), k
+        assert np.array_equal(res["wide"][k], res["tma128"][k]), k
         assert np.abs(res["wide"][k][:, 1]).sum() == 0 and np.abs(res["wide"][k][:, 0]).sum() > 0
 
 
