@@ -1895,11 +1895,15 @@ static bool oz_wide_for(int S, int fo, int mode, int K) {
   if (!v) return false;
   return ((S == 16 || S == 14) && mode == 0 && fo == DD && (K >= 4096 || v == 2)) || (S == 31 && fo == QD && v == 2) ||
          (S == 8 && mode == 0 && fo == F64 && K >= 4096) ||   // Y = X^s at fp64 precision (64-column tiles)
-         ((S == 2 || S == 3) && mode == 1 && fo != QD && K >= 4096);   // few-plane Horner levels (128 columns)
+         ((S == 2 || S == 3) && mode == 1 && fo != QD && K >= 4096);   // few-plane Horner levels
+  // (4 planes: the 32-byte-box NT = 128 kernel measured 4.7 vs 4.9 ms for a
+  // 64-column wide one at cfg5, so S >= 4 levels stay there)
 }
-// N tile of the wide kernel: 8-plane fp64 products fill TMEM with 64 columns,
-// 2-3-plane Horner levels with 128 (chunked staged epilogue)
-static int oz_wide_nt(int S, int mode) { return (mode == 1 && S <= 4) ? 128 : S == 8 ? 64 : S > 16 ? 16 : 32; }
+// N tile of the wide kernel: 8-plane fp64 products fill TMEM with 64 columns;
+// 2-3-plane Horner levels 128 columns (chunked staged epilogue)
+static int oz_wide_nt(int S, int mode) {
+  return (mode == 1 && S <= 3) ? 128 : S == 8 ? 64 : S > 16 ? 16 : 32;
+}
 
 static int dispatch_oz_wide(mpps_handle *h, int S, int fo, int mode, const oz::OzTmaArgs &a, int nb) {
 #define OZ(SS, NT, FF, MM) if (S == SS && fo == FF && mode == MM) return launch_oz_wide<SS, NT, FF, MM>(h, a, nb);

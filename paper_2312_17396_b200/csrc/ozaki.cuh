@@ -1416,7 +1416,7 @@ __host__ __device__ constexpr bool oz_staged() {
 // N = 256 MMAs; the epilogue stages 32-column chunks of the tile in turn.
 template <int S, int NT, int FO, int MODE>
 __host__ __device__ constexpr bool oz_chunked() {
-  return NT == 128 && S <= 4 && FO != QD && MODE == 1;
+  return ((NT == 128 && S <= 4) || (NT == 64 && S <= 8)) && FO != QD && MODE == 1;
 }
 constexpr int kEpiChunk = 32;
 template <int S, int NT, int FO, int MODE>

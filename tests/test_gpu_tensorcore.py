@@ -161,7 +161,8 @@ h = _lib.handle_for()
 rng = np.random.default_rng(3)
 B, M, N = 3, 200, 300
 out = {}
-for K, S, fo in ((2080, 2, 7), (2080, 3, 15), (2080, 4, 31), (2080, 2, 31), (4160, 2, 7), (4160, 3, 31)):
+for K, S, fo in ((2080, 2, 7), (2080, 3, 15), (2080, 4, 31), (2080, 2, 31), (4160, 2, 7), (4160, 3, 31),
+                 (4160, 4, 31)):
     Y = MatBatch(torch.from_numpy(rng.standard_normal((1, B, M, K))).cuda(), 15)
     P = MatBatch(torch.from_numpy(rng.standard_normal((1, B, K, N))).cuda(), 15)
     Bp = MatBatch(torch.from_numpy(rng.standard_normal((2, B, M, N)) * np.array([1, 2.0 ** -60])[:, None, None, None]).cuda(), 31)
