@@ -1,0 +1,65 @@
+"""The committed bench lines agree with the committed ncu launch lists of the
+same command (profiles/r02_*): the dominant kernel's share of the step and
+its mean launch time, and the line's roofline fraction recomputes from its
+own fields (the fraction must follow from the profiles)."""
+import collections
+import csv
+import json
+import os
+
+import pytest
+
+PROF = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles")
+
+
+def _lines():
+    p = os.path.join(PROF, "r02_bench_default.jsonl")
+    if not os.path.exists(p):
+        pytest.skip("no committed bench lines")
+    return {json.loads(l)["config"]["name"]: json.loads(l) for l in open(p) if l.startswith("{")}
+
+
+def _launches(name):
+    rows = list(csv.reader(open(os.path.join(PROF, f"r02_launches_bench_{name}.csv"))))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h = rows[hi]
+    ki, mi, vi, ui = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
+    out = []
+    for r in rows[hi + 1:]:
+        if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
+            continue
+        v = float(r[vi].replace(",", ""))
+        scale = {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3}.get(r[ui], 1.0)
+        out.append((r[ki], v * scale))
+    return [(k, t) for k, t in out if "probe" not in k]
+
+
+def test_roofline_fraction_recomputes():
+    for name, line in _lines().items():
+        r = line["roofline"]
+        if "algorithmic_ops_per_launch" not in r:
+            continue
+        achieved = r["algorithmic_ops_per_launch"] / r["mean_launch_s"] / 1e12
+        assert abs(achieved - r["achieved"]) <= 1e-6 * r["achieved"], name
+        assert abs(achieved / r["peak"] - r["frac"]) <= 1e-9, name
+
+
+@pytest.mark.parametrize("name,kernel", [("cfg5", "oz_gemm_wide_kernel<14"), ("cfg2", "oz_gemm_ring_kernel<14")])
+def test_dominant_share_matches_launch_list(name, kernel):
+    line = _lines()[name]
+    r = line["roofline"]
+    launches = _launches(name)
+    total = sum(t for _, t in launches)
+    mine = [t for k, t in launches if kernel in k]
+    assert mine, kernel
+    # the key's launches: this kernel runs 3 times per evaluation in both
+    # configs (cfg5: Z, Z^2, [Z^3|Z^4]; cfg2: X^2, [X^3|X^4], [X^5|X^6]); a
+    # paired key (N = 2M) takes the longest launches_per_step of each
+    # evaluation, an N = M key the shortest
+    M, N = (int(x) for x in r["kernel"].split()[2].split("x")[:2])
+    count = int(round(r["launches_per_step"] * len(mine) / 3.0))
+    longest = sorted(mine)[-count:] if N != M else sorted(mine)[:count]
+    share_ncu = sum(longest) / total
+    assert abs(share_ncu - r["share_of_step"]) <= 0.12, (share_ncu, r["share_of_step"])
+    mean_ncu = sum(longest) / len(longest)
+    assert 0.6 <= mean_ncu / r["mean_launch_s"] <= 1.4, (mean_ncu, r["mean_launch_s"])
