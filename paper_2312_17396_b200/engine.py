@@ -65,6 +65,7 @@ _SMALL = _os.environ.get("MPPS_SMALL", "1") != "0"
 #: mixed evaluators with an odd s >= 5 form Y = X^s at fp64 precision and at dd only for the
 #: matrices whose plan keeps a Horner level at dd (MPPS_Y_LOW=0: Y always at dd)
 _Y_LOW = _os.environ.get("MPPS_Y_LOW", "1") != "0"
+_Y_LOW_MIN_N = 4096
 
 
 def _torch():
@@ -316,10 +317,14 @@ def _form_powers(h, Xt, wf: int, s: int, timer: _Buckets, x_is_working: Optional
     return powers
 
 
-def _y_low_ok(wf: int, s: int, lowp: bool) -> bool:
+def _y_low_ok(wf: int, s: int, lowp: bool, n: int) -> bool:
     """Y = X^s at fp64 precision first (see _paired_powers): mixed evaluators
-    on the dd tensor-core chain whose last power is a single GEMM (odd s)."""
-    return (_Y_LOW and lowp and wf == DD and s >= 5 and s % 2 == 1 and _PAIRED
+    on the dd tensor-core chain whose last power is a single GEMM (odd s),
+    for n >= 4096, where the 8-plane product runs on the 128-byte-box kernel
+    at ~0.36 of the dd product's time (at n = 1024 it takes ~0.52 of it, so
+    cfg3, whose plans mostly keep a dd level and then recompute Y at dd, was
+    2.5 % slower with it)."""
+    return (_Y_LOW and lowp and wf == DD and s >= 5 and s % 2 == 1 and _PAIRED and n >= _Y_LOW_MIN_N
             and complexmat.scope() is None)
 
 
@@ -453,7 +458,8 @@ def _prepare(h, Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: in
     # kernels (both the mixed and the all-dd ones read an fp64 X^1)
     x64 = (wf == DD and complexmat.scope() is None and h.assemble_hc_supported(wf, s, m)
            and (not lowp or _lowp_blocks(h, wf, s, m) > 0))
-    y_low = _y_low_ok(wf, s, lowp)
+    n = Xt.shape[-1] if Xt is not None else x_is_working.rows
+    y_low = _y_low_ok(wf, s, lowp, n)
     powers = _form_powers(h, Xt, wf, s, timer, x_is_working, x_fp64_ok=x64, y_low=y_low)
     prep = _assemble(h, powers, series, ctx, wf, s, timer, sync, lowp)
     prep.y_low = y_low and powers[s - 1].fmt != wf
@@ -808,7 +814,7 @@ def _graph_stages(Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: 
     """(key, build_pre, run_post) of the graphed batched pipeline."""
     d = ctx.decimal_digits
     key = (tuple(Xt.shape), str(Xt.device if Xt.is_cuda else "host"), series.token, d, wf, s, kind, delta,
-           apply_switch, ge.engine(), complexmat.scope())
+           apply_switch, ge.engine(), complexmat.scope(), _y_low_ok(wf, s, kind == "mixed", Xt.shape[-1]))
 
     def build_pre(xstatic, capture):
         return _prepare(_lib.handle_for(), xstatic, series, ctx, wf, s, _Buckets(False), None, sync=False,

@@ -495,6 +495,14 @@ def test_y_low_precision_rule(cuda, oracle_lib):
     ctx = m.PrecisionCtx(d)
     norms = [2.5, 0.01, 2.0, 0.02]
     X = np.stack([synth(n, t, 60 + b) for b, t in enumerate(norms)])
+    engine._Y_LOW_MIN_N = 0          # the rule's size threshold (n >= 4096) lowered for the test
+    try:
+        _y_low_checks(m, engine, oracle_lib, X, norms, n, d, ctx)
+    finally:
+        engine._Y_LOW_MIN_N = 4096
+
+
+def _y_low_checks(m, engine, oracle_lib, X, norms, n, d, ctx):
     rep = m.ps_mixed_exp(X, 42, ctx)
     fm = [r.diagnostics["level_formats"] for r in rep]
     has_dd = [("dd" in f[1:]) for f in fm]
