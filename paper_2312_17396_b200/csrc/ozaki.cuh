@@ -1174,7 +1174,7 @@ __host__ __device__ constexpr double pow2c(int e) {  // compile-time 2^e
 // sum_d D_d 2^-(12+DB d) for S <= 16 as a dd (groups of three digits are
 // exact int64 -> double; group weights are compile-time constants).
 template <int S, int DB = 7>
-__device__ __forceinline__ mp::dd combine_dd(const int32_t *D) {
+__device__ __forceinline__ mp::dd combine_dd_chain(const int32_t *D) {
   mp::dd acc = mp::dd_make(0.0, 0.0);
 #pragma unroll
   for (int g = 0; g < (S + 2) / 3; ++g) {
@@ -1187,6 +1187,77 @@ __device__ __forceinline__ mp::dd combine_dd(const int32_t *D) {
     else acc = mp::dd_add_d(acc, gv);
   }
   return acc;
+}
+
+// m * 2^-q for an integer 0 <= m < 2^52, exactly: m dropped into the mantissa
+// of 2^(52-q) (one logic op on the high word) minus that power of two (one
+// DADD) -- no I2F.  `bias` is subtracted as well (signed values enter as
+// m = v + 2^51 with bias 2^(51-q)).
+template <int Q>
+__device__ __forceinline__ double u52_scaled(unsigned long long m, double bias = 0.0) {
+  constexpr unsigned long long EXPO = (unsigned long long)(1075 - Q) << 52;
+  constexpr double BASE = pow2c(52 - Q);
+  return __longlong_as_double((long long)(EXPO | m)) - (BASE + bias);
+}
+
+// The same sum through integer carries (the epilogue's FP64 work: ~10 DADD
+// instead of ~40 DADD + 5 I2F.S64 per output).  The groups of three digits,
+// weights 2^(3 DB) apart, are carry-normalised into base-2^(3 DB) digits
+// (top signed, the rest in [0, 2^(3 DB))); pairs of digits are exact doubles
+// P0 > P1 > ... that do not overlap, so FastTwoSum(P0, P1), one add of the
+// tail and a final FastTwoSum give the normalised dd of the exact sum
+// (one rounding of the low word, relative error <= 2^-105).
+template <int S, int DB = 7>
+__device__ __forceinline__ mp::dd combine_dd(const int32_t *D) {
+  constexpr int NG = (S + 2) / 3;
+  constexpr int WB = 3 * DB;
+  long long G[NG];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    const int d0 = 3 * g;
+    G[g] = (long long)D[d0] << (2 * DB);
+    if (d0 + 1 < S) G[g] += (long long)D[d0 + 1] << DB;
+    if (d0 + 2 < S) G[g] += (long long)D[d0 + 2];
+  }
+  if constexpr (NG == 1) {
+    return mp::dd_make((double)G[0] * pow2c(-(12 + DB * 2)), 0.0);
+  } else {
+    unsigned long long dig[NG];
+    long long c = 0;
+#pragma unroll
+    for (int g = NG - 1; g >= 1; --g) {
+      const long long t = G[g] + c;
+      dig[g] = (unsigned long long)t & ((1ull << WB) - 1ull);
+      c = t >> WB;
+    }
+    // |top| < 2^(31 + 2 DB + 1) <= 2^48
+    const unsigned long long top = (unsigned long long)(G[0] + c + (1ll << 51));
+    const double p0 = u52_scaled<12 + DB * 2>(top, pow2c(51 - (12 + DB * 2)));
+    // pairs (1,2), (3,4), ...; a last single digit keeps its own weight
+    constexpr int NP = (NG - 1 + 1) / 2;
+    double p[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const int a = 1 + 2 * k;
+      if (a + 1 < NG) {
+        const unsigned long long m = (dig[a] << WB) | dig[a + 1];
+        p[k] = k == 0 ? u52_scaled<12 + DB * (3 * 2 + 2)>(m)
+             : k == 1 ? u52_scaled<12 + DB * (3 * 4 + 2)>(m)
+                      : u52_scaled<12 + DB * (3 * 6 + 2)>(m);
+      } else {
+        p[k] = k == 0 ? u52_scaled<12 + DB * (3 * 1 + 2)>(dig[a])
+             : k == 1 ? u52_scaled<12 + DB * (3 * 3 + 2)>(dig[a])
+                      : u52_scaled<12 + DB * (3 * 5 + 2)>(dig[a]);
+      }
+    }
+    static_assert(NP <= 3, "combine_dd: S <= 16");
+    const double s = p0 + p[0];
+    double lo = p[0] - (s - p0);          // FastTwoSum: |p0| >= |p[0]| or p0 == 0
+    if constexpr (NP == 2) lo += p[1];
+    if constexpr (NP == 3) lo += p[1] + p[2];
+    const double hi = s + lo;             // |s| >= |lo| or s == 0
+    return mp::dd_make(hi, lo - (hi - s));
+  }
 }
 
 // fp64 value of the recombined diagonals (one rounding per group beyond the
@@ -1339,16 +1410,26 @@ __device__ __forceinline__ void oz_epilogue_db(const Args &args, const EpiPre<S,
 // spends a few instructions per MMA instead of ~150 cycles of descriptor
 // and loop arithmetic (which left the tensor pipe idle between MMAs).
 // acc0: accumulate flag of the K step's first write to every diagonal.
+// More than 256 columns are issued as equal chunks (multiples of 16 columns)
+// instead of 256 + remainder: a kind::i8 MMA costs ~0.55 clk per column down
+// to N = 112 but never less than ~60 clk (tools/mma_probe_n.py), so 288
+// columns cost 141 + 60 clk as 256 + 32 and 2 x 80 as 144 + 144 (dd, 14
+// planes: 2011 -> 1938 clk of MMAs per K step).
+__host__ __device__ constexpr int oz_chunk_w(int ncols) {
+  const int nc = (ncols + 255) / 256;
+  return ((ncols + nc - 1) / nc + 15) / 16 * 16;
+}
 template <int S, int NT, uint32_t A_SLICE, uint32_t B_SLICE>
 __device__ __forceinline__ void oz_issue_kstep(uint32_t tmem, uint64_t ad0, uint64_t bd0, uint32_t acc0) {
+  constexpr uint32_t B_ROW = B_SLICE / NT;   // bytes per B row
 #pragma unroll
   for (int s = 0; s < S; ++s) {
+    const int ncols = (S - s) * NT, cw = oz_chunk_w(ncols);
 #pragma unroll
-    for (int t0 = 0; t0 < S - s; t0 += 256 / NT) {
-      constexpr int kMaxN = 256;
-      const int nn = ((S - s - t0) * NT > kMaxN) ? kMaxN : (S - s - t0) * NT;
-      mma_i8(tmem + (uint32_t)((s + t0) * NT), ad0 + (uint64_t)((s * A_SLICE) >> 4),
-             bd0 + (uint64_t)((t0 * B_SLICE) >> 4), idesc_i8(kTileM, nn), s > 0 ? 1u : acc0);
+    for (int c0 = 0; c0 < ncols; c0 += cw) {
+      const int nn = ncols - c0 > cw ? cw : ncols - c0;
+      mma_i8(tmem + (uint32_t)(s * NT + c0), ad0 + (uint64_t)((s * A_SLICE) >> 4),
+             bd0 + (uint64_t)((c0 * B_ROW) >> 4), idesc_i8(kTileM, nn), s > 0 ? 1u : acc0);
     }
   }
 }
@@ -1606,8 +1687,11 @@ __device__ __forceinline__ void oz_kernel_epilogue(const OzTmaArgs &args, double
       if constexpr (oz_has7<S>())
         oz_stage_compute<S, NT, FO, MODE, 7, SCW>(args, ebuf, ebs, tmem, quarter, cb, ce, b, m0, lane);
     }
+    if (tr) tr[5] = globaltimer();
     __syncthreads();
+    if (tr) tr[6] = globaltimer();
     oz_stage_store<FO, NT, EW>(args.C, ebuf, args.M, args.N, b, m0, n0, warp, lane);
+    if (tr) tr[7] = globaltimer();
   } else {
     EpiPre<S, NT, FO, MODE> pre;
     oz_epi_prefetch<S, NT, FO, MODE>(args, pre, quarter, cb, ce, b, m0, n0, lane);
@@ -1668,7 +1752,7 @@ __device__ __forceinline__ void oz_kernel_epilogue_chunked(const OzTmaArgs &args
 __device__ __forceinline__ unsigned long long *oz_trace_begin(const OzTmaArgs &args) {
   if (!args.trace || threadIdx.x != 64) return nullptr;
   unsigned long long *tr =
-      args.trace + 5ull * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+      args.trace + 8ull * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
   tr[0] = globaltimer();
   tr[4] = smid();
   return tr;
@@ -1768,13 +1852,15 @@ __global__ void __launch_bounds__(32 * EW, EW == 8 ? oz_ctas_per_sm<S, MODE, NT>
 // at ad0 + (s - s0) * A_SLICE), fully unrolled like oz_issue_kstep.
 template <int S, int NT, uint32_t A_SLICE, uint32_t B_SLICE, int S0, int SG>
 __device__ __forceinline__ void oz_issue_planes(uint32_t tmem, uint64_t ad0, uint64_t bd0, uint32_t acc0) {
+  constexpr uint32_t B_ROW = B_SLICE / NT;   // bytes per B row
 #pragma unroll
   for (int s = S0; s < S0 + SG && s < S; ++s) {
+    const int ncols = (S - s) * NT, cw = oz_chunk_w(ncols);
 #pragma unroll
-    for (int t0 = 0; t0 < S - s; t0 += 256 / NT) {
-      const int nn = ((S - s - t0) * NT > 256) ? 256 : (S - s - t0) * NT;
-      mma_i8(tmem + (uint32_t)((s + t0) * NT), ad0 + (uint64_t)(((s - S0) * A_SLICE) >> 4),
-             bd0 + (uint64_t)((t0 * B_SLICE) >> 4), idesc_i8(kTileM, nn), s > 0 ? 1u : acc0);
+    for (int c0 = 0; c0 < ncols; c0 += cw) {
+      const int nn = ncols - c0 > cw ? cw : ncols - c0;
+      mma_i8(tmem + (uint32_t)(s * NT + c0), ad0 + (uint64_t)(((s - S0) * A_SLICE) >> 4),
+             bd0 + (uint64_t)((c0 * B_ROW) >> 4), idesc_i8(kTileM, nn), s > 0 ? 1u : acc0);
     }
   }
 }
@@ -1867,14 +1953,17 @@ __global__ void __launch_bounds__(32 * EW, 1) oz_gemm_ring_kernel(const __grid_c
     for (int kb = 0; kb < ksteps; ++kb) {
       const int bst = kb % R::NBS;
       if (kb >= R::NBS) mbar_wait(smem_u32(&b_empty[bst]), ((kb / R::NBS) - 1) & 1);
-      mbar_expect_tx(smem_u32(&b_full[bst]), R::B_BYTES);
-      tma_load_3d(smem_u32(bring + bst * R::B_STRIDE), &args.mapB, kb * kKStep, rowB, 0, smem_u32(&b_full[bst]));
+      const bool feed = !(args.dbg & 2);   // diagnostics: MMA-only run (no loads)
+      mbar_expect_tx(smem_u32(&b_full[bst]), feed ? R::B_BYTES : 0);
+      if (feed)
+        tma_load_3d(smem_u32(bring + bst * R::B_STRIDE), &args.mapB, kb * kKStep, rowB, 0, smem_u32(&b_full[bst]));
       for (int g = 0; g < R::NG; ++g, ++ai) {
         const int ast = ai % R::NAS;
         if (ai >= R::NAS) mbar_wait(smem_u32(&a_empty[ast]), ((ai / R::NAS) - 1) & 1);
-        mbar_expect_tx(smem_u32(&a_full[ast]), R::A_BYTES);
-        tma_load_3d(smem_u32(aring + ast * R::A_BYTES), &args.mapA, kb * kKStep, rowA, g * R::SG,
-                    smem_u32(&a_full[ast]));
+        mbar_expect_tx(smem_u32(&a_full[ast]), feed ? R::A_BYTES : 0);
+        if (feed)
+          tma_load_3d(smem_u32(aring + ast * R::A_BYTES), &args.mapA, kb * kKStep, rowA, g * R::SG,
+                      smem_u32(&a_full[ast]));
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -1884,6 +1973,12 @@ __global__ void __launch_bounds__(32 * EW, 1) oz_gemm_ring_kernel(const __grid_c
       const int bst = kb % R::NBS;
       mbar_wait(smem_u32(&b_full[bst]), (kb / R::NBS) & 1);
       const uint32_t sb = smem_u32(bring + bst * R::B_STRIDE);
+      if (args.dbg & 1) {                  // diagnostics: feed-only run (no MMAs)
+        for (int g = 0; g < R::NG; ++g, ++ai) {
+          mbar_wait(smem_u32(&a_full[ai % R::NAS]), (ai / R::NAS) & 1);
+          mma_commit(smem_u32(&a_empty[ai % R::NAS]));
+        }
+      } else
       oz_ring_groups<S, NT, A_SLICE, B_SLICE, R::SG>(tmem, umma_desc(sb, 16, 256, 6), kb > 0 ? 1u : 0u, ai, aring,
                                                       a_full, a_empty, R::NAS, R::A_BYTES);
       mma_commit(smem_u32(&b_empty[bst]));
@@ -1944,11 +2039,12 @@ struct OzWide {
 // MMAs of plane s for K step kk of a stage: A_s x [B_0 .. B_{S-1-s}]
 template <int S, int NT, int s>
 __device__ __forceinline__ void oz_wide_plane(uint32_t tmem, uint64_t ad, uint64_t bd0, uint32_t acc) {
-  constexpr uint32_t B_PLANE = OzWide<S, NT>::B_PLANE;
+  constexpr uint32_t B_ROW = OzWide<S, NT>::KB;   // bytes per B row (128-byte swizzle atoms of 8 rows)
+  constexpr int ncols = (S - s) * NT, cw = oz_chunk_w(ncols);
 #pragma unroll
-  for (int t0 = 0; t0 < S - s; t0 += 256 / NT) {
-    const int nn = ((S - s - t0) * NT > 256) ? 256 : (S - s - t0) * NT;
-    mma_i8(tmem + (uint32_t)((s + t0) * NT), ad, bd0 + (uint64_t)((t0 * B_PLANE) >> 4), idesc_i8(kTileM, nn),
+  for (int c0 = 0; c0 < ncols; c0 += cw) {
+    const int nn = ncols - c0 > cw ? cw : ncols - c0;
+    mma_i8(tmem + (uint32_t)(s * NT + c0), ad, bd0 + (uint64_t)((c0 * B_ROW) >> 4), idesc_i8(kTileM, nn),
            s > 0 ? 1u : acc);
   }
 }

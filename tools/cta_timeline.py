@@ -13,12 +13,12 @@ B, n = 64, 256
 
 
 def run(label, fn, nctas):
-    buf = torch.zeros(nctas * 5, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(nctas * 8, dtype=torch.int64, device="cuda")
     fn(); torch.cuda.synchronize()
     lib.mpps_debug_oz_trace(buf.data_ptr())
     fn(); torch.cuda.synchronize()
     lib.mpps_debug_oz_trace(None)
-    t = buf.view(nctas, 5).cpu().numpy()
+    t = buf.view(nctas, 8).cpu().numpy()
     t0 = t[:, 0].min()
     st, su, dn, en, sm = (t[:, i] - (t0 if i < 4 else 0) for i in range(5))
     span = en.max()
@@ -27,6 +27,18 @@ def run(label, fn, nctas):
           f"setup {np.median(su - st)/1e3:.2f} us, mainloop {np.median(dn - su)/1e3:.2f} us, "
           f"epilogue {np.median(en - dn)/1e3:.2f} us, CTA total {np.median(en - st)/1e3:.2f} us; "
           f"start-time spread: first wave ends {np.sort(en)[147]/1e3:.1f} us", flush=True)
+    if t[:, 5].any():
+        c5, c6, c7 = (t[:, i] - t0 for i in (5, 6, 7))
+        print(f"    epilogue (thread 64): combine {np.median(c5 - dn)/1e3:.2f} us, sync {np.median(c6 - c5)/1e3:.2f} us, "
+              f"store {np.median(c7 - c6)/1e3:.2f} us, exit sync {np.median(en - c7)/1e3:.2f} us", flush=True)
+    # gaps between consecutive CTAs of one SM
+    gaps = []
+    for m in np.unique(sm):
+        idx = np.where(sm == m)[0]
+        o = idx[np.argsort(st[idx])]
+        gaps += list(st[o][1:] - en[o][:-1])
+    if gaps:
+        print(f"    gap between consecutive CTAs of an SM: median {np.median(gaps)/1e3:.2f} us", flush=True)
     # concurrency: average CTAs resident
     ev = np.concatenate([np.stack([st, np.ones_like(st)], 1), np.stack([en, -np.ones_like(en)], 1)])
     ev = ev[np.argsort(ev[:, 0], kind="stable")]
@@ -46,6 +58,11 @@ ys = h.slice(Y, 0, 16)
 ysb = h.slice(Y, 1, 16)
 ps4, ps8 = h.slice(P, 1, 4), h.slice(P64, 1, 8)
 nct = B * (n // 128) * (n // 32)
+ys14, ysb14 = h.slice(Y, 0, 14, None, 8), h.slice(Y, 1, 14, None, 8)
+run("S=14 (8-bit) gemm dd", lambda: h.gemm_sliced(ys14, ysb14, 14, o128), nct)
+run("S=14 (8-bit) horner dd", lambda: h.horner_step_sliced(ys14, ysb14, 14, Bp, o128, fmt_in=31), nct)
+if len(sys.argv) > 1:
+    sys.exit(0)
 run("S=16 gemm dd", lambda: h.gemm_sliced(ys, ysb, 16, o128), nct)
 run("S=16 horner dd", lambda: h.horner_step_sliced(ys, ysb, 16, Bp, o128, fmt_in=31), nct)
 run("S=8 horner fp64", lambda: h.horner_step_sliced(ys, ps8, 8, Bp, o64, fmt_in=15), nct)

@@ -8,7 +8,7 @@ h = _lib.handle_for()
 scratch = torch.zeros(16, dtype=torch.int32, device="cuda")
 iters = 20000
 clk = 1.965e9
-for n in (16, 32, 64, 96, 128, 160, 192, 224, 256):
+for n in range(16, 257, 16):
     h.lib.mpps_debug_probe_i8mma_n(h.h, 148, 100, n, scratch.data_ptr())
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
