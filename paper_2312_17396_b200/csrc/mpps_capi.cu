@@ -1818,6 +1818,46 @@ static int launch_oz_pwide(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
   return after_launch(h, "oz_gemm_pwide_kernel");
 }
 
+// Persistent 128-byte-box kernel with 16 epilogue warps for the 8-bit dd
+// products below the CTA-pair wide kernel's K range (MPPS_OZ_PW16=0 restores
+// the 32-byte-box ring kernel there).
+template <int S, int NT, int DB>
+static int launch_oz_pw16(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
+  constexpr size_t smem = oz::OzPw16<S, NT>::SMEM;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_pw16_kernel<S, NT, DB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz pw16 attr: %s", cudaGetErrorString(e));
+    configured = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  oz::OzTmaArgs t = a;
+  t.mtiles = (a.M + oz::kTileM - 1) / oz::kTileM;
+  t.ntiles = (a.N + NT - 1) / NT;
+  t.group = oz_group();
+  t.nbatch = nb;
+  if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
+  const long long tiles = (long long)nb * t.mtiles * t.ntiles;
+  launch_k(oz::oz_gemm_pw16_kernel<S, NT, DB>, dim3((unsigned)(tiles < sms ? tiles : sms)), dim3(oz::kThreadsPw16), smem,
+           h->stream, t);
+  return after_launch(h, "oz_gemm_pw16_kernel");
+}
+static bool oz_pw16_for(int S, int fo, int mode, int K, int db) {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MPPS_OZ_PW16");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0 && S == 14 && db == 8 && fo == DD && mode == 0 && K < 4096;
+}
+
 // persistent double-buffered kernel for the dd power-chain GEMMs:
 // MPPS_OZ_PERS = 0 (default) off, 1 single CTAs, 2 CTA pairs multicasting A, 3 persistent with 128-byte K
 // boxes (oz_gemm_pwide_kernel); measured no faster than the ring kernel (DESIGN 5.1)
@@ -1933,7 +1973,8 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   oz::OzTmaArgs t;
   memset(&t, 0, sizeof(t));
   const bool wide = oz_wide_for(S, fo, mode, a.K);
-  const int pmode = wide ? 0 : oz_pers_mode(S, fo, mode);
+  const bool pw16 = !wide && oz_pw16_for(S, fo, mode, a.K, slice_db(A));
+  const int pmode = (wide || pw16) ? 0 : oz_pers_mode(S, fo, mode);
   const bool pers = pmode != 0;
   // default: streamed-plane ring for dd / qd (S >= 16), 2-4 stage TMA ring below
   const bool ring = pers || oz_mode() == 2 || (oz_mode() == 3 && S >= 14) || S == 14 || S == 28;
@@ -1942,7 +1983,7 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   const int NT = wide ? oz_wide_nt(S, mode) : (S > 16 || pers) ? 16 : (nt128 ? 128 : nt64 ? 64 : 32);
   const int abox = ring ? (S < 4 ? S : (S == 14 ? 7 : 4)) : S;   // OzRing<S, NT>::SG
   int rc;
-  if (wide || pmode == 3) {
+  if (wide || pmode == 3 || pw16) {
     if ((rc = make_slice_map(h, &t.mapA, A, oz::kTileM, 1, 128)) || (rc = make_slice_map(h, &t.mapB, B, NT, S, 128)))
       return rc;
   } else if ((rc = make_slice_map(h, &t.mapA, A, oz::kTileM, abox)) || (rc = make_slice_map(h, &t.mapB, B, NT, S))) {
@@ -1952,6 +1993,7 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   t.trace = g_oz_trace;
   t.dbg = g_oz_dbg;
   if (wide) return dispatch_oz_wide(h, S, fo, mode, t, nb);
+  if (pw16) return launch_oz_pw16<14, 32, 8>(h, t, nb);
   if (pmode == 3) return launch_oz_pwide<16, 16, DD, 0>(h, t, nb);
   if (pmode == 1) return launch_oz_pers<16, 16, DD, 0, 1>(h, t, nb);
   if (pmode == 2) return launch_oz_pers<16, 16, DD, 0, 2>(h, t, nb);

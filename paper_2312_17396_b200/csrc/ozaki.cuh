@@ -2535,6 +2535,175 @@ __global__ void __launch_bounds__(kThreadsPers, 1) oz_gemm_pwide_kernel(const __
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
+// ------------- persistent, 128-byte K boxes, one accumulator set, 16 epilogue warps
+// The dd products of the power chain at small and medium K (cfg2: K = 256,
+// cfg3: K = 1024).  Per 128 x 32 tile the 32-byte-box ring kernel spends
+// 0.2 us of set-up, a mainloop bound by its feed (12.4 us at K = 256 where
+// the MMAs alone take 9), 3.9 us of epilogue and 1.15 us until the SM's next
+// CTA starts (tools/cta_timeline.py).  Here one CTA per SM walks the tiles:
+// the producer streams the next tile's planes (128-byte boxes) while the
+// epilogue drains the accumulators, so a tile's MMAs start on a full ring;
+// the 14 x 32 accumulators fill TMEM, so the MMAs of tile i+1 wait for the
+// epilogue's last TMEM load of tile i (signalled before its arithmetic and
+// stores of the last columns).  Warp 0: TMA producer, warp 1: MMA issuer,
+// warps 2..17: epilogue (TMEM lane quarter = warp % 4, 8 columns each).
+constexpr int kThreadsPw16 = 576;
+
+template <int S, int NT>
+struct OzPw16 {
+  using W = OzWide<S, NT>;
+  static constexpr int NBS = 2;
+  static constexpr int NAS_FIT = (int)((226ll * 1024 - 2048 - NBS * (long long)W::B_STRIDE) / W::A_BYTES);
+  static constexpr int NAS = NAS_FIT > 8 ? 8 : NAS_FIT;
+  static constexpr int ACC = S * NT;
+  static_assert(ACC <= 512 && NT == 32, "one accumulator set of S x 32 columns");
+  static constexpr size_t SMEM = (size_t)NBS * W::B_STRIDE + (size_t)NAS * W::A_BYTES + 2048;
+};
+
+template <int S, int NT, int DB>
+__global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __grid_constant__ OzTmaArgs args) {
+  MPPS_PDL_ENTER();
+  using W = OzWide<S, NT>;
+  using P = OzPw16<S, NT>;
+  constexpr int NAS = P::NAS;
+  static_assert(NAS >= 4, "A ring does not fit");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t *bring = smem;
+  uint8_t *aring = smem + P::NBS * W::B_STRIDE;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(aring + NAS * W::A_BYTES);
+  uint64_t *b_full = bar, *b_empty = bar + P::NBS;
+  uint64_t *a_full = bar + 2 * P::NBS, *a_empty = a_full + NAS;
+  uint64_t *acc_full = a_empty + NAS, *acc_empty = acc_full + 1;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int kpad = args.A.kpad;
+  const int kstages = (kpad + W::KB - 1) / W::KB;
+  const int total = args.nbatch * args.mtiles * args.ntiles;
+
+  if (warp == 0) tmem_alloc<512>(smem_u32(tmem_slot));
+  if (tid == 32) {
+    for (int i = 0; i < P::NBS; ++i) { mbar_init(smem_u32(&b_full[i]), 1); mbar_init(smem_u32(&b_empty[i]), 1); }
+    for (int i = 0; i < NAS; ++i) { mbar_init(smem_u32(&a_full[i]), 1); mbar_init(smem_u32(&a_empty[i]), 1); }
+    mbar_init(smem_u32(acc_full), 1);
+    mbar_init(smem_u32(acc_empty), 16);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer (ring positions continue across tiles)
+      int kg = 0, ai = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        int bz, m0, n0;
+        oz_pers_tile<1>(args, t, NT, 0, bz, m0, n0);
+        const int b = args.sel ? args.sel[bz] : bz;
+        const int rowA = b * args.A.rpad + m0, rowB = b * args.B.rpad + n0;
+        for (int kb = 0; kb < kstages; ++kb, ++kg) {
+          const int bst = kg % P::NBS;
+          if (kg >= P::NBS) mbar_wait(smem_u32(&b_empty[bst]), ((kg / P::NBS) - 1) & 1);
+          mbar_expect_tx(smem_u32(&b_full[bst]), W::B_BYTES);
+          tma_load_3d(smem_u32(bring + bst * W::B_STRIDE), &args.mapB, kb * W::KB, rowB, 0, smem_u32(&b_full[bst]));
+          for (int s = 0; s < S; ++s, ++ai) {
+            const int ast = ai % NAS;
+            if (ai >= NAS) mbar_wait(smem_u32(&a_empty[ast]), ((ai / NAS) - 1) & 1);
+            mbar_expect_tx(smem_u32(&a_full[ast]), W::A_BYTES);
+            tma_load_3d(smem_u32(aring + ast * W::A_BYTES), &args.mapA, kb * W::KB, rowA, s, smem_u32(&a_full[ast]));
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- MMA issuer
+      int kg = 0, ai = 0, i = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
+        if (i >= 1) mbar_wait(smem_u32(acc_empty), (i - 1) & 1);   // the epilogue has read tile i-1 out of TMEM
+        fence_after();
+        for (int kb = 0; kb < kstages; ++kb, ++kg) {
+          const int bst = kg % P::NBS;
+          mbar_wait(smem_u32(&b_full[bst]), (kg / P::NBS) & 1);
+          fence_after();
+          const int left = (kpad - kb * W::KB) / kKStep;
+          const int nk = left < 4 ? left : 4;
+          oz_wide_stage<S, NT>(tmem, smem_u32(bring + bst * W::B_STRIDE), nk, kb > 0 ? 1u : 0u, ai, aring, a_full,
+                               a_empty, NAS);
+          mma_commit(smem_u32(&b_empty[bst]));
+        }
+        mma_commit(smem_u32(acc_full));
+      }
+    }
+  } else {
+    // ---- epilogue warps: thread = tile row, 8 columns in two loads of 4
+    const int quarter = warp & 3, cb = ((warp - 2) >> 2) * 8;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    const MatRef &C = args.C;
+    int i = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
+      int bz, m0, n0;
+      oz_pers_tile<1>(args, t, NT, 0, bz, m0, n0);
+      const int b = args.sel ? args.sel[bz] : bz;
+      const int row = m0 + quarter * 32 + lane;
+      const int col0 = n0 + cb;
+      const int ea = row < args.M ? args.A.exps[(long long)b * args.A.rpad + row] : 0;
+      int eb[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) eb[j] = col0 + j < args.N ? args.B.exps[(long long)b * args.B.rpad + col0 + j] : 0;
+      mbar_wait(smem_u32(acc_full), i & 1);
+      fence_after();
+      double hi[8], lo[8];
+#pragma unroll
+      for (int i0 = 0; i0 < 8; i0 += 4) {
+        int32_t D[S][4];
+#pragma unroll
+        for (int d = 0; d < S; ++d) tmem_ld4(lane_base + (uint32_t)(d * NT + cb + i0), D[d]);
+        tmem_ld_wait();
+        if (i0 == 4) {
+          // every accumulator of this warp's part is in registers: the next
+          // tile's MMAs may overwrite TMEM while the last columns are combined
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(acc_empty));
+        }
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          int32_t Dj[S];
+#pragma unroll
+          for (int d = 0; d < S; ++d) Dj[d] = D[d][jj];
+          const mp::dd v = combine_dd<S, DB>(Dj);
+          const double sc = pow2i(ea + eb[i0 + jj]);
+          hi[i0 + jj] = v.hi * sc;
+          lo[i0 + jj] = v.lo * sc;
+        }
+      }
+      if (row < args.M) {
+        double *p = (double *)C.data + (long long)b * C.bstride + (long long)row * C.ld + col0;
+        double *q = p + C.plane;
+        if (col0 + 8 <= args.N && ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(q)) & 15) == 0) {
+#pragma unroll
+          for (int j = 0; j < 8; j += 2) {
+            *reinterpret_cast<double2 *>(p + j) = make_double2(hi[j], hi[j + 1]);
+            *reinterpret_cast<double2 *>(q + j) = make_double2(lo[j], lo[j + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (col0 + j < args.N) { p[j] = hi[j]; q[j] = lo[j]; }
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
 // Global -> shared ingest probe: one CTA per SM streams 16 KB bulk copies
 // (the TMA engine, 8 in flight) from an L2-resident buffer; the tensor-core
 // GEMMs are bound by this per-SM fill rate (~25 B/clk with every SM
