@@ -1821,12 +1821,12 @@ static int launch_oz_pwide(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
 // Persistent 128-byte-box kernel with 16 epilogue warps for the 8-bit dd
 // products below the CTA-pair wide kernel's K range (MPPS_OZ_PW16=0 restores
 // the 32-byte-box ring kernel there).
-template <int S, int NT, int DB>
+template <int S, int NT, int DB, int SGP>
 static int launch_oz_pw16(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
-  constexpr size_t smem = oz::OzPw16<S, NT>::SMEM;
+  constexpr size_t smem = oz::OzPw16<S, NT, SGP>::SMEM;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_pw16_kernel<S, NT, DB>,
+    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_pw16_kernel<S, NT, DB, SGP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz pw16 attr: %s", cudaGetErrorString(e));
     configured = true;
@@ -1845,7 +1845,7 @@ static int launch_oz_pw16(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
   t.nbatch = nb;
   if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
   const long long tiles = (long long)nb * t.mtiles * t.ntiles;
-  launch_k(oz::oz_gemm_pw16_kernel<S, NT, DB>, dim3((unsigned)(tiles < sms ? tiles : sms)), dim3(oz::kThreadsPw16), smem,
+  launch_k(oz::oz_gemm_pw16_kernel<S, NT, DB, SGP>, dim3((unsigned)(tiles < sms ? tiles : sms)), dim3(oz::kThreadsPw16), smem,
            h->stream, t);
   return after_launch(h, "oz_gemm_pw16_kernel");
 }
@@ -1855,7 +1855,7 @@ static bool oz_pw16_for(int S, int fo, int mode, int K, int db) {
     const char *e = getenv("MPPS_OZ_PW16");
     v = e ? atoi(e) : 1;
   }
-  return v != 0 && S == 14 && db == 8 && fo == DD && mode == 0 && K < 4096;
+  return v != 0 && S == 14 && db == 8 && fo == DD && mode == 0 && (K < 4096 || v == 2);   // 2: every K (diagnostics)
 }
 
 // persistent double-buffered kernel for the dd power-chain GEMMs:
@@ -1972,8 +1972,8 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   if (oz_mode() == 0) return dispatch_oz(h, S, fo, mode, a, nb);
   oz::OzTmaArgs t;
   memset(&t, 0, sizeof(t));
-  const bool wide = oz_wide_for(S, fo, mode, a.K);
-  const bool pw16 = !wide && oz_pw16_for(S, fo, mode, a.K, slice_db(A));
+  const bool pw16 = oz_pw16_for(S, fo, mode, a.K, slice_db(A));
+  const bool wide = !pw16 && oz_wide_for(S, fo, mode, a.K);
   const int pmode = (wide || pw16) ? 0 : oz_pers_mode(S, fo, mode);
   const bool pers = pmode != 0;
   // default: streamed-plane ring for dd / qd (S >= 16), 2-4 stage TMA ring below
@@ -1993,7 +1993,7 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   t.trace = g_oz_trace;
   t.dbg = g_oz_dbg;
   if (wide) return dispatch_oz_wide(h, S, fo, mode, t, nb);
-  if (pw16) return launch_oz_pw16<14, 32, 8>(h, t, nb);
+  if (pw16) return a.K >= 1024 ? launch_oz_pw16<14, 32, 8, 2>(h, t, nb) : launch_oz_pw16<14, 32, 8, 1>(h, t, nb);
   if (pmode == 3) return launch_oz_pwide<16, 16, DD, 0>(h, t, nb);
   if (pmode == 1) return launch_oz_pers<16, 16, DD, 0, 1>(h, t, nb);
   if (pmode == 2) return launch_oz_pers<16, 16, DD, 0, 2>(h, t, nb);
@@ -2184,12 +2184,16 @@ int mpps_probe_ingest(mpps_handle *h, int blocks, int iters, const void *src, lo
   return after_launch(h, "ingest_probe_kernel");
 }
 
-int mpps_debug_probe_i8mma_n(mpps_handle *h, int blocks, int iters, int n, void *scratch) {
-  if (!scratch || blocks < 1 || iters < 1 || n < 16 || n > 256 || n % 16)
+int mpps_debug_probe_i8mma_n(mpps_handle *h, int blocks, int iters, int n_acc, void *scratch) {
+  // n_acc: N | (independent accumulators - 1) << 16
+  // bits 24..: issuing threads - 1 (then one accumulator per issuer)
+  const int n = n_acc & 0xffff, nis = (n_acc >> 24) + 1;
+  const int nacc = nis > 1 ? -nis : ((n_acc >> 16) & 0xff) + 1;
+  if (!scratch || blocks < 1 || iters < 1 || n < 16 || n > 256 || n % 16 || (nacc < 0 ? nis : nacc) * n > 512 || nis > 4)
     return set_err(h, MPPS_EINVAL, "probe: bad arguments");
   int rc = mpps_probe_i8mma(h, blocks, 1, scratch);  // configures the kernel attribute
   if (rc) return rc;
-  oz::i8_mma_probe_kernel<<<blocks, 128, 40960 + 2048, h->stream>>>(iters, (int *)scratch, n);
+  oz::i8_mma_probe_kernel<<<blocks, 128, 40960 + 2048, h->stream>>>(iters, (int *)scratch, n, nacc);
   return after_launch(h, "i8_mma_probe_kernel");
 }
 

@@ -2021,10 +2021,22 @@ __device__ __forceinline__ void mma_commit_mc(uint32_t mbar, uint16_t mask) {
 // 32-byte K step selected by +32 B on the descriptor start address).
 // B: all S planes of NT rows x 128 B per stage (2 stages); A: one plane of
 // 128 rows x 128 B per ring slot, its 4 K steps of MMAs issued back to back.
-template <int S, int NT>
+// A ring slots hold SG = 2 planes for even S >= 14 (the pair (j, S-1-j) of
+// the issue order below, two TMA loads on one barrier): half the barrier
+// waits, fences and tcgen05.commit of the issuing thread, which costs ~70 clk
+// per instruction.
+#ifndef MPPS_OZ_SLOT_PLANES
+#define MPPS_OZ_SLOT_PLANES 2
+#endif
+template <int S>
+__host__ __device__ constexpr int oz_slot_planes() { return (MPPS_OZ_SLOT_PLANES == 2 && S % 2 == 0 && S >= 14) ? 2 : 1; }
+template <int S, int NT, int SGP = oz_slot_planes<S>()>
 struct OzWide {
   static constexpr int KB = 128;                                  // K bytes per stage
-  static constexpr uint32_t A_BYTES = kTileM * KB;                // 16 KB: one plane
+  static constexpr int SG = SGP;
+  static constexpr int NSLOT = S / SG;                            // ring slots per stage
+  static constexpr uint32_t A_PLANE = kTileM * KB;                // 16 KB: one plane
+  static constexpr uint32_t A_BYTES = SG * A_PLANE;
   static constexpr uint32_t B_PLANE = NT * KB;                    // bytes per B plane
   static constexpr uint32_t B_BYTES = S * B_PLANE;
   static constexpr uint32_t B_STRIDE = (B_BYTES + 1023) / 1024 * 1024;
@@ -2032,7 +2044,7 @@ struct OzWide {
   template <uint32_t EBUF>
   __host__ __device__ static constexpr int nas() {
     constexpr long long room = 225ll * 1024 - 2048 - (long long)EBUF - NBS * (long long)B_STRIDE;
-    return room / A_BYTES > 8 ? 8 : (int)(room / A_BYTES);
+    return room / A_BYTES > 8 / SG ? 8 / SG : (int)(room / A_BYTES);
   }
 };
 
@@ -2049,25 +2061,47 @@ __device__ __forceinline__ void oz_wide_plane(uint32_t tmem, uint64_t ad, uint64
   }
 }
 
-template <int S, int NT, int CL = 1, int s = 0>
+// Order in which the A planes of a stage are loaded and issued: low and high
+// planes alternate (0, S-1, 1, S-2, ...).  One thread issues every MMA and
+// spends ~70 clk per tcgen05.mma / tcgen05.commit whatever the shape
+// (tools/mma_probe_n.py: two issuing threads reach 42 clk at N = 32), so a
+// run of narrow planes (s >= S-4: N <= 128 columns, 42-71 clk of tensor
+// pipe each) leaves the pipe idle; next to a wide plane (N = 448: 247 clk)
+// the issue time of the narrow one hides behind the queued wide MMAs.
+// Plane 0 stays first (it initialises every accumulator of a tile).
+#ifndef MPPS_OZ_INTERLEAVE
+#define MPPS_OZ_INTERLEAVE 1
+#endif
+template <int S>
+__host__ __device__ constexpr int oz_plane_at(int i) {
+  return MPPS_OZ_INTERLEAVE ? ((i & 1) ? S - 1 - i / 2 : i / 2) : i;
+}
+
+template <int S, int NT, int CL = 1, int j = 0, int SGP = oz_slot_planes<S>()>
 __device__ __forceinline__ void oz_wide_stage(uint32_t tmem, uint32_t sb, int nk, uint32_t acc0, int &ai,
                                               uint8_t *aring, uint64_t *a_full, uint64_t *a_empty, int nas) {
-  if constexpr (s < S) {
+  using W = OzWide<S, NT, SGP>;
+  if constexpr (j < W::NSLOT) {
+    constexpr int s0 = oz_plane_at<S>(j * W::SG), s1 = oz_plane_at<S>(j * W::SG + W::SG - 1);
     const int ast = ai % nas;
     mbar_wait(smem_u32(&a_full[ast]), (ai / nas) & 1);
     fence_after();
-    const uint32_t sa = smem_u32(aring + ast * OzWide<S, NT>::A_BYTES);
+    const uint32_t sa = smem_u32(aring + ast * W::A_BYTES);
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk)
-      if (kk < nk)
-        oz_wide_plane<S, NT, s>(tmem, umma_desc(sa + kk * 32, 16, 1024, 2), umma_desc(sb + kk * 32, 16, 1024, 2),
-                                kk > 0 ? 1u : acc0);
+      if (kk < nk) {
+        oz_wide_plane<S, NT, s0>(tmem, umma_desc(sa + kk * 32, 16, 1024, 2), umma_desc(sb + kk * 32, 16, 1024, 2),
+                                 kk > 0 ? 1u : acc0);
+        if constexpr (W::SG == 2)
+          oz_wide_plane<S, NT, s1>(tmem, umma_desc(sa + W::A_PLANE + kk * 32, 16, 1024, 2),
+                                   umma_desc(sb + kk * 32, 16, 1024, 2), kk > 0 ? 1u : acc0);
+      }
     // the slot is refilled by a multicast into every CTA of the pair: it is
     // free only when all of their MMAs have read it
     if constexpr (CL == 1) mma_commit(smem_u32(&a_empty[ast]));
     else mma_commit_mc(smem_u32(&a_empty[ast]), (uint16_t)((1u << CL) - 1u));
     ++ai;
-    oz_wide_stage<S, NT, CL, s + 1>(tmem, sb, nk, acc0, ai, aring, a_full, a_empty, nas);
+    oz_wide_stage<S, NT, CL, j + 1, SGP>(tmem, sb, nk, acc0, ai, aring, a_full, a_empty, nas);
   }
 }
 
@@ -2142,15 +2176,19 @@ __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_wide_kernel(const __gr
       if (kb >= W::NBS) mbar_wait(smem_u32(&b_empty[bst]), ((kb / W::NBS) - 1) & 1);
       mbar_expect_tx(smem_u32(&b_full[bst]), W::B_BYTES);
       tma_load_3d(smem_u32(bring + bst * W::B_STRIDE), &args.mapB, kb * W::KB, rowB, 0, smem_u32(&b_full[bst]));
-      for (int s = 0; s < S; ++s, ++ai) {
+      for (int j = 0; j < W::NSLOT; ++j, ++ai) {
         const int ast = ai % NAS;
         if (ai >= NAS) mbar_wait(smem_u32(&a_empty[ast]), ((ai / NAS) - 1) & 1);
         mbar_expect_tx(smem_u32(&a_full[ast]), W::A_BYTES);
-        if constexpr (CL == 1)
-          tma_load_3d(smem_u32(aring + ast * W::A_BYTES), &args.mapA, kb * W::KB, rowA, s, smem_u32(&a_full[ast]));
-        else if (s % CL == rank)
-          tma_load_3d_mc(smem_u32(aring + ast * W::A_BYTES), &args.mapA, kb * W::KB, rowA, s, smem_u32(&a_full[ast]),
-                         (uint16_t)((1u << CL) - 1u));
+#pragma unroll
+        for (int q = 0; q < W::SG; ++q) {
+          const int pl = oz_plane_at<S>(j * W::SG + q);
+          const uint32_t dst = smem_u32(aring + ast * W::A_BYTES + q * W::A_PLANE);
+          if constexpr (CL == 1)
+            tma_load_3d(dst, &args.mapA, kb * W::KB, rowA, pl, smem_u32(&a_full[ast]));
+          else if (j % CL == rank)
+            tma_load_3d_mc(dst, &args.mapA, kb * W::KB, rowA, pl, smem_u32(&a_full[ast]), (uint16_t)((1u << CL) - 1u));
+        }
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -2372,7 +2410,7 @@ __global__ void __launch_bounds__(kThreadsPers, 1) oz_gemm_pers_kernel(const __g
 // INT8 tensor-pipe peak probe: one CTA per SM issues back-to-back
 // 128x256x32 kind::i8 MMAs (operands: 40 KB of zeroed shared memory) into a
 // 256-column TMEM accumulator.  2*128*256*32 ops per MMA.
-__global__ void __launch_bounds__(128, 1) i8_mma_probe_kernel(int iters, int *out, int n = 256) {
+__global__ void __launch_bounds__(128, 1) i8_mma_probe_kernel(int iters, int *out, int n = 256, int nacc = 1) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t *done = reinterpret_cast<uint64_t *>(smem + 40960);
@@ -2384,9 +2422,11 @@ __global__ void __launch_bounds__(128, 1) i8_mma_probe_kernel(int iters, int *ou
     x ^= x >> 15; x *= 2246822519u; x ^= x >> 13;
     reinterpret_cast<uint32_t *>(smem)[i] = x;
   }
-  if (threadIdx.x < 32) tmem_alloc<256>(smem_u32(slot));
+  if (threadIdx.x < 32) tmem_alloc<512>(smem_u32(slot));
+  // nacc < 0: -nacc issuing threads (lane 0 of warps 0..), one accumulator each
+  const int nissue = nacc < 0 ? -nacc : 1;
   if (threadIdx.x == 32) {
-    mbar_init(smem_u32(done), 1);
+    mbar_init(smem_u32(done), nissue);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   fence_proxy_async();
@@ -2394,11 +2434,25 @@ __global__ void __launch_bounds__(128, 1) i8_mma_probe_kernel(int iters, int *ou
   __syncthreads();
   fence_after();
   const uint32_t tmem = *slot;
-  if (threadIdx.x == 0) {
+  if (nacc < 0) {
+    if ((threadIdx.x & 31) == 0 && (threadIdx.x >> 5) < nissue) {
+      const uint32_t sa = smem_u32(smem), sb = sa + 4096;
+      const uint64_t ad = umma_desc(sa, 16, 256, 6), bd = umma_desc(sb, 16, 256, 6);
+      const uint32_t idesc = idesc_i8(128, n);
+      const uint32_t acc = tmem + (uint32_t)((threadIdx.x >> 5) * n);
+      for (int i = 0; i < iters; ++i) mma_i8(acc, ad, bd, idesc, i > 0 ? 1u : 0u);
+      mma_commit(smem_u32(done));
+    }
+  } else if (threadIdx.x == 0) {
     const uint32_t sa = smem_u32(smem), sb = sa + 4096;
     const uint64_t ad = umma_desc(sa, 16, 256, 6), bd = umma_desc(sb, 16, 256, 6);
     const uint32_t idesc = idesc_i8(128, n);
-    for (int i = 0; i < iters; ++i) mma_i8(tmem, ad, bd, idesc, i > 0 ? 1u : 0u);
+    // nacc > 1: consecutive MMAs rotate over nacc independent accumulators
+    int a = 0;
+    for (int i = 0; i < iters; ++i) {
+      mma_i8(tmem + (uint32_t)(a * n), ad, bd, idesc, i >= nacc ? 1u : 0u);
+      a = a + 1 == nacc ? 0 : a + 1;
+    }
     mma_commit(smem_u32(done));
   }
   __syncwarp();
@@ -2407,7 +2461,7 @@ __global__ void __launch_bounds__(128, 1) i8_mma_probe_kernel(int iters, int *ou
   if (threadIdx.x == 0 && iters < 0) out[0] = 1;
   fence_before();
   __syncthreads();
-  if (threadIdx.x < 32) tmem_dealloc<256>(tmem);
+  if (threadIdx.x < 32) tmem_dealloc<512>(tmem);
 }
 
 // --------------------- persistent + double-buffered TMEM + 128-byte K boxes
@@ -2421,7 +2475,7 @@ struct OzPWide {
   using W = OzWide<S, NT>;
   static constexpr int NBS = 2;
   static constexpr int NAS_FIT = (int)((222ll * 1024 - 2048 - NBS * (long long)W::B_STRIDE) / W::A_BYTES);
-  static constexpr int NAS = NAS_FIT > 12 ? 12 : NAS_FIT;
+  static constexpr int NAS = NAS_FIT > 12 / W::SG ? 12 / W::SG : NAS_FIT;
   static constexpr int ACC = S * NT;
   static_assert(2 * ACC <= 512, "two accumulator sets must fit in TMEM");
   static constexpr size_t SMEM = (size_t)NBS * W::B_STRIDE + (size_t)NAS * W::A_BYTES + 2048;
@@ -2432,7 +2486,7 @@ __global__ void __launch_bounds__(kThreadsPers, 1) oz_gemm_pwide_kernel(const __
   using W = OzWide<S, NT>;
   using P = OzPWide<S, NT>;
   constexpr int NAS = P::NAS;
-  static_assert(NAS >= 3, "A ring does not fit");
+  static_assert(NAS * W::SG >= 3, "A ring does not fit");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t *bring = smem;
@@ -2473,11 +2527,14 @@ __global__ void __launch_bounds__(kThreadsPers, 1) oz_gemm_pwide_kernel(const __
           if (kg >= P::NBS) mbar_wait(smem_u32(&b_empty[bst]), ((kg / P::NBS) - 1) & 1);
           mbar_expect_tx(smem_u32(&b_full[bst]), W::B_BYTES);
           tma_load_3d(smem_u32(bring + bst * W::B_STRIDE), &args.mapB, kb * W::KB, rowB, 0, smem_u32(&b_full[bst]));
-          for (int s = 0; s < S; ++s, ++ai) {
+          for (int j = 0; j < W::NSLOT; ++j, ++ai) {
             const int ast = ai % NAS;
             if (ai >= NAS) mbar_wait(smem_u32(&a_empty[ast]), ((ai / NAS) - 1) & 1);
             mbar_expect_tx(smem_u32(&a_full[ast]), W::A_BYTES);
-            tma_load_3d(smem_u32(aring + ast * W::A_BYTES), &args.mapA, kb * W::KB, rowA, s, smem_u32(&a_full[ast]));
+#pragma unroll
+            for (int q = 0; q < W::SG; ++q)
+              tma_load_3d(smem_u32(aring + ast * W::A_BYTES + q * W::A_PLANE), &args.mapA, kb * W::KB, rowA,
+                          oz_plane_at<S>(j * W::SG + q), smem_u32(&a_full[ast]));
           }
         }
       }
@@ -2500,7 +2557,7 @@ __global__ void __launch_bounds__(kThreadsPers, 1) oz_gemm_pwide_kernel(const __
             oz_wide_stage<S, NT>(tacc, smem_u32(bring + bst * W::B_STRIDE), nk, kb > 0 ? 1u : 0u, ai, aring, a_full,
                                  a_empty, NAS);
           else
-            for (int s = 0; s < S; ++s, ++ai) {   // diagnostics: feed only
+            for (int j = 0; j < W::NSLOT; ++j, ++ai) {   // diagnostics: feed only
               mbar_wait(smem_u32(&a_full[ai % NAS]), (ai / NAS) & 1);
               mma_commit(smem_u32(&a_empty[ai % NAS]));
             }
@@ -2549,24 +2606,27 @@ __global__ void __launch_bounds__(kThreadsPers, 1) oz_gemm_pwide_kernel(const __
 // warps 2..17: epilogue (TMEM lane quarter = warp % 4, 8 columns each).
 constexpr int kThreadsPw16 = 576;
 
-template <int S, int NT>
+template <int S, int NT, int SGP>
 struct OzPw16 {
-  using W = OzWide<S, NT>;
+  using W = OzWide<S, NT, SGP>;
   static constexpr int NBS = 2;
   static constexpr int NAS_FIT = (int)((226ll * 1024 - 2048 - NBS * (long long)W::B_STRIDE) / W::A_BYTES);
-  static constexpr int NAS = NAS_FIT > 8 ? 8 : NAS_FIT;
+  static constexpr int NAS = NAS_FIT > 8 / W::SG ? 8 / W::SG : NAS_FIT;
   static constexpr int ACC = S * NT;
   static_assert(ACC <= 512 && NT == 32, "one accumulator set of S x 32 columns");
   static constexpr size_t SMEM = (size_t)NBS * W::B_STRIDE + (size_t)NAS * W::A_BYTES + 2048;
 };
 
-template <int S, int NT, int DB>
+// SGP: planes per A ring slot -- 2 halves the issuing thread's barrier work
+// (16 x 1024^3: 1114 -> 1081 us) but at K = 256 a tile has only two stages
+// and the coarser ring stalls the feed (64 x 256^3: 105 -> 118 us): 1 there.
+template <int S, int NT, int DB, int SGP>
 __global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __grid_constant__ OzTmaArgs args) {
   MPPS_PDL_ENTER();
-  using W = OzWide<S, NT>;
-  using P = OzPw16<S, NT>;
+  using W = OzWide<S, NT, SGP>;
+  using P = OzPw16<S, NT, SGP>;
   constexpr int NAS = P::NAS;
-  static_assert(NAS >= 4, "A ring does not fit");
+  static_assert(NAS * W::SG >= 4, "A ring does not fit");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t *bring = smem;
@@ -2609,11 +2669,14 @@ __global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __g
           if (kg >= P::NBS) mbar_wait(smem_u32(&b_empty[bst]), ((kg / P::NBS) - 1) & 1);
           mbar_expect_tx(smem_u32(&b_full[bst]), W::B_BYTES);
           tma_load_3d(smem_u32(bring + bst * W::B_STRIDE), &args.mapB, kb * W::KB, rowB, 0, smem_u32(&b_full[bst]));
-          for (int s = 0; s < S; ++s, ++ai) {
+          for (int j = 0; j < W::NSLOT; ++j, ++ai) {
             const int ast = ai % NAS;
             if (ai >= NAS) mbar_wait(smem_u32(&a_empty[ast]), ((ai / NAS) - 1) & 1);
             mbar_expect_tx(smem_u32(&a_full[ast]), W::A_BYTES);
-            tma_load_3d(smem_u32(aring + ast * W::A_BYTES), &args.mapA, kb * W::KB, rowA, s, smem_u32(&a_full[ast]));
+#pragma unroll
+            for (int q = 0; q < W::SG; ++q)
+              tma_load_3d(smem_u32(aring + ast * W::A_BYTES + q * W::A_PLANE), &args.mapA, kb * W::KB, rowA,
+                          oz_plane_at<S>(j * W::SG + q), smem_u32(&a_full[ast]));
           }
         }
       }
@@ -2625,17 +2688,19 @@ __global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __g
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
         if (i >= 1) mbar_wait(smem_u32(acc_empty), (i - 1) & 1);   // the epilogue has read tile i-1 out of TMEM
         fence_after();
+        if (args.trace) args.trace[8ull * t + 0] = globaltimer();
         for (int kb = 0; kb < kstages; ++kb, ++kg) {
           const int bst = kg % P::NBS;
           mbar_wait(smem_u32(&b_full[bst]), (kg / P::NBS) & 1);
           fence_after();
           const int left = (kpad - kb * W::KB) / kKStep;
           const int nk = left < 4 ? left : 4;
-          oz_wide_stage<S, NT>(tmem, smem_u32(bring + bst * W::B_STRIDE), nk, kb > 0 ? 1u : 0u, ai, aring, a_full,
+          oz_wide_stage<S, NT, 1, 0, SGP>(tmem, smem_u32(bring + bst * W::B_STRIDE), nk, kb > 0 ? 1u : 0u, ai, aring, a_full,
                                a_empty, NAS);
           mma_commit(smem_u32(&b_empty[bst]));
         }
         mma_commit(smem_u32(acc_full));
+        if (args.trace) args.trace[8ull * t + 1] = globaltimer();
       }
     }
   } else {
@@ -2656,6 +2721,8 @@ __global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __g
       for (int j = 0; j < 8; ++j) eb[j] = col0 + j < args.N ? args.B.exps[(long long)b * args.B.rpad + col0 + j] : 0;
       mbar_wait(smem_u32(acc_full), i & 1);
       fence_after();
+      unsigned long long *tr = (args.trace && tid == 64) ? args.trace + 8ull * t : nullptr;
+      if (tr) { tr[2] = globaltimer(); tr[5] = smid(); }
       double hi[8], lo[8];
 #pragma unroll
       for (int i0 = 0; i0 < 8; i0 += 4) {
@@ -2669,6 +2736,12 @@ __global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __g
           fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(acc_empty));
+          if (tr) tr[3] = globaltimer();
+        }
+        if (args.dbg & 4) {    // diagnostics: no recombination
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) hi[i0 + jj] = lo[i0 + jj] = (double)D[0][jj];
+          continue;
         }
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
@@ -2681,7 +2754,7 @@ __global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __g
           lo[i0 + jj] = v.lo * sc;
         }
       }
-      if (row < args.M) {
+      if (row < args.M && !(args.dbg & 8)) {
         double *p = (double *)C.data + (long long)b * C.bstride + (long long)row * C.ld + col0;
         double *q = p + C.plane;
         if (col0 + 8 <= args.N && ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(q)) & 15) == 0) {
@@ -2696,6 +2769,7 @@ __global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __g
             if (col0 + j < args.N) { p[j] = hi[j]; q[j] = lo[j]; }
         }
       }
+      if (tr) tr[4] = globaltimer();
     }
   }
   fence_before();

@@ -8,9 +8,10 @@ from paper_2312_17396_b200 import _lib
 from paper_2312_17396_b200.precision import MatBatch
 
 h = _lib.handle_for()
-tag = f"pers={os.environ.get('MPPS_OZ_PERS', '0')} wide={os.environ.get('MPPS_OZ_WIDE', '1')}"
-flagsets = ((0, "full"),) if len(sys.argv) < 2 else ((0, "full"), (1, "no MMA (feed + epilogue)"), (2, "no loads (MMA + epilogue)"), (4, "no epilogue"), (5, "feed only"))
-for B, n in ((64, 256), (16, 1024), (4, 2048)):
+tag = f"pers={os.environ.get('MPPS_OZ_PERS', '0')} wide={os.environ.get('MPPS_OZ_WIDE', '1')} pw16={os.environ.get('MPPS_OZ_PW16', '1')}"
+flagsets = ((0, "full"),) if "flags" not in sys.argv else ((0, "full"), (1, "no MMA (feed + epilogue)"), (2, "no loads (MMA + epilogue)"), (4, "no epilogue"), (5, "feed only"))
+SHAPES = ((1, 8192),) if "big" in sys.argv else ((64, 256), (16, 1024), (4, 2048))
+for B, n in SHAPES:
     torch.manual_seed(1)
     A = MatBatch.empty(31, B, n, device="cuda")
     A.data.normal_()
