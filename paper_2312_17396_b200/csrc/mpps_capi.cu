@@ -1821,12 +1821,12 @@ static int launch_oz_pwide(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
 // Persistent 128-byte-box kernel with 16 epilogue warps for the 8-bit dd
 // products below the CTA-pair wide kernel's K range (MPPS_OZ_PW16=0 restores
 // the 32-byte-box ring kernel there).
-template <int S, int NT, int DB, int SGP>
+template <int S, int NT, int DB, int SGP, int FO = DD, int MODE = 0>
 static int launch_oz_pw16(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
   constexpr size_t smem = oz::OzPw16<S, NT, SGP>::SMEM;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_pw16_kernel<S, NT, DB, SGP>,
+    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_pw16_kernel<S, NT, DB, SGP, FO, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz pw16 attr: %s", cudaGetErrorString(e));
     configured = true;
@@ -1845,17 +1845,39 @@ static int launch_oz_pw16(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
   t.nbatch = nb;
   if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
   const long long tiles = (long long)nb * t.mtiles * t.ntiles;
-  launch_k(oz::oz_gemm_pw16_kernel<S, NT, DB, SGP>, dim3((unsigned)(tiles < sms ? tiles : sms)), dim3(oz::kThreadsPw16), smem,
-           h->stream, t);
+  launch_k(oz::oz_gemm_pw16_kernel<S, NT, DB, SGP, FO, MODE>, dim3((unsigned)(tiles < sms ? tiles : sms)),
+           dim3(oz::kThreadsPw16), smem, h->stream, t);
   return after_launch(h, "oz_gemm_pw16_kernel");
 }
-static bool oz_pw16_for(int S, int fo, int mode, int K, int db) {
+// MPPS_OZ_PW16: 0 off, 1 (default) the dd products (mode 0) at K < 4096 and
+// the fused Horner levels (mode 1) below the K range of the 128-column tiles,
+// 2 the dd products at every K (diagnostics), 3 only the mode-0 products
+static int oz_pw16_env() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("MPPS_OZ_PW16");
     v = e ? atoi(e) : 1;
   }
-  return v != 0 && S == 14 && db == 8 && fo == DD && mode == 0 && (K < 4096 || v == 2);   // 2: every K (diagnostics)
+  return v;
+}
+static bool oz_pw16_for(int S, int fo, int mode, int K, int db, const oz::OzArgs &a) {
+  const int v = oz_pw16_env();
+  if (!v || db != 8) return false;
+  if (mode == 0) return S == 14 && fo == DD && (K < 4096 || v == 2);
+  if (v == 3 || fo == QD || a.epi.Bprev.words > 2) return false;
+  const bool dd_only = S == 10 || S == 12 || S == 14;
+  const bool known = S == 2 || S == 3 || ((S == 5 || S == 6) && fo != F32) || (dd_only && fo == DD);
+  return known && K < (S <= 4 ? oz_nt128_min_k() : 4096);
+}
+static int dispatch_oz_pw16(mpps_handle *h, int S, int fo, int mode, int K, const oz::OzTmaArgs &t, int nb) {
+  if (mode == 0) return K >= 1024 ? launch_oz_pw16<14, 32, 8, 2>(h, t, nb) : launch_oz_pw16<14, 32, 8, 1>(h, t, nb);
+#define OZP(SS, FF) if (S == SS && fo == FF) return launch_oz_pw16<SS, 32, 8, 1, FF, 1>(h, t, nb);
+  OZP(2, F32) OZP(2, F64) OZP(2, DD) OZP(3, F32) OZP(3, F64) OZP(3, DD)
+  OZP(5, F64) OZP(5, DD) OZP(6, F64) OZP(6, DD) OZP(10, DD) OZP(12, DD)
+#undef OZP
+  if (S == 14 && fo == DD)
+    return K >= 1024 ? launch_oz_pw16<14, 32, 8, 2, DD, 1>(h, t, nb) : launch_oz_pw16<14, 32, 8, 1, DD, 1>(h, t, nb);
+  return set_err(h, MPPS_EFMT, "persistent tensor-core GEMM: no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
 }
 
 // persistent double-buffered kernel for the dd power-chain GEMMs:
@@ -1972,7 +1994,7 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   if (oz_mode() == 0) return dispatch_oz(h, S, fo, mode, a, nb);
   oz::OzTmaArgs t;
   memset(&t, 0, sizeof(t));
-  const bool pw16 = oz_pw16_for(S, fo, mode, a.K, slice_db(A));
+  const bool pw16 = oz_pw16_for(S, fo, mode, a.K, slice_db(A), a);
   const bool wide = !pw16 && oz_wide_for(S, fo, mode, a.K);
   const int pmode = (wide || pw16) ? 0 : oz_pers_mode(S, fo, mode);
   const bool pers = pmode != 0;
@@ -1993,7 +2015,7 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   t.trace = g_oz_trace;
   t.dbg = g_oz_dbg;
   if (wide) return dispatch_oz_wide(h, S, fo, mode, t, nb);
-  if (pw16) return a.K >= 1024 ? launch_oz_pw16<14, 32, 8, 2>(h, t, nb) : launch_oz_pw16<14, 32, 8, 1>(h, t, nb);
+  if (pw16) return dispatch_oz_pw16(h, S, fo, mode, a.K, t, nb);
   if (pmode == 3) return launch_oz_pwide<16, 16, DD, 0>(h, t, nb);
   if (pmode == 1) return launch_oz_pers<16, 16, DD, 0, 1>(h, t, nb);
   if (pmode == 2) return launch_oz_pers<16, 16, DD, 0, 2>(h, t, nb);

@@ -2614,19 +2614,30 @@ struct OzPw16 {
   static constexpr int NAS = NAS_FIT > 8 / W::SG ? 8 / W::SG : NAS_FIT;
   static constexpr int ACC = S * NT;
   static_assert(ACC <= 512 && NT == 32, "one accumulator set of S x 32 columns");
+  static constexpr int NACC = (2 * ACC <= 512) ? 2 : 1;
   static constexpr size_t SMEM = (size_t)NBS * W::B_STRIDE + (size_t)NAS * W::A_BYTES + 2048;
 };
 
 // SGP: planes per A ring slot -- 2 halves the issuing thread's barrier work
 // (16 x 1024^3: 1114 -> 1081 us) but at K = 256 a tile has only two stages
 // and the coarser ring stalls the feed (64 x 256^3: 105 -> 118 us): 1 there.
-template <int S, int NT, int DB, int SGP>
+// FO / MODE: MODE 1 is the fused Horner level C = RN_FO(A B 2^-(ey+ei) + B_prev)
+// 2^eo for dd-width outputs (B_prev: 1 or 2 fp64 words, read straight into the
+// registers of its row's thread before the accumulators are awaited).  Plane
+// counts with 2 S NT <= 512 get two accumulator sets: the epilogue of tile i
+// then runs under the MMAs of tile i+1 and is the critical path -- bound by
+// the latency of its row-wise B_prev loads (64 KB in flight per SM; a variant
+// staging B_prev and C through one or two shared-memory tiles with coalesced
+// cp.async measured no faster: 80.6 vs 81.9 us at S = 5, slower at S = 2).
+template <int S, int NT, int DB, int SGP, int FO = DD, int MODE = 0>
 __global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __grid_constant__ OzTmaArgs args) {
   MPPS_PDL_ENTER();
   using W = OzWide<S, NT, SGP>;
   using P = OzPw16<S, NT, SGP>;
   constexpr int NAS = P::NAS;
+  constexpr int NACC = P::NACC;
   static_assert(NAS * W::SG >= 4, "A ring does not fit");
+  static_assert(FO != QD, "dd-width outputs");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t *bring = smem;
@@ -2634,8 +2645,8 @@ __global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __g
   uint64_t *bar = reinterpret_cast<uint64_t *>(aring + NAS * W::A_BYTES);
   uint64_t *b_full = bar, *b_empty = bar + P::NBS;
   uint64_t *a_full = bar + 2 * P::NBS, *a_empty = a_full + NAS;
-  uint64_t *acc_full = a_empty + NAS, *acc_empty = acc_full + 1;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 1);
+  uint64_t *acc_full = a_empty + NAS, *acc_empty = acc_full + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int kpad = args.A.kpad;
@@ -2646,8 +2657,7 @@ __global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __g
   if (tid == 32) {
     for (int i = 0; i < P::NBS; ++i) { mbar_init(smem_u32(&b_full[i]), 1); mbar_init(smem_u32(&b_empty[i]), 1); }
     for (int i = 0; i < NAS; ++i) { mbar_init(smem_u32(&a_full[i]), 1); mbar_init(smem_u32(&a_empty[i]), 1); }
-    mbar_init(smem_u32(acc_full), 1);
-    mbar_init(smem_u32(acc_empty), 16);
+    for (int i = 0; i < 2; ++i) { mbar_init(smem_u32(&acc_full[i]), 1); mbar_init(smem_u32(&acc_empty[i]), 16); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   fence_before();
@@ -2683,11 +2693,14 @@ __global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __g
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---- MMA issuer
+      // ---- MMA issuer: tile i accumulates into set i % NACC
       int kg = 0, ai = 0, i = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
-        if (i >= 1) mbar_wait(smem_u32(acc_empty), (i - 1) & 1);   // the epilogue has read tile i-1 out of TMEM
+        const int buf = i % NACC;
+        // the epilogue has read tile i - NACC out of this accumulator set
+        if (i >= NACC) mbar_wait(smem_u32(&acc_empty[buf]), ((i / NACC) - 1) & 1);
         fence_after();
+        const uint32_t tacc = tmem + (uint32_t)(buf * P::ACC);
         if (args.trace) args.trace[8ull * t + 0] = globaltimer();
         for (int kb = 0; kb < kstages; ++kb, ++kg) {
           const int bst = kg % P::NBS;
@@ -2695,35 +2708,67 @@ __global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __g
           fence_after();
           const int left = (kpad - kb * W::KB) / kKStep;
           const int nk = left < 4 ? left : 4;
-          oz_wide_stage<S, NT, 1, 0, SGP>(tmem, smem_u32(bring + bst * W::B_STRIDE), nk, kb > 0 ? 1u : 0u, ai, aring, a_full,
-                               a_empty, NAS);
+          oz_wide_stage<S, NT, 1, 0, SGP>(tacc, smem_u32(bring + bst * W::B_STRIDE), nk, kb > 0 ? 1u : 0u, ai, aring,
+                                          a_full, a_empty, NAS);
           mma_commit(smem_u32(&b_empty[bst]));
         }
-        mma_commit(smem_u32(acc_full));
+        mma_commit(smem_u32(&acc_full[buf]));
         if (args.trace) args.trace[8ull * t + 1] = globaltimer();
       }
     }
   } else {
     // ---- epilogue warps: thread = tile row, 8 columns in two loads of 4
     const int quarter = warp & 3, cb = ((warp - 2) >> 2) * 8;
-    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     const MatRef &C = args.C;
     int i = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
       int bz, m0, n0;
       oz_pers_tile<1>(args, t, NT, 0, bz, m0, n0);
       const int b = args.sel ? args.sel[bz] : bz;
+      const int buf = i % NACC;
+      const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(buf * P::ACC);
       const int row = m0 + quarter * 32 + lane;
       const int col0 = n0 + cb;
+      const bool full = col0 + 8 <= args.N;
       const int ea = row < args.M ? args.A.exps[(long long)b * args.A.rpad + row] : 0;
       int eb[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) eb[j] = col0 + j < args.N ? args.B.exps[(long long)b * args.B.rpad + col0 + j] : 0;
-      mbar_wait(smem_u32(acc_full), i & 1);
+      // outputs; for the Horner step they first hold B_prev
+      double hi[8], lo[8];
+      int esh = 0, eo = 0;
+      if constexpr (MODE == 1) {
+        if (args.epi.exp_y) esh += args.epi.exp_y[b];
+        if (args.epi.exp_in) esh += args.epi.exp_in[b];
+        if (args.epi.exp_out) eo = args.epi.exp_out[b];
+        const MatRef &Bp = args.epi.Bprev;
+        const double *bp = (const double *)Bp.data + (long long)b * Bp.bstride + (long long)row * Bp.ld + col0;
+        const bool two = Bp.words > 1;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) hi[j] = lo[j] = 0.0;
+        if (row < args.M) {
+          if (full && ((reinterpret_cast<uintptr_t>(bp) | reinterpret_cast<uintptr_t>(bp + Bp.plane)) & 15) == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; j += 2) {
+              const double2 h2 = *reinterpret_cast<const double2 *>(bp + j);
+              hi[j] = h2.x; hi[j + 1] = h2.y;
+              if (two) {
+                const double2 l2 = *reinterpret_cast<const double2 *>(bp + Bp.plane + j);
+                lo[j] = l2.x; lo[j + 1] = l2.y;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (col0 + j < args.N) { hi[j] = bp[j]; if (two) lo[j] = bp[Bp.plane + j]; }
+          }
+        }
+      }
+      mbar_wait(smem_u32(&acc_full[buf]), (i / NACC) & 1);
       fence_after();
       unsigned long long *tr = (args.trace && tid == 64) ? args.trace + 8ull * t : nullptr;
       if (tr) { tr[2] = globaltimer(); tr[5] = smid(); }
-      double hi[8], lo[8];
+      const double so = pow2i(eo);
 #pragma unroll
       for (int i0 = 0; i0 < 8; i0 += 4) {
         int32_t D[S][4];
@@ -2731,11 +2776,11 @@ __global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __g
         for (int d = 0; d < S; ++d) tmem_ld4(lane_base + (uint32_t)(d * NT + cb + i0), D[d]);
         tmem_ld_wait();
         if (i0 == 4) {
-          // every accumulator of this warp's part is in registers: the next
-          // tile's MMAs may overwrite TMEM while the last columns are combined
+          // every accumulator of this warp's part is in registers: the MMAs
+          // of tile i + NACC may overwrite them while the last columns are combined
           fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(acc_empty));
+          if (lane == 0) mbar_arrive(smem_u32(&acc_empty[buf]));
           if (tr) tr[3] = globaltimer();
         }
         if (args.dbg & 4) {    // diagnostics: no recombination
@@ -2748,25 +2793,58 @@ __global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __g
           int32_t Dj[S];
 #pragma unroll
           for (int d = 0; d < S; ++d) Dj[d] = D[d][jj];
-          const mp::dd v = combine_dd<S, DB>(Dj);
-          const double sc = pow2i(ea + eb[i0 + jj]);
-          hi[i0 + jj] = v.hi * sc;
-          lo[i0 + jj] = v.lo * sc;
+          const double sc = pow2i(ea + eb[i0 + jj] - esh);
+          if constexpr (FO != DD && S <= 8) {
+            // fp32 / fp64 outputs of few planes: the sum in fp64 (as the
+            // staged epilogue of the tile-per-CTA kernels)
+            double v = combine_d<S, DB>(Dj) * sc;
+            if constexpr (MODE == 1) v = (hi[i0 + jj] + v) + lo[i0 + jj];
+            if (eo) v *= so;
+            hi[i0 + jj] = FO == F64 ? v : (double)__double2float_rn(v);
+          } else {
+            mp::dd v = combine_dd<S, DB>(Dj);
+            v = mp::dd_make(v.hi * sc, v.lo * sc);
+            if constexpr (MODE == 1) {
+              v = mp::dd_add(mp::dd_make(hi[i0 + jj], lo[i0 + jj]), v);
+              if (eo) v = mp::dd_make(v.hi * so, v.lo * so);
+            }
+            if constexpr (FO == DD) { hi[i0 + jj] = v.hi; lo[i0 + jj] = v.lo; }
+            else if constexpr (FO == F64) hi[i0 + jj] = v.hi;
+            else hi[i0 + jj] = (double)mp::dd_to_float(v.hi, v.lo);
+          }
         }
       }
       if (row < args.M && !(args.dbg & 8)) {
-        double *p = (double *)C.data + (long long)b * C.bstride + (long long)row * C.ld + col0;
-        double *q = p + C.plane;
-        if (col0 + 8 <= args.N && ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(q)) & 15) == 0) {
+        const long long off = (long long)b * C.bstride + (long long)row * C.ld + col0;
+        if constexpr (FO == F32) {
+          float *p = (float *)C.data + off;
+          if (full && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
 #pragma unroll
-          for (int j = 0; j < 8; j += 2) {
-            *reinterpret_cast<double2 *>(p + j) = make_double2(hi[j], hi[j + 1]);
-            *reinterpret_cast<double2 *>(q + j) = make_double2(lo[j], lo[j + 1]);
+            for (int j = 0; j < 8; j += 4)
+              *reinterpret_cast<float4 *>(p + j) =
+                  make_float4((float)hi[j], (float)hi[j + 1], (float)hi[j + 2], (float)hi[j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (col0 + j < args.N) p[j] = (float)hi[j];
           }
         } else {
+          double *p = (double *)C.data + off;
+          double *q = p + C.plane;
+          if (full && ((reinterpret_cast<uintptr_t>(p) | (FO == DD ? reinterpret_cast<uintptr_t>(q) : 0)) & 15) == 0) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (col0 + j < args.N) { p[j] = hi[j]; q[j] = lo[j]; }
+            for (int j = 0; j < 8; j += 2) {
+              *reinterpret_cast<double2 *>(p + j) = make_double2(hi[j], hi[j + 1]);
+              if constexpr (FO == DD) *reinterpret_cast<double2 *>(q + j) = make_double2(lo[j], lo[j + 1]);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (col0 + j < args.N) {
+                p[j] = hi[j];
+                if constexpr (FO == DD) q[j] = lo[j];
+              }
+          }
         }
       }
       if (tr) tr[4] = globaltimer();

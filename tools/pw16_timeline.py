@@ -36,3 +36,35 @@ for B, n in ((64, 256), (16, 1024)):
         lag += list(i0[o][1:] - rel[o][:-1])
         per += list(i0[o][1:] - i0[o][:-1])
     print(f"  released -> next tile's first MMA issued {np.median(lag)/1e3:.2f} us; tile period {np.median(per)/1e3:.2f} us")
+
+# fused Horner levels (mode 1): phi (row-split, S planes) x Y (column-split) + B_prev
+B, n = 64, 256
+Y = MatBatch.empty(31, B, n, device="cuda"); Y.data.normal_(); Y.data[1:] *= 1e-17
+Bp = MatBatch.empty(31, B, n, device="cuda"); Bp.data.normal_(); Bp.data[1:] *= 1e-17
+ysb = h.slice(Y, 1, 14, None, 8)
+for S, fin, fout in ((10, 31, 31), (5, 15, 31), (2, 7, 15), (2, 7, 7)):
+    Pm = MatBatch.empty(fin, B, n, device="cuda"); Pm.data.normal_()
+    if Pm.words > 1:
+        Pm.data[1:] *= 1e-17
+    out = MatBatch.empty(fout, B, n, device="cuda")
+    ps = h.slice(Pm, 0, S, None, 8)
+    nt = B * (n // 128) * (n // 32)
+    buf = torch.zeros(nt * 8, dtype=torch.int64, device="cuda")
+    fn = lambda: h.horner_step_sliced(ps, ysb, S, Bp, out, fmt_in=fin)
+    fn(); torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(); fn(); b.record(); torch.cuda.synchronize()
+    h.lib.mpps_debug_oz_trace(buf.data_ptr())
+    fn(); torch.cuda.synchronize()
+    h.lib.mpps_debug_oz_trace(None)
+    t = buf.view(nt, 8).cpu().numpy().astype(np.float64)
+    t0 = t[:, 0].min()
+    i0, i1, full, rel, done, sm = (t[:, k] - (t0 if k < 5 else 0) for k in range(6))
+    per = []
+    for m in np.unique(sm):
+        idx = np.where(sm == m)[0]
+        o = idx[np.argsort(done[idx])]
+        per += list(done[o][1:] - done[o][:-1])
+    print(f"Horner S={S} -> fmt {fout}: {a.elapsed_time(b)*1e3:.1f} us; MMA issue {np.median(i1 - i0)/1e3:.2f} us; "
+          f"acc complete -> released {np.median(rel - full)/1e3:.2f} us; released -> stored {np.median(done - rel)/1e3:.2f} us; "
+          f"issue end -> acc seen by the epilogue {np.median(full - i1)/1e3:.2f} us; tile period {np.median(per)/1e3:.2f} us")
