@@ -2592,6 +2592,21 @@ __global__ void __launch_bounds__(kThreadsPers, 1) oz_gemm_pwide_kernel(const __
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
+// 256-bit global accesses (sm_100: LDG/STG.256): a row-per-thread epilogue
+// touches one line per lane and instruction, so its cost is the number of
+// instructions -- 4 doubles each instead of 2.
+__device__ __forceinline__ void ldg256(const double *p, double &a, double &b, double &c, double &d) {
+  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];\n" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+__device__ __forceinline__ void stg256(double *p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+__device__ __forceinline__ void stg256f(float *p, const double *v) {
+  asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"l"(p), "f"((float)v[0]), "f"((float)v[1]),
+               "f"((float)v[2]), "f"((float)v[3]), "f"((float)v[4]), "f"((float)v[5]), "f"((float)v[6]), "f"((float)v[7])
+               : "memory");
+}
+
 // ------------- persistent, 128-byte K boxes, one accumulator set, 16 epilogue warps
 // The dd products of the power chain at small and medium K (cfg2: K = 256,
 // cfg3: K = 1024).  Per 128 x 32 tile the 32-byte-box ring kernel spends
@@ -2747,15 +2762,11 @@ __global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __g
 #pragma unroll
         for (int j = 0; j < 8; ++j) hi[j] = lo[j] = 0.0;
         if (row < args.M) {
-          if (full && ((reinterpret_cast<uintptr_t>(bp) | reinterpret_cast<uintptr_t>(bp + Bp.plane)) & 15) == 0) {
+          if (full && ((reinterpret_cast<uintptr_t>(bp) | reinterpret_cast<uintptr_t>(bp + Bp.plane)) & 31) == 0) {
 #pragma unroll
-            for (int j = 0; j < 8; j += 2) {
-              const double2 h2 = *reinterpret_cast<const double2 *>(bp + j);
-              hi[j] = h2.x; hi[j + 1] = h2.y;
-              if (two) {
-                const double2 l2 = *reinterpret_cast<const double2 *>(bp + Bp.plane + j);
-                lo[j] = l2.x; lo[j + 1] = l2.y;
-              }
+            for (int j = 0; j < 8; j += 4) {
+              ldg256(bp + j, hi[j], hi[j + 1], hi[j + 2], hi[j + 3]);
+              if (two) ldg256(bp + Bp.plane + j, lo[j], lo[j + 1], lo[j + 2], lo[j + 3]);
             }
           } else {
 #pragma unroll
@@ -2818,11 +2829,8 @@ __global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __g
         const long long off = (long long)b * C.bstride + (long long)row * C.ld + col0;
         if constexpr (FO == F32) {
           float *p = (float *)C.data + off;
-          if (full && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
-#pragma unroll
-            for (int j = 0; j < 8; j += 4)
-              *reinterpret_cast<float4 *>(p + j) =
-                  make_float4((float)hi[j], (float)hi[j + 1], (float)hi[j + 2], (float)hi[j + 3]);
+          if (full && (reinterpret_cast<uintptr_t>(p) & 31) == 0) {
+            stg256f(p, hi);
           } else {
 #pragma unroll
             for (int j = 0; j < 8; ++j)
@@ -2831,11 +2839,11 @@ __global__ void __launch_bounds__(kThreadsPw16, 1) oz_gemm_pw16_kernel(const __g
         } else {
           double *p = (double *)C.data + off;
           double *q = p + C.plane;
-          if (full && ((reinterpret_cast<uintptr_t>(p) | (FO == DD ? reinterpret_cast<uintptr_t>(q) : 0)) & 15) == 0) {
+          if (full && ((reinterpret_cast<uintptr_t>(p) | (FO == DD ? reinterpret_cast<uintptr_t>(q) : 0)) & 31) == 0) {
 #pragma unroll
-            for (int j = 0; j < 8; j += 2) {
-              *reinterpret_cast<double2 *>(p + j) = make_double2(hi[j], hi[j + 1]);
-              if constexpr (FO == DD) *reinterpret_cast<double2 *>(q + j) = make_double2(lo[j], lo[j + 1]);
+            for (int j = 0; j < 8; j += 4) {
+              stg256(p + j, hi[j], hi[j + 1], hi[j + 2], hi[j + 3]);
+              if constexpr (FO == DD) stg256(q + j, lo[j], lo[j + 1], lo[j + 2], lo[j + 3]);
             }
           } else {
 #pragma unroll
