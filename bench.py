@@ -737,7 +737,8 @@ def run_ours(name, args, rank, world, local_rank, dist):
         durs = [x.elapsed_time(y) * 1e-3 for x, y in evs]
         by_key[key] = (len(durs), sum(durs))
     names = {7: "fp32", 15: "fp64", 31: "dd", 63: "qd"}
-    if not by_key:
+    small = not by_key          # K5 path (n <= 32): no GEMM launches to bracket
+    if small:
         by_key[("none", 31, 31, 1, 1, 1, 1, 0, 0)] = (1, 1.0)
     dom = max(by_key.items(), key=lambda kv: kv[1][1])
     (kind, fin, fout, M, N, K, nb, S_used, db_used), (cnt, sec) = dom
@@ -788,7 +789,20 @@ def run_ours(name, args, rank, world, local_rank, dist):
         roof = {"bound": "fp64-pipe" if fname != "fp32" else "fp32-pipe", "achieved": logical, "peak": peaks[fname],
                 "unit": "TFLOP/s (logical)", "frac": logical / peaks[fname], "mean_launch_s": sec / cnt,
                 "peak_source": "FMA pipe microbenchmark in bench.py on this GPU"}
-    kkey = f"{kind} {fname}->{names[fout]} {M}x{N}x{K} x{nb}"
+    if small:
+        # the fused small-matrix evaluation: two launches around the host
+        # planner, one CTA per matrix -- a latency-bound step; rated as the
+        # evaluation's logical GEMM flops over the step against the fp64 pipe
+        flops = sum(fs * c for c in gem.values())
+        roof = {"bound": "latency", "achieved": flops / step_time / 1e12, "peak": peaks["fp64"],
+                "unit": "TFLOP/s (logical fp64)", "frac": flops / step_time / 1e12 / peaks["fp64"],
+                "mean_launch_s": None,
+                "note": "K5 (csrc/small_ps.cuh): small_prepare_kernel + small_horner_kernel, one CTA per matrix, "
+                        "operands in shared memory; one n = 32 matrix occupies one SM, so the step is launch / "
+                        "host latency, not a pipe or HBM bound (DESIGN 6)",
+                "peak_source": "FMA pipe microbenchmark in bench.py on this GPU"}
+    kkey = (f"{kind} {fname}->{names[fout]} {M}x{N}x{K} x{nb}" if not small
+            else "small_prepare_kernel + small_horner_kernel (fused PS, n <= 32)")
     traffic, tsrc = None, None
     try:   # committed ncu --set full capture of this kernel at this shape (profiles/traffic.json)
         tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
@@ -798,7 +812,8 @@ def run_ours(name, args, rank, world, local_rank, dist):
     except Exception:
         pass
     roof.update({"kernel": kkey, "traffic": traffic, "traffic_source": tsrc,
-                 "share_of_step": sec / args.steps / step_time, "launches_per_step": cnt / args.steps,
+                 "share_of_step": None if small else sec / args.steps / step_time,
+                 "launches_per_step": per_step if small else cnt / args.steps,
                  "eval_frac": t_ideal / step_time,
                  "measured_in": "a second timed pass of the same K steps run eagerly (the value pass "
                                 "replays CUDA graphs, whose kernels cannot be bracketed by events)"})
@@ -876,8 +891,8 @@ def _relaunch_under_torchrun(gpus: int) -> int:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", action="append", choices=sorted(CONFIGS),
                     help="config(s) to run, in order (default: cfg2 then the headline cfg5)")

@@ -44,7 +44,7 @@ def test_roofline_fraction_recomputes():
         assert abs(achieved / r["peak"] - r["frac"]) <= 1e-9, name
 
 
-@pytest.mark.parametrize("name,kernel", [("cfg5", "oz_gemm_wide_kernel<14"), ("cfg2", "oz_gemm_ring_kernel<14")])
+@pytest.mark.parametrize("name,kernel", [("cfg5", "oz_gemm_wide_kernel<14"), ("cfg2", "oz_gemm_pw16_kernel<14, 32, 8, 1, 2, 0>")])
 def test_dominant_share_matches_launch_list(name, kernel):
     line = _lines()[name]
     r = line["roofline"]
