@@ -239,3 +239,76 @@ def test_wide_kernel_cluster_multicast_matches(cuda, tmp_path):
         assert np.array_equal(res["mc"][k], res["solo"][k]), k
         assert np.array_equal(res["mc"][k], res["tma"][k]), k
         assert np.abs(res["mc"][k]).sum() > 0
+
+
+_PW16_SCRIPT = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2312_17396_b200 import _lib
+from paper_2312_17396_b200.precision import MatBatch
+h = _lib.handle_for()
+rng = np.random.default_rng(5)
+out = {}
+dd = np.array([1, 2.0 ** -56])[:, None, None, None]
+# plain dd products (mode 0): one plane per ring slot (K < 1024) and two (K >= 1024), ragged M / N / K,
+# a paired output view (column offset inside a wider buffer) and a batch selection
+for (B, M, K, N) in ((3, 200, 288, 300), (2, 384, 1056, 160), (1, 128, 2080, 512)):
+    A = MatBatch(torch.from_numpy(rng.standard_normal((2, B, M, K)) * dd).cuda(), 31)
+    Bm = MatBatch(torch.from_numpy(rng.standard_normal((2, B, K, N)) * dd).cuda(), 31)
+    C = MatBatch.zeros(31, B, M, N, device="cuda")
+    sel = torch.tensor(list(range(B))[::-1][: max(1, B - 1)], dtype=torch.int32, device="cuda")
+    h.gemm_sliced(h.slice(A, 0, 14, None, 8), h.slice(Bm, 1, 14, None, 8), 14, C, sel)
+    out[f"g_{M}_{K}_{N}"] = C.data.cpu().numpy()
+wide = torch.zeros((2, 2, 256, 512), dtype=torch.float64, device="cuda")
+A = MatBatch(torch.from_numpy(rng.standard_normal((2, 2, 256, 256)) * dd).cuda(), 31)
+sa, sb = h.slice(A, 0, 14, None, 8), h.slice(A, 1, 14, None, 8)
+h.gemm_sliced(sa, sb, 14, MatBatch(wide[:, :, :, 256:], 31))
+out["g_view"] = wide.cpu().numpy()
+# fused Horner levels (mode 1): every plane count of the level kernels, fp32 / fp64 / dd outputs,
+# fp64 (1 word) and dd (2 words) B_prev, level exponents, selection, ragged shapes
+B, M, N = 3, 200, 300
+for K in (288, 1056):
+    Y = MatBatch(torch.from_numpy(rng.standard_normal((2, B, M, K)) * dd).cuda(), 31)
+    P = MatBatch(torch.from_numpy(rng.standard_normal((2, B, K, N)) * dd).cuda(), 31)
+    ys = h.slice(Y, 0, 14, None, 8)
+    for S, fo, fp in ((2, 7, 15), (2, 15, 15), (2, 31, 31), (3, 7, 31), (3, 15, 15), (3, 31, 31), (5, 15, 15),
+                      (5, 31, 31), (6, 15, 31), (6, 31, 31), (10, 31, 31), (12, 31, 31), (14, 31, 31)):
+        w = 2 if fp == 31 else 1
+        Bp = MatBatch(torch.from_numpy(rng.standard_normal((w, B, M, N)) * dd[:w]).cuda(), fp)
+        o = MatBatch.zeros(fo, B, M, N, device="cuda")
+        sel = torch.tensor([2, 0], dtype=torch.int32, device="cuda")
+        ey = torch.tensor([1, 0, -2], dtype=torch.int32, device="cuda")
+        ei = torch.tensor([3, -1, 2], dtype=torch.int32, device="cuda")
+        eo = torch.tensor([-2, 0, 1], dtype=torch.int32, device="cuda")
+        h.horner_step_sliced(ys, h.slice(P, 1, S, None, 8), S, Bp, o, sel, ey, ei, eo, fmt_in=fo)
+        out[f"h_{K}_{S}_{fo}_{fp}"] = o.data.double().cpu().numpy()
+np.savez(sys.argv[2], **out)
+'''
+
+
+def test_persistent_kernel_matches_tile_per_cta_kernels(cuda, tmp_path):
+    """The persistent 128-byte-box kernel (oz_gemm_pw16_kernel: dd products at
+    K < 4096 and the fused Horner levels) gives the same bits as the
+    tile-per-CTA ring / TMA kernels (MPPS_OZ_PW16=0): ragged M / N / K, one
+    and two planes per ring slot, one and two accumulator sets, an output
+    view inside a wider buffer, selections, level exponents, fp32 / fp64 / dd
+    outputs, 1- and 2-word B_prev; separate processes (the switch is read
+    once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "p.py"
+    script.write_text(_PW16_SCRIPT)
+    res = {}
+    for tag, env in (("pw16", {}), ("tiles", {"MPPS_OZ_PW16": "0"})):
+        f = tmp_path / f"{tag}.npz"
+        subprocess.check_call([sys.executable, str(script), root, str(f)], env=dict(os.environ, **env))
+        res[tag] = dict(np.load(f))
+    assert len(res["pw16"]) == 4 + 2 * 13
+    for k in res["pw16"]:
+        assert np.array_equal(res["pw16"][k], res["tiles"][k]), k
+        assert np.abs(res["pw16"][k]).sum() > 0, k
+    # rows of unselected members and the left half of the view stay untouched
+    assert np.abs(res["pw16"]["g_view"][..., :256]).sum() == 0
+    assert np.abs(res["pw16"]["h_288_2_7_15"][:, 1]).sum() == 0

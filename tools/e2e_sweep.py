@@ -6,9 +6,9 @@ import bench
 import paper_2312_17396_b200 as mp
 from paper_2312_17396_b200 import pipeline as pl
 
-wl = bench.Workload("cfg2", 0, 1, torch, mp)
+wl = bench.Workload("cfg2", 0, 1, torch, mp, "weak", 10, 0)
 K = 10
-Xbig = wl.Xpin.repeat(K, 1, 1).pin_memory()
+Xbig = torch.cat([wl.Xpin[t % wl.pool] for t in range(K)]).pin_memory()
 out = torch.empty((2,) + tuple(Xbig.shape), dtype=torch.float64).pin_memory()
 sub = pl.mixed_exp(wl.m, wl.ctx, timing=False)
 for chunks, win in (([16] * 4, 8), ([16] * 4, 12), ([32, 32], 4), ([32, 32], 6), ([64], 2), ([64], 3),

@@ -7,9 +7,9 @@ import bench
 import paper_2312_17396_b200 as mp
 from paper_2312_17396_b200 import pipeline as pl
 
-wl = bench.Workload("cfg2", 0, 1, torch, mp)
+wl = bench.Workload("cfg2", 0, 1, torch, mp, "weak", 10, 0)
 K = 10
-Xbig = wl.Xpin.repeat(K, 1, 1).pin_memory()
+Xbig = torch.cat([wl.Xpin[t % wl.pool] for t in range(K)]).pin_memory()
 out = torch.empty((2,) + tuple(Xbig.shape), dtype=torch.float64).pin_memory()
 sub = pl.mixed_exp(wl.m, wl.ctx, timing=False)
 cases = [
@@ -19,6 +19,9 @@ cases = [
     ([32, 32] + [64] * (K - 2) + [32, 32], 3),
     ([16, 16, 32] + [64] * (K - 2) + [32, 16, 16], 4),
     ([32, 32] * K, 6),
+    ([64] * K, 4),
+    ([64] * K, 6),
+    ([16] * (4 * K), 12),
 ]
 for sizes, win in cases:
     assert sum(sizes) == 64 * K

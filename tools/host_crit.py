@@ -7,7 +7,7 @@ import bench
 import paper_2312_17396_b200 as mp
 from paper_2312_17396_b200 import engine, graphs, planner
 
-wl = bench.Workload("cfg2", 0, 1, torch, mp)
+wl = bench.Workload("cfg2", 0, 1, torch, mp, "weak", 10, 0)
 for _ in range(4):
     wl.step(wl.Xd)
 torch.cuda.synchronize()
