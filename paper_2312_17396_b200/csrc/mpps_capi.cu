@@ -1956,6 +1956,7 @@ static bool oz_wide_for(int S, int fo, int mode, int K) {
   }
   if (!v) return false;
   return ((S == 16 || S == 14) && mode == 0 && fo == DD && (K >= 4096 || v == 2)) || (S == 31 && fo == QD && v == 2) ||
+         (S == 28 && fo == QD && (K >= 1024 || v == 2)) ||   // 8-bit qd: 2048^3 2275 -> 1979 us, 4 x 1024^3 1179 -> 1049 us
          (S == 8 && mode == 0 && fo == F64 && K >= 4096) ||   // Y = X^s at fp64 precision (64-column tiles)
          ((S == 2 || S == 3) && mode == 1 && fo != QD && K >= 4096);   // few-plane Horner levels
   // (4 planes: the 32-byte-box NT = 128 kernel measured 4.7 vs 4.9 ms for a
@@ -1970,6 +1971,7 @@ static int oz_wide_nt(int S, int mode) {
 static int dispatch_oz_wide(mpps_handle *h, int S, int fo, int mode, const oz::OzTmaArgs &a, int nb) {
 #define OZ(SS, NT, FF, MM) if (S == SS && fo == FF && mode == MM) return launch_oz_wide<SS, NT, FF, MM>(h, a, nb);
   OZ(14, 32, DD, 0) OZ(16, 32, DD, 0) OZ(31, 16, QD, 0) OZ(31, 16, QD, 1) OZ(8, 64, F64, 0)
+  OZ(28, 16, QD, 0) OZ(28, 16, QD, 1)
   OZ(2, 128, F32, 1) OZ(2, 128, F64, 1) OZ(2, 128, DD, 1) OZ(3, 128, F32, 1) OZ(3, 128, F64, 1) OZ(3, 128, DD, 1)
 #undef OZ
   return set_err(h, MPPS_EFMT, "wide tensor-core GEMM: no kernel for %d slices -> format %d (mode %d)", S, fo, mode);

@@ -992,8 +992,17 @@ template <int S, int NT>
 __host__ __device__ constexpr size_t oz_smem_bytes() { return oz_stages<S, NT>() * oz_stage_bytes<S, NT>() + 256; }
 
 // value of sum_d D_d 2^-(12+DB d) as a qd (exact grouping in threes)
+template <int S, int DB>
+__device__ __forceinline__ mp::qd combine_qd(const int32_t *D);
+template <int S, int DB>
+__device__ __forceinline__ mp::dd combine_dd(const int32_t *D);
 template <int S, int DB = 7>
 __device__ __forceinline__ mp::qd combine_diagonals(const int32_t *D) {
+  if constexpr (S > 16) return combine_qd<S, DB>(D);
+  else return mp::qd_from_dd(combine_dd<S, DB>(D));
+}
+template <int S, int DB = 7>
+__device__ __forceinline__ mp::qd combine_diagonals_chain(const int32_t *D) {
   mp::qd acc = mp::qd_make(0.0, 0.0, 0.0, 0.0);
   mp::dd accd = mp::dd_make(0.0, 0.0);
 #pragma unroll
@@ -1258,6 +1267,70 @@ __device__ __forceinline__ mp::dd combine_dd(const int32_t *D) {
     const double hi = s + lo;             // |s| >= |lo| or s == 0
     return mp::dd_make(hi, lo - (hi - s));
   }
+}
+
+// The same for qd outputs (S <= 31 planes: up to 11 groups).  The carry-
+// normalised digits pair up into at most six exact, non-overlapping doubles
+// P0 > P1 > ...; three VecSum sweeps (exact TwoSums; the first with
+// FastTwoSum, its operands are ordered) leave the leading three qd words, the
+// fourth takes the rounded rest (relative error <= 2^-205; zero words are
+// moved behind the value).  ~75 DADD per output instead of ~950 for the chain
+// of qd additions.
+template <int S, int DB>
+__device__ __forceinline__ mp::qd combine_qd(const int32_t *D) {
+  constexpr int NG = (S + 2) / 3;
+  constexpr int WB = 3 * DB;
+  static_assert(NG >= 4 && NG <= 11, "combine_qd: 10..31 planes");
+  long long G[NG];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    const int d0 = 3 * g;
+    G[g] = (long long)D[d0] << (2 * DB);
+    if (d0 + 1 < S) G[g] += (long long)D[d0 + 1] << DB;
+    if (d0 + 2 < S) G[g] += (long long)D[d0 + 2];
+  }
+  unsigned long long dig[NG];
+  long long c = 0;
+#pragma unroll
+  for (int g = NG - 1; g >= 1; --g) {
+    const long long t = G[g] + c;
+    dig[g] = (unsigned long long)t & ((1ull << WB) - 1ull);
+    c = t >> WB;
+  }
+  constexpr int NP = 1 + NG / 2;   // P0 and the pairs (1,2), (3,4), ... (a last single digit alone)
+  double p[NP];
+  p[0] = u52_scaled<12 + DB * 2>((unsigned long long)(G[0] + c + (1ll << 51)), pow2c(51 - (12 + DB * 2)));
+#define MPPS_QD_TERM(K)                                                                             \
+  if constexpr (K < NP) {                                                                           \
+    constexpr int a = 2 * K - 1;                                                                    \
+    if constexpr (a + 1 < NG) p[K] = u52_scaled<12 + DB * (3 * (a + 1) + 2)>((dig[a] << WB) | dig[a + 1]); \
+    else p[K] = u52_scaled<12 + DB * (3 * a + 2)>(dig[a]);                                          \
+  }
+  MPPS_QD_TERM(1) MPPS_QD_TERM(2) MPPS_QD_TERM(3) MPPS_QD_TERM(4) MPPS_QD_TERM(5)
+#undef MPPS_QD_TERM
+  // sweep 1 (bottom-up): |p[i-1]| >= |sum below| or p[i-1] == 0, so FastTwoSum is exact
+#pragma unroll
+  for (int i = NP - 1; i >= 1; --i) {
+    const double sum = p[i - 1] + p[i];
+    p[i] = p[i] - (sum - p[i - 1]);
+    p[i - 1] = sum;
+  }
+#pragma unroll
+  for (int k = 1; k <= 2; ++k)   // two more whole sweeps, as mp::qd_renorm
+#pragma unroll
+    for (int i = NP - 1; i >= 1; --i) mp::two_sum(p[i - 1], p[i], p[i - 1], p[i]);
+  double q[4] = {p[0], p[1], p[2], 0.0};
+#pragma unroll
+  for (int i = NP - 1; i >= 3; --i) q[3] += p[i];
+  // heavy cancellation (the leading digits summing to almost nothing) leaves
+  // zero words in front of the value: move them behind it, so that word 0 is
+  // the leading word (the digit splits take row / column maxima from it)
+#pragma unroll
+  for (int pass = 0; pass < 3; ++pass)
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      if (q[i] == 0.0) { q[i] = q[i + 1]; q[i + 1] = 0.0; }
+  return mp::qd_make(q[0], q[1], q[2], q[3]);
 }
 
 // fp64 value of the recombined diagonals (one rounding per group beyond the

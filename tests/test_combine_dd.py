@@ -119,3 +119,104 @@ def test_combine_dd_cancellation(DB):
             D[j] = (1 << DB) - 1
         D[S - 1] = (1 << DB) - 1
         check(D, S, DB)
+
+
+def _two_sum(a, b):
+    s = a + b
+    bb = s - a
+    return s, (a - (s - bb)) + (b - bb)
+
+
+def combine_qd(D, S, DB):
+    """csrc/ozaki.cuh::combine_qd, operation for operation."""
+    NG, WB = (S + 2) // 3, 3 * DB
+    G = []
+    for g in range(NG):
+        d0 = 3 * g
+        v = D[d0] << (2 * DB)
+        if d0 + 1 < S:
+            v += D[d0 + 1] << DB
+        if d0 + 2 < S:
+            v += D[d0 + 2]
+        G.append(v)
+    dig, c = [0] * NG, 0
+    for g in range(NG - 1, 0, -1):
+        t = G[g] + c
+        dig[g] = t & ((1 << WB) - 1)
+        c = t >> WB
+    q0 = 12 + DB * 2
+    NP = 1 + NG // 2
+    p = [_u52_scaled(G[0] + c + (1 << 51), q0, 2.0 ** (51 - q0))]
+    for K in range(1, NP):
+        a = 2 * K - 1
+        if a + 1 < NG:
+            p.append(_u52_scaled((dig[a] << WB) | dig[a + 1], 12 + DB * (3 * (a + 1) + 2)))
+        else:
+            p.append(_u52_scaled(dig[a], 12 + DB * (3 * a + 2)))
+    for i in range(NP - 1, 0, -1):
+        s = p[i - 1] + p[i]
+        p[i] = p[i] - (s - p[i - 1])
+        p[i - 1] = s
+    for k in (1, 2):
+        for i in range(NP - 1, 0, -1):
+            p[i - 1], p[i] = _two_sum(p[i - 1], p[i])
+    q = [p[0], p[1], p[2], 0.0]
+    for i in range(NP - 1, 2, -1):
+        q[3] += p[i]
+    for _ in range(3):
+        for i in range(3):
+            if q[i] == 0.0:
+                q[i], q[i + 1] = q[i + 1], 0.0
+    return tuple(q)
+
+
+def check_qd(D, S, DB):
+    w = combine_qd(D, S, DB)
+    V = exact(D, S, DB)
+    got = sum(Fraction(x) for x in w)
+    assert abs(got - V) <= abs(V) / (1 << 205), (S, DB, D)
+    # word 0 is the value rounded to double (the digit splits take row / column maxima from
+    # it) and word 1 lies below its last place; the lower words may overlap one another
+    # mildly, as after mp::qd_renorm's three sweeps -- the sum is what the kernels use
+    if V != 0:
+        assert w[0] != 0.0 and abs(Fraction(w[0]) - V) <= Fraction(math.ulp(w[0])) / 2
+        assert abs(w[1]) <= math.ulp(w[0]) / 2, (S, DB, D, w)
+    nz = [x for x in w if x != 0.0]
+    for a, b in zip(nz, nz[1:]):
+        assert abs(b) < abs(a), (S, DB, D, w)
+    # a zero word is followed only by zeros (no information behind a gap)
+    seen_zero = False
+    for x in w:
+        if x == 0.0:
+            seen_zero = True
+        else:
+            assert not seen_zero, (S, DB, D, w)
+
+
+@pytest.mark.parametrize("DB,S", [(8, 28), (7, 31), (8, 12), (8, 10)])
+def test_combine_qd(DB, S):
+    rng = random.Random(4321 + DB + S)
+    lim = (1 << 31) - 1
+    for _ in range(400):
+        check_qd([rng.randint(-lim, lim) for _ in range(S)], S, DB)
+    for _ in range(200):
+        check_qd([rng.randint(-(1 << rng.randint(0, 30)), 1 << rng.randint(0, 30)) for _ in range(S)], S, DB)
+    check_qd([lim] * S, S, DB)
+    check_qd([-lim - 1] * S, S, DB)
+    check_qd([0] * S, S, DB)
+    for d in range(S):
+        for v in (1, -1, lim, -lim - 1):
+            check_qd([v if i == d else 0 for i in range(S)], S, DB)
+    for _ in range(300):          # cancelling leading diagonals
+        D = [0] * S
+        k = rng.randint(1, S - 1)
+        D[k] = rng.randint(-(1 << 30), 1 << 30) >> DB << DB
+        D[k - 1] = -(D[k] >> DB) + rng.choice((0, 0, 1, -1))
+        for j in range(k + 1, S):
+            D[j] = rng.randint(-lim, lim) if rng.random() < 0.7 else 0
+        check_qd(D, S, DB)
+    D = [0] * S
+    D[0] = -1
+    for j in range(1, S):
+        D[j] = (1 << DB) - 1
+    check_qd(D, S, DB)
