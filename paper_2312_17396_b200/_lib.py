@@ -26,7 +26,7 @@ MPPS_OK, MPPS_EINVAL, MPPS_EFMT, MPPS_ECUDA = 0, 1, 2, 3
 EXPORTED = (
     "mpps_version", "mpps_create", "mpps_destroy", "mpps_set_stream",
     "mpps_last_error", "mpps_launch_count", "mpps_convert", "mpps_gemm",
-    "mpps_axpy", "mpps_powers", "mpps_slice_into", "mpps_assemble_blocks", "mpps_assemble_blocks_hc", "mpps_assemble_hc_supported", "mpps_assemble_blocks_hc_n", "mpps_assemble_hc_n_supported", "mpps_one_norm", "mpps_one_norm_complex", "mpps_level_exps",
+    "mpps_axpy", "mpps_powers", "mpps_slice_into", "mpps_assemble_blocks", "mpps_assemble_blocks_hc", "mpps_assemble_hc_supported", "mpps_assemble_blocks_hc_n", "mpps_assemble_hc_n_supported", "mpps_one_norm", "mpps_one_norm_complex", "mpps_level_exps", "mpps_store_host",
     "mpps_horner_step", "mpps_horner_scalar_top", "mpps_probe_fma",
     "mpps_assemble_blocks_dist", "mpps_colmax", "mpps_slice", "mpps_gemm_sliced",
     "mpps_horner_step_sliced", "mpps_oz_slices_for", "mpps_oz_slices_for_bits", "mpps_oz_max_k_8bit", "mpps_oz_max_k", "mpps_probe_i8mma", "mpps_debug_oz_trace",
@@ -127,6 +127,7 @@ def load_library(path: Optional[str] = None):
         lib.mpps_one_norm.argtypes = [vp, mp, vp]
         lib.mpps_one_norm_complex.argtypes = [vp, mp, ip, vp, ip]
         lib.mpps_level_exps.argtypes = [vp, vp, ip, ip, ctypes.c_ulonglong, vp, vp]
+        lib.mpps_store_host.argtypes = [vp, vp, vp, ctypes.c_longlong]
         lib.mpps_horner_step.argtypes = [vp, mp, mp, mp, mp, vp, ip, vp, vp, vp]
         lib.mpps_horner_scalar_top.argtypes = [vp, P(ctypes.c_double), ip, mp, mp, mp, vp, ip, vp]
         lib.mpps_probe_fma.argtypes = [vp, ip, ip, ip, vp]
@@ -189,6 +190,7 @@ class Handle:
         self.h = h
         self.device = device
         self.stream_ptr = stream_ptr
+        self._pins = {}           # pinned host buffers of host_array, by size
         # optional per-launch CUDA-event probe (bench.py): key -> [(start, end)]
         self.probe = None
 
@@ -368,6 +370,27 @@ class Handle:
         self._check(self.lib.mpps_level_exps(self.h, norms_dev.data_ptr(), int(norms_dev.shape[0]), int(r),
                                              int(fp32_mask), exps_dev.data_ptr(), exp_y_dev.data_ptr()),
                     "level_exps")
+
+    def store_host(self, src_dev, dst_pinned):
+        """float64 device tensor -> pinned host tensor of the same size, stored by a kernel (no copy
+        engine: a memcpy would queue behind a running result download)."""
+        if not dst_pinned.is_pinned() or dst_pinned.numel() != src_dev.numel() or not src_dev.is_contiguous():
+            raise ValueError("store_host: pinned destination of the source's size, contiguous source")
+        self._check(self.lib.mpps_store_host(self.h, src_dev.data_ptr(), dst_pinned.data_ptr(), src_dev.numel()),
+                    "store_host")
+
+    def host_array(self, src_dev) -> "np.ndarray":
+        """A small float64 device tensor as a numpy array: stored into pinned memory by a kernel
+        (store_host), then one stream synchronisation -- the planner's norms never wait for the
+        device-to-host copy engine."""
+        import torch
+        src = src_dev.contiguous()
+        pin = self._pins.get(src.numel())
+        if pin is None:
+            pin = self._pins[src.numel()] = torch.empty(src.numel(), dtype=torch.float64, pin_memory=True)
+        self.store_host(src, pin)
+        torch.cuda.current_stream(src.device).synchronize()
+        return pin.numpy().reshape(tuple(src.shape)).copy()
 
     def one_norm(self, A: MatBatch, norms_dev):
         a = cmat(A)

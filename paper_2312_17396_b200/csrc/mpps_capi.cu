@@ -1140,6 +1140,14 @@ int mpps_one_norm_complex(mpps_handle *h, const mpps_mat *A, int nc, double *nor
 // every batch member b and level j, e = -rint(log2 ||B_j||) (0 for a zero or
 // non-finite norm); exps[j][b] = e where bit j of fp32_mask is set, else 0;
 // exp_y[b] = e of ||Y|| (norms column r+1).
+// stores into a pinned, device-mapped host buffer (mpps_store_host)
+__global__ void store_host_kernel(const double *src, double *dst, long long n) {
+  MPPS_PDL_ENTER();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+  __threadfence_system();
+}
+
 __global__ void level_exps_kernel(const double *norms, int batch, int r, unsigned long long fp32_mask, int *exps,
                                   int *exp_y) {
   MPPS_PDL_ENTER();
@@ -1162,6 +1170,14 @@ int mpps_level_exps(mpps_handle *h, const double *norms, int batch, int r, unsig
   if (n == 0) return MPPS_OK;
   launch_k(level_exps_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, h->stream, norms, batch, r, fp32_mask, exps, exp_y);
   return after_launch(h, "level_exps_kernel");
+}
+
+int mpps_store_host(mpps_handle *h, const double *src, double *dst_pinned, long long n) {
+  if (!src || !dst_pinned || n < 0) return set_err(h, MPPS_EINVAL, "store_host: bad arguments");
+  if (n == 0) return MPPS_OK;
+  launch_k(store_host_kernel, dim3((unsigned)((n + 255) / 256 > 64 ? 64 : (n + 255) / 256)), dim3(256), 0, h->stream, src,
+           dst_pinned, n);
+  return after_launch(h, "store_host_kernel");
 }
 
 int mpps_horner_scalar_top(mpps_handle *h, const double *bm, int fmt_top, const mpps_mat *Y, const mpps_mat *Bprev,

@@ -418,7 +418,7 @@ def _assemble(h, powers: List[MatBatch], series: CoefficientSeries, ctx: Precisi
         if not sync:
             return _Prepared(wf, s, r, m, powers, blocks, None, cw, norms, lowp=True)
         timer.start("norm_estimation")
-        norms_h = norms.cpu().numpy()
+        norms_h = h.host_array(norms)
         timer.stop()
         return _Prepared(wf, s, r, m, powers, blocks, norms_h, cw, norms, lowp=True)
     hc = h.assemble_hc_supported(wf, s, m)
@@ -443,7 +443,7 @@ def _assemble(h, powers: List[MatBatch], series: CoefficientSeries, ctx: Precisi
     if not sync:
         return _Prepared(wf, s, r, m, powers, blocks, None, cw, norms)
     timer.start("norm_estimation")
-    norms_h = norms.cpu().numpy()   # the one host sync of the pipeline
+    norms_h = h.host_array(norms)   # the one host sync of the pipeline (no copy engine: _lib.host_array)
     timer.stop()
     return _Prepared(wf, s, r, m, powers, blocks, norms_h, cw, norms)
 

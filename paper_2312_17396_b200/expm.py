@@ -59,7 +59,7 @@ def expm_ss(A, ctx: PrecisionCtx, m: int = DEFAULT_M, delta: float = 10.0, timin
     B, n = Aw.batch, Aw.rows
     normsA = torch.empty(B, dtype=torch.float64, device=Aw.device)
     h.one_norm(Aw, normsA)
-    ells = scaling_of(normsA.cpu().numpy(), m)
+    ells = scaling_of(h.host_array(normsA), m)
     wf = ctx.fmt if ctx.fmt != 7 else FP64
     # X = 2^-l A, exact (the widening to the working format is exact too)
     X = MatBatch.empty(wf, B, n, device=Aw.device)

@@ -128,8 +128,11 @@ def submit(key: tuple, Xsrc, build_pre, timer, slot: int = 0) -> Optional[Pendin
             l0 = _lib.total_launches()
             with torch.cuda.graph(g.pre, pool=g.pool):
                 g.prep = build_pre(g.x_in, capture=True)
+                # the norms reach the host through a kernel's stores into pinned memory, not a
+                # memcpy node: a device-to-host copy queues behind a running result download of
+                # the host stream (pipeline.evaluate_host) and the planner would wait for it
                 g.norms_pin = torch.empty(g.prep.norms_dev.shape, dtype=torch.float64, pin_memory=True)
-                g.norms_pin.copy_(g.prep.norms_dev, non_blocking=True)
+                _lib.handle_for().store_host(g.prep.norms_dev.contiguous(), g.norms_pin)
             g.pre_launches = _lib.total_launches() - l0
             _CACHE[key] = g
         g.x_in.copy_(Xsrc, non_blocking=True)

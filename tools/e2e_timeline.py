@@ -14,14 +14,18 @@ K = 10
 Xbig = torch.cat([wl.Xpin[t % wl.pool] for t in range(K)]).pin_memory()
 out = torch.empty((2,) + tuple(Xbig.shape), dtype=torch.float64).pin_memory()
 sub = pl.mixed_exp(wl.m, wl.ctx, timing=False)
-sizes = [32, 32] * K
+sizes = [64] * K if "full" in sys.argv else [32, 32] * K
+ST = 1 if "full" in sys.argv else 2
+WIN = 4 if "full" in sys.argv else 6
 for _ in range(2):
-    pl.evaluate_host(sub, Xbig, out, sizes, streams=2, window=6)
+    pl.evaluate_host(sub, Xbig, out, sizes, streams=ST, ahead=True, window=WIN)
 torch.cuda.synchronize()
 tr = []
 t0 = torch.cuda.Event(enable_timing=True)
 t0.record()
-pl.evaluate_host(sub, Xbig, out, sizes, streams=2, window=6, trace=tr)
+th0 = __import__('time').perf_counter()
+pl.evaluate_host(sub, Xbig, out, sizes, streams=ST, ahead=True, window=WIN, trace=tr)
+th1 = __import__('time').perf_counter()
 t1 = torch.cuda.Event(enable_timing=True)
 t1.record()
 torch.cuda.synchronize()
@@ -32,9 +36,9 @@ rows = []
 for c in range(len(sizes)):
     g = lambda k: (ev.get(f"{k}{c}<", (np.nan, 0))[0], ev.get(f"{k}{c}>", (np.nan, 0))[0])
     rows.append((c,) + g("up") + g("pre") + g("post") + g("down") + ((ev[f"post{c}<"][1] - h0) * 1e3,))
-print(f"total {total:.3f} ms for {K} steps -> {64 * K / total * 1e3:.0f} evals/s")
+print(f"total {total:.3f} ms for {K} steps -> {64 * K / total * 1e3:.0f} evals/s; host returned after {(th1-th0)*1e3:.3f} ms")
 print("chunk  up[<,>]  pre[<,>] post[<,>] down[<,>]  host_post_issue(ms)")
-for r in rows[:8] + rows[-4:]:
+for r in rows[:12] + rows[-4:]:
     print(" ".join(f"{x:7.3f}" if isinstance(x, float) else f"{x:3d}" for x in r))
 down = sum(r[8] - r[7] for r in rows)
 up = sum(r[2] - r[1] for r in rows)
