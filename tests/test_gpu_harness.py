@@ -189,3 +189,39 @@ def test_c7a_bound_containment_device(cuda):
         assert err <= bound, (trial, float(err), float(bound))
         checked += 1
     assert checked >= 20
+
+
+def test_store_host_moves_planner_norms_without_the_copy_engine(cuda):
+    """mpps_store_host / Handle.host_array: a kernel's stores into pinned
+    memory deliver the exact values, also while a large device-to-host copy
+    occupies the copy engine on another stream (the situation of the host
+    stream, where a memcpy of the norms would wait for that copy)."""
+    import time
+    import torch
+    from paper_2312_17396_b200 import _lib
+    h = _lib.handle_for()
+    src = torch.randn(64, 7, dtype=torch.float64, device="cuda")
+    got = h.host_array(src)
+    assert got.shape == (64, 7) and np.array_equal(got, src.cpu().numpy())
+    pin = torch.empty(src.numel(), dtype=torch.float64).pin_memory()
+    h.store_host(src.reshape(-1).contiguous(), pin)
+    torch.cuda.synchronize()
+    assert np.array_equal(pin.numpy().reshape(64, 7), src.cpu().numpy())
+    with pytest.raises(ValueError):
+        h.store_host(src, torch.empty(src.numel(), dtype=torch.float64))      # not pinned
+    # behind a 512 MiB download on another stream the kernel path returns long before the copy ends
+    big = torch.empty(64 << 20, dtype=torch.float64, device="cuda")
+    big_h = torch.empty(64 << 20, dtype=torch.float64).pin_memory()
+    side = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(side):
+        big_h.copy_(big, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(side)
+    t0 = time.perf_counter()
+    got = h.host_array(src)
+    t_kernel = time.perf_counter() - t0
+    finished_early = not done.query()
+    done.synchronize()
+    assert np.array_equal(got, src.cpu().numpy())
+    assert finished_early, f"host_array took {t_kernel * 1e3:.2f} ms: it waited for the download"
