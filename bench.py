@@ -41,7 +41,6 @@ import math
 import os
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -99,94 +98,81 @@ def _grid_shape(world):
 
 
 # ----------------------------------------------------------------- clocks
+_SAMPLER_SRC = r"""
+import sys, time
+period = float(sys.argv[2])
+try:
+    import pynvml as nv
+    nv.nvmlInit()
+    hdl = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+    get = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+    bits = (nv.nvmlClocksThrottleReasonHwSlowdown, nv.nvmlClocksThrottleReasonHwThermalSlowdown,
+            nv.nvmlClocksThrottleReasonSwThermalSlowdown, nv.nvmlClocksThrottleReasonSwPowerCap)
+    print("max", float(nv.nvmlDeviceGetMaxClockInfo(hdl, nv.NVML_CLOCK_SM)), flush=True)
+    while True:
+        r = int(get(hdl))
+        print(time.monotonic(), float(nv.nvmlDeviceGetClockInfo(hdl, nv.NVML_CLOCK_SM)),
+              "".join("1" if r & b else "0" for b in bits), flush=True)
+        time.sleep(period)
+except Exception as e:
+    print("error", repr(e)[:200], flush=True)
+"""
+
+
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled DURING the timed
-    region: an NVML polling thread (~0.5 ms period, so even a few-ms region
-    gets many samples); nvidia-smi -lms 200 when NVML is unavailable."""
+    region by a separate process polling NVML (2 ms period; CLOCK_MONOTONIC
+    timestamps, the bench keeps the samples inside [start, stop]).  A polling
+    thread inside this process made the device-resident cfg2 loop bimodal
+    (57K or 27-35K evals/s from run to run: its NVML calls and the GIL
+    hand-overs delay the step's graph launches; 8 of 8 runs at 57-58K
+    without it), hence the process."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, index):
-        self.index = index
-        self.proc = None
-        self.lines = []
-        self.nvml = None
-        self.samples = []
-        self.running = False
-
-    def start(self):
+    def __init__(self, index, period=0.002):
+        self.t0 = self.t1 = None
         try:
-            import pynvml as nv
-            nv.nvmlInit()
-            self.nvml = nv
-            self.hdl = nv.nvmlDeviceGetHandleByIndex(self.index)
-            self.smax = float(nv.nvmlDeviceGetMaxClockInfo(self.hdl, nv.NVML_CLOCK_SM))
-            get = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
-                nv.nvmlDeviceGetCurrentClocksThrottleReasons
-            self.bits = (nv.nvmlClocksThrottleReasonHwSlowdown, nv.nvmlClocksThrottleReasonHwThermalSlowdown,
-                         nv.nvmlClocksThrottleReasonSwThermalSlowdown, nv.nvmlClocksThrottleReasonSwPowerCap)
-            self.running = True
-
-            def poll():
-                while self.running:
-                    try:
-                        self.samples.append((float(nv.nvmlDeviceGetClockInfo(self.hdl, nv.NVML_CLOCK_SM)),
-                                             int(get(self.hdl))))
-                    except Exception:
-                        pass
-                    time.sleep(0.0005)
-            self.thread = threading.Thread(target=poll, daemon=True)
-            self.thread.start()
-            return
-        except Exception:
-            self.nvml = None
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER_SRC, str(index), str(period)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def start(self):
+        self.t0 = time.monotonic()
 
     def stop(self):
-        if self.nvml is not None:
-            self.running = False
-            self.thread.join(timeout=2)
-            sm = [c for c, _ in self.samples]
-            reasons = {nm for _, r in self.samples for nm, bit in zip(self.NAMES, self.bits) if r & bit}
-            return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.smax,
-                    "reasons": sorted(reasons), "samples": len(sm), "source": "nvml"}
+        self.t1 = time.monotonic()
         if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampler unavailable"]}
+        time.sleep(0.005)
         self.proc.terminate()
         try:
-            self.proc.wait(timeout=5)
+            out, _ = self.proc.communicate(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, smax, reasons = [], None, set()
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
+            out = ""
+        smax, sm, reasons, err = None, [], set(), None
+        for ln in out.splitlines():
+            parts = ln.split()
+            if not parts:
                 continue
-            try:
-                sm.append(float(parts[0]))
+            if parts[0] == "max":
                 smax = float(parts[1])
-            except ValueError:
-                continue
-            for nm, v in zip(self.NAMES, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi"}
+            elif parts[0] == "error":
+                err = " ".join(parts[1:])
+            elif len(parts) == 3:
+                try:
+                    t, c = float(parts[0]), float(parts[1])
+                except ValueError:
+                    continue
+                if self.t0 <= t <= self.t1:
+                    sm.append(c)
+                    reasons.update(nm for nm, bit in zip(self.NAMES, parts[2]) if bit == "1")
+        if err and not sm:
+            return {"sm_mhz": None, "sm_max_mhz": smax, "reasons": [f"clock sampler: {err}"]}
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm), "source": "nvml (separate process, 2 ms period)"}
 
 
 # ------------------------------------------------------------- peaks
@@ -561,6 +547,8 @@ def run_ours(name, args, rank, world, local_rank, dist):
     import paper_2312_17396_b200 as mp
     from paper_2312_17396_b200 import _lib, graphs as _graphs
 
+    # the clock sampler process starts now, so that it is polling by the time the warm-up is over
+    clocks = ClockSampler(local_rank) if (rank == 0 and not args.no_clocks) else None
     wl = Workload(name, rank, world, torch, mp, args.scaling, args.steps, args.warmup)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     h = _lib.handle_for()
@@ -579,7 +567,7 @@ def run_ours(name, args, rank, world, local_rank, dist):
         torch.cuda.synchronize()
 
     # ---- device-resident timed region (value): step t reads input t ----
-    clocks = ClockSampler(local_rank) if (rank == 0 and not args.no_clocks) else None
+
     spec0 = _graphs.speculation_stats()
     barrier()
     if clocks:
