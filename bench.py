@@ -690,6 +690,12 @@ def run_ours(name, args, rank, world, local_rank, dist):
         del rep
         Xs = [wl.Xpin[t % P] for t in range(args.steps)]
         outl = [outs[t % 2] for t in range(args.steps)]
+        # one untimed pass over the distinct inputs of the pool: every plan
+        # structure of the stream has its Horner graph captured before the
+        # timed region (as the warm-up pass of the batched host stream above)
+        _pl.evaluate_stream(wl.step, Xs[:min(args.steps, P)], outl[:min(args.steps, P)], wl.results,
+                            keep_reports=False)
+        torch.cuda.synchronize()
         flush.zero_()
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
