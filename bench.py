@@ -121,7 +121,7 @@ except Exception as e:
 
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled DURING the timed
-    region by a separate process polling NVML (2 ms period; CLOCK_MONOTONIC
+    region by a separate process polling NVML (1 ms period; CLOCK_MONOTONIC
     timestamps, the bench keeps the samples inside [start, stop]).  A polling
     thread inside this process made the device-resident cfg2 loop bimodal
     (57K or 27-35K evals/s from run to run: its NVML calls and the GIL
@@ -130,11 +130,14 @@ class ClockSampler:
 
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, index, period=0.002):
+    def __init__(self, index, period=0.001):
         self.t0 = self.t1 = None
         try:
+            import tempfile
+            # samples go to a file, not a pipe: a full pipe would block the sampler mid-run
+            self.log = tempfile.NamedTemporaryFile("w+", prefix="mpps_clocks_", suffix=".txt", delete=False)
             self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER_SRC, str(index), str(period)],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                                         stdout=self.log, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
 
@@ -148,9 +151,15 @@ class ClockSampler:
         time.sleep(0.005)
         self.proc.terminate()
         try:
-            out, _ = self.proc.communicate(timeout=5)
+            self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
+        try:
+            self.log.flush()
+            out = open(self.log.name).read()
+            self.log.close()
+            os.unlink(self.log.name)
+        except Exception:
             out = ""
         smax, sm, reasons, err = None, [], set(), None
         for ln in out.splitlines():
@@ -172,7 +181,7 @@ class ClockSampler:
         if err and not sm:
             return {"sm_mhz": None, "sm_max_mhz": smax, "reasons": [f"clock sampler: {err}"]}
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm), "source": "nvml (separate process, 2 ms period)"}
+                "samples": len(sm), "source": "nvml (separate process, 1 ms period)"}
 
 
 # ------------------------------------------------------------- peaks
