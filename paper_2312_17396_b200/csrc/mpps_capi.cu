@@ -1412,9 +1412,6 @@ static oz::SliceRef sref(const mpps_slices *s) {
   return r;
 }
 
-// column split with the exponents in the same kernel (MPPS_OZ_COLS_FUSED=1).
-// Measured slower at cfg2 (dd split 37 + 8 -> 66 us: one CTA per 32-column
-// strip leaves too few CTAs in flight), so off by default.
 // MPPS_OZ_COLS_FIXED=0 restores slice_cols_kernel (32 x 32 tiles) for 8-bit splits
 static bool oz_cols_fixed() {
   static int v = -1;
@@ -1424,27 +1421,6 @@ static bool oz_cols_fixed() {
   }
   return v != 0;
 }
-// MPPS_OZ_COLS_CLUSTER=1: one-pass cluster column split for K <= 256.  Off by
-// default: at cfg2 it measured 40.5 / 36.7 / 36.3 us for <2,14> / <2,10> /
-// <1,14> against 39.5 / 35.9 / 33.0 for col_exps_kernel + slice_cols_kernel
-// (the cluster barrier between the loads and the split serialises them)
-static bool oz_cols_cluster() {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("MPPS_OZ_COLS_CLUSTER");
-    v = e ? atoi(e) : 0;
-  }
-  return v != 0;
-}
-static bool oz_cols_fused() {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("MPPS_OZ_COLS_FUSED");
-    v = e ? atoi(e) : 0;
-  }
-  return v != 0;
-}
-
 static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices *out, const int *sel, int nsel,
                       int row0, int nrows, int mode = 0);
 
@@ -1520,41 +1496,6 @@ static int slice_impl(mpps_handle *h, const mpps_mat *src, int side, mpps_slices
     return set_err(h, MPPS_EINVAL, "slice: no row kernel for %d words x %d planes", W, S);
 #undef SR
     return after_launch(h, "slice_rows_kernel");
-  }
-  if (oz_cols_fused() && nrows < 0 && mode == 0) {
-    dim3 grid(out->rpad / 32, nb);
-#define SCF(WW, SS) \
-  if (W == WW && S == SS) launch_k(oz::slice_cols_fused_kernel<WW, SS>, dim3(grid), dim3(256), 0, h->stream, ref_of(src), src->rows, src->cols, fi, o, sel); else
-    SCF(1, 4) SCF(1, 8) SCF(1, 14) SCF(1, 16) SCF(1, 28) SCF(1, 31) SCF(2, 4) SCF(2, 8) SCF(2, 14) SCF(2, 16) SCF(2, 28)
-    SCF(2, 31) SCF(4, 4) SCF(4, 8) SCF(4, 14) SCF(4, 16) SCF(4, 28) SCF(4, 31)
-    SCF(1, 2) SCF(1, 3) SCF(1, 5) SCF(1, 6) SCF(2, 2) SCF(2, 3) SCF(2, 5) SCF(2, 6) SCF(2, 10) SCF(2, 12)
-    return set_err(h, MPPS_EINVAL, "slice: no column kernel for %d words x %d planes", W, S);
-#undef SCF
-    return after_launch(h, "slice_cols_fused_kernel");
-  }
-  if (slice_db(out) == 8 && W <= 2 && S <= 14 && out->kpad / 32 <= 8 && oz_cols_cluster() && mode == 0) {
-    // one cluster of kpad/32 CTAs per 32-column strip: exponents and digits in one pass
-    const unsigned ky = (unsigned)(out->kpad / 32);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(gx, ky, nb);
-    cfg.blockDim = dim3(256);
-    cfg.stream = h->stream;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 1;
-    at[0].val.clusterDim.y = ky;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled() ? 2 : 1;
-#define SCC(WW, SS) \
-  if (W == WW && S == SS) cudaLaunchKernelEx(&cfg, oz::slice_cols_cluster_kernel<WW, SS>, ref_of(src), src->rows, src->cols, fi, o, sel); else
-    SCC(1, 2) SCC(1, 3) SCC(1, 4) SCC(1, 5) SCC(1, 6) SCC(1, 8) SCC(1, 10) SCC(1, 12) SCC(1, 14)
-    SCC(2, 2) SCC(2, 3) SCC(2, 4) SCC(2, 5) SCC(2, 6) SCC(2, 8) SCC(2, 10) SCC(2, 12) SCC(2, 14)
-    return set_err(h, MPPS_EINVAL, "slice: no cluster column kernel for %d words x %d planes", W, S);
-#undef SCC
-    return after_launch(h, "slice_cols_cluster_kernel");
   }
   if (mode == 0) {
     launch_k(oz::col_exps_kernel, dim3(dim3(gx, nb)), dim3(256), 0, h->stream, ref_of(src), src->rows, src->cols, fi, o,
@@ -1713,8 +1654,6 @@ static int dispatch_oz_tma64(mpps_handle *h, int S, int fo, int mode, const oz::
   return set_err(h, MPPS_EFMT, "tensor-core GEMM (NT=64): no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
 }
 
-static int dispatch_oz(mpps_handle *h, int S, int fo, int mode, const oz::OzArgs &a, int nb);
-
 // 16 epilogue warps for the staged dd ring kernels (MPPS_OZ_EW=8 selects 8)
 static int oz_ring_ew() {
   static int v = -1;
@@ -1758,80 +1697,6 @@ static int dispatch_oz_ring(mpps_handle *h, int S, int fo, int mode, const oz::O
   OZ(31, 16, QD, 0) OZ(31, 16, QD, 1)
 #undef OZ
   return set_err(h, MPPS_EFMT, "tensor-core GEMM: no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
-}
-
-template <int S, int NT, int FO, int MODE, int CL>
-static int launch_oz_pers(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
-  constexpr size_t smem = oz::OzPers<S, NT>::SMEM;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_pers_kernel<S, NT, FO, MODE, CL>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz pers attr: %s", cudaGetErrorString(e));
-    configured = true;
-  }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-    const char *cap = getenv("MPPS_OZ_SMS");   // diagnostics: cap the persistent grid
-    if (cap && atoi(cap) > 0 && atoi(cap) < sms) sms = atoi(cap);
-  }
-  oz::OzTmaArgs t = a;
-  t.mtiles = (a.M + oz::kTileM - 1) / oz::kTileM;
-  t.ntiles = (a.N + NT - 1) / NT;
-  t.group = oz_group();
-  t.nbatch = nb;
-  if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
-  const long long groups = (long long)nb * t.mtiles * ((t.ntiles + CL - 1) / CL);
-  const long long maxg = sms / CL;
-  cudaLaunchConfig_t cfg;
-  memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3((unsigned)(CL * (groups < maxg ? groups : maxg)), 1, 1);
-  cfg.blockDim = dim3(oz::kThreadsPers, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = h->stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, oz::oz_gemm_pers_kernel<S, NT, FO, MODE, CL>, t);
-  if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz pers launch: %s", cudaGetErrorString(e));
-  return after_launch(h, "oz_gemm_pers_kernel");
-}
-
-template <int S, int NT, int FO, int MODE>
-static int launch_oz_pwide(mpps_handle *h, const oz::OzTmaArgs &a, int nb) {
-  constexpr size_t smem = oz::OzPWide<S, NT>::SMEM;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_pwide_kernel<S, NT, FO, MODE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz pwide attr: %s", cudaGetErrorString(e));
-    configured = true;
-  }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  oz::OzTmaArgs t = a;
-  t.mtiles = (a.M + oz::kTileM - 1) / oz::kTileM;
-  t.ntiles = (a.N + NT - 1) / NT;
-  t.group = oz_group();
-  t.nbatch = nb;
-  if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
-  const long long tiles = (long long)nb * t.mtiles * t.ntiles;
-  oz::oz_gemm_pwide_kernel<S, NT, FO, MODE><<<(unsigned)(tiles < sms ? tiles : sms), oz::kThreadsPers, smem,
-                                              h->stream>>>(t);
-  return after_launch(h, "oz_gemm_pwide_kernel");
 }
 
 // Persistent 128-byte-box kernel with 16 epilogue warps for the 8-bit dd
@@ -1894,18 +1759,6 @@ static int dispatch_oz_pw16(mpps_handle *h, int S, int fo, int mode, int K, cons
   if (S == 14 && fo == DD)
     return K >= 1024 ? launch_oz_pw16<14, 32, 8, 2, DD, 1>(h, t, nb) : launch_oz_pw16<14, 32, 8, 1, DD, 1>(h, t, nb);
   return set_err(h, MPPS_EFMT, "persistent tensor-core GEMM: no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
-}
-
-// persistent double-buffered kernel for the dd power-chain GEMMs:
-// MPPS_OZ_PERS = 0 (default) off, 1 single CTAs, 2 CTA pairs multicasting A, 3 persistent with 128-byte K
-// boxes (oz_gemm_pwide_kernel); measured no faster than the ring kernel (DESIGN 5.1)
-static int oz_pers_mode(int S, int fo, int mode) {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("MPPS_OZ_PERS");
-    v = e ? atoi(e) : 0;
-  }
-  return (S == 16 && fo == DD && mode == 0) ? v : 0;
 }
 
 static int oz_wide_cluster() {   // MPPS_OZ_WIDE_MC=0: one CTA per tile, no A multicast
@@ -1993,15 +1846,15 @@ static int dispatch_oz_wide(mpps_handle *h, int S, int fo, int mode, const oz::O
   return set_err(h, MPPS_EFMT, "wide tensor-core GEMM: no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
 }
 
-static int oz_mode() {   // 0 cp.async, 1 TMA stage ring, 2 TMA streamed planes, 3 (default) streamed for S >= 16
+// MPPS_OZ_TMA=2: the streamed-plane ring kernel also below 14 planes (diagnostics); default: ring for dd / qd
+static int oz_mode() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("MPPS_OZ_TMA");
-    v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 3;
+    v = (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 3;
   }
   return v;
 }
-
 
 // diagnostics: per-CTA phase timestamps of the next TMA-fed GEMMs
 static unsigned long long *g_oz_trace = nullptr;
@@ -2009,21 +1862,18 @@ static int g_oz_dbg = 0;
 
 static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, int S, int fo, int mode,
                   const oz::OzArgs &a, int nb) {
-  if (oz_mode() == 0) return dispatch_oz(h, S, fo, mode, a, nb);
   oz::OzTmaArgs t;
   memset(&t, 0, sizeof(t));
   const bool pw16 = oz_pw16_for(S, fo, mode, a.K, slice_db(A), a);
   const bool wide = !pw16 && oz_wide_for(S, fo, mode, a.K);
-  const int pmode = (wide || pw16) ? 0 : oz_pers_mode(S, fo, mode);
-  const bool pers = pmode != 0;
-  // default: streamed-plane ring for dd / qd (S >= 16), 2-4 stage TMA ring below
-  const bool ring = pers || oz_mode() == 2 || (oz_mode() == 3 && S >= 14) || S == 14 || S == 28;
+  // default: streamed-plane ring for dd / qd (S >= 14), 2-4 stage TMA ring below
+  const bool ring = oz_mode() == 2 || S >= 14;
   const bool nt128 = !wide && !ring && oz_nt128_for(S, fo, mode, a.K, slice_db(A));
   const bool nt64 = !wide && !ring && !nt128 && oz_nt64_for(S, fo, mode);
-  const int NT = wide ? oz_wide_nt(S, mode) : (S > 16 || pers) ? 16 : (nt128 ? 128 : nt64 ? 64 : 32);
+  const int NT = wide ? oz_wide_nt(S, mode) : S > 16 ? 16 : (nt128 ? 128 : nt64 ? 64 : 32);
   const int abox = ring ? (S < 4 ? S : (S == 14 ? 7 : 4)) : S;   // OzRing<S, NT>::SG
   int rc;
-  if (wide || pmode == 3 || pw16) {
+  if (wide || pw16) {
     if ((rc = make_slice_map(h, &t.mapA, A, oz::kTileM, 1, 128)) || (rc = make_slice_map(h, &t.mapB, B, NT, S, 128)))
       return rc;
   } else if ((rc = make_slice_map(h, &t.mapA, A, oz::kTileM, abox)) || (rc = make_slice_map(h, &t.mapB, B, NT, S))) {
@@ -2034,37 +1884,9 @@ static int run_oz(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, in
   t.dbg = g_oz_dbg;
   if (wide) return dispatch_oz_wide(h, S, fo, mode, t, nb);
   if (pw16) return dispatch_oz_pw16(h, S, fo, mode, a.K, t, nb);
-  if (pmode == 3) return launch_oz_pwide<16, 16, DD, 0>(h, t, nb);
-  if (pmode == 1) return launch_oz_pers<16, 16, DD, 0, 1>(h, t, nb);
-  if (pmode == 2) return launch_oz_pers<16, 16, DD, 0, 2>(h, t, nb);
   if (nt128) return dispatch_oz_tma128(h, S, fo, t, nb);
   if (nt64) return dispatch_oz_tma64(h, S, fo, mode, t, nb);
   return ring ? dispatch_oz_ring(h, S, fo, mode, t, nb) : dispatch_oz_tma(h, S, fo, mode, t, nb);
-}
-
-template <int S, int NT, int FO, int MODE>
-static int launch_oz(mpps_handle *h, const oz::OzArgs &a, int nb) {
-  constexpr size_t smem = oz::oz_smem_bytes<S, NT>();
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(oz::oz_gemm_kernel<S, NT, FO, MODE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "oz attr: %s", cudaGetErrorString(e));
-    configured = true;
-  }
-  dim3 grid((a.N + NT - 1) / NT, (a.M + oz::kTileM - 1) / oz::kTileM, nb);
-  if (nb == 0 || a.M == 0 || a.N == 0) return MPPS_OK;
-  oz::oz_gemm_kernel<S, NT, FO, MODE><<<grid, oz::kThreadsOz, smem, h->stream>>>(a);
-  return after_launch(h, "oz_gemm_kernel");
-}
-
-static int dispatch_oz(mpps_handle *h, int S, int fo, int mode, const oz::OzArgs &a, int nb) {
-#define OZ(SS, NT, FF, MM) if (S == SS && fo == FF && mode == MM) return launch_oz<SS, NT, FF, MM>(h, a, nb);
-  OZ(8, 32, F64, 0) OZ(8, 32, F64, 1) OZ(8, 32, DD, 1) OZ(8, 32, QD, 1)
-  OZ(16, 32, DD, 0) OZ(16, 32, DD, 1) OZ(16, 32, QD, 1)
-  OZ(31, 16, QD, 0) OZ(31, 16, QD, 1)
-#undef OZ
-  return set_err(h, MPPS_EFMT, "tensor-core GEMM: no kernel for %d slices -> format %d (mode %d)", S, fo, mode);
 }
 
 static int check_sliced(mpps_handle *h, const mpps_slices *A, const mpps_slices *B, int S, int M, int N, int K) {

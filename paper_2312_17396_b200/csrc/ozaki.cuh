@@ -30,7 +30,6 @@ namespace oz {
 
 constexpr int kTileM = 128;
 constexpr int kKStep = 32;      // int8 MMA K per instruction (32 bytes)
-constexpr int kThreadsOz = 128;
 constexpr int kThreadsEpi = 256;   // TMA/ring kernels: 8 warps (producer, MMA issuer, 8 epilogue)
 
 // ------------------------------------------------------------ PTX helpers
@@ -852,127 +851,6 @@ __global__ void slice_cols_kernel(MatRef B, int rows, int cols, int fi, SliceRef
   }
 }
 
-// Column exponents and digits in one pass for K <= 256 (8-bit digits, <= 14
-// planes): the kpad/32 CTAs of a 32-column strip form one thread-block
-// cluster; each CTA loads its 32 x 32 tile once (4 consecutive k per thread),
-// publishes its partial column maxima in shared memory, reads the other CTAs'
-// over DSMEM, and splits the registers it already holds.  Replaces
-// col_exps_kernel's separate pass over the matrix (3 launches per cfg2 step).
-template <int W, int S>
-__global__ void __launch_bounds__(256) slice_cols_cluster_kernel(MatRef B, int rows, int cols, int fi, SliceRef out,
-                                                                 const int *sel) {
-  MPPS_PDL_ENTER();
-  namespace cg = cooperative_groups;
-  static_assert(W <= 2 && S <= 14, "fixed-point column split");
-  __shared__ __align__(16) uint32_t tw[S][32][9];
-  __shared__ double red[8][33];
-  __shared__ double cmax[32];
-  __shared__ int ecs[32];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int j0 = blockIdx.x * 32, j = j0 + tx;
-  const int k0 = blockIdx.y * 32, kb0 = k0 + 4 * ty;
-  const int b = sel ? sel[blockIdx.z] : (int)blockIdx.z;
-  double h[4], l[4];
-  double mx = 0.0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int k = kb0 + q;
-    h[q] = 0.0;
-    l[q] = 0.0;
-    if (k < rows && j < cols) {
-      const long long off = (long long)b * B.bstride + (long long)k * B.ld + j;
-      if (fi == F32) {
-        h[q] = (double)((const float *)B.data)[off];
-      } else {
-        h[q] = ((const double *)B.data)[off];
-        if constexpr (W > 1) l[q] = ((const double *)B.data)[off + B.plane];
-      }
-    }
-    mx = fmax(mx, fabs(h[q]));
-  }
-  red[ty][tx] = mx;
-  __syncthreads();
-  if (ty == 0) {
-#pragma unroll
-    for (int g = 1; g < 8; ++g) mx = fmax(mx, red[g][tx]);
-    cmax[tx] = mx;
-  }
-  cluster.sync();                                   // every CTA's partial maxima visible
-  if (ty == 0) {
-    const int nr = (int)cluster.num_blocks();
-    double m = 0.0;
-    for (int r = 0; r < nr; ++r) m = fmax(m, cluster.map_shared_rank(cmax, r)[tx]);
-    const int e = row_exponent(m);
-    ecs[tx] = e;
-    if (blockIdx.y == 0 && out.row0 + j < out.rpad && j < out.nrows) out.exps[(long long)b * out.rpad + out.row0 + j] = e;
-  }
-  cluster.sync();                                   // remote reads done (no CTA exits early); ecs visible
-  double p1, p2;
-  fixed_scale<S>(j < cols ? ecs[tx] : 0, p1, p2);
-  unsigned __int128 Y[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) Y[q] = fixed_biased_fp<W, S>(h[q], l[q], p1, p2);
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const int kb = S - 1 - s, wj = kb >> 2, bsel = kb & 3;
-    const uint32_t lo = __byte_perm(fixed_word(Y[0], wj), fixed_word(Y[1], wj), bsel | ((bsel + 4) << 4));
-    const uint32_t hi = __byte_perm(fixed_word(Y[2], wj), fixed_word(Y[3], wj), bsel | ((bsel + 4) << 4));
-    uint32_t wv = __byte_perm(lo, hi, 0x5410);
-    if (s > 0) wv ^= 0x80808080u;
-    tw[s][tx][ty] = wv;
-  }
-  __syncthreads();
-  const long long plane = out.plane();
-  const int jj = threadIdx.x >> 3, kq = threadIdx.x & 7;
-  const int jo = j0 + jj;
-  if (out.row0 + jo < out.rpad && jo < out.nrows && k0 + 4 * kq < out.kpad)
-#pragma unroll
-    for (int s = 0; s < S; ++s)
-      *reinterpret_cast<uint32_t *>(out.digits + s * plane + ((long long)b * out.rpad + out.row0 + jo) * out.kpad + k0 +
-                                    4 * kq) = tw[s][jj][kq];
-}
-
-// Column exponents and digits in one kernel: a CTA owns a strip of 32
-// columns over all K rows (its column maxima first, then the 32 x 32 tiles
-// of the strip; the second read of the strip hits L1/L2).  Saves the
-// separate col_exps pass over the matrix.
-template <int W, int S>
-__global__ void slice_cols_fused_kernel(MatRef B, int rows, int cols, int fi, SliceRef out, const int *sel) {
-  MPPS_PDL_ENTER();
-  __shared__ __align__(16) int8_t tile[S][32][36];
-  __shared__ double red[8][33];
-  __shared__ int ecs[32];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int j = blockIdx.x * 32 + tx;
-  const int bz = blockIdx.y;
-  const int b = sel ? sel[bz] : bz;
-  double mx = 0.0;
-  if (j < cols)
-    for (int k = ty; k < rows; k += 8) {
-      const long long off = (long long)b * B.bstride + (long long)k * B.ld + j;
-      mx = fmax(mx, fabs(fi == F32 ? (double)((const float *)B.data)[off] : ((const double *)B.data)[off]));
-    }
-  red[ty][tx] = mx;
-  __syncthreads();
-  if (ty == 0) {
-#pragma unroll
-    for (int g = 1; g < 8; ++g) mx = fmax(mx, red[g][tx]);
-    const int e = row_exponent(mx);
-    ecs[tx] = e;
-    if (j < out.rpad) out.exps[(long long)b * out.rpad + j] = e;
-  }
-  __syncthreads();
-  for (int k0 = 0; k0 < out.kpad; k0 += 32) {
-    if (oz_db_of<S>(out.db) == 8) {
-      if constexpr (S != 16 && S != 31) slice_cols_body<W, S, 8>(B, rows, cols, fi, out, sel, tile, k0, bz, ecs);
-    } else {
-      if constexpr (oz_has7<S>()) slice_cols_body<W, S, 7>(B, rows, cols, fi, out, sel, tile, k0, bz, ecs);
-    }
-    __syncthreads();    // the tile is rewritten by the next K step
-  }
-}
-
 // -------------------------------------------------------------- GEMM
 struct OzArgs {
   SliceRef A, B;   // A: rows = M (row-scaled); B: rows = N (transposed B, col-scaled)
@@ -986,12 +864,8 @@ struct OzArgs {
 // Smem per stage: S slices of A (128 x 32 B) + S slices of B (NT x 32 B).
 template <int S, int NT>
 __host__ __device__ constexpr size_t oz_stage_bytes() { return (size_t)S * (kTileM + NT) * kKStep; }
-template <int S, int NT>
-__host__ __device__ constexpr int oz_stages() { return 2 * oz_stage_bytes<S, NT>() + 1024 <= 200 * 1024 ? 2 : 1; }
-template <int S, int NT>
-__host__ __device__ constexpr size_t oz_smem_bytes() { return oz_stages<S, NT>() * oz_stage_bytes<S, NT>() + 256; }
 
-// value of sum_d D_d 2^-(12+DB d) as a qd (exact grouping in threes)
+// sum_d D_d 2^-(12+DB d) as a qd (dd-width sums for S <= 16)
 template <int S, int DB>
 __device__ __forceinline__ mp::qd combine_qd(const int32_t *D);
 template <int S, int DB>
@@ -1001,176 +875,6 @@ __device__ __forceinline__ mp::qd combine_diagonals(const int32_t *D) {
   if constexpr (S > 16) return combine_qd<S, DB>(D);
   else return mp::qd_from_dd(combine_dd<S, DB>(D));
 }
-template <int S, int DB = 7>
-__device__ __forceinline__ mp::qd combine_diagonals_chain(const int32_t *D) {
-  mp::qd acc = mp::qd_make(0.0, 0.0, 0.0, 0.0);
-  mp::dd accd = mp::dd_make(0.0, 0.0);
-#pragma unroll
-  for (int g = 0; g < (S + 2) / 3; ++g) {
-    const int d0 = 3 * g;
-    long long G = (long long)D[d0] << (2 * DB);
-    if (d0 + 1 < S) G += (long long)D[d0 + 1] << DB;
-    if (d0 + 2 < S) G += (long long)D[d0 + 2];
-    double gv = ldexp((double)G, -(12 + DB * (d0 + 2)));  // exact
-    if constexpr (S > 16) acc = mp::qd_add(acc, mp::qd_from_d(gv));
-    else accd = mp::dd_add_d(accd, gv);
-  }
-  if constexpr (S > 16) return acc;
-  else return mp::qd_from_dd(accd);
-}
-
-template <int S, int NT, int FO, int MODE>
-__global__ void __launch_bounds__(kThreadsOz, 1) oz_gemm_kernel(const OzArgs args) {
-  constexpr int STAGES = oz_stages<S, NT>();
-  constexpr size_t STAGE = oz_stage_bytes<S, NT>();
-  constexpr int A_SLICE = kTileM * kKStep;   // bytes per A slice block
-  constexpr int B_SLICE = NT * kKStep;
-  constexpr int TCOLS = tmem_cols_for(S * NT);
-  constexpr uint32_t IDESC = idesc_i8(kTileM, NT);
-
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t *stage_base = smem;
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE);
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + STAGES * STAGE + 64);
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int bz = blockIdx.z;
-  const int b = args.sel ? args.sel[bz] : bz;
-  const int m0 = blockIdx.y * kTileM, n0 = blockIdx.x * NT;
-  const int ksteps = args.A.kpad / kKStep;
-
-  if (warp == 0) tmem_alloc<TCOLS>(smem_u32(tmem_slot));
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&mbar[s]), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  const long long aplane = args.A.plane(), bplane = args.B.plane();
-  const int8_t *Ab = args.A.digits + ((long long)b * args.A.rpad + m0) * args.A.kpad;
-  const int8_t *Bb = args.B.digits + ((long long)b * args.B.rpad + n0) * args.B.kpad;
-
-  auto load_stage = [&](int st, int kb) {
-    const uint32_t sa = smem_u32(stage_base + st * STAGE);
-    const uint32_t sb = sa + S * A_SLICE;
-    const int k0 = kb * kKStep;
-    // A: S slices x 128 rows x 2 chunks
-    for (int c = tid; c < S * kTileM * 2; c += kThreadsOz) {
-      const int s = c / (kTileM * 2), rem = c % (kTileM * 2);
-      const int row = rem >> 1, kc = rem & 1;
-      const uint32_t dst = sa + s * A_SLICE + (((row >> 3) * 2 + kc) << 7) + ((row & 7) << 4);
-      cp16(dst, Ab + s * aplane + (long long)row * args.A.kpad + k0 + kc * 16);
-    }
-    for (int c = tid; c < S * NT * 2; c += kThreadsOz) {
-      const int s = c / (NT * 2), rem = c % (NT * 2);
-      const int row = rem >> 1, kc = rem & 1;
-      const uint32_t dst = sb + s * B_SLICE + (((row >> 3) * 2 + kc) << 7) + ((row & 7) << 4);
-      cp16(dst, Bb + s * bplane + (long long)row * args.B.kpad + k0 + kc * 16);
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-  };
-
-  uint32_t phase[2] = {0u, 0u};
-  load_stage(0, 0);
-  for (int kb = 0; kb < ksteps; ++kb) {
-    const int st = (STAGES == 2) ? (kb & 1) : 0;
-    if (STAGES == 2 && kb + 1 < ksteps) {
-      const int nst = st ^ 1;
-      if (kb >= 1) {  // stage nst was read by the MMAs of step kb-1
-        mbar_wait(smem_u32(&mbar[nst]), phase[nst]);
-        phase[nst] ^= 1u;
-      }
-      load_stage(nst, kb + 1);
-      asm volatile("cp.async.wait_group 1;\n" ::);
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::);
-    }
-    fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-      fence_after();
-      const uint32_t sa = smem_u32(stage_base + st * STAGE);
-      const uint32_t sb = sa + S * A_SLICE;
-      // A_s times the concatenated B slices [B_0 .. B_{S-1-s}] (stacked along
-      // N in smem, 8-row groups every 256 B) lands in the adjacent diagonal
-      // accumulators d = s .. S-1 (column offset s*NT): one wide MMA (split
-      // at the 256-column instruction limit) instead of S-s narrow ones.
-#pragma unroll 1
-      for (int s = 0; s < S; ++s) {
-        const uint64_t ad = umma_desc(sa + s * A_SLICE, 128, 256);
-        int ncols = (S - s) * NT;
-        int t0 = 0;
-        while (ncols > 0) {
-          const int nn = ncols > 256 ? 256 : ncols;
-          const uint64_t bd = umma_desc(sb + t0 * B_SLICE, 128, 256);
-          const uint32_t idesc = idesc_i8(kTileM, nn);
-          mma_i8(tmem + (uint32_t)((s + t0) * NT), ad, bd, idesc, (kb > 0 || s > 0) ? 1u : 0u);
-          t0 += nn / NT;
-          ncols -= nn;
-        }
-      }
-      mma_commit(smem_u32(&mbar[st]));
-    }
-    if (STAGES == 1) {
-      mbar_wait(smem_u32(&mbar[0]), phase[0]);
-      phase[0] ^= 1u;
-      if (kb + 1 < ksteps) load_stage(0, kb + 1);
-    }
-  }
-  if (STAGES == 2) {
-    const int last = (ksteps - 1) & 1;
-    mbar_wait(smem_u32(&mbar[last]), phase[last]);
-  }
-  fence_after();
-
-  // ---------------------------------------------------------- epilogue
-  const int row = m0 + warp * 32 + lane;  // TMEM lane == tile row
-  const int ea = args.A.exps[(long long)b * args.A.rpad + m0 + warp * 32 + lane];
-  const MatRef &C = args.C;
-  int ey = 0, ei = 0, eo = 0;
-  if constexpr (MODE == 1) {
-    if (args.epi.exp_y) ey = args.epi.exp_y[b];
-    if (args.epi.exp_in) ei = args.epi.exp_in[b];
-    if (args.epi.exp_out) eo = args.epi.exp_out[b];
-  }
-  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-  constexpr int CW = (S > 16) ? 4 : 8;
-  for (int c0 = 0; c0 < NT; c0 += CW) {
-    int32_t D[S][CW];
-#pragma unroll
-    for (int d = 0; d < S; ++d) {
-      if constexpr (CW == 8) tmem_ld8(lane_base + (uint32_t)(d * NT + c0), D[d]);
-      else tmem_ld4(lane_base + (uint32_t)(d * NT + c0), D[d]);
-    }
-    tmem_ld_wait();
-#pragma unroll
-    for (int jj = 0; jj < CW; ++jj) {
-      const int col = n0 + c0 + jj;
-      if (row >= args.M || col >= args.N) continue;
-      int32_t Dj[S];
-#pragma unroll
-      for (int d = 0; d < S; ++d) Dj[d] = D[d][jj];
-      mp::qd v = oz_db_of<S>(args.A.db) == 8 ? combine_diagonals<S, 8>(Dj) : combine_diagonals<S, 7>(Dj);
-      const int eb = args.B.exps[(long long)b * args.B.rpad + col];
-      v = mp::qd_ldexp(v, ea + eb);
-      const long long off = (long long)b * C.bstride + (long long)row * C.ld + col;
-      if constexpr (MODE == 0) {
-        store_fmt<FO>(C, off, v, 0);
-      } else {
-        const int sh = -(ey + ei);
-        if (sh) v = mp::qd_ldexp(v, sh);
-        mp::qd bv = load_qd(args.epi.Bprev, (long long)b * args.epi.Bprev.bstride + (long long)row * args.epi.Bprev.ld + col);
-        store_fmt<FO>(C, off, horner_add<FO>(bv, v), eo);
-      }
-    }
-  }
-  fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc<TCOLS>(tmem);
-}
 
 // ------------------------------------------------------ shared epilogue
 __host__ __device__ constexpr double pow2c(int e) {  // compile-time 2^e
@@ -1178,24 +882,6 @@ __host__ __device__ constexpr double pow2c(int e) {  // compile-time 2^e
   if (e >= 0) for (int i = 0; i < e; ++i) r *= 2.0;
   else for (int i = 0; i < -e; ++i) r *= 0.5;
   return r;
-}
-
-// sum_d D_d 2^-(12+DB d) for S <= 16 as a dd (groups of three digits are
-// exact int64 -> double; group weights are compile-time constants).
-template <int S, int DB = 7>
-__device__ __forceinline__ mp::dd combine_dd_chain(const int32_t *D) {
-  mp::dd acc = mp::dd_make(0.0, 0.0);
-#pragma unroll
-  for (int g = 0; g < (S + 2) / 3; ++g) {
-    const int d0 = 3 * g;
-    long long G = (long long)D[d0] << (2 * DB);
-    if (d0 + 1 < S) G += (long long)D[d0 + 1] << DB;
-    if (d0 + 2 < S) G += (long long)D[d0 + 2];
-    const double gv = (double)G * pow2c(-(12 + DB * (d0 + 2)));  // exact
-    if (g == 0) acc = mp::dd_make(gv, 0.0);
-    else acc = mp::dd_add_d(acc, gv);
-  }
-  return acc;
 }
 
 // m * 2^-q for an integer 0 <= m < 2^52, exactly: m dropped into the mantissa
@@ -1209,8 +895,9 @@ __device__ __forceinline__ double u52_scaled(unsigned long long m, double bias =
   return __longlong_as_double((long long)(EXPO | m)) - (BASE + bias);
 }
 
-// The same sum through integer carries (the epilogue's FP64 work: ~10 DADD
-// instead of ~40 DADD + 5 I2F.S64 per output).  The groups of three digits,
+// sum_d D_d 2^-(12+DB d) for S <= 16 as a dd, through integer carries (the
+// epilogue's FP64 work: ~10 DADD; a chain of dd additions of the exact
+// three-digit groups cost ~40 DADD + 5 I2F.S64 per output).  The groups of three digits,
 // weights 2^(3 DB) apart, are carry-normalised into base-2^(3 DB) digits
 // (top signed, the rest in [0, 2^(3 DB))); pairs of digits are exact doubles
 // P0 > P1 > ... that do not overlap, so FastTwoSum(P0, P1), one add of the
@@ -2293,46 +1980,7 @@ __global__ void __launch_bounds__(kThreadsEpi, 1) oz_gemm_wide_kernel(const __gr
   if (warp == 0) tmem_dealloc<TCOLS>(tmem);
 }
 
-// ------------------------------------- persistent, double-buffered TMEM
-// One CTA per SM walks the tiles of the whole batch; consecutive CTAs hold
-// consecutive tiles of the grouped raster.  Two accumulator sets of S*NT
-// TMEM columns (NT = 16 for dd: 2 x 256 columns) let the MMAs of tile i+1
-// run while the epilogue warps drain tile i, and the TMA producer streams
-// the next tile's planes during the epilogue instead of each CTA paying the
-// pipeline fill.
-//
-// CL = 2: CTA pairs (a 2-CTA cluster) take the two N tiles 2p, 2p+1 of one
-// M tile.  Both need the same A planes, so each CTA loads every other A
-// plane group and multicasts it into both CTAs' rings: the L2 -> SM traffic
-// of A (16 of the 18 KB per K step and 16 output columns) halves.  A ring
-// slot is refilled only after BOTH CTAs' MMAs have released it (the MMA
-// issuers' commits arrive on the a_empty barriers of both CTAs).
-//
-// Warp 0: TMA producer, warp 1: MMA issuer, warps 2..9: epilogue (warp w
-// reads TMEM lane quarter w % 4; warps 2..5 take the first half of the
-// columns, 6..9 the second).
-constexpr int kThreadsPers = 320;
-
-template <int S, int NT>
-struct OzPers {
-  // deeper rings than OzRing: a K step of 16 columns takes ~0.7 us of MMAs,
-  // shorter than a TMA round trip, so several B steps and A groups must be
-  // in flight
-  static constexpr int SG = OzRing<S, NT>::SG, NG = OzRing<S, NT>::NG;
-  static constexpr uint32_t A_BYTES = OzRing<S, NT>::A_BYTES, B_BYTES = OzRing<S, NT>::B_BYTES;
-  static constexpr uint32_t B_STRIDE = (B_BYTES + 1023) / 1024 * 1024;
-  static constexpr size_t kBudget = 212u * 1024u;
-  static constexpr int NBS = (B_STRIDE * 6 <= kBudget / 4) ? 6 : 2;
-  static constexpr int NAS_FIT = (int)((kBudget - NBS * (size_t)B_STRIDE) / A_BYTES);
-  static constexpr int NAS = NAS_FIT > 12 ? 12 : NAS_FIT;
-  static constexpr int ACC = S * NT;  // TMEM columns per accumulator set
-  // two sets when they fit (epilogue overlaps the next tile's MMAs); one set
-  // otherwise (NT = 32 dd: only the feed runs ahead during the epilogue)
-  static constexpr int NACC = (2 * ACC <= 512) ? 2 : 1;
-  static_assert(NACC * ACC <= 512, "accumulators must fit in TMEM");
-  static constexpr size_t SMEM = (size_t)NBS * B_STRIDE + (size_t)NAS * A_BYTES + 2048;
-};
-
+// ------------------------------------------------ persistent kernels
 // tile t of a CL-CTA group: (batch member, M offset, N offset of this CTA)
 template <int CL>
 __device__ __forceinline__ void oz_pers_tile(const OzTmaArgs &a, int t, int nt, int rank, int &bz, int &m0, int &n0) {
@@ -2343,141 +1991,6 @@ __device__ __forceinline__ void oz_pers_tile(const OzTmaArgs &a, int t, int nt, 
   g.ntiles = npairs;
   oz_tile_at(g, t - bz * per, nt * CL, m0, n0);
   n0 += rank * nt;
-}
-
-template <int S, int NT, uint32_t A_SLICE, uint32_t B_SLICE, int SG, int CL, int G = 0>
-__device__ __forceinline__ void oz_ring_groups_mc(uint32_t tmem, uint64_t bd0, uint32_t acc0, int &ai, uint8_t *aring,
-                                                  uint64_t *a_full, uint64_t *a_empty, int nas, uint32_t a_bytes,
-                                                  bool issue = true) {
-  if constexpr (G * SG < S) {
-    const int ast = ai % nas;
-    mbar_wait(smem_u32(&a_full[ast]), (ai / nas) & 1);
-    fence_after();
-    if (issue)
-      oz_issue_planes<S, NT, A_SLICE, B_SLICE, G * SG, SG>(tmem, umma_desc(smem_u32(aring + ast * a_bytes), 16, 256, 6),
-                                                           bd0, acc0);
-    if constexpr (CL == 1) mma_commit(smem_u32(&a_empty[ast]));
-    else mma_commit_mc(smem_u32(&a_empty[ast]), (uint16_t)((1u << CL) - 1u));
-    ++ai;
-    oz_ring_groups_mc<S, NT, A_SLICE, B_SLICE, SG, CL, G + 1>(tmem, bd0, acc0, ai, aring, a_full, a_empty, nas,
-                                                              a_bytes, issue);
-  }
-}
-
-template <int S, int NT, int FO, int MODE, int CL>
-__global__ void __launch_bounds__(kThreadsPers, 1) oz_gemm_pers_kernel(const __grid_constant__ OzTmaArgs args) {
-  using P = OzPers<S, NT>;
-  using R = P;
-  constexpr uint32_t A_SLICE = kTileM * kKStep;
-  constexpr uint32_t B_SLICE = NT * kKStep;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint8_t *bring = smem;
-  uint8_t *aring = smem + R::NBS * R::B_STRIDE;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(aring + R::NAS * R::A_BYTES);
-  uint64_t *b_full = bar, *b_empty = bar + R::NBS;
-  uint64_t *a_full = bar + 2 * R::NBS, *a_empty = a_full + R::NAS;
-  uint64_t *acc_full = a_empty + R::NAS, *acc_empty = acc_full + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ksteps = args.A.kpad / kKStep;
-  const int rank = CL > 1 ? (int)cluster_rank() : 0;
-  const int group0 = blockIdx.x / CL, ngroups = gridDim.x / CL;
-  const int total = args.nbatch * args.mtiles * ((args.ntiles + CL - 1) / CL);
-
-  if (warp == 0) tmem_alloc<512>(smem_u32(tmem_slot));
-  if (tid == 32) {
-    for (int i = 0; i < R::NBS; ++i) { mbar_init(smem_u32(&b_full[i]), 1); mbar_init(smem_u32(&b_empty[i]), 1); }
-    for (int i = 0; i < R::NAS; ++i) { mbar_init(smem_u32(&a_full[i]), 1); mbar_init(smem_u32(&a_empty[i]), CL); }
-    for (int i = 0; i < 2; ++i) { mbar_init(smem_u32(&acc_full[i]), 1); mbar_init(smem_u32(&acc_empty[i]), 8); }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  fence_before();
-  if constexpr (CL > 1) cluster_sync();   // peers' barriers initialised before any multicast
-  else __syncthreads();
-  fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // ---- TMA producer (ring positions continue across tiles)
-      int kg = 0, ai = 0;
-      for (int t = group0; t < total; t += ngroups) {
-        int bz, m0, n0;
-        oz_pers_tile<CL>(args, t, NT, rank, bz, m0, n0);
-        const int b = args.sel ? args.sel[bz] : bz;
-        const int rowA = b * args.A.rpad + m0, rowB = b * args.B.rpad + n0;
-        for (int kb = 0; kb < ksteps; ++kb, ++kg) {
-          const int bst = kg % R::NBS;
-          if (kg >= R::NBS) mbar_wait(smem_u32(&b_empty[bst]), ((kg / R::NBS) - 1) & 1);
-          mbar_expect_tx(smem_u32(&b_full[bst]), R::B_BYTES);
-          tma_load_3d(smem_u32(bring + bst * R::B_STRIDE), &args.mapB, kb * kKStep, rowB, 0, smem_u32(&b_full[bst]));
-          for (int g = 0; g < R::NG; ++g, ++ai) {
-            const int ast = ai % R::NAS;
-            // both CTAs' MMAs released the slot (CL arrivals)
-            if (ai >= R::NAS) mbar_wait(smem_u32(&a_empty[ast]), ((ai / R::NAS) - 1) & 1);
-            mbar_expect_tx(smem_u32(&a_full[ast]), R::A_BYTES);
-            if constexpr (CL == 1) {
-              tma_load_3d(smem_u32(aring + ast * R::A_BYTES), &args.mapA, kb * kKStep, rowA, g * R::SG,
-                          smem_u32(&a_full[ast]));
-            } else if (g % CL == rank) {
-              tma_load_3d_mc(smem_u32(aring + ast * R::A_BYTES), &args.mapA, kb * kKStep, rowA, g * R::SG,
-                             smem_u32(&a_full[ast]), (uint16_t)((1u << CL) - 1u));
-            }
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // ---- MMA issuer: tile i accumulates into set i & 1
-      int kg = 0, ai = 0, i = 0;
-      for (int t = group0; t < total; t += ngroups, ++i) {
-        const int buf = i % P::NACC;
-        if (i >= P::NACC) mbar_wait(smem_u32(&acc_empty[buf]), ((i / P::NACC) - 1) & 1);
-        fence_after();
-        const uint32_t tacc = tmem + (uint32_t)(buf * P::ACC);
-        for (int kb = 0; kb < ksteps; ++kb, ++kg) {
-          const int bst = kg % R::NBS;
-          mbar_wait(smem_u32(&b_full[bst]), (kg / R::NBS) & 1);
-          fence_after();
-          const uint32_t sb = smem_u32(bring + bst * R::B_STRIDE);
-          oz_ring_groups_mc<S, NT, A_SLICE, B_SLICE, R::SG, CL>(tacc, umma_desc(sb, 16, 256, 6), kb > 0 ? 1u : 0u,
-                                                                ai, aring, a_full, a_empty, R::NAS, R::A_BYTES,
-                                                                !(args.dbg & 1));
-          mma_commit(smem_u32(&b_empty[bst]));
-        }
-        mma_commit(smem_u32(&acc_full[buf]));
-      }
-    }
-  } else {
-    // ---- epilogue warps
-    const int quarter = warp & 3, half = (warp - 2) >> 2;
-    const int cb = half ? EpiCols<S, NT>::HALF : 0, ce = half ? NT : EpiCols<S, NT>::HALF;
-    int i = 0;
-    for (int t = group0; t < total; t += ngroups, ++i) {
-      int bz, m0, n0;
-      oz_pers_tile<CL>(args, t, NT, rank, bz, m0, n0);
-      const int b = args.sel ? args.sel[bz] : bz;
-      const int buf = i % P::NACC;
-      EpiPre<S, NT, FO, MODE> pre;
-      oz_epi_prefetch<S, NT, FO, MODE>(args, pre, quarter, cb, ce, b, m0, n0, lane);
-      mbar_wait(smem_u32(&acc_full[buf]), (i / P::NACC) & 1);
-      fence_after();
-      if (!(args.dbg & 4))
-        oz_epilogue_db<S, NT, FO, MODE>(args, pre, tmem + (uint32_t)(buf * P::ACC), quarter, cb, ce, b, m0, n0, lane);
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&acc_empty[buf]));
-    }
-  }
-  fence_before();
-  // no CTA leaves while its peer may still multicast into its ring or barriers
-  if constexpr (CL > 1) cluster_sync();
-  else __syncthreads();
-  fence_after();
-  if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
 // INT8 tensor-pipe peak probe: one CTA per SM issues back-to-back
@@ -2535,134 +2048,6 @@ __global__ void __launch_bounds__(128, 1) i8_mma_probe_kernel(int iters, int *ou
   fence_before();
   __syncthreads();
   if (threadIdx.x < 32) tmem_dealloc<512>(tmem);
-}
-
-// --------------------- persistent + double-buffered TMEM + 128-byte K boxes
-// The wide feed keeps the L2 slices at ~22 % (vs ~64 % for 32-byte boxes,
-// ncu lts__throughput at n = 1024), which leaves room for NT = 16 tiles:
-// two 256-column accumulator sets, the epilogue of tile i overlapping the
-// MMAs of tile i+1 and the producer streaming across tile boundaries.
-// Warp 0: TMA producer, warp 1: MMA issuer, warps 2..9: epilogue.
-template <int S, int NT>
-struct OzPWide {
-  using W = OzWide<S, NT>;
-  static constexpr int NBS = 2;
-  static constexpr int NAS_FIT = (int)((222ll * 1024 - 2048 - NBS * (long long)W::B_STRIDE) / W::A_BYTES);
-  static constexpr int NAS = NAS_FIT > 12 / W::SG ? 12 / W::SG : NAS_FIT;
-  static constexpr int ACC = S * NT;
-  static_assert(2 * ACC <= 512, "two accumulator sets must fit in TMEM");
-  static constexpr size_t SMEM = (size_t)NBS * W::B_STRIDE + (size_t)NAS * W::A_BYTES + 2048;
-};
-
-template <int S, int NT, int FO, int MODE>
-__global__ void __launch_bounds__(kThreadsPers, 1) oz_gemm_pwide_kernel(const __grid_constant__ OzTmaArgs args) {
-  using W = OzWide<S, NT>;
-  using P = OzPWide<S, NT>;
-  constexpr int NAS = P::NAS;
-  static_assert(NAS * W::SG >= 3, "A ring does not fit");
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint8_t *bring = smem;
-  uint8_t *aring = smem + P::NBS * W::B_STRIDE;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(aring + NAS * W::A_BYTES);
-  uint64_t *b_full = bar, *b_empty = bar + P::NBS;
-  uint64_t *a_full = bar + 2 * P::NBS, *a_empty = a_full + NAS;
-  uint64_t *acc_full = a_empty + NAS, *acc_empty = acc_full + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int kpad = args.A.kpad;
-  const int kstages = (kpad + W::KB - 1) / W::KB;
-  const int total = args.nbatch * args.mtiles * args.ntiles;
-
-  if (warp == 0) tmem_alloc<512>(smem_u32(tmem_slot));
-  if (tid == 32) {
-    for (int i = 0; i < P::NBS; ++i) { mbar_init(smem_u32(&b_full[i]), 1); mbar_init(smem_u32(&b_empty[i]), 1); }
-    for (int i = 0; i < NAS; ++i) { mbar_init(smem_u32(&a_full[i]), 1); mbar_init(smem_u32(&a_empty[i]), 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(smem_u32(&acc_full[i]), 1); mbar_init(smem_u32(&acc_empty[i]), 8); }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int kg = 0, ai = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        int bz, m0, n0;
-        oz_pers_tile<1>(args, t, NT, 0, bz, m0, n0);
-        const int b = args.sel ? args.sel[bz] : bz;
-        const int rowA = b * args.A.rpad + m0, rowB = b * args.B.rpad + n0;
-        for (int kb = 0; kb < kstages; ++kb, ++kg) {
-          const int bst = kg % P::NBS;
-          if (kg >= P::NBS) mbar_wait(smem_u32(&b_empty[bst]), ((kg / P::NBS) - 1) & 1);
-          mbar_expect_tx(smem_u32(&b_full[bst]), W::B_BYTES);
-          tma_load_3d(smem_u32(bring + bst * W::B_STRIDE), &args.mapB, kb * W::KB, rowB, 0, smem_u32(&b_full[bst]));
-          for (int j = 0; j < W::NSLOT; ++j, ++ai) {
-            const int ast = ai % NAS;
-            if (ai >= NAS) mbar_wait(smem_u32(&a_empty[ast]), ((ai / NAS) - 1) & 1);
-            mbar_expect_tx(smem_u32(&a_full[ast]), W::A_BYTES);
-#pragma unroll
-            for (int q = 0; q < W::SG; ++q)
-              tma_load_3d(smem_u32(aring + ast * W::A_BYTES + q * W::A_PLANE), &args.mapA, kb * W::KB, rowA,
-                          oz_plane_at<S>(j * W::SG + q), smem_u32(&a_full[ast]));
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      int kg = 0, ai = 0, i = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
-        const int buf = i & 1;
-        if (i >= 2) mbar_wait(smem_u32(&acc_empty[buf]), ((i >> 1) - 1) & 1);
-        fence_after();
-        const uint32_t tacc = tmem + (uint32_t)(buf * P::ACC);
-        for (int kb = 0; kb < kstages; ++kb, ++kg) {
-          const int bst = kg % P::NBS;
-          mbar_wait(smem_u32(&b_full[bst]), (kg / P::NBS) & 1);
-          fence_after();
-          const int left = (kpad - kb * W::KB) / kKStep;
-          const int nk = left < 4 ? left : 4;
-          if (!(args.dbg & 1))
-            oz_wide_stage<S, NT>(tacc, smem_u32(bring + bst * W::B_STRIDE), nk, kb > 0 ? 1u : 0u, ai, aring, a_full,
-                                 a_empty, NAS);
-          else
-            for (int j = 0; j < W::NSLOT; ++j, ++ai) {   // diagnostics: feed only
-              mbar_wait(smem_u32(&a_full[ai % NAS]), (ai / NAS) & 1);
-              mma_commit(smem_u32(&a_empty[ai % NAS]));
-            }
-          mma_commit(smem_u32(&b_empty[bst]));
-        }
-        mma_commit(smem_u32(&acc_full[buf]));
-      }
-    }
-  } else {
-    const int quarter = warp & 3, half = (warp - 2) >> 2;
-    const int cb = half ? EpiCols<S, NT>::HALF : 0, ce = half ? NT : EpiCols<S, NT>::HALF;
-    int i = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
-      int bz, m0, n0;
-      oz_pers_tile<1>(args, t, NT, 0, bz, m0, n0);
-      const int b = args.sel ? args.sel[bz] : bz;
-      const int buf = i & 1;
-      EpiPre<S, NT, FO, MODE> pre;
-      oz_epi_prefetch<S, NT, FO, MODE>(args, pre, quarter, cb, ce, b, m0, n0, lane);
-      mbar_wait(smem_u32(&acc_full[buf]), (i >> 1) & 1);
-      fence_after();
-      if (!(args.dbg & 4))
-        oz_epilogue_db<S, NT, FO, MODE>(args, pre, tmem + (uint32_t)(buf * P::ACC), quarter, cb, ce, b, m0, n0, lane);
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&acc_empty[buf]));
-    }
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
 // 256-bit global accesses (sm_100: LDG/STG.256): a row-per-thread epilogue

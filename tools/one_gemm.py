@@ -1,5 +1,5 @@
 """One tensor-core GEMM config, a few launches (for ncu captures):
-python tools/one_gemm.py FMT B N [reps]   (MPPS_OZ_WIDE / MPPS_OZ_PERS select the kernel)"""
+python tools/one_gemm.py FMT B N [reps]   (MPPS_OZ_WIDE / MPPS_OZ_PW16 select the kernel)"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch

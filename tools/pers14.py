@@ -1,4 +1,4 @@
-"""8-bit 14-plane dd GEMM under the kernel selected by MPPS_OZ_PERS / MPPS_OZ_WIDE (dev tool):
+"""8-bit 14-plane dd GEMM under the kernel selected by MPPS_OZ_PW16 / MPPS_OZ_WIDE (dev tool):
 time (CUDA events, best of 7), debug-flag variants and a checksum of the result bits so that
 runs of different kernels can be compared for bitwise equality."""
 import os, sys, hashlib
@@ -8,7 +8,7 @@ from paper_2312_17396_b200 import _lib
 from paper_2312_17396_b200.precision import MatBatch
 
 h = _lib.handle_for()
-tag = f"pers={os.environ.get('MPPS_OZ_PERS', '0')} wide={os.environ.get('MPPS_OZ_WIDE', '1')} pw16={os.environ.get('MPPS_OZ_PW16', '1')}"
+tag = f"wide={os.environ.get('MPPS_OZ_WIDE', '1')} pw16={os.environ.get('MPPS_OZ_PW16', '1')}"
 flagsets = ((0, "full"),) if "flags" not in sys.argv else ((0, "full"), (1, "no MMA (feed + epilogue)"), (2, "no loads (MMA + epilogue)"), (4, "no epilogue"), (5, "feed only"))
 SHAPES = ((1, 8192),) if "big" in sys.argv else ((64, 256), (16, 1024), (4, 2048))
 for B, n in SHAPES:
