@@ -112,6 +112,10 @@ int after_launch(mpps_handle *h, const char *what) {
 }
 
 // ----------------------------------------------------------- value helpers
+// max that keeps a NaN: the planner's norms must show a non-finite input
+// (fmax drops NaNs, and the digit splits turn them into finite digits)
+__device__ __forceinline__ double nan_max(double a, double b) { return (b > a || b != b) ? b : a; }
+
 __device__ __forceinline__ mp::qd load_any(const MatRef &m, long long off, int fi) {
   if (fi == F32) return mp::qd_from_d((double)((const float *)m.data)[off]);
   return load_qd(m, off);
@@ -459,13 +463,13 @@ __global__ void norm_reduce_kernel(const double *partial, double *norms, int nbl
     double s = 0.0;
     for (int c = 0; c < nchunk; ++c)
       s += partial[(((long long)b * nchunk + c) * nblk + k) * cols + col];
-    best = fmax(best, s);
+    best = nan_max(best, s);
   }
   __shared__ double red[256];
   red[threadIdx.x] = best;
   __syncthreads();
   for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+    if (threadIdx.x < w) red[threadIdx.x] = nan_max(red[threadIdx.x], red[threadIdx.x + w]);
     __syncthreads();
   }
   if (threadIdx.x == 0) norms[(long long)b * nblk + k] = red[0];
@@ -515,13 +519,13 @@ __global__ void norm_reduce_strided_kernel(const double *partial, double *out, i
   for (int col = threadIdx.x; col < cols; col += blockDim.x) {
     double s = 0.0;
     for (int c = 0; c < nchunk; ++c) s += partial[((long long)b * nchunk + c) * cols + col];
-    best = fmax(best, s);
+    best = nan_max(best, s);
   }
   __shared__ double red[256];
   red[threadIdx.x] = best;
   __syncthreads();
   for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+    if (threadIdx.x < w) red[threadIdx.x] = nan_max(red[threadIdx.x], red[threadIdx.x + w]);
     __syncthreads();
   }
   if (threadIdx.x == 0) out[(long long)b * stride] = red[0];

@@ -250,8 +250,20 @@ __device__ __forceinline__ void split_digits_w(const mp::qd &v, int8_t (&dg)[S])
   for (int s = 0; s < S; ++s) dg[s] = (int8_t)di[s];
 }
 
+// Non-finite entries: a NaN or Inf in a row (column) must not come back as
+// finite digits.  abs_keep maps both to +Inf in the running maximum (fmax
+// drops NaNs; an integer test on the high word, no FP64 compare), and
+// row_exponent answers Inf with kExpNonFinite: every product entry of that
+// row (column) is then scaled by 2^kExpNonFinite = Inf in the GEMM epilogues
+// (pow2i), i.e. comes out Inf or NaN as mat_mul's would (precision.py:160-184),
+// and the block norms carry it to the planner, which raises.
+constexpr int kExpNonFinite = 1 << 20;
+__device__ __forceinline__ double abs_keep(double v) {
+  return ((__double2hiint(v) & 0x7ff00000) == 0x7ff00000) ? __longlong_as_double(0x7ff0000000000000ll) : fabs(v);
+}
 __device__ __forceinline__ int row_exponent(double mx) {
   int e = 0;
+  if (!(mx < __longlong_as_double(0x7ff0000000000000ll))) return kExpNonFinite;
   if (mx > 0.0) {
     frexp(mx, &e);  // mx in [2^(e-1), 2^e)
     // a multiword value may exceed its leading word by half an ulp: one bit
@@ -470,7 +482,7 @@ __device__ __forceinline__ void slice_rows_regs(const MatRef &A, long long base,
 #pragma unroll
   for (int it = 0; it < NIT; ++it)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) mx = fmax(mx, fabs(h[it][q]));
+    for (int q = 0; q < 4; ++q) mx = fmax(mx, abs_keep(h[it][q]));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   const int e = row_exponent(mx);
@@ -523,7 +535,7 @@ __device__ __forceinline__ void slice_rows_body(const MatRef &A, int rows, int c
     if (i < rows)
       for (int k = lane; k < cols; k += 32) {
         double v = fi == F32 ? (double)((const float *)A.data)[base + k] : ((const double *)A.data)[base + k];
-        mx = fmax(mx, fabs(v));
+        mx = fmax(mx, abs_keep(v));
       }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -641,7 +653,7 @@ __global__ void row_exps_kernel(MatRef A, int rows, int cols, int fi, SliceRef o
   if (i < rows)
     for (int k = lane; k < cols; k += 32) {
       double v = fi == F32 ? (double)((const float *)A.data)[base + k] : ((const double *)A.data)[base + k];
-      mx = fmax(mx, fabs(v));
+      mx = fmax(mx, abs_keep(v));
     }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -663,7 +675,7 @@ __global__ void col_exps_kernel(MatRef B, int rows, int cols, int fi, SliceRef o
     for (int k = ty; k < rows; k += 8) {
       const long long off = (long long)b * B.bstride + (long long)k * B.ld + j;
       double v = fi == F32 ? (double)((const float *)B.data)[off] : ((const double *)B.data)[off];
-      mx = fmax(mx, fabs(v));
+      mx = fmax(mx, abs_keep(v));
     }
   red[ty][tx] = mx;
   __syncthreads();
@@ -1136,6 +1148,8 @@ __device__ __forceinline__ void oz_epilogue(const Args &args, const EpiPre<S, NT
       } else {
         mp::qd v = combine_diagonals<S, DB>(Dj);
         v = mp::qd_ldexp(v, ea + eb);
+        // a non-finite operand row / column (row_exponent): ldexp leaves a zero sum zero
+        if (ea + eb >= kExpNonFinite / 2) v = mp::qd_make(__longlong_as_double(0x7ff8000000000000ll), 0.0, 0.0, 0.0);
         if constexpr (MODE == 0) {
           store_fmt<FO>(C, off, v, 0);
         } else {

@@ -79,7 +79,10 @@ __device__ __forceinline__ double one_norm_warp(const double *M, int n, int lane
   if (lane < n)
     for (int i = 0; i < n; ++i) s += fabs(M[i * n + lane]);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+  for (int o = 16; o > 0; o >>= 1) {   // a NaN column sum stays (fmax would drop it)
+    const double t = __shfl_xor_sync(0xffffffffu, s, o);
+    s = (t > s || t != t) ? t : s;
+  }
   return s;
 }
 

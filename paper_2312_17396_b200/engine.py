@@ -679,6 +679,39 @@ def _check_square(Xt, Xw):
     return Xw.batch, Xw.rows
 
 
+def _require_finite_norms(norms) -> None:
+    """The evaluators without a planner on their path (fixed precision,
+    explicit powers) reject a non-finite input the way the planner of the
+    mixed ones does (one_norm of a block with a NaN / Inf entry, engine.py:
+    467-472): the digit splits carry non-finite entries into the block
+    norms, never into finite digits."""
+    if not np.isfinite(np.asarray(norms, dtype=np.float64)).all():
+        raise ValueError("non-finite float")
+
+
+def _degenerate_shape(Xt, Xw, single, series, ctx, kind, delta=10.0, apply_switch=True, fix_params=True):
+    """An empty batch or 0 x 0 matrices: nothing to launch.  The reference
+    returns an empty result whose plan comes from zero norms
+    (engine.py:390-482 on ``from_rows([])``); a batch of none returns an
+    empty BatchReport.  None for every other shape."""
+    B, n = _check_square(Xt, Xw)
+    if B > 0 and n > 0:
+        return None
+    dev = Xt.device if Xt is not None else Xw.device
+    if dev.type != "cuda":
+        dev = "cuda"
+    res = MatBatch.empty(_working_format(ctx), B, n, device=dev)
+    m = series.degree
+    s = default_block_size(m) if m >= 1 else 1
+    r = m // s
+    zeros = np.zeros(r + 2)
+    if kind == "fixed":
+        fns = [(lambda: fixed_plan(tuple([0.0] * (r + 1)), 0.0, ctx, s)) for _ in range(B)]
+    else:
+        fns = [_plan_fn(zeros, r, ctx, delta, s, apply_switch, fix_params) for _ in range(B)]
+    return _reports(res, fns, None, kind, {}, False, single and B > 0)
+
+
 def _reports(result: MatBatch, plan_fns, executed, counts_mode, sec, with_bound, single, extra=None):
     frac = _fractions(sec)
     n = result.rows
@@ -786,6 +819,7 @@ def _small_eval(X, series: CoefficientSeries, ctx: PrecisionCtx, kind: str, delt
         h.small_ps_horner(Y, blocks, fm, m, s, float(cw[m]), result)
         timer.stop()
     if kind == "fixed":
+        _require_finite_norms(norms)
         fns = [(lambda nb=tuple(float(x) for x in norms[b, :r + 1]), ny=float(norms[b, r + 1]):
                 fixed_plan(nb, ny, ctx, s)) for b in range(B)]
         return _reports(result, fns, None, "fixed", timer.seconds(), with_bound, single)
@@ -823,6 +857,7 @@ def _graph_stages(Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: 
     def run_post(prep, norms):
         r = prep.r
         if kind == "fixed":
+            _require_finite_norms(norms)
             digits = np.full((norms.shape[0], r), d, dtype=np.int64)
             nu = np.full(norms.shape[0], r + 1, dtype=np.int64)
             nil = np.zeros(norms.shape[0], dtype=bool)
@@ -909,7 +944,7 @@ def _submit(X, series, ctx, delta, fix_params, with_bound, timing, slot, eager, 
     B, n = _check_square(Xt, Xw)
     if series.degree < 1:
         raise ValueError("series degree must be >= 1")
-    if Xt is None or not graphs.enabled() or _small_ok(Xt, series, ctx):
+    if B == 0 or n == 0 or Xt is None or not graphs.enabled() or _small_ok(Xt, series, ctx):
         rep = eager()
         return PendingEvaluation(lambda: rep)
     timer = _Buckets(timing)
@@ -922,7 +957,10 @@ def _submit(X, series, ctx, delta, fix_params, with_bound, timing, slot, eager, 
         return PendingEvaluation(lambda: rep)
 
     def fin():
-        prep, norms, result, (digits, nu, nil) = graphs.finish(pend, run_post, clone=not static_result)
+        try:
+            prep, norms, result, (digits, nu, nil) = graphs.finish(pend, run_post, clone=not static_result)
+        except graphs.PlanError as pe:
+            raise pe.orig
         return _graphed_reports((prep, digits, nu, nil, result), ctx, delta, True, fix_params, with_bound,
                                 single, timer)
     return PendingEvaluation(fin, pend)
@@ -934,6 +972,8 @@ def ps_fixed(X, series: CoefficientSeries, ctx: PrecisionCtx, with_bound: bool =
     """Fixed-precision PS with s = ceil(sqrt(m)) (engine.py:304-345)."""
     Xt, Xw, single = _input(X)
     B, n = _check_square(Xt, Xw)
+    if B == 0 or n == 0:
+        return _degenerate_shape(Xt, Xw, single, series, ctx, "fixed")
     h = _lib.handle_for()
     timer = _Buckets(timing)
     d = ctx.decimal_digits
@@ -960,6 +1000,7 @@ def ps_fixed(X, series: CoefficientSeries, ctx: PrecisionCtx, with_bound: bool =
         r = prep.r
     else:
         prep = _prepare(h, Xt, series, ctx, wf, s, timer, Xw)
+        _require_finite_norms(prep.norms)
         r = prep.r
         digits = np.full((B, r), d, dtype=np.int64)
         result = _horner(h, prep, digits, np.zeros(B, dtype=bool), timer)
@@ -980,6 +1021,8 @@ def ps_mixed_general(X, series: CoefficientSeries, ctx: PrecisionCtx, delta: flo
     m = series.degree
     if m < 1:
         raise ValueError("series degree must be >= 1")
+    if B == 0 or n == 0:
+        return _degenerate_shape(Xt, Xw, single, series, ctx, "mixed", delta)
     if _small_ok(X, series, ctx):
         return _small_eval(X, series, ctx, "mixed", delta, True, True, with_bound, timing)
     h = _lib.handle_for()
@@ -1021,6 +1064,8 @@ def ps_mixed_exp(X, m: int, ctx: PrecisionCtx, fix_params: bool = True, delta: f
         raise ValueError("m must be >= 1")
     series = taylor_exp_coeffs(m)
     s = default_block_size(m)
+    if B == 0 or n == 0:
+        return _degenerate_shape(Xt, Xw, single, series, ctx, "mixed", delta, True, fix_params)
     if not fix_params:
         # growth decisions are per matrix (host loop over norms), so the
         # batch is split; the common fixed-s case stays batched.
@@ -1083,6 +1128,7 @@ def _explicit_powers(Xt, Xw, m, ctx, s, series, delta, apply_switch, fix_params,
     wf = _working_format(ctx)
     # blocks of the s == m layout: r = 1, B_0 = sum_{j<s} b_j X^j, B_1 = b_m I
     prep = _prepare(h, Xt, series, ctx, wf, s, timer, Xw)
+    _require_finite_norms(prep.norms)
     Y = prep.powers[s - 1]
     res = MatBatch.empty(wf, Y.batch, Y.rows, device=Y.device)
     timer.start("coefficient_assembly")

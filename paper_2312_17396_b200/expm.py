@@ -57,9 +57,15 @@ def expm_ss(A, ctx: PrecisionCtx, m: int = DEFAULT_M, delta: float = 10.0, timin
     if Aw is None:
         Aw = MatBatch(At.unsqueeze(0), FP64)
     B, n = Aw.batch, Aw.rows
+    if B == 0 or n == 0:      # nothing to launch: the PS stage's empty report
+        rep = ps_mixed_exp(Aw, m, ctx, delta=delta, timing=timing)
+        return (rep, None) if return_stage else rep
     normsA = torch.empty(B, dtype=torch.float64, device=Aw.device)
     h.one_norm(Aw, normsA)
-    ells = scaling_of(h.host_array(normsA), m)
+    na = h.host_array(normsA)
+    if not np.isfinite(na).all():
+        raise ValueError("non-finite float")
+    ells = scaling_of(na, m)
     wf = ctx.fmt if ctx.fmt != 7 else FP64
     # X = 2^-l A, exact (the widening to the working format is exact too)
     X = MatBatch.empty(wf, B, n, device=Aw.device)

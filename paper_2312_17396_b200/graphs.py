@@ -87,6 +87,14 @@ def last_launches() -> int:
     return _LAST_LAUNCHES
 
 
+class PlanError(Exception):
+    """The host planner raised inside finish(); ``orig`` is its exception."""
+
+    def __init__(self, orig):
+        super().__init__(str(orig))
+        self.orig = orig
+
+
 class Pending:
     """A submitted evaluation: the pre graph is enqueued and the norms are
     on their way to pinned memory (``ready`` is recorded after the copy)."""
@@ -170,7 +178,12 @@ def finish(p: Pending, run_post, clone: bool = True):
     norms = g.norms_pin.numpy().copy()
     timer.stop()
     g.prep.norms = norms
-    post_key, post_fn, info = run_post(g.prep, norms)
+    try:
+        post_key, post_fn, info = run_post(g.prep, norms)
+    except Exception as exc:
+        # the planner rejected the norms (a non-finite input: engine.py:467-472 raises the same
+        # way in the reference): the caller's error, not a capture problem -- the graphs stay
+        raise PlanError(exc) from exc
     entry = g.post.get(post_key)
     if entry is None:
         s = torch.cuda.Stream()
@@ -221,6 +234,8 @@ def run(key: tuple, Xsrc, build_pre, run_post, timer):
         return None
     try:
         return finish(p, run_post)
+    except PlanError as pe:
+        raise pe.orig
     except Exception as exc:  # pragma: no cover - capture problems fall back to eager
         _FAILED.add(key + (("slot", 0),))
         import warnings

@@ -552,3 +552,59 @@ def test_small_path_certified_planner_fallback(cuda):
     if planned:
         p = m.plan_precisions(norms[0, :5], norms[0, 5], ctx, 1e15, s=4)
         assert tuple(digits[0]) == p.level_digits and nu[0] == p.nu
+
+
+@pytest.mark.parametrize("d,n", [(15, 8), (15, 40), (31, 40)])
+def test_non_finite_input_raises_and_keeps_the_graphs(cuda, d, n):
+    """A NaN or Inf entry must not come back as finite digits: the block
+    norms carry it to the planner (NaN-keeping column maxima), which raises
+    ValueError as the reference's does for a non-finite norm
+    (engine.py:467-472 -> precision.py one_norm); the cached graphs of the
+    shape stay usable afterwards (no eager fallback, no warning)."""
+    import warnings
+    m = mp()
+    ctx = m.PrecisionCtx(d)
+    X = synth(n, 1.0, 3)
+    good = words_of(m.ps_mixed_exp(X, 16, ctx))
+    for bad in (np.nan, np.inf, -np.inf):
+        Xb = X.copy()
+        Xb[n // 2, 1] = bad
+        with warnings.catch_warnings():
+            warnings.simplefilter("error")
+            with pytest.raises(ValueError):
+                m.ps_mixed_exp(Xb, 16, ctx)
+            again = words_of(m.ps_mixed_exp(X, 16, ctx))
+        assert np.array_equal(good, again)
+    # one bad member of a batch fails the call (the reference has no batches)
+    Xs = np.stack([X, X])
+    Xs[1, 0, 0] = np.nan
+    with pytest.raises(ValueError):
+        m.ps_mixed_exp(Xs, 16, ctx)
+    # the other evaluators: fixed precision and explicit powers (no planner on their path),
+    # the cosine's Z = X X (a product before any norm), Pade pairs, scaling and squaring
+    Xb = X.copy()
+    Xb[1, n - 1] = np.nan
+    for fn in (lambda: m.ps_fixed(Xb, m.taylor_exp_coeffs(12), ctx),
+               lambda: m.ps_mixed_exp(Xb, 2, ctx),
+               lambda: m.ps_mixed_exp(Xb, 16, ctx, fix_params=False),
+               lambda: m.ps_mixed_general(m.cos_argument(Xb, ctx), m.taylor_cos_coeffs(12), ctx),
+               lambda: m.ps_mixed_pade(Xb, 13, ctx),
+               lambda: m.expm_ss(Xb, ctx, 16)):
+        with pytest.raises(ValueError):
+            fn()
+
+
+def test_empty_batch_and_empty_matrix(cuda):
+    """No kernel is launched for an empty batch or 0 x 0 matrices; the
+    reference returns an empty result for from_rows([]) (engine.py:390-482)."""
+    m = mp()
+    for ctx in (m.PrecisionCtx(15), m.PrecisionCtx(31)):
+        reps = m.ps_mixed_exp(np.zeros((0, 8, 8)), 16, ctx)
+        assert len(reps) == 0
+        reps = m.ps_mixed_general(np.zeros((0, 40, 40)), m.taylor_cos_coeffs(12), ctx)
+        assert len(reps) == 0
+        assert len(m.ps_fixed(np.zeros((0, 8, 8)), m.taylor_exp_coeffs(9), ctx)) == 0
+        rep = m.ps_mixed_exp(np.zeros((0, 0)), 8, ctx)
+        assert tuple(rep.result.data.shape[-2:]) == (0, 0)
+        assert all(x == 1 for x in rep.plan.level_digits)
+        assert len(m.expm_ss(np.zeros((0, 8, 8)), ctx, 16)) == 0

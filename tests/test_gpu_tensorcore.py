@@ -87,6 +87,47 @@ def test_abi_gemm_and_horner_step_on_plain_matrices(cuda):
     assert torch.equal(O1.data, O2.data)
 
 
+@pytest.mark.parametrize("fmt,B,n", [(15, 3, 96), (31, 2, 200), (31, 1, 1024), (63, 1, 64), (7, 2, 128)])
+def test_mat_mul_propagates_non_finite_entries(cuda, fmt, B, n):
+    """mat_mul (precision.py:160-184) of an operand with a NaN / Inf entry: row i of the
+    product is non-finite for a bad A[i, k], column j for a bad B[k, j] (the digit splits
+    answer a non-finite row / column maximum with an Inf scale instead of cutting finite
+    digits out of it); every other entry is bit-identical to the product of the clean
+    operands (row and column scales are independent)."""
+    import torch
+    from paper_2312_17396_b200 import _lib
+    from paper_2312_17396_b200.precision import MatBatch
+    h = _lib.handle_for()
+    torch.manual_seed(fmt + n)
+    A = MatBatch.empty(fmt, B, n, device=cuda)
+    Bm = MatBatch.empty(fmt, B, n, device=cuda)
+    for M in (A, Bm):
+        M.data[0].normal_()
+        for w in range(1, M.words):
+            M.data[w] = M.data[0] * 2.0 ** (-55 * w) if fmt != 7 else 0
+    C0 = MatBatch.zeros(fmt, B, n, device=cuda)
+    h.gemm(A, Bm, C0)
+    assert torch.isfinite(C0.data).all()
+    bad_rows = [(0, 2, 3, float("nan")), (B - 1, n - 1, 0, float("inf"))]
+    bad_cols = [(0, 1, 4, float("-inf")), (B - 1, 7, n - 2, float("nan"))]
+    A2, B2 = MatBatch(A.data.clone(), fmt), MatBatch(Bm.data.clone(), fmt)
+    for b, i, k, v in bad_rows:
+        A2.data[0, b, i, k] = v
+    for b, k, j, v in bad_cols:
+        B2.data[0, b, k, j] = v
+    C = MatBatch.zeros(fmt, B, n, device=cuda)
+    h.gemm(A2, B2, C)
+    clean = torch.ones((B, n, n), dtype=torch.bool, device=cuda)
+    for b, i, _, _ in bad_rows:
+        assert not torch.isfinite(C.data[0, b, i, :]).any()
+        clean[b, i, :] = False
+    for b, _, j, _ in bad_cols:
+        assert not torch.isfinite(C.data[0, b, :, j]).any()
+        clean[b, :, j] = False
+    for w in range(C.words):
+        assert torch.equal(C.data[w][clean], C0.data[w][clean])
+
+
 def test_tc_digit_width_rules(cuda):
     """8-bit digits: operands of one product must share the width; K beyond
     the exact-int32 limit is refused; every digit lies in [-128, 127] and the
