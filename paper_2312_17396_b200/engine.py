@@ -183,6 +183,37 @@ class BatchReport(list):
         self.seconds = seconds
 
 
+# kernels index the batch with blockIdx.y / blockIdx.z (<= 65535)
+_MAX_BATCH = 32768
+
+
+def _chunked(fn):
+    """Batches beyond the grid's y / z range run as consecutive sub-batches
+    (a matrix gets the same bits in any batch); one BatchReport comes back."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(X, *args, **kw):
+        if isinstance(X, MatBatch):
+            B = X.batch
+        else:
+            shp = getattr(X, "shape", None)
+            B = shp[0] if shp is not None and len(shp) == 3 else 0
+        if B <= _MAX_BATCH:
+            return fn(X, *args, **kw)
+        reps, parts, sec = [], [], {}
+        for lo in range(0, B, _MAX_BATCH):
+            hi = min(B, lo + _MAX_BATCH)
+            part = MatBatch(X.data[:, lo:hi], X.fmt) if isinstance(X, MatBatch) else X[lo:hi]
+            out = fn(part, *args, **kw)
+            reps.extend(out)
+            parts.append(out.result.data)
+            for k, v in (out.seconds or {}).items():
+                sec[k] = sec.get(k, 0.0) + v
+        return BatchReport(reps, MatBatch(_torch().cat(parts, dim=1), out.result.fmt), sec)
+    return wrapper
+
+
 # ---------------------------------------------------------------- timing
 class _Buckets:
     """CUDA-event timing of the reference's four buckets (engine.py:268-280);
@@ -967,6 +998,7 @@ def _submit(X, series, ctx, delta, fix_params, with_bound, timing, slot, eager, 
 
 
 @complexmat.complex_aware
+@_chunked
 def ps_fixed(X, series: CoefficientSeries, ctx: PrecisionCtx, with_bound: bool = False,
              timing: bool = True):
     """Fixed-precision PS with s = ceil(sqrt(m)) (engine.py:304-345)."""
@@ -1013,6 +1045,7 @@ def ps_fixed(X, series: CoefficientSeries, ctx: PrecisionCtx, with_bound: bool =
 
 
 @complexmat.complex_aware
+@_chunked
 def ps_mixed_general(X, series: CoefficientSeries, ctx: PrecisionCtx, delta: float = 10.0,
                      with_bound: bool = False, timing: bool = True):
     """Mixed-precision PS for decaying coefficients (engine.py:348-387)."""
@@ -1053,6 +1086,7 @@ def _mixed_tail(h, prep, ctx, delta, apply_switch, fix_params, with_bound, singl
 
 
 @complexmat.complex_aware
+@_chunked
 def ps_mixed_exp(X, m: int, ctx: PrecisionCtx, fix_params: bool = True, delta: float = 10.0,
                  with_bound: bool = False, timing: bool = True):
     """Mixed-precision PS for the order-m Taylor approximant of exp

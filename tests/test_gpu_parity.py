@@ -608,3 +608,20 @@ def test_empty_batch_and_empty_matrix(cuda):
         assert tuple(rep.result.data.shape[-2:]) == (0, 0)
         assert all(x == 1 for x in rep.plan.level_digits)
         assert len(m.expm_ss(np.zeros((0, 8, 8)), ctx, 16)) == 0
+
+
+def test_batches_beyond_the_grid_range(cuda):
+    """More matrices than blockIdx.y / z can index run as sub-batches; every
+    member keeps the bits it has alone (batch invariance)."""
+    import torch
+    m = mp()
+    for d, B, n in ((31, 70000, 4), (15, 66000, 33)):
+        ctx = m.PrecisionCtx(d)
+        Xb = np.random.default_rng(d).standard_normal((B, n, n)) / n
+        reps = m.ps_mixed_exp(Xb, 8, ctx)
+        assert len(reps) == B and reps.result.batch == B
+        for b in (0, 32767, 32768, B - 1):
+            solo = m.ps_mixed_exp(Xb[b], 8, ctx)
+            assert torch.equal(reps.result.data[:, b], solo.result.data[:, 0])
+            assert torch.equal(reps[b].result.data.reshape(-1), solo.result.data.reshape(-1))
+            assert reps[b].plan.level_digits == solo.plan.level_digits
