@@ -188,3 +188,67 @@ def test_cfg5_full_cosine_summa_path(cuda, oracle_lib, fx, cols_fx):
     assert list(plan.level_digits) == rec["digits"] and plan.nu == rec["nu"]
     e = _check_cols(oracle_lib, res.block, 0, rec, cols_fx["cfg5"], plan.r, n, d)
     print(f"cfg5 SUMMA 1x1 column error {e:.3e}")
+
+
+# ------------------------------------------------- worst-case accumulators
+def _const_poly_exact(x, n, coeffs):
+    """X = x J (n x n, every entry x): X^k = n^(k-1) x^k J exactly, so
+    p(X) = b_0 I + (sum_{k>=1} b_k n^(k-1) x^k) J.  Returns (diagonal, off-diagonal)."""
+    from fractions import Fraction
+    xf = Fraction(x)
+    off = sum(Fraction(c) * n ** (k - 1) * xf ** k for k, c in enumerate(coeffs) if k >= 1)
+    return Fraction(coeffs[0]) + off, off
+
+
+def _check_const(res, diag, off, n, d, r):
+    from fractions import Fraction
+    import torch
+    data = res.data.double()[:, 0]
+    worst = Fraction(0)
+    for (i, j) in ((0, 0), (0, 1), (n - 1, n - 1), (n - 1, 0), (n // 2, n // 3), (n // 2, n // 2)):
+        v = sum(Fraction(float(data[w][i, j])) for w in range(data.shape[0]))
+        worst = max(worst, abs(v - (diag if i == j else off)))
+    # every row and column has the same digits: the off-diagonal entries agree to the bit
+    hi = data[0].clone()
+    hi.fill_diagonal_(float(data[0][0, 1]))
+    assert (hi.max() - hi.min()).item() == 0.0
+    normp = abs(diag) + (n - 1) * abs(off)
+    assert float(worst * n / normp) <= tol(r, n, d), (float(worst * n / normp), tol(r, n, d))
+
+
+@pytest.mark.parametrize("n,a", [(256, 0.99), (1024, 0.7123456789012345), (8192, 0.99999999999), (8192, 0.501)])
+def test_constant_matrices_fill_the_int32_accumulators(cuda, n, a):
+    """Size-independent property with an exact answer at the BASELINE sizes: for X = x J all
+    products of a digit-plane pair have one sign, so every int32 diagonal accumulator of the
+    tensor-core GEMMs reaches K d_i d_j (random matrices never come near: their sums grow like
+    sqrt(K)).  exp (Taylor m = 30: cfg2 / cfg3 kernels) and the cosine in Z = X X (cfg5 path) at
+    dd against the exact rational value."""
+    import torch
+    import paper_2312_17396_b200 as mp
+    ctx = mp.PrecisionCtx(31)
+    x = a / n
+    X = torch.full((n, n), x, dtype=torch.float64, device="cuda")
+    rep = mp.ps_mixed_exp(X, 30, ctx)
+    diag, off = _const_poly_exact(x, n, mp.taylor_exp_coeffs(30).coeffs)
+    _check_const(rep.result, diag, off, n, 31, rep.plan.r)
+    del rep
+    from fractions import Fraction
+    Z = mp.cos_argument(X, ctx)
+    rep = mp.ps_mixed_general(Z, mp.taylor_cos_coeffs(24), ctx)
+    z = n * Fraction(x) ** 2          # Z = X X = n x^2 J exactly (Z itself is rounded to dd: within the gate)
+    diag, off = _const_poly_exact(z, n, mp.taylor_cos_coeffs(24).coeffs)
+    _check_const(rep.result, diag, off, n, 31, rep.plan.r)
+
+
+def test_constant_matrix_qd_pade(cuda):
+    """The same worst case on the qd kernels (cfg4 shape: Pade [26/26], n = 2048, ||X||_1 = 2)."""
+    import torch
+    import paper_2312_17396_b200 as mp
+    n = 2048
+    x = 1.9999 / n
+    X = torch.full((n, n), x, dtype=torch.float64, device="cuda")
+    num, den = mp.ps_mixed_pade(X, 26, mp.PrecisionCtx(63))
+    pc, qc = mp.pade_exp_coeffs(26, 26)
+    for rep, cs in ((num, pc), (den, qc)):
+        diag, off = _const_poly_exact(x, n, cs.coeffs)
+        _check_const(rep.result, diag, off, n, 63, rep.plan.r)
