@@ -27,10 +27,13 @@ MPPS_GRAPHS=0 timeout 600 ncu --set full --clock-control none --import-source on
   --launch-skip 1 -c 1 -f -o $O/r02_ncu_cfg2_pw16 python tools/one_step.py cfg2 1 > $O/ncu_full_cfg2.log 2>&1
 MPPS_GRAPHS=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:oz_gemm_wide_kernel \
   --launch-skip 1 -c 1 -f -o $O/r02_ncu_cfg5_wide python tools/one_step.py cfg5 1 > $O/ncu_full_cfg5.log 2>&1
+# the headline's dominant launch itself: the paired [Z^3 | Z^4] product (N = 2n), third launch of the kernel
+MPPS_GRAPHS=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:oz_gemm_wide_kernel \
+  --launch-skip 2 -c 1 -f -o $O/r02_ncu_cfg5_wide_paired python tools/one_step.py cfg5 1 > $O/ncu_full_cfg5p.log 2>&1
 MPPS_GRAPHS=0 timeout 600 ncu --set full --clock-control none --import-source on -k regex:oz_gemm_pw16_kernel \
   --launch-skip 0 -c 1 -f -o $O/r02_ncu_cfg3_pw16 python tools/one_step.py cfg3 1 > $O/ncu_full_cfg3.log 2>&1
 # text exports (the reports themselves exceed what gpurun copies back)
-for r in r02_ncu_cfg2_pw16 r02_ncu_cfg5_wide r02_ncu_cfg3_pw16; do
+for r in r02_ncu_cfg2_pw16 r02_ncu_cfg5_wide r02_ncu_cfg5_wide_paired r02_ncu_cfg3_pw16; do
   if [ -f $O/$r.ncu-rep ]; then
     ncu -i $O/$r.ncu-rep --page details > $O/$r.txt 2>/dev/null
     ncu -i $O/$r.ncu-rep --page raw --csv > $O/${r}_raw.csv 2>/dev/null
