@@ -28,6 +28,7 @@ the graph path off for that shape (eager execution, same kernels).
 
 from __future__ import annotations
 
+import collections
 import os
 from typing import Dict, Optional, Tuple
 
@@ -37,8 +38,13 @@ from .precision import FP64, MatBatch
 
 _ENABLED = os.environ.get("MPPS_GRAPHS", "1") != "0"
 _SPECULATE = os.environ.get("MPPS_SPECULATE", "1") != "0"
-_CACHE: Dict[tuple, "_ShapeGraphs"] = {}
+_CACHE: "collections.OrderedDict[tuple, _ShapeGraphs]" = collections.OrderedDict()   # least recently used first
 _FAILED = set()
+# Every cached shape keeps its intermediates (powers, digit planes, blocks) in a private pool --
+# ~1 GB at cfg2, ~20 GB at cfg5 -- so the cache is bounded by bytes: before a new shape is
+# captured, least recently used shapes are dropped until the recorded pools fit the budget
+# (MPPS_GRAPH_CACHE_GB; default: half of the device memory).
+_BUDGET = None
 
 
 def enabled() -> bool:
@@ -55,8 +61,51 @@ def _torch():
     return torch
 
 
+def cache_budget() -> int:
+    global _BUDGET
+    if _BUDGET is None:
+        env = os.environ.get("MPPS_GRAPH_CACHE_GB")
+        if env:
+            _BUDGET = int(float(env) * (1 << 30))
+        else:
+            _BUDGET = _torch().cuda.get_device_properties(_torch().cuda.current_device()).total_memory // 2
+    return _BUDGET
+
+
+def set_cache_budget(nbytes: Optional[int]) -> None:
+    """Bytes of graph pools kept across shapes (None: the default)."""
+    global _BUDGET
+    _BUDGET = None if nbytes is None else int(nbytes)
+
+
+def cache_info() -> dict:
+    return {"shapes": len(_CACHE), "bytes": sum(g.bytes for g in _CACHE.values()), "budget": cache_budget()}
+
+
+def clear() -> None:
+    """Drop every cached graph and its pool (after the device is idle)."""
+    if _CACHE:
+        _torch().cuda.synchronize()
+        _CACHE.clear()
+
+
+def _make_room(keep: tuple) -> None:
+    """Drop least recently used shapes while the recorded pools exceed the
+    budget.  Evaluations in flight hold their graphs through ``Pending.g``;
+    the device is drained first so no replay still reads a released pool."""
+    budget = cache_budget()
+    drained = False
+    while len(_CACHE) > 1 and sum(g.bytes for g in _CACHE.values()) > budget:
+        key = next(k for k in _CACHE if k != keep)
+        if not drained:
+            _torch().cuda.synchronize()
+            drained = True
+        del _CACHE[key]
+
+
 class _ShapeGraphs:
     def __init__(self):
+        self.bytes = 0            # device memory reserved while this entry was captured (its private pool + warm-up)
         self.pool = None
         self.x_in = None
         self.pre = None
@@ -120,6 +169,8 @@ def submit(key: tuple, Xsrc, build_pre, timer, slot: int = 0) -> Optional[Pendin
     g = _CACHE.get(key)
     try:
         if g is None:
+            _make_room(key)
+            mem0 = torch.cuda.memory_reserved()
             g = _ShapeGraphs()
             g.pool = torch.cuda.graph_pool_handle()
             g.x_in = torch.empty(Xsrc.shape, dtype=torch.float64, device="cuda")
@@ -142,7 +193,10 @@ def submit(key: tuple, Xsrc, build_pre, timer, slot: int = 0) -> Optional[Pendin
                 g.norms_pin = torch.empty(g.prep.norms_dev.shape, dtype=torch.float64, pin_memory=True)
                 _lib.handle_for().store_host(g.prep.norms_dev.contiguous(), g.norms_pin)
             g.pre_launches = _lib.total_launches() - l0
+            g.bytes = max(0, torch.cuda.memory_reserved() - mem0)
             _CACHE[key] = g
+        else:
+            _CACHE.move_to_end(key)
         g.x_in.copy_(Xsrc, non_blocking=True)
         timer.start("power_formation")
         g.pre.replay()
@@ -186,6 +240,7 @@ def finish(p: Pending, run_post, clone: bool = True):
         raise PlanError(exc) from exc
     entry = g.post.get(post_key)
     if entry is None:
+        mem0 = torch.cuda.memory_reserved()
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
@@ -199,6 +254,7 @@ def finish(p: Pending, run_post, clone: bool = True):
             res = post_fn(g.prep)
         entry = (graph, res, post_fn, _lib.total_launches() - l0)  # post_fn keeps its index tensors alive
         g.post[post_key] = entry
+        g.bytes += max(0, torch.cuda.memory_reserved() - mem0)
     graph, res, _, post_launches = entry
     global _LAST_LAUNCHES
     _LAST_LAUNCHES = g.pre_launches + post_launches

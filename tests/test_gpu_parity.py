@@ -625,3 +625,33 @@ def test_batches_beyond_the_grid_range(cuda):
             assert torch.equal(reps.result.data[:, b], solo.result.data[:, 0])
             assert torch.equal(reps[b].result.data.reshape(-1), solo.result.data.reshape(-1))
             assert reps[b].plan.level_digits == solo.plan.level_digits
+
+
+def test_graph_cache_is_bounded_by_bytes(cuda):
+    """Cached shapes keep their intermediates in private pools; least recently used shapes are
+    dropped once the recorded pools exceed the budget, and an evicted shape is simply captured
+    again (same bits)."""
+    import torch
+    from paper_2312_17396_b200 import graphs
+    m = mp()
+    ctx = m.PrecisionCtx(31)
+    graphs.clear()
+    try:
+        Xs = {n: np.stack([synth(n, 1.0, 10 * n + i) for i in range(4)]) for n in (40, 48, 56, 64)}
+        first = {n: m.ps_mixed_exp(X, 16, ctx).result.data.clone() for n, X in Xs.items()}
+        info = graphs.cache_info()
+        assert info["shapes"] == 4 and info["bytes"] > 0
+        per = info["bytes"] // 4
+        graphs.set_cache_budget(2 * per + per // 2)
+        for n, X in list(Xs.items()) * 2:
+            assert torch.equal(m.ps_mixed_exp(X, 16, ctx).result.data, first[n])
+            assert graphs.cache_info()["shapes"] <= 4
+        X72 = np.stack([synth(72, 1.0, i) for i in range(4)])
+        m.ps_mixed_exp(X72, 16, ctx)
+        assert graphs.cache_info()["shapes"] <= 3
+        for n, X in Xs.items():            # evicted shapes are captured again
+            assert torch.equal(m.ps_mixed_exp(X, 16, ctx).result.data, first[n])
+        assert graphs.cache_info()["shapes"] <= 4
+    finally:
+        graphs.set_cache_budget(None)
+        graphs.clear()
