@@ -251,16 +251,23 @@ __device__ __forceinline__ void split_digits_w(const mp::qd &v, int8_t (&dg)[S])
 }
 
 // Non-finite entries: a NaN or Inf in a row (column) must not come back as
-// finite digits.  abs_keep maps both to +Inf in the running maximum (fmax
-// drops NaNs; an integer test on the high word, no FP64 compare), and
-// row_exponent answers Inf with kExpNonFinite: every product entry of that
+// finite digits.  AbsMax reports such a row (column) maximum as +Inf (fmax
+// alone drops NaNs), and row_exponent answers Inf with kExpNonFinite: every product entry of that
 // row (column) is then scaled by 2^kExpNonFinite = Inf in the GEMM epilogues
 // (pow2i), i.e. comes out Inf or NaN as mat_mul's would (precision.py:160-184),
 // and the block norms carry it to the planner, which raises.
 constexpr int kExpNonFinite = 1 << 20;
-__device__ __forceinline__ double abs_keep(double v) {
-  return ((__double2hiint(v) & 0x7ff00000) == 0x7ff00000) ? __longlong_as_double(0x7ff0000000000000ll) : fabs(v);
-}
+// running maximum of |v| taken on the bit patterns: for non-negative doubles
+// the integer order is the numeric order and Inf / NaN are the largest
+// patterns, so a non-finite entry stays (fmax drops NaNs) at the cost of the
+// integer compare-and-select that replaces fmax's DSETP + selects
+struct AbsMax {
+  long long m = 0;
+  __device__ __forceinline__ void add(double v) { m = max(m, __double_as_longlong(v) & 0x7fffffffffffffffll); }
+  __device__ __forceinline__ double value() const {
+    return m >= 0x7ff0000000000000ll ? __longlong_as_double(0x7ff0000000000000ll) : __longlong_as_double(m);
+  }
+};
 __device__ __forceinline__ int row_exponent(double mx) {
   int e = 0;
   if (!(mx < __longlong_as_double(0x7ff0000000000000ll))) return kExpNonFinite;
@@ -478,11 +485,12 @@ __device__ __forceinline__ void slice_rows_regs(const MatRef &A, long long base,
       for (int q = 0; q < 4; ++q) h[it][q] = l[it][q] = 0.0;
     }
   }
-  double mx = 0.0;
+  AbsMax am;
 #pragma unroll
   for (int it = 0; it < NIT; ++it)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) mx = fmax(mx, abs_keep(h[it][q]));
+    for (int q = 0; q < 4; ++q) am.add(h[it][q]);
+  double mx = am.value();
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   const int e = row_exponent(mx);
@@ -531,12 +539,15 @@ __device__ __forceinline__ void slice_rows_body(const MatRef &A, int rows, int c
     // row), so this block's digits are exactly those of the gathered panel
     e = out.exps[(long long)b * out.rpad + i];
   } else {
-    double mx = 0.0;
-    if (i < rows)
+    AbsMax am;
+    if (i < rows) {
+#pragma unroll 4
       for (int k = lane; k < cols; k += 32) {
         double v = fi == F32 ? (double)((const float *)A.data)[base + k] : ((const double *)A.data)[base + k];
-        mx = fmax(mx, abs_keep(v));
+        am.add(v);
       }
+    }
+    double mx = am.value();
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     e = row_exponent(mx);
@@ -648,13 +659,16 @@ __global__ void row_exps_kernel(MatRef A, int rows, int cols, int fi, SliceRef o
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int b = sel ? sel[blockIdx.y] : (int)blockIdx.y;
   if (i >= out.rpad) return;
-  double mx = 0.0;
+  AbsMax am;
   const long long base = (long long)b * A.bstride + (long long)i * A.ld;
-  if (i < rows)
+  if (i < rows) {
+#pragma unroll 4
     for (int k = lane; k < cols; k += 32) {
       double v = fi == F32 ? (double)((const float *)A.data)[base + k] : ((const double *)A.data)[base + k];
-      mx = fmax(mx, abs_keep(v));
+      am.add(v);
     }
+  }
+  double mx = am.value();
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if (lane == 0) out.exps[(long long)b * out.rpad + i] = row_exponent(mx);
@@ -670,13 +684,16 @@ __global__ void col_exps_kernel(MatRef B, int rows, int cols, int fi, SliceRef o
   const int j = blockIdx.x * 32 + tx;
   const int bz = blockIdx.y;
   const int b = sel ? sel[bz] : bz;
-  double mx = 0.0;
-  if (j < cols)
+  AbsMax am;
+  if (j < cols) {
+#pragma unroll 4
     for (int k = ty; k < rows; k += 8) {
       const long long off = (long long)b * B.bstride + (long long)k * B.ld + j;
       double v = fi == F32 ? (double)((const float *)B.data)[off] : ((const double *)B.data)[off];
-      mx = fmax(mx, abs_keep(v));
+      am.add(v);
     }
+  }
+  double mx = am.value();
   red[ty][tx] = mx;
   __syncthreads();
   if (ty == 0 && out.row0 + j < out.rpad && j < out.nrows) {
