@@ -274,12 +274,16 @@ int mpps_small_ps_prepare(mpps_handle *h, const mpps_mat *X, int m, int s, const
                           double *blocks, double *Y, double *norms);
 int mpps_small_ps_horner(mpps_handle *h, const double *Y, const double *blocks, const signed char *level_fmt,
                          int m, int s, double bm, mpps_mat *out);
-/* The whole small evaluation in one call: prepare, the norms to the host
- * (norms_host, (B, r+2)), the planner's digit rule in certified float64
- * (digits_host (B, r), nu_host (B); fixed != 0: all levels at d), Horner.
- * Returns 4 (MPPS_NEED_PLAN) without running Horner when some e_i lies within
- * 1e-8 of a digit boundary: the caller then plans exactly and calls
- * mpps_small_ps_horner. */
+/* The whole small evaluation (engine.py:390-482 for one matrix per CTA) in
+ * one call and one launch: prepare, the planner's digit rule in certified
+ * float64 on the device (digits_host (B, r), nu_host (B); fixed != 0: all
+ * levels at d), Horner from the blocks still in shared memory.  The norms
+ * (norms_host, (B, r+2)) and the plan reach the host through pinned memory;
+ * the call returns when every matrix is planned, the Horner chains may still
+ * be running on the handle's stream.  Returns 4 (MPPS_NEED_PLAN) when some e_i
+ * lies within 1e-8 of a digit boundary (those matrices' Horner chains are not
+ * run): the caller then plans exactly and calls mpps_small_ps_horner on the
+ * blocks, Y and norms this call left in place. */
 #define MPPS_NEED_PLAN 4
 int mpps_small_ps_eval(mpps_handle *h, const mpps_mat *X, int m, int s, const double *coeff, int d, double delta,
                        int apply_switch, int fixed, double *blocks, double *Y, double *norms_dev,

@@ -14,6 +14,7 @@
 #include <stdarg.h>
 #include <string.h>
 #include <stdlib.h>
+#include <vector>
 
 #include "../../include/mpps_b200.h"
 #include "formats.cuh"
@@ -56,6 +57,9 @@ struct mpps_handle {
   cudaStream_t stream;
   long long launches;
   char err[512];
+  // K5: pinned (device-mapped) hand-over buffer of the one-launch small-matrix evaluation
+  double *small_pin = nullptr;
+  size_t small_pin_doubles = 0;
 };
 
 namespace {
@@ -845,6 +849,7 @@ int mpps_create(int device, void *stream, mpps_handle **out) {
 }
 
 int mpps_destroy(mpps_handle *h) {
+  if (h && h->small_pin) cudaFreeHost(h->small_pin);
   delete h;
   return MPPS_OK;
 }
@@ -1345,13 +1350,112 @@ static int small_plan_row(const double *nb, double y, int r, int d, double delta
   return 0;
 }
 
+// MPPS_SMALL_FUSED=0: the two-launch path (prepare, host rule, Horner)
+static int small_fused_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MPPS_SMALL_FUSED");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
+// One launch per evaluation (small_fused_kernel): the digit rule runs on the
+// device between the block norms and the Horner chain.  Each CTA's thread 0
+// stores its matrix's norms and plan into pinned (device-mapped) host memory
+// and counts itself in; the host spins on that counter, so the call returns
+// as soon as every matrix is planned -- while the Horner chains still run --
+// without a stream synchronisation or a copy-engine transfer.  Returns
+// MPPS_OK, 4 (some matrix's rule declined: blocks, Y and norms are in place
+// for mpps_small_ps_horner), or an error.
+static int small_ps_eval_fused(mpps_handle *h, const mpps_mat *X, int m, int s, const double *coeff, int d, double delta,
+                               int apply_switch, int fixed, double *blocks, double *Y, double *norms_dev,
+                               double *norms_host, int *digits_host, int *nu_host, mpps_mat *out) {
+  int rc = check_mat(h, X, "small_ps.X");
+  if (!rc) rc = check_mat(h, out, "small_ps.out");
+  if (rc) return rc;
+  const int n = X->rows, B = X->batch, r = m / s;
+  if (out->fmt != MPPS_FP64 || out->rows != n || out->cols != n || out->ld != n || out->batch_stride != (long long)n * n ||
+      out->batch != B)
+    return set_err(h, MPPS_EINVAL, "small_ps: contiguous square fp64 output of the input's shape expected");
+  const int per = 2 * (r + 2);                       // norms (r + 2), digits (r), nu, declined
+  const size_t need = 2 + (size_t)B * per;           // [0]: arrival counter (as unsigned)
+  if (h->small_pin_doubles < need) {
+    if (h->small_pin) cudaFreeHost(h->small_pin);
+    h->small_pin = nullptr;
+    h->small_pin_doubles = 0;
+    const size_t cap = need < 4096 ? 4096 : 2 * need;
+    cudaError_t e = cudaHostAlloc((void **)&h->small_pin, sizeof(double) * cap, cudaHostAllocMapped);
+    if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "small_ps pinned buffer: %s", cudaGetErrorString(e));
+    h->small_pin_doubles = cap;
+  }
+  volatile unsigned *cnt = reinterpret_cast<volatile unsigned *>(h->small_pin);
+  *cnt = 0;
+  static thread_local mpps::small::FusedArgs a;
+  memset(&a.p, 0, sizeof(a.p));
+  a.p.X = (const double *)X->data; a.p.xbs = X->batch_stride; a.p.ldx = X->ld;
+  a.p.n = n; a.p.m = m; a.p.s = s; a.p.r = r; a.p.top_scalar = (m % s) == 0;
+  for (int k = 0; k <= m; ++k) a.p.coef[k] = coeff[k];
+  a.p.blocks = blocks; a.p.Y = Y; a.p.norms = norms_dev; a.p.batch = B;
+  a.out = (double *)out->data; a.delta = delta; a.d = d; a.apply_switch = apply_switch; a.fixed = fixed;
+  a.host = h->small_pin + 2;
+  a.arrived = reinterpret_cast<unsigned *>(h->small_pin);
+  const size_t smem = sizeof(double) * ((size_t)n * n * (s + r + 1 + 2) + r + 2) + 64;
+  static bool configured = false;
+  if (!configured) {
+    const size_t mx = sizeof(double) * ((size_t)mpps::small::kMaxN * mpps::small::kMaxN *
+                                            (mpps::small::kMaxS + mpps::small::kMaxBlocks + 2) + mpps::small::kMaxBlocks + 1) + 64;
+    cudaError_t e = cudaFuncSetAttribute(mpps::small::small_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    if (e != cudaSuccess) return set_err(h, MPPS_ECUDA, "small_ps attr: %s", cudaGetErrorString(e));
+    configured = true;
+  }
+  launch_k(mpps::small::small_fused_kernel, dim3(B), dim3(mpps::small::kThreads), smem, h->stream, a);
+  rc = after_launch(h, "small_fused_kernel");
+  if (rc) return rc;
+  // wait for the B plans (not for the kernel): spin on the arrival counter, checking now and
+  // then that the stream has not ended without them (a failed launch must not hang the host)
+  unsigned long long spins = 0;
+  while (*cnt < (unsigned)B) {
+    if ((++spins & 0x3fff) == 0) {
+      cudaError_t q = cudaStreamQuery(h->stream);
+      if (q != cudaErrorNotReady) {
+        if (*cnt >= (unsigned)B) break;
+        return set_err(h, MPPS_ECUDA, "small_ps_eval: the evaluation ended without its plans (%s)",
+                       q == cudaSuccess ? "no error reported" : cudaGetErrorString(q));
+      }
+    }
+  }
+  __atomic_thread_fence(__ATOMIC_ACQUIRE);
+  const volatile double *hp = h->small_pin + 2;
+  int declined = 0;
+  for (int b = 0; b < B; ++b) {
+    const volatile double *pb = hp + (size_t)b * per;
+    for (int k = 0; k < r + 2; ++k) norms_host[(size_t)b * (r + 2) + k] = pb[k];
+    for (int i = 0; i < r; ++i) digits_host[(size_t)b * r + i] = (int)pb[r + 2 + i];
+    nu_host[b] = (int)pb[2 * r + 2];
+    declined |= (int)pb[2 * r + 3];
+  }
+  return declined ? 4 : MPPS_OK;
+}
+
 int mpps_small_ps_eval(mpps_handle *h, const mpps_mat *X, int m, int s, const double *coeff, int d, double delta,
                        int apply_switch, int fixed, double *blocks, double *Y, double *norms_dev, double *norms_host,
                        int *digits_host, int *nu_host, mpps_mat *out) {
-  int rc = mpps_small_ps_prepare(h, X, m, s, coeff, blocks, Y, norms_dev);
-  if (rc) return rc;
+  if (!coeff || !blocks || !Y || !norms_dev || !norms_host || !digits_host || !nu_host || !X || !out)
+    return set_err(h, MPPS_EINVAL, "small_ps_eval: null argument");
+  if (X->batch == 0) return MPPS_OK;
+  if (X->rows != X->cols || X->fmt != MPPS_FP64 || !mpps_small_ps_supported(X->rows, m, MPPS_FP64))
+    return set_err(h, MPPS_EINVAL, "small_ps_eval: unsupported n=%d m=%d", X->rows, m);
+  int sd = 1;
+  while (sd * sd < m) ++sd;
+  if (s != sd) return set_err(h, MPPS_EINVAL, "small_ps: s must be ceil(sqrt(m)) = %d", sd);
   const int B = X->batch, r = m / s;
   if (r > 63) return set_err(h, MPPS_EINVAL, "small_ps_eval: r too large");
+  if (small_fused_enabled())
+    return small_ps_eval_fused(h, X, m, s, coeff, d, delta, apply_switch, fixed, blocks, Y, norms_dev, norms_host,
+                               digits_host, nu_host, out);
+  int rc = mpps_small_ps_prepare(h, X, m, s, coeff, blocks, Y, norms_dev);
+  if (rc) return rc;
   cudaError_t e = cudaMemcpyAsync(norms_host, norms_dev, sizeof(double) * (size_t)B * (r + 2), cudaMemcpyDeviceToHost,
                                   h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);     // the one host sync (planner norms)

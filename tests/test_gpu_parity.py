@@ -655,3 +655,51 @@ def test_graph_cache_is_bounded_by_bytes(cuda):
     finally:
         graphs.set_cache_budget(None)
         graphs.clear()
+
+
+def test_small_path_one_launch_equals_two_launches(cuda):
+    """mpps_small_ps_eval runs prepare, the digit rule (on the device) and the Horner chain in one
+    launch; the same operations as small_ps_prepare + the host rule + small_ps_horner, hence the
+    same bits, digits and nu -- mixed and fixed, batches with heterogeneous plans, n = 32 / 17 / 5."""
+    import torch
+    from paper_2312_17396_b200 import _lib, planner
+    from paper_2312_17396_b200.coefficients import coeff_words
+    from paper_2312_17396_b200.precision import MatBatch, FP64
+    m_ = mp()
+    h = _lib.handle_for()
+    ctx = m_.PrecisionCtx(15)
+    for n, B, deg in ((32, 6, 16), (17, 3, 30), (5, 4, 9), (32, 1, 25)):
+        series = m_.taylor_exp_coeffs(deg)
+        s = planner.default_block_size(deg)
+        r = deg // s
+        cw = np.ascontiguousarray(coeff_words(series, ctx)[:, 0])
+        Xs = np.stack([synth(n, 10.0 ** (-b), 7 * n + b) for b in range(B)])      # norms 1 .. 1e-5: different plans
+        X = MatBatch(torch.from_numpy(Xs).cuda().unsqueeze(0), FP64)
+        for fixed in (False, True):
+            l0 = _lib.total_launches()
+            blocks = torch.empty((r + 1, B, n, n), dtype=torch.float64, device=cuda)
+            Y = torch.empty((B, n, n), dtype=torch.float64, device=cuda)
+            nd = torch.empty((B, r + 2), dtype=torch.float64, device=cuda)
+            out = MatBatch.empty(FP64, B, n, device=cuda)
+            norms, digits, nu, planned = h.small_ps_eval(X, deg, s, cw, 15, 10.0, True, fixed, blocks, Y, nd, out)
+            assert planned and _lib.total_launches() - l0 == 1
+            # the two-launch path with the exact host planner
+            blocks2, Y2, nd2 = torch.empty_like(blocks), torch.empty_like(Y), torch.empty_like(nd)
+            h.small_ps_prepare(X, deg, s, cw, blocks2, Y2, nd2)
+            norms2 = nd2.cpu().numpy()
+            assert np.array_equal(norms, norms2) and torch.equal(Y, Y2)
+            top = deg % s == 0
+            assert torch.equal(blocks[:r if top else r + 1], blocks2[:r if top else r + 1])
+            fm = np.ones((B, r + 1), dtype=np.int8)
+            for b in range(B):
+                if fixed:
+                    dg, nu_b = (15,) * r, r + 1
+                else:
+                    p = planner.plan_precisions(tuple(float(x) for x in norms2[b, :r + 1]), float(norms2[b, r + 1]), ctx,
+                                                10.0, s=s)
+                    dg, nu_b = p.level_digits, p.nu
+                assert tuple(int(x) for x in digits[b]) == tuple(dg) and int(nu[b]) == nu_b
+                fm[b, 1:] = [0 if x <= 7 else 1 for x in dg]
+            out2 = MatBatch.empty(FP64, B, n, device=cuda)
+            h.small_ps_horner(Y2, blocks2, fm, deg, s, float(cw[deg]), out2)
+            assert torch.equal(out.data, out2.data)
