@@ -1006,6 +1006,9 @@ int mpps_assemble_blocks_hc(mpps_handle *h, const mpps_mat *powers, int s, int m
 #define AC(WW, NB_, NP_) \
   if (wf == WW && r + 1 == NB_ && s - 1 == NP_) return launch_assemble_c<WW, NB_, NP_>(h, powers, m, coeff_host, blocks, norms, skip_top);
   AC(DD, 6, 5) AC(DD, 7, 6) AC(DD, 5, 4) AC(DD, 4, 3) AC(DD, 5, 3) AC(F64, 5, 3) AC(F64, 4, 3)
+  // m = 17-19, 26-29, 37-41 (r + 1 = s - 1 + 1): the all-dd re-assembly of a (nearly) flat plan after the
+  // two-pass assembly (engine._dd_blocks) had no kernel for them (found by tools/fuzz_vs_oracle.py)
+  AC(DD, 4, 4) AC(DD, 5, 5) AC(DD, 6, 6)
 #undef AC
   return set_err(h, MPPS_EFMT, "assemble_hc: no constant-coefficient kernel for r+1=%d, s=%d at format %d", r + 1, s,
                  powers[pref].fmt);
@@ -1075,7 +1078,7 @@ int mpps_assemble_hc_n_supported(int block_fmt, int s, int m, int nblocks) {
 int mpps_assemble_hc_supported(int fmt, int s, int m) {
   const int wf = fmt_index(fmt), r = m / s, nb = r + 1, np = s - 1;
   if (wf == DD) return (nb == 6 && np == 5) || (nb == 7 && np == 6) || (nb == 5 && np == 4) || (nb == 4 && np == 3) ||
-                       (nb == 5 && np == 3);
+                       (nb == 5 && np == 3) || (nb == 4 && np == 4) || (nb == 5 && np == 5) || (nb == 6 && np == 6);
   if (wf == F64) return (nb == 5 && np == 3) || (nb == 4 && np == 3);
   return 0;
 }

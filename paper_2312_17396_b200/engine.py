@@ -316,6 +316,11 @@ class _Prepared:
     norms_dev: object = None   # the same norms on the device (level scalings)
     lowp: bool = False         # blocks are fp64 (two-pass assembly): dd ones are made per plan in _horner
     y_low: bool = False        # Y = X^s is at fp64 precision: groups with a dd level get a dd Y in _horner
+    # device tensors from module-level caches (coefficients, member selections) that this state's
+    # kernels read: a captured graph bakes their addresses into its kernel nodes and outlives the
+    # caches' clear() -- without this reference a replay after the cache rolled over read freed
+    # memory (wrong blocks and norms; found by tools/fuzz_vs_oracle.py after > 64 distinct series)
+    keep: list = field(default_factory=list)
 
 
 def _form_powers(h, Xt, wf: int, s: int, timer: _Buckets, x_is_working: Optional[MatBatch] = None,
@@ -447,11 +452,11 @@ def _assemble(h, powers: List[MatBatch], series: CoefficientSeries, ctx: Precisi
             blocks.append(MatBatch.empty(wf, 1, 1, device=dev))
         timer.stop()
         if not sync:
-            return _Prepared(wf, s, r, m, powers, blocks, None, cw, norms, lowp=True)
+            return _Prepared(wf, s, r, m, powers, blocks, None, cw, norms, lowp=True, keep=[coeffs])
         timer.start("norm_estimation")
         norms_h = h.host_array(norms)
         timer.stop()
-        return _Prepared(wf, s, r, m, powers, blocks, norms_h, cw, norms, lowp=True)
+        return _Prepared(wf, s, r, m, powers, blocks, norms_h, cw, norms, lowp=True, keep=[coeffs])
     hc = h.assemble_hc_supported(wf, s, m)
     # B_r = b_m I when m mod s == 0: the K3 Horner step uses b_m itself, so
     # the constant-coefficient kernel does not store it (norm still reported)
@@ -472,11 +477,11 @@ def _assemble(h, powers: List[MatBatch], series: CoefficientSeries, ctx: Precisi
         h.one_norm_complex(powers[s - 1], nc, norms[:, r + 1], r + 2)
     timer.stop()
     if not sync:
-        return _Prepared(wf, s, r, m, powers, blocks, None, cw, norms)
+        return _Prepared(wf, s, r, m, powers, blocks, None, cw, norms, keep=[coeffs])
     timer.start("norm_estimation")
     norms_h = h.host_array(norms)   # the one host sync of the pipeline (no copy engine: _lib.host_array)
     timer.stop()
-    return _Prepared(wf, s, r, m, powers, blocks, norms_h, cw, norms)
+    return _Prepared(wf, s, r, m, powers, blocks, norms_h, cw, norms, keep=[coeffs])
 
 
 def _prepare(h, Xt, series: CoefficientSeries, ctx: PrecisionCtx, wf: int, s: int,
@@ -606,6 +611,8 @@ def _horner(h, prep: _Prepared, digits: np.ndarray, nil: np.ndarray, timer: _Buc
         # at the working planes (X^s = X^(s-1) X), for those members only
         dd_mem = sorted(b for key, mem in group_list if DD in key[0][1:] for b in mem)
         sel_dd = None if len(dd_mem) == B else _selection_of(dd_mem, dev)
+        if sel_dd is not None:
+            prep.keep.append(sel_dd)
         Y_dd = MatBatch.empty(DD, B, n, device=dev)
         ge.gemm(h, ge.prepare(h, prep.powers[s - 2], 0, wf, sel_dd, wf=wf),
                 ge.prepare(h, prep.powers[0], 1, wf, sel_dd, wf=wf), Y_dd, sel_dd)

@@ -703,3 +703,72 @@ def test_small_path_one_launch_equals_two_launches(cuda):
             out2 = MatBatch.empty(FP64, B, n, device=cuda)
             h.small_ps_horner(Y2, blocks2, fm, deg, s, float(cw[deg]), out2)
             assert torch.equal(out.data, out2.data)
+
+
+@pytest.mark.parametrize("m", [17, 19, 26, 29, 37, 38, 41])
+def test_flat_plans_after_two_pass_assembly(cuda, oracle_lib, m):
+    """dd evaluations whose plan keeps (nearly) every level at dd (a large ||X||) re-assemble all
+    blocks in dd after the two-pass assembly; for r + 1 = s blocks (m = 17-19, 26-29, 37-41) that
+    pass had no compiled kernel and the evaluation raised (found by tools/fuzz_vs_oracle.py).
+    Oracle parity, alone and next to a small-norm batch mate (batch invariance)."""
+    import torch
+    import oracle
+    mm = mp()
+    ctx = mm.PrecisionCtx(31)
+    n = 30
+    X = synth(n, 6.0, m)
+    rep = mm.ps_mixed_exp(X, m, ctx)
+    ref = oracle.ps_eval(X, mm.taylor_exp_coeffs(m).coeffs, 31)
+    _check(rep, ref, n, 31)
+    assert sum(1 for x in rep.plan.level_digits if x > 15) >= 2      # dd levels beyond B_0, B_1: a re-assembly
+    both = mm.ps_mixed_exp(np.stack([X, synth(n, 1e-3, m + 1)]), m, ctx)
+    assert torch.equal(both[0].result.data.reshape(-1), rep.result.data.reshape(-1))
+    num, den = mm.ps_mixed_pade(X, m if m < 30 else 18, ctx)
+    pc, qc = mm.pade_exp_coeffs(m if m < 30 else 18, m if m < 30 else 18)
+    _check(num, oracle.ps_eval(X, pc.coeffs, 31), n, 31)
+    _check(den, oracle.ps_eval(X, qc.coeffs, 31), n, 31)
+
+
+def test_graph_replay_after_the_coefficient_cache_rolled_over(cuda):
+    """A captured graph bakes the device address of the coefficient tensor into its assembly
+    kernel; the tensor lives in a module-level cache that is cleared after 64 distinct series.
+    The prepared state of the graph must keep it alive: replaying the first shape after 70 other
+    series used to read freed memory (blocks without their b_0 I, garbage norms).  Found by
+    tools/fuzz_vs_oracle.py."""
+    import torch
+    from paper_2312_17396_b200 import graphs
+    m = mp()
+    ctx = m.PrecisionCtx(31)
+    series = m.taylor_exp_coeffs(1)            # s = 1: the run-time-coefficient assembly kernel
+    X1, X2 = synth(19, 0.13, 1), synth(19, 0.2, 2)
+    first = m.ps_fixed(X1, series, ctx).result.data.clone()          # captures
+    small = synth(6, 0.3, 3)
+    for deg in range(2, 38):
+        for d in (15, 31):
+            m.ps_fixed(small, m.taylor_exp_coeffs(deg), m.PrecisionCtx(d))
+    # whatever the rolled-over cache freed is reallocated and overwritten (the tensor was
+    # allocated on the capture's warm-up side stream, so the junk goes through torch's stream pool)
+    junk = []
+    for _ in range(40):
+        side = torch.cuda.Stream()
+        with torch.cuda.stream(side):
+            junk += [torch.full((k % 60 + 4,), float("nan"), dtype=torch.float64, device=cuda) for k in range(200)]
+    torch.cuda.synchronize()
+    again = m.ps_fixed(X1, series, ctx).result.data                  # replays
+    assert torch.equal(first, again)
+    del junk
+    # (whether freed memory is actually handed out again depends on the allocator's stream pools, so
+    # the mechanism is checked too: the graph's prepared state owns the coefficient tensor)
+    from paper_2312_17396_b200.coefficients import coeff_words
+    g = next(v for k, v in graphs._CACHE.items() if k[0] == (1, 19, 19))
+    kept = [t for t in g.prep.keep if torch.is_tensor(t) and t.dtype == torch.float64]
+    assert kept and np.array_equal(kept[0].cpu().numpy(), np.asarray(coeff_words(series, ctx), dtype=np.float64))
+    got = m.ps_fixed(X2, series, ctx).result.data.clone()
+    graphs.set_enabled(False)
+    try:
+        want = m.ps_fixed(X2, series, ctx).result.data
+    finally:
+        graphs.set_enabled(True)
+    assert torch.equal(got, want)
+    rep = m.ps_mixed_general(X2, m.taylor_cos_coeffs(24), ctx)
+    assert rep.plan.level_digits[0] > 1
