@@ -271,6 +271,12 @@ def finish(p: Pending, run_post, clone: bool = True):
         p.done.record()
     g.last_post = post_key
     out = MatBatch(res.data.clone(), res.fmt) if clone else MatBatch(res.data, res.fmt)
+    if clone:
+        # the caller's tensor is final only after the copy out of the static buffer: a consumer on
+        # another stream (pipeline.evaluate_host's download) waited for the event recorded after the
+        # Horner replay and could read the clone before it was written (tools/fuzz_pipeline.py)
+        p.done = torch.cuda.Event()
+        p.done.record()
     timer.stop()
     return g.prep, norms, out, info
 

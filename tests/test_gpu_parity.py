@@ -772,3 +772,26 @@ def test_graph_replay_after_the_coefficient_cache_rolled_over(cuda):
     assert torch.equal(got, want)
     rep = m.ps_mixed_general(X2, m.taylor_cos_coeffs(24), ctx)
     assert rep.plan.level_digits[0] > 1
+
+
+def test_host_batches_one_stream_download_waits_for_the_result_copy(cuda):
+    """pipeline.evaluate_host in its default mode (one stream, chunks one after another) downloads each
+    chunk on a copy stream once the evaluation's done event has fired; for cloned results that event
+    must follow the copy out of the graph's static buffer (it was recorded before it: ~1 % of the
+    calls downloaded a tensor that had not been written yet; found by tools/fuzz_pipeline.py).  Many
+    repetitions of two of the configurations that failed, against the direct call, bitwise."""
+    import torch
+    from paper_2312_17396_b200 import pipeline as pl
+    m = mp()
+    ctx = m.PrecisionCtx(31)
+    for n, B, deg, sizes in ((24, 18, 16, [18]), (64, 12, 9, [5, 7])):
+        X = np.stack([synth(n, 10.0 ** (-0.3 * b), 11 * n + b) for b in range(B)])
+        direct = m.ps_mixed_exp(X, deg, ctx).result.data.cpu()
+        Xh = torch.from_numpy(X).pin_memory()
+        out = torch.empty((2, B, n, n), dtype=torch.float64).pin_memory()
+        sub = pl.mixed_exp(deg, ctx, timing=False)
+        for _ in range(150):
+            out.zero_()
+            pl.evaluate_host(sub, Xh, out, sizes, streams=1)
+            torch.cuda.synchronize()
+            assert torch.equal(out, direct)

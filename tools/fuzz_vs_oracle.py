@@ -10,11 +10,13 @@ from _util import synth
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+NMIN = int(sys.argv[3]) if len(sys.argv) > 3 else 1          # sizes: n in [NMIN, NMAX) (qd: half of NMAX)
+NMAX = int(sys.argv[4]) if len(sys.argv) > 4 else 72
 bad = 0
 t0 = time.time()
 for it in range(N):
     d = int(rng.choice([15, 31, 63, 15, 31]))
-    n = int(rng.integers(1, 72 if d < 63 else 40))
+    n = int(rng.integers(NMIN, NMAX if d < 63 else max(NMIN + 1, NMAX // 2)))
     kind = str(rng.choice(["exp", "exp", "cos", "fixed", "pade"]))
     m = int(rng.integers(1, 41)) if kind != "pade" else int(rng.integers(2, 20))
     norm = float(10.0 ** rng.uniform(-4, 1.3))
