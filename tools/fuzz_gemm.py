@@ -1,6 +1,6 @@
 """Dev tool: the operator mat_mul (mpps_gemm on plain matrices, the library splits internally) at random
 ragged M x K x N, formats, badly scaled rows / columns, zero rows, against the CPU oracle's mat_mul
-(entrywise: |C - C_oracle| <= 4 K u |A| |B|), plus a Horner step against gemm + add."""
+(entrywise: |C - C_oracle| <= 4 K u |A| |B| + the digit-plane truncation term, below)."""
 import sys, os, time
 from fractions import Fraction
 import numpy as np, torch
@@ -53,7 +53,12 @@ for it in range(N_):
             i, j = int(rng.integers(M)), int(rng.integers(N))
             g = sum(Fraction(float(x)) for x in got[:, i, j])
             o = sum(Fraction(float(x)) for x in Co[:, i, j])
-            lim = 4 * K * u * Fraction(float(absAB[i, j]))
+            # entrywise 4 K u |A| |B|, plus the digit-plane truncation: every operand entry is cut at
+            # 2^-(8 S - 2) of its ROW (column) maximum, so an entry far below that maximum carries
+            # fewer bits than its own format (the scheme's error is normwise per row and column)
+            S = {7: 4, 15: 8, 31: 14, 63: 28}[fmt]
+            trunc = 2 * K * Fraction(1, 2 ** (8 * S - 2)) * Fraction(float(np.abs(Aw[0][i]).max())) * Fraction(float(np.abs(Bw[0][:, j]).max()))
+            lim = 4 * K * u * Fraction(float(absAB[i, j])) + trunc
             if abs(g - o) > lim:
                 bad += 1
                 print("VALUE", tag, (i, j), float(g - o), float(lim), flush=True)
